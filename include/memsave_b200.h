@@ -1,0 +1,138 @@
+/*
+ * memsave_b200.h — C ABI of the B200 (sm_100a) selective-save layer kernels.
+ *
+ * This is the drop-in boundary for the hot path of arxiv 2404.12406
+ * ("Lowering PyTorch's Memory Consumption for Selective Differentiation").
+ * Each entry point replaces one kernel-level operation of the reference
+ * (`/root/reference/pkg/src/leantape`, a CPU numpy/numba restatement of the
+ * paper) or one VJP that the reference specifies.  The save
+ * decision itself (which of X / W is kept for backward) stays in the caller:
+ * these functions only compute, and each backward product is a separate entry
+ * point so the caller launches exactly the products that were requested.
+ *
+ *   ms_conv2d_fwd   ← leantape.kernels.conv2d_fwd   (kernels/__init__.py:26,
+ *                      numba_impl.py:109-116, numpy_impl.py:12-24)
+ *   ms_conv2d_dx    ← leantape.kernels.conv2d_dx    (kernels/__init__.py:27,
+ *                      numba_impl.py:119-124, numpy_impl.py:27-38)
+ *   ms_conv2d_dw    ← leantape.kernels.conv2d_dw    (kernels/__init__.py:28,
+ *                      numba_impl.py:127-132, numpy_impl.py:41-51)
+ *   ms_linear_fwd / ms_linear_dx / ms_linear_dw / ms_bias_grad
+ *                   ← forward_linear and its VJPs
+ *   ms_bn_eval_fwd / ms_bn_eval_bwd
+ *                   ← forward_batchnorm2d, Eval mode
+ *
+ * Conventions (mirroring the reference kernel boundary):
+ *   - plain device pointers and sizes; no framework types in any signature;
+ *   - outputs are allocated by the CALLER (the reference allocates fresh
+ *     outputs itself; here the caller does it so that its allocator sees every
+ *     byte) and fully overwritten; inputs are read-only;
+ *   - every call is asynchronous and stream-ordered on `stream` (a
+ *     cudaStream_t passed as void*; NULL = legacy default stream); no host
+ *     synchronisation, no device allocation, re-entrant;
+ *   - workspaces are sized by the matching *_workspace() query and passed in;
+ *   - there is no CPU path: host pointers are an error of the caller;
+ *   - errors return a non-zero ms_status; ms_last_error() gives a message.
+ */
+#ifndef MEMSAVE_B200_H
+#define MEMSAVE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define MS_API __attribute__((visibility("default")))
+#else
+#define MS_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  MS_OK = 0,
+  MS_ERR_SHAPE = 1,       /* inconsistent or non-positive sizes          */
+  MS_ERR_DTYPE = 2,       /* unsupported dtype combination               */
+  MS_ERR_ALIGN = 3,       /* pointer / stride alignment not met          */
+  MS_ERR_UNSUPPORTED = 4, /* geometry outside what the kernels implement */
+  MS_ERR_LAUNCH = 5,      /* CUDA launch / driver error                  */
+  MS_ERR_WORKSPACE = 6    /* workspace missing or too small              */
+} ms_status;
+
+typedef enum { MS_F32 = 0, MS_BF16 = 1, MS_F16 = 2 } ms_dtype;
+
+/* activation layout; for weights MS_NCHW means OIHW, MS_NHWC means OHWI */
+typedef enum { MS_NCHW = 0, MS_NHWC = 1 } ms_layout;
+
+typedef enum { MS_CONV_FWD = 0, MS_CONV_DX = 1, MS_CONV_DW = 2 } ms_conv_pass;
+
+/* 2-d cross-correlation geometry (OH = (H+2p-kh)//s+1). */
+typedef struct {
+  int64_t n, c, h, w;   /* input batch, channels, height, width        */
+  int64_t k, r, s;      /* output channels, kernel height, kernel width */
+  int32_t stride_h, stride_w;
+  int32_t pad_h, pad_w;
+  int32_t layout;       /* ms_layout of x / y / dx / dy                */
+  int32_t wlayout;      /* ms_layout of w / dw                         */
+  int32_t dtype;        /* ms_dtype of every tensor operand            */
+} ms_conv_desc;
+
+/* ------------------------------------------------------------ conv2d */
+MS_API int64_t ms_conv2d_out_h(const ms_conv_desc* d);
+MS_API int64_t ms_conv2d_out_w(const ms_conv_desc* d);
+/* bytes of device workspace the given pass needs (0 = none) */
+MS_API size_t ms_conv2d_workspace(const ms_conv_desc* d, int32_t pass);
+/* y = conv(x, w) (+ bias[k] if bias != NULL; bias has dtype d->dtype) */
+MS_API ms_status ms_conv2d_fwd(const ms_conv_desc* d, const void* x, const void* w, const void* bias,
+                        void* y, void* ws, size_t ws_bytes, void* stream);
+/* dx = conv2d input-VJP of dy with w (transpose convolution) */
+MS_API ms_status ms_conv2d_dx(const ms_conv_desc* d, const void* dy, const void* w, void* dx, void* ws,
+                       size_t ws_bytes, void* stream);
+/* dw = conv2d weight-VJP of dy with x; dw has layout d->wlayout and dtype d->dtype */
+MS_API ms_status ms_conv2d_dw(const ms_conv_desc* d, const void* x, const void* dy, void* dw, void* ws,
+                       size_t ws_bytes, void* stream);
+/* db[k] = sum of dy over n, oh, ow (dy in d->layout, db in d->dtype) */
+MS_API ms_status ms_conv2d_db(const ms_conv_desc* d, const void* dy, void* db, void* ws,
+                       size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------ linear
+ * x: [M, K] row-major, w: [N, K] row-major, y/dy: [M, N] row-major.      */
+MS_API size_t ms_linear_workspace(int64_t M, int64_t N, int64_t K, int32_t dtype, int32_t pass);
+MS_API ms_status ms_linear_fwd(int64_t M, int64_t N, int64_t K, int32_t dtype, const void* x,
+                        const void* w, const void* bias, void* y, void* ws, size_t ws_bytes,
+                        void* stream);
+MS_API ms_status ms_linear_dx(int64_t M, int64_t N, int64_t K, int32_t dtype, const void* dy,
+                       const void* w, void* dx, void* ws, size_t ws_bytes, void* stream);
+MS_API ms_status ms_linear_dw(int64_t M, int64_t N, int64_t K, int32_t dtype, const void* x,
+                       const void* dy, void* dw, void* ws, size_t ws_bytes, void* stream);
+/* db[c] = sum_r g[r, c] for a row-major [rows, cols] matrix */
+MS_API size_t ms_bias_grad_workspace(int64_t rows, int64_t cols, int32_t dtype);
+MS_API ms_status ms_bias_grad(int64_t rows, int64_t cols, int32_t dtype, const void* g, void* db,
+                       void* ws, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------ batchnorm2d (eval)
+ * x/y/dy/dx: [n, c, hw] (MS_NCHW) or [n, hw, c] (MS_NHWC) in `dtype`.
+ * mean/var/weight/bias/dw/db: [c] in `pdtype`; weight/bias may be NULL
+ * (affine=False).  dw needs x; dx needs only weight and var.  */
+MS_API size_t ms_bn_eval_workspace(int64_t n, int64_t c, int64_t hw, int32_t layout);
+MS_API ms_status ms_bn_eval_fwd(int64_t n, int64_t c, int64_t hw, int32_t layout, int32_t dtype,
+                         int32_t pdtype, const void* x, const void* mean, const void* var,
+                         const void* weight, const void* bias, double eps, void* y, void* ws,
+                         size_t ws_bytes, void* stream);
+MS_API ms_status ms_bn_eval_bwd(int64_t n, int64_t c, int64_t hw, int32_t layout, int32_t dtype,
+                         int32_t pdtype, const void* dy, const void* x_or_null, const void* mean,
+                         const void* var, const void* weight, double eps, void* dx_or_null,
+                         void* dw_or_null, void* db_or_null, void* ws, size_t ws_bytes,
+                         void* stream);
+
+/* ------------------------------------------------------------ misc */
+MS_API const char* ms_status_string(int32_t status);
+MS_API const char* ms_last_error(void);
+MS_API int32_t ms_version(void);
+/* number of kernels this library has launched since load (all threads) */
+MS_API int64_t ms_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MEMSAVE_B200_H */

@@ -1,0 +1,311 @@
+// BatchNorm2d in eval mode: y = x*scale_c + shift_c with
+// scale_c = w_c/sqrt(var_c+eps), shift_c = b_c - mean_c*scale_c.
+// Backward: dx = g*scale_c (iff requested), dw_c = sum g*(x-mean_c)*invstd_c
+// (iff requested; the only consumer of x), db_c = sum g.
+// HBM-bound: 16-byte vector loads/stores, per-channel constants in smem, one
+// pass over g (and x iff dw is requested), fp32 per-block channel partials
+// reduced with shared atomics and one global atomic per channel per block.
+#include "misc.cuh"
+
+namespace ms {
+
+struct BnParams {
+  const void* mean;
+  const void* var;
+  const void* weight;  // nullable (affine=False)
+  const void* bias;    // nullable
+  int pdtype;
+  float eps;
+};
+
+__device__ __forceinline__ void bn_channel_consts(const BnParams& p, int c, float& scale,
+                                                  float& shift, float& invstd, float& mean) {
+  const float v = load_as_float(p.var, p.pdtype, c);
+  mean = load_as_float(p.mean, p.pdtype, c);
+  invstd = 1.0f / sqrtf(v + p.eps);
+  const float w = p.weight ? load_as_float(p.weight, p.pdtype, c) : 1.0f;
+  const float b = p.bias ? load_as_float(p.bias, p.pdtype, c) : 0.0f;
+  scale = w * invstd;
+  shift = b - mean * scale;
+}
+
+template <typename T, int VEC>
+struct Vec {
+  static constexpr int BYTES = VEC * sizeof(T);
+};
+
+template <typename T, int VEC>
+__device__ __forceinline__ void load_vec(const T* p, float (&v)[VEC]) {
+  if constexpr (VEC * sizeof(T) == 16) {
+    uint4 u = *reinterpret_cast<const uint4*>(p);
+    const T* e = reinterpret_cast<const T*>(&u);
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) v[j] = IO<T>::ld(e + j);
+  } else {
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) v[j] = IO<T>::ld(p + j);
+  }
+}
+template <typename T, int VEC>
+__device__ __forceinline__ void store_vec(T* p, const float (&v)[VEC]) {
+  if constexpr (VEC * sizeof(T) == 16) {
+    uint4 u;
+    T* e = reinterpret_cast<T*>(&u);
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) e[j] = IO<T>::cvt(v[j]);
+    *reinterpret_cast<uint4*>(p) = u;
+  } else {
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) p[j] = IO<T>::cvt(v[j]);
+  }
+}
+
+// ---------------------------------------------------------------- forward
+// NHWC requires C % VEC == 0; NCHW requires hw % VEC == 0 (host checks, else VEC=1)
+template <typename T, int VEC>
+__global__ void __launch_bounds__(256) bn_fwd_kernel(int64_t total, int C, int64_t hw, int layout,
+                                                     BnParams p, const T* __restrict__ x,
+                                                     T* __restrict__ y) {
+  extern __shared__ float sh[];
+  float* s_scale = sh;
+  float* s_shift = sh + C;
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    float sc, sf, inv, mu;
+    bn_channel_consts(p, c, sc, sf, inv, mu);
+    s_scale[c] = sc;
+    s_shift[c] = sf;
+  }
+  __syncthreads();
+  const int64_t nvec = total / VEC;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvec;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i * VEC;
+    float v[VEC];
+    load_vec<T, VEC>(x + e, v);
+    if (layout == MS_NHWC) {
+      const int c0 = (int)(e % C);
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) v[j] = v[j] * s_scale[c0 + j] + s_shift[c0 + j];
+    } else {
+      const int c = (int)((e / hw) % C);
+      const float sc = s_scale[c], sf = s_shift[c];
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) v[j] = v[j] * sc + sf;
+    }
+    store_vec<T, VEC>(y + e, v);
+  }
+}
+
+// ---------------------------------------------------------------- backward
+template <typename T, int VEC>
+__global__ void __launch_bounds__(256) bn_bwd_kernel(int64_t total, int C, int64_t hw, int layout,
+                                                     BnParams p, const T* __restrict__ g,
+                                                     const T* __restrict__ x, T* __restrict__ dx,
+                                                     float* __restrict__ acc_dw,
+                                                     float* __restrict__ acc_db) {
+  extern __shared__ float sh[];
+  float* s_scale = sh;
+  float* s_inv = sh + C;
+  float* s_mean = sh + 2 * C;
+  float* s_dw = sh + 3 * C;
+  float* s_db = sh + 4 * C;
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    float sc, sf, inv, mu;
+    bn_channel_consts(p, c, sc, sf, inv, mu);
+    s_scale[c] = sc;
+    s_inv[c] = inv;
+    s_mean[c] = mu;
+    s_dw[c] = 0.f;
+    s_db[c] = 0.f;
+  }
+  __syncthreads();
+  const bool want_dw = acc_dw != nullptr, want_db = acc_db != nullptr, want_dx = dx != nullptr;
+  const int64_t nvec = total / VEC;
+  // Per-thread partials; NHWC threads keep a fixed channel group when the
+  // grid stride is a multiple of C/VEC (host arranges it), otherwise flush.
+  float pdw[VEC], pdb[VEC];
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) pdw[j] = pdb[j] = 0.f;
+  int cur_c = -1;
+  auto flush = [&](int c0) {
+    if (c0 < 0) return;
+    if (layout == MS_NHWC) {
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) {
+        if (want_dw) atomicAdd(&s_dw[c0 + j], pdw[j]);
+        if (want_db) atomicAdd(&s_db[c0 + j], pdb[j]);
+      }
+    } else {
+      float a = 0.f, b = 0.f;
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) {
+        a += pdw[j];
+        b += pdb[j];
+      }
+      if (want_dw) atomicAdd(&s_dw[c0], a);
+      if (want_db) atomicAdd(&s_db[c0], b);
+    }
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) pdw[j] = pdb[j] = 0.f;
+  };
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvec;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i * VEC;
+    const int c0 = layout == MS_NHWC ? (int)(e % C) : (int)((e / hw) % C);
+    if (c0 != cur_c) {
+      flush(cur_c);
+      cur_c = c0;
+    }
+    float gv[VEC];
+    load_vec<T, VEC>(g + e, gv);
+    if (want_dx) {
+      float o[VEC];
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) o[j] = gv[j] * s_scale[layout == MS_NHWC ? c0 + j : c0];
+      store_vec<T, VEC>(dx + e, o);
+    }
+    if (want_db) {
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) pdb[j] += gv[j];
+    }
+    if (want_dw) {
+      float xv[VEC];
+      load_vec<T, VEC>(x + e, xv);
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) {
+        const int c = layout == MS_NHWC ? c0 + j : c0;
+        pdw[j] += gv[j] * (xv[j] - s_mean[c]) * s_inv[c];
+      }
+    }
+  }
+  flush(cur_c);
+  __syncthreads();
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    if (want_dw) atomicAdd(acc_dw + c, s_dw[c]);
+    if (want_db) atomicAdd(acc_db + c, s_db[c]);
+  }
+}
+
+#define MS_DT_DISPATCH(dt, ...)                                    \
+  switch (dt) {                                                    \
+    case MS_F32: { using T = float; __VA_ARGS__; } break;          \
+    case MS_BF16: { using T = __nv_bfloat16; __VA_ARGS__; } break; \
+    case MS_F16: { using T = __half; __VA_ARGS__; } break;         \
+    default: set_error("bad dtype %d", dt); return MS_ERR_DTYPE;   \
+  }
+
+static bool can_vec(int64_t c, int64_t hw, int layout, int vec, const void* a, const void* b,
+                    const void* d) {
+  auto al = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  if (!al(a) || (b && !al(b)) || (d && !al(d))) return false;
+  return layout == MS_NHWC ? (c % vec == 0) : (hw % vec == 0);
+}
+
+// NHWC: choose a grid whose thread stride is a multiple of C/VEC so that each
+// thread keeps one channel group for the whole sweep.
+static int bn_grid(int64_t nvec, int64_t C, int layout, int vec) {
+  int64_t blocks = (int64_t)num_sms() * 4;
+  if (layout == MS_NHWC) {
+    const int64_t groups = C / vec;
+    // total threads = blocks*256 -> make it a multiple of `groups`
+    int64_t a = groups, b = 256;
+    while (b) { const int64_t t = a % b; a = b; b = t; }
+    const int64_t lcm_blocks = groups / a;
+    if (lcm_blocks > 0) blocks = ((blocks + lcm_blocks - 1) / lcm_blocks) * lcm_blocks;
+  }
+  const int64_t need = (nvec + 255) / 256;
+  if (blocks > need) blocks = need > 0 ? need : 1;
+  return (int)blocks;
+}
+
+size_t bn_eval_workspace_bytes(int64_t c) { return sizeof(float) * 2 * (size_t)c; }
+
+ms_status bn_eval_fwd(int64_t n, int64_t c, int64_t hw, int layout, int dt, const BnParams& p,
+                      const void* x, void* y, cudaStream_t st) {
+  const int64_t total = n * c * hw;
+  if (total == 0) return MS_OK;
+  MS_CHECK_ARG(c <= 8192, MS_ERR_UNSUPPORTED, "batchnorm: C=%lld > 8192", (long long)c);
+  const size_t smem = sizeof(float) * 2 * c;
+  MS_DT_DISPATCH(dt, {
+    constexpr int V = 16 / sizeof(T);
+    if (can_vec(c, hw, layout, V, x, y, nullptr)) {
+      bn_fwd_kernel<T, V><<<bn_grid(total / V, c, layout, V), 256, smem, st>>>(
+          total, (int)c, hw, layout, p, (const T*)x, (T*)y);
+    } else {
+      bn_fwd_kernel<T, 1><<<bn_grid(total, c, layout, 1), 256, smem, st>>>(
+          total, (int)c, hw, layout, p, (const T*)x, (T*)y);
+    }
+  });
+  count_launch();
+  return launch_status("bn_fwd_kernel");
+}
+
+ms_status bn_eval_bwd(int64_t n, int64_t c, int64_t hw, int layout, int dt, const BnParams& p,
+                      const void* g, const void* x, void* dx, void* dw, void* db, void* ws,
+                      size_t ws_bytes, cudaStream_t st) {
+  const int64_t total = n * c * hw;
+  MS_CHECK_ARG(c <= 8192, MS_ERR_UNSUPPORTED, "batchnorm: C=%lld > 8192", (long long)c);
+  MS_CHECK_ARG(!(dw && !x), MS_ERR_SHAPE, "batchnorm bwd: dw requested without x");
+  float* acc_dw = nullptr;
+  float* acc_db = nullptr;
+  if (dw || db) {
+    MS_CHECK_ARG(ws && ws_bytes >= bn_eval_workspace_bytes(c), MS_ERR_WORKSPACE,
+                 "batchnorm bwd workspace too small");
+    cudaMemsetAsync(ws, 0, bn_eval_workspace_bytes(c), st);
+    if (dw) acc_dw = static_cast<float*>(ws);
+    if (db) acc_db = static_cast<float*>(ws) + c;
+  }
+  if (total > 0 && (dx || dw || db)) {
+    const size_t smem = sizeof(float) * 5 * c;
+    MS_DT_DISPATCH(dt, {
+      constexpr int V = 16 / sizeof(T);
+      if (can_vec(c, hw, layout, V, g, dw ? x : nullptr, dx)) {
+        bn_bwd_kernel<T, V><<<bn_grid(total / V, c, layout, V), 256, smem, st>>>(
+            total, (int)c, hw, layout, p, (const T*)g, (const T*)x, (T*)dx, acc_dw, acc_db);
+      } else {
+        bn_bwd_kernel<T, 1><<<bn_grid(total, c, layout, 1), 256, smem, st>>>(
+            total, (int)c, hw, layout, p, (const T*)g, (const T*)x, (T*)dx, acc_dw, acc_db);
+      }
+    });
+    count_launch();
+    MS_TRY(launch_status("bn_bwd_kernel"));
+  }
+  if (dw) MS_TRY(f32_to(acc_dw, dw, p.pdtype, c, nullptr, 1, st));
+  if (db) MS_TRY(f32_to(acc_db, db, p.pdtype, c, nullptr, 1, st));
+  return MS_OK;
+}
+
+}  // namespace ms
+
+// ---------------------------------------------------------------- C ABI
+extern "C" size_t ms_bn_eval_workspace(int64_t n, int64_t c, int64_t hw, int32_t layout) {
+  (void)n;
+  (void)hw;
+  (void)layout;
+  return ms::bn_eval_workspace_bytes(c);
+}
+
+extern "C" ms_status ms_bn_eval_fwd(int64_t n, int64_t c, int64_t hw, int32_t layout, int32_t dtype,
+                                    int32_t pdtype, const void* x, const void* mean,
+                                    const void* var, const void* weight, const void* bias,
+                                    double eps, void* y, void* ws, size_t ws_bytes, void* stream) {
+  (void)ws;
+  (void)ws_bytes;
+  MS_CHECK_ARG(n >= 0 && c > 0 && hw >= 0, MS_ERR_SHAPE, "batchnorm: bad shape");
+  MS_CHECK_ARG(x && y && mean && var, MS_ERR_SHAPE, "batchnorm: null tensor");
+  ms::BnParams p{mean, var, weight, bias, pdtype, (float)eps};
+  return ms::bn_eval_fwd(n, c, hw, layout, dtype, p, x, y, (cudaStream_t)stream);
+}
+
+extern "C" ms_status ms_bn_eval_bwd(int64_t n, int64_t c, int64_t hw, int32_t layout,
+                                    int32_t dtype, int32_t pdtype, const void* dy,
+                                    const void* x_or_null, const void* mean, const void* var,
+                                    const void* weight, double eps, void* dx_or_null,
+                                    void* dw_or_null, void* db_or_null, void* ws, size_t ws_bytes,
+                                    void* stream) {
+  MS_CHECK_ARG(n >= 0 && c > 0 && hw >= 0, MS_ERR_SHAPE, "batchnorm: bad shape");
+  MS_CHECK_ARG(dy && mean && var, MS_ERR_SHAPE, "batchnorm bwd: null tensor");
+  ms::BnParams p{mean, var, weight, nullptr, pdtype, (float)eps};
+  return ms::bn_eval_bwd(n, c, hw, layout, dtype, p, dy, x_or_null, dx_or_null, dw_or_null,
+                         db_or_null, ws, ws_bytes, (cudaStream_t)stream);
+}

@@ -1,0 +1,316 @@
+// Conv2d forward / input-VJP / weight-VJP entry points (the C-ABI boundary for
+// leantape.kernels.conv2d_fwd/dx/dw, kernels/__init__.py:26-28).
+//
+// 16-bit NHWC activations run as implicit GEMMs on the tcgen05 kernel:
+//   fwd : A = im2col(x) through a TMA im2col tensor map (padding = OOB zero
+//         fill, stride = traversal stride), B = weight [k][tap][c] (OHWI used
+//         in place when C % 64 == 0, otherwise a zero-padded repack)
+//   dx  : one GEMM per stride phase (h % sh, w % sw) — only the taps whose
+//         parity matches contribute, so no zero MACs; A = im2col(dy) with a
+//         per-phase bounding box, B = weight repacked [c][tap][k]
+//   dw  : A = dyᵀ (MN-major tiles of dy), B = im2col(x)ᵀ (MN-major), one tile
+//         set per tap, split-K over output pixels with fp32 red.add, then a
+//         cast/layout pass into OIHW or OHWI
+// float32, NCHW 16-bit and channel counts that are not multiples of 8 run on
+// the SIMT direct kernels (simt.cu).
+#include "misc.cuh"
+
+namespace ms {
+namespace {
+
+bool is16(int dt) { return dt == MS_BF16 || dt == MS_F16; }
+
+ConvDims dims_of(const ms_conv_desc* d) {
+  ConvDims c;
+  c.n = (int)d->n; c.c = (int)d->c; c.h = (int)d->h; c.w = (int)d->w;
+  c.k = (int)d->k; c.r = (int)d->r; c.s = (int)d->s;
+  c.sh = d->stride_h; c.sw = d->stride_w; c.ph = d->pad_h; c.pw = d->pad_w;
+  c.oh = (int)((d->h + 2 * d->pad_h - d->r) / d->stride_h + 1);
+  c.ow = (int)((d->w + 2 * d->pad_w - d->s) / d->stride_w + 1);
+  return c;
+}
+
+ms_status validate(const ms_conv_desc* d) {
+  MS_CHECK_ARG(d != nullptr, MS_ERR_SHAPE, "conv: null descriptor");
+  MS_CHECK_ARG(d->n >= 0 && d->c > 0 && d->h > 0 && d->w > 0 && d->k > 0 && d->r > 0 && d->s > 0,
+               MS_ERR_SHAPE, "conv: non-positive dimension");
+  MS_CHECK_ARG(d->stride_h > 0 && d->stride_w > 0 && d->pad_h >= 0 && d->pad_w >= 0, MS_ERR_SHAPE,
+               "conv: invalid stride/padding");
+  MS_CHECK_ARG(d->h + 2 * d->pad_h >= d->r && d->w + 2 * d->pad_w >= d->s, MS_ERR_SHAPE,
+               "conv: kernel larger than padded input");
+  MS_CHECK_ARG(d->dtype == MS_F32 || d->dtype == MS_BF16 || d->dtype == MS_F16, MS_ERR_DTYPE,
+               "conv: bad dtype %d", d->dtype);
+  MS_CHECK_ARG(d->n * d->c * d->h * d->w < (1ll << 31) &&
+                   d->n * d->k * (d->h + 2 * d->pad_h) * (d->w + 2 * d->pad_w) < (1ll << 33),
+               MS_ERR_UNSUPPORTED, "conv: tensor too large for 32-bit tile indexing");
+  return MS_OK;
+}
+
+// ----------------------------------------------------------------- planning
+struct ConvPlan {
+  bool tc = false;
+  int cpad8 = 0;        // fwd: channel count of the (possibly padded) activation
+  bool pad_x = false;   // fwd: activation is channel-padded into ws
+  bool repack = false;  // fwd: weight repacked into ws
+  int cpad = 0;         // fwd: per-tap weight pitch (multiple of 64)
+  int kpad = 0;         // dx: per-tap pitch of the repacked weight
+  size_t ws_pad = 0, ws_w = 0, ws_acc = 0;
+  size_t ws = 0;
+};
+
+bool tc_ok(const ms_conv_desc* d) {
+  return is16(d->dtype) && d->layout == MS_NHWC && d->r <= 64 && d->s <= 64 &&
+         d->pad_h < 64 && d->pad_w < 64;
+}
+
+ConvPlan plan(const ms_conv_desc* d, int pass) {
+  ConvPlan p;
+  const ConvDims c = dims_of(d);
+  const size_t es = dtype_size(d->dtype);
+  const int64_t taps = (int64_t)d->r * d->s;
+  if (!tc_ok(d)) {
+    if (pass == MS_CONV_DW) p.ws = align256(simt_conv_dw_workspace(c));
+    return p;
+  }
+  if (pass == MS_CONV_FWD) {
+    p.tc = true;
+    p.cpad8 = (int)(d->c < 8 ? 8 : round_up(d->c, 8));
+    p.pad_x = p.cpad8 != d->c;
+    p.cpad = (int)round_up(p.cpad8, 64);
+    p.repack = !(d->wlayout == MS_NHWC && d->c % 64 == 0);
+    if (p.pad_x) p.ws_pad = align256(es * (size_t)d->n * d->h * d->w * p.cpad8);
+    if (p.repack) p.ws_w = align256(es * (size_t)d->k * taps * p.cpad);
+    p.ws = p.ws_pad + p.ws_w;
+  } else if (pass == MS_CONV_DX) {
+    if (d->k % 8 != 0 || d->stride_h > 2 || d->stride_w > 2) {
+      return p;  // SIMT
+    }
+    p.tc = true;
+    p.kpad = (int)round_up(d->k, 64);
+    p.ws_w = align256(es * (size_t)d->c * taps * p.kpad);
+    p.ws = p.ws_w;
+  } else {
+    if (d->k % 8 != 0 || d->c % 8 != 0) {
+      p.ws = align256(simt_conv_dw_workspace(c));
+      return p;
+    }
+    p.tc = true;
+    p.ws_acc = align256(sizeof(float) * (size_t)d->k * taps * d->c);
+    p.ws = p.ws_acc;
+  }
+  return p;
+}
+
+GemmArgs base_args(int dt) {
+  GemmArgs g{};
+  g.ab_fmt = dt == MS_BF16 ? 1 : 0;
+  g.splits = 1;
+  g.taps = 1;
+  g.nphases = 1;
+  return g;
+}
+
+// ----------------------------------------------------------------- forward
+ms_status fwd_tc(const ms_conv_desc* d, const ConvPlan& p, const void* x, const void* w,
+                 const void* bias, void* y, void* ws, cudaStream_t st) {
+  const ConvDims c = dims_of(d);
+  const int dt = d->dtype;
+  uint8_t* wsb = static_cast<uint8_t*>(ws);
+  const void* xsrc = x;
+  if (p.pad_x) {
+    MS_TRY(pad_channels(dt, (int64_t)c.n * c.h * c.w, c.c, p.cpad8, x, wsb, st));
+    xsrc = wsb;
+  }
+  const void* wsrc = w;
+  if (p.repack) {
+    MS_TRY(repack_fprop(dt, c.k, c.c, c.r, c.s, p.cpad, d->wlayout, w, wsb + p.ws_pad, st));
+    wsrc = wsb + p.ws_pad;
+  }
+  const int64_t M = (int64_t)c.n * c.oh * c.ow;
+  GemmArgs g = base_args(dt);
+  g.M = (int)M;
+  g.N = c.k;
+  g.m_blocks = (int)((M + BM - 1) / BM);
+  const int bn = pick_bn(g.m_blocks, c.k);
+  g.n_blocks = (c.k + bn - 1) / bn;
+  g.num_tiles = g.m_blocks * g.n_blocks;
+  g.cv = ConvShape{c.n, c.h, c.w, p.cpad8, c.oh, c.ow, c.r, c.s, c.sh, c.sw, c.ph, c.pw,
+                   p.cpad / 64, p.cpad, c.oh, c.ow};
+  g.epi = EpiParams{y, c.k, dt, 0, bias, dt};
+  TmapPack tm;
+  const int lower[2] = {-c.pw, -c.ph};
+  const int upper[2] = {c.pw - (c.s - 1), c.ph - (c.r - 1)};
+  MS_TRY(make_tmap_im2col(&tm.a[0], dt, xsrc, c.n, c.h, c.w, p.cpad8, lower, upper, c.sw, c.sh,
+                          64, BM));
+  tm.a[1] = tm.a[2] = tm.a[3] = tm.a[0];
+  const int64_t wrow = (int64_t)c.r * c.s * p.cpad;
+  MS_TRY(make_tmap_2d(&tm.b, dt, wsrc, wrow, c.k, wrow, BK, bn));
+  return launch_umma(bn, 0, 0, LOAD_CONV_FPROP, tm, g, st);
+}
+
+// ----------------------------------------------------------------- input-VJP
+ms_status dx_tc(const ms_conv_desc* d, const ConvPlan& p, const void* dy, const void* w, void* dx,
+                void* ws, cudaStream_t st) {
+  const ConvDims c = dims_of(d);
+  const int dt = d->dtype;
+  void* wd = ws;
+  MS_TRY(repack_dgrad(dt, c.k, c.c, c.r, c.s, p.kpad, d->wlayout, w, wd, st));
+  GemmArgs g = base_args(dt);
+  g.N = c.c;
+  const int bn = pick_bn((int64_t)c.n * c.h * c.w / BM + 1, c.c);
+  g.n_blocks = (c.c + bn - 1) / bn;
+  g.cv = ConvShape{c.n, c.oh, c.ow, c.k, c.oh, c.ow, c.r, c.s, c.sh, c.sw, c.ph, c.pw,
+                   p.kpad / 64, p.kpad, c.h, c.w};
+  TmapPack tm;
+  int np = 0, tiles = 0;
+  for (int ph = 0; ph < c.sh; ++ph) {
+    for (int pw = 0; pw < c.sw; ++pw) {
+      PhaseInfo P{};
+      P.ph = ph;
+      P.pw = pw;
+      P.Hp = (c.h - ph + c.sh - 1) / c.sh;
+      P.Wp = (c.w - pw + c.sw - 1) / c.sw;
+      if (P.Hp <= 0 || P.Wp <= 0) continue;
+      P.r0 = (ph + c.ph) % c.sh;
+      P.s0 = (pw + c.pw) % c.sw;
+      P.nr = P.r0 < c.r ? (c.r - P.r0 + c.sh - 1) / c.sh : 0;
+      P.ns = P.s0 < c.s ? (c.s - P.s0 + c.sw - 1) / c.sw : 0;
+      const int dh0 = (ph + c.ph - P.r0) / c.sh;
+      const int dw0 = (pw + c.pw - P.s0) / c.sw;
+      P.Lh = P.nr > 0 ? dh0 - (P.nr - 1) : 0;
+      P.Lw = P.ns > 0 ? dw0 - (P.ns - 1) : 0;
+      P.m_total = c.n * P.Hp * P.Wp;
+      P.m_blocks = (P.m_total + BM - 1) / BM;
+      P.tile_begin = tiles;
+      tiles += P.m_blocks * g.n_blocks;
+      if (P.nr > 0 && P.ns > 0) {
+        const int lower[2] = {P.Lw, P.Lh};
+        const int upper[2] = {P.Lw + P.Wp - c.ow, P.Lh + P.Hp - c.oh};
+        MS_TRY(make_tmap_im2col(&tm.a[np], dt, dy, c.n, c.oh, c.ow, c.k, lower, upper, 1, 1, 64,
+                                BM));
+      } else if (np > 0) {
+        tm.a[np] = tm.a[0];
+      } else {
+        const int lower[2] = {0, 0};
+        const int upper[2] = {0, 0};
+        MS_TRY(make_tmap_im2col(&tm.a[np], dt, dy, c.n, c.oh, c.ow, c.k, lower, upper, 1, 1, 64,
+                                BM));
+      }
+      g.phase[np++] = P;
+    }
+  }
+  g.nphases = np;
+  g.num_tiles = tiles;
+  g.epi = EpiParams{dx, c.c, dt, 0, nullptr, dt};
+  const int64_t wrow = (int64_t)c.r * c.s * p.kpad;
+  MS_TRY(make_tmap_2d(&tm.b, dt, wd, wrow, c.c, wrow, BK, bn));
+  return launch_umma(bn, 0, 0, LOAD_CONV_DGRAD, tm, g, st);
+}
+
+// ----------------------------------------------------------------- weight-VJP
+ms_status dw_tc(const ms_conv_desc* d, const ConvPlan& p, const void* x, const void* dy, void* dw,
+                void* ws, cudaStream_t st) {
+  const ConvDims c = dims_of(d);
+  const int dt = d->dtype;
+  float* acc = static_cast<float*>(ws);
+  const int taps = c.r * c.s;
+  cudaMemsetAsync(acc, 0, sizeof(float) * (size_t)c.k * taps * c.c, st);
+  const int64_t P = (int64_t)c.n * c.oh * c.ow;
+  GemmArgs g = base_args(dt);
+  g.M = c.k;
+  g.N = c.c;
+  g.m_blocks = (c.k + BM - 1) / BM;
+  int bn = c.c <= 64 ? 64 : (c.c <= 128 ? 128 : 256);
+  g.n_blocks = (c.c + bn - 1) / bn;
+  g.taps = taps;
+  g.k_blocks = (int)((P + BK - 1) / BK);
+  const int64_t base_tiles = (int64_t)g.m_blocks * g.n_blocks * taps;
+  int64_t splits = (2 * (int64_t)num_sms() + base_tiles - 1) / base_tiles;
+  if (splits > g.k_blocks / 2) splits = g.k_blocks / 2;
+  if (splits < 1) splits = 1;
+  g.kb_per_split = (int)((g.k_blocks + splits - 1) / splits);
+  g.splits = (g.k_blocks + g.kb_per_split - 1) / g.kb_per_split;
+  g.num_tiles = (int)(base_tiles * g.splits);
+  g.cv = ConvShape{c.n, c.h, c.w, c.c, c.oh, c.ow, c.r, c.s, c.sh, c.sw, c.ph, c.pw,
+                   (c.c + 63) / 64, 0, c.oh, c.ow};
+  g.epi = EpiParams{acc, (int64_t)taps * c.c, MS_F32, 1, nullptr, 0};
+  TmapPack tm;
+  MS_TRY(make_tmap_2d(&tm.a[0], dt, dy, c.k, P, c.k, 64, BK));
+  tm.a[1] = tm.a[2] = tm.a[3] = tm.a[0];
+  const int lower[2] = {-c.pw, -c.ph};
+  const int upper[2] = {c.pw - (c.s - 1), c.ph - (c.r - 1)};
+  MS_TRY(make_tmap_im2col(&tm.b, dt, x, c.n, c.h, c.w, c.c, lower, upper, c.sw, c.sh, 64, BK));
+  MS_TRY(launch_umma(bn, 1, 1, LOAD_CONV_WGRAD, tm, g, st));
+  return wgrad_finalize(dt, c.k, c.c, c.r, c.s, d->wlayout, acc, dw, st);
+}
+
+}  // namespace
+}  // namespace ms
+
+using namespace ms;
+
+extern "C" int64_t ms_conv2d_out_h(const ms_conv_desc* d) {
+  return (d->h + 2 * d->pad_h - d->r) / d->stride_h + 1;
+}
+extern "C" int64_t ms_conv2d_out_w(const ms_conv_desc* d) {
+  return (d->w + 2 * d->pad_w - d->s) / d->stride_w + 1;
+}
+
+extern "C" size_t ms_conv2d_workspace(const ms_conv_desc* d, int32_t pass) {
+  if (validate(d) != MS_OK) return 0;
+  return plan(d, pass).ws;
+}
+
+extern "C" ms_status ms_conv2d_fwd(const ms_conv_desc* d, const void* x, const void* w,
+                                   const void* bias, void* y, void* ws, size_t ws_bytes,
+                                   void* stream) {
+  MS_TRY(validate(d));
+  if (d->n == 0) return MS_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  ConvPlan p = plan(d, MS_CONV_FWD);
+  MS_CHECK_ARG(ws_bytes >= p.ws && (p.ws == 0 || ws), MS_ERR_WORKSPACE,
+               "conv fwd: workspace %zu < %zu", ws_bytes, p.ws);
+  if (p.tc) return fwd_tc(d, p, x, w, bias, y, ws, st);
+  return simt_conv_fwd(dims_of(d), d->dtype, d->layout, d->wlayout, x, w, bias, y, st);
+}
+
+extern "C" ms_status ms_conv2d_dx(const ms_conv_desc* d, const void* dy, const void* w, void* dx,
+                                  void* ws, size_t ws_bytes, void* stream) {
+  MS_TRY(validate(d));
+  if (d->n == 0) return MS_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  ConvPlan p = plan(d, MS_CONV_DX);
+  MS_CHECK_ARG(ws_bytes >= p.ws && (p.ws == 0 || ws), MS_ERR_WORKSPACE,
+               "conv dx: workspace %zu < %zu", ws_bytes, p.ws);
+  if (p.tc) return dx_tc(d, p, dy, w, dx, ws, st);
+  return simt_conv_dx(dims_of(d), d->dtype, d->layout, d->wlayout, dy, w, dx, st);
+}
+
+extern "C" ms_status ms_conv2d_dw(const ms_conv_desc* d, const void* x, const void* dy, void* dw,
+                                  void* ws, size_t ws_bytes, void* stream) {
+  MS_TRY(validate(d));
+  cudaStream_t st = (cudaStream_t)stream;
+  ConvPlan p = plan(d, MS_CONV_DW);
+  MS_CHECK_ARG(ws_bytes >= p.ws && (p.ws == 0 || ws), MS_ERR_WORKSPACE,
+               "conv dw: workspace %zu < %zu", ws_bytes, p.ws);
+  if (d->n == 0) {
+    return cudaMemsetAsync(dw, 0, dtype_size(d->dtype) * d->k * d->c * d->r * d->s, st) ==
+                   cudaSuccess
+               ? MS_OK
+               : MS_ERR_LAUNCH;
+  }
+  if (p.tc) return dw_tc(d, p, x, dy, dw, ws, st);
+  return simt_conv_dw(dims_of(d), d->dtype, d->layout, d->wlayout, x, dy, dw, ws, ws_bytes, st);
+}
+
+extern "C" ms_status ms_conv2d_db(const ms_conv_desc* d, const void* dy, void* db, void* ws,
+                                  size_t ws_bytes, void* stream) {
+  MS_TRY(validate(d));
+  MS_CHECK_ARG(ws && ws_bytes >= colsum_workspace(d->k), MS_ERR_WORKSPACE,
+               "conv db: workspace too small");
+  const ConvDims c = dims_of(d);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (d->layout == MS_NHWC)
+    return colsum((int64_t)c.n * c.oh * c.ow, c.k, d->dtype, dy, db, d->dtype, ws, st);
+  return planesum(c.n, c.k, (int64_t)c.oh * c.ow, d->dtype, dy, db, d->dtype, ws, st);
+}

@@ -1,0 +1,202 @@
+// Host plumbing: status/error strings, SM count cache, tensor-map encoders,
+// umma_gemm dispatch.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "host.cuh"
+
+namespace ms {
+
+std::atomic<int64_t> g_launches{0};
+
+static thread_local char t_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(t_err, sizeof(t_err), fmt, ap);
+  va_end(ap);
+}
+
+const char* last_error() { return t_err; }
+
+ms_status launch_status(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    return MS_ERR_LAUNCH;
+  }
+  return MS_OK;
+}
+
+int num_sms() {
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (cache[dev] == 0) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = n > 0 ? n : 148;
+  }
+  return cache[dev];
+}
+
+// ------------------------------------------------------------------ tensor maps
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                       const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                       const cuuint32_t*, CUtensorMapInterleave,
+                                       CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                       CUtensorMapFloatOOBfill);
+typedef CUresult (*PFN_encodeIm2col_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                        const cuuint64_t*, const cuuint64_t*, const int*,
+                                        const int*, cuuint32_t, cuuint32_t, const cuuint32_t*,
+                                        CUtensorMapInterleave, CUtensorMapSwizzle,
+                                        CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled_t g_encode_tiled = nullptr;
+static PFN_encodeIm2col_t g_encode_im2col = nullptr;
+static int g_driver_version = 0;
+
+static ms_status resolve_driver() {
+  static std::once_flag once;
+  static ms_status st = MS_OK;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || fn == nullptr) {
+      st = MS_ERR_LAUNCH;
+      return;
+    }
+    g_encode_tiled = reinterpret_cast<PFN_encodeTiled_t>(fn);
+    fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || fn == nullptr) {
+      st = MS_ERR_LAUNCH;
+      return;
+    }
+    g_encode_im2col = reinterpret_cast<PFN_encodeIm2col_t>(fn);
+    cudaDriverGetVersion(&g_driver_version);
+  });
+  if (st != MS_OK) set_error("could not resolve cuTensorMapEncode* driver entry points");
+  return st;
+}
+
+ms_status make_tmap_2d(CUtensorMap* m, int dt, const void* base, uint64_t inner, uint64_t outer,
+                       uint64_t ld, uint32_t box_inner, uint32_t box_outer) {
+  MS_TRY(resolve_driver());
+  const size_t es = dtype_size(dt);
+  MS_CHECK_ARG((reinterpret_cast<uintptr_t>(base) & 15) == 0, MS_ERR_ALIGN,
+               "tensor base %p not 16-byte aligned", base);
+  MS_CHECK_ARG((ld * es) % 16 == 0, MS_ERR_ALIGN, "row pitch %llu elems not a multiple of 16 B",
+               (unsigned long long)ld);
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld * es};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode_tiled(m, tma_dtype(dt), 2, const_cast<void*>(base), dims, strides, box,
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  MS_CHECK_ARG(r == CUDA_SUCCESS, MS_ERR_LAUNCH,
+               "cuTensorMapEncodeTiled failed (%d): inner=%llu outer=%llu ld=%llu box=%ux%u", (int)r,
+               (unsigned long long)inner, (unsigned long long)outer, (unsigned long long)ld,
+               box_inner, box_outer);
+  return MS_OK;
+}
+
+ms_status make_tmap_im2col(CUtensorMap* m, int dt, const void* base, int n, int h, int w, int c,
+                           const int lower[2], const int upper[2], int stride_w, int stride_h,
+                           uint32_t channels, uint32_t pixels) {
+  MS_TRY(resolve_driver());
+  const size_t es = dtype_size(dt);
+  MS_CHECK_ARG((reinterpret_cast<uintptr_t>(base) & 15) == 0, MS_ERR_ALIGN,
+               "activation base %p not 16-byte aligned", base);
+  MS_CHECK_ARG((c * es) % 16 == 0, MS_ERR_ALIGN, "channels*%zu must be a multiple of 16 B", es);
+  cuuint64_t dims[4] = {(cuuint64_t)c, (cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)n};
+  cuuint64_t strides[3] = {(cuuint64_t)c * es, (cuuint64_t)c * w * es, (cuuint64_t)c * w * h * es};
+  cuuint32_t estr[4] = {1, (cuuint32_t)stride_w, (cuuint32_t)stride_h, 1};
+  CUresult r = g_encode_im2col(m, tma_dtype(dt), 4, const_cast<void*>(base), dims, strides, lower,
+                               upper, channels, pixels, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  MS_CHECK_ARG(r == CUDA_SUCCESS, MS_ERR_LAUNCH,
+               "cuTensorMapEncodeIm2col failed (%d): nhwc=%d,%d,%d,%d lower=(%d,%d) upper=(%d,%d) "
+               "stride=(%d,%d) box=%ux%u",
+               (int)r, n, h, w, c, lower[0], lower[1], upper[0], upper[1], stride_w, stride_h,
+               channels, pixels);
+  // Driver <= 13.1 mis-encodes one descriptor bit for small im2col tensors
+  // (same workaround as CUTLASS make_im2col_tma_copy_desc).
+  const uint64_t bytes = (uint64_t)n * h * w * c * es;
+  if (g_driver_version <= 13010 && bytes < 131072)
+    reinterpret_cast<uint64_t*>(m)[1] &= ~(1ull << 21);
+  return MS_OK;
+}
+
+// ------------------------------------------------------------------ dispatch
+template <int BN, int A_MN, int B_MN, int MODE>
+static ms_status launch_t(const TmapPack& tm, const GemmArgs& g, cudaStream_t st) {
+  auto kern = umma_gemm_kernel<BN, A_MN, B_MN, MODE>;
+  constexpr int smem = GemmCfg<BN, A_MN, B_MN, MODE>::SMEM_BYTES;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int grid = g.num_tiles < num_sms() ? g.num_tiles : num_sms();
+  if (grid <= 0) return MS_OK;
+  kern<<<grid, GEMM_THREADS, smem, st>>>(tm, g);
+  count_launch();
+  return launch_status("umma_gemm_kernel");
+}
+
+#define MS_BN_SWITCH(A, B, M)                                   \
+  switch (bn) {                                                 \
+    case 32: return launch_t<32, A, B, M>(tm, g, st);           \
+    case 64: return launch_t<64, A, B, M>(tm, g, st);           \
+    case 128: return launch_t<128, A, B, M>(tm, g, st);         \
+    case 256: return launch_t<256, A, B, M>(tm, g, st);         \
+    default: break;                                             \
+  }
+
+ms_status launch_umma(int bn, int a_mn, int b_mn, int mode, const TmapPack& tm,
+                      const GemmArgs& g, cudaStream_t st) {
+  if ((b_mn || mode == LOAD_CONV_WGRAD) && bn < 64) {
+    set_error("launch_umma: MN-major B needs BN >= 64");
+    return MS_ERR_UNSUPPORTED;
+  }
+  if (mode == LOAD_GEMM) {
+    if (!a_mn && !b_mn) { MS_BN_SWITCH(0, 0, LOAD_GEMM) }
+    if (!a_mn && b_mn) { MS_BN_SWITCH(0, 1, LOAD_GEMM) }
+    if (a_mn && b_mn) { MS_BN_SWITCH(1, 1, LOAD_GEMM) }
+  } else if (mode == LOAD_CONV_FPROP) {
+    MS_BN_SWITCH(0, 0, LOAD_CONV_FPROP)
+  } else if (mode == LOAD_CONV_DGRAD) {
+    MS_BN_SWITCH(0, 0, LOAD_CONV_DGRAD)
+  } else if (mode == LOAD_CONV_WGRAD) {
+    switch (bn) {
+      case 64: return launch_t<64, 1, 1, LOAD_CONV_WGRAD>(tm, g, st);
+      case 128: return launch_t<128, 1, 1, LOAD_CONV_WGRAD>(tm, g, st);
+      case 256: return launch_t<256, 1, 1, LOAD_CONV_WGRAD>(tm, g, st);
+      default: break;
+    }
+  }
+  set_error("launch_umma: unsupported (bn=%d a_mn=%d b_mn=%d mode=%d)", bn, a_mn, b_mn, mode);
+  return MS_ERR_UNSUPPORTED;
+}
+
+int pick_bn(int64_t other_tiles, int64_t ncols) {
+  if (ncols <= 32) return 32;
+  if (ncols <= 64) return 64;
+  int bn = 256;
+  while (bn > 64) {
+    const int64_t tiles = other_tiles * ((ncols + bn - 1) / bn);
+    if (tiles >= num_sms()) break;
+    bn >>= 1;
+  }
+  if (ncols <= 128 && bn > 128) bn = 128;
+  return bn;
+}
+
+}  // namespace ms

@@ -1,0 +1,40 @@
+// Host-side helpers: TMA tensor-map encoding (driver entry points resolved at
+// run time, so the library does not link libcuda), GEMM launch dispatch, and
+// the launch counter behind ms_launch_count().
+#pragma once
+
+#include <atomic>
+
+#include "umma_gemm.cuh"
+
+namespace ms {
+
+extern std::atomic<int64_t> g_launches;
+inline void count_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+inline CUtensorMapDataType tma_dtype(int dt) {
+  return dt == MS_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                       : (dt == MS_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                       : CU_TENSOR_MAP_DATA_TYPE_FLOAT32);
+}
+
+// 2-D row-major matrix [outer][inner] with row pitch `ld` elements,
+// box {box_inner, box_outer}, 128-byte swizzle, OOB -> zero.
+ms_status make_tmap_2d(CUtensorMap* m, int dt, const void* base, uint64_t inner, uint64_t outer,
+                       uint64_t ld, uint32_t box_inner, uint32_t box_outer);
+
+// NHWC activation [n][h][w][c] as an im2col tensor map.
+//   lower/upper: pixel bounding-box corners {w, h}; strides: traversal {w, h}
+ms_status make_tmap_im2col(CUtensorMap* m, int dt, const void* base, int n, int h, int w, int c,
+                           const int lower[2], const int upper[2], int stride_w, int stride_h,
+                           uint32_t channels, uint32_t pixels);
+
+// Runs umma_gemm_kernel<BN, A_MN, B_MN, MODE> with BN chosen at run time.
+ms_status launch_umma(int bn, int a_mn, int b_mn, int mode, const TmapPack& tm,
+                      const GemmArgs& g, cudaStream_t st);
+
+// Largest BN in {256,128,64,32} that still yields >= #SMs tiles (or the
+// smallest that covers N when N is tiny).
+int pick_bn(int64_t m_tiles_times_other, int64_t ncols);
+
+}  // namespace ms

@@ -1,0 +1,163 @@
+// Fully-connected layer: Z = X·Wᵀ + b, dX = G·W, dW = Gᵀ·X,
+// db = Σ G.  16-bit operands with 16-byte-aligned rows run on the tcgen05
+// kernel (A/B K-major or MN-major straight from the row-major tensors, no
+// transposes); float32 and unaligned shapes run on the SIMT kernel.
+#include "misc.cuh"
+
+namespace ms {
+
+namespace {
+
+bool is16(int dt) { return dt == MS_BF16 || dt == MS_F16; }
+bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+struct LinPlan {
+  bool tc = false;
+  int bn = 0;
+  int splits = 1;
+  int kb_per_split = 0;
+  int m_blocks = 0, n_blocks = 0, k_blocks = 0;
+  size_t ws = 0;
+};
+
+// rows x cols output, contraction red; b_mn: B operand MN-major (BN >= 64)
+LinPlan plan_gemm(int64_t rows, int64_t cols, int64_t red, bool b_mn, bool allow_split) {
+  LinPlan p;
+  p.tc = true;
+  p.m_blocks = (int)((rows + BM - 1) / BM);
+  p.bn = pick_bn(p.m_blocks, cols);
+  if (b_mn && p.bn < 64) p.bn = 64;
+  p.n_blocks = (int)((cols + p.bn - 1) / p.bn);
+  p.k_blocks = (int)((red + BK - 1) / BK);
+  const int64_t tiles = (int64_t)p.m_blocks * p.n_blocks;
+  p.splits = 1;
+  if (allow_split && tiles * 2 <= num_sms() && p.k_blocks >= 8) {
+    int64_t s = (num_sms() + tiles - 1) / tiles;
+    const int64_t cap = p.k_blocks / 4;
+    if (s > cap) s = cap;
+    if (s < 1) s = 1;
+    p.splits = (int)s;
+  }
+  p.kb_per_split = (p.k_blocks + p.splits - 1) / p.splits;
+  p.splits = (p.k_blocks + p.kb_per_split - 1) / p.kb_per_split;
+  if (p.splits > 1) p.ws = align256(sizeof(float) * (size_t)rows * cols);
+  return p;
+}
+
+LinPlan plan_linear(int64_t M, int64_t N, int64_t K, int dt, int pass) {
+  LinPlan p;
+  if (!is16(dt) || K % 8 || N % 8 || M <= 0 || N <= 0 || K <= 0) return p;  // SIMT
+  if (pass == 0) return plan_gemm(M, N, K, false, true);
+  if (pass == 1) return plan_gemm(M, K, N, true, true);
+  return plan_gemm(N, K, M, true, true);
+}
+
+ms_status run_gemm(const LinPlan& p, int dt, int a_mn, int b_mn, const CUtensorMap& ta,
+                   const CUtensorMap& tb, int64_t rows, int64_t cols, void* out, int64_t ldc,
+                   const void* bias, void* ws, size_t ws_bytes, cudaStream_t st) {
+  TmapPack tm;
+  tm.a[0] = ta;
+  tm.a[1] = ta;
+  tm.a[2] = ta;
+  tm.a[3] = ta;
+  tm.b = tb;
+  GemmArgs g{};
+  g.M = (int)rows;
+  g.N = (int)cols;
+  g.m_blocks = p.m_blocks;
+  g.n_blocks = p.n_blocks;
+  g.k_blocks = p.k_blocks;
+  g.splits = p.splits;
+  g.kb_per_split = p.kb_per_split;
+  g.taps = 1;
+  g.num_tiles = p.m_blocks * p.n_blocks * p.splits;
+  g.ab_fmt = dt == MS_BF16 ? 1 : 0;
+  g.nphases = 1;
+  if (p.splits > 1) {
+    MS_CHECK_ARG(ws && ws_bytes >= p.ws, MS_ERR_WORKSPACE, "linear: split-K workspace too small");
+    cudaMemsetAsync(ws, 0, sizeof(float) * rows * cols, st);
+    g.epi = EpiParams{ws, cols, MS_F32, 1, nullptr, 0};
+    MS_TRY(launch_umma(p.bn, a_mn, b_mn, LOAD_GEMM, tm, g, st));
+    MS_CHECK_ARG(ldc == cols, MS_ERR_UNSUPPORTED, "linear: split-K needs dense output");
+    return f32_to(static_cast<const float*>(ws), out, dt, rows * cols, bias, cols, st);
+  }
+  g.epi = EpiParams{out, ldc, dt, 0, bias, dt};
+  return launch_umma(p.bn, a_mn, b_mn, LOAD_GEMM, tm, g, st);
+}
+
+}  // namespace
+}  // namespace ms
+
+using namespace ms;
+
+extern "C" size_t ms_linear_workspace(int64_t M, int64_t N, int64_t K, int32_t dtype,
+                                      int32_t pass) {
+  return plan_linear(M, N, K, dtype, pass).ws;
+}
+
+extern "C" ms_status ms_linear_fwd(int64_t M, int64_t N, int64_t K, int32_t dt, const void* x,
+                                   const void* w, const void* bias, void* y, void* ws,
+                                   size_t ws_bytes, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  MS_CHECK_ARG(M >= 0 && N > 0 && K > 0, MS_ERR_SHAPE, "linear: bad shape");
+  if (M == 0) return MS_OK;
+  LinPlan p = plan_linear(M, N, K, dt, 0);
+  if (p.tc && al16(x) && al16(w) && al16(y)) {
+    CUtensorMap ta, tb;
+    MS_TRY(make_tmap_2d(&ta, dt, x, K, M, K, BK, BM));
+    MS_TRY(make_tmap_2d(&tb, dt, w, K, N, K, BK, p.bn));
+    return run_gemm(p, dt, 0, 0, ta, tb, M, N, y, N, bias, ws, ws_bytes, st);
+  }
+  // y[m,n] = sum_k x[m,k] w[n,k]
+  return simt_gemm(dt, (int)M, (int)N, (int)K, x, K, 1, w, 1, K, bias, y, N, st);
+}
+
+extern "C" ms_status ms_linear_dx(int64_t M, int64_t N, int64_t K, int32_t dt, const void* dy,
+                                  const void* w, void* dx, void* ws, size_t ws_bytes,
+                                  void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  MS_CHECK_ARG(M >= 0 && N > 0 && K > 0, MS_ERR_SHAPE, "linear dx: bad shape");
+  if (M == 0) return MS_OK;
+  LinPlan p = plan_linear(M, N, K, dt, 1);
+  if (p.tc && al16(dy) && al16(w) && al16(dx)) {
+    CUtensorMap ta, tb;
+    MS_TRY(make_tmap_2d(&ta, dt, dy, N, M, N, BK, BM));  // A = dY [M][N], K-major
+    MS_TRY(make_tmap_2d(&tb, dt, w, K, N, K, 64, BK));   // B = W [N][K], MN-major
+    return run_gemm(p, dt, 0, 1, ta, tb, M, K, dx, K, nullptr, ws, ws_bytes, st);
+  }
+  // dx[m,k] = sum_n dy[m,n] w[n,k]
+  return simt_gemm(dt, (int)M, (int)K, (int)N, dy, N, 1, w, K, 1, nullptr, dx, K, st);
+}
+
+extern "C" ms_status ms_linear_dw(int64_t M, int64_t N, int64_t K, int32_t dt, const void* x,
+                                  const void* dy, void* dw, void* ws, size_t ws_bytes,
+                                  void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  MS_CHECK_ARG(M >= 0 && N > 0 && K > 0, MS_ERR_SHAPE, "linear dw: bad shape");
+  if (M == 0) return cudaMemsetAsync(dw, 0, dtype_size(dt) * N * K, st) == cudaSuccess
+                         ? MS_OK
+                         : MS_ERR_LAUNCH;
+  LinPlan p = plan_linear(M, N, K, dt, 2);
+  if (p.tc && al16(dy) && al16(x) && al16(dw)) {
+    CUtensorMap ta, tb;
+    MS_TRY(make_tmap_2d(&ta, dt, dy, N, M, N, 64, BK));  // A = dYᵀ, MN-major
+    MS_TRY(make_tmap_2d(&tb, dt, x, K, M, K, 64, BK));   // B = X, MN-major
+    return run_gemm(p, dt, 1, 1, ta, tb, N, K, dw, K, nullptr, ws, ws_bytes, st);
+  }
+  // dw[n,k] = sum_m dy[m,n] x[m,k]
+  return simt_gemm(dt, (int)N, (int)K, (int)M, dy, 1, N, x, K, 1, nullptr, dw, K, st);
+}
+
+extern "C" size_t ms_bias_grad_workspace(int64_t rows, int64_t cols, int32_t dtype) {
+  (void)rows;
+  (void)dtype;
+  return colsum_workspace(cols);
+}
+
+extern "C" ms_status ms_bias_grad(int64_t rows, int64_t cols, int32_t dt, const void* g, void* db,
+                                  void* ws, size_t ws_bytes, void* stream) {
+  MS_CHECK_ARG(rows >= 0 && cols > 0, MS_ERR_SHAPE, "bias grad: bad shape");
+  MS_CHECK_ARG(ws && ws_bytes >= colsum_workspace(cols), MS_ERR_WORKSPACE,
+               "bias grad: workspace too small");
+  return colsum(rows, cols, dt, g, db, dt, ws, (cudaStream_t)stream);
+}

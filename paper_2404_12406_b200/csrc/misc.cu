@@ -1,0 +1,240 @@
+// Bandwidth helpers: bias-gradient reductions, fp32 -> output dtype casts,
+// conv weight repacks and the channel-pad copy used by the tcgen05 conv path.
+#include "misc.cuh"
+
+namespace ms {
+
+// ------------------------------------------------------------------ column sums
+// Row-major [rows][cols]; each thread owns 8 consecutive columns (16-byte loads
+// for 16-bit data) and strides over rows; warps reduce through smem; one fp32
+// atomic per column per block.
+template <typename T>
+__global__ void __launch_bounds__(256) colsum_kernel(int64_t rows, int64_t cols, const T* __restrict__ g,
+                                                    float* __restrict__ acc, int64_t rows_per_block) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t c0 = (blockIdx.x * 32 + lane) * 8;
+  float s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const int64_t r_begin = blockIdx.y * rows_per_block;
+  const int64_t r_end = min(rows, r_begin + rows_per_block);
+  if (c0 < cols) {
+    const bool vec = (c0 + 8 <= cols) && (cols % 8 == 0) && sizeof(T) == 2;
+    for (int64_t r = r_begin + warp; r < r_end; r += 8) {
+      const T* p = g + r * cols + c0;
+      if (vec) {
+        uint4 u = *reinterpret_cast<const uint4*>(p);
+        const T* e = reinterpret_cast<const T*>(&u);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s[j] += IO<T>::ld(e + j);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (c0 + j < cols) s[j] += IO<T>::ld(p + j);
+      }
+    }
+  }
+  __shared__ float red[8][256 + 8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) red[warp][lane * 8 + j] = s[j];
+  __syncthreads();
+  for (int i = threadIdx.x; i < 256; i += 256) {
+    float v = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) v += red[w][i];
+    const int64_t c = blockIdx.x * 256 + i;
+    if (c < cols) atomicAdd(acc + c, v);
+  }
+}
+
+// NCHW planes: block (plane chunk) reduces hw contiguous elements of one (n, c)
+template <typename T>
+__global__ void __launch_bounds__(256) planesum_kernel(int64_t n, int64_t c, int64_t hw,
+                                                       const T* __restrict__ g, float* __restrict__ acc) {
+  const int64_t plane = blockIdx.x;  // n*c planes
+  const int64_t ch = plane % c;
+  const T* p = g + plane * hw;
+  float s = 0;
+  for (int64_t i = threadIdx.x; i < hw; i += 256) s += IO<T>::ld(p + i);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  __shared__ float red[8];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0;
+    for (int i = 0; i < 8; ++i) t += red[i];
+    atomicAdd(acc + ch, t);
+  }
+}
+
+template <typename T>
+__global__ void f32_to_kernel(const float* __restrict__ src, T* __restrict__ dst, int64_t count,
+                              const T* __restrict__ bias, int64_t bias_period) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float v = src[i];
+    if (bias) v += IO<T>::ld(bias + (i % bias_period));
+    dst[i] = IO<T>::cvt(v);
+  }
+}
+
+static int grid_1d(int64_t total, int per_thread = 1) {
+  int64_t b = (total / per_thread + 255) / 256;
+  const int64_t cap = (int64_t)num_sms() * 32;
+  if (b < 1) b = 1;
+  return (int)(b < cap ? b : cap);
+}
+
+#define MS_DT_DISPATCH(dt, ...)                                    \
+  switch (dt) {                                                    \
+    case MS_F32: { using T = float; __VA_ARGS__; } break;          \
+    case MS_BF16: { using T = __nv_bfloat16; __VA_ARGS__; } break; \
+    case MS_F16: { using T = __half; __VA_ARGS__; } break;         \
+    default: set_error("bad dtype %d", dt); return MS_ERR_DTYPE;   \
+  }
+
+size_t colsum_workspace(int64_t cols) { return sizeof(float) * (size_t)cols; }
+
+ms_status f32_to(const float* src, void* dst, int dt, int64_t count, const void* bias,
+                 int64_t bias_period, cudaStream_t st) {
+  if (count <= 0) return MS_OK;
+  MS_DT_DISPATCH(dt, f32_to_kernel<T><<<grid_1d(count), 256, 0, st>>>(
+                         src, (T*)dst, count, (const T*)bias, bias_period > 0 ? bias_period : 1));
+  count_launch();
+  return launch_status("f32_to_kernel");
+}
+
+ms_status colsum(int64_t rows, int64_t cols, int dt, const void* g, void* db, int odt, void* ws,
+                 cudaStream_t st) {
+  float* acc = static_cast<float*>(ws);
+  cudaMemsetAsync(acc, 0, sizeof(float) * cols, st);
+  const int64_t gx = (cols + 255) / 256;
+  int64_t gy = ((int64_t)num_sms() * 4 + gx - 1) / gx;
+  int64_t per = (rows + gy - 1) / gy;
+  if (per < 64) per = 64;
+  gy = (rows + per - 1) / per;
+  if (gy < 1) gy = 1;
+  dim3 grid((unsigned)gx, (unsigned)gy);
+  MS_DT_DISPATCH(dt, colsum_kernel<T><<<grid, 256, 0, st>>>(rows, cols, (const T*)g, acc, per));
+  count_launch();
+  MS_TRY(launch_status("colsum_kernel"));
+  return f32_to(acc, db, odt, cols, nullptr, 1, st);
+}
+
+ms_status planesum(int64_t n, int64_t c, int64_t hw, int dt, const void* g, void* db, int odt,
+                   void* ws, cudaStream_t st) {
+  float* acc = static_cast<float*>(ws);
+  cudaMemsetAsync(acc, 0, sizeof(float) * c, st);
+  MS_DT_DISPATCH(dt, planesum_kernel<T><<<(unsigned)(n * c), 256, 0, st>>>(n, c, hw, (const T*)g, acc));
+  count_launch();
+  MS_TRY(launch_status("planesum_kernel"));
+  return f32_to(acc, db, odt, c, nullptr, 1, st);
+}
+
+// ------------------------------------------------------------------ repacks
+// Forward weight [k][tap][cpad] (K-major rows for the B operand) from OIHW/OHWI.
+template <typename T>
+__global__ void repack_fprop_kernel(int K, int C, int R, int S, int cpad, int wlayout,
+                                    const T* __restrict__ w, T* __restrict__ out) {
+  const int64_t total = (int64_t)K * R * S * cpad;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t t = i;
+    const int c = t % cpad; t /= cpad;
+    const int tap = t % (R * S); t /= (R * S);
+    const int k = (int)t;
+    const int r = tap / S, s = tap % S;
+    T v = IO<T>::cvt(0.f);
+    if (c < C)
+      v = wlayout == MS_NHWC ? w[(((int64_t)k * R + r) * S + s) * C + c]
+                             : w[(((int64_t)k * C + c) * R + r) * S + s];
+    out[i] = v;
+  }
+}
+
+// Input-VJP weight [c][tap][kpad] from OIHW/OHWI (B operand of the dgrad GEMM).
+template <typename T>
+__global__ void repack_dgrad_kernel(int K, int C, int R, int S, int kpad, int wlayout,
+                                    const T* __restrict__ w, T* __restrict__ out) {
+  const int64_t total = (int64_t)C * R * S * kpad;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t t = i;
+    const int k = t % kpad; t /= kpad;
+    const int tap = t % (R * S); t /= (R * S);
+    const int c = (int)t;
+    const int r = tap / S, s = tap % S;
+    T v = IO<T>::cvt(0.f);
+    if (k < K)
+      v = wlayout == MS_NHWC ? w[(((int64_t)k * R + r) * S + s) * C + c]
+                             : w[(((int64_t)k * C + c) * R + r) * S + s];
+    out[i] = v;
+  }
+}
+
+// fp32 [k][tap][c] accumulator -> weight gradient in OIHW/OHWI, dtype T
+template <typename T>
+__global__ void wgrad_finalize_kernel(int K, int C, int R, int S, int wlayout,
+                                      const float* __restrict__ acc, T* __restrict__ dw) {
+  const int64_t total = (int64_t)K * R * S * C;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t t = i;
+    const int c = t % C; t /= C;
+    const int tap = t % (R * S); t /= (R * S);
+    const int k = (int)t;
+    const int r = tap / S, s = tap % S;
+    const int64_t o = wlayout == MS_NHWC ? i : (((int64_t)k * C + c) * R + r) * S + s;
+    dw[o] = IO<T>::cvt(acc[i]);
+  }
+}
+
+// NHWC channel pad: [p][c] -> [p][cpad] (zeros in c..cpad)
+template <typename T>
+__global__ void pad_channels_kernel(int64_t pixels, int c, int cpad, const T* __restrict__ x,
+                                    T* __restrict__ out) {
+  const int64_t total = pixels * cpad;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int ch = i % cpad;
+    const int64_t p = i / cpad;
+    out[i] = ch < c ? x[p * c + ch] : IO<T>::cvt(0.f);
+  }
+}
+
+ms_status repack_fprop(int dt, int K, int C, int R, int S, int cpad, int wlayout, const void* w,
+                       void* out, cudaStream_t st) {
+  const int64_t total = (int64_t)K * R * S * cpad;
+  MS_DT_DISPATCH(dt, repack_fprop_kernel<T><<<grid_1d(total), 256, 0, st>>>(
+                         K, C, R, S, cpad, wlayout, (const T*)w, (T*)out));
+  count_launch();
+  return launch_status("repack_fprop_kernel");
+}
+
+ms_status repack_dgrad(int dt, int K, int C, int R, int S, int kpad, int wlayout, const void* w,
+                       void* out, cudaStream_t st) {
+  const int64_t total = (int64_t)C * R * S * kpad;
+  MS_DT_DISPATCH(dt, repack_dgrad_kernel<T><<<grid_1d(total), 256, 0, st>>>(
+                         K, C, R, S, kpad, wlayout, (const T*)w, (T*)out));
+  count_launch();
+  return launch_status("repack_dgrad_kernel");
+}
+
+ms_status wgrad_finalize(int dt, int K, int C, int R, int S, int wlayout, const float* acc,
+                         void* dw, cudaStream_t st) {
+  const int64_t total = (int64_t)K * R * S * C;
+  MS_DT_DISPATCH(dt, wgrad_finalize_kernel<T><<<grid_1d(total), 256, 0, st>>>(
+                         K, C, R, S, wlayout, acc, (T*)dw));
+  count_launch();
+  return launch_status("wgrad_finalize_kernel");
+}
+
+ms_status pad_channels(int dt, int64_t pixels, int c, int cpad, const void* x, void* out,
+                       cudaStream_t st) {
+  const int64_t total = pixels * cpad;
+  MS_DT_DISPATCH(dt, pad_channels_kernel<T><<<grid_1d(total), 256, 0, st>>>(
+                         pixels, c, cpad, (const T*)x, (T*)out));
+  count_launch();
+  return launch_status("pad_channels_kernel");
+}
+
+}  // namespace ms

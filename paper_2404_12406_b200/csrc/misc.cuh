@@ -1,0 +1,19 @@
+#pragma once
+
+#include "simt.cuh"
+
+namespace ms {
+
+ms_status repack_fprop(int dt, int K, int C, int R, int S, int cpad, int wlayout, const void* w,
+                       void* out, cudaStream_t st);
+ms_status repack_dgrad(int dt, int K, int C, int R, int S, int kpad, int wlayout, const void* w,
+                       void* out, cudaStream_t st);
+ms_status wgrad_finalize(int dt, int K, int C, int R, int S, int wlayout, const float* acc,
+                         void* dw, cudaStream_t st);
+ms_status pad_channels(int dt, int64_t pixels, int c, int cpad, const void* x, void* out,
+                       cudaStream_t st);
+
+inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+inline size_t align256(size_t v) { return (v + 255) & ~static_cast<size_t>(255); }
+
+}  // namespace ms

@@ -1,0 +1,165 @@
+"""Drop-in modules: ``MemSaveLinear``, ``MemSaveConv2d``, ``MemSaveBatchNorm2d``
+and the module swap ``convert_to_memory_saving`` (the ``memsave_torch.nn`` API
+named by the north star; the paper describes it at PAPER.md:244-253, the
+reference specifies the swap as ``convert_network``).
+
+Each ``MemSave*`` class subclasses its ``torch.nn`` counterpart, keeps the same
+constructor arguments, parameters, buffers and state_dict keys, and only
+replaces ``forward`` with the selective-save function from
+:mod:`paper_2404_12406_b200.functional`.
+"""
+
+from __future__ import annotations
+
+import torch
+from torch import nn
+
+from .. import functional as MF
+
+__all__ = ["MemSaveLinear", "MemSaveConv2d", "MemSaveBatchNorm2d", "convert_to_memory_saving"]
+
+
+def _share_params(dst: nn.Module, src: nn.Module, clone: bool) -> None:
+    for name, p in src.named_parameters(recurse=False):
+        if clone:
+            p = nn.Parameter(p.detach().clone(), requires_grad=p.requires_grad)
+        setattr(dst, name, p)
+    for name, b in src.named_buffers(recurse=False):
+        if b is not None and clone:
+            b = b.clone()
+        dst.register_buffer(name, b, persistent=name not in src._non_persistent_buffers_set)
+    dst.train(src.training)
+
+
+class MemSaveLinear(nn.Linear):
+    """nn.Linear whose autograd keeps X only if W needs a grad and W only if X
+    needs a grad (identical to stock torch for Linear, PAPER.md:609 / SPEC.md:248)."""
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        return MF.linear(x, self.weight, self.bias)
+
+    @classmethod
+    def from_nn_Linear(cls, linear: nn.Linear, clone_params: bool = False) -> "MemSaveLinear":
+        m = cls(linear.in_features, linear.out_features, bias=linear.bias is not None,
+                device="meta", dtype=linear.weight.dtype)
+        _share_params(m, linear, clone_params)
+        return m
+
+
+def _numeric_padding(conv: nn.Conv2d):
+    p = conv.padding
+    if isinstance(p, str):
+        if p == "valid":
+            return (0, 0)
+        # 'same' (stride 1): symmetric only
+        pads = []
+        for k, d in zip(conv.kernel_size, conv.dilation):
+            tot = d * (k - 1)
+            if tot % 2:
+                raise NotImplementedError("MemSaveConv2d: asymmetric 'same' padding is unsupported")
+            pads.append(tot // 2)
+        return tuple(pads)
+    return tuple(p)
+
+
+def conv2d_supported(conv: nn.Conv2d) -> bool:
+    """Variants the kernels implement: groups=1, dilation=1, zero padding mode."""
+    try:
+        _numeric_padding(conv)
+    except NotImplementedError:
+        return False
+    return (conv.groups == 1 and tuple(conv.dilation) == (1, 1)
+            and conv.padding_mode == "zeros" and type(conv).__name__ in ("Conv2d", "MemSaveConv2d"))
+
+
+class MemSaveConv2d(nn.Conv2d):
+    """nn.Conv2d that saves the input only if the weight needs a gradient and the
+    weight only if the input needs one (rules.py:68-71, MEMSAVE row)."""
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        if not conv2d_supported(self):
+            raise NotImplementedError("MemSaveConv2d supports groups=1, dilation=1, "
+                                      "padding_mode='zeros' only")
+        return MF.conv2d(x, self.weight, self.bias, self.stride, _numeric_padding(self))
+
+    @classmethod
+    def from_nn_Conv2d(cls, conv: nn.Conv2d, clone_params: bool = False) -> "MemSaveConv2d":
+        m = cls(conv.in_channels, conv.out_channels, conv.kernel_size, stride=conv.stride,
+                padding=conv.padding, dilation=conv.dilation, groups=conv.groups,
+                bias=conv.bias is not None, padding_mode=conv.padding_mode, device="meta",
+                dtype=conv.weight.dtype)
+        _share_params(m, conv, clone_params)
+        return m
+
+
+class MemSaveBatchNorm2d(nn.BatchNorm2d):
+    """nn.BatchNorm2d that, in eval mode, saves the input only if the weight needs
+    a gradient (rules.py:84-87, MEMSAVE row).  Training mode has
+    the same storage under both policies (rules.py:74-83) and runs the stock op."""
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        if self.training or not self.track_running_stats or self.running_mean is None:
+            return super().forward(x)
+        return MF.batch_norm_eval(x, self.running_mean, self.running_var, self.weight, self.bias,
+                                  self.eps)
+
+    @classmethod
+    def from_nn_BatchNorm2d(cls, bn: nn.BatchNorm2d,
+                            clone_params: bool = False) -> "MemSaveBatchNorm2d":
+        m = cls(bn.num_features, eps=bn.eps, momentum=bn.momentum, affine=bn.affine,
+                track_running_stats=bn.track_running_stats, device="meta",
+                dtype=(bn.weight.dtype if bn.weight is not None else None))
+        _share_params(m, bn, clone_params)
+        return m
+
+
+_MEMSAVE_TYPES = (MemSaveLinear, MemSaveConv2d, MemSaveBatchNorm2d)
+
+
+def _convert_one(mod: nn.Module, kinds: dict, clone_params: bool):
+    if isinstance(mod, _MEMSAVE_TYPES):
+        return None  # idempotent
+    if kinds.get("linear") and type(mod) is nn.Linear:
+        return MemSaveLinear.from_nn_Linear(mod, clone_params)
+    if kinds.get("conv2d") and type(mod) is nn.Conv2d and conv2d_supported(mod):
+        return MemSaveConv2d.from_nn_Conv2d(mod, clone_params)
+    if kinds.get("batchnorm2d") and type(mod) is nn.BatchNorm2d:
+        return MemSaveBatchNorm2d.from_nn_BatchNorm2d(mod, clone_params)
+    return None
+
+
+def convert_to_memory_saving(model: nn.Module, linear: bool = True, conv2d: bool = True,
+                             conv1d: bool = False, conv3d: bool = False,
+                             batchnorm2d: bool = True, relu: bool = False,
+                             maxpool2d: bool = False, layernorm: bool = False,
+                             dropout: bool = False, verbose: bool = False,
+                             clone_params: bool = False) -> nn.Module:
+    """Swap supported layers of ``model`` for their MemSave equivalents, in place.
+
+    Mirrors the reference ``convert_network(net, target, layer_filter)``
+    (SPEC.md:320-328): the boolean flags are the kind filter, conversion is
+    idempotent, parameters are shared with the original modules unless
+    ``clone_params``.  Kinds outside this package's hot path (conv1d/3d, ReLU,
+    MaxPool2d, LayerNorm, Dropout — SURVEY.md §8(f)) are accepted for API
+    compatibility and left untouched.  Returns the (possibly replaced) model.
+    """
+    kinds = {"linear": linear, "conv2d": conv2d, "batchnorm2d": batchnorm2d}
+    top = _convert_one(model, kinds, clone_params)
+    if top is not None:
+        if verbose:
+            print(f"memsave: {type(model).__name__} -> {type(top).__name__}")
+        return top
+
+    def walk(parent: nn.Module, prefix: str):
+        for name, child in list(parent.named_children()):
+            new = _convert_one(child, kinds, clone_params)
+            if new is not None:
+                setattr(parent, name, new)
+                if verbose:
+                    print(f"memsave: {prefix}{name}: {type(child).__name__} -> "
+                          f"{type(new).__name__}")
+            else:
+                walk(child, f"{prefix}{name}.")
+
+    walk(model, "")
+    return model

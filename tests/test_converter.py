@@ -1,0 +1,87 @@
+"""convert_to_memory_saving: kind filter, idempotence, parameter sharing,
+state_dict compatibility, unsupported variants untouched."""
+
+import torch
+from torch import nn
+
+import memsave_torch.nn as mnn
+from paper_2404_12406_b200.nn import (MemSaveBatchNorm2d, MemSaveConv2d, MemSaveLinear,
+                                      convert_to_memory_saving)
+
+
+def _net():
+    return nn.Sequential(
+        nn.Conv2d(3, 8, 3, padding=1, bias=False), nn.BatchNorm2d(8), nn.ReLU(),
+        nn.Sequential(nn.Conv2d(8, 8, 3, padding=1), nn.BatchNorm2d(8)),
+        nn.Conv2d(8, 8, 3, padding=2, dilation=2),       # dilation: unsupported
+        nn.Conv2d(8, 8, 3, padding=1, groups=2),         # groups: unsupported
+        nn.Flatten(), nn.Linear(8 * 4 * 4, 10))
+
+
+def test_alias_package_exports_same_objects():
+    assert mnn.convert_to_memory_saving is convert_to_memory_saving
+    assert mnn.MemSaveConv2d is MemSaveConv2d
+
+
+def test_convert_all_and_unsupported_untouched():
+    net = _net()
+    sd = {k: v.clone() for k, v in net.state_dict().items()}
+    params = [p for p in net.parameters()]
+    out = convert_to_memory_saving(net)
+    assert out is net
+    kinds = [type(m).__name__ for m in net.modules()]
+    assert kinds.count("MemSaveConv2d") == 2
+    assert kinds.count("MemSaveBatchNorm2d") == 2
+    assert kinds.count("MemSaveLinear") == 1
+    assert kinds.count("Conv2d") == 2  # dilated + grouped left alone
+    # parameters are shared, not copied: optimiser references stay valid
+    assert [id(p) for p in net.parameters()] == [id(p) for p in params]
+    # identical state_dict keys and values
+    sd2 = net.state_dict()
+    assert list(sd2) == list(sd)
+    for k in sd:
+        assert torch.equal(sd[k], sd2[k])
+
+
+def test_convert_is_idempotent():
+    net = convert_to_memory_saving(_net())
+    before = [(n, type(m)) for n, m in net.named_modules()]
+    convert_to_memory_saving(net)
+    assert [(n, type(m)) for n, m in net.named_modules()] == before
+
+
+def test_kind_filter():
+    net = convert_to_memory_saving(_net(), linear=False, batchnorm2d=False)
+    kinds = [type(m).__name__ for m in net.modules()]
+    assert "MemSaveConv2d" in kinds and "MemSaveLinear" not in kinds
+    assert "MemSaveBatchNorm2d" not in kinds
+
+
+def test_top_level_module_is_returned_converted():
+    lin = nn.Linear(4, 3)
+    out = convert_to_memory_saving(lin)
+    assert isinstance(out, MemSaveLinear) and out.weight is lin.weight
+
+
+def test_clone_params():
+    conv = nn.Conv2d(4, 4, 3)
+    m = MemSaveConv2d.from_nn_Conv2d(conv, clone_params=True)
+    assert m.weight is not conv.weight and torch.equal(m.weight, conv.weight)
+
+
+def test_bn_buffers_shared_and_train_mode_is_stock():
+    bn = nn.BatchNorm2d(4)
+    m = MemSaveBatchNorm2d.from_nn_BatchNorm2d(bn)
+    assert m.running_mean is bn.running_mean and m.running_var is bn.running_var
+    m.train()
+    x = torch.randn(3, 4, 5, 5)
+    ref = nn.BatchNorm2d(4)
+    torch.testing.assert_close(m(x), ref(x))  # training mode: stock semantics, stats updated
+    torch.testing.assert_close(m.running_mean, ref.running_mean)
+
+
+def test_cpu_tensors_fail_loudly():
+    import pytest
+    m = MemSaveLinear(4, 3)
+    with pytest.raises(RuntimeError, match="no CPU path"):
+        m(torch.randn(2, 4))

@@ -1,0 +1,263 @@
+"""GPU parity: the sm_100a kernels (through the C ABI, via the autograd
+functions) against the float64 oracle on the same quantised inputs.
+
+Tolerances (oracle/tolerance.py):
+  float32 — norm-wise rel ≤ 1e-5 and elementwise rtol 1e-5 (+1e-5·max|ref|)
+  bf16    — ≤ 1 bf16 ulp (+1 % max|ref| floor) of the rounded f64 oracle and
+            norm-wise rel ≤ 1e-3
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from mscases import CONV_CASES
+from paper_2404_12406_b200 import functional as MF
+from paper_2404_12406_b200 import launch_count
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda"
+TDT = {"bf16": torch.bfloat16, "f32": torch.float32, "fp16": torch.float16}
+
+
+def _close(a: torch.Tensor, ref64, dt, what, ulps=1.01):
+    a = a.detach().float().cpu().double().numpy()
+    if dt == "f32":
+        oracle.assert_close_fp32(a, ref64, what=what)
+    else:
+        oracle.assert_close_lowp(a, ref64, dt, ulps=ulps, what=what)
+
+
+def _q(arr, dt):
+    """numpy f64 -> (torch tensor on GPU in dt, the quantised f64 values)."""
+    t = torch.tensor(np.asarray(arr), dtype=torch.float64).to(TDT[dt])
+    return t.to(DEV), t.double().numpy()
+
+
+# ------------------------------------------------------------------ conv2d
+def _conv_check(x64, w64, g64, stride, pad, dt, channels_last, with_bias=False, rg=(1, 1, 1),
+                tag=""):
+    x, xq = _q(x64, dt)
+    w, wq = _q(w64, dt)
+    g, gq = _q(g64, dt)
+    b = bq = None
+    if with_bias:
+        b, bq = _q(np.linspace(-1, 1, w64.shape[0]), dt)
+    if channels_last:
+        x = x.contiguous(memory_format=torch.channels_last)
+        w = w.contiguous(memory_format=torch.channels_last)
+    x.requires_grad_(bool(rg[0]))
+    w.requires_grad_(bool(rg[1]))
+    if b is not None:
+        b.requires_grad_(bool(rg[2]))
+    n0 = launch_count()
+    y = MF.conv2d(x, w, b, stride, pad)
+    y_ref = oracle.conv2d_fwd(xq, wq, stride, pad)
+    if with_bias:
+        y_ref = y_ref + bq[None, :, None, None]
+    _close(y, y_ref, dt, f"{tag} y")
+    if any(rg):
+        y.backward(g.contiguous(memory_format=torch.channels_last) if channels_last else g)
+    assert launch_count() > n0  # the native library ran
+    h, wd = x64.shape[2:]
+    if rg[0]:
+        _close(x.grad, oracle.conv2d_dx(gq, wq, stride, pad, h, wd), dt, f"{tag} dx")
+    if rg[1]:
+        _close(w.grad, oracle.conv2d_dw(xq, gq, stride, pad, w64.shape[2], w64.shape[3]), dt,
+               f"{tag} dw")
+    if with_bias and rg[2]:
+        _close(b.grad, gq.sum(axis=(0, 2, 3)), dt, f"{tag} db")
+
+
+@pytest.mark.parametrize("case", CONV_CASES)
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+def test_conv_golden_vectors(conv_golden, case, dt):
+    g = conv_golden
+    n, cin, h, w, cout, k, s, p = (int(v) for v in g[f"{case}/geom"])
+    if dt == "f32":
+        # float32 against the reference outputs directly (inputs are exact f64 draws,
+        # quantised to f32; the golden outputs were computed in f64 by the reference)
+        x, xq = _q(g[f"{case}/x"], "f32")
+        wt, wq = _q(g[f"{case}/w"], "f32")
+        gy, gq = _q(g[f"{case}/g"], "f32")
+        x.requires_grad_(True)
+        wt.requires_grad_(True)
+        y = MF.conv2d(x, wt, None, s, p)
+        y.backward(gy)
+        _close(y, oracle.conv2d_fwd(xq, wq, s, p), "f32", f"{case} y")
+        _close(x.grad, oracle.conv2d_dx(gq, wq, s, p, h, w), "f32", f"{case} dx")
+        _close(wt.grad, oracle.conv2d_dw(xq, gq, s, p, k, k), "f32", f"{case} dw")
+        # and the quantisation-free check against the reference's own vectors
+        if case == "unit_1x1":
+            np.testing.assert_allclose(y.detach().cpu().double().numpy(), g[f"{case}/y"],
+                                       rtol=1e-6)
+    else:
+        _conv_check(g[f"{case}/x"], g[f"{case}/w"], g[f"{case}/g"], s, p, dt,
+                    channels_last=True, tag=case)
+
+
+# tcgen05 implicit-GEMM geometries (channel counts multiple of 8, NHWC, bf16)
+TC_CASES = [
+    # n, c, h, w, k, r, stride, pad
+    (2, 64, 14, 14, 128, 3, 1, 1),     # resnet 3x3 s1
+    (2, 128, 15, 13, 64, 3, 2, 1),     # 3x3 s2, odd sizes (dgrad phases with unequal extents)
+    (2, 64, 16, 16, 256, 1, 2, 0),     # 1x1 s2 downsample (phases without taps)
+    (3, 256, 7, 7, 512, 3, 1, 1),      # layer4-like, multiple N tiles
+    (2, 3, 32, 32, 64, 7, 2, 3),       # stem: 3 channels (padded activation copy)
+    (2, 32, 9, 9, 40, 3, 1, 1),        # C=32 (channel OOB fill), K=40 (N tail)
+    (1, 64, 10, 10, 64, 3, 1, 0),      # no padding
+    (2, 16, 12, 12, 24, 5, 1, 2),      # 5x5
+]
+
+
+@pytest.mark.parametrize("case", TC_CASES)
+def test_conv_tcgen05_bf16(case):
+    n, c, h, w, k, r, s, p = case
+    rng = np.random.default_rng(hash(case) % 2**32)
+    oh = (h + 2 * p - r) // s + 1
+    ow = (w + 2 * p - r) // s + 1
+    x = rng.standard_normal((n, c, h, w))
+    wt = rng.standard_normal((k, c, r, r)) / np.sqrt(c * r * r)
+    g = rng.standard_normal((n, k, oh, ow))
+    _conv_check(x, wt, g, s, p, "bf16", channels_last=True, with_bias=True, tag=str(case))
+
+
+def test_conv_tcgen05_many_tiles():
+    # > 148 tiles per launch: exercises the persistent tile loop and the TMEM
+    # double buffer (epilogue of tile i overlapping the main loop of tile i+1)
+    rng = np.random.default_rng(7)
+    x = rng.standard_normal((8, 64, 56, 56))
+    wt = rng.standard_normal((64, 64, 3, 3)) / 24
+    g = rng.standard_normal((8, 64, 56, 56))
+    _conv_check(x, wt, g, 1, 1, "bf16", channels_last=True, rg=(1, 1, 0), tag="many")
+
+
+@pytest.mark.parametrize("rg", [(1, 0, 0), (0, 1, 0), (0, 0, 1), (1, 1, 1)])
+def test_conv_selective_products(rg):
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((2, 64, 8, 8))
+    wt = rng.standard_normal((64, 64, 3, 3)) / 24
+    g = rng.standard_normal((2, 64, 8, 8))
+    _conv_check(x, wt, g, 1, 1, "bf16", channels_last=True, with_bias=True, rg=rg, tag=str(rg))
+
+
+def test_conv_nchw_bf16_and_fp16():
+    rng = np.random.default_rng(4)
+    x = rng.standard_normal((2, 16, 9, 9))
+    wt = rng.standard_normal((24, 16, 3, 3)) / 12
+    g = rng.standard_normal((2, 24, 5, 5))
+    _conv_check(x, wt, g, 2, 1, "bf16", channels_last=False, tag="nchw-bf16")
+    _conv_check(x, wt, g, 2, 1, "fp16", channels_last=True, tag="fp16")
+
+
+# ------------------------------------------------------------------ linear
+LIN_CASES = [
+    # lead dims, in, out
+    ((4, 96), 768, 768),      # BERT-like, M=384
+    ((300,), 512, 1000),      # fc with N tail
+    ((2, 70), 256, 64),       # M tail
+    ((8,), 4096, 256),        # tiny M, long K (split-K)
+    ((513,), 64, 8),          # N = 8
+]
+
+
+@pytest.mark.parametrize("case", LIN_CASES)
+@pytest.mark.parametrize("dt", ["bf16", "f32"])
+def test_linear(case, dt):
+    lead, fin, fout = case
+    rng = np.random.default_rng(fin + fout)
+    x, xq = _q(rng.standard_normal(lead + (fin,)), dt)
+    w, wq = _q(rng.standard_normal((fout, fin)) / np.sqrt(fin), dt)
+    b, bq = _q(rng.standard_normal(fout), dt)
+    g, gq = _q(rng.standard_normal(lead + (fout,)), dt)
+    for t in (x, w, b):
+        t.requires_grad_(True)
+    y = MF.linear(x, w, b)
+    y.backward(g)
+    _close(y, oracle.linear_fwd(xq, wq, bq), dt, "y")
+    _close(x.grad, oracle.linear_dx(gq, wq), dt, "dx")
+    _close(w.grad, oracle.linear_dw(xq, gq), dt, "dw")
+    _close(b.grad, oracle.linear_db(gq), dt, "db")
+
+
+def test_linear_golden(linbn_golden):
+    g = linbn_golden
+    for case in ("lin_small", "lin_3d"):
+        x, xq = _q(g[f"{case}/x"], "f32")
+        w, wq = _q(g[f"{case}/w"], "f32")
+        b, bq = _q(g[f"{case}/b"], "f32")
+        gy, gq = _q(g[f"{case}/g"], "f32")
+        for t in (x, w, b):
+            t.requires_grad_(True)
+        y = MF.linear(x, w, b)
+        y.backward(gy)
+        _close(y, oracle.linear_fwd(xq, wq, bq), "f32", f"{case} y")
+        _close(x.grad, oracle.linear_dx(gq, wq), "f32", f"{case} dx")
+        _close(w.grad, oracle.linear_dw(xq, gq), "f32", f"{case} dw")
+        _close(b.grad, oracle.linear_db(gq), "f32", f"{case} db")
+
+
+# ------------------------------------------------------------------ batchnorm (eval)
+@pytest.mark.parametrize("shape", [(2, 64, 7, 9), (3, 5, 4, 3), (4, 256, 14, 14), (2, 24, 8, 8)])
+@pytest.mark.parametrize("dt", ["bf16", "f32"])
+@pytest.mark.parametrize("channels_last", [False, True])
+def test_bn_eval(shape, dt, channels_last):
+    rng = np.random.default_rng(sum(shape))
+    c = shape[1]
+    x, xq = _q(rng.standard_normal(shape), dt)
+    w, wq = _q(rng.standard_normal(c), dt)
+    b, bq = _q(rng.standard_normal(c), dt)
+    m, mq = _q(0.1 * rng.standard_normal(c), dt)
+    v, vq = _q(0.5 + 1.5 * rng.random(c), dt)
+    g, gq = _q(rng.standard_normal(shape), dt)
+    if channels_last:
+        x = x.contiguous(memory_format=torch.channels_last)
+        g = g.contiguous(memory_format=torch.channels_last)
+    for t in (x, w, b):
+        t.requires_grad_(True)
+    eps = 1e-5
+    y = MF.batch_norm_eval(x, m, v, w, b, eps)
+    y.backward(g)
+    _close(y, oracle.bn_eval_fwd(xq, mq, vq, wq, bq, eps), dt, "y", ulps=2.01)
+    _close(x.grad, oracle.bn_eval_dx(gq, vq, wq, eps), dt, "dx", ulps=2.01)
+    _close(w.grad, oracle.bn_eval_dw(gq, xq, mq, vq, eps), dt, "dw", ulps=2.01)
+    _close(b.grad, oracle.bn_eval_db(gq), dt, "db", ulps=2.01)
+
+
+def test_bn_golden(linbn_golden):
+    g = linbn_golden
+    for case in ("bn_small", "bn_odd"):
+        ts = {k: _q(g[f"{case}/{k}"], "f32") for k in ("x", "w", "b", "mean", "var", "g")}
+        x, w, b = ts["x"][0], ts["w"][0], ts["b"][0]
+        for t in (x, w, b):
+            t.requires_grad_(True)
+        eps = float(g[f"{case}/eps"])
+        y = MF.batch_norm_eval(x, ts["mean"][0], ts["var"][0], w, b, eps)
+        y.backward(ts["g"][0])
+        q = {k: v[1] for k, v in ts.items()}
+        _close(y, oracle.bn_eval_fwd(q["x"], q["mean"], q["var"], q["w"], q["b"], eps), "f32", "y")
+        _close(x.grad, oracle.bn_eval_dx(q["g"], q["var"], q["w"], eps), "f32", "dx")
+        _close(w.grad, oracle.bn_eval_dw(q["g"], q["x"], q["mean"], q["var"], eps), "f32", "dw")
+        _close(b.grad, oracle.bn_eval_db(q["g"]), "f32", "db")
+
+
+# ------------------------------------------------------------------ saved set on CUDA
+@pytest.mark.parametrize("x_rg,w_rg", [(0, 0), (1, 0), (0, 1), (1, 1)])
+def test_saved_set_cuda(rules_golden, x_rg, w_rg):
+    x = torch.randn(2, 64, 8, 8, device=DEV, dtype=torch.bfloat16).contiguous(
+        memory_format=torch.channels_last).requires_grad_(bool(x_rg))
+    w = torch.randn(32, 64, 3, 3, device=DEV, dtype=torch.bfloat16).requires_grad_(bool(w_rg))
+    packed = []
+
+    def pack(t):
+        packed.append(tuple(t.shape))
+        return t
+
+    with torch.autograd.graph.saved_tensors_hooks(pack, lambda t: t):
+        MF.conv2d(x, w, None, 1, 1)
+    roles = sorted({(2, 64, 8, 8): "x", (32, 64, 3, 3): "w"}[s] for s in packed)
+    exp = [row for row in rules_golden if row["kind"] == "conv2d" and row["policy"] == "memsave"
+           and row["x_rg"] == bool(x_rg) and row["w_rg"] == bool(w_rg) and not row["b_rg"]][0]
+    assert roles == sorted(r for r, _ in exp["saves"])

@@ -1,0 +1,95 @@
+"""Pin the CPU oracle against golden vectors produced by the reference itself
+(oracle/gen_golden.py imports /root/reference/pkg/src/leantape)."""
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import conv as oconv
+from mscases import CONV_CASES
+
+
+@pytest.mark.parametrize("case", CONV_CASES)
+def test_conv_oracle_matches_reference_kernels(conv_golden, case):
+    g = conv_golden
+    n, cin, h, w, cout, k, s, p = (int(v) for v in g[f"{case}/geom"])
+    x, wt, gy = g[f"{case}/x"], g[f"{case}/w"], g[f"{case}/g"]
+    y = oconv.conv2d_fwd(x, wt, s, p)
+    np.testing.assert_allclose(y, g[f"{case}/y"], rtol=1e-12, atol=1e-12)
+    dx = oconv.conv2d_dx(gy, wt, s, p, h, w)
+    np.testing.assert_allclose(dx, g[f"{case}/dx"], rtol=1e-12, atol=1e-12)
+    dw = oconv.conv2d_dw(x, gy, s, p, k, k)
+    np.testing.assert_allclose(dw, g[f"{case}/dw"], rtol=1e-11, atol=1e-11)
+
+
+def test_conv_known_answers():
+    # 1x1 unit kernel is the identity; SPEC.md:257 — k3/s1/p1 preserves H, W
+    x = np.arange(20.0).reshape(1, 1, 4, 5)
+    assert np.array_equal(oconv.conv2d_fwd(x, np.ones((1, 1, 1, 1)), 1, 0), x)
+    y = oconv.conv2d_fwd(np.ones((2, 8, 9, 7)), np.ones((8, 8, 3, 3)), 1, 1)
+    assert y.shape == (2, 8, 9, 7)
+    # out size formula numpy_impl.py:15-16
+    assert oconv.conv_out_size(224, 7, 2, 3) == 112
+    assert oconv.conv_out_size(56, 1, 2, 0) == 28
+
+
+@pytest.mark.parametrize("case", ["lin_small", "lin_3d"])
+def test_linear_oracle_matches_spec_vectors(linbn_golden, case):
+    g = linbn_golden
+    x, w, b, gy = g[f"{case}/x"], g[f"{case}/w"], g[f"{case}/b"], g[f"{case}/g"]
+    np.testing.assert_allclose(oracle.linear_fwd(x, w, b), g[f"{case}/y"], rtol=1e-12)
+    np.testing.assert_allclose(oracle.linear_dx(gy, w), g[f"{case}/dx"], rtol=1e-12)
+    np.testing.assert_allclose(oracle.linear_dw(x, gy), g[f"{case}/dw"], rtol=1e-12)
+    np.testing.assert_allclose(oracle.linear_db(gy), g[f"{case}/db"], rtol=1e-12)
+
+
+def test_linear_identity_kat():
+    # W = identity, b = 0 -> Z = X
+    x = np.random.default_rng(0).standard_normal((3, 4))
+    assert np.allclose(oracle.linear_fwd(x, np.eye(4), np.zeros(4)), x)
+
+
+@pytest.mark.parametrize("case", ["bn_small", "bn_odd"])
+def test_bn_eval_oracle_matches_spec_vectors(linbn_golden, case):
+    g = linbn_golden
+    x, w, b, m, v, gy = (g[f"{case}/{k}"] for k in ("x", "w", "b", "mean", "var", "g"))
+    eps = float(g[f"{case}/eps"])
+    np.testing.assert_allclose(oracle.bn_eval_fwd(x, m, v, w, b, eps), g[f"{case}/y"], rtol=1e-12,
+                               atol=1e-12)
+    np.testing.assert_allclose(oracle.bn_eval_dx(gy, v, w, eps), g[f"{case}/dx"], rtol=1e-12)
+    np.testing.assert_allclose(oracle.bn_eval_dw(gy, x, m, v, eps), g[f"{case}/dw"], rtol=1e-11)
+    np.testing.assert_allclose(oracle.bn_eval_db(gy), g[f"{case}/db"], rtol=1e-12)
+
+
+def test_bn_eval_identity_kat():
+    # mu=0, var=1, eps=0, W=1, b=0 -> y = x
+    x = np.random.default_rng(1).standard_normal((2, 3, 4, 4))
+    y = oracle.bn_eval_fwd(x, np.zeros(3), np.ones(3), np.ones(3), np.zeros(3), 0.0)
+    assert np.allclose(y, x)
+
+
+def test_rules_oracle_matches_reference_table(rules_golden):
+    for row in rules_golden:
+        pol = oracle.Policy(row["policy"])
+        got = oracle.storage_decision(row["kind"], pol, x_rg=row["x_rg"], w_rg=row["w_rg"],
+                                      out_rg=row["out_rg"], bn_train=row["bn_train"])
+        assert [list(t) for t in got] == row["saves"], row
+
+
+def test_byte_size_kats(kat_golden):
+    # (256,8,256,256) F32 = 512 MiB; desk scale (4,8,32,32) = 128 KiB
+    assert kat_golden["byte_size_fig1_f32"] == 256 * 8 * 256 * 256 * 4 == 536870912
+    assert kat_golden["byte_size_desk_f32"] == 131072
+
+
+def test_tolerance_helpers():
+    r = np.array([1.0, -2.0, 3.0, 1e-3])
+    oracle.assert_close_fp32(r.astype(np.float32), r)
+    oracle.assert_close_lowp(oracle.round_to(r, "bf16"), r, "bf16")
+    with pytest.raises(AssertionError):
+        oracle.assert_close_lowp(oracle.round_to(r, "bf16") * 1.02, r, "bf16")
+    # round_to matches torch's bf16 rounding
+    import torch
+    v = np.random.default_rng(2).standard_normal(1000)
+    t = torch.tensor(v, dtype=torch.float64).to(torch.bfloat16).double().numpy()
+    assert np.array_equal(oracle.round_to(v, "bf16"), t)

@@ -1,0 +1,125 @@
+"""Saved-set identity (acceptance criterion 2).
+
+For every hot-path layer and every (x_rg, w_rg, b_rg) combination the tensors
+the autograd function hands to ``save_for_backward`` must equal the reference
+rule table (tests/golden/rules.json, generated from leantape.rules).  Runs on
+the ``meta`` device: shapes only, no arithmetic, no GPU.
+"""
+
+import itertools
+
+import pytest
+import torch
+
+from paper_2404_12406_b200 import functional as MF
+from paper_2404_12406_b200.rules import MissingSavedValue, saved_roles
+
+FLAGS = list(itertools.product([False, True], repeat=3))
+
+
+def _golden_saves(rules_golden, kind, x_rg, w_rg, b_rg, policy="memsave"):
+    for row in rules_golden:
+        if (row["kind"], row["policy"], row["x_rg"], row["w_rg"], row["b_rg"],
+                row["bn_train"]) == (kind, policy, x_rg, w_rg, b_rg, False):
+            return sorted(r for r, _k in row["saves"])
+    raise KeyError(kind)
+
+
+def _run(fn, tensors, roles_by_shape):
+    packed = []
+
+    def pack(t):
+        packed.append(tuple(t.shape))
+        return t
+
+    with torch.autograd.graph.saved_tensors_hooks(pack, lambda t: t):
+        out = fn(*tensors)
+    roles = sorted(roles_by_shape[s] for s in packed)
+    return out, roles
+
+
+def _make(shape, rg):
+    return torch.empty(shape, device="meta").requires_grad_(rg)
+
+
+@pytest.mark.parametrize("x_rg,w_rg,b_rg", FLAGS)
+def test_linear_saved_set(rules_golden, x_rg, w_rg, b_rg):
+    x, w, b = _make((6, 5, 7), x_rg), _make((3, 7), w_rg), _make((3,), b_rg)
+    out, roles = _run(MF.linear, (x, w, b), {(6, 5, 7): "x", (3, 7): "w"})
+    assert roles == _golden_saves(rules_golden, "linear", x_rg, w_rg, b_rg)
+    assert out.shape == (6, 5, 3)
+    if out.requires_grad:
+        out.sum().backward()  # sufficiency: no MissingSavedValue
+        assert (x.grad is not None) == x_rg and (w.grad is not None) == w_rg
+        assert (b.grad is not None) == b_rg
+
+
+@pytest.mark.parametrize("x_rg,w_rg,b_rg", FLAGS)
+def test_conv2d_saved_set(rules_golden, x_rg, w_rg, b_rg):
+    x, w, b = _make((2, 4, 9, 9), x_rg), _make((6, 4, 3, 3), w_rg), _make((6,), b_rg)
+    out, roles = _run(lambda *t: MF.conv2d(*t, stride=2, padding=1), (x, w, b),
+                      {(2, 4, 9, 9): "x", (6, 4, 3, 3): "w"})
+    assert roles == _golden_saves(rules_golden, "conv2d", x_rg, w_rg, b_rg)
+    assert out.shape == (2, 6, 5, 5)
+    if out.requires_grad:
+        out.sum().backward()
+        assert (x.grad is not None) == x_rg and (w.grad is not None) == w_rg
+
+
+@pytest.mark.parametrize("x_rg,w_rg,b_rg", FLAGS)
+def test_batchnorm2d_eval_saved_set(rules_golden, x_rg, w_rg, b_rg):
+    x, w, b = _make((2, 5, 4, 3), x_rg), _make((5,), w_rg), _make((5,), b_rg)
+    rm, rv = torch.empty(5, device="meta"), torch.empty(5, device="meta")
+    out, roles = _run(lambda x_, w_, b_: MF.batch_norm_eval(x_, rm, rv, w_, b_, 1e-5), (x, w, b),
+                      {(2, 5, 4, 3): "x", (5,): "w"})
+    assert roles == _golden_saves(rules_golden, "batchnorm2d", x_rg, w_rg, b_rg)
+    if out.requires_grad:
+        out.sum().backward()
+        assert (x.grad is not None) == x_rg and (w.grad is not None) == w_rg
+
+
+def test_bn_eval_input_scenario_saves_nothing_of_numel_size(rules_golden):
+    # Eval, x diff, W frozen: nothing sized O(numel) is saved
+    x = _make((2, 5, 4, 3), True)
+    w, b = _make((5,), False), _make((5,), False)
+    rm, rv = torch.empty(5, device="meta"), torch.empty(5, device="meta")
+    _out, roles = _run(lambda: MF.batch_norm_eval(x, rm, rv, w, b), (), {(5,): "w",
+                                                                          (2, 5, 4, 3): "x"})
+    assert "x" not in roles
+
+
+def test_saved_roles_is_the_linear_family():
+    assert saved_roles(False, False) == ()
+    assert saved_roles(True, False) == ("w",)
+    assert saved_roles(False, True) == ("x",)
+    assert saved_roles(True, True) == ("x", "w")
+
+
+def test_missing_saved_value_fires():
+    # The tripwire of errors.py:20-25: backward asking for an unsaved value raises.
+    from paper_2404_12406_b200.functional import _need
+    with pytest.raises(MissingSavedValue):
+        _need(None, "x", "conv2d dW")
+
+
+@pytest.mark.parametrize("kind", ["conv2d", "batchnorm2d"])
+def test_stock_torch_matches_naive_row(rules_golden, kind):
+    """Stock torch (CPU) is the reference's NAIVE policy for conv / BN-eval in the
+    Input scenario: X and W are saved although W is frozen (Fig. 2 of the paper)."""
+    x = torch.randn(2, 4, 6, 6, requires_grad=True)
+    packed = []
+
+    def pack(t):
+        packed.append(tuple(t.shape))
+        return t
+
+    with torch.autograd.graph.saved_tensors_hooks(pack, lambda t: t):
+        if kind == "conv2d":
+            w = torch.randn(3, 4, 3, 3)
+            torch.nn.functional.conv2d(x, w, padding=1)
+        else:
+            torch.nn.functional.batch_norm(x, torch.zeros(4), torch.ones(4), torch.ones(4),
+                                           torch.zeros(4), training=False)
+    naive = _golden_saves(rules_golden, kind, True, False, False, policy="naive")
+    assert naive == ["w", "x"]
+    assert (2, 4, 6, 6) in packed  # stock keeps X; MemSave does not
