@@ -1,0 +1,452 @@
+#!/usr/bin/env python
+"""Benchmark: fwd+bwd throughput and peak memory of the selective-save layers
+on B200 vs stock PyTorch (BASELINE.json metric), one JSON line on rank 0.
+
+    python bench.py [--gpus N --steps K --warmup W --config resnet18|fig1]
+    python bench.py --impl reference ...   # the reference's CPU algorithm, host cores
+
+Default workload = BASELINE.json configs[1]: ResNet-18, frozen weights,
+input-only gradient, batch 256x3x224x224 bf16, channels_last, eval-mode BN.
+A "step" = forward + cross-entropy + backward to the input (x.grad).  With N
+GPUs (torchrun) every rank runs the full per-GPU batch (weak scaling); the
+input-only workload has no trainable parameter, so the ranks are replicas and
+no collective runs in the data path.
+"""
+
+from __future__ import annotations
+
+import argparse
+import copy
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "peak fwd+bwd memory (MiB) and fwd+bwd samples/sec vs PyTorch, at 1/2/4/8 B200"
+
+
+def _peaks():
+    """Roofline denominators: MEASURED_PEAKS.json (driver-written), else the
+    profiling recipe's fallback."""
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return {"gbs": float(d["hbm_gbs"]), "tflops": float(d["bf16_tflops"]),
+                "tflops_sustained": float(d.get("bf16_tflops_sustained", d["bf16_tflops"])),
+                "source": "measured (MEASURED_PEAKS.json)"}
+    except Exception:
+        return {"gbs": 6650.0, "tflops": 1590.0, "tflops_sustained": 1400.0,
+                "source": "fallback (B200_PROFILING.md)"}
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.lines = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ GPU arm
+def _dist_setup(args):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif world == 1:
+        torch.cuda.set_device(local)
+    return world, rank, local
+
+
+def _barrier(world):
+    import torch.distributed as dist
+    if world > 1:
+        dist.barrier()
+
+
+def _max_over_ranks(v: float, world: int) -> float:
+    import torch
+    import torch.distributed as dist
+    if world == 1:
+        return v
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def run_arm(wl, model, batch_inputs, steps, warmup, world, dev, sync=None):
+    """Time `steps` fwd+bwd steps (device time, CUDA events, max over ranks)."""
+    import torch
+
+    x = batch_inputs[0]
+
+    def step():
+        if wl.input_requires_grad:
+            x.grad = None
+        for p in model.parameters():
+            p.grad = None
+        loss = wl.loss_fn(model, *batch_inputs)
+        loss.backward()
+        if sync is not None:
+            sync.finish()
+        return loss
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    _barrier(world)
+    torch.cuda.synchronize(dev)
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    start.record()
+    for _ in range(steps):
+        step()
+    end.record()
+    torch.cuda.synchronize(dev)
+    _barrier(world)
+    ms = start.elapsed_time(end)
+    return _max_over_ranks(ms, world), step
+
+
+def peak_memory(step, dev):
+    import torch
+    torch.cuda.synchronize(dev)
+    torch.cuda.empty_cache()
+    base = torch.cuda.memory_allocated(dev)
+    torch.cuda.reset_peak_memory_stats(dev)
+    step()
+    torch.cuda.synchronize(dev)
+    peak = torch.cuda.max_memory_allocated(dev)
+    return peak / 2**20, (peak - base) / 2**20
+
+
+def e2e_arm(wl, model, steps, warmup, world, dev, sync=None):
+    """Same step through the public API, inputs copied from pinned host memory
+    and the loss read back every step (H2D/D2H inside the timed region)."""
+    import torch
+
+    dev_inputs = wl.make_batch(wl.batch, dev)
+    host = [t.detach().cpu().pin_memory() for t in dev_inputs]
+    loss_host = torch.empty((), dtype=torch.float32).pin_memory()
+    h2d = sum(t.numel() * t.element_size() for t in host)
+    d2h = loss_host.numel() * loss_host.element_size()
+
+    if wl.input_requires_grad:
+        dev_inputs[0].requires_grad_(True)
+
+    def step():
+        with torch.no_grad():
+            for d, h in zip(dev_inputs, host):
+                d.copy_(h, non_blocking=True)
+        x = dev_inputs[0]
+        if wl.input_requires_grad:
+            x.grad = None
+        for p in model.parameters():
+            p.grad = None
+        loss = wl.loss_fn(model, *dev_inputs)
+        loss.backward()
+        if sync is not None:
+            sync.finish()
+        loss_host.copy_(loss.detach(), non_blocking=True)
+        return loss
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    _barrier(world)
+    torch.cuda.synchronize(dev)
+    s = torch.cuda.Event(enable_timing=True)
+    e = torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    s.record()
+    for _ in range(steps):
+        step()
+    e.record()
+    torch.cuda.synchronize(dev)
+    wall = time.perf_counter() - t0
+    ms = _max_over_ranks(s.elapsed_time(e), world)
+    return ms, wall, h2d, d2h
+
+
+def gpu_main(args):
+    import torch
+
+    import paper_2404_12406_b200 as pkg
+    from benchkit import kernels as KB
+    from benchkit import models as BM
+    from paper_2404_12406_b200.distributed import TrainableGradAllReduce
+    from paper_2404_12406_b200.nn import convert_to_memory_saving
+
+    world, rank, local = _dist_setup(args)
+    dev = torch.device("cuda", local)
+    peaks = _peaks()
+    pkg.lib()  # fail loudly if the native library is missing
+
+    builder = BM.WORKLOADS[args.config]
+    wl = builder(batch=args.batch) if args.batch else builder()
+    if world > 1 and args.config != "resnet18":
+        pass  # weak scaling: every rank keeps the full per-GPU batch
+    stock_model = copy.deepcopy(wl.model)
+    convert_to_memory_saving(wl.model)
+    inputs = list(wl.make_batch(wl.batch, dev))
+    if wl.input_requires_grad:
+        inputs[0].requires_grad_(True)
+    sync = TrainableGradAllReduce(wl.model) if world > 1 else None
+
+    # ---------------- memsave arm (the product)
+    n0 = pkg.launch_count()
+    fam0 = pkg.launch_stats()
+    with ClockSampler(local) as clocks:
+        ms, step = run_arm(wl, wl.model, inputs, args.steps, args.warmup, world, dev, sync)
+    launches = pkg.launch_count() - n0
+    fam1 = pkg.launch_stats()
+    # launches of the warm-up steps are included above; count one clean step too
+    n1 = pkg.launch_count()
+    step()
+    torch.cuda.synchronize(dev)
+    per_step_launches = pkg.launch_count() - n1
+    peak_mib, act_peak_mib = peak_memory(step, dev)
+    e2e_ms, e2e_wall, h2d, d2h = e2e_arm(wl, wl.model, args.steps, max(1, args.warmup // 2),
+                                         world, dev, sync)
+
+    samples = wl.batch * args.steps * world
+    value = samples / (ms / 1e3)
+    e2e_value = samples / (e2e_ms / 1e3)
+
+    # ---------------- stock arm (same weights, unconverted) for the "vs PyTorch" part
+    del step
+    inputs.clear()
+    stock = {}
+    if not args.no_stock:
+        torch.cuda.empty_cache()
+        sinputs = list(wl.make_batch(wl.batch, dev))
+        if wl.input_requires_grad:
+            sinputs[0].requires_grad_(True)
+        ssync = TrainableGradAllReduce(stock_model) if world > 1 else None
+        sms, sstep = run_arm(wl, stock_model, sinputs, args.steps, args.warmup, world, dev, ssync)
+        speak, sact = peak_memory(sstep, dev)
+        stock = {"value": samples / (sms / 1e3), "ms_per_step": sms / args.steps,
+                 "peak_mib": speak, "activation_peak_mib": sact,
+                 "impl": "torch %s stock modules (cuDNN/cuBLAS), same weights/inputs"
+                         % torch.__version__}
+        del sstep, sinputs
+        torch.cuda.empty_cache()
+
+    # ---------------- roofline of the dominant kernel (rank 0)
+    roof = None
+    layers = []
+    if rank == 0 and not args.no_roofline and args.config == "resnet18":
+        for (n, c, h, w, k, r, s, p, cnt) in BM.resnet18_conv_shapes(wl.batch):
+            for ent in KB.conv_roofline(n, c, h, w, k, r, s, p, dev, peaks, reps=5):
+                ent["count_per_step"] = cnt
+                layers.append(ent)
+        dom = max(layers, key=lambda e: e["ms"] * e["count_per_step"])
+        roof = {"bound": dom["bound"], "achieved": round(dom["achieved"], 2),
+                "peak": dom["peak"], "unit": dom["unit"], "frac": round(dom["frac"], 4),
+                "traffic": None, "kernel": "umma_gemm_kernel (%s)" % dom["kind"],
+                "geom": dom["geom"], "launch_ms": round(dom["ms"], 4),
+                "per_unit": "2*N*OH*OW*K*C*R*S flops per launch (implicit GEMM)",
+                "peak_source": peaks["source"] + ", burst (kernel timed alone)"}
+        total_conv_ms = sum(e["ms"] * e["count_per_step"] for e in layers)
+        roof["conv_share_of_step"] = round(total_conv_ms / (ms / args.steps), 3)
+        with open(os.path.join(ROOT, "gpurun_out" if os.path.isdir(
+                os.path.join(ROOT, "gpurun_out")) else ".", "bench_layers.json"), "w") as f:
+            json.dump(layers, f, indent=1)
+
+    # ---------------- CPU baseline (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(args.config, wl, min_seconds=args.cpu_seconds)
+
+    out = {
+        "metric": METRIC,
+        "value": round(value, 2),
+        "unit": "samples/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms / args.steps, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": str(wl.dtype).replace("torch.", "").replace("bfloat16", "bf16"),
+        "data": "synthetic (random-init weights, seeded normal inputs)",
+        "config": dict(wl.config, parallelism=(f"dp{world}" if world > 1 else "single"),
+                       l2="activations > 126 MB L2 (no explicit flush between steps)"),
+        "peak_mib": round(peak_mib, 1),
+        "activation_peak_mib": round(act_peak_mib, 1),
+        "stock": {k: (round(v, 3) if isinstance(v, float) else v) for k, v in stock.items()},
+        "speedup_vs_stock": (round(value / stock["value"], 3) if stock else None),
+        "peak_ratio_vs_stock": (round(peak_mib / stock["peak_mib"], 3) if stock else None),
+        "e2e": {"value": round(e2e_value, 2), "unit": "samples/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms / args.steps, 4),
+                "wall_s": round(e2e_wall, 3)},
+        "gpu_launches": launches,
+        "gpu_launches_per_step": per_step_launches,
+        "launch_families_timed_region": {k: fam1[k] - fam0[k] for k in fam1},
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "clocks": clocks.summary(),
+        "impl": "memsave_b200",
+    }
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------ CPU legs
+def cpu_baseline(config, wl=None, min_seconds=10.0):
+    """The reference algorithm (oracle port, numpy f32, all host cores) on a
+    bounded sample of the same workload."""
+    import numpy as np
+    import torch
+
+    from benchkit.cpu_port import ResNet18InputGradCPU, time_cpu
+    cores = os.cpu_count()
+    if config != "resnet18":
+        return None
+    if wl is None:
+        from benchkit import models as BM
+        wl = BM.resnet18_input_only(batch=1, dtype=torch.float32, device="cpu")
+    port = ResNet18InputGradCPU(wl.model.state_dict())
+    rng = np.random.default_rng(0)
+    nb = 1
+    x = rng.standard_normal((nb, 3, 224, 224)).astype(np.float32)
+    y = rng.integers(0, 1000, nb)
+    sec, calls = time_cpu(lambda: port.step(x, y), min_seconds=min_seconds)
+    return {"value": round(nb / sec, 4), "unit": "samples/s", "cores": cores, "kind": "port",
+            "sample": f"{calls} steps of 1 image (3x224x224) fp32: full ResNet-18 forward + "
+                      f"input-gradient backward through the oracle restatement of the "
+                      f"reference numpy conv (numpy_impl.py:12-38), BLAS on {cores} threads"}
+
+
+def reference_main(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    if args.config != "resnet18":
+        print(json.dumps({"impl": "reference", "unavailable": f"no CPU port for {args.config}"}))
+        return
+    import numpy as np
+    import torch
+
+    from benchkit import models as BM
+    from benchkit.cpu_port import ResNet18InputGradCPU
+    wl = BM.resnet18_input_only(batch=1, dtype=torch.float32, device="cpu")
+    port = ResNet18InputGradCPU(wl.model.state_dict())
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal((1, 3, 224, 224)).astype(np.float32)
+    y = rng.integers(0, 1000, 1)
+    for _ in range(max(1, args.warmup)):
+        port.step(x, y)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        port.step(x, y)
+    sec = (time.perf_counter() - t0) / args.steps
+    v = round(1.0 / sec, 4)
+    cores = os.cpu_count()
+    print(json.dumps({
+        "metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(sec * 1e3, 2), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": dict(wl.config, global_batch=1,
+                       note="each step is a bounded sample: 1 image of the 256-image batch"),
+        "impl": "reference",
+        "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cores, "kind": "port",
+                         "sample": "1 image per step, fp32, oracle restatement of the reference "
+                                   "numpy conv (the reference is Python and cannot travel)"},
+        "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="memsave", choices=["memsave", "reference"])
+    ap.add_argument("--config", default="resnet18", choices=["resnet18", "fig1"])
+    ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--no-stock", action="store_true")
+    ap.add_argument("--no-roofline", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "memsave":
+        args.warmup = 3  # timing rule: >= 3 warm-up steps
+    if args.impl == "reference":
+        reference_main(args)
+    else:
+        gpu_main(args)
+
+
+if __name__ == "__main__":
+    main()

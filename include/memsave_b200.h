@@ -131,6 +131,9 @@ MS_API const char* ms_last_error(void);
 MS_API int32_t ms_version(void);
 /* number of kernels this library has launched since load (all threads) */
 MS_API int64_t ms_launch_count(void);
+/* launches by kernel family: [0] tcgen05 GEMM/implicit-GEMM, [1] SIMT (CUDA-core)
+ * GEMM/conv, [2] batchnorm, [3] reductions / casts / repacks */
+MS_API void ms_launch_stats(int64_t* out4);
 
 #ifdef __cplusplus
 }

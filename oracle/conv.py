@@ -30,21 +30,23 @@ def conv_out_size(size: int, k: int, stride: int, padding: int) -> int:
     return (size + 2 * padding - k) // stride + 1
 
 
-def conv2d_fwd(x, w, stride=1, padding=0):
+def conv2d_fwd(x, w, stride=1, padding=0, dtype=np.float64):
     """out[b,co,i,j] = sum_{ci,p,q} x[b,ci,i*s-pad+p, j*s-pad+q] * w[co,ci,p,q].
 
     Follows numpy_impl.py:12-24 (pad + one einsum per kernel offset).
+    ``dtype`` is the accumulation dtype: float64 when checking; the CPU
+    baseline passes float32, which is what the reference computes in.
     """
     sh, sw = _pair(stride)
     ph, pw = _pair(padding)
-    x = np.asarray(x, dtype=np.float64)
-    w = np.asarray(w, dtype=np.float64)
+    x = np.asarray(x, dtype=dtype)
+    w = np.asarray(w, dtype=dtype)
     n, cin, h, wd = x.shape
     cout, _, kh, kw = w.shape
     oh = conv_out_size(h, kh, sh, ph)
     ow = conv_out_size(wd, kw, sw, pw)
     xp = np.pad(x, ((0, 0), (0, 0), (ph, ph), (pw, pw)))
-    out = np.zeros((n, cout, oh, ow), dtype=np.float64)
+    out = np.zeros((n, cout, oh, ow), dtype=dtype)
     for i in range(kh):
         for j in range(kw):
             xs = xp[:, :, i:i + sh * (oh - 1) + 1:sh, j:j + sw * (ow - 1) + 1:sw]
@@ -52,18 +54,18 @@ def conv2d_fwd(x, w, stride=1, padding=0):
     return out
 
 
-def conv2d_dx(g, w, stride, padding, h, wd):
+def conv2d_dx(g, w, stride, padding, h, wd, dtype=np.float64):
     """Input-VJP as a scatter (transpose conv), numpy_impl.py:27-38.
 
     ``h, wd`` are explicit because stride > 1 makes the input size ambiguous.
     """
     sh, sw = _pair(stride)
     ph, pw = _pair(padding)
-    g = np.asarray(g, dtype=np.float64)
-    w = np.asarray(w, dtype=np.float64)
+    g = np.asarray(g, dtype=dtype)
+    w = np.asarray(w, dtype=dtype)
     n, cout, oh, ow = g.shape
     _, cin, kh, kw = w.shape
-    dxp = np.zeros((n, cin, h + 2 * ph + sh, wd + 2 * pw + sw), dtype=np.float64)
+    dxp = np.zeros((n, cin, h + 2 * ph + sh, wd + 2 * pw + sw), dtype=dtype)
     for i in range(kh):
         for j in range(kw):
             contrib = np.einsum("nohw,oc->nchw", g, w[:, :, i, j], optimize=True)

@@ -9,7 +9,7 @@ Public API (drop-in for ``memsave_torch``):
 """
 
 from . import rules  # noqa: F401
-from ._lib import LIB_PATH, launch_count, lib  # noqa: F401
+from ._lib import LIB_PATH, launch_count, launch_stats, lib  # noqa: F401
 
 __version__ = "0.1.0"
 

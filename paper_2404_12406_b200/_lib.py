@@ -58,6 +58,7 @@ SIGNATURES = {
     "ms_last_error": (ctypes.c_char_p, []),
     "ms_version": (_c_i32, []),
     "ms_launch_count": (_c_i64, []),
+    "ms_launch_stats": (None, [ctypes.POINTER(_c_i64)]),
 }
 
 _lock = threading.Lock()
@@ -97,3 +98,13 @@ def check(status: int, what: str) -> None:
 
 def launch_count() -> int:
     return int(lib().ms_launch_count())
+
+
+FAMILIES = ("umma", "simt", "bn", "misc")
+
+
+def launch_stats() -> dict:
+    """Kernel launches since load, by family (tcgen05 GEMM, SIMT, BN, misc)."""
+    buf = (_c_i64 * 4)()
+    lib().ms_launch_stats(buf)
+    return dict(zip(FAMILIES, (int(v) for v in buf)))

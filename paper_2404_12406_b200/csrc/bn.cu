@@ -236,7 +236,7 @@ ms_status bn_eval_fwd(int64_t n, int64_t c, int64_t hw, int layout, int dt, cons
           total, (int)c, hw, layout, p, (const T*)x, (T*)y);
     }
   });
-  count_launch();
+  count_launch(1, KF_BN);
   return launch_status("bn_fwd_kernel");
 }
 
@@ -267,7 +267,7 @@ ms_status bn_eval_bwd(int64_t n, int64_t c, int64_t hw, int layout, int dt, cons
             total, (int)c, hw, layout, p, (const T*)g, (const T*)x, (T*)dx, acc_dw, acc_db);
       }
     });
-    count_launch();
+    count_launch(1, KF_BN);
     MS_TRY(launch_status("bn_bwd_kernel"));
   }
   if (dw) MS_TRY(f32_to(acc_dw, dw, p.pdtype, c, nullptr, 1, st));
@@ -289,6 +289,7 @@ extern "C" ms_status ms_bn_eval_fwd(int64_t n, int64_t c, int64_t hw, int32_t la
                                     int32_t pdtype, const void* x, const void* mean,
                                     const void* var, const void* weight, const void* bias,
                                     double eps, void* y, void* ws, size_t ws_bytes, void* stream) {
+  MS_TRY(ms::bind_device(y));
   (void)ws;
   (void)ws_bytes;
   MS_CHECK_ARG(n >= 0 && c > 0 && hw >= 0, MS_ERR_SHAPE, "batchnorm: bad shape");
@@ -303,6 +304,7 @@ extern "C" ms_status ms_bn_eval_bwd(int64_t n, int64_t c, int64_t hw, int32_t la
                                     const void* weight, double eps, void* dx_or_null,
                                     void* dw_or_null, void* db_or_null, void* ws, size_t ws_bytes,
                                     void* stream) {
+  MS_TRY(ms::bind_device(dy));
   MS_CHECK_ARG(n >= 0 && c > 0 && hw >= 0, MS_ERR_SHAPE, "batchnorm: bad shape");
   MS_CHECK_ARG(dy && mean && var, MS_ERR_SHAPE, "batchnorm bwd: null tensor");
   ms::BnParams p{mean, var, weight, nullptr, pdtype, (float)eps};

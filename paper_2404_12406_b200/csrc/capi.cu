@@ -21,3 +21,7 @@ const char* last_error();
 extern "C" const char* ms_last_error(void) { return ms::last_error(); }
 extern "C" int32_t ms_version(void) { return 1; }
 extern "C" int64_t ms_launch_count(void) { return ms::g_launches.load(); }
+
+extern "C" void ms_launch_stats(int64_t* out4) {
+  for (int i = 0; i < ms::KF_COUNT; ++i) out4[i] = ms::g_family[i].load();
+}

@@ -265,6 +265,7 @@ extern "C" ms_status ms_conv2d_fwd(const ms_conv_desc* d, const void* x, const v
                                    const void* bias, void* y, void* ws, size_t ws_bytes,
                                    void* stream) {
   MS_TRY(validate(d));
+  MS_TRY(bind_device(y));
   if (d->n == 0) return MS_OK;
   cudaStream_t st = (cudaStream_t)stream;
   ConvPlan p = plan(d, MS_CONV_FWD);
@@ -277,6 +278,7 @@ extern "C" ms_status ms_conv2d_fwd(const ms_conv_desc* d, const void* x, const v
 extern "C" ms_status ms_conv2d_dx(const ms_conv_desc* d, const void* dy, const void* w, void* dx,
                                   void* ws, size_t ws_bytes, void* stream) {
   MS_TRY(validate(d));
+  MS_TRY(bind_device(dx));
   if (d->n == 0) return MS_OK;
   cudaStream_t st = (cudaStream_t)stream;
   ConvPlan p = plan(d, MS_CONV_DX);
@@ -289,6 +291,7 @@ extern "C" ms_status ms_conv2d_dx(const ms_conv_desc* d, const void* dy, const v
 extern "C" ms_status ms_conv2d_dw(const ms_conv_desc* d, const void* x, const void* dy, void* dw,
                                   void* ws, size_t ws_bytes, void* stream) {
   MS_TRY(validate(d));
+  MS_TRY(bind_device(dw));
   cudaStream_t st = (cudaStream_t)stream;
   ConvPlan p = plan(d, MS_CONV_DW);
   MS_CHECK_ARG(ws_bytes >= p.ws && (p.ws == 0 || ws), MS_ERR_WORKSPACE,
@@ -306,6 +309,7 @@ extern "C" ms_status ms_conv2d_dw(const ms_conv_desc* d, const void* x, const vo
 extern "C" ms_status ms_conv2d_db(const ms_conv_desc* d, const void* dy, void* db, void* ws,
                                   size_t ws_bytes, void* stream) {
   MS_TRY(validate(d));
+  MS_TRY(bind_device(db));
   MS_CHECK_ARG(ws && ws_bytes >= colsum_workspace(d->k), MS_ERR_WORKSPACE,
                "conv db: workspace too small");
   const ConvDims c = dims_of(d);

@@ -10,6 +10,7 @@
 namespace ms {
 
 std::atomic<int64_t> g_launches{0};
+std::atomic<int64_t> g_family[KF_COUNT];
 
 static thread_local char t_err[512] = "";
 
@@ -26,6 +27,28 @@ ms_status launch_status(const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error("%s: %s", what, cudaGetErrorString(e));
+    return MS_ERR_LAUNCH;
+  }
+  return MS_OK;
+}
+
+ms_status bind_device(const void* p) {
+  // The autograd engine calls backward on its own device thread, where neither
+  // this library's runtime nor the driver API has a current context yet: bind
+  // the device that owns the operand before any driver call (tensor-map
+  // encoding) or launch.
+  int dev = -1;
+  if (p != nullptr) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) == cudaSuccess && a.type == cudaMemoryTypeDevice)
+      dev = a.device;
+    else
+      cudaGetLastError();
+  }
+  if (dev < 0) cudaGetDevice(&dev);
+  if (cudaSetDevice(dev) != cudaSuccess) {
+    set_error("cudaSetDevice(%d) failed", dev);
+    cudaGetLastError();
     return MS_ERR_LAUNCH;
   }
   return MS_OK;
@@ -147,7 +170,7 @@ static ms_status launch_t(const TmapPack& tm, const GemmArgs& g, cudaStream_t st
   const int grid = g.num_tiles < num_sms() ? g.num_tiles : num_sms();
   if (grid <= 0) return MS_OK;
   kern<<<grid, GEMM_THREADS, smem, st>>>(tm, g);
-  count_launch();
+  count_launch(1, KF_UMMA);
   return launch_status("umma_gemm_kernel");
 }
 

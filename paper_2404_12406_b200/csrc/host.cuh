@@ -9,8 +9,14 @@
 
 namespace ms {
 
+// launch counters by kernel family (ms_launch_stats)
+enum KernelFamily : int { KF_UMMA = 0, KF_SIMT = 1, KF_BN = 2, KF_MISC = 3, KF_COUNT = 4 };
 extern std::atomic<int64_t> g_launches;
-inline void count_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+extern std::atomic<int64_t> g_family[KF_COUNT];
+inline void count_launch(int n = 1, int family = KF_MISC) {
+  g_launches.fetch_add(n, std::memory_order_relaxed);
+  g_family[family].fetch_add(n, std::memory_order_relaxed);
+}
 
 inline CUtensorMapDataType tma_dtype(int dt) {
   return dt == MS_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16

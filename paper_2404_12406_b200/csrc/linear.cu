@@ -98,6 +98,7 @@ extern "C" size_t ms_linear_workspace(int64_t M, int64_t N, int64_t K, int32_t d
 extern "C" ms_status ms_linear_fwd(int64_t M, int64_t N, int64_t K, int32_t dt, const void* x,
                                    const void* w, const void* bias, void* y, void* ws,
                                    size_t ws_bytes, void* stream) {
+  MS_TRY(bind_device(y));
   cudaStream_t st = (cudaStream_t)stream;
   MS_CHECK_ARG(M >= 0 && N > 0 && K > 0, MS_ERR_SHAPE, "linear: bad shape");
   if (M == 0) return MS_OK;
@@ -115,6 +116,7 @@ extern "C" ms_status ms_linear_fwd(int64_t M, int64_t N, int64_t K, int32_t dt, 
 extern "C" ms_status ms_linear_dx(int64_t M, int64_t N, int64_t K, int32_t dt, const void* dy,
                                   const void* w, void* dx, void* ws, size_t ws_bytes,
                                   void* stream) {
+  MS_TRY(bind_device(dx));
   cudaStream_t st = (cudaStream_t)stream;
   MS_CHECK_ARG(M >= 0 && N > 0 && K > 0, MS_ERR_SHAPE, "linear dx: bad shape");
   if (M == 0) return MS_OK;
@@ -132,6 +134,7 @@ extern "C" ms_status ms_linear_dx(int64_t M, int64_t N, int64_t K, int32_t dt, c
 extern "C" ms_status ms_linear_dw(int64_t M, int64_t N, int64_t K, int32_t dt, const void* x,
                                   const void* dy, void* dw, void* ws, size_t ws_bytes,
                                   void* stream) {
+  MS_TRY(bind_device(dw));
   cudaStream_t st = (cudaStream_t)stream;
   MS_CHECK_ARG(M >= 0 && N > 0 && K > 0, MS_ERR_SHAPE, "linear dw: bad shape");
   if (M == 0) return cudaMemsetAsync(dw, 0, dtype_size(dt) * N * K, st) == cudaSuccess
@@ -156,6 +159,7 @@ extern "C" size_t ms_bias_grad_workspace(int64_t rows, int64_t cols, int32_t dty
 
 extern "C" ms_status ms_bias_grad(int64_t rows, int64_t cols, int32_t dt, const void* g, void* db,
                                   void* ws, size_t ws_bytes, void* stream) {
+  MS_TRY(bind_device(db));
   MS_CHECK_ARG(rows >= 0 && cols > 0, MS_ERR_SHAPE, "bias grad: bad shape");
   MS_CHECK_ARG(ws && ws_bytes >= colsum_workspace(cols), MS_ERR_WORKSPACE,
                "bias grad: workspace too small");

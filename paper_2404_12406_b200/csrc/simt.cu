@@ -96,7 +96,7 @@ ms_status simt_gemm(int dt, int M, int N, int K, const void* A, int64_t sam, int
       set_error("simt_gemm: bad dtype %d", dt);
       return MS_ERR_DTYPE;
   }
-  count_launch();
+  count_launch(1, KF_SIMT);
   return launch_status("simt_gemm_kernel");
 }
 
@@ -265,7 +265,7 @@ ms_status simt_conv_fwd(const ConvDims& d, int dt, int layout, int wlayout, cons
                          d, (const T*)x, act_strides(d, layout, false), (const T*)w,
                          wt_strides(d, wlayout), (const T*)bias, (T*)y,
                          act_strides(d, layout, true)));
-  count_launch();
+  count_launch(1, KF_SIMT);
   return launch_status("direct_conv_fwd_kernel");
 }
 
@@ -275,7 +275,7 @@ ms_status simt_conv_dx(const ConvDims& d, int dt, int layout, int wlayout, const
   MS_DT_DISPATCH(dt, direct_conv_dx_kernel<T><<<grid_for(total), 256, 0, st>>>(
                          d, (const T*)g, act_strides(d, layout, true), (const T*)w,
                          wt_strides(d, wlayout), (T*)dx, act_strides(d, layout, false)));
-  count_launch();
+  count_launch(1, KF_SIMT);
   return launch_status("direct_conv_dx_kernel");
 }
 
@@ -304,7 +304,7 @@ ms_status simt_conv_dw(const ConvDims& d, int dt, int layout, int wlayout, const
                          act_strides(d, layout, true), acc, per);
                  f64_to_weight_kernel<T><<<grid_for(kc * d.r * d.s), 256, 0, st>>>(
                      d, acc, (T*)dw, wt_strides(d, wlayout)));
-  count_launch(2);
+  count_launch(2, KF_SIMT);
   return launch_status("direct_conv_dw_kernel");
 }
 

@@ -14,7 +14,7 @@ import torch
 import oracle
 from mscases import CONV_CASES
 from paper_2404_12406_b200 import functional as MF
-from paper_2404_12406_b200 import launch_count
+from paper_2404_12406_b200 import launch_count, launch_stats
 
 pytestmark = pytest.mark.gpu
 
@@ -121,7 +121,11 @@ def test_conv_tcgen05_bf16(case):
     x = rng.standard_normal((n, c, h, w))
     wt = rng.standard_normal((k, c, r, r)) / np.sqrt(c * r * r)
     g = rng.standard_normal((n, k, oh, ow))
+    u0 = launch_stats()["umma"]
     _conv_check(x, wt, g, s, p, "bf16", channels_last=True, with_bias=True, tag=str(case))
+    used = launch_stats()["umma"] - u0
+    # fwd + dx always run on tcgen05; dw too when both channel counts are multiples of 8
+    assert used >= (3 if c % 8 == 0 else 2), used
 
 
 def test_conv_tcgen05_many_tiles():
@@ -174,8 +178,11 @@ def test_linear(case, dt):
     g, gq = _q(rng.standard_normal(lead + (fout,)), dt)
     for t in (x, w, b):
         t.requires_grad_(True)
+    u0 = launch_stats()["umma"]
     y = MF.linear(x, w, b)
     y.backward(g)
+    if dt == "bf16":
+        assert launch_stats()["umma"] - u0 == 3  # fwd, dX, dW on tcgen05
     _close(y, oracle.linear_fwd(xq, wq, bq), dt, "y")
     _close(x.grad, oracle.linear_dx(gq, wq), dt, "dx")
     _close(w.grad, oracle.linear_dw(xq, gq), dt, "dw")
