@@ -54,6 +54,8 @@ struct ConvPlan {
   bool repack = false;  // fwd: weight repacked into ws
   int cpad = 0;         // fwd: per-tap weight pitch (multiple of 64)
   int kpad = 0;         // dx: per-tap pitch of the repacked weight
+  bool c8 = false;      // fwd: 8-channel im2col variant (stem)
+  bool scatter = false; // dx: tiny-Cin col2im scatter variant (stem input gradient)
   size_t ws_pad = 0, ws_w = 0, ws_acc = 0;
   size_t ws = 0;
 };
@@ -76,15 +78,26 @@ ConvPlan plan(const ms_conv_desc* d, int pass) {
     p.tc = true;
     p.cpad8 = (int)(d->c < 8 ? 8 : round_up(d->c, 8));
     p.pad_x = p.cpad8 != d->c;
-    p.cpad = (int)round_up(p.cpad8, 64);
+    p.c8 = p.cpad8 == 8;
+    p.cpad = p.c8 ? 8 : (int)round_up(p.cpad8, 64);
     p.repack = !(d->wlayout == MS_NHWC && d->c % 64 == 0);
     if (p.pad_x) p.ws_pad = align256(es * (size_t)d->n * d->h * d->w * p.cpad8);
     if (p.repack) p.ws_w = align256(es * (size_t)d->k * taps * p.cpad);
     p.ws = p.ws_pad + p.ws_w;
   } else if (pass == MS_CONV_DX) {
-    if (d->k % 8 != 0 || d->stride_h > 2 || d->stride_w > 2) {
-      return p;  // SIMT
+    if (d->k % 8 != 0) return p;  // SIMT
+    const int64_t region = (int64_t)d->r * ((c.ow - 1) * d->stride_w + d->s) * d->c * 4;
+    if (d->c < 8 && region <= SCATTER_REGION_BYTES && d->r * d->s * d->c <= 1024) {
+      // tiny input-channel count (the stem): dY x W GEMM + col2im scatter
+      p.tc = true;
+      p.scatter = true;
+      p.kpad = (int)round_up(d->k, 64);
+      p.ws_w = align256(es * (size_t)taps * d->c * p.kpad);
+      p.ws_acc = align256(sizeof(float) * (size_t)d->n * d->h * d->w * d->c);
+      p.ws = p.ws_w + p.ws_acc;
+      return p;
     }
+    if (d->stride_h > 2 || d->stride_w > 2) return p;  // SIMT
     p.tc = true;
     p.kpad = (int)round_up(d->k, 64);
     p.ws_w = align256(es * (size_t)d->c * taps * p.kpad);
@@ -134,25 +147,56 @@ ms_status fwd_tc(const ms_conv_desc* d, const ConvPlan& p, const void* x, const 
   const int bn = pick_bn(g.m_blocks, c.k);
   g.n_blocks = (c.k + bn - 1) / bn;
   g.num_tiles = g.m_blocks * g.n_blocks;
+  g.k_blocks = (c.r * c.s + 7) / 8;  // C8 variant: 8 taps per k-block
   g.cv = ConvShape{c.n, c.h, c.w, p.cpad8, c.oh, c.ow, c.r, c.s, c.sh, c.sw, c.ph, c.pw,
-                   p.cpad / 64, p.cpad, c.oh, c.ow};
+                   p.c8 ? 1 : p.cpad / 64, p.cpad, c.oh, c.ow};
   g.epi = EpiParams{y, c.k, dt, 0, bias, dt};
   TmapPack tm;
   const int lower[2] = {-c.pw, -c.ph};
   const int upper[2] = {c.pw - (c.s - 1), c.ph - (c.r - 1)};
   MS_TRY(make_tmap_im2col(&tm.a[0], dt, xsrc, c.n, c.h, c.w, p.cpad8, lower, upper, c.sw, c.sh,
-                          64, BM));
+                          p.c8 ? 8 : 64, BM, !p.c8));
   tm.a[1] = tm.a[2] = tm.a[3] = tm.a[0];
   const int64_t wrow = (int64_t)c.r * c.s * p.cpad;
   MS_TRY(make_tmap_2d(&tm.b, dt, wsrc, wrow, c.k, wrow, BK, bn));
-  return launch_umma(bn, 0, 0, LOAD_CONV_FPROP, tm, g, st);
+  return launch_umma(bn, 0, 0, p.c8 ? LOAD_CONV_FPROP_C8 : LOAD_CONV_FPROP, tm, g, st);
 }
 
 // ----------------------------------------------------------------- input-VJP
+ms_status dx_scatter(const ms_conv_desc* d, const ConvPlan& p, const void* dy, const void* w,
+                     void* dx, void* ws, cudaStream_t st) {
+  const ConvDims c = dims_of(d);
+  const int dt = d->dtype;
+  uint8_t* wsb = static_cast<uint8_t*>(ws);
+  void* wt = wsb;
+  float* acc = reinterpret_cast<float*>(wsb + p.ws_w);
+  MS_TRY(repack_scatter(dt, c.k, c.c, c.r, c.s, p.kpad, d->wlayout, w, wt, st));
+  const int64_t outn = (int64_t)c.n * c.h * c.w * c.c;
+  cudaMemsetAsync(acc, 0, sizeof(float) * outn, st);
+  const int ncols = c.r * c.s * c.c;
+  const int bn = ncols <= 32 ? 32 : (ncols <= 64 ? 64 : (ncols <= 128 ? 128 : 256));
+  GemmArgs g = base_args(dt);
+  g.M = c.n * c.oh * c.ow;
+  g.N = ncols;
+  g.n_blocks = (ncols + bn - 1) / bn;
+  g.k_blocks = p.kpad / 64;
+  g.num_tiles = c.n * c.oh * g.n_blocks;
+  g.cv = ConvShape{c.n, c.oh, c.ow, c.c, c.oh, c.ow, c.r, c.s, c.sh, c.sw, c.ph, c.pw,
+                   p.kpad / 64, p.kpad, c.h, c.w};
+  g.epi = EpiParams{acc, 0, MS_F32, 1, nullptr, 0};
+  TmapPack tm;
+  MS_TRY(make_tmap_2d(&tm.a[0], dt, dy, c.k, (uint64_t)c.n * c.oh * c.ow, c.k, BK, BM));
+  tm.a[1] = tm.a[2] = tm.a[3] = tm.a[0];
+  MS_TRY(make_tmap_2d(&tm.b, dt, wt, p.kpad, ncols, p.kpad, BK, bn));
+  MS_TRY(launch_umma(bn, 0, 0, LOAD_CONV_DGRAD_SCATTER, tm, g, st));
+  return f32_to(acc, dx, dt, outn, nullptr, 1, st);
+}
+
 ms_status dx_tc(const ms_conv_desc* d, const ConvPlan& p, const void* dy, const void* w, void* dx,
                 void* ws, cudaStream_t st) {
   const ConvDims c = dims_of(d);
   const int dt = d->dtype;
+  if (p.scatter) return dx_scatter(d, p, dy, w, dx, ws, st);
   void* wd = ws;
   MS_TRY(repack_dgrad(dt, c.k, c.c, c.r, c.s, p.kpad, d->wlayout, w, wd, st));
   GemmArgs g = base_args(dt);

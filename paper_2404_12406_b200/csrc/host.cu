@@ -135,7 +135,7 @@ ms_status make_tmap_2d(CUtensorMap* m, int dt, const void* base, uint64_t inner,
 
 ms_status make_tmap_im2col(CUtensorMap* m, int dt, const void* base, int n, int h, int w, int c,
                            const int lower[2], const int upper[2], int stride_w, int stride_h,
-                           uint32_t channels, uint32_t pixels) {
+                           uint32_t channels, uint32_t pixels, bool swizzle128) {
   MS_TRY(resolve_driver());
   const size_t es = dtype_size(dt);
   MS_CHECK_ARG((reinterpret_cast<uintptr_t>(base) & 15) == 0, MS_ERR_ALIGN,
@@ -146,7 +146,8 @@ ms_status make_tmap_im2col(CUtensorMap* m, int dt, const void* base, int n, int 
   cuuint32_t estr[4] = {1, (cuuint32_t)stride_w, (cuuint32_t)stride_h, 1};
   CUresult r = g_encode_im2col(m, tma_dtype(dt), 4, const_cast<void*>(base), dims, strides, lower,
                                upper, channels, pixels, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                               swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   MS_CHECK_ARG(r == CUDA_SUCCESS, MS_ERR_LAUNCH,
                "cuTensorMapEncodeIm2col failed (%d): nhwc=%d,%d,%d,%d lower=(%d,%d) upper=(%d,%d) "
@@ -197,6 +198,10 @@ ms_status launch_umma(int bn, int a_mn, int b_mn, int mode, const TmapPack& tm,
     MS_BN_SWITCH(0, 0, LOAD_CONV_FPROP)
   } else if (mode == LOAD_CONV_DGRAD) {
     MS_BN_SWITCH(0, 0, LOAD_CONV_DGRAD)
+  } else if (mode == LOAD_CONV_FPROP_C8) {
+    MS_BN_SWITCH(0, 0, LOAD_CONV_FPROP_C8)
+  } else if (mode == LOAD_CONV_DGRAD_SCATTER) {
+    MS_BN_SWITCH(0, 0, LOAD_CONV_DGRAD_SCATTER)
   } else if (mode == LOAD_CONV_WGRAD) {
     switch (bn) {
       case 64: return launch_t<64, 1, 1, LOAD_CONV_WGRAD>(tm, g, st);

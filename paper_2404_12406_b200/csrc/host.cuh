@@ -33,7 +33,7 @@ ms_status make_tmap_2d(CUtensorMap* m, int dt, const void* base, uint64_t inner,
 //   lower/upper: pixel bounding-box corners {w, h}; strides: traversal {w, h}
 ms_status make_tmap_im2col(CUtensorMap* m, int dt, const void* base, int n, int h, int w, int c,
                            const int lower[2], const int upper[2], int stride_w, int stride_h,
-                           uint32_t channels, uint32_t pixels);
+                           uint32_t channels, uint32_t pixels, bool swizzle128 = true);
 
 // Runs umma_gemm_kernel<BN, A_MN, B_MN, MODE> with BN chosen at run time.
 ms_status launch_umma(int bn, int a_mn, int b_mn, int mode, const TmapPack& tm,

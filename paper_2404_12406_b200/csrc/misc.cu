@@ -171,6 +171,27 @@ __global__ void repack_dgrad_kernel(int K, int C, int R, int S, int kpad, int wl
   }
 }
 
+// Scatter input-VJP weight [(tap, c)][kpad] (row = one output column of the
+// dY x W GEMM) from OIHW/OHWI.
+template <typename T>
+__global__ void repack_scatter_kernel(int K, int C, int R, int S, int kpad, int wlayout,
+                                      const T* __restrict__ w, T* __restrict__ out) {
+  const int64_t total = (int64_t)R * S * C * kpad;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t t = i;
+    const int k = t % kpad; t /= kpad;
+    const int c = t % C; t /= C;
+    const int tap = (int)t;
+    const int r = tap / S, s = tap % S;
+    T v = IO<T>::cvt(0.f);
+    if (k < K)
+      v = wlayout == MS_NHWC ? w[(((int64_t)k * R + r) * S + s) * C + c]
+                             : w[(((int64_t)k * C + c) * R + r) * S + s];
+    out[i] = v;
+  }
+}
+
 // fp32 [k][tap][c] accumulator -> weight gradient in OIHW/OHWI, dtype T
 template <typename T>
 __global__ void wgrad_finalize_kernel(int K, int C, int R, int S, int wlayout,
@@ -217,6 +238,15 @@ ms_status repack_dgrad(int dt, int K, int C, int R, int S, int kpad, int wlayout
                          K, C, R, S, kpad, wlayout, (const T*)w, (T*)out));
   count_launch();
   return launch_status("repack_dgrad_kernel");
+}
+
+ms_status repack_scatter(int dt, int K, int C, int R, int S, int kpad, int wlayout, const void* w,
+                         void* out, cudaStream_t st) {
+  const int64_t total = (int64_t)R * S * C * kpad;
+  MS_DT_DISPATCH(dt, repack_scatter_kernel<T><<<grid_1d(total), 256, 0, st>>>(
+                         K, C, R, S, kpad, wlayout, (const T*)w, (T*)out));
+  count_launch();
+  return launch_status("repack_scatter_kernel");
 }
 
 ms_status wgrad_finalize(int dt, int K, int C, int R, int S, int wlayout, const float* acc,

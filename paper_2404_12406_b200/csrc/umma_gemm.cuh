@@ -21,7 +21,15 @@
 
 namespace ms {
 
-enum : int { LOAD_GEMM = 0, LOAD_CONV_FPROP = 1, LOAD_CONV_DGRAD = 2, LOAD_CONV_WGRAD = 3 };
+enum : int {
+  LOAD_GEMM = 0,
+  LOAD_CONV_FPROP = 1,
+  LOAD_CONV_DGRAD = 2,
+  LOAD_CONV_WGRAD = 3,
+  LOAD_CONV_FPROP_C8 = 4,    // 8-channel activations: 8 taps x 8 ch per k-block, no swizzle
+  LOAD_CONV_DGRAD_SCATTER = 5  // tiny-Cin input-VJP: dY rows x (tap,c) GEMM + col2im scatter
+};
+constexpr int SCATTER_REGION_BYTES = 32 * 1024;
 
 constexpr int BM = 128;        // UMMA M (cta_group::1)
 constexpr int BK = 64;         // K elements per stage (128 bytes of bf16)
@@ -103,6 +111,13 @@ __device__ __forceinline__ TileInfo decode_tile(const GemmArgs& g, int t) {
     ti.nb = lt / P.m_blocks;
     ti.kb_begin = 0;
     ti.kb_end = P.nr * P.ns * g.cv.cblocks;
+  } else if constexpr (MODE == LOAD_CONV_DGRAD_SCATTER) {
+    // one tile = one dY row (n, oh): rows ow in [0, Q) of the [N*P*Q][K] matrix
+    const int row = t / g.n_blocks;
+    ti.nb = t - row * g.n_blocks;
+    ti.m0 = row;  // row index (n*P + oh); the A coordinate is row*Q
+    ti.kb_begin = 0;
+    ti.kb_end = g.k_blocks;
   } else {
     const int mb = t % g.m_blocks;
     int rest = t / g.m_blocks;
@@ -117,6 +132,9 @@ __device__ __forceinline__ TileInfo decode_tile(const GemmArgs& g, int t) {
     } else if constexpr (MODE == LOAD_CONV_FPROP) {
       ti.kb_begin = 0;
       ti.kb_end = g.cv.R * g.cv.S * g.cv.cblocks;
+    } else if constexpr (MODE == LOAD_CONV_FPROP_C8) {
+      ti.kb_begin = 0;
+      ti.kb_end = g.k_blocks;
     } else {
       const int split = rest;
       ti.kb_begin = split * g.kb_per_split;
@@ -131,9 +149,11 @@ struct GemmCfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
+  static constexpr int EXTRA = MODE == LOAD_CONV_DGRAD_SCATTER ? SCATTER_REGION_BYTES : 0;
+  static constexpr int STAGES_MAX = (200 * 1024 - EXTRA) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_MAX > 8 ? 8 : STAGES_MAX;
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EXTRA + 1024 /*align*/ + 256 /*barriers*/;
 };
 
 template <int BN, int A_MN, int B_MN, int MODE>
@@ -148,7 +168,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* ring = smem;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+  float* region = reinterpret_cast<float*>(smem + STAGES * Cfg::STAGE_BYTES);  // scatter mode
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES + Cfg::EXTRA);
   uint64_t* full_bar = bars;
   uint64_t* empty_bar = bars + STAGES;
   uint64_t* tfull_bar = bars + 2 * STAGES;
@@ -171,6 +192,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     tma_prefetch_desc(&tm.b);
     tma_prefetch_desc(&tm.a[0]);
   }
+  if constexpr (MODE == LOAD_CONV_DGRAD_SCATTER)
+    for (int i = threadIdx.x; i < SCATTER_REGION_BYTES / 4; i += blockDim.x) region[i] = 0.f;
   if (warp == 1) tmem_alloc(smem_u32(tmem_holder), Cfg::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
@@ -188,7 +211,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         // per-tile conv coordinates
         int cn = 0, ch = 0, cw = 0;
         const CUtensorMap* amap = &tm.a[0];
-        if constexpr (MODE == LOAD_CONV_FPROP) {
+        if constexpr (MODE == LOAD_CONV_FPROP || MODE == LOAD_CONV_FPROP_C8) {
           const int pq = g.cv.P * g.cv.Q;
           cn = ti.m0 / pq;
           int rem = ti.m0 - cn * pq;
@@ -231,6 +254,24 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             const int r = tap / g.cv.S, s = tap - (tap / g.cv.S) * g.cv.S;
             tma_load_im2col_4d(sA, amap, fb, cb * 64, cw, ch, cn, (uint16_t)s, (uint16_t)r);
             tma_load_2d(sB, &tm.b, fb, tap * g.cv.wrow_cpad + cb * 64, n0);
+          } else if constexpr (MODE == LOAD_CONV_FPROP_C8) {
+            // 8 taps x 8 channels; each tap is one 128-pixel x 16-byte im2col box
+            const int taps = g.cv.R * g.cv.S;
+#pragma unroll 1
+            for (int j = 0; j < 8; ++j) {
+              const int tap = kb * 8 + j;
+              if (tap < taps) {
+                const int r = tap / g.cv.S, s = tap - (tap / g.cv.S) * g.cv.S;
+                tma_load_im2col_4d(sA + j * 2048, amap, fb, 0, cw, ch, cn, (uint16_t)s,
+                                   (uint16_t)r);
+              } else {  // past the last tap: an all-out-of-bounds box loads zeros
+                tma_load_im2col_4d(sA + j * 2048, amap, fb, 0, cw, ch, g.cv.N, 0, 0);
+              }
+            }
+            tma_load_2d(sB, &tm.b, fb, kb * BK, n0);
+          } else if constexpr (MODE == LOAD_CONV_DGRAD_SCATTER) {
+            tma_load_2d(sA, &tm.a[0], fb, kb * BK, ti.m0 * g.cv.Q);
+            tma_load_2d(sB, &tm.b, fb, kb * BK, n0);
           } else if constexpr (MODE == LOAD_CONV_DGRAD) {
             const PhaseInfo& P = g.phase[ti.phase];
             const int cb = kb % g.cv.cblocks;
@@ -288,7 +329,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll
           for (int k = 0; k < BK / UMMA_K; ++k) {
             uint64_t ad, bd;
-            if constexpr (A_MN) ad = make_smem_desc(sA + k * 2048, 8192, 1024, LAYOUT_SWIZZLE_128B);
+            if constexpr (MODE == LOAD_CONV_FPROP_C8)  // core matrices 8 rows x 16 B, no swizzle
+              ad = make_smem_desc(sA + k * 4096, 2048, 128, LAYOUT_SWIZZLE_NONE);
+            else if constexpr (A_MN) ad = make_smem_desc(sA + k * 2048, 8192, 1024, LAYOUT_SWIZZLE_128B);
             else ad = make_smem_desc(sA + k * 32, 16, 1024, LAYOUT_SWIZZLE_128B);
             if constexpr (B_MN) bd = make_smem_desc(sB + k * 2048, 8192, 1024, LAYOUT_SWIZZLE_128B);
             else bd = make_smem_desc(sB + k * 32, 16, 1024, LAYOUT_SWIZZLE_128B);
@@ -317,6 +360,63 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       mbar_wait(smem_u32(&tfull_bar[acc]), use & 1);
       tc_fence_after();
       const bool zero = ti.kb_end <= ti.kb_begin;
+
+      if constexpr (MODE == LOAD_CONV_DGRAD_SCATTER) {
+        // Tile = dY row (nn, oh); TMEM lane `row` = output pixel ow of that row;
+        // column j = (tap, ci).  Accumulate dX contributions of the whole row in
+        // a shared-memory window (R dX rows x region width x C), then flush the
+        // window to the fp32 dX accumulator with red.add (windows of adjacent
+        // rows overlap, so the flush must be atomic).
+        const int nn = ti.m0 / g.cv.P, oh = ti.m0 - (ti.m0 / g.cv.P) * g.cv.P;
+        const int C = g.cv.C, S = g.cv.S;
+        const int RW = (g.cv.Q - 1) * g.cv.sw + S;
+        const int ow = row;
+        const bool rvalid = ow < g.cv.Q;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tmem_base + ((quarter * 32u) << 16) + acc * BN + c, r);
+          tmem_ld_wait();
+          if (rvalid) {
+            // (tap, ci) of the chunk's first column, then walk forward
+            int col = n0 + c;
+            int tap = col / C, ci = col - tap * C;
+            int rr = tap / S, ss = tap - rr * S;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              if (col < g.N)
+                atomicAdd(&region[(rr * RW + ow * g.cv.sw + ss) * C + ci], __uint_as_float(r[j]));
+              ++col;
+              if (++ci == C) {
+                ci = 0;
+                if (++ss == S) {
+                  ss = 0;
+                  ++rr;
+                }
+              }
+            }
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(smem_u32(&tempty_bar[acc]));  // TMEM is free once values are in smem
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        const int total = g.cv.R * RW * C;
+        float* outp = static_cast<float*>(e.out);
+        const int tid = (static_cast<int>(warp) - 2) * 32 + static_cast<int>(lane);
+        for (int i = tid; i < total; i += EPI_WARPS * 32) {
+          const int ci = i % C;
+          const int rest = i / C;
+          const int cc = rest % RW, rr = rest / RW;
+          const int h = oh * g.cv.sh - g.cv.ph + rr, w = cc - g.cv.pw;
+          const float v = region[i];
+          region[i] = 0.f;
+          if (h >= 0 && h < g.cv.outH && w >= 0 && w < g.cv.outW && v != 0.f)
+            red_add_f32(outp + ((static_cast<int64_t>(nn) * g.cv.outH + h) * g.cv.outW + w) * C + ci,
+                        v);
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        continue;
+      }
 
       // ---- output row address
       const int m = ti.m0 + row;

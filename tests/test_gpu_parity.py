@@ -109,6 +109,8 @@ TC_CASES = [
     (2, 32, 9, 9, 40, 3, 1, 1),        # C=32 (channel OOB fill), K=40 (N tail)
     (1, 64, 10, 10, 64, 3, 1, 0),      # no padding
     (2, 16, 12, 12, 24, 5, 1, 2),      # 5x5
+    (3, 3, 45, 37, 64, 7, 2, 3),       # stem, odd sizes: C8 fprop + scatter dgrad
+    (2, 8, 20, 20, 32, 3, 1, 1),       # C=8: C8 fprop, 8-channel dgrad phases
 ]
 
 
@@ -126,6 +128,15 @@ def test_conv_tcgen05_bf16(case):
     used = launch_stats()["umma"] - u0
     # fwd + dx always run on tcgen05; dw too when both channel counts are multiples of 8
     assert used >= (3 if c % 8 == 0 else 2), used
+
+
+def test_stem_full_width():
+    # ResNet stem geometry at batch 2 (224x224): many scatter tiles overlapping
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal((2, 3, 224, 224))
+    wt = rng.standard_normal((64, 3, 7, 7)) / 12
+    g = rng.standard_normal((2, 64, 112, 112))
+    _conv_check(x, wt, g, 2, 3, "bf16", channels_last=True, rg=(1, 0, 0), tag="stem224")
 
 
 def test_conv_tcgen05_many_tiles():
