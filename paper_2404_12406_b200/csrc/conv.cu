@@ -13,6 +13,8 @@
 //         cast/layout pass into OIHW or OHWI
 // float32, NCHW 16-bit and channel counts that are not multiples of 8 run on
 // the SIMT direct kernels (simt.cu).
+#include <algorithm>
+
 #include "misc.cuh"
 
 namespace ms {
@@ -54,8 +56,11 @@ struct ConvPlan {
   bool repack = false;  // fwd: weight repacked into ws
   int cpad = 0;         // fwd: per-tap weight pitch (multiple of 64)
   int kpad = 0;         // dx: per-tap pitch of the repacked weight
-  bool c8 = false;      // fwd: 8-channel im2col variant (stem)
-  bool scatter = false; // dx: tiny-Cin col2im scatter variant (stem input gradient)
+  bool c8 = false;      // fwd: 8-channel im2col variant
+  bool rowseg = false;  // fwd: <=4-channel stride-2 stem, row-segment loads
+  int xw_pad = 0;       // rowseg: padded width of the 4-channel activation copy
+  bool band = false;    // dx: <8-channel input gradient (the stem), band col2im
+  int band_h = 16;
   size_t ws_pad = 0, ws_w = 0, ws_acc = 0;
   size_t ws = 0;
 };
@@ -63,6 +68,25 @@ struct ConvPlan {
 bool tc_ok(const ms_conv_desc* d) {
   return is16(d->dtype) && d->layout == MS_NHWC && d->r <= 64 && d->s <= 64 &&
          d->pad_h < 64 && d->pad_w < 64;
+}
+
+// Row-segment stem forward: one A row = S*4 consecutive elements of a
+// 4-channel input row; consecutive output pixels start sw*8 bytes apart, which
+// TMA needs to be a multiple of 16 (stride 2).  Checked once against the driver.
+bool rowseg_ok(const ms_conv_desc* d, const ConvDims& c) {
+  if (!(d->c <= 4 && d->stride_w == 2 && d->s * 4 <= 32 && c.ow <= BM)) return false;
+  static int cached = -1;
+  if (cached < 0) {
+    CUtensorMap m;
+    const uint64_t dims[4] = {32, 112, 224, 2};
+    const uint64_t str[3] = {16, 232 * 8, 224ull * 232 * 8};
+    const uint32_t box[4] = {32, BM, 1, 1};
+    cached = make_tmap_nd(&m, MS_BF16, reinterpret_cast<void*>(0x100000), 4, dims, str, box, 64) ==
+                     MS_OK
+                 ? 1
+                 : 0;
+  }
+  return cached == 1;
 }
 
 ConvPlan plan(const ms_conv_desc* d, int pass) {
@@ -76,6 +100,14 @@ ConvPlan plan(const ms_conv_desc* d, int pass) {
   }
   if (pass == MS_CONV_FWD) {
     p.tc = true;
+    if (rowseg_ok(d, c)) {
+      p.rowseg = true;
+      p.xw_pad = (int)std::max<int64_t>(d->w + 2 * d->pad_w, (int64_t)(c.ow - 1) * 2 + 8);
+      p.ws_pad = align256(es * (size_t)d->n * d->h * p.xw_pad * 4);
+      p.ws_w = align256(es * (size_t)d->k * d->r * 32);
+      p.ws = p.ws_pad + p.ws_w;
+      return p;
+    }
     p.cpad8 = (int)(d->c < 8 ? 8 : round_up(d->c, 8));
     p.pad_x = p.cpad8 != d->c;
     p.c8 = p.cpad8 == 8;
@@ -86,15 +118,14 @@ ConvPlan plan(const ms_conv_desc* d, int pass) {
     p.ws = p.ws_pad + p.ws_w;
   } else if (pass == MS_CONV_DX) {
     if (d->k % 8 != 0) return p;  // SIMT
-    const int64_t region = (int64_t)d->r * ((c.ow - 1) * d->stride_w + d->s) * d->c * 4;
-    if (d->c < 8 && region <= SCATTER_REGION_BYTES && d->r * d->s * d->c <= 1024) {
-      // tiny input-channel count (the stem): dY x W GEMM + col2im scatter
+    const int64_t win = 4ll * p.band_h * (31 * d->stride_w + d->s) * d->c * 4;
+    if (d->c < 8 && c.ow <= BM && win <= BAND_WINDOW_BYTES && taps * d->c <= 256) {
+      // tiny input-channel count (the stem): per dX-row band, dY-row x W GEMM + col2im
       p.tc = true;
-      p.scatter = true;
+      p.band = true;
       p.kpad = (int)round_up(d->k, 64);
       p.ws_w = align256(es * (size_t)taps * d->c * p.kpad);
-      p.ws_acc = align256(sizeof(float) * (size_t)d->n * d->h * d->w * d->c);
-      p.ws = p.ws_w + p.ws_acc;
+      p.ws = p.ws_w;
       return p;
     }
     if (d->stride_h > 2 || d->stride_w > 2) return p;  // SIMT
@@ -123,9 +154,52 @@ GemmArgs base_args(int dt) {
   return g;
 }
 
+ConvShape shape_of(const ConvDims& c, int C, int H, int W, int cblocks, int wpitch, int outH,
+                   int outW) {
+  ConvShape s{};
+  s.N = c.n; s.H = H; s.W = W; s.C = C;
+  s.P = c.oh; s.Q = c.ow; s.R = c.r; s.S = c.s;
+  s.sh = c.sh; s.sw = c.sw; s.ph = c.ph; s.pw = c.pw;
+  s.cblocks = cblocks; s.wrow_cpad = wpitch; s.outH = outH; s.outW = outW;
+  return s;
+}
+
 // ----------------------------------------------------------------- forward
+ms_status fwd_rowseg(const ms_conv_desc* d, const ConvPlan& p, const void* x, const void* w,
+                     const void* bias, void* y, void* ws, cudaStream_t st) {
+  const ConvDims c = dims_of(d);
+  const int dt = d->dtype;
+  uint8_t* wsb = static_cast<uint8_t*>(ws);
+  void* x4 = wsb;
+  void* wr = wsb + p.ws_pad;
+  MS_TRY(pad_rowseg(dt, c.n, c.h, c.w, c.c, c.pw, p.xw_pad, x, x4, st));
+  MS_TRY(repack_rowseg(dt, c.k, c.c, c.r, c.s, d->wlayout, w, wr, st));
+  GemmArgs g = base_args(dt);
+  g.M = c.n * c.oh * c.ow;
+  g.N = c.k;
+  const int bn = c.k <= 32 ? 32 : (c.k <= 64 ? 64 : (c.k <= 128 ? 128 : 256));
+  g.n_blocks = (c.k + bn - 1) / bn;
+  g.num_tiles = c.n * c.oh * g.n_blocks;
+  g.cv = shape_of(c, 4, c.h, p.xw_pad, 1, 32, c.oh, c.ow);
+  g.epi = EpiParams{y, c.k, dt, 0, bias, dt};
+  TmapPack tm;
+  const size_t es = dtype_size(dt);
+  const uint64_t dims[4] = {32, (uint64_t)c.ow, (uint64_t)c.h, (uint64_t)c.n};
+  const uint64_t str[3] = {(uint64_t)c.sw * 4 * es, (uint64_t)p.xw_pad * 4 * es,
+                           (uint64_t)c.h * p.xw_pad * 4 * es};
+  const uint32_t box[4] = {32, BM, 1, 1};
+  MS_TRY(make_tmap_nd(&tm.a[0], dt, x4, 4, dims, str, box, 64));
+  tm.a[1] = tm.a[2] = tm.a[3] = tm.a[0];
+  const uint64_t wd[2] = {(uint64_t)c.r * 32, (uint64_t)c.k};
+  const uint64_t ws2[1] = {(uint64_t)c.r * 32 * es};
+  const uint32_t wb[2] = {32, (uint32_t)bn};
+  MS_TRY(make_tmap_nd(&tm.b, dt, wr, 2, wd, ws2, wb, 64));
+  return launch_umma(bn, 0, 0, LOAD_CONV_FPROP_ROWSEG, tm, g, st);
+}
+
 ms_status fwd_tc(const ms_conv_desc* d, const ConvPlan& p, const void* x, const void* w,
                  const void* bias, void* y, void* ws, cudaStream_t st) {
+  if (p.rowseg) return fwd_rowseg(d, p, x, w, bias, y, ws, st);
   const ConvDims c = dims_of(d);
   const int dt = d->dtype;
   uint8_t* wsb = static_cast<uint8_t*>(ws);
@@ -148,8 +222,7 @@ ms_status fwd_tc(const ms_conv_desc* d, const ConvPlan& p, const void* x, const 
   g.n_blocks = (c.k + bn - 1) / bn;
   g.num_tiles = g.m_blocks * g.n_blocks;
   g.k_blocks = (c.r * c.s + 7) / 8;  // C8 variant: 8 taps per k-block
-  g.cv = ConvShape{c.n, c.h, c.w, p.cpad8, c.oh, c.ow, c.r, c.s, c.sh, c.sw, c.ph, c.pw,
-                   p.c8 ? 1 : p.cpad / 64, p.cpad, c.oh, c.ow};
+  g.cv = shape_of(c, p.cpad8, c.h, c.w, p.c8 ? 1 : p.cpad / 64, p.cpad, c.oh, c.ow);
   g.epi = EpiParams{y, c.k, dt, 0, bias, dt};
   TmapPack tm;
   const int lower[2] = {-c.pw, -c.ph};
@@ -163,48 +236,50 @@ ms_status fwd_tc(const ms_conv_desc* d, const ConvPlan& p, const void* x, const 
 }
 
 // ----------------------------------------------------------------- input-VJP
-ms_status dx_scatter(const ms_conv_desc* d, const ConvPlan& p, const void* dy, const void* w,
-                     void* dx, void* ws, cudaStream_t st) {
+ms_status dx_band(const ms_conv_desc* d, const ConvPlan& p, const void* dy, const void* w,
+                  void* dx, void* ws, cudaStream_t st) {
   const ConvDims c = dims_of(d);
   const int dt = d->dtype;
-  uint8_t* wsb = static_cast<uint8_t*>(ws);
-  void* wt = wsb;
-  float* acc = reinterpret_cast<float*>(wsb + p.ws_w);
+  void* wt = ws;
   MS_TRY(repack_scatter(dt, c.k, c.c, c.r, c.s, p.kpad, d->wlayout, w, wt, st));
-  const int64_t outn = (int64_t)c.n * c.h * c.w * c.c;
-  cudaMemsetAsync(acc, 0, sizeof(float) * outn, st);
   const int ncols = c.r * c.s * c.c;
-  const int bn = ncols <= 32 ? 32 : (ncols <= 64 ? 64 : (ncols <= 128 ? 128 : 256));
+  const int bn = ncols <= 32 ? 32 : ncols <= 64 ? 64 : ncols <= 128 ? 128 : ncols <= 160 ? 160 : 256;
   GemmArgs g = base_args(dt);
   g.M = c.n * c.oh * c.ow;
   g.N = ncols;
-  g.n_blocks = (ncols + bn - 1) / bn;
+  g.n_blocks = 1;
   g.k_blocks = p.kpad / 64;
-  g.num_tiles = c.n * c.oh * g.n_blocks;
-  g.cv = ConvShape{c.n, c.oh, c.ow, c.c, c.oh, c.ow, c.r, c.s, c.sh, c.sw, c.ph, c.pw,
-                   p.kpad / 64, p.kpad, c.h, c.w};
-  g.epi = EpiParams{acc, 0, MS_F32, 1, nullptr, 0};
+  g.cv = shape_of(c, c.k, c.oh, c.ow, p.kpad / 64, p.kpad, c.h, c.w);
+  g.cv.outC = c.c;
+  g.cv.band_h = p.band_h;
+  g.cv.band_sub = (p.band_h + c.r - 2) / c.sh + 1;
+  g.cv.bands_per_img = (c.h + p.band_h - 1) / p.band_h;
+  g.num_tiles = c.n * g.cv.bands_per_img;
+  g.epi = EpiParams{dx, 0, dt, 0, nullptr, 0};
   TmapPack tm;
-  MS_TRY(make_tmap_2d(&tm.a[0], dt, dy, c.k, (uint64_t)c.n * c.oh * c.ow, c.k, BK, BM));
+  const size_t es = dtype_size(dt);
+  const uint64_t dims[4] = {(uint64_t)c.k, (uint64_t)c.ow, (uint64_t)c.oh, (uint64_t)c.n};
+  const uint64_t str[3] = {(uint64_t)c.k * es, (uint64_t)c.ow * c.k * es,
+                           (uint64_t)c.oh * c.ow * c.k * es};
+  const uint32_t box[4] = {64, BM, 1, 1};
+  MS_TRY(make_tmap_nd(&tm.a[0], dt, dy, 4, dims, str, box, 128));
   tm.a[1] = tm.a[2] = tm.a[3] = tm.a[0];
   MS_TRY(make_tmap_2d(&tm.b, dt, wt, p.kpad, ncols, p.kpad, BK, bn));
-  MS_TRY(launch_umma(bn, 0, 0, LOAD_CONV_DGRAD_SCATTER, tm, g, st));
-  return f32_to(acc, dx, dt, outn, nullptr, 1, st);
+  return launch_umma(bn, 0, 0, LOAD_CONV_DGRAD_BAND, tm, g, st);
 }
 
 ms_status dx_tc(const ms_conv_desc* d, const ConvPlan& p, const void* dy, const void* w, void* dx,
                 void* ws, cudaStream_t st) {
   const ConvDims c = dims_of(d);
   const int dt = d->dtype;
-  if (p.scatter) return dx_scatter(d, p, dy, w, dx, ws, st);
+  if (p.band) return dx_band(d, p, dy, w, dx, ws, st);
   void* wd = ws;
   MS_TRY(repack_dgrad(dt, c.k, c.c, c.r, c.s, p.kpad, d->wlayout, w, wd, st));
   GemmArgs g = base_args(dt);
   g.N = c.c;
   const int bn = pick_bn((int64_t)c.n * c.h * c.w / BM + 1, c.c);
   g.n_blocks = (c.c + bn - 1) / bn;
-  g.cv = ConvShape{c.n, c.oh, c.ow, c.k, c.oh, c.ow, c.r, c.s, c.sh, c.sw, c.ph, c.pw,
-                   p.kpad / 64, p.kpad, c.h, c.w};
+  g.cv = shape_of(c, c.k, c.oh, c.ow, p.kpad / 64, p.kpad, c.h, c.w);
   TmapPack tm;
   int np = 0, tiles = 0;
   for (int ph = 0; ph < c.sh; ++ph) {
@@ -275,8 +350,7 @@ ms_status dw_tc(const ms_conv_desc* d, const ConvPlan& p, const void* x, const v
   g.kb_per_split = (int)((g.k_blocks + splits - 1) / splits);
   g.splits = (g.k_blocks + g.kb_per_split - 1) / g.kb_per_split;
   g.num_tiles = (int)(base_tiles * g.splits);
-  g.cv = ConvShape{c.n, c.h, c.w, c.c, c.oh, c.ow, c.r, c.s, c.sh, c.sw, c.ph, c.pw,
-                   (c.c + 63) / 64, 0, c.oh, c.ow};
+  g.cv = shape_of(c, c.c, c.h, c.w, (c.c + 63) / 64, 0, c.oh, c.ow);
   g.epi = EpiParams{acc, (int64_t)taps * c.c, MS_F32, 1, nullptr, 0};
   TmapPack tm;
   MS_TRY(make_tmap_2d(&tm.a[0], dt, dy, c.k, P, c.k, 64, BK));

@@ -133,6 +133,32 @@ ms_status make_tmap_2d(CUtensorMap* m, int dt, const void* base, uint64_t inner,
   return MS_OK;
 }
 
+ms_status make_tmap_nd(CUtensorMap* m, int dt, const void* base, int rank, const uint64_t* dims,
+                       const uint64_t* strides_bytes, const uint32_t* box, int swizzle) {
+  MS_TRY(resolve_driver());
+  MS_CHECK_ARG((reinterpret_cast<uintptr_t>(base) & 15) == 0, MS_ERR_ALIGN,
+               "tensor base %p not 16-byte aligned", base);
+  cuuint64_t d[5];
+  cuuint64_t s[4];
+  cuuint32_t b[5], e[5];
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    b[i] = box[i];
+    e[i] = 1;
+    if (i + 1 < rank) s[i] = strides_bytes[i];
+  }
+  const CUtensorMapSwizzle sw = swizzle == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : swizzle == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                : CU_TENSOR_MAP_SWIZZLE_NONE;
+  CUresult r = g_encode_tiled(m, tma_dtype(dt), rank, const_cast<void*>(base), d, s, b, e,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  MS_CHECK_ARG(r == CUDA_SUCCESS, MS_ERR_LAUNCH, "cuTensorMapEncodeTiled (rank %d) failed (%d)",
+               rank, (int)r);
+  return MS_OK;
+}
+
 ms_status make_tmap_im2col(CUtensorMap* m, int dt, const void* base, int n, int h, int w, int c,
                            const int lower[2], const int upper[2], int stride_w, int stride_h,
                            uint32_t channels, uint32_t pixels, bool swizzle128) {
@@ -200,8 +226,11 @@ ms_status launch_umma(int bn, int a_mn, int b_mn, int mode, const TmapPack& tm,
     MS_BN_SWITCH(0, 0, LOAD_CONV_DGRAD)
   } else if (mode == LOAD_CONV_FPROP_C8) {
     MS_BN_SWITCH(0, 0, LOAD_CONV_FPROP_C8)
-  } else if (mode == LOAD_CONV_DGRAD_SCATTER) {
-    MS_BN_SWITCH(0, 0, LOAD_CONV_DGRAD_SCATTER)
+  } else if (mode == LOAD_CONV_FPROP_ROWSEG) {
+    MS_BN_SWITCH(0, 0, LOAD_CONV_FPROP_ROWSEG)
+  } else if (mode == LOAD_CONV_DGRAD_BAND) {
+    if (bn == 160) return launch_t<160, 0, 0, LOAD_CONV_DGRAD_BAND>(tm, g, st);
+    MS_BN_SWITCH(0, 0, LOAD_CONV_DGRAD_BAND)
   } else if (mode == LOAD_CONV_WGRAD) {
     switch (bn) {
       case 64: return launch_t<64, 1, 1, LOAD_CONV_WGRAD>(tm, g, st);

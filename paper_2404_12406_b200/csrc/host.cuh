@@ -29,6 +29,11 @@ inline CUtensorMapDataType tma_dtype(int dt) {
 ms_status make_tmap_2d(CUtensorMap* m, int dt, const void* base, uint64_t inner, uint64_t outer,
                        uint64_t ld, uint32_t box_inner, uint32_t box_outer);
 
+// General tiled tensor map: dims[0] innermost, strides in bytes for dims 1..rank-1.
+// swizzle: 0 none, 64, 128 (bytes).
+ms_status make_tmap_nd(CUtensorMap* m, int dt, const void* base, int rank, const uint64_t* dims,
+                       const uint64_t* strides_bytes, const uint32_t* box, int swizzle);
+
 // NHWC activation [n][h][w][c] as an im2col tensor map.
 //   lower/upper: pixel bounding-box corners {w, h}; strides: traversal {w, h}
 ms_status make_tmap_im2col(CUtensorMap* m, int dt, const void* base, int n, int h, int w, int c,
