@@ -186,6 +186,116 @@ __global__ void __launch_bounds__(256) bn_bwd_kernel(int64_t total, int C, int64
   }
 }
 
+// ---------------------------------------------------------------- NHWC fast paths
+// Thread (rl, grp): channel group grp (VEC channels) of rows rl, rl+RPB, ...;
+// per-channel constants live in registers, each thread keeps UNR 16-byte
+// loads in flight (memory-level parallelism for HBM).
+constexpr int BN_UNR = 4;
+
+template <typename T, int VEC>
+__global__ void __launch_bounds__(256, 3) bn_fwd_nhwc_kernel(int64_t rows, int C, BnParams p,
+                                                          const T* __restrict__ x,
+                                                          T* __restrict__ y) {
+  const int G = C / VEC;
+  const int rpb = 256 / G;
+  const int tid = threadIdx.x;
+  if (tid >= rpb * G) return;
+  const int grp = tid % G, rl = tid / G;
+  float sc[VEC], sf[VEC];
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) {
+    float inv, mu;
+    bn_channel_consts(p, grp * VEC + j, sc[j], sf[j], inv, mu);
+  }
+  const int64_t step = (int64_t)gridDim.x * rpb;
+  for (int64_t r0 = (int64_t)blockIdx.x * rpb + rl; r0 < rows; r0 += step * BN_UNR) {
+    float v[BN_UNR][VEC];
+#pragma unroll
+    for (int u = 0; u < BN_UNR; ++u) {
+      const int64_t r = r0 + u * step;
+      if (r < rows) load_vec<T, VEC>(x + r * C + grp * VEC, v[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < BN_UNR; ++u) {
+      const int64_t r = r0 + u * step;
+      if (r < rows) {
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) v[u][j] = v[u][j] * sc[j] + sf[j];
+        store_vec<T, VEC>(y + r * C + grp * VEC, v[u]);
+      }
+    }
+  }
+}
+
+template <typename T, int VEC>
+__global__ void __launch_bounds__(256, 3) bn_bwd_nhwc_kernel(int64_t rows, int C, BnParams p,
+                                                          const T* __restrict__ g,
+                                                          const T* __restrict__ x,
+                                                          T* __restrict__ dx,
+                                                          float* __restrict__ acc_dw,
+                                                          float* __restrict__ acc_db) {
+  __shared__ float s_dw[2048], s_db[2048];
+  const int G = C / VEC;
+  const int rpb = 256 / G;
+  const int tid = threadIdx.x;
+  for (int c = tid; c < C; c += 256) s_dw[c] = s_db[c] = 0.f;
+  __syncthreads();
+  const bool want_dw = acc_dw != nullptr, want_db = acc_db != nullptr, want_dx = dx != nullptr;
+  if (tid < rpb * G) {
+    const int grp = tid % G, rl = tid / G;
+    float sc[VEC], inv[VEC], mu[VEC], pdw[VEC], pdb[VEC];
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) {
+      float sf;
+      bn_channel_consts(p, grp * VEC + j, sc[j], sf, inv[j], mu[j]);
+      pdw[j] = pdb[j] = 0.f;
+    }
+    const int64_t step = (int64_t)gridDim.x * rpb;
+    for (int64_t r0 = (int64_t)blockIdx.x * rpb + rl; r0 < rows; r0 += step * BN_UNR) {
+      float gv[BN_UNR][VEC];
+      float xv[BN_UNR][VEC];
+#pragma unroll
+      for (int u = 0; u < BN_UNR; ++u) {
+        const int64_t r = r0 + u * step;
+        if (r < rows) {
+          load_vec<T, VEC>(g + r * C + grp * VEC, gv[u]);
+          if (want_dw) load_vec<T, VEC>(x + r * C + grp * VEC, xv[u]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < BN_UNR; ++u) {
+        const int64_t r = r0 + u * step;
+        if (r >= rows) continue;
+        if (want_dx) {
+          float o[VEC];
+#pragma unroll
+          for (int j = 0; j < VEC; ++j) o[j] = gv[u][j] * sc[j];
+          store_vec<T, VEC>(dx + r * C + grp * VEC, o);
+        }
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) {
+          pdb[j] += gv[u][j];
+          if (want_dw) pdw[j] += gv[u][j] * (xv[u][j] - mu[j]) * inv[j];
+        }
+      }
+    }
+    if (want_dw || want_db) {
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) {
+        if (want_dw) atomicAdd(&s_dw[grp * VEC + j], pdw[j]);
+        if (want_db) atomicAdd(&s_db[grp * VEC + j], pdb[j]);
+      }
+    }
+  }
+  if (want_dw || want_db) {
+    __syncthreads();
+    for (int c = tid; c < C; c += 256) {
+      if (want_dw) atomicAdd(acc_dw + c, s_dw[c]);
+      if (want_db) atomicAdd(acc_db + c, s_db[c]);
+    }
+  }
+}
+
 #define MS_DT_DISPATCH(dt, ...)                                    \
   switch (dt) {                                                    \
     case MS_F32: { using T = float; __VA_ARGS__; } break;          \
@@ -218,6 +328,15 @@ static int bn_grid(int64_t nvec, int64_t C, int layout, int vec) {
   return (int)blocks;
 }
 
+// rows of an NHWC tensor, G channel groups per row: 256/G rows per block pass
+static int nhwc_grid(int64_t rows, int64_t G) {
+  const int64_t rpb = 256 / G;
+  int64_t need = (rows + rpb * BN_UNR - 1) / (rpb * BN_UNR);
+  const int64_t cap = (int64_t)num_sms() * 8;
+  if (need > cap) need = cap;
+  return (int)(need > 0 ? need : 1);
+}
+
 size_t bn_eval_workspace_bytes(int64_t c) { return sizeof(float) * 2 * (size_t)c; }
 
 ms_status bn_eval_fwd(int64_t n, int64_t c, int64_t hw, int layout, int dt, const BnParams& p,
@@ -228,7 +347,11 @@ ms_status bn_eval_fwd(int64_t n, int64_t c, int64_t hw, int layout, int dt, cons
   const size_t smem = sizeof(float) * 2 * c;
   MS_DT_DISPATCH(dt, {
     constexpr int V = 16 / sizeof(T);
-    if (can_vec(c, hw, layout, V, x, y, nullptr)) {
+    if (layout == MS_NHWC && can_vec(c, hw, layout, V, x, y, nullptr) && c / V <= 256) {
+      const int64_t rows = n * hw;
+      bn_fwd_nhwc_kernel<T, V><<<nhwc_grid(rows, c / V), 256, 0, st>>>(rows, (int)c, p,
+                                                                      (const T*)x, (T*)y);
+    } else if (can_vec(c, hw, layout, V, x, y, nullptr)) {
       bn_fwd_kernel<T, V><<<bn_grid(total / V, c, layout, V), 256, smem, st>>>(
           total, (int)c, hw, layout, p, (const T*)x, (T*)y);
     } else {
@@ -259,7 +382,12 @@ ms_status bn_eval_bwd(int64_t n, int64_t c, int64_t hw, int layout, int dt, cons
     const size_t smem = sizeof(float) * 5 * c;
     MS_DT_DISPATCH(dt, {
       constexpr int V = 16 / sizeof(T);
-      if (can_vec(c, hw, layout, V, g, dw ? x : nullptr, dx)) {
+      if (layout == MS_NHWC && can_vec(c, hw, layout, V, g, dw ? x : nullptr, dx) &&
+          c / V <= 256 && c <= 2048) {
+        const int64_t rows = n * hw;
+        bn_bwd_nhwc_kernel<T, V><<<nhwc_grid(rows, c / V), 256, 0, st>>>(
+            rows, (int)c, p, (const T*)g, (const T*)x, (T*)dx, acc_dw, acc_db);
+      } else if (can_vec(c, hw, layout, V, g, dw ? x : nullptr, dx)) {
         bn_bwd_kernel<T, V><<<bn_grid(total / V, c, layout, V), 256, smem, st>>>(
             total, (int)c, hw, layout, p, (const T*)g, (const T*)x, (T*)dx, acc_dw, acc_db);
       } else {

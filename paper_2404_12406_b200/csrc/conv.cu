@@ -118,7 +118,7 @@ ConvPlan plan(const ms_conv_desc* d, int pass) {
     p.ws = p.ws_pad + p.ws_w;
   } else if (pass == MS_CONV_DX) {
     if (d->k % 8 != 0) return p;  // SIMT
-    const int64_t win = 4ll * p.band_h * (31 * d->stride_w + d->s) * d->c * 4;
+    const int64_t win = (int64_t)BAND_WINDOWS * p.band_h * (31 * d->stride_w + d->s) * d->c * 4;
     if (d->c < 8 && c.ow <= BM && win <= BAND_WINDOW_BYTES && taps * d->c <= 256) {
       // tiny input-channel count (the stem): per dX-row band, dY-row x W GEMM + col2im
       p.tc = true;

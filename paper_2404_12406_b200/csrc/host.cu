@@ -196,7 +196,7 @@ static ms_status launch_t(const TmapPack& tm, const GemmArgs& g, cudaStream_t st
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int grid = g.num_tiles < num_sms() ? g.num_tiles : num_sms();
   if (grid <= 0) return MS_OK;
-  kern<<<grid, GEMM_THREADS, smem, st>>>(tm, g);
+  kern<<<grid, GemmCfg<BN, A_MN, B_MN, MODE>::THREADS, smem, st>>>(tm, g);
   count_launch(1, KF_UMMA);
   return launch_status("umma_gemm_kernel");
 }

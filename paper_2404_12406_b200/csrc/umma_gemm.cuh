@@ -33,7 +33,8 @@ enum : int {
   LOAD_CONV_FPROP_ROWSEG = 6,
   LOAD_CONV_DGRAD_BAND = 7
 };
-constexpr int BAND_WINDOW_BYTES = 64 * 1024;
+constexpr int BAND_WINDOWS = 8;  // one private col2im window per epilogue warp
+constexpr int BAND_WINDOW_BYTES = 112 * 1024;
 
 constexpr int BM = 128;        // UMMA M (cta_group::1)
 constexpr int BK = 64;         // K elements per stage (128 bytes of bf16)
@@ -185,10 +186,12 @@ struct GemmCfg {
   static constexpr int STAGES = STAGES_MAX > 8 ? 8 : STAGES_MAX;
   static constexpr int TMEM_COLS = pow2_cols(2 * BN);
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EXTRA + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int EPI = MODE == LOAD_CONV_DGRAD_BAND ? BAND_WINDOWS : EPI_WARPS;
+  static constexpr int THREADS = 64 + 32 * EPI;
 };
 
 template <int BN, int A_MN, int B_MN, int MODE>
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
+__global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE>::THREADS, 1)
     umma_gemm_kernel(const __grid_constant__ TmapPack tm, const __grid_constant__ GemmArgs g) {
   using Cfg = GemmCfg<BN, A_MN, B_MN, MODE>;
   constexpr int STAGES = Cfg::STAGES;
@@ -218,14 +221,23 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(smem_u32(&tfull_bar[i]), 1);
-      mbar_init(smem_u32(&tempty_bar[i]), EPI_WARPS * 32);
+      mbar_init(smem_u32(&tempty_bar[i]), Cfg::EPI * 32);
     }
     fence_mbar_init();
     tma_prefetch_desc(&tm.b);
     tma_prefetch_desc(&tm.a[0]);
   }
-  if constexpr (MODE == LOAD_CONV_DGRAD_BAND)
+  // band dgrad: column -> (kernel row, offset within a window row) lookup table
+  __shared__ int band_tab[256];
+  if constexpr (MODE == LOAD_CONV_DGRAD_BAND) {
     for (int i = threadIdx.x; i < BAND_WINDOW_BYTES / 4; i += blockDim.x) region[i] = 0.f;
+    for (int col = threadIdx.x; col < 256; col += blockDim.x) {
+      const int C = g.cv.outC, S = g.cv.S;
+      const int tap = col / C, ci = col - tap * C;
+      const int rr = tap / S, ss = tap - rr * S;
+      band_tab[col] = (rr << 16) | (ss * C + ci);
+    }
+  }
   if (warp == 1) tmem_alloc(smem_u32(tmem_holder), Cfg::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
@@ -415,15 +427,21 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int n0 = ti.nb * BN;
 
       if constexpr (MODE == LOAD_CONV_DGRAD_BAND) {
-        // ---- band of dX rows [h0, h0 + band_h) of image nn; thread = dY pixel ow
+        // ---- band of dX rows [h0, h0 + band_h) of image nn.  Thread = dY pixel
+        // ow = its TMEM lane; each epilogue warp owns a private window (its 32
+        // pixels x its half of the columns), so no shared atomics are needed: for
+        // a fixed column the 32 lanes write 32 distinct addresses.
         const ConvShape& cv = g.cv;
         const int nn = ti.m0 / cv.bands_per_img;
         const int h0 = (ti.m0 - nn * cv.bands_per_img) * cv.band_h;
         const int oh0 = band_first_row(cv, h0);
-        const int C = cv.outC, S = cv.S;
-        const int WC = 31 * cv.sw + S;  // window columns covered by one warp (32 dY pixels)
-        const int WIN = cv.band_h * WC * C;
-        float* win = region + quarter * WIN;
+        const int C = cv.outC;
+        const int WC = 31 * cv.sw + cv.S;  // window columns covered by 32 dY pixels
+        const int WCC = WC * C;
+        const int WIN = cv.band_h * WCC;
+        const int ew = static_cast<int>(warp) - 2;  // 0..7
+        const int half = ew >> 2;                   // which chunks of 32 columns
+        float* win = region + ew * WIN + static_cast<int>(lane) * cv.sw * C;
         const int ow = row;
         for (int sub = 0; sub < ti.nsub; ++sub, ++local) {
           const int acc = local & 1;
@@ -432,43 +450,32 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           tc_fence_after();
           const int oh = oh0 + sub;
           const bool rvalid = ow < cv.Q && oh >= 0 && oh < cv.P;
+          const int hbase = oh * cv.sh - cv.ph - h0;
 #pragma unroll 1
-          for (int c = 0; c < BN; c += 32) {
+          for (int c = half * 32; c < BN; c += 64) {
             uint32_t r[32];
             tmem_ld_32x32b_x32(tmem_base + ((quarter * 32u) << 16) + acc * BN + c, r);
             tmem_ld_wait();
-            if (!rvalid || n0 + c >= g.N) continue;
-            int col = n0 + c;
-            int tap = col / C;
-            int ci = col - tap * C;
-            int rr = tap / S, ss = tap - rr * S;
+            if (!rvalid) continue;
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-              const int hh = oh * cv.sh - cv.ph + rr - h0;
-              if (col < g.N && hh >= 0 && hh < cv.band_h) {
-                // for a fixed column the 32 lanes hit 32 distinct addresses
-                float* p = win + (hh * WC + static_cast<int>(lane) * cv.sw + ss) * C + ci;
-                *p += __uint_as_float(r[j]);
-              }
-              ++col;
-              if (++ci == C) {
-                ci = 0;
-                if (++ss == S) {
-                  ss = 0;
-                  ++rr;
-                }
-              }
+              const int col = n0 + c + j;
+              const int e = band_tab[col & 255];
+              const int hh = hbase + (e >> 16);
+              if (col < g.N && static_cast<unsigned>(hh) < static_cast<unsigned>(cv.band_h))
+                win[hh * WCC + (e & 0xFFFF)] += __uint_as_float(r[j]);
             }
           }
           tc_fence_before();
           mbar_arrive(smem_u32(&tempty_bar[acc]));
         }
-        // ---- flush: sum the (up to 2) warp windows covering each dX pixel
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        const int tid = (static_cast<int>(warp) - 2) * 32 + static_cast<int>(lane);
+        // ---- flush: sum the warp windows covering each dX pixel, store dX directly
+        constexpr int NT = BAND_WINDOWS * 32;
+        asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+        const int tid = ew * 32 + static_cast<int>(lane);
         const int rows = min(cv.band_h, cv.outH - h0);
         const int total = rows * cv.outW * C;
-        for (int i = tid; i < total; i += EPI_WARPS * 32) {
+        for (int i = tid; i < total; i += NT) {
           const int ci = i % C;
           const int pix = i / C;
           const int w = pix % cv.outW, hh = pix / cv.outW;
@@ -476,15 +483,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const int x = w + cv.pw - 32 * q * cv.sw;
-            if (x >= 0 && x < WC) v += region[q * WIN + (hh * WC + x) * C + ci];
+            if (x >= 0 && x < WC) {
+              const int o = (hh * WC + x) * C + ci;
+              v += region[q * WIN + o] + region[(q + 4) * WIN + o];
+            }
           }
           const int64_t o =
               ((static_cast<int64_t>(nn) * cv.outH + h0 + hh) * cv.outW + w) * C + ci;
           store_from_float(e.out, e.out_dtype, o, v);
         }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        for (int i = tid; i < 4 * WIN; i += EPI_WARPS * 32) region[i] = 0.f;
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+        for (int i = tid; i < BAND_WINDOWS * WIN; i += NT) region[i] = 0.f;
+        asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
       } else {
         const int acc = local & 1;
         const uint32_t use = static_cast<uint32_t>(local >> 1);
