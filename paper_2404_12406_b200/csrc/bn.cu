@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(256, 3) bn_fwd_nhwc_kernel(int64_t rows, int C
 }
 
 template <typename T, int VEC>
-__global__ void __launch_bounds__(256, 3) bn_bwd_nhwc_kernel(int64_t rows, int C, BnParams p,
+__global__ void __launch_bounds__(256, 2) bn_bwd_nhwc_kernel(int64_t rows, int C, BnParams p,
                                                           const T* __restrict__ g,
                                                           const T* __restrict__ x,
                                                           T* __restrict__ dx,
