@@ -227,8 +227,8 @@ __global__ void __launch_bounds__(256, 3) bn_fwd_nhwc_kernel(int64_t rows, int C
   }
 }
 
-template <typename T, int VEC>
-__global__ void __launch_bounds__(256, 2) bn_bwd_nhwc_kernel(int64_t rows, int C, BnParams p,
+template <typename T, int VEC, bool WANT_DW>
+__global__ void __launch_bounds__(256, WANT_DW ? 2 : 3) bn_bwd_nhwc_kernel(int64_t rows, int C, BnParams p,
                                                           const T* __restrict__ g,
                                                           const T* __restrict__ x,
                                                           T* __restrict__ dx,
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(256, 2) bn_bwd_nhwc_kernel(int64_t rows, int C
   const int tid = threadIdx.x;
   for (int c = tid; c < C; c += 256) s_dw[c] = s_db[c] = 0.f;
   __syncthreads();
-  const bool want_dw = acc_dw != nullptr, want_db = acc_db != nullptr, want_dx = dx != nullptr;
+  const bool want_dw = WANT_DW, want_db = acc_db != nullptr, want_dx = dx != nullptr;
   if (tid < rpb * G) {
     const int grp = tid % G, rl = tid / G;
     float sc[VEC], inv[VEC], mu[VEC], pdw[VEC], pdb[VEC];
@@ -253,13 +253,13 @@ __global__ void __launch_bounds__(256, 2) bn_bwd_nhwc_kernel(int64_t rows, int C
     const int64_t step = (int64_t)gridDim.x * rpb;
     for (int64_t r0 = (int64_t)blockIdx.x * rpb + rl; r0 < rows; r0 += step * BN_UNR) {
       float gv[BN_UNR][VEC];
-      float xv[BN_UNR][VEC];
+      float xv[WANT_DW ? BN_UNR : 1][VEC];
 #pragma unroll
       for (int u = 0; u < BN_UNR; ++u) {
         const int64_t r = r0 + u * step;
         if (r < rows) {
           load_vec<T, VEC>(g + r * C + grp * VEC, gv[u]);
-          if (want_dw) load_vec<T, VEC>(x + r * C + grp * VEC, xv[u]);
+          if constexpr (WANT_DW) load_vec<T, VEC>(x + r * C + grp * VEC, xv[u]);
         }
       }
 #pragma unroll
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(256, 2) bn_bwd_nhwc_kernel(int64_t rows, int C
 #pragma unroll
         for (int j = 0; j < VEC; ++j) {
           pdb[j] += gv[u][j];
-          if (want_dw) pdw[j] += gv[u][j] * (xv[u][j] - mu[j]) * inv[j];
+          if constexpr (WANT_DW) pdw[j] += gv[u][j] * (xv[WANT_DW ? u : 0][j] - mu[j]) * inv[j];
         }
       }
     }
@@ -385,8 +385,12 @@ ms_status bn_eval_bwd(int64_t n, int64_t c, int64_t hw, int layout, int dt, cons
       if (layout == MS_NHWC && can_vec(c, hw, layout, V, g, dw ? x : nullptr, dx) &&
           c / V <= 256 && c <= 2048) {
         const int64_t rows = n * hw;
-        bn_bwd_nhwc_kernel<T, V><<<nhwc_grid(rows, c / V), 256, 0, st>>>(
-            rows, (int)c, p, (const T*)g, (const T*)x, (T*)dx, acc_dw, acc_db);
+        if (dw)
+          bn_bwd_nhwc_kernel<T, V, true><<<nhwc_grid(rows, c / V), 256, 0, st>>>(
+              rows, (int)c, p, (const T*)g, (const T*)x, (T*)dx, acc_dw, acc_db);
+        else
+          bn_bwd_nhwc_kernel<T, V, false><<<nhwc_grid(rows, c / V), 256, 0, st>>>(
+              rows, (int)c, p, (const T*)g, (const T*)x, (T*)dx, acc_dw, acc_db);
       } else if (can_vec(c, hw, layout, V, g, dw ? x : nullptr, dx)) {
         bn_bwd_kernel<T, V><<<bn_grid(total / V, c, layout, V), 256, smem, st>>>(
             total, (int)c, hw, layout, p, (const T*)g, (const T*)x, (T*)dx, acc_dw, acc_db);

@@ -441,7 +441,9 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE>::THREADS, 1)
         const int WIN = cv.band_h * WCC;
         const int ew = static_cast<int>(warp) - 2;  // 0..7
         const int half = ew >> 2;                   // which chunks of 32 columns
-        float* win = region + ew * WIN + static_cast<int>(lane) * cv.sw * C;
+        // window index = half*4 + TMEM lane quarter (the flush below relies on it)
+        float* win = region + (half * 4 + static_cast<int>(quarter)) * WIN +
+                     static_cast<int>(lane) * cv.sw * C;
         const int ow = row;
         for (int sub = 0; sub < ti.nsub; ++sub, ++local) {
           const int acc = local & 1;
