@@ -118,11 +118,12 @@ ConvPlan plan(const ms_conv_desc* d, int pass) {
     p.ws = p.ws_pad + p.ws_w;
   } else if (pass == MS_CONV_DX) {
     if (d->k % 8 != 0) return p;  // SIMT
-    const int64_t win = (int64_t)BAND_WINDOWS * p.band_h * (31 * d->stride_w + d->s) * d->c * 4;
-    if (d->c < 8 && c.ow <= BM && win <= BAND_WINDOW_BYTES && taps * d->c <= 256) {
-      // tiny input-channel count (the stem): per dX-row band, dY-row x W GEMM + col2im
+    if (d->c == BAND_C && d->r == BAND_R && d->s == BAND_S && d->stride_w == BAND_SW &&
+        d->stride_h == BAND_SW && c.ow <= BM && (int64_t)BAND_WINDOWS * BAND_WIN * 4 <= BAND_WINDOW_BYTES) {
+      // the 3-channel 7x7/2 stem: per dX-row band, dY-row x W GEMM + col2im
       p.tc = true;
       p.band = true;
+      p.band_h = BAND_H;
       p.kpad = (int)round_up(d->k, 64);
       p.ws_w = align256(es * (size_t)taps * d->c * p.kpad);
       p.ws = p.ws_w;
@@ -243,7 +244,7 @@ ms_status dx_band(const ms_conv_desc* d, const ConvPlan& p, const void* dy, cons
   void* wt = ws;
   MS_TRY(repack_scatter(dt, c.k, c.c, c.r, c.s, p.kpad, d->wlayout, w, wt, st));
   const int ncols = c.r * c.s * c.c;
-  const int bn = ncols <= 32 ? 32 : ncols <= 64 ? 64 : ncols <= 128 ? 128 : ncols <= 160 ? 160 : 256;
+  const int bn = 160;  // band kernel is specialised to 7*7*3 = 147 columns
   GemmArgs g = base_args(dt);
   g.M = c.n * c.oh * c.ow;
   g.N = ncols;

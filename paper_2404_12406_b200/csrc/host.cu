@@ -230,7 +230,6 @@ ms_status launch_umma(int bn, int a_mn, int b_mn, int mode, const TmapPack& tm,
     MS_BN_SWITCH(0, 0, LOAD_CONV_FPROP_ROWSEG)
   } else if (mode == LOAD_CONV_DGRAD_BAND) {
     if (bn == 160) return launch_t<160, 0, 0, LOAD_CONV_DGRAD_BAND>(tm, g, st);
-    MS_BN_SWITCH(0, 0, LOAD_CONV_DGRAD_BAND)
   } else if (mode == LOAD_CONV_WGRAD) {
     switch (bn) {
       case 64: return launch_t<64, 1, 1, LOAD_CONV_WGRAD>(tm, g, st);

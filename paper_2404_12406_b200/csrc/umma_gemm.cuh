@@ -35,6 +35,15 @@ enum : int {
 };
 constexpr int BAND_WINDOWS = 8;  // one private col2im window per epilogue warp
 constexpr int BAND_WINDOW_BYTES = 112 * 1024;
+// The band input-VJP is specialised to the ResNet/VGG-style stem geometry so
+// that every accumulator column's (kernel row, kernel col, channel) is a
+// compile-time constant: C = 3 input channels, 7x7 kernel, stride 2.
+constexpr int BAND_C = 3, BAND_R = 7, BAND_S = 7, BAND_SW = 2, BAND_H = 16;
+constexpr int BAND_WC = 31 * BAND_SW + BAND_S;       // window columns of 32 dY pixels (69)
+constexpr int BAND_WH = (BAND_WC + 1) / 2;           // per parity plane (35)
+constexpr int BAND_ROWF = BAND_C * 2 * BAND_WH;      // floats per window row (210)
+constexpr int BAND_WIN = BAND_H * BAND_ROWF;         // floats per window (3360)
+template <int V> struct IntC { static constexpr int value = V; };
 
 constexpr int BM = 128;        // UMMA M (cta_group::1)
 constexpr int BK = 64;         // K elements per stage (128 bytes of bf16)
@@ -197,6 +206,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE>::THREADS, 1)
   constexpr int STAGES = Cfg::STAGES;
   constexpr int KMMA = Cfg::KBYTES / 32;  // tcgen05.mma (K=16) per stage
   static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN");
+  static_assert(MODE != LOAD_CONV_DGRAD_BAND || BN == 160, "band dgrad is specialised to BN=160");
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment for the swizzle atoms
@@ -227,17 +237,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE>::THREADS, 1)
     tma_prefetch_desc(&tm.b);
     tma_prefetch_desc(&tm.a[0]);
   }
-  // band dgrad: column -> (kernel row, offset within a window row) lookup table
-  __shared__ int band_tab[256];
-  if constexpr (MODE == LOAD_CONV_DGRAD_BAND) {
+  if constexpr (MODE == LOAD_CONV_DGRAD_BAND)
     for (int i = threadIdx.x; i < BAND_WINDOW_BYTES / 4; i += blockDim.x) region[i] = 0.f;
-    for (int col = threadIdx.x; col < 256; col += blockDim.x) {
-      const int C = g.cv.outC, S = g.cv.S;
-      const int tap = col / C, ci = col - tap * C;
-      const int rr = tap / S, ss = tap - rr * S;
-      band_tab[col] = (rr << 16) | (ss * C + ci);
-    }
-  }
   if (warp == 1) tmem_alloc(smem_u32(tmem_holder), Cfg::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
@@ -427,23 +428,19 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE>::THREADS, 1)
       const int n0 = ti.nb * BN;
 
       if constexpr (MODE == LOAD_CONV_DGRAD_BAND) {
-        // ---- band of dX rows [h0, h0 + band_h) of image nn.  Thread = dY pixel
-        // ow = its TMEM lane; each epilogue warp owns a private window (its 32
-        // pixels x its half of the columns), so no shared atomics are needed: for
-        // a fixed column the 32 lanes write 32 distinct addresses.
+        // ---- band of dX rows [h0, h0 + BAND_H) of image nn.  Thread = dY pixel
+        // ow = its TMEM lane.  Each epilogue warp owns a private window covering
+        // its 32 pixels, stored as [row][ci][x parity][x/2] so that for a fixed
+        // accumulator column the 32 lanes touch 32 consecutive floats.
         const ConvShape& cv = g.cv;
         const int nn = ti.m0 / cv.bands_per_img;
-        const int h0 = (ti.m0 - nn * cv.bands_per_img) * cv.band_h;
+        const int h0 = (ti.m0 - nn * cv.bands_per_img) * BAND_H;
         const int oh0 = band_first_row(cv, h0);
-        const int C = cv.outC;
-        const int WC = 31 * cv.sw + cv.S;  // window columns covered by 32 dY pixels
-        const int WCC = WC * C;
-        const int WIN = cv.band_h * WCC;
         const int ew = static_cast<int>(warp) - 2;  // 0..7
         const int half = ew >> 2;                   // which chunks of 32 columns
-        // window index = half*4 + TMEM lane quarter (the flush below relies on it)
-        float* win = region + (half * 4 + static_cast<int>(quarter)) * WIN +
-                     static_cast<int>(lane) * cv.sw * C;
+        // window index = half*4 + TMEM lane quarter (the flush relies on it)
+        float* win = region + (half * 4 + static_cast<int>(quarter)) * BAND_WIN +
+                     static_cast<int>(lane);
         const int ow = row;
         for (int sub = 0; sub < ti.nsub; ++sub, ++local) {
           const int acc = local & 1;
@@ -452,21 +449,33 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE>::THREADS, 1)
           tc_fence_after();
           const int oh = oh0 + sub;
           const bool rvalid = ow < cv.Q && oh >= 0 && oh < cv.P;
-          const int hbase = oh * cv.sh - cv.ph - h0;
-#pragma unroll 1
-          for (int c = half * 32; c < BN; c += 64) {
+          const int hbase = oh * cv.sh - cv.ph - h0;  // window row of kernel row 0
+          auto chunk = [&](auto cc) {
+            constexpr int c = decltype(cc)::value;
             uint32_t r[32];
             tmem_ld_32x32b_x32(tmem_base + ((quarter * 32u) << 16) + acc * BN + c, r);
             tmem_ld_wait();
-            if (!rvalid) continue;
+            if (!rvalid) return;
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-              const int col = n0 + c + j;
-              const int e = band_tab[col & 255];
-              const int hh = hbase + (e >> 16);
-              if (col < g.N && static_cast<unsigned>(hh) < static_cast<unsigned>(cv.band_h))
-                win[hh * WCC + (e & 0xFFFF)] += __uint_as_float(r[j]);
+              const int col = c + j;  // compile-time after unrolling
+              if (col < BAND_R * BAND_S * BAND_C) {
+                const int tap = col / BAND_C, ci = col % BAND_C;
+                const int rr = tap / BAND_S, ss = tap % BAND_S;
+                const int hh = hbase + rr;
+                if (static_cast<unsigned>(hh) < static_cast<unsigned>(BAND_H))
+                  win[hh * BAND_ROWF + (ci * 2 + (ss & 1)) * BAND_WH + (ss >> 1)] +=
+                      __uint_as_float(r[j]);
+              }
             }
+          };
+          if (half == 0) {
+            chunk(IntC<0>{});
+            chunk(IntC<64>{});
+            chunk(IntC<128>{});
+          } else {
+            chunk(IntC<32>{});
+            chunk(IntC<96>{});
           }
           tc_fence_before();
           mbar_arrive(smem_u32(&tempty_bar[acc]));
@@ -475,27 +484,27 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE>::THREADS, 1)
         constexpr int NT = BAND_WINDOWS * 32;
         asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
         const int tid = ew * 32 + static_cast<int>(lane);
-        const int rows = min(cv.band_h, cv.outH - h0);
-        const int total = rows * cv.outW * C;
-        for (int i = tid; i < total; i += NT) {
-          const int ci = i % C;
-          const int pix = i / C;
-          const int w = pix % cv.outW, hh = pix / cv.outW;
-          float v = 0.f;
+        const int rows = min(BAND_H, cv.outH - h0);
+        const int per_row = cv.outW * BAND_C;
+        for (int hh = 0; hh < rows; ++hh) {
+          const int64_t obase = ((static_cast<int64_t>(nn) * cv.outH + h0 + hh) * cv.outW) * BAND_C;
+          for (int i = tid; i < per_row; i += NT) {
+            const int w = i / BAND_C, ci = i - (i / BAND_C) * BAND_C;
+            const int xg = w + cv.pw;  // window column for quarter 0
+            float v = 0.f;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int x = w + cv.pw - 32 * q * cv.sw;
-            if (x >= 0 && x < WC) {
-              const int o = (hh * WC + x) * C + ci;
-              v += region[q * WIN + o] + region[(q + 4) * WIN + o];
+            for (int q = 0; q < 4; ++q) {
+              const int x = xg - 32 * q * BAND_SW;
+              if (x >= 0 && x < BAND_WC) {
+                const int o = hh * BAND_ROWF + (ci * 2 + (x & 1)) * BAND_WH + (x >> 1);
+                v += region[q * BAND_WIN + o] + region[(q + 4) * BAND_WIN + o];
+              }
             }
+            store_from_float(e.out, e.out_dtype, obase + i, v);
           }
-          const int64_t o =
-              ((static_cast<int64_t>(nn) * cv.outH + h0 + hh) * cv.outW + w) * C + ci;
-          store_from_float(e.out, e.out_dtype, o, v);
         }
         asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
-        for (int i = tid; i < BAND_WINDOWS * WIN; i += NT) region[i] = 0.f;
+        for (int i = tid; i < BAND_WINDOWS * BAND_WIN; i += NT) region[i] = 0.f;
         asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
       } else {
         const int acc = local & 1;
