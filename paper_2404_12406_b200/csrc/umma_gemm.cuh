@@ -439,8 +439,11 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE>::THREADS, 1)
         const int ew = static_cast<int>(warp) - 2;  // 0..7
         const int half = ew >> 2;                   // which chunks of 32 columns
         // window index = half*4 + TMEM lane quarter (the flush relies on it)
-        float* win = region + (half * 4 + static_cast<int>(quarter)) * BAND_WIN +
-                     static_cast<int>(lane);
+        // volatile: lane l's column (s+2) aliases lane l+1's column s, so the
+        // per-column read-modify-writes must stay in program order (the warp
+        // executes them in lockstep; the compiler must not batch them).
+        volatile float* win = region + (half * 4 + static_cast<int>(quarter)) * BAND_WIN +
+                              static_cast<int>(lane);
         const int ow = row;
         for (int sub = 0; sub < ti.nsub; ++sub, ++local) {
           const int acc = local & 1;
