@@ -251,6 +251,7 @@ def gpu_main(args):
     if world > 1 and args.config != "resnet18":
         pass  # weak scaling: every rank keeps the full per-GPU batch
     stock_model = copy.deepcopy(wl.model)
+    layers_model = copy.deepcopy(wl.model) if not args.no_stock else None
     convert_to_memory_saving(wl.model)
     inputs = list(wl.make_batch(wl.batch, dev))
     if wl.input_requires_grad:
@@ -294,6 +295,21 @@ def gpu_main(args):
                  "impl": "torch %s stock modules (cuDNN/cuBLAS), same weights/inputs"
                          % torch.__version__}
         del sstep, sinputs
+        torch.cuda.empty_cache()
+        # the north star's layer set only (Linear / Conv2d / BatchNorm2d-eval), ReLU and
+        # MaxPool2d left stock: isolates the paper's Fig. 2 effect from the §8(f) swaps
+        convert_to_memory_saving(layers_model, relu=False, maxpool2d=False)
+        linputs = list(wl.make_batch(wl.batch, dev))
+        if wl.input_requires_grad:
+            linputs[0].requires_grad_(True)
+        lsync = TrainableGradAllReduce(layers_model) if world > 1 else None
+        lms, lstep = run_arm(wl, layers_model, linputs, args.steps, args.warmup, world, dev, lsync)
+        lpeak, lact = peak_memory(lstep, dev)
+        stock["memsave_layers_only"] = {
+            "value": round(samples / (lms / 1e3), 2), "ms_per_step": round(lms / args.steps, 4),
+            "peak_mib": round(lpeak, 1), "activation_peak_mib": round(lact, 1),
+            "swaps": "Linear, Conv2d, BatchNorm2d(eval) only"}
+        del lstep, linputs
         torch.cuda.empty_cache()
 
     # ---------------- roofline of the dominant kernel (rank 0)
@@ -430,7 +446,7 @@ def reference_main(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="memsave", choices=["memsave", "reference"])
     ap.add_argument("--config", default="resnet18", choices=["resnet18", "fig1"])

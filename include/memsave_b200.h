@@ -125,6 +125,34 @@ MS_API ms_status ms_bn_eval_bwd(int64_t n, int64_t c, int64_t hw, int32_t layout
                          void* dw_or_null, void* db_or_null, void* ws, size_t ws_bytes,
                          void* stream);
 
+/* ------------------------------------------------------------ relu (bit mask)
+ * MemSave ReLU (rules.py:98-101, saved.py:53-71): y = max(x, 0) over a dense
+ * buffer of `numel` elements (any memory format: the mask follows storage
+ * order); mask bit i = (x_i > 0), ceil(numel/8) bytes, bit j of byte i/8.
+ * y may alias x; dx may alias g.                                            */
+MS_API ms_status ms_relu_fwd(int64_t numel, int32_t dtype, const void* x, void* y,
+                             void* mask_or_null, void* stream);
+MS_API ms_status ms_relu_bwd(int64_t numel, int32_t dtype, const void* g, const void* mask,
+                             void* dx, void* stream);
+
+/* ------------------------------------------------------------ maxpool2d (index map)
+ * MemSave MaxPool2d (rules.py:108-109, saved.py:111-125, kernels
+ * numpy_impl.py:54-78): the argmax is kept as the window-local offset
+ * r*kw + s in one byte per output element (the reference keeps a 4-byte flat
+ * index); first occurrence wins ties; padding is -inf.                      */
+typedef struct {
+  int64_t n, c, h, w;
+  int32_t kh, kw, stride_h, stride_w, pad_h, pad_w;
+  int32_t layout; /* ms_layout of x / y / g / dx / idx */
+  int32_t dtype;
+} ms_pool_desc;
+MS_API int64_t ms_maxpool2d_out_h(const ms_pool_desc* p);
+MS_API int64_t ms_maxpool2d_out_w(const ms_pool_desc* p);
+MS_API ms_status ms_maxpool2d_fwd(const ms_pool_desc* p, const void* x, void* y,
+                                  void* idx_or_null, void* stream);
+MS_API ms_status ms_maxpool2d_bwd(const ms_pool_desc* p, const void* g, const void* idx,
+                                  void* dx, void* stream);
+
 /* ------------------------------------------------------------ misc */
 MS_API const char* ms_status_string(int32_t status);
 MS_API const char* ms_last_error(void);

@@ -19,5 +19,6 @@ are therefore "pinned to the SPEC", not to reference code.
 from .conv import conv2d_fwd, conv2d_dx, conv2d_dw, conv_out_size  # noqa: F401
 from .linear import linear_fwd, linear_dx, linear_dw, linear_db  # noqa: F401
 from .batchnorm import bn_eval_fwd, bn_eval_dx, bn_eval_dw, bn_eval_db  # noqa: F401
+from .pool import maxpool2d_fwd, maxpool2d_bwd, relu_fwd, relu_bwd  # noqa: F401
 from .rules import Policy, storage_decision, linear_family  # noqa: F401
 from .tolerance import assert_close_fp32, assert_close_lowp, round_to  # noqa: F401

@@ -57,9 +57,33 @@ def gen_conv(core, kernels):
     return out
 
 
+POOL_CASES = [
+    # name, shape, kh, kw, sh, sw
+    ("mp_2x2s2", (2, 3, 8, 6), 2, 2, 2, 2),
+    ("mp_3x3s2", (2, 4, 9, 11), 3, 3, 2, 2),
+    ("mp_3x3s1", (1, 2, 7, 5), 3, 3, 1, 1),
+    ("mp_ties", (1, 2, 6, 6), 3, 3, 2, 2),
+]
+
+
+def gen_pool(core, kernels):
+    out = {}
+    for name, shape, kh, kw, sh, sw in POOL_CASES:
+        x = core.Rng(3, 0).normal(shape, core.Dtype.F64)
+        if name == "mp_ties":
+            x = np.round(x)  # many ties: checks the first-occurrence rule
+        y, idx = kernels.maxpool2d_fwd(x, kh, kw, sh, sw)
+        g = core.Rng(3, 2).normal(y.shape, core.Dtype.F64)
+        dx = kernels.maxpool2d_bwd(g, idx, shape[2], shape[3])
+        for key, val in dict(x=x, y=y, idx=idx, g=g, dx=dx).items():
+            out[f"{name}/{key}"] = np.ascontiguousarray(val)
+        out[f"{name}/geom"] = np.array([kh, kw, sh, sw], dtype=np.int64)
+    return out
+
+
 def gen_rules(rules):
     table = []
-    for kind in ("linear", "conv2d", "conv_transpose2d", "batchnorm2d"):
+    for kind in ("linear", "conv2d", "conv_transpose2d", "batchnorm2d", "relu", "maxpool2d"):
         for bn_train in ((False, True) if kind == "batchnorm2d" else (False,)):
             for pol in (rules.Policy.NAIVE, rules.Policy.MEMSAVE):
                 for x_rg in (False, True):
@@ -132,6 +156,7 @@ def main():
                    "table": gen_rules(rules)}, f, indent=1)
 
     np.savez_compressed(os.path.join(GOLDEN, "linear_bn_spec.npz"), **gen_linear_bn(core))
+    np.savez_compressed(os.path.join(GOLDEN, "maxpool_ref.npz"), **gen_pool(core, kernels))
 
     # SPEC known-answer examples
     kat = {

@@ -3,7 +3,8 @@
 Restates /root/reference/pkg/src/leantape/rules.py for the rows on the hot
 path: linear (rules.py:64-66), conv2d / conv_transpose2d (rules.py:68-71),
 batchnorm2d in eval mode (rules.py:84-87) and the shared ``_linear_family``
-rule (rules.py:133-141).  Golden tables produced by importing the reference
+rule (rules.py:133-141), plus the first "next" rows: relu (rules.py:98-101)
+and maxpool2d (rules.py:108-109).  Golden tables produced by importing the reference
 (tests/golden/rules.json) pin this restatement.
 """
 
@@ -47,4 +48,10 @@ def storage_decision(kind: str, policy: Policy, *, x_rg: bool, w_rg: bool,
         if policy is Policy.MEMSAVE:
             return linear_family(x_rg, w_rg)
         return [("x", "full"), ("w", "full")] if out_rg else []
+    if kind == "relu":  # rules.py:98-101
+        if not out_rg:
+            return []
+        return [("mask", "bitmask")] if policy is Policy.MEMSAVE else [("y", "full")]
+    if kind == "maxpool2d":  # rules.py:108-109
+        return [("idx", "indexmap")] if out_rg else []
     raise ValueError(f"no hot-path storage rule for op kind {kind!r}")

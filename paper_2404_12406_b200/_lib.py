@@ -34,6 +34,14 @@ class ConvDesc(ctypes.Structure):
                 ("layout", _c_i32), ("wlayout", _c_i32), ("dtype", _c_i32)]
 
 
+class PoolDesc(ctypes.Structure):
+    """ms_pool_desc (include/memsave_b200.h)."""
+
+    _fields_ = [("n", _c_i64), ("c", _c_i64), ("h", _c_i64), ("w", _c_i64),
+                ("kh", _c_i32), ("kw", _c_i32), ("stride_h", _c_i32), ("stride_w", _c_i32),
+                ("pad_h", _c_i32), ("pad_w", _c_i32), ("layout", _c_i32), ("dtype", _c_i32)]
+
+
 # (name, restype, argtypes) for every symbol the header declares
 SIGNATURES = {
     "ms_conv2d_out_h": (_c_i64, [ctypes.POINTER(ConvDesc)]),
@@ -54,6 +62,12 @@ SIGNATURES = {
                                 _vp, _vp, ctypes.c_double, _vp, _vp, _c_sz, _vp]),
     "ms_bn_eval_bwd": (_c_i32, [_c_i64, _c_i64, _c_i64, _c_i32, _c_i32, _c_i32, _vp, _vp, _vp,
                                 _vp, _vp, ctypes.c_double, _vp, _vp, _vp, _vp, _c_sz, _vp]),
+    "ms_relu_fwd": (_c_i32, [_c_i64, _c_i32, _vp, _vp, _vp, _vp]),
+    "ms_relu_bwd": (_c_i32, [_c_i64, _c_i32, _vp, _vp, _vp, _vp]),
+    "ms_maxpool2d_out_h": (_c_i64, [ctypes.POINTER(PoolDesc)]),
+    "ms_maxpool2d_out_w": (_c_i64, [ctypes.POINTER(PoolDesc)]),
+    "ms_maxpool2d_fwd": (_c_i32, [ctypes.POINTER(PoolDesc), _vp, _vp, _vp, _vp]),
+    "ms_maxpool2d_bwd": (_c_i32, [ctypes.POINTER(PoolDesc), _vp, _vp, _vp, _vp]),
     "ms_status_string": (ctypes.c_char_p, [_c_i32]),
     "ms_last_error": (ctypes.c_char_p, []),
     "ms_version": (_c_i32, []),

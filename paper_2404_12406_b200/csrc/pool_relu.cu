@@ -1,0 +1,400 @@
+// ReLU with a bit-packed mask and MaxPool2d with a 1-byte window-argmax map:
+// the reference's MemSave ReLU / MaxPool storage (rules.py:98-101, :108-109;
+// saved.py:53-71 BitMask, saved.py:111-125 IndexMap) and kernels
+// (numpy_impl.py:54-78, numba_impl.py:78-106).  Both are HBM-bound.
+//
+// ReLU: y = max(x, 0); mask bit i = (x_i > 0) (ties at 0 -> 0, SPEC.md "ReLU at
+//   exactly 0 -> mask bit 0"); dx = g where the bit is set.  8 elements per
+//   thread-step = one mask byte; y/dx may alias x/g (in-place).
+// MaxPool2d: the argmax is stored as the window-local offset r*kw + s (one
+//   byte) instead of the reference's 4-byte flat index; ties keep the first
+//   occurrence in row-major window order (numpy_impl.py:60-69), padding is
+//   -inf.  Backward is a gather: every input element checks the <= ceil(k/s)^2
+//   windows that contain it, so no atomics and a fully written dx.
+#include "misc.cuh"
+
+namespace ms {
+namespace {
+
+#define MS_DT_DISPATCH(dt, ...)                                    \
+  switch (dt) {                                                    \
+    case MS_F32: { using T = float; __VA_ARGS__; } break;          \
+    case MS_BF16: { using T = __nv_bfloat16; __VA_ARGS__; } break; \
+    case MS_F16: { using T = __half; __VA_ARGS__; } break;         \
+    default: set_error("bad dtype %d", dt); return MS_ERR_DTYPE;   \
+  }
+
+int grid_for(int64_t work) {
+  int64_t b = (work + 255) / 256;
+  const int64_t cap = (int64_t)num_sms() * 16;
+  if (b > cap) b = cap;
+  return (int)(b > 0 ? b : 1);
+}
+
+template <typename T>
+__device__ __forceinline__ void ld8(const T* p, float (&v)[8], bool vec) {
+  if (vec) {
+    if constexpr (sizeof(T) == 2) {
+      uint4 u = *reinterpret_cast<const uint4*>(p);
+      const T* e = reinterpret_cast<const T*>(&u);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = IO<T>::ld(e + j);
+    } else {
+      float4 a = *reinterpret_cast<const float4*>(p);
+      float4 b = *reinterpret_cast<const float4*>(p + 4);
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+      v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = IO<T>::ld(p + j);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void st8(T* p, const float (&v)[8], bool vec) {
+  if (vec) {
+    if constexpr (sizeof(T) == 2) {
+      uint4 u;
+      T* e = reinterpret_cast<T*>(&u);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) e[j] = IO<T>::cvt(v[j]);
+      *reinterpret_cast<uint4*>(p) = u;
+    } else {
+      *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+      *reinterpret_cast<float4*>(p + 4) = make_float4(v[4], v[5], v[6], v[7]);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) p[j] = IO<T>::cvt(v[j]);
+  }
+}
+
+// ---------------------------------------------------------------- ReLU
+template <typename T>
+__global__ void __launch_bounds__(256) relu_fwd_kernel(int64_t n, const T* x, T* y,
+                                                       uint8_t* __restrict__ mask, bool vec) {
+  const int64_t groups = (n + 7) / 8;
+  for (int64_t gi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gi < groups;
+       gi += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = gi * 8;
+    float v[8];
+    uint32_t bits = 0;
+    if (e + 8 <= n) {
+      ld8<T>(x + e, v, vec);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const bool pos = !(v[j] <= 0.f);  // x > 0, and NaN propagates like torch.relu
+        bits |= (pos ? 1u : 0u) << j;
+        v[j] = pos ? v[j] : 0.f;
+      }
+      st8<T>(y + e, v, vec);
+    } else {
+      for (int j = 0; j < 8 && e + j < n; ++j) {
+        const float a = IO<T>::ld(x + e + j);
+        const bool pos = !(a <= 0.f);
+        bits |= (pos ? 1u : 0u) << j;
+        y[e + j] = IO<T>::cvt(pos ? a : 0.f);
+      }
+    }
+    if (mask) mask[gi] = static_cast<uint8_t>(bits);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) relu_bwd_kernel(int64_t n, const T* g,
+                                                       const uint8_t* __restrict__ mask, T* dx,
+                                                       bool vec) {
+  const int64_t groups = (n + 7) / 8;
+  for (int64_t gi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gi < groups;
+       gi += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = gi * 8;
+    const uint32_t bits = mask[gi];
+    if (e + 8 <= n) {
+      float v[8];
+      ld8<T>(g + e, v, vec);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = (bits >> j) & 1u ? v[j] : 0.f;
+      st8<T>(dx + e, v, vec);
+    } else {
+      for (int j = 0; j < 8 && e + j < n; ++j)
+        dx[e + j] = IO<T>::cvt((bits >> j) & 1u ? IO<T>::ld(g + e + j) : 0.f);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- MaxPool2d
+struct PoolDims {
+  int n, c, h, w, oh, ow, kh, kw, sh, sw, ph, pw;
+};
+
+// NHWC, 8 channels per thread (C % 8 == 0, 16-byte aligned)
+template <typename T>
+__global__ void __launch_bounds__(256) maxpool_fwd_nhwc8(PoolDims d, const T* __restrict__ x,
+                                                         T* __restrict__ y,
+                                                         uint8_t* __restrict__ idx) {
+  const int G = d.c / 8;
+  const int64_t total = (int64_t)d.n * d.oh * d.ow * G;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int g = t % G;
+    int64_t p = t / G;
+    const int ow = p % d.ow;
+    p /= d.ow;
+    const int oh = p % d.oh;
+    const int n = (int)(p / d.oh);
+    float best[8];
+    uint32_t arg[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      best[j] = -INFINITY;
+      arg[j] = 0;
+    }
+    bool first = true;
+    for (int r = 0; r < d.kh; ++r) {
+      const int ih = oh * d.sh - d.ph + r;
+      if (ih < 0 || ih >= d.h) continue;
+      for (int s = 0; s < d.kw; ++s) {
+        const int iw = ow * d.sw - d.pw + s;
+        if (iw < 0 || iw >= d.w) continue;
+        float v[8];
+        ld8<T>(x + (((int64_t)n * d.h + ih) * d.w + iw) * d.c + g * 8, v, true);
+        const uint32_t k = r * d.kw + s;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (first || v[j] > best[j] || (v[j] != v[j] && best[j] == best[j])) {
+            best[j] = v[j];
+            arg[j] = k;
+          }
+        }
+        first = false;
+      }
+    }
+    const int64_t o = (((int64_t)n * d.oh + oh) * d.ow + ow) * d.c + g * 8;
+    st8<T>(y + o, best, true);
+    if (idx) {
+      uint2 u;
+      u.x = arg[0] | (arg[1] << 8) | (arg[2] << 16) | (arg[3] << 24);
+      u.y = arg[4] | (arg[5] << 8) | (arg[6] << 16) | (arg[7] << 24);
+      *reinterpret_cast<uint2*>(idx + o) = u;
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) maxpool_bwd_nhwc8(PoolDims d, const T* __restrict__ g,
+                                                         const uint8_t* __restrict__ idx,
+                                                         T* __restrict__ dx) {
+  const int G = d.c / 8;
+  const int64_t total = (int64_t)d.n * d.h * d.w * G;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int gg = t % G;
+    int64_t p = t / G;
+    const int iw = p % d.w;
+    p /= d.w;
+    const int ih = p % d.h;
+    const int n = (int)(p / d.h);
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    // windows (oh, ow) with oh*sh - ph <= ih <= oh*sh - ph + kh - 1
+    const int oh_lo = max(0, (ih + d.ph - d.kh + d.sh) / d.sh);
+    const int oh_hi = min(d.oh - 1, (ih + d.ph) / d.sh);
+    const int ow_lo = max(0, (iw + d.pw - d.kw + d.sw) / d.sw);
+    const int ow_hi = min(d.ow - 1, (iw + d.pw) / d.sw);
+    for (int oh = oh_lo; oh <= oh_hi; ++oh) {
+      const int r = ih + d.ph - oh * d.sh;
+      if (r < 0 || r >= d.kh) continue;
+      for (int ow = ow_lo; ow <= ow_hi; ++ow) {
+        const int s = iw + d.pw - ow * d.sw;
+        if (s < 0 || s >= d.kw) continue;
+        const uint32_t k = r * d.kw + s;
+        const int64_t o = (((int64_t)n * d.oh + oh) * d.ow + ow) * d.c + gg * 8;
+        const uint2 u = *reinterpret_cast<const uint2*>(idx + o);
+        float gv[8];
+        ld8<T>(g + o, gv, true);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t a = ((j < 4 ? u.x : u.y) >> (8 * (j & 3))) & 0xFFu;
+          if (a == k) acc[j] += gv[j];
+        }
+      }
+    }
+    st8<T>(dx + (((int64_t)n * d.h + ih) * d.w + iw) * d.c + gg * 8, acc, true);
+  }
+}
+
+// generic (any layout via strides, scalar)
+struct S4 {
+  int64_t n, c, h, w;
+};
+
+template <typename T>
+__global__ void maxpool_fwd_generic(PoolDims d, const T* __restrict__ x, S4 xs, T* __restrict__ y,
+                                    S4 ys, uint8_t* __restrict__ idx) {
+  const int64_t total = (int64_t)d.n * d.c * d.oh * d.ow;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t p = t;
+    const int ow = p % d.ow; p /= d.ow;
+    const int oh = p % d.oh; p /= d.oh;
+    const int c = p % d.c;
+    const int n = (int)(p / d.c);
+    float best = -INFINITY;
+    uint32_t arg = 0;
+    bool first = true;
+    for (int r = 0; r < d.kh; ++r) {
+      const int ih = oh * d.sh - d.ph + r;
+      if (ih < 0 || ih >= d.h) continue;
+      for (int s = 0; s < d.kw; ++s) {
+        const int iw = ow * d.sw - d.pw + s;
+        if (iw < 0 || iw >= d.w) continue;
+        const float v = IO<T>::ld(x + n * xs.n + c * xs.c + ih * xs.h + iw * xs.w);
+        if (first || v > best || (v != v && best == best)) {
+          best = v;
+          arg = r * d.kw + s;
+        }
+        first = false;
+      }
+    }
+    const int64_t o = n * ys.n + c * ys.c + oh * ys.h + ow * ys.w;
+    y[o] = IO<T>::cvt(best);
+    if (idx) idx[o] = (uint8_t)arg;
+  }
+}
+
+template <typename T>
+__global__ void maxpool_bwd_generic(PoolDims d, const T* __restrict__ g, S4 gs,
+                                    const uint8_t* __restrict__ idx, T* __restrict__ dx, S4 xs) {
+  const int64_t total = (int64_t)d.n * d.c * d.h * d.w;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t p = t;
+    const int iw = p % d.w; p /= d.w;
+    const int ih = p % d.h; p /= d.h;
+    const int c = p % d.c;
+    const int n = (int)(p / d.c);
+    float acc = 0.f;
+    const int oh_lo = max(0, (ih + d.ph - d.kh + d.sh) / d.sh);
+    const int oh_hi = min(d.oh - 1, (ih + d.ph) / d.sh);
+    const int ow_lo = max(0, (iw + d.pw - d.kw + d.sw) / d.sw);
+    const int ow_hi = min(d.ow - 1, (iw + d.pw) / d.sw);
+    for (int oh = oh_lo; oh <= oh_hi; ++oh) {
+      const int r = ih + d.ph - oh * d.sh;
+      if (r < 0 || r >= d.kh) continue;
+      for (int ow = ow_lo; ow <= ow_hi; ++ow) {
+        const int s = iw + d.pw - ow * d.sw;
+        if (s < 0 || s >= d.kw) continue;
+        const int64_t o = n * gs.n + c * gs.c + oh * gs.h + ow * gs.w;
+        if (idx[o] == (uint8_t)(r * d.kw + s)) acc += IO<T>::ld(g + o);
+      }
+    }
+    dx[n * xs.n + c * xs.c + ih * xs.h + iw * xs.w] = IO<T>::cvt(acc);
+  }
+}
+
+S4 strides_of(int layout, int64_t c, int64_t h, int64_t w) {
+  if (layout == MS_NHWC) return S4{h * w * c, 1, w * c, c};
+  return S4{c * h * w, h * w, w, 1};
+}
+
+bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+}  // namespace
+}  // namespace ms
+
+using namespace ms;
+
+extern "C" ms_status ms_relu_fwd(int64_t numel, int32_t dt, const void* x, void* y,
+                                 void* mask_or_null, void* stream) {
+  MS_CHECK_ARG(numel >= 0 && x && y, MS_ERR_SHAPE, "relu: bad arguments");
+  if (numel == 0) return MS_OK;
+  MS_TRY(bind_device(y));
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool vec = al16(x) && al16(y);
+  MS_DT_DISPATCH(dt, relu_fwd_kernel<T><<<grid_for((numel + 7) / 8), 256, 0, st>>>(
+                         numel, (const T*)x, (T*)y, (uint8_t*)mask_or_null, vec));
+  count_launch();
+  return launch_status("relu_fwd_kernel");
+}
+
+extern "C" ms_status ms_relu_bwd(int64_t numel, int32_t dt, const void* g, const void* mask,
+                                 void* dx, void* stream) {
+  MS_CHECK_ARG(numel >= 0 && g && mask && dx, MS_ERR_SHAPE, "relu bwd: bad arguments");
+  if (numel == 0) return MS_OK;
+  MS_TRY(bind_device(dx));
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool vec = al16(g) && al16(dx);
+  MS_DT_DISPATCH(dt, relu_bwd_kernel<T><<<grid_for((numel + 7) / 8), 256, 0, st>>>(
+                         numel, (const T*)g, (const uint8_t*)mask, (T*)dx, vec));
+  count_launch();
+  return launch_status("relu_bwd_kernel");
+}
+
+static ms_status pool_dims(const ms_pool_desc* p, PoolDims& d) {
+  MS_CHECK_ARG(p && p->n >= 0 && p->c > 0 && p->h > 0 && p->w > 0 && p->kh > 0 && p->kw > 0 &&
+                   p->stride_h > 0 && p->stride_w > 0 && p->pad_h >= 0 && p->pad_w >= 0,
+               MS_ERR_SHAPE, "maxpool: bad geometry");
+  MS_CHECK_ARG(p->kh * p->kw <= 256, MS_ERR_UNSUPPORTED, "maxpool: window larger than 256");
+  MS_CHECK_ARG(2 * p->pad_h <= p->kh && 2 * p->pad_w <= p->kw, MS_ERR_SHAPE,
+               "maxpool: padding must be at most half the window");
+  d = PoolDims{(int)p->n, (int)p->c, (int)p->h, (int)p->w, 0, 0, p->kh, p->kw, p->stride_h,
+               p->stride_w, p->pad_h, p->pad_w};
+  d.oh = (int)((p->h + 2 * p->pad_h - p->kh) / p->stride_h + 1);
+  d.ow = (int)((p->w + 2 * p->pad_w - p->kw) / p->stride_w + 1);
+  MS_CHECK_ARG(d.oh > 0 && d.ow > 0, MS_ERR_SHAPE, "maxpool: empty output");
+  return MS_OK;
+}
+
+extern "C" int64_t ms_maxpool2d_out_h(const ms_pool_desc* p) {
+  return (p->h + 2 * p->pad_h - p->kh) / p->stride_h + 1;
+}
+extern "C" int64_t ms_maxpool2d_out_w(const ms_pool_desc* p) {
+  return (p->w + 2 * p->pad_w - p->kw) / p->stride_w + 1;
+}
+
+extern "C" ms_status ms_maxpool2d_fwd(const ms_pool_desc* p, const void* x, void* y,
+                                      void* idx_or_null, void* stream) {
+  PoolDims d;
+  MS_TRY(pool_dims(p, d));
+  if (d.n == 0) return MS_OK;
+  MS_TRY(bind_device(y));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int dt = p->dtype;
+  if (p->layout == MS_NHWC && d.c % 8 == 0 && al16(x) && al16(y) &&
+      (!idx_or_null || (reinterpret_cast<uintptr_t>(idx_or_null) & 7) == 0)) {
+    const int64_t work = (int64_t)d.n * d.oh * d.ow * (d.c / 8);
+    MS_DT_DISPATCH(dt, maxpool_fwd_nhwc8<T><<<grid_for(work), 256, 0, st>>>(
+                           d, (const T*)x, (T*)y, (uint8_t*)idx_or_null));
+  } else {
+    const int64_t work = (int64_t)d.n * d.c * d.oh * d.ow;
+    MS_DT_DISPATCH(dt, maxpool_fwd_generic<T><<<grid_for(work), 256, 0, st>>>(
+                           d, (const T*)x, strides_of(p->layout, d.c, d.h, d.w), (T*)y,
+                           strides_of(p->layout, d.c, d.oh, d.ow), (uint8_t*)idx_or_null));
+  }
+  count_launch();
+  return launch_status("maxpool_fwd");
+}
+
+extern "C" ms_status ms_maxpool2d_bwd(const ms_pool_desc* p, const void* g, const void* idx,
+                                      void* dx, void* stream) {
+  PoolDims d;
+  MS_TRY(pool_dims(p, d));
+  MS_CHECK_ARG(g && idx && dx, MS_ERR_SHAPE, "maxpool bwd: null tensor");
+  if (d.n == 0) return MS_OK;
+  MS_TRY(bind_device(dx));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int dt = p->dtype;
+  if (p->layout == MS_NHWC && d.c % 8 == 0 && al16(g) && al16(dx) &&
+      (reinterpret_cast<uintptr_t>(idx) & 7) == 0) {
+    const int64_t work = (int64_t)d.n * d.h * d.w * (d.c / 8);
+    MS_DT_DISPATCH(dt, maxpool_bwd_nhwc8<T><<<grid_for(work), 256, 0, st>>>(
+                           d, (const T*)g, (const uint8_t*)idx, (T*)dx));
+  } else {
+    const int64_t work = (int64_t)d.n * d.c * d.h * d.w;
+    MS_DT_DISPATCH(dt, maxpool_bwd_generic<T><<<grid_for(work), 256, 0, st>>>(
+                           d, (const T*)g, strides_of(p->layout, d.c, d.oh, d.ow),
+                           (const uint8_t*)idx, (T*)dx, strides_of(p->layout, d.c, d.h, d.w)));
+  }
+  count_launch();
+  return launch_status("maxpool_bwd");
+}

@@ -370,3 +370,128 @@ class _BatchNorm2dEvalFn(torch.autograd.Function):
 def batch_norm_eval(x, running_mean, running_var, weight=None, bias=None, eps=1e-5):
     """Differentiability-agnostic eval-mode batch norm."""
     return _BatchNorm2dEvalFn.apply(x, weight, bias, running_mean, running_var, eps)
+
+
+# =============================================================== relu (bit mask)
+def _dense_format(t: torch.Tensor):
+    """Memory format in which ``t`` is dense (the mask follows storage order)."""
+    if t.is_contiguous():
+        return torch.contiguous_format
+    if _is_channels_last(t):
+        return torch.channels_last
+    return None
+
+
+class _ReLUFn(torch.autograd.Function):
+    """MemSave ReLU (rules.py:98-101, MEMSAVE row): keeps a bit-packed mask of
+    x > 0 (saved.py:53-71, ceil(numel/8) bytes) instead of the output tensor."""
+
+    @staticmethod
+    def forward(ctx, x, inplace: bool):
+        x_rg = ctx.needs_input_grad[0]
+        if _is_meta(x):
+            ctx.save_for_backward(torch.empty((x.numel() + 7) // 8, dtype=torch.uint8,
+                                              device="meta") if x_rg else None)
+            ctx.fmt = torch.contiguous_format
+            return x.new_empty(x.shape)
+        _require_cuda("relu", x)
+        fmt = _dense_format(x)
+        if fmt is None:
+            x = x.contiguous()
+            fmt = torch.contiguous_format
+            inplace = False
+        ctx.fmt = fmt
+        n = x.numel()
+        mask = torch.empty((n + 7) // 8, dtype=torch.uint8, device=x.device) if x_rg else None
+        y = x if inplace else torch.empty_like(x, memory_format=fmt)
+        L = _lib.lib()
+        _lib.check(L.ms_relu_fwd(n, _dtype_code(x), _ptr(x), _ptr(y), _ptr(mask),
+                                 _stream(x.device)), "ms_relu_fwd")
+        if inplace:
+            ctx.mark_dirty(x)
+        ctx.save_for_backward(mask)
+        return y
+
+    @staticmethod
+    def backward(ctx, gy):
+        (mask,) = ctx.saved_tensors
+        if not ctx.needs_input_grad[0]:
+            return None, None
+        mask = _need(mask, "mask", "relu dX")
+        if _is_meta(gy):
+            return gy.new_empty(gy.shape), None
+        g = gy.contiguous(memory_format=ctx.fmt)
+        dx = torch.empty_like(g, memory_format=ctx.fmt)
+        L = _lib.lib()
+        _lib.check(L.ms_relu_bwd(g.numel(), _dtype_code(g), _ptr(g), _ptr(mask), _ptr(dx),
+                                 _stream(g.device)), "ms_relu_bwd")
+        return dx, None
+
+
+def relu(x: torch.Tensor, inplace: bool = False) -> torch.Tensor:
+    """ReLU whose backward reads a 1-bit mask (SPEC.md forward_relu, Masked)."""
+    return _ReLUFn.apply(x, inplace)
+
+
+# =============================================================== maxpool2d (index map)
+class _MaxPool2dFn(torch.autograd.Function):
+    """MemSave MaxPool2d: keeps a 1-byte window-local argmax per output element
+    (rules.py:108-109; the reference's IndexMap, saved.py:111-125, is 4 bytes)."""
+
+    @staticmethod
+    def forward(ctx, x, kernel_size, stride, padding):
+        kh, kw = _pair(kernel_size)
+        sh, sw = _pair(stride)
+        ph, pw = _pair(padding)
+        x_rg = ctx.needs_input_grad[0]
+        if x.dim() != 4:
+            raise RuntimeError("max_pool2d: expected a 4-d input")
+        n, c, h, w = x.shape
+        oh = (h + 2 * ph - kh) // sh + 1
+        ow = (w + 2 * pw - kw) // sw + 1
+        ctx.geom = (tuple(x.shape), kh, kw, sh, sw, ph, pw)
+        if _is_meta(x):
+            ctx.layout = _lib.MS_NCHW
+            ctx.save_for_backward(torch.empty((n, c, oh, ow), dtype=torch.uint8, device="meta")
+                                  if x_rg else None)
+            return x.new_empty((n, c, oh, ow))
+        _require_cuda("max_pool2d", x)
+        layout = _lib.MS_NHWC if (_is_channels_last(x) and not x.is_contiguous()) else _lib.MS_NCHW
+        xl = _as_layout(x, layout)
+        ctx.layout = layout
+        d = _lib.PoolDesc(n, c, h, w, kh, kw, sh, sw, ph, pw, layout, _dtype_code(x))
+        y = _empty4((n, c, oh, ow), x, layout)
+        idx = None
+        if x_rg:
+            mf = torch.channels_last if layout == _lib.MS_NHWC else torch.contiguous_format
+            idx = torch.empty((n, c, oh, ow), dtype=torch.uint8, device=x.device,
+                              memory_format=mf)
+        L = _lib.lib()
+        _lib.check(L.ms_maxpool2d_fwd(ctypes.byref(d), _ptr(xl), _ptr(y), _ptr(idx),
+                                      _stream(x.device)), "ms_maxpool2d_fwd")
+        ctx.save_for_backward(idx)
+        return y
+
+    @staticmethod
+    def backward(ctx, gy):
+        (idx,) = ctx.saved_tensors
+        if not ctx.needs_input_grad[0]:
+            return None, None, None, None
+        idx = _need(idx, "idx", "max_pool2d dX")
+        x_shape, kh, kw, sh, sw, ph, pw = ctx.geom
+        if _is_meta(gy):
+            return gy.new_empty(x_shape), None, None, None
+        layout = ctx.layout
+        g = _as_layout(gy, layout)
+        n, c, h, w = x_shape
+        d = _lib.PoolDesc(n, c, h, w, kh, kw, sh, sw, ph, pw, layout, _dtype_code(g))
+        dx = _empty4(x_shape, g, layout)
+        L = _lib.lib()
+        _lib.check(L.ms_maxpool2d_bwd(ctypes.byref(d), _ptr(g), _ptr(idx), _ptr(dx),
+                                      _stream(g.device)), "ms_maxpool2d_bwd")
+        return dx, None, None, None
+
+
+def max_pool2d(x, kernel_size, stride=None, padding=0):
+    """Max pooling whose backward reads a 1-byte argmax map (SPEC.md forward_maxpool2d)."""
+    return _MaxPool2dFn.apply(x, kernel_size, kernel_size if stride is None else stride, padding)

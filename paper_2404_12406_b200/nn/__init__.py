@@ -16,7 +16,8 @@ from torch import nn
 
 from .. import functional as MF
 
-__all__ = ["MemSaveLinear", "MemSaveConv2d", "MemSaveBatchNorm2d", "convert_to_memory_saving"]
+__all__ = ["MemSaveLinear", "MemSaveConv2d", "MemSaveBatchNorm2d", "MemSaveReLU",
+           "MemSaveMaxPool2d", "convert_to_memory_saving"]
 
 
 def _share_params(dst: nn.Module, src: nn.Module, clone: bool) -> None:
@@ -113,7 +114,46 @@ class MemSaveBatchNorm2d(nn.BatchNorm2d):
         return m
 
 
-_MEMSAVE_TYPES = (MemSaveLinear, MemSaveConv2d, MemSaveBatchNorm2d)
+class MemSaveReLU(nn.ReLU):
+    """nn.ReLU that keeps a 1-bit mask of x > 0 for backward instead of its output
+    (rules.py:98-101, MEMSAVE row; saved.py:53-71)."""
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        return MF.relu(x, self.inplace)
+
+    @classmethod
+    def from_nn_ReLU(cls, relu: nn.ReLU) -> "MemSaveReLU":
+        m = cls(inplace=relu.inplace)
+        m.train(relu.training)
+        return m
+
+
+def maxpool2d_supported(mp: nn.MaxPool2d) -> bool:
+    d = mp.dilation if isinstance(mp.dilation, tuple) else (mp.dilation, mp.dilation)
+    return (not mp.ceil_mode and not mp.return_indices and tuple(d) == (1, 1)
+            and type(mp).__name__ in ("MaxPool2d", "MemSaveMaxPool2d"))
+
+
+class MemSaveMaxPool2d(nn.MaxPool2d):
+    """nn.MaxPool2d that keeps a 1-byte window argmax for backward instead of an
+    int64 index tensor (rules.py:108-109; saved.py:111-125)."""
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        if not maxpool2d_supported(self):
+            raise NotImplementedError("MemSaveMaxPool2d supports dilation=1, ceil_mode=False, "
+                                      "return_indices=False only")
+        return MF.max_pool2d(x, self.kernel_size, self.stride, self.padding)
+
+    @classmethod
+    def from_nn_MaxPool2d(cls, mp: nn.MaxPool2d) -> "MemSaveMaxPool2d":
+        m = cls(mp.kernel_size, stride=mp.stride, padding=mp.padding, dilation=mp.dilation,
+                return_indices=mp.return_indices, ceil_mode=mp.ceil_mode)
+        m.train(mp.training)
+        return m
+
+
+_MEMSAVE_TYPES = (MemSaveLinear, MemSaveConv2d, MemSaveBatchNorm2d, MemSaveReLU,
+                  MemSaveMaxPool2d)
 
 
 def _convert_one(mod: nn.Module, kinds: dict, clone_params: bool):
@@ -125,13 +165,17 @@ def _convert_one(mod: nn.Module, kinds: dict, clone_params: bool):
         return MemSaveConv2d.from_nn_Conv2d(mod, clone_params)
     if kinds.get("batchnorm2d") and type(mod) is nn.BatchNorm2d:
         return MemSaveBatchNorm2d.from_nn_BatchNorm2d(mod, clone_params)
+    if kinds.get("relu") and type(mod) is nn.ReLU:
+        return MemSaveReLU.from_nn_ReLU(mod)
+    if kinds.get("maxpool2d") and type(mod) is nn.MaxPool2d and maxpool2d_supported(mod):
+        return MemSaveMaxPool2d.from_nn_MaxPool2d(mod)
     return None
 
 
 def convert_to_memory_saving(model: nn.Module, linear: bool = True, conv2d: bool = True,
                              conv1d: bool = False, conv3d: bool = False,
-                             batchnorm2d: bool = True, relu: bool = False,
-                             maxpool2d: bool = False, layernorm: bool = False,
+                             batchnorm2d: bool = True, relu: bool = True,
+                             maxpool2d: bool = True, layernorm: bool = False,
                              dropout: bool = False, verbose: bool = False,
                              clone_params: bool = False) -> nn.Module:
     """Swap supported layers of ``model`` for their MemSave equivalents, in place.
@@ -139,11 +183,13 @@ def convert_to_memory_saving(model: nn.Module, linear: bool = True, conv2d: bool
     Mirrors the reference ``convert_network(net, target, layer_filter)``
     (SPEC.md:320-328): the boolean flags are the kind filter, conversion is
     idempotent, parameters are shared with the original modules unless
-    ``clone_params``.  Kinds outside this package's hot path (conv1d/3d, ReLU,
-    MaxPool2d, LayerNorm, Dropout — SURVEY.md §8(f)) are accepted for API
-    compatibility and left untouched.  Returns the (possibly replaced) model.
+    ``clone_params``.  ReLU (bit mask) and MaxPool2d (1-byte argmax) are the
+    first "next" rows of SURVEY.md §8(f); conv1d/3d, LayerNorm and Dropout are
+    accepted for API compatibility and left untouched.  Returns the (possibly
+    replaced) model.
     """
-    kinds = {"linear": linear, "conv2d": conv2d, "batchnorm2d": batchnorm2d}
+    kinds = {"linear": linear, "conv2d": conv2d, "batchnorm2d": batchnorm2d, "relu": relu,
+             "maxpool2d": maxpool2d}
     top = _convert_one(model, kinds, clone_params)
     if top is not None:
         if verbose:

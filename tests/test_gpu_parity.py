@@ -279,3 +279,66 @@ def test_saved_set_cuda(rules_golden, x_rg, w_rg):
     exp = [row for row in rules_golden if row["kind"] == "conv2d" and row["policy"] == "memsave"
            and row["x_rg"] == bool(x_rg) and row["w_rg"] == bool(w_rg) and not row["b_rg"]][0]
     assert roles == sorted(r for r, _ in exp["saves"])
+
+
+
+# ------------------------------------------------------------------ relu / maxpool
+@pytest.mark.parametrize("dt", ["bf16", "f32"])
+@pytest.mark.parametrize("channels_last", [False, True])
+@pytest.mark.parametrize("inplace", [False, True])
+def test_relu_bitmask(dt, channels_last, inplace):
+    rng = np.random.default_rng(5)
+    x64 = rng.standard_normal((3, 16, 7, 9))
+    x64[0, 0, 0, :4] = 0.0  # ties at zero -> mask 0
+    x, xq = _q(x64, dt)
+    g, gq = _q(rng.standard_normal(x64.shape), dt)
+    if channels_last:
+        x = x.contiguous(memory_format=torch.channels_last)
+    leaf = x.clone().requires_grad_(True)
+    h = leaf * 1.0  # non-leaf so that in-place is allowed
+    y = MF.relu(h, inplace)
+    y.backward(g)
+    yr, mr = oracle.relu_fwd(xq)
+    np.testing.assert_array_equal(y.detach().float().cpu().numpy(), yr)
+    np.testing.assert_array_equal(leaf.grad.float().cpu().numpy(), oracle.relu_bwd(gq, mr))
+
+
+def test_relu_odd_numel():
+    x = torch.randn(1001, device=DEV, dtype=torch.bfloat16, requires_grad=True)
+    y = MF.relu(x)
+    y.backward(torch.ones_like(y))
+    torch.testing.assert_close(y, torch.relu(x.detach()))
+    torch.testing.assert_close(x.grad, (x.detach() > 0).to(torch.bfloat16))
+
+
+def test_maxpool_golden():
+    import os
+    gd = dict(np.load(os.path.join(os.path.dirname(__file__), "golden", "maxpool_ref.npz")))
+    for case in ("mp_2x2s2", "mp_3x3s2", "mp_3x3s1", "mp_ties"):
+        kh, kw, sh, sw = (int(v) for v in gd[f"{case}/geom"])
+        x = torch.tensor(gd[f"{case}/x"], dtype=torch.float32, device=DEV, requires_grad=True)
+        y = MF.max_pool2d(x, (kh, kw), (sh, sw), 0)
+        y.backward(torch.tensor(gd[f"{case}/g"], dtype=torch.float32, device=DEV))
+        np.testing.assert_allclose(y.detach().cpu().double().numpy(), gd[f"{case}/y"], rtol=1e-6)
+        np.testing.assert_allclose(x.grad.cpu().double().numpy(), gd[f"{case}/dx"], rtol=1e-5,
+                                   atol=1e-6)
+
+
+@pytest.mark.parametrize("shape,k,s,p", [((4, 64, 56, 56), 3, 2, 1), ((2, 24, 15, 13), 3, 2, 1),
+                                          ((2, 8, 9, 9), 2, 2, 0), ((3, 5, 10, 8), 3, 1, 1)])
+@pytest.mark.parametrize("dt", ["bf16", "f32"])
+def test_maxpool_padded(shape, k, s, p, dt):
+    rng = np.random.default_rng(sum(shape))
+    x, xq = _q(rng.standard_normal(shape), dt)
+    x = x.contiguous(memory_format=torch.channels_last).requires_grad_(True)
+    y = MF.max_pool2d(x, k, s, p)
+    yr, local, flat = oracle.maxpool2d_fwd(xq, k, k, s, s, p, p)
+    g, gq = _q(rng.standard_normal(yr.shape), dt)
+    y.backward(g)
+    np.testing.assert_array_equal(y.detach().float().cpu().double().numpy(), yr)
+    _close(x.grad, oracle.maxpool2d_bwd(gq, flat, shape[2], shape[3]), dt, "maxpool dx",
+           ulps=2.01)
+    # against torch's own max_pool2d on the same values (ties: first occurrence)
+    xt = x.detach().float().cpu().requires_grad_(True)
+    torch.nn.functional.max_pool2d(xt, k, s, p).backward(g.float().cpu())
+    np.testing.assert_allclose(x.grad.float().cpu().numpy(), xt.grad.numpy(), rtol=1e-2, atol=1e-2)

@@ -93,3 +93,28 @@ def test_tolerance_helpers():
     v = np.random.default_rng(2).standard_normal(1000)
     t = torch.tensor(v, dtype=torch.float64).to(torch.bfloat16).double().numpy()
     assert np.array_equal(oracle.round_to(v, "bf16"), t)
+
+
+POOL_CASES = ["mp_2x2s2", "mp_3x3s2", "mp_3x3s1", "mp_ties"]
+
+
+@pytest.mark.parametrize("case", POOL_CASES)
+def test_maxpool_oracle_matches_reference_kernels(case):
+    import os
+    g = dict(np.load(os.path.join(os.path.dirname(__file__), "golden", "maxpool_ref.npz")))
+    kh, kw, sh, sw = (int(v) for v in g[f"{case}/geom"])
+    x = g[f"{case}/x"]
+    y, local, flat = oracle.maxpool2d_fwd(x, kh, kw, sh, sw)
+    np.testing.assert_array_equal(y, g[f"{case}/y"])
+    np.testing.assert_array_equal(flat, g[f"{case}/idx"])  # same first-occurrence argmax
+    dx = oracle.maxpool2d_bwd(g[f"{case}/g"], flat, x.shape[2], x.shape[3])
+    np.testing.assert_allclose(dx, g[f"{case}/dx"], rtol=1e-12, atol=1e-12)
+
+
+def test_relu_known_answers():
+    # SPEC.md forward_relu: x = [-1, 2, 0, 3] -> y = [0, 2, 0, 3], mask bits (0, 1, 0, 1)
+    y, mask = oracle.relu_fwd(np.array([-1.0, 2.0, 0.0, 3.0]))
+    assert y.tolist() == [0, 2, 0, 3] and mask.tolist() == [False, True, False, True]
+    assert oracle.relu_bwd(np.ones(4), mask).tolist() == [0, 1, 0, 1]
+    # BitMask byte cost for numel 10^6: 125000 B (SPEC.md, "32x reduction")
+    assert (10**6 + 7) // 8 == 125000

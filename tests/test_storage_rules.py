@@ -123,3 +123,45 @@ def test_stock_torch_matches_naive_row(rules_golden, kind):
     naive = _golden_saves(rules_golden, kind, True, False, False, policy="naive")
     assert naive == ["w", "x"]
     assert (2, 4, 6, 6) in packed  # stock keeps X; MemSave does not
+
+
+@pytest.mark.parametrize("x_rg", [False, True])
+def test_relu_saved_set_is_a_bitmask(rules_golden, x_rg):
+    x = _make((2, 5, 4, 3), x_rg)
+    packed = []
+
+    def pack(t):
+        packed.append((tuple(t.shape), t.dtype))
+        return t
+
+    with torch.autograd.graph.saved_tensors_hooks(pack, lambda t: t):
+        out = MF.relu(x)
+    exp = _golden_saves(rules_golden, "relu", x_rg, False, False)
+    assert exp == (["mask"] if x_rg else [])
+    if x_rg:
+        # one bit per element, not a copy of the output (saved.py:53-71)
+        assert packed == [(((2 * 5 * 4 * 3 + 7) // 8,), torch.uint8)]
+        out.sum().backward()
+    else:
+        assert packed == []
+
+
+@pytest.mark.parametrize("x_rg", [False, True])
+def test_maxpool_saved_set_is_an_index_map(rules_golden, x_rg):
+    x = _make((2, 5, 9, 9), x_rg)
+    packed = []
+
+    def pack(t):
+        packed.append((tuple(t.shape), t.dtype))
+        return t
+
+    with torch.autograd.graph.saved_tensors_hooks(pack, lambda t: t):
+        out = MF.max_pool2d(x, 3, 2, 1)
+    exp = _golden_saves(rules_golden, "maxpool2d", x_rg, False, False)
+    assert exp == (["idx"] if x_rg else [])
+    assert out.shape == (2, 5, 5, 5)
+    if x_rg:
+        assert packed == [((2, 5, 5, 5), torch.uint8)]  # 1 byte per output element
+        out.sum().backward()
+    else:
+        assert packed == []
