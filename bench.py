@@ -342,6 +342,8 @@ def gpu_main(args):
         "metric": METRIC,
         "value": round(value, 2),
         "unit": "samples/s",
+        "tokens_per_s": (round(value * wl.config["seq_len"], 1) if "seq_len" in wl.config
+                         else None),
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
@@ -449,7 +451,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="memsave", choices=["memsave", "reference"])
-    ap.add_argument("--config", default="resnet18", choices=["resnet18", "fig1"])
+    ap.add_argument("--config", default="resnet18",
+                    choices=["resnet18", "fig1", "resnet101", "vgg16", "bert", "llama"])
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--no-stock", action="store_true")
     ap.add_argument("--no-roofline", action="store_true")

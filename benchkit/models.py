@@ -92,7 +92,122 @@ def fig1_cnn(batch: int = 32, dtype=torch.float32, device="cuda", depth: int = 8
                      "image": [8, 256, 256], "layout": "NCHW", "trainable": "0.weight"})
 
 
-WORKLOADS = {"resnet18": resnet18_input_only, "fig1": fig1_cnn}
+def _image_batch(dtype, requires_grad=False, classes=1000):
+    def make_batch(b, dev):
+        gen = torch.Generator(device=dev).manual_seed(1)
+        x = torch.randn((b, 3, 224, 224), generator=gen, device=dev, dtype=dtype)
+        x = x.contiguous(memory_format=torch.channels_last)
+        y = torch.randint(0, classes, (b,), generator=gen, device=dev)
+        return x, y
+    return make_batch
+
+
+def _ce_loss(model, x, y):
+    return nn.functional.cross_entropy(model(x).float(), y)
+
+
+def resnet101_finetune(batch: int = 128, dtype=torch.bfloat16, device="cuda") -> Workload:
+    """configs[2] (ResNet-101 reading): last 2 Bottlenecks (layer4.1, layer4.2) + fc + all
+    BN affine params trainable, BN in eval mode, input without grad."""
+    import torchvision
+    torch.manual_seed(0)
+    m = torchvision.models.resnet101()
+    randomize_bn_stats(m)
+    m = m.to(device=device, dtype=dtype).to(memory_format=torch.channels_last).eval()
+    for name, p in m.named_parameters():
+        p.requires_grad_(name.startswith(("layer4.1.", "layer4.2.", "fc.")) or ".bn" in name
+                         or "downsample.1" in name or name.startswith("bn1"))
+    ntrain = sum(p.numel() for p in m.parameters() if p.requires_grad)
+    return Workload("resnet101_finetune", m, _image_batch(dtype), _ce_loss, batch, False, dtype,
+                    {"workload": "ResNet-101 fine-tuning: layer4.1, layer4.2, fc and all BN "
+                                 "affine parameters trainable, BN eval", "model": "resnet101",
+                     "global_batch": batch, "image": [3, 224, 224], "layout": "channels_last",
+                     "trainable_params": ntrain})
+
+
+def vgg16_finetune(batch: int = 128, dtype=torch.bfloat16, device="cuda") -> Workload:
+    """configs[2] (VGG-16 reading): conv blocks 4-5 (features[17:]) + classifier trainable,
+    eval mode (dropout off), input without grad."""
+    import torchvision
+    torch.manual_seed(0)
+    m = torchvision.models.vgg16()
+    m = m.to(device=device, dtype=dtype).to(memory_format=torch.channels_last).eval()
+    for name, p in m.named_parameters():
+        layer = name.split(".")
+        trainable = name.startswith("classifier.") or (layer[0] == "features" and
+                                                       int(layer[1]) >= 17)
+        p.requires_grad_(trainable)
+    ntrain = sum(p.numel() for p in m.parameters() if p.requires_grad)
+    return Workload("vgg16_finetune", m, _image_batch(dtype), _ce_loss, batch, False, dtype,
+                    {"workload": "VGG-16 fine-tuning: conv blocks 4-5 (features[17:]) and the "
+                                 "classifier trainable", "model": "vgg16", "global_batch": batch,
+                     "image": [3, 224, 224], "layout": "channels_last",
+                     "trainable_params": ntrain})
+
+
+def bert_base_biases(batch: int = 64, seq: int = 512, dtype=torch.bfloat16,
+                     device="cuda") -> Workload:
+    """configs[3]: BERT-base random init, only the attention Linear biases and the
+    classifier trainable, train mode (dropout 0.1), seq 512, batch 64."""
+    from transformers import BertConfig, BertForSequenceClassification
+    torch.manual_seed(0)
+    cfg = BertConfig(num_labels=2, attn_implementation="sdpa")
+    m = BertForSequenceClassification(cfg).to(device=device, dtype=dtype).train()
+    for name, p in m.named_parameters():
+        p.requires_grad_(name.startswith("classifier.") or (
+            ".attention." in name and name.endswith(".bias") and "LayerNorm" not in name))
+    ntrain = sum(p.numel() for p in m.parameters() if p.requires_grad)
+
+    def make_batch(b, dev):
+        gen = torch.Generator(device=dev).manual_seed(1)
+        ids = torch.randint(0, cfg.vocab_size, (b, seq), generator=gen, device=dev)
+        y = torch.randint(0, 2, (b,), generator=gen, device=dev)
+        return ids, y
+
+    def loss_fn(model, ids, y):
+        return nn.functional.cross_entropy(model(input_ids=ids).logits.float(), y)
+
+    return Workload("bert_base_biases", m, make_batch, loss_fn, batch, False, dtype,
+                    {"workload": "BERT-base random init, attention Linear biases + classifier "
+                                 "trainable, train mode", "model": "bert-base", "global_batch": batch,
+                     "seq_len": seq, "trainable_params": ntrain})
+
+
+def llama3_8b_last4(batch: int = 2, seq: int = 2048, dtype=torch.bfloat16, device="cuda",
+                    layers: int = 32) -> Workload:
+    """configs[4]: Llama-3-8B architecture, random init, frozen except the last 4 decoder
+    layers, seq 2048, batch 2 per GPU."""
+    from transformers import LlamaConfig, LlamaForCausalLM
+    torch.manual_seed(0)
+    cfg = LlamaConfig(vocab_size=128256, hidden_size=4096, intermediate_size=14336,
+                      num_hidden_layers=layers, num_attention_heads=32, num_key_value_heads=8,
+                      max_position_embeddings=8192, rope_theta=500000.0,
+                      attn_implementation="sdpa", torch_dtype=dtype)
+    with torch.device(device):
+        m = LlamaForCausalLM(cfg).to(dtype)
+    m.train()
+    for name, p in m.named_parameters():
+        parts = name.split(".")
+        trainable = len(parts) > 3 and parts[1] == "layers" and int(parts[2]) >= layers - 4
+        p.requires_grad_(trainable)
+    ntrain = sum(p.numel() for p in m.parameters() if p.requires_grad)
+
+    def make_batch(b, dev):
+        gen = torch.Generator(device=dev).manual_seed(1)
+        return (torch.randint(0, cfg.vocab_size, (b, seq), generator=gen, device=dev),)
+
+    def loss_fn(model, ids):
+        return model(input_ids=ids, labels=ids).loss
+
+    return Workload("llama3_8b_last4", m, make_batch, loss_fn, batch, False, dtype,
+                    {"workload": "Llama-3-8B architecture random init, last 4 decoder layers "
+                                 "trainable", "model": "llama3-8b-arch", "global_batch": batch,
+                     "seq_len": seq, "trainable_params": ntrain})
+
+
+WORKLOADS = {"resnet18": resnet18_input_only, "fig1": fig1_cnn,
+             "resnet101": resnet101_finetune, "vgg16": vgg16_finetune,
+             "bert": bert_base_biases, "llama": llama3_8b_last4}
 
 
 def resnet18_conv_shapes(batch: int):

@@ -71,33 +71,54 @@ __device__ __forceinline__ void st8(T* p, const float (&v)[8], bool vec) {
 }
 
 // ---------------------------------------------------------------- ReLU
+// Each thread handles RELU_UNR groups of 8 elements per iteration, loads first
+// (memory-level parallelism), then computes and stores.
+constexpr int RELU_UNR = 4;
+
+template <typename T>
+__device__ __forceinline__ uint32_t relu8(float (&v)[8]) {
+  uint32_t bits = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const bool pos = !(v[j] <= 0.f);  // x > 0, and NaN propagates like torch.relu
+    bits |= (pos ? 1u : 0u) << j;
+    v[j] = pos ? v[j] : 0.f;
+  }
+  return bits;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) relu_fwd_kernel(int64_t n, const T* x, T* y,
                                                        uint8_t* __restrict__ mask, bool vec) {
-  const int64_t groups = (n + 7) / 8;
-  for (int64_t gi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gi < groups;
-       gi += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e = gi * 8;
-    float v[8];
-    uint32_t bits = 0;
-    if (e + 8 <= n) {
-      ld8<T>(x + e, v, vec);
+  const int64_t full = n / 8;  // complete groups
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t g0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g0 < full;
+       g0 += stride * RELU_UNR) {
+    float v[RELU_UNR][8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const bool pos = !(v[j] <= 0.f);  // x > 0, and NaN propagates like torch.relu
-        bits |= (pos ? 1u : 0u) << j;
-        v[j] = pos ? v[j] : 0.f;
-      }
-      st8<T>(y + e, v, vec);
-    } else {
-      for (int j = 0; j < 8 && e + j < n; ++j) {
-        const float a = IO<T>::ld(x + e + j);
-        const bool pos = !(a <= 0.f);
-        bits |= (pos ? 1u : 0u) << j;
-        y[e + j] = IO<T>::cvt(pos ? a : 0.f);
-      }
+    for (int u = 0; u < RELU_UNR; ++u) {
+      const int64_t gi = g0 + u * stride;
+      if (gi < full) ld8<T>(x + gi * 8, v[u], vec);
     }
-    if (mask) mask[gi] = static_cast<uint8_t>(bits);
+#pragma unroll
+    for (int u = 0; u < RELU_UNR; ++u) {
+      const int64_t gi = g0 + u * stride;
+      if (gi >= full) continue;
+      const uint32_t bits = relu8<T>(v[u]);
+      st8<T>(y + gi * 8, v[u], vec);
+      if (mask) mask[gi] = static_cast<uint8_t>(bits);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && full * 8 < n) {  // tail group
+    const int64_t e = full * 8;
+    uint32_t bits = 0;
+    for (int j = 0; e + j < n; ++j) {
+      const float a = IO<T>::ld(x + e + j);
+      const bool pos = !(a <= 0.f);
+      bits |= (pos ? 1u : 0u) << j;
+      y[e + j] = IO<T>::cvt(pos ? a : 0.f);
+    }
+    if (mask) mask[full] = static_cast<uint8_t>(bits);
   }
 }
 
@@ -105,21 +126,34 @@ template <typename T>
 __global__ void __launch_bounds__(256) relu_bwd_kernel(int64_t n, const T* g,
                                                        const uint8_t* __restrict__ mask, T* dx,
                                                        bool vec) {
-  const int64_t groups = (n + 7) / 8;
-  for (int64_t gi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gi < groups;
-       gi += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e = gi * 8;
-    const uint32_t bits = mask[gi];
-    if (e + 8 <= n) {
-      float v[8];
-      ld8<T>(g + e, v, vec);
+  const int64_t full = n / 8;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t g0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g0 < full;
+       g0 += stride * RELU_UNR) {
+    float v[RELU_UNR][8];
+    uint32_t bits[RELU_UNR];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) v[j] = (bits >> j) & 1u ? v[j] : 0.f;
-      st8<T>(dx + e, v, vec);
-    } else {
-      for (int j = 0; j < 8 && e + j < n; ++j)
-        dx[e + j] = IO<T>::cvt((bits >> j) & 1u ? IO<T>::ld(g + e + j) : 0.f);
+    for (int u = 0; u < RELU_UNR; ++u) {
+      const int64_t gi = g0 + u * stride;
+      if (gi < full) {
+        ld8<T>(g + gi * 8, v[u], vec);
+        bits[u] = mask[gi];
+      }
     }
+#pragma unroll
+    for (int u = 0; u < RELU_UNR; ++u) {
+      const int64_t gi = g0 + u * stride;
+      if (gi >= full) continue;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[u][j] = (bits[u] >> j) & 1u ? v[u][j] : 0.f;
+      st8<T>(dx + gi * 8, v[u], vec);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && full * 8 < n) {
+    const int64_t e = full * 8;
+    const uint32_t bits = mask[full];
+    for (int j = 0; e + j < n; ++j)
+      dx[e + j] = IO<T>::cvt((bits >> j) & 1u ? IO<T>::ld(g + e + j) : 0.f);
   }
 }
 
@@ -133,16 +167,17 @@ template <typename T>
 __global__ void __launch_bounds__(256) maxpool_fwd_nhwc8(PoolDims d, const T* __restrict__ x,
                                                          T* __restrict__ y,
                                                          uint8_t* __restrict__ idx) {
-  const int G = d.c / 8;
-  const int64_t total = (int64_t)d.n * d.oh * d.ow * G;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int g = t % G;
-    int64_t p = t / G;
-    const int ow = p % d.ow;
-    p /= d.ow;
-    const int oh = p % d.oh;
-    const int n = (int)(p / d.oh);
+  // 32-bit index math: the host routes tensors with >= 2^31 vector groups to
+  // the generic kernel
+  const int G = d.c >> 3;
+  const int total = d.n * d.oh * d.ow * G;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const int pix = t / G;
+    const int g = t - pix * G;
+    const int ow = pix % d.ow;
+    const int nh = pix / d.ow;
+    const int oh = nh % d.oh;
+    const int n = nh / d.oh;
     float best[8];
     uint32_t arg[8];
 #pragma unroll
@@ -151,6 +186,7 @@ __global__ void __launch_bounds__(256) maxpool_fwd_nhwc8(PoolDims d, const T* __
       arg[j] = 0;
     }
     bool first = true;
+    const T* xn = x + (int64_t)n * d.h * d.w * d.c + g * 8;
     for (int r = 0; r < d.kh; ++r) {
       const int ih = oh * d.sh - d.ph + r;
       if (ih < 0 || ih >= d.h) continue;
@@ -158,7 +194,7 @@ __global__ void __launch_bounds__(256) maxpool_fwd_nhwc8(PoolDims d, const T* __
         const int iw = ow * d.sw - d.pw + s;
         if (iw < 0 || iw >= d.w) continue;
         float v[8];
-        ld8<T>(x + (((int64_t)n * d.h + ih) * d.w + iw) * d.c + g * 8, v, true);
+        ld8<T>(xn + ((int64_t)ih * d.w + iw) * d.c, v, true);
         const uint32_t k = r * d.kw + s;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
@@ -170,7 +206,7 @@ __global__ void __launch_bounds__(256) maxpool_fwd_nhwc8(PoolDims d, const T* __
         first = false;
       }
     }
-    const int64_t o = (((int64_t)n * d.oh + oh) * d.ow + ow) * d.c + g * 8;
+    const int64_t o = (int64_t)pix * d.c + g * 8;
     st8<T>(y + o, best, true);
     if (idx) {
       uint2 u;
@@ -185,22 +221,22 @@ template <typename T>
 __global__ void __launch_bounds__(256) maxpool_bwd_nhwc8(PoolDims d, const T* __restrict__ g,
                                                          const uint8_t* __restrict__ idx,
                                                          T* __restrict__ dx) {
-  const int G = d.c / 8;
-  const int64_t total = (int64_t)d.n * d.h * d.w * G;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int gg = t % G;
-    int64_t p = t / G;
-    const int iw = p % d.w;
-    p /= d.w;
-    const int ih = p % d.h;
-    const int n = (int)(p / d.h);
+  const int G = d.c >> 3;
+  const int total = d.n * d.h * d.w * G;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const int pix = t / G;
+    const int gg = t - pix * G;
+    const int iw = pix % d.w;
+    const int nh = pix / d.w;
+    const int ih = nh % d.h;
+    const int n = nh / d.h;
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     // windows (oh, ow) with oh*sh - ph <= ih <= oh*sh - ph + kh - 1
     const int oh_lo = max(0, (ih + d.ph - d.kh + d.sh) / d.sh);
     const int oh_hi = min(d.oh - 1, (ih + d.ph) / d.sh);
     const int ow_lo = max(0, (iw + d.pw - d.kw + d.sw) / d.sw);
     const int ow_hi = min(d.ow - 1, (iw + d.pw) / d.sw);
+    const int64_t nbase = (int64_t)n * d.oh * d.ow;
     for (int oh = oh_lo; oh <= oh_hi; ++oh) {
       const int r = ih + d.ph - oh * d.sh;
       if (r < 0 || r >= d.kh) continue;
@@ -208,8 +244,14 @@ __global__ void __launch_bounds__(256) maxpool_bwd_nhwc8(PoolDims d, const T* __
         const int s = iw + d.pw - ow * d.sw;
         if (s < 0 || s >= d.kw) continue;
         const uint32_t k = r * d.kw + s;
-        const int64_t o = (((int64_t)n * d.oh + oh) * d.ow + ow) * d.c + gg * 8;
+        const int64_t o = (nbase + (int64_t)oh * d.ow + ow) * d.c + gg * 8;
         const uint2 u = *reinterpret_cast<const uint2*>(idx + o);
+        // skip the gradient load when no lane of this window picked (ih, iw)
+        const uint32_t kk = k * 0x01010101u;
+        const uint32_t hx = u.x ^ kk, hy = u.y ^ kk;
+        const bool any = ((hx - 0x01010101u) & ~hx & 0x80808080u) ||
+                         ((hy - 0x01010101u) & ~hy & 0x80808080u);
+        if (!any) continue;
         float gv[8];
         ld8<T>(g + o, gv, true);
 #pragma unroll
@@ -219,7 +261,7 @@ __global__ void __launch_bounds__(256) maxpool_bwd_nhwc8(PoolDims d, const T* __
         }
       }
     }
-    st8<T>(dx + (((int64_t)n * d.h + ih) * d.w + iw) * d.c + gg * 8, acc, true);
+    st8<T>(dx + (int64_t)pix * d.c + gg * 8, acc, true);
   }
 }
 
@@ -311,7 +353,7 @@ extern "C" ms_status ms_relu_fwd(int64_t numel, int32_t dt, const void* x, void*
   MS_TRY(bind_device(y));
   cudaStream_t st = (cudaStream_t)stream;
   const bool vec = al16(x) && al16(y);
-  MS_DT_DISPATCH(dt, relu_fwd_kernel<T><<<grid_for((numel + 7) / 8), 256, 0, st>>>(
+  MS_DT_DISPATCH(dt, relu_fwd_kernel<T><<<grid_for((numel + 31) / 32), 256, 0, st>>>(
                          numel, (const T*)x, (T*)y, (uint8_t*)mask_or_null, vec));
   count_launch();
   return launch_status("relu_fwd_kernel");
@@ -324,7 +366,7 @@ extern "C" ms_status ms_relu_bwd(int64_t numel, int32_t dt, const void* g, const
   MS_TRY(bind_device(dx));
   cudaStream_t st = (cudaStream_t)stream;
   const bool vec = al16(g) && al16(dx);
-  MS_DT_DISPATCH(dt, relu_bwd_kernel<T><<<grid_for((numel + 7) / 8), 256, 0, st>>>(
+  MS_DT_DISPATCH(dt, relu_bwd_kernel<T><<<grid_for((numel + 31) / 32), 256, 0, st>>>(
                          numel, (const T*)g, (const uint8_t*)mask, (T*)dx, vec));
   count_launch();
   return launch_status("relu_bwd_kernel");
@@ -361,7 +403,8 @@ extern "C" ms_status ms_maxpool2d_fwd(const ms_pool_desc* p, const void* x, void
   cudaStream_t st = (cudaStream_t)stream;
   const int dt = p->dtype;
   if (p->layout == MS_NHWC && d.c % 8 == 0 && al16(x) && al16(y) &&
-      (!idx_or_null || (reinterpret_cast<uintptr_t>(idx_or_null) & 7) == 0)) {
+      (!idx_or_null || (reinterpret_cast<uintptr_t>(idx_or_null) & 7) == 0) &&
+      (int64_t)d.n * d.h * d.w * (d.c / 8) < (1ll << 31)) {
     const int64_t work = (int64_t)d.n * d.oh * d.ow * (d.c / 8);
     MS_DT_DISPATCH(dt, maxpool_fwd_nhwc8<T><<<grid_for(work), 256, 0, st>>>(
                            d, (const T*)x, (T*)y, (uint8_t*)idx_or_null));
@@ -385,7 +428,8 @@ extern "C" ms_status ms_maxpool2d_bwd(const ms_pool_desc* p, const void* g, cons
   cudaStream_t st = (cudaStream_t)stream;
   const int dt = p->dtype;
   if (p->layout == MS_NHWC && d.c % 8 == 0 && al16(g) && al16(dx) &&
-      (reinterpret_cast<uintptr_t>(idx) & 7) == 0) {
+      (reinterpret_cast<uintptr_t>(idx) & 7) == 0 &&
+      (int64_t)d.n * d.h * d.w * (d.c / 8) < (1ll << 31)) {
     const int64_t work = (int64_t)d.n * d.h * d.w * (d.c / 8);
     MS_DT_DISPATCH(dt, maxpool_bwd_nhwc8<T><<<grid_for(work), 256, 0, st>>>(
                            d, (const T*)g, (const uint8_t*)idx, (T*)dx));
