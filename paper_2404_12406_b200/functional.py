@@ -93,13 +93,15 @@ class _LinearFn(torch.autograd.Function):
         w = weight.contiguous()
         b = None if bias is None else bias.to(x.dtype).contiguous()
         M = x2.shape[0]
-        y = torch.empty((M, N), dtype=x.dtype, device=x.device)
+        # allocated in its final shape: returning a view of an internal buffer would
+        # make in-place consumers (e.g. ReLU(inplace=True)) illegal for autograd
+        y = torch.empty(out_shape, dtype=x.dtype, device=x.device)
         L = _lib.lib()
         dt = _dtype_code(x)
         ws, nb = _workspace(L.ms_linear_workspace(M, N, K, dt, 0), x.device)
         _lib.check(L.ms_linear_fwd(M, N, K, dt, _ptr(x2), _ptr(w), _ptr(b), _ptr(y), _ptr(ws), nb,
                                    _stream(x.device)), "ms_linear_fwd")
-        return y.view(out_shape)
+        return y
 
     @staticmethod
     def backward(ctx, gy):
@@ -124,11 +126,10 @@ class _LinearFn(torch.autograd.Function):
         if need_x:
             w = _need(w, "w", "linear dX")
             K = w.shape[1]
-            dx = torch.empty((M, K), dtype=g2.dtype, device=g2.device)
+            dx = torch.empty(ctx.x_shape, dtype=g2.dtype, device=g2.device)
             ws, nb = _workspace(L.ms_linear_workspace(M, N, K, dt, 1), g2.device)
             _lib.check(L.ms_linear_dx(M, N, K, dt, _ptr(g2), _ptr(w.contiguous()), _ptr(dx),
                                       _ptr(ws), nb, st), "ms_linear_dx")
-            dx = dx.view(ctx.x_shape)
         if need_w:
             x = _need(x, "x", "linear dW")
             K = x.shape[-1]
