@@ -391,6 +391,11 @@ extern "C" ms_status ms_conv2d_fwd(const ms_conv_desc* d, const void* x, const v
   MS_CHECK_ARG(ws_bytes >= p.ws && (p.ws == 0 || ws), MS_ERR_WORKSPACE,
                "conv fwd: workspace %zu < %zu", ws_bytes, p.ws);
   if (p.tc) return fwd_tc(d, p, x, w, bias, y, ws, st);
+  if (d->dtype == MS_F32 && !bias) {
+    const ms_status s = small_conv_fp32(MS_CONV_FWD, dims_of(d), d->layout, d->wlayout, x, w, y,
+                                        ws, ws_bytes, st);
+    if (s != MS_ERR_UNSUPPORTED) return s;
+  }
   return simt_conv_fwd(dims_of(d), d->dtype, d->layout, d->wlayout, x, w, bias, y, st);
 }
 
@@ -404,6 +409,11 @@ extern "C" ms_status ms_conv2d_dx(const ms_conv_desc* d, const void* dy, const v
   MS_CHECK_ARG(ws_bytes >= p.ws && (p.ws == 0 || ws), MS_ERR_WORKSPACE,
                "conv dx: workspace %zu < %zu", ws_bytes, p.ws);
   if (p.tc) return dx_tc(d, p, dy, w, dx, ws, st);
+  if (d->dtype == MS_F32) {
+    const ms_status s = small_conv_fp32(MS_CONV_DX, dims_of(d), d->layout, d->wlayout, dy, w, dx,
+                                        ws, ws_bytes, st);
+    if (s != MS_ERR_UNSUPPORTED) return s;
+  }
   return simt_conv_dx(dims_of(d), d->dtype, d->layout, d->wlayout, dy, w, dx, st);
 }
 
@@ -422,6 +432,11 @@ extern "C" ms_status ms_conv2d_dw(const ms_conv_desc* d, const void* x, const vo
                : MS_ERR_LAUNCH;
   }
   if (p.tc) return dw_tc(d, p, x, dy, dw, ws, st);
+  if (d->dtype == MS_F32) {
+    const ms_status s = small_conv_fp32(MS_CONV_DW, dims_of(d), d->layout, d->wlayout, x, dy, dw,
+                                        ws, ws_bytes, st);
+    if (s != MS_ERR_UNSUPPORTED) return s;
+  }
   return simt_conv_dw(dims_of(d), d->dtype, d->layout, d->wlayout, x, dy, dw, ws, ws_bytes, st);
 }
 

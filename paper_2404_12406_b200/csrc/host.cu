@@ -206,6 +206,7 @@ static ms_status launch_t(const TmapPack& tm, const GemmArgs& g, cudaStream_t st
     case 32: return launch_t<32, A, B, M>(tm, g, st);           \
     case 64: return launch_t<64, A, B, M>(tm, g, st);           \
     case 128: return launch_t<128, A, B, M>(tm, g, st);         \
+    case 192: return launch_t<192, A, B, M>(tm, g, st);         \
     case 256: return launch_t<256, A, B, M>(tm, g, st);         \
     default: break;                                             \
   }
@@ -233,6 +234,7 @@ ms_status launch_umma(int bn, int a_mn, int b_mn, int mode, const TmapPack& tm,
   } else if (mode == LOAD_CONV_WGRAD) {
     switch (bn) {
       case 64: return launch_t<64, 1, 1, LOAD_CONV_WGRAD>(tm, g, st);
+      case 192: return launch_t<192, 1, 1, LOAD_CONV_WGRAD>(tm, g, st);
       case 128: return launch_t<128, 1, 1, LOAD_CONV_WGRAD>(tm, g, st);
       case 256: return launch_t<256, 1, 1, LOAD_CONV_WGRAD>(tm, g, st);
       default: break;
@@ -245,14 +247,23 @@ ms_status launch_umma(int bn, int a_mn, int b_mn, int mode, const TmapPack& tm,
 int pick_bn(int64_t other_tiles, int64_t ncols) {
   if (ncols <= 32) return 32;
   if (ncols <= 64) return 64;
-  int bn = 256;
-  while (bn > 64) {
+  // Persistent CTAs take tiles round-robin, so a launch costs about
+  // ceil(tiles / #SMs) tile-times; a tile costs ~ (BN + 64) column-units (the
+  // constant is the per-tile epilogue / pipeline overhead).  Pick the cheapest.
+  static const int cands[] = {256, 192, 128, 64};
+  int best = 256;
+  double best_cost = 1e30;
+  for (int bn : cands) {
+    if (bn > 128 && ncols <= 128) continue;
     const int64_t tiles = other_tiles * ((ncols + bn - 1) / bn);
-    if (tiles >= num_sms()) break;
-    bn >>= 1;
+    const int64_t waves = (tiles + num_sms() - 1) / num_sms();
+    const double cost = (double)waves * (bn + 64);
+    if (cost < best_cost * 0.97) {  // prefer the larger tile on near-ties
+      best_cost = cost;
+      best = bn;
+    }
   }
-  if (ncols <= 128 && bn > 128) bn = 128;
-  return bn;
+  return best;
 }
 
 }  // namespace ms

@@ -23,6 +23,11 @@ size_t simt_conv_dw_workspace(const ConvDims& d);
 ms_status simt_conv_dw(const ConvDims& d, int dt, int layout, int wlayout, const void* x,
                        const void* g, void* dw, void* ws, size_t ws_bytes, cudaStream_t st);
 
+// specialised float32 3x3/1 conv for 8 -> 8 channels, NCHW (smallconv.cu);
+// MS_ERR_UNSUPPORTED when the geometry does not match
+ms_status small_conv_fp32(int pass, const ConvDims& d, int layout, int wlayout, const void* a,
+                          const void* b, void* out, void* ws, size_t ws_bytes, cudaStream_t st);
+
 // reductions / elementwise helpers (misc.cu)
 size_t colsum_workspace(int64_t cols);
 // db[c] = sum_r g[r*ld + c] (row-major [rows][cols]) -> dtype `odt`

@@ -556,18 +556,47 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE>::THREADS, 1)
           float v[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+          const bool full = (nc + 32 <= ncols);
           if (e.bias != nullptr) {
+            // every thread of the tile reads the same 32 bias values: 16-byte
+            // vector loads (L1 broadcast) when the chunk is complete and aligned
+            const uint16_t* b16 = static_cast<const uint16_t*>(e.bias) + nc;
+            if (e.bias_dtype != MS_F32 && full && (reinterpret_cast<uintptr_t>(b16) & 15) == 0) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (nc + j < ncols) v[j] += load_as_float(e.bias, e.bias_dtype, nc + j);
+              for (int q = 0; q < 4; ++q) {
+                const uint4 u = __ldg(reinterpret_cast<const uint4*>(b16) + q);
+                const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                  float lo, hi;
+                  if (e.bias_dtype == MS_BF16) {
+                    lo = __uint_as_float(w4[h] << 16);
+                    hi = __uint_as_float(w4[h] & 0xFFFF0000u);
+                  } else {
+                    lo = __half2float(__ushort_as_half((unsigned short)(w4[h] & 0xFFFF)));
+                    hi = __half2float(__ushort_as_half((unsigned short)(w4[h] >> 16)));
+                  }
+                  v[q * 8 + 2 * h] += lo;
+                  v[q * 8 + 2 * h + 1] += hi;
+                }
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (nc + j < ncols) v[j] += load_as_float(e.bias, e.bias_dtype, nc + j);
+            }
           }
           const int64_t off = orow * e.ldc + col_base + c;
-          const bool full = (nc + 32 <= ncols);
           if (e.atomic) {
             float* o = static_cast<float*>(e.out) + off;
+            if (full && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (full || nc + j < ncols) red_add_f32(o + j, v[j]);
+              for (int j = 0; j < 32; j += 4) red_add_v4_f32(o + j, v[j], v[j + 1], v[j + 2], v[j + 3]);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (full || nc + j < ncols) red_add_f32(o + j, v[j]);
+            }
           } else if (e.out_dtype == MS_F32) {
             float* o = static_cast<float*>(e.out) + off;
             if (full && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {

@@ -342,3 +342,21 @@ def test_maxpool_padded(shape, k, s, p, dt):
     xt = x.detach().float().cpu().requires_grad_(True)
     torch.nn.functional.max_pool2d(xt, k, s, p).backward(g.float().cpu())
     np.testing.assert_allclose(x.grad.float().cpu().numpy(), xt.grad.numpy(), rtol=1e-2, atol=1e-2)
+
+
+@pytest.mark.parametrize("shape", [(2, 8, 40, 70), (1, 8, 16, 64), (3, 8, 33, 17)])
+def test_fig1_fp32_tiled_kernel(shape):
+    # the specialised float32 8->8 3x3/1 kernels (fwd, dX via flipped weights, dW)
+    rng = np.random.default_rng(shape[2])
+    x, xq = _q(rng.standard_normal(shape), "f32")
+    w, wq = _q(rng.standard_normal((8, 8, 3, 3)) / 8, "f32")
+    g, gq = _q(rng.standard_normal(shape), "f32")
+    x.requires_grad_(True)
+    w.requires_grad_(True)
+    s0 = launch_stats()["simt"]
+    y = MF.conv2d(x, w, None, 1, 1)
+    y.backward(g)
+    assert launch_stats()["simt"] - s0 >= 3
+    _close(y, oracle.conv2d_fwd(xq, wq, 1, 1), "f32", "y")
+    _close(x.grad, oracle.conv2d_dx(gq, wq, 1, 1, shape[2], shape[3]), "f32", "dx")
+    _close(w.grad, oracle.conv2d_dw(xq, gq, 1, 1, 3, 3), "f32", "dw")
