@@ -189,14 +189,35 @@ ms_status make_tmap_im2col(CUtensorMap* m, int dt, const void* base, int n, int 
 }
 
 // ------------------------------------------------------------------ dispatch
-template <int BN, int A_MN, int B_MN, int MODE>
+template <int BN, int A_MN, int B_MN, int MODE, int CL = 1>
 static ms_status launch_t(const TmapPack& tm, const GemmArgs& g, cudaStream_t st) {
-  auto kern = umma_gemm_kernel<BN, A_MN, B_MN, MODE>;
+  auto kern = umma_gemm_kernel<BN, A_MN, B_MN, MODE, CL>;
   constexpr int smem = GemmCfg<BN, A_MN, B_MN, MODE>::SMEM_BYTES;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  const int grid = g.num_tiles < num_sms() ? g.num_tiles : num_sms();
+  const int sms = num_sms();
+  int grid = g.num_tiles < sms / CL ? g.num_tiles * CL : (sms / CL) * CL;
   if (grid <= 0) return MS_OK;
-  kern<<<grid, GemmCfg<BN, A_MN, B_MN, MODE>::THREADS, smem, st>>>(tm, g);
+  if constexpr (CL == 1) {
+    kern<<<grid, GemmCfg<BN, A_MN, B_MN, MODE>::THREADS, smem, st>>>(tm, g);
+  } else {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(GemmCfg<BN, A_MN, B_MN, MODE>::THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tm, g);
+    if (e != cudaSuccess) {
+      set_error("cudaLaunchKernelEx (cluster %d): %s", CL, cudaGetErrorString(e));
+      return MS_ERR_LAUNCH;
+    }
+  }
   count_launch(1, KF_UMMA);
   return launch_status("umma_gemm_kernel");
 }
@@ -212,10 +233,26 @@ static ms_status launch_t(const TmapPack& tm, const GemmArgs& g, cudaStream_t st
   }
 
 ms_status launch_umma(int bn, int a_mn, int b_mn, int mode, const TmapPack& tm,
-                      const GemmArgs& g, cudaStream_t st) {
+                      const GemmArgs& g, cudaStream_t st, int g_cluster) {
   if ((b_mn || mode == LOAD_CONV_WGRAD) && bn < 64) {
     set_error("launch_umma: MN-major B needs BN >= 64");
     return MS_ERR_UNSUPPORTED;
+  }
+  if (mode == LOAD_GEMM && g_cluster == 2) {
+    switch (bn) {
+#define MS_CL2(BNV)                                                         \
+  case BNV:                                                                 \
+    if (!a_mn && !b_mn) return launch_t<BNV, 0, 0, LOAD_GEMM, 2>(tm, g, st); \
+    if (!a_mn && b_mn) return launch_t<BNV, 0, 1, LOAD_GEMM, 2>(tm, g, st);  \
+    if (a_mn && b_mn) return launch_t<BNV, 1, 1, LOAD_GEMM, 2>(tm, g, st);   \
+    break;
+      MS_CL2(64)
+      MS_CL2(128)
+      MS_CL2(192)
+      MS_CL2(256)
+#undef MS_CL2
+      default: break;
+    }
   }
   if (mode == LOAD_GEMM) {
     if (!a_mn && !b_mn) { MS_BN_SWITCH(0, 0, LOAD_GEMM) }

@@ -41,8 +41,10 @@ ms_status make_tmap_im2col(CUtensorMap* m, int dt, const void* base, int n, int 
                            uint32_t channels, uint32_t pixels, bool swizzle128 = true);
 
 // Runs umma_gemm_kernel<BN, A_MN, B_MN, MODE> with BN chosen at run time.
+// cluster = 2: plain GEMM with the B tile multicast across a CTA pair (g.m_blocks
+// then counts pairs of M tiles)
 ms_status launch_umma(int bn, int a_mn, int b_mn, int mode, const TmapPack& tm,
-                      const GemmArgs& g, cudaStream_t st);
+                      const GemmArgs& g, cudaStream_t st, int cluster = 1);
 
 // Largest BN in {256,128,64,32} that still yields >= #SMs tiles (or the
 // smallest that covers N when N is tiny).

@@ -2,6 +2,8 @@
 // db = Σ G.  16-bit operands with 16-byte-aligned rows run on the tcgen05
 // kernel (A/B K-major or MN-major straight from the row-major tensors, no
 // transposes); float32 and unaligned shapes run on the SIMT kernel.
+#include <cstdlib>
+
 #include "misc.cuh"
 
 namespace ms {
@@ -13,6 +15,7 @@ bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 struct LinPlan {
   bool tc = false;
+  int cl = 1;   // 2: B tile multicast across a CTA pair on adjacent M tiles
   int bn = 0;
   int splits = 1;
   int kb_per_split = 0;
@@ -41,6 +44,11 @@ LinPlan plan_gemm(int64_t rows, int64_t cols, int64_t red, bool b_mn, bool allow
   p.kb_per_split = (p.k_blocks + p.splits - 1) / p.splits;
   p.splits = (p.k_blocks + p.kb_per_split - 1) / p.kb_per_split;
   if (p.splits > 1) p.ws = align256(sizeof(float) * (size_t)rows * cols);
+  static const int env_cl = [] {
+    const char* e = getenv("MS_GEMM_CLUSTER");
+    return e ? atoi(e) : 2;
+  }();
+  p.cl = (env_cl == 2 && p.m_blocks >= 2 && p.bn >= 64) ? 2 : 1;
   return p;
 }
 
@@ -64,25 +72,25 @@ ms_status run_gemm(const LinPlan& p, int dt, int a_mn, int b_mn, const CUtensorM
   GemmArgs g{};
   g.M = (int)rows;
   g.N = (int)cols;
-  g.m_blocks = p.m_blocks;
+  g.m_blocks = (p.m_blocks + p.cl - 1) / p.cl;  // pairs of M tiles when clustered
   g.n_blocks = p.n_blocks;
   g.k_blocks = p.k_blocks;
   g.splits = p.splits;
   g.kb_per_split = p.kb_per_split;
   g.taps = 1;
-  g.num_tiles = p.m_blocks * p.n_blocks * p.splits;
+  g.num_tiles = g.m_blocks * p.n_blocks * p.splits;
   g.ab_fmt = dt == MS_BF16 ? 1 : 0;
   g.nphases = 1;
   if (p.splits > 1) {
     MS_CHECK_ARG(ws && ws_bytes >= p.ws, MS_ERR_WORKSPACE, "linear: split-K workspace too small");
     cudaMemsetAsync(ws, 0, sizeof(float) * rows * cols, st);
     g.epi = EpiParams{ws, cols, MS_F32, 1, nullptr, 0};
-    MS_TRY(launch_umma(p.bn, a_mn, b_mn, LOAD_GEMM, tm, g, st));
+    MS_TRY(launch_umma(p.bn, a_mn, b_mn, LOAD_GEMM, tm, g, st, p.cl));
     MS_CHECK_ARG(ldc == cols, MS_ERR_UNSUPPORTED, "linear: split-K needs dense output");
     return f32_to(static_cast<const float*>(ws), out, dt, rows * cols, bias, cols, st);
   }
   g.epi = EpiParams{out, ldc, dt, 0, bias, dt};
-  return launch_umma(p.bn, a_mn, b_mn, LOAD_GEMM, tm, g, st);
+  return launch_umma(p.bn, a_mn, b_mn, LOAD_GEMM, tm, g, st, p.cl);
 }
 
 }  // namespace
@@ -106,7 +114,7 @@ extern "C" ms_status ms_linear_fwd(int64_t M, int64_t N, int64_t K, int32_t dt, 
   if (p.tc && al16(x) && al16(w) && al16(y)) {
     CUtensorMap ta, tb;
     MS_TRY(make_tmap_2d(&ta, dt, x, K, M, K, BK, BM));
-    MS_TRY(make_tmap_2d(&tb, dt, w, K, N, K, BK, p.bn));
+    MS_TRY(make_tmap_2d(&tb, dt, w, K, N, K, BK, p.bn / p.cl));  // each CTA loads BN/cl rows
     return run_gemm(p, dt, 0, 0, ta, tb, M, N, y, N, bias, ws, ws_bytes, st);
   }
   // y[m,n] = sum_k x[m,k] w[n,k]

@@ -118,8 +118,8 @@ __device__ __forceinline__ int floor_div(int a, int b) {
   return a >= 0 ? a / b : -((-a + b - 1) / b);
 }
 
-template <int MODE>
-__device__ __forceinline__ TileInfo decode_tile(const GemmArgs& g, int t) {
+template <int MODE, int CL = 1>
+__device__ __forceinline__ TileInfo decode_tile(const GemmArgs& g, int t, int crank = 0) {
   TileInfo ti;
   ti.phase = 0;
   ti.tap = 0;
@@ -150,9 +150,9 @@ __device__ __forceinline__ TileInfo decode_tile(const GemmArgs& g, int t) {
     ti.kb_end = g.k_blocks;
     ti.nsub = g.cv.band_sub;
   } else {
-    const int mb = t % g.m_blocks;
+    const int mb = t % g.m_blocks;  // CL == 2: m_blocks counts pairs of M tiles
     int rest = t / g.m_blocks;
-    ti.m0 = mb * BM;
+    ti.m0 = (CL * mb + crank) * BM;
     ti.nb = rest % g.n_blocks;
     rest /= g.n_blocks;
     if constexpr (MODE == LOAD_CONV_WGRAD) {
@@ -199,7 +199,10 @@ struct GemmCfg {
   static constexpr int THREADS = 64 + 32 * EPI;
 };
 
-template <int BN, int A_MN, int B_MN, int MODE>
+// CL = 2: a cluster of two CTAs on adjacent M tiles of the same N tile; each
+// loads half of the B tile and multicasts it to both, halving B's L2 traffic;
+// a stage is refilled once both CTAs' MMAs have released it.
+template <int BN, int A_MN, int B_MN, int MODE, int CL = 1>
 __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE>::THREADS, 1)
     umma_gemm_kernel(const __grid_constant__ TmapPack tm, const __grid_constant__ GemmArgs g) {
   using Cfg = GemmCfg<BN, A_MN, B_MN, MODE>;
@@ -207,6 +210,10 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE>::THREADS, 1)
   constexpr int KMMA = Cfg::KBYTES / 32;  // tcgen05.mma (K=16) per stage
   static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN");
   static_assert(MODE != LOAD_CONV_DGRAD_BAND || BN == 160, "band dgrad is specialised to BN=160");
+  static_assert(CL == 1 || MODE == LOAD_GEMM, "B multicast is implemented for plain GEMMs");
+  const int crank = CL > 1 ? static_cast<int>(cluster_ctarank()) : 0;
+  const int t_first = static_cast<int>(blockIdx.x) / CL;
+  const int t_step = static_cast<int>(gridDim.x) / CL;
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment for the swizzle atoms
@@ -227,7 +234,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE>::THREADS, 1)
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(smem_u32(&full_bar[i]), 1);
-      mbar_init(smem_u32(&empty_bar[i]), 1);
+      mbar_init(smem_u32(&empty_bar[i]), CL);  // released by the MMA of every CTA that reads it
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(smem_u32(&tfull_bar[i]), 1);
@@ -242,6 +249,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE>::THREADS, 1)
   if (warp == 1) tmem_alloc(smem_u32(tmem_holder), Cfg::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
+  if constexpr (CL > 1) cluster_sync();  // peer barriers initialised before any multicast
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
@@ -250,8 +258,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE>::THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < g.num_tiles; t += gridDim.x) {
-        TileInfo ti = decode_tile<MODE>(g, t);
+      for (int t = t_first; t < g.num_tiles; t += t_step) {
+        TileInfo ti = decode_tile<MODE, CL>(g, t, crank);
         const int n0 = ti.nb * BN;
         // per-tile conv coordinates
         int cn = 0, ch = 0, cw = 0;
@@ -296,7 +304,17 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE>::THREADS, 1)
               } else {
                 tma_load_2d(sA, &tm.a[0], fb, k0, ti.m0);
               }
-              if constexpr (B_MN) {
+              if constexpr (CL > 1) {
+                if constexpr (B_MN) {
+#pragma unroll
+                  for (int j = 0; j < BN / 64; ++j)
+                    if (j % CL == crank)
+                      tma_load_2d_mc(sB + j * 8192, &tm.b, fb, n0 + 64 * j, k0, (1u << CL) - 1);
+                } else {  // rows [crank*BN/2, (crank+1)*BN/2) of the K-major B tile
+                  tma_load_2d_mc(sB + crank * (BN / CL) * 128, &tm.b, fb, k0, n0 + crank * (BN / CL),
+                                 (1u << CL) - 1);
+                }
+              } else if constexpr (B_MN) {
 #pragma unroll
                 for (int j = 0; j < BN / 64; ++j)
                   tma_load_2d(sB + j * 8192, &tm.b, fb, n0 + 64 * j, k0);
@@ -371,8 +389,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE>::THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
-      for (int t = blockIdx.x; t < g.num_tiles; t += gridDim.x) {
-        TileInfo ti = decode_tile<MODE>(g, t);
+      for (int t = t_first; t < g.num_tiles; t += t_step) {
+        TileInfo ti = decode_tile<MODE, CL>(g, t, crank);
         for (int sub = 0; sub < ti.nsub; ++sub, ++local) {
           const int acc = local & 1;
           const uint32_t use = static_cast<uint32_t>(local >> 1);
@@ -407,7 +425,9 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE>::THREADS, 1)
                 bd = make_smem_desc(sB + k * 32, 16, 1024, LAYOUT_SWIZZLE_128B);
               umma_f16(dcol, ad, bd, idesc, (kb > ti.kb_begin || k > 0) ? 1u : 0u);
             }
-            umma_commit(smem_u32(&empty_bar[stage]));  // frees the smem slot when MMAs retire
+            // frees the smem slot (in every CTA whose B half landed here) when MMAs retire
+            if constexpr (CL > 1) umma_commit_mc(smem_u32(&empty_bar[stage]), (1u << CL) - 1);
+            else umma_commit(smem_u32(&empty_bar[stage]));
             if (++stage == STAGES) {
               stage = 0;
               phase ^= 1;
@@ -423,8 +443,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE>::THREADS, 1)
     const int row = quarter * 32 + lane;
     int local = 0;
     const EpiParams& e = g.epi;
-    for (int t = blockIdx.x; t < g.num_tiles; t += gridDim.x) {
-      TileInfo ti = decode_tile<MODE>(g, t);
+    for (int t = t_first; t < g.num_tiles; t += t_step) {
+      TileInfo ti = decode_tile<MODE, CL>(g, t, crank);
       const int n0 = ti.nb * BN;
 
       if constexpr (MODE == LOAD_CONV_DGRAD_BAND) {
@@ -635,6 +655,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE>::THREADS, 1)
   }
 
   __syncthreads();
+  if constexpr (CL > 1) cluster_sync();  // no CTA leaves while its peer may still signal it
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
