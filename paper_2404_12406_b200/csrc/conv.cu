@@ -233,6 +233,7 @@ ms_status fwd_tc(const ms_conv_desc* d, const ConvPlan& p, const void* x, const 
   tm.a[1] = tm.a[2] = tm.a[3] = tm.a[0];
   const int64_t wrow = (int64_t)c.r * c.s * p.cpad;
   MS_TRY(make_tmap_2d(&tm.b, dt, wsrc, wrow, c.k, wrow, BK, bn));
+  MS_TRY(setup_tma_store(tm, g, dt, y, M, c.k, c.k));
   return launch_umma(bn, 0, 0, p.c8 ? LOAD_CONV_FPROP_C8 : LOAD_CONV_FPROP, tm, g, st);
 }
 

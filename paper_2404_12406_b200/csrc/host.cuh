@@ -40,6 +40,11 @@ ms_status make_tmap_im2col(CUtensorMap* m, int dt, const void* base, int n, int 
                            const int lower[2], const int upper[2], int stride_w, int stride_h,
                            uint32_t channels, uint32_t pixels, bool swizzle128 = true);
 
+// Epilogue through TMA stores when the output is 16-bit, 16-byte aligned and
+// densely pitched (sets g.tma_store and tm.c; MS_TMA_STORE=0 disables).
+ms_status setup_tma_store(TmapPack& tm, GemmArgs& g, int dt, void* out, int64_t rows,
+                          int64_t cols, int64_t ldc);
+
 // Runs umma_gemm_kernel<BN, A_MN, B_MN, MODE> with BN chosen at run time.
 // cluster = 2: plain GEMM with the B tile multicast across a CTA pair (g.m_blocks
 // then counts pairs of M tiles)

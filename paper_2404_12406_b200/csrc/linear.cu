@@ -90,6 +90,7 @@ ms_status run_gemm(const LinPlan& p, int dt, int a_mn, int b_mn, const CUtensorM
     return f32_to(static_cast<const float*>(ws), out, dt, rows * cols, bias, cols, st);
   }
   g.epi = EpiParams{out, ldc, dt, 0, bias, dt};
+  MS_TRY(setup_tma_store(tm, g, dt, out, rows, cols, ldc));
   return launch_umma(p.bn, a_mn, b_mn, LOAD_GEMM, tm, g, st, p.cl);
 }
 

@@ -93,6 +93,7 @@ struct GemmArgs {
   int taps;          // WGRAD: R*S
   int num_tiles;
   int ab_fmt;        // 1 = bf16, 0 = fp16
+  int tma_store;     // 1: epilogue stages 32x32 chunks in smem and stores them by TMA
   ConvShape cv;
   int nphases;
   PhaseInfo phase[4];
@@ -102,6 +103,7 @@ struct GemmArgs {
 struct TmapPack {
   CUtensorMap a[4];  // A operand (per dgrad phase; a[0] otherwise)
   CUtensorMap b;     // B operand
+  CUtensorMap c;     // output (GEMM / conv fwd, 16-bit): box {32 cols, 32 rows}, SW64
 };
 
 struct TileInfo {
@@ -191,10 +193,15 @@ struct GemmCfg {
   static constexpr int B_BYTES = BN * KBYTES;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int EXTRA = MODE == LOAD_CONV_DGRAD_BAND ? BAND_WINDOW_BYTES : 0;
-  static constexpr int STAGES_MAX = (200 * 1024 - EXTRA) / STAGE_BYTES;
+  // TMA-store staging: 4 epilogue warps x 2 buffers x (32 rows x 64 B)
+  static constexpr bool CAN_TMA_STORE = MODE == LOAD_GEMM || MODE == LOAD_CONV_FPROP ||
+                                        MODE == LOAD_CONV_FPROP_C8;
+  static constexpr int STG = CAN_TMA_STORE ? EPI_WARPS * 2 * 2048 : 0;
+  static constexpr int STAGES_MAX = (200 * 1024 - EXTRA - STG) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_MAX > 8 ? 8 : STAGES_MAX;
   static constexpr int TMEM_COLS = pow2_cols(2 * BN);
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EXTRA + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int SMEM_BYTES =
+      STAGES * STAGE_BYTES + STG + EXTRA + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr int EPI = MODE == LOAD_CONV_DGRAD_BAND ? BAND_WINDOWS : EPI_WARPS;
   static constexpr int THREADS = 64 + 32 * EPI;
 };
@@ -220,8 +227,10 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE>::THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* ring = smem;
-  float* region = reinterpret_cast<float*>(smem + STAGES * Cfg::STAGE_BYTES);  // band windows
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES + Cfg::EXTRA);
+  uint8_t* staging = smem + STAGES * Cfg::STAGE_BYTES;  // TMA-store chunks (1024-aligned)
+  float* region = reinterpret_cast<float*>(staging + Cfg::STG);  // band windows
+  uint64_t* bars =
+      reinterpret_cast<uint64_t*>(staging + Cfg::STG + Cfg::EXTRA);
   uint64_t* full_bar = bars;
   uint64_t* empty_bar = bars + STAGES;
   uint64_t* tfull_bar = bars + 2 * STAGES;
@@ -442,6 +451,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE>::THREADS, 1)
     const uint32_t quarter = warp & 3;  // TMEM lane quarter this warp may access
     const int row = quarter * 32 + lane;
     int local = 0;
+    uint32_t stg_count = 0;  // TMA-store staging buffer parity
     const EpiParams& e = g.epi;
     for (int t = t_first; t < g.num_tiles; t += t_step) {
       TileInfo ti = decode_tile<MODE, CL>(g, t, crank);
@@ -572,7 +582,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE>::THREADS, 1)
             for (int j = 0; j < 32; ++j) r[j] = 0u;
           }
           const int nc = n0 + c;  // first column of this chunk in GEMM-N space
-          if (!valid || nc >= ncols) continue;
+          const bool tma_st = Cfg::CAN_TMA_STORE && g.tma_store;
+          if (nc >= ncols || (!valid && !tma_st)) continue;
           float v[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
@@ -604,6 +615,37 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE>::THREADS, 1)
 #pragma unroll
               for (int j = 0; j < 32; ++j)
                 if (nc + j < ncols) v[j] += load_as_float(e.bias, e.bias_dtype, nc + j);
+            }
+          }
+          if constexpr (Cfg::CAN_TMA_STORE) {
+            if (tma_st) {
+              // pack, stage this warp's 32 rows x 32 columns (64-byte rows, 64B swizzle),
+              // and let one lane store the chunk with TMA (clips the M / N tails)
+              uint32_t p[16];
+              if (e.out_dtype == MS_BF16) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) p[j] = pack2<__nv_bfloat16>(v[2 * j], v[2 * j + 1]);
+              } else {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) p[j] = pack2<__half>(v[2 * j], v[2 * j + 1]);
+              }
+              const int ew = static_cast<int>(warp) - 2;
+              uint8_t* stg = staging + (ew * 2 + (stg_count & 1)) * 2048;
+              if (lane == 0) bulk_wait_read<1>();  // the store issued 2 chunks ago has read it
+              __syncwarp();
+              const int rr = static_cast<int>(lane);
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                *reinterpret_cast<uint4*>(stg + rr * 64 + ((q ^ ((rr >> 1) & 3)) << 4)) =
+                    make_uint4(p[4 * q], p[4 * q + 1], p[4 * q + 2], p[4 * q + 3]);
+              fence_proxy_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                tma_store_2d(&tm.c, smem_u32(stg), nc, ti.m0 + static_cast<int>(quarter) * 32);
+                bulk_commit();
+              }
+              ++stg_count;
+              continue;
             }
           }
           const int64_t off = orow * e.ldc + col_base + c;
@@ -654,6 +696,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE>::THREADS, 1)
     }
   }
 
+  if constexpr (Cfg::CAN_TMA_STORE)
+    if (warp >= 2 && lane == 0) bulk_wait_all();  // TMA stores complete before exit
   __syncthreads();
   if constexpr (CL > 1) cluster_sync();  // no CTA leaves while its peer may still signal it
   if (warp == 1) {
