@@ -211,17 +211,16 @@ ms_status setup_tma_store(TmapPack& tm, GemmArgs& g, int dt, void* out, int64_t 
 template <int BN, int A_MN, int B_MN, int MODE, int CL = 1>
 static ms_status launch_t(const TmapPack& tm, const GemmArgs& g, cudaStream_t st) {
   auto kern = umma_gemm_kernel<BN, A_MN, B_MN, MODE, CL>;
-  constexpr int smem = GemmCfg<BN, A_MN, B_MN, MODE>::SMEM_BYTES;
+  constexpr int smem = GemmCfg<BN, A_MN, B_MN, MODE, CL>::SMEM_BYTES;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int sms = num_sms();
-  int grid = g.num_tiles < sms / CL ? g.num_tiles * CL : (sms / CL) * CL;
-  if (grid <= 0) return MS_OK;
+  if (g.num_tiles <= 0) return MS_OK;
   if constexpr (CL == 1) {
-    kern<<<grid, GemmCfg<BN, A_MN, B_MN, MODE>::THREADS, smem, st>>>(tm, g);
+    const int grid = g.num_tiles < sms ? g.num_tiles : sms;
+    kern<<<grid, GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, smem, st>>>(tm, g);
   } else {
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(GemmCfg<BN, A_MN, B_MN, MODE>::THREADS);
+    cfg.blockDim = dim3(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -231,6 +230,20 @@ static ms_status launch_t(const TmapPack& tm, const GemmArgs& g, cudaStream_t st
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    // persistent grid = the clusters that can be co-resident (GPCs with an odd
+    // SM count leave one SM out of the pairs), not #SMs / 2
+    static int max_clusters = 0;
+    if (max_clusters == 0) {
+      cfg.gridDim = dim3(sms / CL * CL);
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) {
+        cudaGetLastError();
+        n = sms / CL;
+      }
+      max_clusters = n;
+    }
+    const int clusters = g.num_tiles < max_clusters ? g.num_tiles : max_clusters;
+    cfg.gridDim = dim3(clusters * CL);
     const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tm, g);
     if (e != cudaSuccess) {
       set_error("cudaLaunchKernelEx (cluster %d): %s", CL, cudaGetErrorString(e));
@@ -265,9 +278,7 @@ ms_status launch_umma(int bn, int a_mn, int b_mn, int mode, const TmapPack& tm,
     if (!a_mn && b_mn) return launch_t<BNV, 0, 1, LOAD_GEMM, 2>(tm, g, st);  \
     if (a_mn && b_mn) return launch_t<BNV, 1, 1, LOAD_GEMM, 2>(tm, g, st);   \
     break;
-      MS_CL2(64)
       MS_CL2(128)
-      MS_CL2(192)
       MS_CL2(256)
 #undef MS_CL2
       default: break;

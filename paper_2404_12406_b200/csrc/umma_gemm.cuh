@@ -134,7 +134,7 @@ __device__ __forceinline__ TileInfo decode_tile(const GemmArgs& g, int t, int cr
     const PhaseInfo& P = g.phase[p];
     const int lt = t - P.tile_begin;
     ti.phase = p;
-    ti.m0 = (lt % P.m_blocks) * BM;
+    ti.m0 = (CL * (lt % P.m_blocks) + crank) * BM;  // CL == 2: m_blocks counts pairs
     ti.nb = lt / P.m_blocks;
     ti.kb_begin = 0;
     ti.kb_end = P.nr * P.ns * g.cv.cblocks;
@@ -186,18 +186,19 @@ constexpr int pow2_cols(int c) {
   return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512;
 }
 
-template <int BN, int A_MN, int B_MN, int MODE>
+template <int BN, int A_MN, int B_MN, int MODE, int CL = 1>
 struct GemmCfg {
   static constexpr int KBYTES = MODE == LOAD_CONV_FPROP_ROWSEG ? 64 : 128;  // K bytes per row
   static constexpr int A_BYTES = BM * KBYTES;
-  static constexpr int B_BYTES = BN * KBYTES;
+  static constexpr int B_BYTES = BN / CL * KBYTES;  // this CTA's share of the B tile
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int EXTRA = MODE == LOAD_CONV_DGRAD_BAND ? BAND_WINDOW_BYTES : 0;
   // TMA-store staging: 4 epilogue warps x 2 buffers x (32 rows x 64 B)
   static constexpr bool CAN_TMA_STORE = MODE == LOAD_GEMM || MODE == LOAD_CONV_FPROP ||
                                         MODE == LOAD_CONV_FPROP_C8;
   static constexpr int STG = CAN_TMA_STORE ? EPI_WARPS * 2 * 2048 : 0;
-  static constexpr int STAGES_MAX = (200 * 1024 - EXTRA - STG) / STAGE_BYTES;
+  static constexpr int SMEM_MAX = 227 * 1024;
+  static constexpr int STAGES_MAX = (SMEM_MAX - 1280 - EXTRA - STG) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_MAX > 8 ? 8 : STAGES_MAX;
   static constexpr int TMEM_COLS = pow2_cols(2 * BN);
   static constexpr int SMEM_BYTES =
@@ -206,18 +207,26 @@ struct GemmCfg {
   static constexpr int THREADS = 64 + 32 * EPI;
 };
 
-// CL = 2: a cluster of two CTAs on adjacent M tiles of the same N tile; each
-// loads half of the B tile and multicasts it to both, halving B's L2 traffic;
-// a stage is refilled once both CTAs' MMAs have released it.
+// CL = 2: a CTA pair (cluster of 2 on one TPC) computes a 256 x BN tile with
+// tcgen05.mma.cta_group::2 (M = 256).  Each CTA TMA-loads its own 128 rows of A
+// and half of the B tile into its smem, signalling the even CTA's full barrier;
+// the even CTA alone issues the MMAs, whose commits arrive on both CTAs' empty /
+// accumulator-full barriers.  Each CTA's epilogue drains its own TMEM lanes and
+// releases the accumulator on the even CTA's barrier.  Per SM this halves the B
+// bytes staged through shared memory per FLOP (the 1-CTA 128x256 tile is smem-
+// bandwidth bound at ~2/3 of tensor peak).
 template <int BN, int A_MN, int B_MN, int MODE, int CL = 1>
-__global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE>::THREADS, 1)
+__global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
     umma_gemm_kernel(const __grid_constant__ TmapPack tm, const __grid_constant__ GemmArgs g) {
-  using Cfg = GemmCfg<BN, A_MN, B_MN, MODE>;
+  using Cfg = GemmCfg<BN, A_MN, B_MN, MODE, CL>;
   constexpr int STAGES = Cfg::STAGES;
   constexpr int KMMA = Cfg::KBYTES / 32;  // tcgen05.mma (K=16) per stage
   static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN");
   static_assert(MODE != LOAD_CONV_DGRAD_BAND || BN == 160, "band dgrad is specialised to BN=160");
-  static_assert(CL == 1 || MODE == LOAD_GEMM, "B multicast is implemented for plain GEMMs");
+  static_assert(CL == 1 || MODE == LOAD_GEMM || MODE == LOAD_CONV_FPROP ||
+                    MODE == LOAD_CONV_DGRAD,
+                "CTA pairs are implemented for GEMM and im2col conv fprop / dgrad");
+  static_assert(CL == 1 || (BN / CL) % 16 == 0, "pair: B half must be a multiple of 16 rows");
   const int crank = CL > 1 ? static_cast<int>(cluster_ctarank()) : 0;
   const int t_first = static_cast<int>(blockIdx.x) / CL;
   const int t_step = static_cast<int>(gridDim.x) / CL;
@@ -243,11 +252,12 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE>::THREADS, 1)
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(smem_u32(&full_bar[i]), 1);
-      mbar_init(smem_u32(&empty_bar[i]), CL);  // released by the MMA of every CTA that reads it
+      mbar_init(smem_u32(&empty_bar[i]), 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(smem_u32(&tfull_bar[i]), 1);
-      mbar_init(smem_u32(&tempty_bar[i]), Cfg::EPI * 32);
+      // CL = 2: one arrival per epilogue warp of both CTAs (on the even CTA's barrier)
+      mbar_init(smem_u32(&tempty_bar[i]), CL == 1 ? Cfg::EPI * 32 : CL * Cfg::EPI);
     }
     fence_mbar_init();
     tma_prefetch_desc(&tm.b);
@@ -255,10 +265,13 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE>::THREADS, 1)
   }
   if constexpr (MODE == LOAD_CONV_DGRAD_BAND)
     for (int i = threadIdx.x; i < BAND_WINDOW_BYTES / 4; i += blockDim.x) region[i] = 0.f;
-  if (warp == 1) tmem_alloc(smem_u32(tmem_holder), Cfg::TMEM_COLS);
+  if (warp == 1) {
+    if constexpr (CL == 1) tmem_alloc(smem_u32(tmem_holder), Cfg::TMEM_COLS);
+    else tmem_alloc_cg2(smem_u32(tmem_holder), Cfg::TMEM_COLS);
+  }
   tc_fence_before();
   __syncthreads();
-  if constexpr (CL > 1) cluster_sync();  // peer barriers initialised before any multicast
+  if constexpr (CL > 1) cluster_sync();  // peer barriers initialised before any remote signal
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
@@ -301,28 +314,39 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE>::THREADS, 1)
         for (int sub = 0; sub < ti.nsub; ++sub) {
           for (int kb = ti.kb_begin; kb < ti.kb_end; ++kb) {
             mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
-            const uint32_t fb = smem_u32(&full_bar[stage]);
+            // CL = 2: both CTAs' loads complete on the even CTA's full barrier
+            const uint32_t fb = CL == 1 ? smem_u32(&full_bar[stage])
+                                        : mapa_shared(smem_u32(&full_bar[stage]), 0);
             const uint32_t sA = smem_u32(ring + stage * Cfg::STAGE_BYTES);
             const uint32_t sB = sA + Cfg::A_BYTES;
-            mbar_arrive_expect_tx(fb, Cfg::STAGE_BYTES);
+            if (crank == 0)
+              mbar_arrive_expect_tx(smem_u32(&full_bar[stage]), CL * Cfg::STAGE_BYTES);
             if constexpr (MODE == LOAD_GEMM) {
               const int k0 = kb * BK;
-              if constexpr (A_MN) {
-                tma_load_2d(sA, &tm.a[0], fb, ti.m0, k0);
-                tma_load_2d(sA + 8192, &tm.a[0], fb, ti.m0 + 64, k0);
-              } else {
-                tma_load_2d(sA, &tm.a[0], fb, k0, ti.m0);
-              }
               if constexpr (CL > 1) {
+                if constexpr (A_MN) {
+                  tma_load_2d_cg2(sA, &tm.a[0], fb, ti.m0, k0);
+                  tma_load_2d_cg2(sA + 8192, &tm.a[0], fb, ti.m0 + 64, k0);
+                } else {
+                  tma_load_2d_cg2(sA, &tm.a[0], fb, k0, ti.m0);
+                }
+                const int nh = n0 + crank * (BN / CL);  // this CTA's half of the B tile
                 if constexpr (B_MN) {
 #pragma unroll
-                  for (int j = 0; j < BN / 64; ++j)
-                    if (j % CL == crank)
-                      tma_load_2d_mc(sB + j * 8192, &tm.b, fb, n0 + 64 * j, k0, (1u << CL) - 1);
-                } else {  // rows [crank*BN/2, (crank+1)*BN/2) of the K-major B tile
-                  tma_load_2d_mc(sB + crank * (BN / CL) * 128, &tm.b, fb, k0, n0 + crank * (BN / CL),
-                                 (1u << CL) - 1);
+                  for (int j = 0; j < BN / CL / 64; ++j)
+                    tma_load_2d_cg2(sB + j * 8192, &tm.b, fb, nh + 64 * j, k0);
+                } else {
+                  tma_load_2d_cg2(sB, &tm.b, fb, k0, nh);
                 }
+              } else {
+                if constexpr (A_MN) {
+                  tma_load_2d(sA, &tm.a[0], fb, ti.m0, k0);
+                  tma_load_2d(sA + 8192, &tm.a[0], fb, ti.m0 + 64, k0);
+                } else {
+                  tma_load_2d(sA, &tm.a[0], fb, k0, ti.m0);
+                }
+              }
+              if constexpr (CL > 1) {
               } else if constexpr (B_MN) {
 #pragma unroll
                 for (int j = 0; j < BN / 64; ++j)
@@ -334,8 +358,14 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE>::THREADS, 1)
               const int tap = kb / g.cv.cblocks;
               const int cb = kb - tap * g.cv.cblocks;
               const int r = tap / g.cv.S, s = tap - (tap / g.cv.S) * g.cv.S;
-              tma_load_im2col_4d(sA, amap, fb, cb * 64, cw, ch, cn, (uint16_t)s, (uint16_t)r);
-              tma_load_2d(sB, &tm.b, fb, tap * g.cv.wrow_cpad + cb * 64, n0);
+              if constexpr (CL > 1) {
+                tma_load_im2col_4d_cg2(sA, amap, fb, cb * 64, cw, ch, cn, (uint16_t)s, (uint16_t)r);
+                tma_load_2d_cg2(sB, &tm.b, fb, tap * g.cv.wrow_cpad + cb * 64,
+                                n0 + crank * (BN / CL));
+              } else {
+                tma_load_im2col_4d(sA, amap, fb, cb * 64, cw, ch, cn, (uint16_t)s, (uint16_t)r);
+                tma_load_2d(sB, &tm.b, fb, tap * g.cv.wrow_cpad + cb * 64, n0);
+              }
             } else if constexpr (MODE == LOAD_CONV_FPROP_C8) {
               // 8 taps x 8 channels; each tap is one 128-pixel x 16-byte im2col box
               const int taps = g.cv.R * g.cv.S;
@@ -365,9 +395,16 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE>::THREADS, 1)
               const int tt = kb / g.cv.cblocks;
               const int ts = tt % P.ns, tr = tt / P.ns;
               const int r = P.r0 + g.cv.sh * tr, s = P.s0 + g.cv.sw * ts;
-              tma_load_im2col_4d(sA, amap, fb, cb * 64, cw, ch, cn, (uint16_t)(P.ns - 1 - ts),
-                                 (uint16_t)(P.nr - 1 - tr));
-              tma_load_2d(sB, &tm.b, fb, (r * g.cv.S + s) * g.cv.wrow_cpad + cb * 64, n0);
+              if constexpr (CL > 1) {
+                tma_load_im2col_4d_cg2(sA, amap, fb, cb * 64, cw, ch, cn,
+                                       (uint16_t)(P.ns - 1 - ts), (uint16_t)(P.nr - 1 - tr));
+                tma_load_2d_cg2(sB, &tm.b, fb, (r * g.cv.S + s) * g.cv.wrow_cpad + cb * 64,
+                                n0 + crank * (BN / CL));
+              } else {
+                tma_load_im2col_4d(sA, amap, fb, cb * 64, cw, ch, cn, (uint16_t)(P.ns - 1 - ts),
+                                   (uint16_t)(P.nr - 1 - tr));
+                tma_load_2d(sB, &tm.b, fb, (r * g.cv.S + s) * g.cv.wrow_cpad + cb * 64, n0);
+              }
             } else {  // LOAD_CONV_WGRAD: K = output pixels
               const int p0 = kb * BK;
               const int pq = g.cv.P * g.cv.Q;
@@ -393,8 +430,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE>::THREADS, 1)
     }
   } else if (warp == 1) {
     // ============================ MMA issuer ============================
-    if (lane == 0) {
-      const uint32_t idesc = make_idesc_f16(g.ab_fmt, BM, BN, A_MN, B_MN);
+    if (lane == 0 && crank == 0) {
+      const uint32_t idesc = make_idesc_f16(g.ab_fmt, BM * CL, BN, A_MN, B_MN);
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
@@ -403,11 +440,18 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE>::THREADS, 1)
         for (int sub = 0; sub < ti.nsub; ++sub, ++local) {
           const int acc = local & 1;
           const uint32_t use = static_cast<uint32_t>(local >> 1);
-          mbar_wait(smem_u32(&tempty_bar[acc]), (use & 1) ^ 1);
+          if constexpr (CL == 1) mbar_wait(smem_u32(&tempty_bar[acc]), (use & 1) ^ 1);
+          else mbar_wait_cluster(smem_u32(&tempty_bar[acc]), (use & 1) ^ 1);
           tc_fence_after();
           const uint32_t dcol = tmem_base + acc * BN;
           if (ti.kb_end <= ti.kb_begin) {
-            mbar_arrive(smem_u32(&tfull_bar[acc]));  // empty reduction: epilogue writes zeros
+            // empty reduction: the epilogue writes zeros
+            if constexpr (CL == 1) {
+              mbar_arrive(smem_u32(&tfull_bar[acc]));
+            } else {
+              for (int c = 0; c < CL; ++c)
+                mbar_arrive_cluster(mapa_shared(smem_u32(&tfull_bar[acc]), c));
+            }
             continue;
           }
           for (int kb = ti.kb_begin; kb < ti.kb_end; ++kb) {
@@ -432,17 +476,21 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE>::THREADS, 1)
                 bd = make_smem_desc(sB + k * 2048, 8192, 1024, LAYOUT_SWIZZLE_128B);
               else
                 bd = make_smem_desc(sB + k * 32, 16, 1024, LAYOUT_SWIZZLE_128B);
-              umma_f16(dcol, ad, bd, idesc, (kb > ti.kb_begin || k > 0) ? 1u : 0u);
+              const uint32_t accum = (kb > ti.kb_begin || k > 0) ? 1u : 0u;
+              if constexpr (CL == 1) umma_f16(dcol, ad, bd, idesc, accum);
+              else umma_f16_cg2(dcol, ad, bd, idesc, accum);
             }
-            // frees the smem slot (in every CTA whose B half landed here) when MMAs retire
-            if constexpr (CL > 1) umma_commit_mc(smem_u32(&empty_bar[stage]), (1u << CL) - 1);
+            // frees the smem slot (in both CTAs of a pair) when the MMAs retire
+            if constexpr (CL > 1) umma_commit_cg2_mc(smem_u32(&empty_bar[stage]), (1u << CL) - 1);
             else umma_commit(smem_u32(&empty_bar[stage]));
             if (++stage == STAGES) {
               stage = 0;
               phase ^= 1;
             }
           }
-          umma_commit(smem_u32(&tfull_bar[acc]));  // accumulator ready for the epilogue
+          // accumulator ready for the epilogue (of both CTAs of a pair)
+          if constexpr (CL > 1) umma_commit_cg2_mc(smem_u32(&tfull_bar[acc]), (1u << CL) - 1);
+          else umma_commit(smem_u32(&tfull_bar[acc]));
         }
       }
     }
@@ -691,7 +739,12 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE>::THREADS, 1)
           }
         }
         tc_fence_before();
-        mbar_arrive(smem_u32(&tempty_bar[acc]));
+        if constexpr (CL == 1) {
+          mbar_arrive(smem_u32(&tempty_bar[acc]));
+        } else {  // one arrival per warp on the even CTA's barrier
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty_bar[acc]), 0));
+        }
       }
     }
   }
@@ -702,7 +755,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE>::THREADS, 1)
   if constexpr (CL > 1) cluster_sync();  // no CTA leaves while its peer may still signal it
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+    if constexpr (CL == 1) tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+    else tmem_dealloc_cg2(tmem_base, Cfg::TMEM_COLS);
   }
 }
 

@@ -175,6 +175,8 @@ LIN_CASES = [
     ((2, 70), 256, 64),       # M tail
     ((8,), 4096, 256),        # tiny M, long K (split-K)
     ((513,), 64, 8),          # N = 8
+    ((2, 1024), 1024, 1536),  # CTA-pair tiles (M=256 MMA), several tiles per CTA
+    ((1, 640), 384, 320),     # pair with a partial second M tile, N tail of a BN=64 pair
 ]
 
 
