@@ -218,8 +218,10 @@ ms_status fwd_tc(const ms_conv_desc* d, const ConvPlan& p, const void* x, const 
   GemmArgs g = base_args(dt);
   g.M = (int)M;
   g.N = c.k;
-  g.m_blocks = (int)((M + BM - 1) / BM);
-  const int bn = pick_bn(g.m_blocks, c.k);
+  const int m_tiles = (int)((M + BM - 1) / BM);
+  const TilePick tp = pick_tiles(m_tiles, c.k, !p.c8, false);
+  const int bn = tp.bn;
+  g.m_blocks = (m_tiles + tp.cl - 1) / tp.cl;  // pairs of M tiles when clustered
   g.n_blocks = (c.k + bn - 1) / bn;
   g.num_tiles = g.m_blocks * g.n_blocks;
   g.k_blocks = (c.r * c.s + 7) / 8;  // C8 variant: 8 taps per k-block
@@ -232,9 +234,9 @@ ms_status fwd_tc(const ms_conv_desc* d, const ConvPlan& p, const void* x, const 
                           p.c8 ? 8 : 64, BM, !p.c8));
   tm.a[1] = tm.a[2] = tm.a[3] = tm.a[0];
   const int64_t wrow = (int64_t)c.r * c.s * p.cpad;
-  MS_TRY(make_tmap_2d(&tm.b, dt, wsrc, wrow, c.k, wrow, BK, bn));
+  MS_TRY(make_tmap_2d(&tm.b, dt, wsrc, wrow, c.k, wrow, BK, bn / tp.cl));
   MS_TRY(setup_tma_store(tm, g, dt, y, M, c.k, c.k));
-  return launch_umma(bn, 0, 0, p.c8 ? LOAD_CONV_FPROP_C8 : LOAD_CONV_FPROP, tm, g, st);
+  return launch_umma(bn, 0, 0, p.c8 ? LOAD_CONV_FPROP_C8 : LOAD_CONV_FPROP, tm, g, st, tp.cl);
 }
 
 // ----------------------------------------------------------------- input-VJP
@@ -279,7 +281,8 @@ ms_status dx_tc(const ms_conv_desc* d, const ConvPlan& p, const void* dy, const 
   MS_TRY(repack_dgrad(dt, c.k, c.c, c.r, c.s, p.kpad, d->wlayout, w, wd, st));
   GemmArgs g = base_args(dt);
   g.N = c.c;
-  const int bn = pick_bn((int64_t)c.n * c.h * c.w / BM + 1, c.c);
+  const TilePick tp = pick_tiles((int64_t)c.n * c.h * c.w / BM + 1, c.c, true, false);
+  const int bn = tp.bn;
   g.n_blocks = (c.c + bn - 1) / bn;
   g.cv = shape_of(c, c.k, c.oh, c.ow, p.kpad / 64, p.kpad, c.h, c.w);
   TmapPack tm;
@@ -301,7 +304,7 @@ ms_status dx_tc(const ms_conv_desc* d, const ConvPlan& p, const void* dy, const 
       P.Lh = P.nr > 0 ? dh0 - (P.nr - 1) : 0;
       P.Lw = P.ns > 0 ? dw0 - (P.ns - 1) : 0;
       P.m_total = c.n * P.Hp * P.Wp;
-      P.m_blocks = (P.m_total + BM - 1) / BM;
+      P.m_blocks = ((P.m_total + BM - 1) / BM + tp.cl - 1) / tp.cl;  // pairs when clustered
       P.tile_begin = tiles;
       tiles += P.m_blocks * g.n_blocks;
       if (P.nr > 0 && P.ns > 0) {
@@ -324,8 +327,8 @@ ms_status dx_tc(const ms_conv_desc* d, const ConvPlan& p, const void* dy, const 
   g.num_tiles = tiles;
   g.epi = EpiParams{dx, c.c, dt, 0, nullptr, dt};
   const int64_t wrow = (int64_t)c.r * c.s * p.kpad;
-  MS_TRY(make_tmap_2d(&tm.b, dt, wd, wrow, c.c, wrow, BK, bn));
-  return launch_umma(bn, 0, 0, LOAD_CONV_DGRAD, tm, g, st);
+  MS_TRY(make_tmap_2d(&tm.b, dt, wd, wrow, c.c, wrow, BK, bn / tp.cl));
+  return launch_umma(bn, 0, 0, LOAD_CONV_DGRAD, tm, g, st, tp.cl);
 }
 
 // ----------------------------------------------------------------- weight-VJP

@@ -270,19 +270,23 @@ ms_status launch_umma(int bn, int a_mn, int b_mn, int mode, const TmapPack& tm,
     set_error("launch_umma: MN-major B needs BN >= 64");
     return MS_ERR_UNSUPPORTED;
   }
-  if (mode == LOAD_GEMM && g_cluster == 2) {
+  if (g_cluster == 2) {
     switch (bn) {
-#define MS_CL2(BNV)                                                         \
-  case BNV:                                                                 \
-    if (!a_mn && !b_mn) return launch_t<BNV, 0, 0, LOAD_GEMM, 2>(tm, g, st); \
-    if (!a_mn && b_mn) return launch_t<BNV, 0, 1, LOAD_GEMM, 2>(tm, g, st);  \
-    if (a_mn && b_mn) return launch_t<BNV, 1, 1, LOAD_GEMM, 2>(tm, g, st);   \
+#define MS_CL2(BNV)                                                                       \
+  case BNV:                                                                               \
+    if (mode == LOAD_GEMM && !a_mn && !b_mn) return launch_t<BNV, 0, 0, LOAD_GEMM, 2>(tm, g, st); \
+    if (mode == LOAD_GEMM && !a_mn && b_mn) return launch_t<BNV, 0, 1, LOAD_GEMM, 2>(tm, g, st);  \
+    if (mode == LOAD_GEMM && a_mn && b_mn) return launch_t<BNV, 1, 1, LOAD_GEMM, 2>(tm, g, st);   \
+    if (mode == LOAD_CONV_FPROP) return launch_t<BNV, 0, 0, LOAD_CONV_FPROP, 2>(tm, g, st);       \
+    if (mode == LOAD_CONV_DGRAD) return launch_t<BNV, 0, 0, LOAD_CONV_DGRAD, 2>(tm, g, st);       \
     break;
       MS_CL2(128)
       MS_CL2(256)
 #undef MS_CL2
       default: break;
     }
+    set_error("launch_umma: no CTA-pair variant (bn=%d mode=%d)", bn, mode);
+    return MS_ERR_UNSUPPORTED;
   }
   if (mode == LOAD_GEMM) {
     if (!a_mn && !b_mn) { MS_BN_SWITCH(0, 0, LOAD_GEMM) }
@@ -331,6 +335,47 @@ int pick_bn(int64_t other_tiles, int64_t ncols) {
     }
   }
   return best;
+}
+
+TilePick pick_tiles(int64_t m_blocks, int64_t cols, bool allow_pair, bool b_mn) {
+  static const int env_cl = [] {
+    const char* e = getenv("MS_GEMM_CLUSTER");
+    return e ? atoi(e) : 2;
+  }();
+  static const int env_bn = [] {
+    const char* e = getenv("MS_GEMM_BN");
+    return e ? atoi(e) : 0;
+  }();
+  // A persistent launch costs about ceil(tiles / slots) tile-times; a tile-time
+  // ~ (BN + 64) column-units (the constant is the per-tile epilogue / pipeline
+  // overhead), and a pair tile is ~0.7x a single tile per SM (half the B bytes
+  // staged through shared memory).  The pair splits B in halves of BN/2 rows,
+  // which the hardware accepts for BN in {128, 256} (96- and 32-row halves hang
+  // the MMA), so those are the only pair widths.
+  static const TilePick cands[] = {{2, 256}, {2, 128}, {1, 256}, {1, 192},
+                                   {1, 128}, {1, 64},  {1, 32}};
+  const int sms = num_sms();
+  double best = 1e30;
+  TilePick pick{1, 0};
+  for (const TilePick& c : cands) {
+    if (c.cl == 2 && (!allow_pair || env_cl != 2 || m_blocks < 2)) continue;
+    if (env_bn && c.bn != env_bn) continue;
+    if (b_mn && c.bn < 64) continue;
+    if (c.bn > 128 && cols <= 128) continue;
+    if (c.bn > 64 && cols <= 32) continue;
+    if (c.bn > 32 && cols <= 16) continue;
+    const int64_t mt = (m_blocks + c.cl - 1) / c.cl;
+    const int64_t tiles = mt * ((cols + c.bn - 1) / c.bn);
+    const int64_t slots = sms / c.cl;
+    const int64_t waves = (tiles + slots - 1) / slots;
+    const double cost = (double)waves * (c.bn + 64) * (c.cl == 2 ? 0.7 : 1.0);
+    if (cost < best * 0.97) {  // candidates are ordered large-first: prefer them on near-ties
+      best = cost;
+      pick = c;
+    }
+  }
+  if (pick.bn == 0) pick = TilePick{1, env_bn ? env_bn : (b_mn ? 64 : 32)};
+  return pick;
 }
 
 }  // namespace ms

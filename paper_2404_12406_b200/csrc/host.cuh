@@ -45,14 +45,22 @@ ms_status make_tmap_im2col(CUtensorMap* m, int dt, const void* base, int n, int 
 ms_status setup_tma_store(TmapPack& tm, GemmArgs& g, int dt, void* out, int64_t rows,
                           int64_t cols, int64_t ldc);
 
-// Runs umma_gemm_kernel<BN, A_MN, B_MN, MODE> with BN chosen at run time.
-// cluster = 2: plain GEMM with the B tile multicast across a CTA pair (g.m_blocks
-// then counts pairs of M tiles)
+// Runs umma_gemm_kernel<BN, A_MN, B_MN, MODE, cluster> with BN chosen at run
+// time.  cluster = 2: CTA-pair tiles (tcgen05 cta_group::2, 256 x BN; g.m_blocks
+// / PhaseInfo::m_blocks then count pairs of 128-row M tiles).
 ms_status launch_umma(int bn, int a_mn, int b_mn, int mode, const TmapPack& tm,
                       const GemmArgs& g, cudaStream_t st, int cluster = 1);
 
-// Largest BN in {256,128,64,32} that still yields >= #SMs tiles (or the
-// smallest that covers N when N is tiny).
+// Single-CTA BN for `m_tiles_times_other` 128-row tiles over `ncols` columns.
 int pick_bn(int64_t m_tiles_times_other, int64_t ncols);
+
+// Tile shape for a persistent launch over m_blocks 128-row tiles x ncols:
+// single-CTA 128 x BN (BN in 32..256) or CTA-pair 256 x BN (BN in {128, 256})
+// by a wave-quantisation cost model.  MS_GEMM_CLUSTER=1 / MS_GEMM_BN=<n>
+// override it (tuning and debugging).
+struct TilePick {
+  int cl, bn;
+};
+TilePick pick_tiles(int64_t m_blocks, int64_t ncols, bool allow_pair, bool mn_major_b);
 
 }  // namespace ms

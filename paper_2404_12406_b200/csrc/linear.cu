@@ -24,47 +24,16 @@ struct LinPlan {
 };
 
 // rows x cols output, contraction red; b_mn: B operand MN-major (BN >= 64).
-// Tile choice: single-CTA 128 x BN tiles (BN in 64..256) or CTA-pair 256 x BN
-// tiles (BN in {128, 256}: the pair splits B in halves of BN/2 rows, which the
-// hardware accepts for 64 and 128 here).  A persistent launch costs about
-// ceil(tiles / slots) tile-times; a tile-time ~ (BN + 64) column-units, and a
-// pair tile is ~0.7x a single tile per SM (half the B bytes through smem).
+// Tile shape from pick_tiles (single-CTA or CTA-pair); split-K when the output
+// tiles cannot fill the GPU.
 LinPlan plan_gemm(int64_t rows, int64_t cols, int64_t red, bool b_mn, bool allow_split) {
   LinPlan p;
   p.tc = true;
   p.m_blocks = (int)((rows + BM - 1) / BM);
-  static const int env_cl = [] {
-    const char* e = getenv("MS_GEMM_CLUSTER");  // 1: single-CTA tiles only
-    return e ? atoi(e) : 2;
-  }();
-  static const int env_bn = [] {
-    const char* e = getenv("MS_GEMM_BN");  // tuning / debugging override
-    return e ? atoi(e) : 0;
-  }();
   const int sms = num_sms();
-  double best = 1e30;
-  p.bn = 0;
-  p.cl = 1;
-  struct Cand { int cl, bn; };
-  static const Cand cands[] = {{2, 256}, {2, 128}, {1, 256}, {1, 192}, {1, 128}, {1, 64}, {1, 32}};
-  for (const Cand& c : cands) {
-    if (c.cl == 2 && (env_cl != 2 || p.m_blocks < 2)) continue;
-    if (env_bn && c.bn != env_bn) continue;
-    if (b_mn && c.bn < 64) continue;
-    if (c.bn > 128 && cols <= 128) continue;
-    if (c.bn > 64 && cols <= 32) continue;
-    const int64_t mt = (p.m_blocks + c.cl - 1) / c.cl;
-    const int64_t tiles = mt * ((cols + c.bn - 1) / c.bn);
-    const int64_t slots = sms / c.cl;
-    const int64_t waves = (tiles + slots - 1) / slots;
-    const double cost = (double)waves * (c.bn + 64) * (c.cl == 2 ? 0.7 : 1.0);
-    if (cost < best * 0.97) {  // candidates are ordered large-first: prefer them on near-ties
-      best = cost;
-      p.bn = c.bn;
-      p.cl = c.cl;
-    }
-  }
-  if (p.bn == 0) p.bn = env_bn ? env_bn : 64;
+  const TilePick tp = pick_tiles(p.m_blocks, cols, true, b_mn);
+  p.bn = tp.bn;
+  p.cl = tp.cl;
   p.n_blocks = (int)((cols + p.bn - 1) / p.bn);
   p.k_blocks = (int)((red + BK - 1) / BK);
   const int64_t tiles = (int64_t)((p.m_blocks + p.cl - 1) / p.cl) * p.n_blocks;

@@ -193,17 +193,22 @@ struct GemmCfg {
   static constexpr int B_BYTES = BN / CL * KBYTES;  // this CTA's share of the B tile
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int EXTRA = MODE == LOAD_CONV_DGRAD_BAND ? BAND_WINDOW_BYTES : 0;
-  // TMA-store staging: 4 epilogue warps x 2 buffers x (32 rows x 64 B)
+  // TMA-store staging: 4 epilogue warps x 4 buffers x (32 rows x 64 B)
   static constexpr bool CAN_TMA_STORE = MODE == LOAD_GEMM || MODE == LOAD_CONV_FPROP ||
                                         MODE == LOAD_CONV_FPROP_C8;
-  static constexpr int STG = CAN_TMA_STORE ? EPI_WARPS * 2 * 2048 : 0;
+  // epilogue warps: 8 (two per TMEM lane quarter, each draining half of the
+  // columns) so a second warp per SM sub-partition hides TMEM-load / store
+  // latency; the band dgrad has its own 8-window layout
+  static constexpr int EPI = MODE == LOAD_CONV_DGRAD_BAND ? BAND_WINDOWS : (BN >= 64 ? 8 : 4);
+  static constexpr int EPI_H = MODE == LOAD_CONV_DGRAD_BAND ? 1 : EPI / 4;  // warps per quarter
+  static constexpr int STG_BUFS = 4 / EPI_H;
+  static constexpr int STG = CAN_TMA_STORE ? EPI * STG_BUFS * 2048 : 0;
   static constexpr int SMEM_MAX = 227 * 1024;
   static constexpr int STAGES_MAX = (SMEM_MAX - 1280 - EXTRA - STG) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_MAX > 8 ? 8 : STAGES_MAX;
   static constexpr int TMEM_COLS = pow2_cols(2 * BN);
   static constexpr int SMEM_BYTES =
       STAGES * STAGE_BYTES + STG + EXTRA + 1024 /*align*/ + 256 /*barriers*/;
-  static constexpr int EPI = MODE == LOAD_CONV_DGRAD_BAND ? BAND_WINDOWS : EPI_WARPS;
   static constexpr int THREADS = 64 + 32 * EPI;
 };
 
@@ -591,6 +596,21 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
         const int acc = local & 1;
         const uint32_t use = static_cast<uint32_t>(local >> 1);
         ++local;
+        const bool tma_st = Cfg::CAN_TMA_STORE && g.tma_store;
+        const int ncols = g.N;
+        // this warp drains columns [c_lo, c_lo + BN / EPI_H) of the accumulator
+        constexpr int WCOLS = BN / Cfg::EPI_H;
+        const int c_lo = (Cfg::EPI_H == 1 ? 0 : ((static_cast<int>(warp) - 2) >> 2)) * WCOLS;
+        // 16-bit bias of this warp's columns, fetched before the accumulator wait
+        // so its latency overlaps the main loop: lane j holds columns 8j .. 8j + 7
+        const bool bias_vec = e.bias != nullptr && e.bias_dtype != MS_F32 && (ncols & 7) == 0 &&
+                              (reinterpret_cast<uintptr_t>(e.bias) & 15) == 0;
+        uint4 bq = make_uint4(0u, 0u, 0u, 0u);
+        if (bias_vec) {
+          const int bc = n0 + c_lo + 8 * static_cast<int>(lane);
+          if (static_cast<int>(lane) < WCOLS / 8 && bc < ncols)
+            bq = __ldg(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(e.bias) + bc));
+        }
         mbar_wait(smem_u32(&tfull_bar[acc]), use & 1);
         tc_fence_after();
         const bool zero = ti.kb_end <= ti.kb_begin;
@@ -599,7 +619,6 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
         const int m = ti.m0 + row;
         bool valid;
         int64_t orow;
-        int ncols = g.N;
         if constexpr (MODE == LOAD_CONV_DGRAD) {
           const PhaseInfo& P = g.phase[ti.phase];
           valid = m < P.m_total;
@@ -619,52 +638,53 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
         int64_t col_base = n0;
         if constexpr (MODE == LOAD_CONV_WGRAD) col_base += static_cast<int64_t>(ti.tap) * g.N;
 
+        const uint32_t taddr = tmem_base + ((quarter * 32u) << 16) + acc * BN;
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
+        for (int ci = 0; ci < WCOLS / 32; ++ci) {
+          const int c = c_lo + ci * 32;
           uint32_t r[32];
+          __syncwarp();  // tcgen05.ld / wait are warp-collective: reconverge invalid rows
           if (!zero) {
-            tmem_ld_32x32b_x32(tmem_base + ((quarter * 32u) << 16) + acc * BN + c, r);
-            tmem_ld_wait();
+            tmem_ld_32x32b_x32(taddr + c, r);
+            tmem_ld_wait_regs(r);
           } else {
 #pragma unroll
             for (int j = 0; j < 32; ++j) r[j] = 0u;
           }
           const int nc = n0 + c;  // first column of this chunk in GEMM-N space
-          const bool tma_st = Cfg::CAN_TMA_STORE && g.tma_store;
-          if (nc >= ncols || (!valid && !tma_st)) continue;
+          if (nc >= ncols) continue;  // warp-uniform
           float v[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
           const bool full = (nc + 32 <= ncols);
-          if (e.bias != nullptr) {
-            // every thread of the tile reads the same 32 bias values: 16-byte
-            // vector loads (L1 broadcast) when the chunk is complete and aligned
-            const uint16_t* b16 = static_cast<const uint16_t*>(e.bias) + nc;
-            if (e.bias_dtype != MS_F32 && full && (reinterpret_cast<uintptr_t>(b16) & 15) == 0) {
+          if (bias_vec) {  // full-warp shuffles: before any per-row exit
 #pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                const uint4 u = __ldg(reinterpret_cast<const uint4*>(b16) + q);
-                const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+            for (int q = 0; q < 4; ++q) {
+              const int src = ci * 4 + q;  // lane holding columns c + 8q .. + 7
+              const uint32_t w4[4] = {__shfl_sync(0xffffffffu, bq.x, src),
+                                      __shfl_sync(0xffffffffu, bq.y, src),
+                                      __shfl_sync(0xffffffffu, bq.z, src),
+                                      __shfl_sync(0xffffffffu, bq.w, src)};
 #pragma unroll
-                for (int h = 0; h < 4; ++h) {
-                  float lo, hi;
-                  if (e.bias_dtype == MS_BF16) {
-                    lo = __uint_as_float(w4[h] << 16);
-                    hi = __uint_as_float(w4[h] & 0xFFFF0000u);
-                  } else {
-                    lo = __half2float(__ushort_as_half((unsigned short)(w4[h] & 0xFFFF)));
-                    hi = __half2float(__ushort_as_half((unsigned short)(w4[h] >> 16)));
-                  }
-                  v[q * 8 + 2 * h] += lo;
-                  v[q * 8 + 2 * h + 1] += hi;
+              for (int h = 0; h < 4; ++h) {
+                float lo, hi;
+                if (e.bias_dtype == MS_BF16) {
+                  lo = __uint_as_float(w4[h] << 16);
+                  hi = __uint_as_float(w4[h] & 0xFFFF0000u);
+                } else {
+                  lo = __half2float(__ushort_as_half((unsigned short)(w4[h] & 0xFFFF)));
+                  hi = __half2float(__ushort_as_half((unsigned short)(w4[h] >> 16)));
                 }
+                v[q * 8 + 2 * h] += lo;
+                v[q * 8 + 2 * h + 1] += hi;
               }
-            } else {
-#pragma unroll
-              for (int j = 0; j < 32; ++j)
-                if (nc + j < ncols) v[j] += load_as_float(e.bias, e.bias_dtype, nc + j);
             }
+          } else if (e.bias != nullptr) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (nc + j < ncols) v[j] += load_as_float(e.bias, e.bias_dtype, nc + j);
           }
+          if (!valid && !tma_st) continue;
           if constexpr (Cfg::CAN_TMA_STORE) {
             if (tma_st) {
               // pack, stage this warp's 32 rows x 32 columns (64-byte rows, 64B swizzle),
@@ -678,13 +698,15 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
                 for (int j = 0; j < 16; ++j) p[j] = pack2<__half>(v[2 * j], v[2 * j + 1]);
               }
               const int ew = static_cast<int>(warp) - 2;
-              uint8_t* stg = staging + (ew * 2 + (stg_count & 1)) * 2048;
-              if (lane == 0) bulk_wait_read<1>();  // the store issued 2 chunks ago has read it
+              uint8_t* stg = staging + (ew * Cfg::STG_BUFS + (stg_count % Cfg::STG_BUFS)) * 2048;
+              static_assert(Cfg::STG_BUFS >= 2, "staging ring");
+              // the store issued STG_BUFS chunks ago has finished reading this buffer
+              if (lane == 0) bulk_wait_read<Cfg::STG_BUFS - 1>();
               __syncwarp();
-              const int rr = static_cast<int>(lane);
+              const int rw = static_cast<int>(lane);
 #pragma unroll
               for (int q = 0; q < 4; ++q)
-                *reinterpret_cast<uint4*>(stg + rr * 64 + ((q ^ ((rr >> 1) & 3)) << 4)) =
+                *reinterpret_cast<uint4*>(stg + rw * 64 + ((q ^ ((rw >> 1) & 3)) << 4)) =
                     make_uint4(p[4 * q], p[4 * q + 1], p[4 * q + 2], p[4 * q + 3]);
               fence_proxy_async_smem();
               __syncwarp();

@@ -26,6 +26,7 @@ for name in (sys.argv[1:] or list(SHAPES)):
     x = torch.randn(M, K, device=dev, dtype=torch.bfloat16)
     w = torch.randn(N, K, device=dev, dtype=torch.bfloat16) * 0.02
     y = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
+    b = torch.randn(N, device=dev, dtype=torch.bfloat16)
     dy = torch.randn(M, N, device=dev, dtype=torch.bfloat16)
     dx = torch.empty(M, K, device=dev, dtype=torch.bfloat16)
     dw = torch.empty(N, K, device=dev, dtype=torch.bfloat16)
@@ -33,6 +34,8 @@ for name in (sys.argv[1:] or list(SHAPES)):
     for ps, fn_ours, fn_ref in (
         ("fwd", lambda: L.ms_linear_fwd(M, N, K, 1, P(x), P(w), None, P(y), None, 0, st),
          lambda: torch.matmul(x, w.t(), out=y)),
+        ("fwd+bias", lambda: L.ms_linear_fwd(M, N, K, 1, P(x), P(w), P(b), P(y), None, 0, st),
+         lambda: torch.addmm(b, x, w.t(), out=y)),
         ("dx", lambda: L.ms_linear_dx(M, N, K, 1, P(dy), P(w), P(dx), None, 0, st),
          lambda: torch.matmul(dy, w, out=dx)),
     ):
