@@ -265,6 +265,124 @@ __global__ void __launch_bounds__(256) maxpool_bwd_nhwc8(PoolDims d, const T* __
   }
 }
 
+// The ResNet/VGG stem pool (3x3, stride 2, pad 1), NHWC, 8 channels per
+// thread, 2-D grid (blockIdx.y = image row, x = (column, channel group)) so no
+// per-element division.  Window (oh, ow) covers rows 2oh-1 .. 2oh+1, so input
+// row 2i is only in window row i (tap r = 1) and row 2i+1 in rows i (r = 2) and
+// i+1 (r = 0); the same holds for columns.
+template <typename T>
+__global__ void __launch_bounds__(256) maxpool_fwd_k3s2p1(PoolDims d, const T* __restrict__ x,
+                                                          T* __restrict__ y,
+                                                          uint8_t* __restrict__ idx) {
+  const int G = d.c >> 3;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= d.ow * G) return;
+  const int ow = t / G;
+  const int gg = t - ow * G;
+  const int n = blockIdx.y / d.oh;
+  const int oh = blockIdx.y - n * d.oh;
+  const T* xn = x + (int64_t)n * d.h * d.w * d.c + gg * 8;
+  float best[8];
+  uint32_t arg[8];
+  bool first = true;
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    const int ih = 2 * oh - 1 + r;
+    if (ih < 0 || ih >= d.h) continue;
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+      const int iw = 2 * ow - 1 + s;
+      if (iw < 0 || iw >= d.w) continue;
+      float v[8];
+      ld8<T>(xn + ((int64_t)ih * d.w + iw) * d.c, v, true);
+      const uint32_t k = r * 3 + s;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (first || v[j] > best[j] || (v[j] != v[j] && best[j] == best[j])) {
+          best[j] = v[j];
+          arg[j] = k;
+        }
+      }
+      first = false;
+    }
+  }
+  const int64_t o = (((int64_t)n * d.oh + oh) * d.ow + ow) * d.c + gg * 8;
+  st8<T>(y + o, best, true);
+  if (idx) {
+    uint2 u;
+    u.x = arg[0] | (arg[1] << 8) | (arg[2] << 16) | (arg[3] << 24);
+    u.y = arg[4] | (arg[5] << 8) | (arg[6] << 16) | (arg[7] << 24);
+    *reinterpret_cast<uint2*>(idx + o) = u;
+  }
+}
+
+// add g[j] to acc[j] for the channels whose window argmax is tap k
+template <typename T>
+__device__ __forceinline__ void route8(float (&acc)[8], const uint2 u, const float (&gv)[8],
+                                       uint32_t k) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t a = ((j < 4 ? u.x : u.y) >> (8 * (j & 3))) & 0xFFu;
+    if (a == k) acc[j] += gv[j];
+  }
+}
+
+// Backward of the 3x3/2/1 pool: one thread per 2x2 input block (rows 2i, 2i+1,
+// cols 2j, 2j+1) x 8 channels reads the <= 4 windows (i..i+1) x (j..j+1) once
+// and writes the 4 input pixels (two 2-pixel runs), every dx element exactly once.
+template <typename T>
+__global__ void __launch_bounds__(256) maxpool_bwd_k3s2p1(PoolDims d, const T* __restrict__ g,
+                                                          const uint8_t* __restrict__ idx,
+                                                          T* __restrict__ dx) {
+  const int G = d.c >> 3;
+  const int jn = (d.w + 1) >> 1;
+  const int in = (d.h + 1) >> 1;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= jn * G) return;
+  const int j = t / G;
+  const int gg = t - j * G;
+  const int n = blockIdx.y / in;
+  const int i = blockIdx.y - n * in;
+  float gv[2][2][8];
+  uint2 u[2][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const int oh = i + a, ow = j + b;
+      if (oh < d.oh && ow < d.ow) {
+        const int64_t o = (((int64_t)n * d.oh + oh) * d.ow + ow) * d.c + gg * 8;
+        u[a][b] = __ldg(reinterpret_cast<const uint2*>(idx + o));
+        ld8<T>(g + o, gv[a][b], true);
+      } else {
+        u[a][b] = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);  // matches no tap
+#pragma unroll
+        for (int q = 0; q < 8; ++q) gv[a][b][q] = 0.f;
+      }
+    }
+  // taps: window (i, j) -> input (2i + r - 1, 2j + s - 1), k = 3r + s
+  float o00[8] = {0, 0, 0, 0, 0, 0, 0, 0}, o01[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  float o10[8] = {0, 0, 0, 0, 0, 0, 0, 0}, o11[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  route8<T>(o00, u[0][0], gv[0][0], 4);  // (2i,   2j  ) <- (i, j) r1 s1
+  route8<T>(o01, u[0][0], gv[0][0], 5);  // (2i,   2j+1) <- (i, j) r1 s2
+  route8<T>(o01, u[0][1], gv[0][1], 3);  //                (i, j+1) r1 s0
+  route8<T>(o10, u[0][0], gv[0][0], 7);  // (2i+1, 2j  ) <- (i, j) r2 s1
+  route8<T>(o10, u[1][0], gv[1][0], 1);  //                (i+1, j) r0 s1
+  route8<T>(o11, u[0][0], gv[0][0], 8);  // (2i+1, 2j+1) <- (i, j) r2 s2
+  route8<T>(o11, u[0][1], gv[0][1], 6);  //                (i, j+1) r2 s0
+  route8<T>(o11, u[1][0], gv[1][0], 2);  //                (i+1, j) r0 s2
+  route8<T>(o11, u[1][1], gv[1][1], 0);  //                (i+1, j+1) r0 s0
+  const int h0 = 2 * i, w0 = 2 * j;
+  T* base = dx + ((int64_t)n * d.h + h0) * d.w * d.c + gg * 8;
+  st8<T>(base + (int64_t)w0 * d.c, o00, true);
+  if (w0 + 1 < d.w) st8<T>(base + (int64_t)(w0 + 1) * d.c, o01, true);
+  if (h0 + 1 < d.h) {
+    T* b1 = base + (int64_t)d.w * d.c;
+    st8<T>(b1 + (int64_t)w0 * d.c, o10, true);
+    if (w0 + 1 < d.w) st8<T>(b1 + (int64_t)(w0 + 1) * d.c, o11, true);
+  }
+}
+
 // generic (any layout via strides, scalar)
 struct S4 {
   int64_t n, c, h, w;
@@ -387,6 +505,13 @@ static ms_status pool_dims(const ms_pool_desc* p, PoolDims& d) {
   return MS_OK;
 }
 
+// the 3x3/2/1 specialisation; grid.y = n * rows must fit the 65535 limit
+static bool is_k3s2p1(const PoolDims& d) {
+  return d.kh == 3 && d.kw == 3 && d.sh == 2 && d.sw == 2 && d.ph == 1 && d.pw == 1 &&
+         (int64_t)d.n * d.oh <= 65535 && (int64_t)d.n * ((d.h + 1) / 2) <= 65535 &&
+         d.oh == (d.h + 1) / 2 && d.ow == (d.w + 1) / 2;
+}
+
 extern "C" int64_t ms_maxpool2d_out_h(const ms_pool_desc* p) {
   return (p->h + 2 * p->pad_h - p->kh) / p->stride_h + 1;
 }
@@ -405,9 +530,15 @@ extern "C" ms_status ms_maxpool2d_fwd(const ms_pool_desc* p, const void* x, void
   if (p->layout == MS_NHWC && d.c % 8 == 0 && al16(x) && al16(y) &&
       (!idx_or_null || (reinterpret_cast<uintptr_t>(idx_or_null) & 7) == 0) &&
       (int64_t)d.n * d.h * d.w * (d.c / 8) < (1ll << 31)) {
-    const int64_t work = (int64_t)d.n * d.oh * d.ow * (d.c / 8);
-    MS_DT_DISPATCH(dt, maxpool_fwd_nhwc8<T><<<grid_for(work), 256, 0, st>>>(
-                           d, (const T*)x, (T*)y, (uint8_t*)idx_or_null));
+    if (is_k3s2p1(d)) {
+      const dim3 grid((unsigned)((d.ow * (d.c / 8) + 255) / 256), (unsigned)(d.n * d.oh));
+      MS_DT_DISPATCH(dt, maxpool_fwd_k3s2p1<T><<<grid, 256, 0, st>>>(d, (const T*)x, (T*)y,
+                                                                     (uint8_t*)idx_or_null));
+    } else {
+      const int64_t work = (int64_t)d.n * d.oh * d.ow * (d.c / 8);
+      MS_DT_DISPATCH(dt, maxpool_fwd_nhwc8<T><<<grid_for(work), 256, 0, st>>>(
+                             d, (const T*)x, (T*)y, (uint8_t*)idx_or_null));
+    }
   } else {
     const int64_t work = (int64_t)d.n * d.c * d.oh * d.ow;
     MS_DT_DISPATCH(dt, maxpool_fwd_generic<T><<<grid_for(work), 256, 0, st>>>(
@@ -430,9 +561,16 @@ extern "C" ms_status ms_maxpool2d_bwd(const ms_pool_desc* p, const void* g, cons
   if (p->layout == MS_NHWC && d.c % 8 == 0 && al16(g) && al16(dx) &&
       (reinterpret_cast<uintptr_t>(idx) & 7) == 0 &&
       (int64_t)d.n * d.h * d.w * (d.c / 8) < (1ll << 31)) {
-    const int64_t work = (int64_t)d.n * d.h * d.w * (d.c / 8);
-    MS_DT_DISPATCH(dt, maxpool_bwd_nhwc8<T><<<grid_for(work), 256, 0, st>>>(
-                           d, (const T*)g, (const uint8_t*)idx, (T*)dx));
+    if (is_k3s2p1(d)) {
+      const dim3 grid((unsigned)((((d.w + 1) / 2) * (d.c / 8) + 255) / 256),
+                      (unsigned)(d.n * ((d.h + 1) / 2)));
+      MS_DT_DISPATCH(dt, maxpool_bwd_k3s2p1<T><<<grid, 256, 0, st>>>(d, (const T*)g,
+                                                                     (const uint8_t*)idx, (T*)dx));
+    } else {
+      const int64_t work = (int64_t)d.n * d.h * d.w * (d.c / 8);
+      MS_DT_DISPATCH(dt, maxpool_bwd_nhwc8<T><<<grid_for(work), 256, 0, st>>>(
+                             d, (const T*)g, (const uint8_t*)idx, (T*)dx));
+    }
   } else {
     const int64_t work = (int64_t)d.n * d.c * d.h * d.w;
     MS_DT_DISPATCH(dt, maxpool_bwd_generic<T><<<grid_for(work), 256, 0, st>>>(

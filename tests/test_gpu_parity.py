@@ -362,3 +362,20 @@ def test_fig1_fp32_tiled_kernel(shape):
     _close(y, oracle.conv2d_fwd(xq, wq, 1, 1), "f32", "y")
     _close(x.grad, oracle.conv2d_dx(gq, wq, 1, 1, shape[2], shape[3]), "f32", "dx")
     _close(w.grad, oracle.conv2d_dw(xq, gq, 1, 1, 3, 3), "f32", "dw")
+
+
+@pytest.mark.parametrize("shape", [(2, 64, 16, 16), (1, 16, 11, 14)])
+def test_maxpool_ties_after_relu(shape):
+    # post-ReLU activations: many exact zeros, so window ties are the common case
+    # (first occurrence in row-major window order wins, numpy_impl.py:60-69)
+    rng = np.random.default_rng(7)
+    x64 = np.maximum(np.round(rng.standard_normal(shape) * 2) / 2, 0)
+    x, xq = _q(x64, "bf16")
+    x = x.contiguous(memory_format=torch.channels_last).requires_grad_(True)
+    y = MF.max_pool2d(x, 3, 2, 1)
+    yr, local, flat = oracle.maxpool2d_fwd(xq, 3, 3, 2, 2, 1, 1)
+    g, gq = _q(rng.standard_normal(yr.shape), "bf16")
+    y.backward(g)
+    np.testing.assert_array_equal(y.detach().float().cpu().double().numpy(), yr)
+    _close(x.grad, oracle.maxpool2d_bwd(gq, flat, shape[2], shape[3]), "bf16", "maxpool dx",
+           ulps=2.01)
