@@ -298,7 +298,8 @@ def gpu_main(args):
         torch.cuda.empty_cache()
         # the north star's layer set only (Linear / Conv2d / BatchNorm2d-eval), ReLU and
         # MaxPool2d left stock: isolates the paper's Fig. 2 effect from the §8(f) swaps
-        convert_to_memory_saving(layers_model, relu=False, maxpool2d=False)
+        convert_to_memory_saving(layers_model, relu=False, maxpool2d=False, dropout=False,
+                                 layernorm=False, conv_transpose2d=False)
         linputs = list(wl.make_batch(wl.batch, dev))
         if wl.input_requires_grad:
             linputs[0].requires_grad_(True)

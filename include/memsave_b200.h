@@ -153,6 +153,50 @@ MS_API ms_status ms_maxpool2d_fwd(const ms_pool_desc* p, const void* x, void* y,
 MS_API ms_status ms_maxpool2d_bwd(const ms_pool_desc* p, const void* g, const void* idx,
                                   void* dx, void* stream);
 
+/* ------------------------------------------------------------ conv_transpose2d
+ * ConvTranspose2d forward (rules.py:68-71; SPEC.md forward_conv_transpose2d:
+ * "forward equals conv2d's input-VJP with the same kernel"): `d` describes
+ * the equivalent conv2d, whose INPUT is y ([n][c][h][w], c = out channels of
+ * the transposed conv) and whose OUTPUT is x ([n][k][oh][ow]); w is
+ * [k][c][r][s] (= the ConvTranspose2d weight [C_in][C_out][kh][kw]).  bias
+ * ([c], nullable) is added in the same pass.  Workspace: ms_conv2d_workspace(d,
+ * MS_CONV_DX).  dX and dW of the transposed conv are ms_conv2d_fwd(d, g, w) and
+ * ms_conv2d_dw(d, g, x).                                                    */
+MS_API ms_status ms_conv_transpose2d_fwd(const ms_conv_desc* d, const void* x, const void* w,
+                                         const void* bias_or_null, void* y, void* ws,
+                                         size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------ dropout (RNG replay)
+ * MemSave Dropout (rules.py:103-106, saved.py:91-108 RngSeed; SPEC.md
+ * forward_dropout): element i is kept iff U_i >= p, U_i the i-th double of the
+ * reference generator leantape.core.Rng(seed, stream_id).uniform()
+ * (core.py:100-124: numpy Philox4x64-10, key [seed, stream_id]); kept
+ * elements are scaled by 1/(1-p).  Backward regenerates the same mask from
+ * (seed, stream_id, p): nothing O(numel) is stored.  mask_or_null receives the
+ * keep flags at one byte per element (the NAIVE StoreMask convention, tests).
+ * y may alias x; dx may alias g; 0 <= p < 1.                                */
+MS_API ms_status ms_dropout_fwd(int64_t numel, int32_t dtype, const void* x, void* y,
+                                uint64_t seed, uint64_t stream_id, double p, void* mask_or_null,
+                                void* stream);
+MS_API ms_status ms_dropout_bwd(int64_t numel, int32_t dtype, const void* g, void* dx,
+                                uint64_t seed, uint64_t stream_id, double p, void* stream);
+
+/* ------------------------------------------------------------ layernorm
+ * LayerNorm over the last dimension (rules.py:89-96; SPEC.md forward_layernorm):
+ * x is [rows][dim] row-major; w / b ([dim], dtype of x) may be NULL; mean and
+ * rstd are fp32 [rows] (the "stats" the rule saves; NULL in inference).
+ * Backward products are independent: dx, dw, db may each be NULL.  dw / db
+ * need the workspace sized by ms_layernorm_workspace.                       */
+MS_API size_t ms_layernorm_workspace(int64_t rows, int64_t dim, int32_t dtype);
+MS_API ms_status ms_layernorm_fwd(int64_t rows, int64_t dim, int32_t dtype, const void* x,
+                                  const void* w_or_null, const void* b_or_null, double eps,
+                                  void* y, float* mean_or_null, float* rstd_or_null,
+                                  void* stream);
+MS_API ms_status ms_layernorm_bwd(int64_t rows, int64_t dim, int32_t dtype, const void* g,
+                                  const void* x, const float* mean, const float* rstd,
+                                  const void* w_or_null, void* dx_or_null, void* dw_or_null,
+                                  void* db_or_null, void* ws, size_t ws_bytes, void* stream);
+
 /* ------------------------------------------------------------ misc */
 MS_API const char* ms_status_string(int32_t status);
 MS_API const char* ms_last_error(void);

@@ -83,7 +83,8 @@ def gen_pool(core, kernels):
 
 def gen_rules(rules):
     table = []
-    for kind in ("linear", "conv2d", "conv_transpose2d", "batchnorm2d", "relu", "maxpool2d"):
+    for kind in ("linear", "conv2d", "conv_transpose2d", "batchnorm2d", "relu", "maxpool2d",
+                 "dropout", "layernorm"):
         for bn_train in ((False, True) if kind == "batchnorm2d" else (False,)):
             for pol in (rules.Policy.NAIVE, rules.Policy.MEMSAVE):
                 for x_rg in (False, True):
@@ -135,6 +136,57 @@ def gen_linear_bn(core):
     return out
 
 
+def gen_dropout(core):
+    """Dropout keep masks from the reference generator: Rng(seed, stream).uniform
+    (core.py:100-124) >= p, for streams DROPOUT_STREAM_BASE + node."""
+    out = {}
+    base = core.Rng.DROPOUT_STREAM_BASE
+    for name, seed, node, p, n in (("d_small", 0, 0, 0.1, 37), ("d_half", 12345, 3, 0.5, 1000),
+                                   ("d_big", 2 ** 61 + 7, 11, 0.25, 4099)):
+        u = core.Rng(seed, base + node).uniform((n,))
+        out[f"{name}/key"] = np.array([seed, base + node], dtype=np.uint64)
+        out[f"{name}/p"] = np.array(p)
+        out[f"{name}/mask"] = (u >= p).astype(np.uint8)
+    return out
+
+
+def gen_layernorm(core):
+    """LayerNorm (SPEC.md forward_layernorm): torch-CPU float64 autograd."""
+    import torch
+    out = {}
+    for name, shape, d in (("ln_small", (3, 8), 8), ("ln_3d", (2, 5, 24), 24)):
+        x = core.Rng(3, 0).normal(shape, core.Dtype.F64)
+        w = core.Rng(3, 1).normal((d,), core.Dtype.F64)
+        b = core.Rng(3, 3).normal((d,), core.Dtype.F64)
+        tx, tw, tb = (torch.tensor(a, requires_grad=True) for a in (x, w, b))
+        y = torch.nn.functional.layer_norm(tx, (d,), tw, tb, eps=1e-5)
+        g = core.Rng(3, 2).normal(shape, core.Dtype.F64)
+        y.backward(torch.tensor(g))
+        for key, val in dict(x=x, w=w, b=b, y=y.detach().numpy(), g=g, dx=tx.grad.numpy(),
+                             dw=tw.grad.numpy(), db=tb.grad.numpy()).items():
+            out[f"{name}/{key}"] = np.ascontiguousarray(val)
+    return out
+
+
+def gen_conv_transpose(core, kernels):
+    """ConvTranspose2d through the reference conv kernels (SPEC.md: convT forward
+    = conv2d input-VJP with the same kernel)."""
+    out = {}
+    for name, n, cin, h, w, cout, k, s, p in (("ct_s2", 2, 6, 5, 4, 4, 3, 2, 1),
+                                              ("ct_s1", 1, 3, 6, 6, 5, 3, 1, 1)):
+        x = core.Rng(4, 0).normal((n, cin, h, w), core.Dtype.F64)
+        wt = core.Rng(4, 1).normal((cin, cout, k, k), core.Dtype.F64)
+        ho, wo = (h - 1) * s - 2 * p + k, (w - 1) * s - 2 * p + k
+        y = kernels.conv2d_dx(x, wt, s, p, ho, wo)
+        g = core.Rng(4, 2).normal((n, cout, ho, wo), core.Dtype.F64)
+        dx = kernels.conv2d_fwd(g, wt, s, p)
+        dw = kernels.conv2d_dw(g, x, s, p, k, k)
+        for key, val in dict(x=x, w=wt, y=y, g=g, dx=dx, dw=dw).items():
+            out[f"{name}/{key}"] = np.ascontiguousarray(val)
+        out[f"{name}/geom"] = np.array([s, p], dtype=np.int64)
+    return out
+
+
 def main():
     sys.path.insert(0, "/root/reference/pkg/src")
     from leantape import core, rules  # noqa: E402
@@ -157,6 +209,10 @@ def main():
 
     np.savez_compressed(os.path.join(GOLDEN, "linear_bn_spec.npz"), **gen_linear_bn(core))
     np.savez_compressed(os.path.join(GOLDEN, "maxpool_ref.npz"), **gen_pool(core, kernels))
+    np.savez_compressed(os.path.join(GOLDEN, "dropout_ref.npz"), **gen_dropout(core))
+    np.savez_compressed(os.path.join(GOLDEN, "layernorm_spec.npz"), **gen_layernorm(core))
+    np.savez_compressed(os.path.join(GOLDEN, "conv_transpose_ref.npz"),
+                        **gen_conv_transpose(core, kernels))
 
     # SPEC known-answer examples
     kat = {

@@ -4,7 +4,8 @@ Restates /root/reference/pkg/src/leantape/rules.py for the rows on the hot
 path: linear (rules.py:64-66), conv2d / conv_transpose2d (rules.py:68-71),
 batchnorm2d in eval mode (rules.py:84-87) and the shared ``_linear_family``
 rule (rules.py:133-141), plus the first "next" rows: relu (rules.py:98-101)
-and maxpool2d (rules.py:108-109).  Golden tables produced by importing the reference
+and maxpool2d (rules.py:108-109), then dropout (rules.py:103-106) and layernorm
+(rules.py:89-96).  Golden tables produced by importing the reference
 (tests/golden/rules.json) pin this restatement.
 """
 
@@ -54,4 +55,15 @@ def storage_decision(kind: str, policy: Policy, *, x_rg: bool, w_rg: bool,
         return [("mask", "bitmask")] if policy is Policy.MEMSAVE else [("y", "full")]
     if kind == "maxpool2d":  # rules.py:108-109
         return [("idx", "indexmap")] if out_rg else []
+    if kind == "dropout":  # rules.py:103-106
+        if not out_rg:
+            return []
+        return [("seed", "seed")] if policy is Policy.MEMSAVE else [("mask", "bytemask")]
+    if kind == "layernorm":  # rules.py:89-96, identical under both policies
+        saves = []
+        if x_rg or w_rg:
+            saves += [("x", "full"), ("stats", "stats")]
+        if x_rg:
+            saves.append(("w", "full"))
+        return saves
     raise ValueError(f"no hot-path storage rule for op kind {kind!r}")

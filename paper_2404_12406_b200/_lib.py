@@ -68,6 +68,17 @@ SIGNATURES = {
     "ms_maxpool2d_out_w": (_c_i64, [ctypes.POINTER(PoolDesc)]),
     "ms_maxpool2d_fwd": (_c_i32, [ctypes.POINTER(PoolDesc), _vp, _vp, _vp, _vp]),
     "ms_maxpool2d_bwd": (_c_i32, [ctypes.POINTER(PoolDesc), _vp, _vp, _vp, _vp]),
+    "ms_conv_transpose2d_fwd": (_c_i32, [ctypes.POINTER(ConvDesc), _vp, _vp, _vp, _vp, _vp, _c_sz,
+                                         _vp]),
+    "ms_dropout_fwd": (_c_i32, [_c_i64, _c_i32, _vp, _vp, ctypes.c_uint64, ctypes.c_uint64,
+                                ctypes.c_double, _vp, _vp]),
+    "ms_dropout_bwd": (_c_i32, [_c_i64, _c_i32, _vp, _vp, ctypes.c_uint64, ctypes.c_uint64,
+                                ctypes.c_double, _vp]),
+    "ms_layernorm_workspace": (_c_sz, [_c_i64, _c_i64, _c_i32]),
+    "ms_layernorm_fwd": (_c_i32, [_c_i64, _c_i64, _c_i32, _vp, _vp, _vp, ctypes.c_double, _vp,
+                                  _vp, _vp, _vp]),
+    "ms_layernorm_bwd": (_c_i32, [_c_i64, _c_i64, _c_i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                  _vp, _vp, _c_sz, _vp]),
     "ms_status_string": (ctypes.c_char_p, [_c_i32]),
     "ms_last_error": (ctypes.c_char_p, []),
     "ms_version": (_c_i32, []),

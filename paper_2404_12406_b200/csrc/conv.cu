@@ -89,7 +89,7 @@ bool rowseg_ok(const ms_conv_desc* d, const ConvDims& c) {
   return cached == 1;
 }
 
-ConvPlan plan(const ms_conv_desc* d, int pass) {
+ConvPlan plan(const ms_conv_desc* d, int pass, bool dx_bias = false) {
   ConvPlan p;
   const ConvDims c = dims_of(d);
   const size_t es = dtype_size(d->dtype);
@@ -118,7 +118,7 @@ ConvPlan plan(const ms_conv_desc* d, int pass) {
     p.ws = p.ws_pad + p.ws_w;
   } else if (pass == MS_CONV_DX) {
     if (d->k % 8 != 0) return p;  // SIMT
-    if (d->c == BAND_C && d->r == BAND_R && d->s == BAND_S && d->stride_w == BAND_SW &&
+    if (!dx_bias && d->c == BAND_C && d->r == BAND_R && d->s == BAND_S && d->stride_w == BAND_SW &&
         d->stride_h == BAND_SW && c.ow <= BM && (int64_t)BAND_WINDOWS * BAND_WIN * 4 <= BAND_WINDOW_BYTES) {
       // the 3-channel 7x7/2 stem: per dX-row band, dY-row x W GEMM + col2im
       p.tc = true;
@@ -273,7 +273,7 @@ ms_status dx_band(const ms_conv_desc* d, const ConvPlan& p, const void* dy, cons
 }
 
 ms_status dx_tc(const ms_conv_desc* d, const ConvPlan& p, const void* dy, const void* w, void* dx,
-                void* ws, cudaStream_t st) {
+                void* ws, cudaStream_t st, const void* bias = nullptr) {
   const ConvDims c = dims_of(d);
   const int dt = d->dtype;
   if (p.band) return dx_band(d, p, dy, w, dx, ws, st);
@@ -325,7 +325,7 @@ ms_status dx_tc(const ms_conv_desc* d, const ConvPlan& p, const void* dy, const 
   }
   g.nphases = np;
   g.num_tiles = tiles;
-  g.epi = EpiParams{dx, c.c, dt, 0, nullptr, dt};
+  g.epi = EpiParams{dx, c.c, dt, 0, bias, dt};  // bias: conv_transpose2d forward
   const int64_t wrow = (int64_t)c.r * c.s * p.kpad;
   MS_TRY(make_tmap_2d(&tm.b, dt, wd, wrow, c.c, wrow, BK, bn / tp.cl));
   return launch_umma(bn, 0, 0, LOAD_CONV_DGRAD, tm, g, st, tp.cl);
@@ -365,6 +365,41 @@ ms_status dw_tc(const ms_conv_desc* d, const ConvPlan& p, const void* x, const v
   MS_TRY(make_tmap_im2col(&tm.b, dt, x, c.n, c.h, c.w, c.c, lower, upper, c.sw, c.sh, 64, BK));
   MS_TRY(launch_umma(bn, 1, 1, LOAD_CONV_WGRAD, tm, g, st));
   return wgrad_finalize(dt, c.k, c.c, c.r, c.s, d->wlayout, acc, dw, st);
+}
+
+// y[n, c, ...] += bias[c] (NCHW planes or NHWC rows)
+template <typename T>
+__global__ void add_channel_bias_kernel(int64_t total, int64_t c, int64_t hw, int nhwc, T* y,
+                                        const T* bias) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t ch = nhwc ? i % c : (i / hw) % c;
+    y[i] = IO<T>::cvt(IO<T>::ld(y + i) + IO<T>::ld(bias + ch));
+  }
+}
+
+ms_status add_channel_bias(int dt, int layout, int64_t n, int64_t c, int64_t hw, void* y,
+                           const void* bias, cudaStream_t st) {
+  const int64_t total = n * c * hw;
+  if (total == 0) return MS_OK;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
+  const int nhwc = layout == MS_NHWC;
+  switch (dt) {
+    case MS_F32:
+      add_channel_bias_kernel<float><<<(unsigned)blocks, 256, 0, st>>>(total, c, hw, nhwc,
+                                                                      (float*)y, (const float*)bias);
+      break;
+    case MS_BF16:
+      add_channel_bias_kernel<__nv_bfloat16><<<(unsigned)blocks, 256, 0, st>>>(
+          total, c, hw, nhwc, (__nv_bfloat16*)y, (const __nv_bfloat16*)bias);
+      break;
+    default:
+      add_channel_bias_kernel<__half><<<(unsigned)blocks, 256, 0, st>>>(
+          total, c, hw, nhwc, (__half*)y, (const __half*)bias);
+  }
+  count_launch();
+  return launch_status("add_channel_bias");
 }
 
 }  // namespace
@@ -455,4 +490,27 @@ extern "C" ms_status ms_conv2d_db(const ms_conv_desc* d, const void* dy, void* d
   if (d->layout == MS_NHWC)
     return colsum((int64_t)c.n * c.oh * c.ow, c.k, d->dtype, dy, db, d->dtype, ws, st);
   return planesum(c.n, c.k, (int64_t)c.oh * c.ow, d->dtype, dy, db, d->dtype, ws, st);
+}
+
+extern "C" ms_status ms_conv_transpose2d_fwd(const ms_conv_desc* d, const void* x, const void* w,
+                                             const void* bias, void* y, void* ws,
+                                             size_t ws_bytes, void* stream) {
+  // the input-VJP of the conv2d `d` (whose input is y, output x), plus a bias
+  // per conv-input channel fused into the tcgen05 epilogue
+  MS_TRY(validate(d));
+  MS_TRY(bind_device(y));
+  if (d->n == 0) return MS_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  ConvPlan p = plan(d, MS_CONV_DX, bias != nullptr);
+  MS_CHECK_ARG(ws_bytes >= p.ws && (p.ws == 0 || ws), MS_ERR_WORKSPACE,
+               "conv_transpose2d fwd: workspace %zu < %zu", ws_bytes, p.ws);
+  if (p.tc) return dx_tc(d, p, x, w, y, ws, st, bias);
+  ms_status s = MS_ERR_UNSUPPORTED;
+  if (d->dtype == MS_F32)
+    s = small_conv_fp32(MS_CONV_DX, dims_of(d), d->layout, d->wlayout, x, w, y, ws, ws_bytes, st);
+  if (s == MS_ERR_UNSUPPORTED)
+    s = simt_conv_dx(dims_of(d), d->dtype, d->layout, d->wlayout, x, w, y, st);
+  MS_TRY(s);
+  if (bias) MS_TRY(add_channel_bias(d->dtype, d->layout, d->n, d->c, d->h * d->w, y, bias, st));
+  return MS_OK;
 }

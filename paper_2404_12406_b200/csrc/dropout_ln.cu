@@ -1,0 +1,460 @@
+// Dropout with RNG replay and LayerNorm.
+//
+// Dropout (rules.py:103-106 MEMSAVE row, saved.py:91-108 RngSeed, SPEC.md
+// forward_dropout): the keep mask is a pure function of (seed, stream, element
+// index), so backward regenerates it instead of reading a stored mask.  The
+// generator is the reference's own: leantape.core.Rng(seed, stream).uniform()
+// (core.py:100-124) is numpy's Philox4x64-10 keyed [seed, stream] with a
+// 256-bit counter that is incremented before each 4-word block, and
+// Generator.random() maps a 64-bit word u to (u >> 11) * 2^-53.  Element i
+// therefore uses word i % 4 of block (i / 4) + 1 and is kept iff
+// U_i >= p  <=>  (u >> 11) >= ceil(p * 2^53), so the mask here is bit-identical
+// to the reference's for the same (seed, stream, p).  Kept elements are scaled
+// by 1 / (1 - p) (SPEC.md DropoutConfig).
+//
+// LayerNorm over the last dimension (rules.py:89-96, SPEC.md forward_layernorm):
+// y = (x - mean) * rstd * w + b with fp32 statistics; the saved set is
+// {x, mean/rstd, w} under both policies.  Backward:
+//   dx = rstd * (g w - mean_j(g w) - xhat * mean_j(g w xhat)),
+//   dw = sum_rows g xhat,  db = sum_rows g   (launched only when requested).
+// One warp per row; rows up to 2048 elements live in registers (8 per lane per
+// 256-column slab), longer or unaligned rows take a block-per-row loop.
+#include "misc.cuh"
+#include "vec.cuh"
+
+namespace ms {
+namespace {
+
+// ---------------------------------------------------------------- Philox4x64-10
+__device__ __forceinline__ void philox4x64_10(uint64_t (&c)[4], uint64_t k0, uint64_t k1) {
+  constexpr uint64_t M0 = 0xD2E7470EE14C6C93ull, M1 = 0xCA5A826395121157ull;
+  constexpr uint64_t W0 = 0x9E3779B97F4A7C15ull, W1 = 0xBB67AE8584CAA73Bull;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) {
+      k0 += W0;
+      k1 += W1;
+    }
+    const uint64_t hi0 = __umul64hi(M0, c[0]), lo0 = M0 * c[0];
+    const uint64_t hi1 = __umul64hi(M1, c[2]), lo1 = M1 * c[2];
+    const uint64_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+    c[0] = n0;
+    c[1] = lo1;
+    c[2] = n2;
+    c[3] = lo0;
+  }
+}
+
+// keep bits of the 4 elements of block `blk` (element 4*(blk-1) + j -> bit j)
+__device__ __forceinline__ uint32_t keep4(uint64_t blk, uint64_t k0, uint64_t k1, uint64_t thr) {
+  uint64_t c[4] = {blk, 0ull, 0ull, 0ull};
+  philox4x64_10(c, k0, k1);
+  uint32_t bits = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) bits |= ((c[j] >> 11) >= thr ? 1u : 0u) << j;
+  return bits;
+}
+
+// y = keep ? x * scale : 0 over groups of 8 elements (two Philox blocks);
+// mask (optional, 1 byte per element) receives the keep flags.
+template <typename T>
+__global__ void __launch_bounds__(256) dropout_kernel(int64_t n, const T* x, T* y, uint64_t k0,
+                                                      uint64_t k1, uint64_t thr, float scale,
+                                                      uint8_t* __restrict__ mask, bool vec) {
+  const int64_t full = n / 8;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t gi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gi < full; gi += stride) {
+    float v[8];
+    ld8<T>(x + gi * 8, v, vec);
+    const uint32_t bits = keep4(2 * gi + 1, k0, k1, thr) | (keep4(2 * gi + 2, k0, k1, thr) << 4);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = (bits >> j) & 1u ? v[j] * scale : 0.f;
+    st8<T>(y + gi * 8, v, vec);
+    if (mask) {
+      uint2 m;
+      m.x = (bits & 1u) | ((bits >> 1) & 1u) << 8 | ((bits >> 2) & 1u) << 16 | ((bits >> 3) & 1u) << 24;
+      m.y = ((bits >> 4) & 1u) | ((bits >> 5) & 1u) << 8 | ((bits >> 6) & 1u) << 16 |
+            ((bits >> 7) & 1u) << 24;
+      if (vec) {
+        *reinterpret_cast<uint2*>(mask + gi * 8) = m;
+      } else {
+        for (int j = 0; j < 8; ++j) mask[gi * 8 + j] = (bits >> j) & 1u;
+      }
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // tail elements
+    for (int64_t e = full * 8; e < n; ++e) {
+      const uint32_t b = keep4(static_cast<uint64_t>(e / 4) + 1, k0, k1, thr);
+      const bool keep = (b >> (e % 4)) & 1u;
+      y[e] = IO<T>::cvt(keep ? IO<T>::ld(x + e) * scale : 0.f);
+      if (mask) mask[e] = keep ? 1 : 0;
+    }
+  }
+}
+
+int grid_for(int64_t work, int per_sm = 16) {
+  int64_t b = (work + 255) / 256;
+  const int64_t cap = (int64_t)num_sms() * per_sm;
+  if (b > cap) b = cap;
+  return (int)(b > 0 ? b : 1);
+}
+
+bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+ms_status dropout_launch(int64_t numel, int dt, const void* x, void* y, uint64_t seed,
+                         uint64_t stream_id, double p, void* mask, cudaStream_t st) {
+  MS_CHECK_ARG(numel >= 0, MS_ERR_SHAPE, "dropout: negative numel");
+  MS_CHECK_ARG(p >= 0.0 && p < 1.0, MS_ERR_SHAPE, "dropout: p must be in [0, 1), got %g", p);
+  if (numel == 0) return MS_OK;
+  // keep iff (u >> 11) >= ceil(p * 2^53); p * 2^53 is exact in double
+  const double t = ceil(p * 9007199254740992.0);
+  const uint64_t thr = static_cast<uint64_t>(t);
+  const float scale = static_cast<float>(1.0 / (1.0 - p));
+  const bool vec = al16(x) && al16(y) && (!mask || (reinterpret_cast<uintptr_t>(mask) & 7) == 0);
+  MS_DT_DISPATCH(dt, dropout_kernel<T><<<grid_for(numel / 8 + 1), 256, 0, st>>>(
+                         numel, (const T*)x, (T*)y, seed, stream_id, thr, scale,
+                         (uint8_t*)mask, vec));
+  count_launch();
+  return launch_status("dropout");
+}
+
+// ---------------------------------------------------------------- LayerNorm
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+constexpr int LN_WARPS = 8;
+
+// one warp per row, KV slabs of 256 columns (8 per lane) held in registers
+template <typename T, int KV>
+__global__ void __launch_bounds__(LN_WARPS * 32) ln_fwd_vec(int64_t rows, int D, const T* x,
+                                                            const T* w, const T* b, float eps,
+                                                            T* y, float* mean, float* rstd) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * LN_WARPS + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const T* xr = x + row * D;
+  float v[KV][8];
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < KV; ++k) {
+    const int col = (k * 32 + lane) * 8;
+    if (col < D) {
+      ld8<T>(xr + col, v[k], true);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s += v[k][j];
+    }
+  }
+  const float mu = warp_sum(s) / D;
+  float q = 0.f;
+#pragma unroll
+  for (int k = 0; k < KV; ++k) {
+    const int col = (k * 32 + lane) * 8;
+    if (col < D) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float d = v[k][j] - mu;
+        q += d * d;
+      }
+    }
+  }
+  const float r = rsqrtf(warp_sum(q) / D + eps);
+  T* yr = y + row * D;
+#pragma unroll
+  for (int k = 0; k < KV; ++k) {
+    const int col = (k * 32 + lane) * 8;
+    if (col < D) {
+      float wv[8], bv[8];
+      if (w) ld8<T>(w + col, wv, true);
+      if (b) ld8<T>(b + col, bv, true);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        float o = (v[k][j] - mu) * r;
+        if (w) o *= wv[j];
+        if (b) o += bv[j];
+        v[k][j] = o;
+      }
+      st8<T>(yr + col, v[k], true);
+    }
+  }
+  if (lane == 0) {
+    if (mean) mean[row] = mu;
+    if (rstd) rstd[row] = r;
+  }
+}
+
+__device__ __forceinline__ float block_sum(float v, float* red) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  float t = 0.f;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+  return t;
+}
+
+// any D / alignment: one block per row, three passes over the row
+template <typename T>
+__global__ void __launch_bounds__(256) ln_fwd_generic(int64_t rows, int D, const T* x, const T* w,
+                                                      const T* b, float eps, T* y, float* mean,
+                                                      float* rstd) {
+  __shared__ float red[8];
+  const int64_t row = blockIdx.x;
+  const T* xr = x + row * D;
+  float s = 0.f;
+  for (int i = threadIdx.x; i < D; i += blockDim.x) s += IO<T>::ld(xr + i);
+  const float mu = block_sum(s, red) / D;
+  float q = 0.f;
+  for (int i = threadIdx.x; i < D; i += blockDim.x) {
+    const float d = IO<T>::ld(xr + i) - mu;
+    q += d * d;
+  }
+  const float r = rsqrtf(block_sum(q, red) / D + eps);
+  T* yr = y + row * D;
+  for (int i = threadIdx.x; i < D; i += blockDim.x) {
+    float o = (IO<T>::ld(xr + i) - mu) * r;
+    if (w) o *= IO<T>::ld(w + i);
+    if (b) o += IO<T>::ld(b + i);
+    yr[i] = IO<T>::cvt(o);
+  }
+  if (threadIdx.x == 0) {
+    if (mean) mean[row] = mu;
+    if (rstd) rstd[row] = r;
+  }
+}
+
+// backward, one warp per row (grid-stride over rows); dw / db partial sums in
+// registers, reduced per block through shared memory, then one fp32 atomic per
+// column per block into the workspace
+template <typename T, int KV>
+__global__ void __launch_bounds__(LN_WARPS * 32) ln_bwd_vec(int64_t rows, int D, const T* g,
+                                                            const T* x, const float* mean,
+                                                            const float* rstd, const T* w, T* dx,
+                                                            float* dw_acc, float* db_acc) {
+  extern __shared__ float sacc[];  // [2][D] when dw / db are requested
+  const int lane = threadIdx.x & 31;
+  const bool wantp = dw_acc || db_acc;
+  if (wantp) {
+    for (int i = threadIdx.x; i < 2 * D; i += blockDim.x) sacc[i] = 0.f;
+    __syncthreads();
+  }
+  float wv[KV][8];
+#pragma unroll
+  for (int k = 0; k < KV; ++k) {
+    const int col = (k * 32 + lane) * 8;
+    if (col < D && w) {
+      ld8<T>(w + col, wv[k], true);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) wv[k][j] = 1.f;
+    }
+  }
+  float pw[KV][8], pb[KV][8];
+#pragma unroll
+  for (int k = 0; k < KV; ++k)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) pw[k][j] = pb[k][j] = 0.f;
+  const int64_t step = (int64_t)gridDim.x * LN_WARPS;
+  for (int64_t row = (int64_t)blockIdx.x * LN_WARPS + (threadIdx.x >> 5); row < rows; row += step) {
+    const float mu = mean[row], r = rstd[row];
+    float xh[KV][8], gv[KV][8];
+    float a = 0.f, c = 0.f;
+#pragma unroll
+    for (int k = 0; k < KV; ++k) {
+      const int col = (k * 32 + lane) * 8;
+      if (col < D) {
+        ld8<T>(x + row * D + col, xh[k], true);
+        ld8<T>(g + row * D + col, gv[k], true);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          xh[k][j] = (xh[k][j] - mu) * r;
+          const float gw = gv[k][j] * wv[k][j];
+          a += gw;
+          c += gw * xh[k][j];
+          pw[k][j] += gv[k][j] * xh[k][j];
+          pb[k][j] += gv[k][j];
+        }
+      }
+    }
+    if (dx) {
+      const float ma = warp_sum(a) / D, mc = warp_sum(c) / D;
+#pragma unroll
+      for (int k = 0; k < KV; ++k) {
+        const int col = (k * 32 + lane) * 8;
+        if (col < D) {
+          float o[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) o[j] = r * (gv[k][j] * wv[k][j] - ma - xh[k][j] * mc);
+          st8<T>(dx + row * D + col, o, true);
+        }
+      }
+    }
+  }
+  if (wantp) {
+#pragma unroll
+    for (int k = 0; k < KV; ++k) {
+      const int col = (k * 32 + lane) * 8;
+      if (col < D) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          atomicAdd(&sacc[col + j], pw[k][j]);
+          atomicAdd(&sacc[D + col + j], pb[k][j]);
+        }
+      }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < D; i += blockDim.x) {
+      if (dw_acc) atomicAdd(&dw_acc[i], sacc[i]);
+      if (db_acc) atomicAdd(&db_acc[i], sacc[D + i]);
+    }
+  }
+}
+
+// any D / alignment: one block per row
+template <typename T>
+__global__ void __launch_bounds__(256) ln_bwd_generic(int64_t rows, int D, const T* g, const T* x,
+                                                      const float* mean, const float* rstd,
+                                                      const T* w, T* dx, float* dw_acc,
+                                                      float* db_acc) {
+  __shared__ float red[8];
+  const int64_t row = blockIdx.x;
+  const float mu = mean[row], r = rstd[row];
+  const T* xr = x + row * D;
+  const T* gr = g + row * D;
+  float a = 0.f, c = 0.f;
+  for (int i = threadIdx.x; i < D; i += blockDim.x) {
+    const float xh = (IO<T>::ld(xr + i) - mu) * r;
+    const float gv = IO<T>::ld(gr + i);
+    const float gw = gv * (w ? IO<T>::ld(w + i) : 1.f);
+    a += gw;
+    c += gw * xh;
+    if (dw_acc) atomicAdd(&dw_acc[i], gv * xh);
+    if (db_acc) atomicAdd(&db_acc[i], gv);
+  }
+  const float ma = block_sum(a, red) / D, mc = block_sum(c, red) / D;
+  if (!dx) return;
+  for (int i = threadIdx.x; i < D; i += blockDim.x) {
+    const float xh = (IO<T>::ld(xr + i) - mu) * r;
+    const float gw = IO<T>::ld(gr + i) * (w ? IO<T>::ld(w + i) : 1.f);
+    dx[row * D + i] = IO<T>::cvt(r * (gw - ma - xh * mc));
+  }
+}
+
+// KV slabs for the register path (0 = generic)
+int ln_kv(int64_t D, int dt, const void* const* ptrs, int nptr) {
+  if (D % 8 != 0 || D > 2048) return 0;
+  for (int i = 0; i < nptr; ++i)
+    if (ptrs[i] && !al16(ptrs[i])) return 0;
+  (void)dt;
+  const int kv = (int)((D + 255) / 256);
+  return kv <= 4 ? kv : (kv <= 6 ? 6 : 8);
+}
+
+#define MS_KV_SWITCH(kv, ...)              \
+  switch (kv) {                            \
+    case 1: { constexpr int KV = 1; __VA_ARGS__; } break; \
+    case 2: { constexpr int KV = 2; __VA_ARGS__; } break; \
+    case 3: { constexpr int KV = 3; __VA_ARGS__; } break; \
+    case 4: { constexpr int KV = 4; __VA_ARGS__; } break; \
+    case 6: { constexpr int KV = 6; __VA_ARGS__; } break; \
+    default: { constexpr int KV = 8; __VA_ARGS__; } break; \
+  }
+
+}  // namespace
+}  // namespace ms
+
+using namespace ms;
+
+extern "C" ms_status ms_dropout_fwd(int64_t numel, int32_t dtype, const void* x, void* y,
+                                    uint64_t seed, uint64_t stream_id, double p,
+                                    void* mask_or_null, void* stream) {
+  MS_TRY(bind_device(y));
+  return dropout_launch(numel, dtype, x, y, seed, stream_id, p, mask_or_null,
+                        (cudaStream_t)stream);
+}
+
+extern "C" ms_status ms_dropout_bwd(int64_t numel, int32_t dtype, const void* g, void* dx,
+                                    uint64_t seed, uint64_t stream_id, double p, void* stream) {
+  MS_TRY(bind_device(dx));
+  // dx = g * mask / (1 - p): the same map as the forward, with the mask replayed
+  return dropout_launch(numel, dtype, g, dx, seed, stream_id, p, nullptr, (cudaStream_t)stream);
+}
+
+extern "C" size_t ms_layernorm_workspace(int64_t rows, int64_t dim, int32_t dtype) {
+  (void)rows;
+  (void)dtype;
+  return (size_t)(2 * dim * sizeof(float) + 255) & ~(size_t)255;
+}
+
+extern "C" ms_status ms_layernorm_fwd(int64_t rows, int64_t dim, int32_t dt, const void* x,
+                                      const void* w, const void* b, double eps, void* y,
+                                      float* mean, float* rstd, void* stream) {
+  MS_TRY(bind_device(y));
+  MS_CHECK_ARG(rows >= 0 && dim > 0 && dim < (1ll << 31), MS_ERR_SHAPE, "layernorm: bad shape");
+  if (rows == 0) return MS_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const void* ps[4] = {x, y, w, b};
+  const int kv = ln_kv(dim, dt, ps, 4);
+  const int D = (int)dim;
+  if (kv > 0) {
+    const unsigned grid = (unsigned)((rows + LN_WARPS - 1) / LN_WARPS);
+    MS_DT_DISPATCH(dt, MS_KV_SWITCH(kv, (ln_fwd_vec<T, KV><<<grid, LN_WARPS * 32, 0, st>>>(
+                                            rows, D, (const T*)x, (const T*)w, (const T*)b,
+                                            (float)eps, (T*)y, mean, rstd))));
+  } else {
+    MS_CHECK_ARG(rows < (1ll << 31), MS_ERR_UNSUPPORTED, "layernorm: too many rows");
+    MS_DT_DISPATCH(dt, (ln_fwd_generic<T><<<(unsigned)rows, 256, 0, st>>>(
+                           rows, D, (const T*)x, (const T*)w, (const T*)b, (float)eps, (T*)y,
+                           mean, rstd)));
+  }
+  count_launch();
+  return launch_status("layernorm_fwd");
+}
+
+extern "C" ms_status ms_layernorm_bwd(int64_t rows, int64_t dim, int32_t dt, const void* g,
+                                      const void* x, const float* mean, const float* rstd,
+                                      const void* w, void* dx, void* dw, void* db, void* ws,
+                                      size_t ws_bytes, void* stream) {
+  MS_TRY(bind_device(g));
+  MS_CHECK_ARG(rows >= 0 && dim > 0 && dim < (1ll << 31), MS_ERR_SHAPE, "layernorm: bad shape");
+  MS_CHECK_ARG(x && mean && rstd, MS_ERR_SHAPE, "layernorm bwd: x / mean / rstd required");
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool wantp = dw || db;
+  float* acc = static_cast<float*>(ws);
+  if (wantp) {
+    MS_CHECK_ARG(ws && ws_bytes >= ms_layernorm_workspace(rows, dim, dt), MS_ERR_WORKSPACE,
+                 "layernorm bwd: workspace too small");
+    if (cudaMemsetAsync(acc, 0, 2 * dim * sizeof(float), st) != cudaSuccess)
+      return launch_status("layernorm memset");
+  }
+  if (rows > 0 && (dx || wantp)) {
+    const void* ps[4] = {g, x, w, dx};
+    const int kv = ln_kv(dim, dt, ps, 4);
+    const int D = (int)dim;
+    float* dwa = dw ? acc : nullptr;
+    float* dba = db ? acc + dim : nullptr;
+    if (kv > 0) {
+      int64_t grid = (rows + LN_WARPS - 1) / LN_WARPS;
+      if (wantp && grid > (int64_t)num_sms() * 4) grid = num_sms() * 4;  // amortise the atomics
+      if (grid > (1ll << 30)) grid = 1ll << 30;
+      const size_t smem = wantp ? 2 * D * sizeof(float) : 0;
+      MS_DT_DISPATCH(dt, MS_KV_SWITCH(kv, (ln_bwd_vec<T, KV><<<(unsigned)grid, LN_WARPS * 32,
+                                                              smem, st>>>(
+                                              rows, D, (const T*)g, (const T*)x, mean, rstd,
+                                              (const T*)w, (T*)dx, dwa, dba))));
+    } else {
+      MS_CHECK_ARG(rows < (1ll << 31), MS_ERR_UNSUPPORTED, "layernorm: too many rows");
+      MS_DT_DISPATCH(dt, (ln_bwd_generic<T><<<(unsigned)rows, 256, 0, st>>>(
+                             rows, D, (const T*)g, (const T*)x, mean, rstd, (const T*)w, (T*)dx,
+                             dwa, dba)));
+    }
+    count_launch();
+    MS_TRY(launch_status("layernorm_bwd"));
+  }
+  if (dw) MS_TRY(f32_to(acc, dw, dt, dim, nullptr, 0, st));
+  if (db) MS_TRY(f32_to(acc + dim, db, dt, dim, nullptr, 0, st));
+  return MS_OK;
+}

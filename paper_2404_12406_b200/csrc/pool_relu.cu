@@ -12,62 +12,16 @@
 //   -inf.  Backward is a gather: every input element checks the <= ceil(k/s)^2
 //   windows that contain it, so no atomics and a fully written dx.
 #include "misc.cuh"
+#include "vec.cuh"
 
 namespace ms {
 namespace {
-
-#define MS_DT_DISPATCH(dt, ...)                                    \
-  switch (dt) {                                                    \
-    case MS_F32: { using T = float; __VA_ARGS__; } break;          \
-    case MS_BF16: { using T = __nv_bfloat16; __VA_ARGS__; } break; \
-    case MS_F16: { using T = __half; __VA_ARGS__; } break;         \
-    default: set_error("bad dtype %d", dt); return MS_ERR_DTYPE;   \
-  }
 
 int grid_for(int64_t work) {
   int64_t b = (work + 255) / 256;
   const int64_t cap = (int64_t)num_sms() * 16;
   if (b > cap) b = cap;
   return (int)(b > 0 ? b : 1);
-}
-
-template <typename T>
-__device__ __forceinline__ void ld8(const T* p, float (&v)[8], bool vec) {
-  if (vec) {
-    if constexpr (sizeof(T) == 2) {
-      uint4 u = *reinterpret_cast<const uint4*>(p);
-      const T* e = reinterpret_cast<const T*>(&u);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) v[j] = IO<T>::ld(e + j);
-    } else {
-      float4 a = *reinterpret_cast<const float4*>(p);
-      float4 b = *reinterpret_cast<const float4*>(p + 4);
-      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
-      v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < 8; ++j) v[j] = IO<T>::ld(p + j);
-  }
-}
-
-template <typename T>
-__device__ __forceinline__ void st8(T* p, const float (&v)[8], bool vec) {
-  if (vec) {
-    if constexpr (sizeof(T) == 2) {
-      uint4 u;
-      T* e = reinterpret_cast<T*>(&u);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) e[j] = IO<T>::cvt(v[j]);
-      *reinterpret_cast<uint4*>(p) = u;
-    } else {
-      *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
-      *reinterpret_cast<float4*>(p + 4) = make_float4(v[4], v[5], v[6], v[7]);
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < 8; ++j) p[j] = IO<T>::cvt(v[j]);
-  }
 }
 
 // ---------------------------------------------------------------- ReLU

@@ -496,3 +496,273 @@ class _MaxPool2dFn(torch.autograd.Function):
 def max_pool2d(x, kernel_size, stride=None, padding=0):
     """Max pooling whose backward reads a 1-byte argmax map (SPEC.md forward_maxpool2d)."""
     return _MaxPool2dFn.apply(x, kernel_size, kernel_size if stride is None else stride, padding)
+
+
+# =============================================================== dropout (RNG replay)
+DROPOUT_STREAM_BASE = 1_000_000  # leantape.core.Rng.DROPOUT_STREAM_BASE (core.py:108)
+
+
+class _DropoutFn(torch.autograd.Function):
+    """MemSave Dropout (rules.py:103-106, MEMSAVE row): keeps only the 16-byte
+    RNG key (seed, stream) (saved.py:91-108, RngSeed) and regenerates the keep
+    mask in backward; the mask is the reference generator's
+    (Rng(seed, stream).uniform() >= p, core.py:100-124)."""
+
+    @staticmethod
+    def forward(ctx, x, p: float, seed: int, stream: int, inplace: bool):
+        out_rg = ctx.needs_input_grad[0]
+        ctx.key = (int(seed), int(stream), float(p))
+        key = torch.tensor([int(seed), int(stream)], dtype=torch.int64) if out_rg else None
+        if _is_meta(x):
+            ctx.save_for_backward(key)
+            return x.new_empty(x.shape)
+        _require_cuda("dropout", x)
+        fmt = _dense_format(x)
+        if fmt is None:
+            x = x.contiguous()
+            fmt = torch.contiguous_format
+            inplace = False
+        ctx.fmt = fmt
+        y = x if inplace else torch.empty_like(x, memory_format=fmt)
+        L = _lib.lib()
+        _lib.check(L.ms_dropout_fwd(x.numel(), _dtype_code(x), _ptr(x), _ptr(y), seed, stream, p,
+                                    None, _stream(x.device)), "ms_dropout_fwd")
+        if inplace:
+            ctx.mark_dirty(x)
+        ctx.save_for_backward(key)
+        return y
+
+    @staticmethod
+    def backward(ctx, gy):
+        (key,) = ctx.saved_tensors
+        if not ctx.needs_input_grad[0]:
+            return None, None, None, None, None
+        _need(key, "seed", "dropout dX")
+        seed, stream, p = ctx.key
+        if _is_meta(gy):
+            return gy.new_empty(gy.shape), None, None, None, None
+        g = gy.contiguous(memory_format=ctx.fmt)
+        dx = torch.empty_like(g, memory_format=ctx.fmt)
+        L = _lib.lib()
+        _lib.check(L.ms_dropout_bwd(g.numel(), _dtype_code(g), _ptr(g), _ptr(dx), seed, stream, p,
+                                    _stream(g.device)), "ms_dropout_bwd")
+        return dx, None, None, None, None
+
+
+def draw_seed() -> int:
+    """A fresh 62-bit dropout seed from torch's default CPU generator (so
+    ``torch.manual_seed`` makes runs reproducible)."""
+    return int(torch.randint(0, 2 ** 62, (1,)).item())
+
+
+def dropout(x: torch.Tensor, p: float = 0.5, training: bool = True, inplace: bool = False,
+            seed: int | None = None, stream: int = DROPOUT_STREAM_BASE) -> torch.Tensor:
+    """Dropout whose backward replays the mask from its RNG key (SPEC.md
+    forward_dropout, RngReplay variant)."""
+    if not 0.0 <= p < 1.0:
+        raise ValueError(f"dropout probability has to be in [0, 1), got {p}")
+    if not training or p == 0.0:
+        return x
+    return _DropoutFn.apply(x, float(p), draw_seed() if seed is None else int(seed), int(stream),
+                            inplace)
+
+
+# =============================================================== layernorm
+class _LayerNormFn(torch.autograd.Function):
+    """LayerNorm over the trailing ``normalized_shape`` dims (rules.py:89-96,
+    identical under both policies): keeps x and the per-row (mean, rstd) iff x
+    or w needs a gradient, and w iff x does; db reads nothing."""
+
+    @staticmethod
+    def forward(ctx, x, normalized_shape, weight, bias, eps):
+        x_rg, w_rg = ctx.needs_input_grad[0], ctx.needs_input_grad[2]
+        nshape = tuple(int(s) for s in normalized_shape)
+        if tuple(x.shape[x.dim() - len(nshape):]) != nshape:
+            raise RuntimeError(f"layer_norm: input {tuple(x.shape)} does not end with {nshape}")
+        dim = 1
+        for s in nshape:
+            dim *= s
+        rows = x.numel() // dim if dim else 0
+        ctx.dims = (rows, dim, tuple(x.shape))
+        ctx.nshape = nshape
+        ctx.p_dtypes = (None if weight is None else weight.dtype,
+                        None if bias is None else bias.dtype)
+        keep_x = x_rg or w_rg
+        if _is_meta(x):
+            mean = torch.empty(rows, dtype=torch.float32, device="meta") if keep_x else None
+            rstd = torch.empty(rows, dtype=torch.float32, device="meta") if keep_x else None
+            ctx.save_for_backward(x if keep_x else None, mean, rstd, weight if x_rg else None)
+            return x.new_empty(x.shape)
+        _require_cuda("layer_norm", x, weight, bias)
+        xc = x.contiguous()
+        w = None if weight is None else weight.to(x.dtype).contiguous()
+        b = None if bias is None else bias.to(x.dtype).contiguous()
+        y = torch.empty_like(xc)
+        mean = torch.empty(rows, dtype=torch.float32, device=x.device) if keep_x else None
+        rstd = torch.empty(rows, dtype=torch.float32, device=x.device) if keep_x else None
+        L = _lib.lib()
+        _lib.check(L.ms_layernorm_fwd(rows, dim, _dtype_code(x), _ptr(xc), _ptr(w), _ptr(b),
+                                      float(eps), _ptr(y), _ptr(mean), _ptr(rstd),
+                                      _stream(x.device)), "ms_layernorm_fwd")
+        ctx.save_for_backward(xc if keep_x else None, mean, rstd, w if x_rg else None)
+        return y
+
+    @staticmethod
+    def backward(ctx, gy):
+        x, mean, rstd, w = ctx.saved_tensors
+        need_x, need_w, need_b = (ctx.needs_input_grad[0], ctx.needs_input_grad[2],
+                                  ctx.needs_input_grad[3])
+        rows, dim, shape = ctx.dims
+        w_dt, b_dt = ctx.p_dtypes
+        dx = dw = db = None
+        if _is_meta(gy):
+            if need_x:
+                _need(x, "x", "layer_norm dX")
+                dx = gy.new_empty(shape)
+            if need_w:
+                _need(x, "x", "layer_norm dW")
+                dw = torch.empty(ctx.nshape, dtype=w_dt, device="meta")
+            if need_b:
+                db = torch.empty(ctx.nshape, dtype=b_dt, device="meta")
+            return dx, None, dw, db, None
+        g = gy.contiguous()
+        dt = _dtype_code(g)
+        L = _lib.lib()
+        st = _stream(g.device)
+        if need_x or need_w:
+            x = _need(x, "x", "layer_norm dX/dW")
+            _need(mean, "stats", "layer_norm dX/dW")
+            if need_x and ctx.p_dtypes[0] is not None:
+                _need(w, "w", "layer_norm dX")
+            dx = torch.empty_like(g) if need_x else None
+            dwt = torch.empty(dim, dtype=g.dtype, device=g.device) if need_w else None
+            dbt = torch.empty(dim, dtype=g.dtype, device=g.device) if need_b else None
+            ws, nb = _workspace(L.ms_layernorm_workspace(rows, dim, dt) if (need_w or need_b)
+                                else 0, g.device)
+            _lib.check(L.ms_layernorm_bwd(rows, dim, dt, _ptr(g), _ptr(x), _ptr(mean), _ptr(rstd),
+                                          _ptr(w), _ptr(dx), _ptr(dwt), _ptr(dbt), _ptr(ws), nb,
+                                          st), "ms_layernorm_bwd")
+            dw, db = dwt, dbt
+        elif need_b:  # db = sum_rows g: nothing saved is read
+            db = torch.empty(dim, dtype=g.dtype, device=g.device)
+            ws, nb = _workspace(L.ms_bias_grad_workspace(rows, dim, dt), g.device)
+            _lib.check(L.ms_bias_grad(rows, dim, dt, _ptr(g), _ptr(db), _ptr(ws), nb, st),
+                       "ms_bias_grad")
+        if dw is not None:
+            dw = dw.view(ctx.nshape).to(w_dt)
+        if db is not None:
+            db = db.view(ctx.nshape).to(b_dt)
+        if dx is not None:
+            dx = dx.view(shape)
+        return dx, None, dw, db, None
+
+
+def layer_norm(x, normalized_shape, weight=None, bias=None, eps: float = 1e-5):
+    """``F.layer_norm`` on the sm_100a kernels (SPEC.md forward_layernorm)."""
+    if isinstance(normalized_shape, int):
+        normalized_shape = (normalized_shape,)
+    return _LayerNormFn.apply(x, tuple(normalized_shape), weight, bias, eps)
+
+
+# =============================================================== conv_transpose2d
+class _ConvTranspose2dFn(torch.autograd.Function):
+    """ConvTranspose2d (rules.py:68-71, MEMSAVE row = linear family; SPEC.md
+    forward_conv_transpose2d).  Its forward is the input-VJP of the conv2d
+    whose weight it shares ([C_in][C_out][kh][kw] = conv [K][C][R][S]), its dX
+    is that conv's forward and its dW the conv's weight-VJP with the operand
+    roles swapped, so it runs on the same kernels (ms_conv2d_dx / _fwd / _dw)."""
+
+    @staticmethod
+    def forward(ctx, x, weight, bias, stride, padding, output_padding):
+        x_rg, w_rg = ctx.needs_input_grad[0], ctx.needs_input_grad[1]
+        roles = saved_roles(x_rg, w_rg)
+        stride, padding, opad = _pair(stride), _pair(padding), _pair(output_padding)
+        if x.dim() != 4 or weight.dim() != 4:
+            raise RuntimeError("conv_transpose2d: expected 4-d input and weight")
+        n, cin, h, w_ = x.shape
+        if weight.shape[0] != cin:
+            raise RuntimeError(f"conv_transpose2d: input channels {cin} != weight.shape[0] "
+                               f"{weight.shape[0]} (groups unsupported)")
+        cout, kh, kw = weight.shape[1], weight.shape[2], weight.shape[3]
+        ho = (h - 1) * stride[0] - 2 * padding[0] + kh + opad[0]
+        wo = (w_ - 1) * stride[1] - 2 * padding[1] + kw + opad[1]
+        if ho <= 0 or wo <= 0 or opad[0] >= max(stride[0], 1) or opad[1] >= max(stride[1], 1):
+            raise RuntimeError("conv_transpose2d: invalid output size / output_padding")
+        # the equivalent conv2d: input (n, cout, ho, wo) -> output (n, cin, h, w)
+        conv_x = (n, cout, ho, wo)
+        ctx.geom = (conv_x, tuple(weight.shape), stride, padding, tuple(x.shape))
+        ctx.w_meta = weight.dtype
+        if _is_meta(x, weight):
+            ctx.save_for_backward(x if "x" in roles else None, weight if "w" in roles else None)
+            ctx.layouts = (_lib.MS_NCHW, _lib.MS_NCHW)
+            return x.new_empty(conv_x)
+        _require_cuda("conv_transpose2d", x, weight, bias)
+        if weight.dtype != x.dtype:
+            raise TypeError(f"conv_transpose2d: input dtype {x.dtype} != weight dtype "
+                            f"{weight.dtype}")
+        layout, wlayout = _conv_layouts(x, weight)
+        xl = _as_layout(x, layout)
+        wl = _as_layout(weight, wlayout)
+        ctx.layouts = (layout, wlayout)
+        ctx.save_for_backward(xl if "x" in roles else None, wl if "w" in roles else None)
+        dt = _dtype_code(x)
+        d = _conv_desc(conv_x, (cin, cout, kh, kw), stride, padding, layout, wlayout, dt)
+        y = _empty4(conv_x, x, layout)
+        L = _lib.lib()
+        st = _stream(x.device)
+        b = None if bias is None else bias.to(x.dtype).contiguous()
+        ws, nb = _workspace(L.ms_conv2d_workspace(ctypes.byref(d), _lib.MS_CONV_DX), x.device)
+        _lib.check(L.ms_conv_transpose2d_fwd(ctypes.byref(d), _ptr(xl), _ptr(wl), _ptr(b), _ptr(y),
+                                             _ptr(ws), nb, st), "ms_conv_transpose2d_fwd")
+        return y
+
+    @staticmethod
+    def backward(ctx, gy):
+        x, w = ctx.saved_tensors
+        need_x, need_w, need_b = ctx.needs_input_grad[:3]
+        conv_x, w_shape, stride, padding, x_shape = ctx.geom
+        dx = dw = db = None
+        if _is_meta(gy):
+            if need_x:
+                _need(w, "w", "conv_transpose2d dX")
+                dx = gy.new_empty(x_shape)
+            if need_w:
+                _need(x, "x", "conv_transpose2d dW")
+                dw = gy.new_empty(w_shape)
+            if need_b:
+                db = gy.new_empty((w_shape[1],))
+            return dx, dw, db, None, None, None
+        layout, wlayout = ctx.layouts
+        g = _as_layout(gy, layout)
+        dt = _dtype_code(g)
+        cin, cout, kh, kw = w_shape
+        d = _conv_desc(conv_x, (cin, cout, kh, kw), stride, padding, layout, wlayout, dt)
+        L = _lib.lib()
+        st = _stream(g.device)
+        if need_x:  # dX = conv2d(g, W)
+            w = _need(w, "w", "conv_transpose2d dX")
+            dx = _empty4(x_shape, g, layout)
+            ws, nb = _workspace(L.ms_conv2d_workspace(ctypes.byref(d), _lib.MS_CONV_FWD), g.device)
+            _lib.check(L.ms_conv2d_fwd(ctypes.byref(d), _ptr(g), _ptr(w), None, _ptr(dx),
+                                       _ptr(ws), nb, st), "ms_conv2d_fwd (conv_transpose2d dX)")
+        if need_w:  # dW = conv2d weight-VJP with the conv input g and conv output-grad x
+            x = _need(x, "x", "conv_transpose2d dW")
+            dw = torch.empty(w_shape, dtype=ctx.w_meta, device=g.device,
+                             memory_format=torch.channels_last if wlayout == _lib.MS_NHWC
+                             else torch.contiguous_format)
+            ws, nb = _workspace(L.ms_conv2d_workspace(ctypes.byref(d), _lib.MS_CONV_DW), g.device)
+            _lib.check(L.ms_conv2d_dw(ctypes.byref(d), _ptr(g), _ptr(x), _ptr(dw), _ptr(ws), nb,
+                                      st), "ms_conv2d_dw (conv_transpose2d dW)")
+        if need_b:  # sum of g over (n, h, w) per output channel
+            n, c, h, w_ = conv_x
+            dd = _lib.ConvDesc(n, c, h, w_, c, 1, 1, 1, 1, 0, 0, layout, wlayout, dt)
+            db = torch.empty((cout,), dtype=g.dtype, device=g.device)
+            ws, nb = _workspace(4 * cout, g.device)
+            _lib.check(L.ms_conv2d_db(ctypes.byref(dd), _ptr(g), _ptr(db), _ptr(ws), nb, st),
+                       "ms_conv2d_db (conv_transpose2d db)")
+        return dx, dw, db, None, None, None
+
+
+def conv_transpose2d(x, weight, bias=None, stride=1, padding=0, output_padding=0):
+    """Differentiability-agnostic ``F.conv_transpose2d`` (groups = dilation = 1)."""
+    return _ConvTranspose2dFn.apply(x, weight, bias, stride, padding, output_padding)

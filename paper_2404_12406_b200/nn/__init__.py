@@ -17,7 +17,8 @@ from torch import nn
 from .. import functional as MF
 
 __all__ = ["MemSaveLinear", "MemSaveConv2d", "MemSaveBatchNorm2d", "MemSaveReLU",
-           "MemSaveMaxPool2d", "convert_to_memory_saving"]
+           "MemSaveMaxPool2d", "MemSaveDropout", "MemSaveLayerNorm", "MemSaveConvTranspose2d",
+           "convert_to_memory_saving"]
 
 
 def _share_params(dst: nn.Module, src: nn.Module, clone: bool) -> None:
@@ -152,13 +153,91 @@ class MemSaveMaxPool2d(nn.MaxPool2d):
         return m
 
 
+class MemSaveDropout(nn.Dropout):
+    """nn.Dropout that keeps only its 16-byte RNG key for backward and replays
+    the mask (rules.py:103-106, MEMSAVE row; saved.py:91-108).  The mask of a
+    call is Rng(seed, stream).uniform() >= p of the reference generator, with a
+    fresh seed per call from torch's default CPU generator and the stream
+    ``DROPOUT_STREAM_BASE + node`` (core.py:104-108)."""
+
+    def __init__(self, p: float = 0.5, inplace: bool = False, node: int = 0):
+        super().__init__(p, inplace)
+        self.node = int(node)
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        return MF.dropout(x, self.p, self.training, self.inplace,
+                          stream=MF.DROPOUT_STREAM_BASE + self.node)
+
+    @classmethod
+    def from_nn_Dropout(cls, do: nn.Dropout, node: int = 0) -> "MemSaveDropout":
+        m = cls(do.p, do.inplace, node)
+        m.train(do.training)
+        return m
+
+
+class MemSaveLayerNorm(nn.LayerNorm):
+    """nn.LayerNorm on the sm_100a kernels.  Its storage rule is the same under
+    both policies (rules.py:89-96: x + per-row stats iff x or w needs a grad, w
+    iff x does); db reads nothing."""
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        return MF.layer_norm(x, self.normalized_shape, self.weight, self.bias, self.eps)
+
+    @classmethod
+    def from_nn_LayerNorm(cls, ln: nn.LayerNorm, clone_params: bool = False) -> "MemSaveLayerNorm":
+        kw = {}
+        if "bias" in nn.LayerNorm.__init__.__code__.co_varnames:
+            kw["bias"] = ln.bias is not None
+        m = cls(ln.normalized_shape, eps=ln.eps, elementwise_affine=ln.elementwise_affine,
+                device="meta", dtype=(ln.weight.dtype if ln.weight is not None else None), **kw)
+        _share_params(m, ln, clone_params)
+        return m
+
+
+def conv_transpose2d_supported(ct: nn.ConvTranspose2d) -> bool:
+    d = ct.dilation if isinstance(ct.dilation, tuple) else (ct.dilation, ct.dilation)
+    return (ct.groups == 1 and tuple(d) == (1, 1) and ct.padding_mode == "zeros"
+            and not isinstance(ct.padding, str))
+
+
+class MemSaveConvTranspose2d(nn.ConvTranspose2d):
+    """nn.ConvTranspose2d with the linear-family storage rule (rules.py:68-71,
+    MEMSAVE): X only if W needs a grad, W only if X needs one."""
+
+    def forward(self, x: torch.Tensor, output_size=None) -> torch.Tensor:
+        if not conv_transpose2d_supported(self):
+            raise NotImplementedError("MemSaveConvTranspose2d supports groups=1, dilation=1, "
+                                      "zeros padding only")
+        opad = self._output_padding(x, output_size, self.stride, self.padding, self.kernel_size,
+                                    2, self.dilation)
+        return MF.conv_transpose2d(x, self.weight, self.bias, self.stride, self.padding, opad)
+
+    @classmethod
+    def from_nn_ConvTranspose2d(cls, ct: nn.ConvTranspose2d,
+                                clone_params: bool = False) -> "MemSaveConvTranspose2d":
+        m = cls(ct.in_channels, ct.out_channels, ct.kernel_size, stride=ct.stride,
+                padding=ct.padding, output_padding=ct.output_padding, groups=ct.groups,
+                bias=ct.bias is not None, dilation=ct.dilation, padding_mode=ct.padding_mode,
+                device="meta", dtype=ct.weight.dtype)
+        _share_params(m, ct, clone_params)
+        return m
+
+
 _MEMSAVE_TYPES = (MemSaveLinear, MemSaveConv2d, MemSaveBatchNorm2d, MemSaveReLU,
-                  MemSaveMaxPool2d)
+                  MemSaveMaxPool2d, MemSaveDropout, MemSaveLayerNorm, MemSaveConvTranspose2d)
 
 
-def _convert_one(mod: nn.Module, kinds: dict, clone_params: bool):
+def _convert_one(mod: nn.Module, kinds: dict, clone_params: bool, counter: list):
     if isinstance(mod, _MEMSAVE_TYPES):
         return None  # idempotent (SPEC.md:328)
+    if kinds.get("dropout") and type(mod) is nn.Dropout:
+        counter[0] += 1
+        return MemSaveDropout.from_nn_Dropout(mod, node=counter[0] - 1)
+    if kinds.get("layernorm") and type(mod) is nn.LayerNorm:
+        return MemSaveLayerNorm.from_nn_LayerNorm(mod, clone_params)
+    if (kinds.get("conv_transpose2d") and type(mod) is nn.ConvTranspose2d
+            and conv_transpose2d_supported(mod)):
+        return MemSaveConvTranspose2d.from_nn_ConvTranspose2d(mod, clone_params)
     if kinds.get("linear") and type(mod) is nn.Linear:
         return MemSaveLinear.from_nn_Linear(mod, clone_params)
     if kinds.get("conv2d") and type(mod) is nn.Conv2d and conv2d_supported(mod):
@@ -175,22 +254,25 @@ def _convert_one(mod: nn.Module, kinds: dict, clone_params: bool):
 def convert_to_memory_saving(model: nn.Module, linear: bool = True, conv2d: bool = True,
                              conv1d: bool = False, conv3d: bool = False,
                              batchnorm2d: bool = True, relu: bool = True,
-                             maxpool2d: bool = True, layernorm: bool = False,
-                             dropout: bool = False, verbose: bool = False,
-                             clone_params: bool = False) -> nn.Module:
+                             maxpool2d: bool = True, layernorm: bool = True,
+                             dropout: bool = True, conv_transpose2d: bool = True,
+                             verbose: bool = False, clone_params: bool = False) -> nn.Module:
     """Swap supported layers of ``model`` for their MemSave equivalents, in place.
 
     Mirrors the reference ``convert_network(net, target, layer_filter)``
     (SPEC.md:320-328): the boolean flags are the kind filter, conversion is
     idempotent, parameters are shared with the original modules unless
-    ``clone_params``.  ReLU (bit mask) and MaxPool2d (1-byte argmax) are the
-    first "next" rows of SURVEY.md §8(f); conv1d/3d, LayerNorm and Dropout are
-    accepted for API compatibility and left untouched.  Returns the (possibly
-    replaced) model.
+    ``clone_params``.  The SURVEY.md §8(f) rows ReLU (bit mask), MaxPool2d
+    (1-byte argmax), Dropout (RNG replay; node i of the traversal draws from
+    stream DROPOUT_STREAM_BASE + i), LayerNorm and ConvTranspose2d are swapped
+    too; conv1d/3d are accepted for API compatibility and left untouched.
+    Returns the (possibly replaced) model.
     """
     kinds = {"linear": linear, "conv2d": conv2d, "batchnorm2d": batchnorm2d, "relu": relu,
-             "maxpool2d": maxpool2d}
-    top = _convert_one(model, kinds, clone_params)
+             "maxpool2d": maxpool2d, "layernorm": layernorm, "dropout": dropout,
+             "conv_transpose2d": conv_transpose2d}
+    counter = [0]
+    top = _convert_one(model, kinds, clone_params, counter)
     if top is not None:
         if verbose:
             print(f"memsave: {type(model).__name__} -> {type(top).__name__}")
@@ -198,7 +280,7 @@ def convert_to_memory_saving(model: nn.Module, linear: bool = True, conv2d: bool
 
     def walk(parent: nn.Module, prefix: str):
         for name, child in list(parent.named_children()):
-            new = _convert_one(child, kinds, clone_params)
+            new = _convert_one(child, kinds, clone_params, counter)
             if new is not None:
                 setattr(parent, name, new)
                 if verbose:

@@ -52,3 +52,17 @@ def kat_golden():
     with open(os.path.join(GOLDEN, "kat.json")) as f:
         return json.load(f)
 
+
+@pytest.fixture(scope="session")
+def dropout_golden():
+    return dict(np.load(os.path.join(GOLDEN, "dropout_ref.npz")))
+
+
+@pytest.fixture(scope="session")
+def ln_golden():
+    return dict(np.load(os.path.join(GOLDEN, "layernorm_spec.npz")))
+
+
+@pytest.fixture(scope="session")
+def convt_golden():
+    return dict(np.load(os.path.join(GOLDEN, "conv_transpose_ref.npz")))

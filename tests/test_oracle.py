@@ -118,3 +118,78 @@ def test_relu_known_answers():
     assert oracle.relu_bwd(np.ones(4), mask).tolist() == [0, 1, 0, 1]
     # BitMask byte cost for numel 10^6: 125000 B (SPEC.md, "32x reduction")
     assert (10**6 + 7) // 8 == 125000
+
+
+# ---------------------------------------------------------------- dropout (RNG replay)
+@pytest.mark.parametrize("seed,stream,n", [(0, 1_000_000, 13), (12345, 1_000_003, 40),
+                                           (2 ** 62 + 5, 7, 9)])
+def test_philox_restatement_matches_reference_generator(seed, stream, n):
+    # the reference Rng is numpy's Philox4x64-10 (core.py:100-124); the block
+    # function restated in oracle/dropout.py must reproduce its doubles bit for bit
+    from oracle import dropout as od
+    np.testing.assert_array_equal(od.uniforms_restated(seed, stream, n),
+                                  od.uniforms(seed, stream, n))
+
+
+@pytest.mark.parametrize("case", ["d_small", "d_half", "d_big"])
+def test_dropout_oracle_matches_reference_masks(dropout_golden, case):
+    g = dropout_golden
+    seed, stream = (int(v) for v in g[f"{case}/key"])
+    p = float(g[f"{case}/p"])
+    mask = g[f"{case}/mask"].astype(bool)
+    np.testing.assert_array_equal(oracle.dropout_mask(seed, stream, p, mask.size), mask)
+    x = np.linspace(-2, 2, mask.size)
+    y, m = oracle.dropout_fwd(x, seed, stream, p)
+    np.testing.assert_array_equal(m, mask)
+    np.testing.assert_allclose(y, np.where(mask, x / (1 - p), 0.0), rtol=0, atol=0)
+    # replay: the backward mask is the forward mask (SPEC.md acceptance 6)
+    np.testing.assert_array_equal(oracle.dropout_bwd(np.ones(mask.size), seed, stream, p) != 0,
+                                  mask)
+
+
+def test_dropout_p0_is_identity():
+    x = np.arange(10.0)
+    y, m = oracle.dropout_fwd(x, 3, 1_000_000, 0.0)
+    assert m.all() and np.array_equal(y, x)
+
+
+# ---------------------------------------------------------------- layernorm
+@pytest.mark.parametrize("case", ["ln_small", "ln_3d"])
+def test_layernorm_oracle_matches_spec_vectors(ln_golden, case):
+    g = ln_golden
+    x, w, b, gy = g[f"{case}/x"], g[f"{case}/w"], g[f"{case}/b"], g[f"{case}/g"]
+    d = w.size
+    y, mean, rstd = oracle.layernorm_fwd(x, w, b, 1e-5, d)
+    np.testing.assert_allclose(y, g[f"{case}/y"], rtol=1e-12, atol=1e-12)
+    dx, dw, db = oracle.layernorm_bwd(gy, x, w, 1e-5, d)
+    np.testing.assert_allclose(dx, g[f"{case}/dx"], rtol=1e-10, atol=1e-12)
+    np.testing.assert_allclose(dw, g[f"{case}/dw"], rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(db, g[f"{case}/db"], rtol=1e-12, atol=1e-12)
+
+
+def test_layernorm_constant_row_kat():
+    # SPEC.md forward_layernorm: a constant input row normalises to 0 (then *w + b)
+    y, _m, _r = oracle.layernorm_fwd(np.full((2, 6), 3.5), np.full(6, 2.0), np.full(6, 0.25),
+                                     1e-5, 6)
+    np.testing.assert_allclose(y, 0.25, atol=1e-12)
+
+
+# ---------------------------------------------------------------- conv_transpose2d
+@pytest.mark.parametrize("case", ["ct_s2", "ct_s1"])
+def test_conv_transpose_oracle_matches_reference_kernels(convt_golden, case):
+    g = convt_golden
+    s, p = (int(v) for v in g[f"{case}/geom"])
+    x, w, gy = g[f"{case}/x"], g[f"{case}/w"], g[f"{case}/g"]
+    np.testing.assert_allclose(oracle.conv_transpose2d_fwd(x, w, None, s, p), g[f"{case}/y"],
+                               rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(oracle.conv_transpose2d_dx(gy, w, s, p), g[f"{case}/dx"],
+                               rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(oracle.conv_transpose2d_dw(x, gy, s, p, w.shape[2], w.shape[3]),
+                               g[f"{case}/dw"], rtol=1e-11, atol=1e-11)
+
+
+def test_conv_transpose_unit_kernel_kat():
+    # SPEC.md forward_conv_transpose2d: 1x1 unit kernel, stride 1 -> Z = X
+    x = np.arange(12.0).reshape(1, 1, 3, 4)
+    np.testing.assert_array_equal(oracle.conv_transpose2d_fwd(x, np.ones((1, 1, 1, 1)), None, 1, 0),
+                                  x)

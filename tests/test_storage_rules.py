@@ -165,3 +165,70 @@ def test_maxpool_saved_set_is_an_index_map(rules_golden, x_rg):
         out.sum().backward()
     else:
         assert packed == []
+
+
+# =============================================================== §8(f) rows
+@pytest.mark.parametrize("x_rg", [False, True])
+def test_dropout_saved_set_is_a_16_byte_key(rules_golden, x_rg):
+    x = _make((4, 6, 10), x_rg)
+    packed = []
+
+    def pack(t):
+        packed.append((tuple(t.shape), t.dtype, t.numel() * t.element_size()))
+        return t
+
+    with torch.autograd.graph.saved_tensors_hooks(pack, lambda t: t):
+        out = MF.dropout(x, 0.3, True, seed=5, stream=MF.DROPOUT_STREAM_BASE + 2)
+    exp = _golden_saves(rules_golden, "dropout", x_rg, False, False)
+    assert exp == (["seed"] if x_rg else [])
+    if x_rg:
+        # RngSeed: <= 16 bytes regardless of the tensor size (saved.py:91-108)
+        assert packed == [((2,), torch.int64, 16)]
+        out.sum().backward()
+        assert x.grad.shape == x.shape
+    else:
+        assert packed == []
+
+
+def test_dropout_eval_and_p0_are_identity():
+    x = _make((3, 4), True)
+    assert MF.dropout(x, 0.5, training=False) is x
+    assert MF.dropout(x, 0.0, training=True) is x
+    with pytest.raises(ValueError):
+        MF.dropout(x, 1.0)
+
+
+@pytest.mark.parametrize("x_rg,w_rg,b_rg", FLAGS)
+def test_layernorm_saved_set(rules_golden, x_rg, w_rg, b_rg):
+    x, w, b = _make((3, 5, 8), x_rg), _make((8,), w_rg), _make((8,), b_rg)
+    packed = []
+
+    def pack(t):
+        packed.append((tuple(t.shape), t.dtype))
+        return t
+
+    with torch.autograd.graph.saved_tensors_hooks(pack, lambda t: t):
+        out = MF.layer_norm(x, (8,), w, b, 1e-5)
+    role = {((3, 5, 8), torch.float32): "x", ((8,), torch.float32): "w",
+            ((15,), torch.float32): "stats"}
+    roles = sorted(set(role[p] for p in packed))
+    assert roles == sorted(set(_golden_saves(rules_golden, "layernorm", x_rg, w_rg, b_rg)))
+    if "stats" in roles:
+        assert sum(1 for p in packed if role[p] == "stats") == 2  # mean and rstd per row
+    if out.requires_grad:
+        out.sum().backward()
+        assert (x.grad is not None) == x_rg and (w.grad is not None) == w_rg
+        assert (b.grad is not None) == b_rg
+
+
+@pytest.mark.parametrize("x_rg,w_rg,b_rg", FLAGS)
+def test_conv_transpose2d_saved_set(rules_golden, x_rg, w_rg, b_rg):
+    x, w, b = _make((2, 4, 5, 5), x_rg), _make((4, 6, 3, 3), w_rg), _make((6,), b_rg)
+    out, roles = _run(lambda *t: MF.conv_transpose2d(*t, stride=2, padding=1), (x, w, b),
+                      {(2, 4, 5, 5): "x", (4, 6, 3, 3): "w"})
+    assert roles == _golden_saves(rules_golden, "conv_transpose2d", x_rg, w_rg, b_rg)
+    assert out.shape == (2, 6, 9, 9)
+    if out.requires_grad:
+        out.sum().backward()
+        assert (x.grad is not None) == x_rg and (w.grad is not None) == w_rg
+        assert (b.grad is not None) == b_rg
