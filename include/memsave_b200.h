@@ -168,18 +168,26 @@ MS_API ms_status ms_conv_transpose2d_fwd(const ms_conv_desc* d, const void* x, c
 
 /* ------------------------------------------------------------ dropout (RNG replay)
  * MemSave Dropout (rules.py:103-106, saved.py:91-108 RngSeed; SPEC.md
- * forward_dropout): element i is kept iff U_i >= p, U_i the i-th double of the
- * reference generator leantape.core.Rng(seed, stream_id).uniform()
- * (core.py:100-124: numpy Philox4x64-10, key [seed, stream_id]); kept
- * elements are scaled by 1/(1-p).  Backward regenerates the same mask from
- * (seed, stream_id, p): nothing O(numel) is stored.  mask_or_null receives the
- * keep flags at one byte per element (the NAIVE StoreMask convention, tests).
- * y may alias x; dx may alias g; 0 <= p < 1.                                */
+ * forward_dropout): the keep mask is a pure function of (seed, stream_id, p,
+ * element index); kept elements are scaled by 1/(1-p).  Backward regenerates
+ * the same mask: nothing O(numel) is stored.  Generators:
+ *   MS_RNG_PHILOX4X32      Philox4x32-10 (Random123), key = seed, counter =
+ *                          (block, stream_id); element 4j+i kept iff word i of
+ *                          block j >= ceil(p * 2^32).  Near HBM speed.
+ *   MS_RNG_PHILOX4X64_REF  the reference generator leantape.core.Rng(seed,
+ *                          stream_id).uniform() (core.py:100-124; numpy
+ *                          Philox4x64-10 keyed [seed, stream_id]); element i
+ *                          kept iff U_i >= p: bit-identical to the reference's
+ *                          mask (seeds < 2^63).  ~4x the integer work.
+ * mask_or_null receives the keep flags at one byte per element (the NAIVE
+ * StoreMask convention, tests).  y may alias x; dx may alias g; 0 <= p < 1. */
+typedef enum { MS_RNG_PHILOX4X32 = 0, MS_RNG_PHILOX4X64_REF = 1 } ms_rng;
 MS_API ms_status ms_dropout_fwd(int64_t numel, int32_t dtype, const void* x, void* y,
-                                uint64_t seed, uint64_t stream_id, double p, void* mask_or_null,
-                                void* stream);
+                                uint64_t seed, uint64_t stream_id, double p, int32_t generator,
+                                void* mask_or_null, void* stream);
 MS_API ms_status ms_dropout_bwd(int64_t numel, int32_t dtype, const void* g, void* dx,
-                                uint64_t seed, uint64_t stream_id, double p, void* stream);
+                                uint64_t seed, uint64_t stream_id, double p, int32_t generator,
+                                void* stream);
 
 /* ------------------------------------------------------------ layernorm
  * LayerNorm over the last dimension (rules.py:89-96; SPEC.md forward_layernorm):

@@ -10,6 +10,8 @@ MemSave variant keep only the key (saved.py:91-108).
 ``philox4x64_10`` restates the generator block function independently of
 numpy (counter incremented before each block, so element i uses word i % 4 of
 block i // 4 + 1); tests pin it against ``np.random.Philox`` itself.
+``philox4x32_10`` restates the product's default (cheaper) generator, pinned
+against the Random123 known-answer vectors.
 """
 
 from __future__ import annotations
@@ -46,16 +48,50 @@ def uniforms(seed: int, stream: int, n: int) -> np.ndarray:
     return np.random.Generator(np.random.Philox(key=[seed, stream])).random(n)
 
 
-def dropout_mask(seed: int, stream: int, p: float, n: int) -> np.ndarray:
-    return uniforms(seed, stream, n) >= p
+def philox4x32_10(ctr, key):
+    """Philox4x32-10 (Salmon et al. 2011, Random123), vectorised over blocks:
+    ctr is a (4, B) uint64 array of 32-bit words, key a pair of 32-bit words."""
+    m0, m1 = np.uint64(0xD2511F53), np.uint64(0xCD9E8D57)
+    w0, w1 = 0x9E3779B9, 0xBB67AE85
+    lo32 = np.uint64(0xFFFFFFFF)
+    c = [np.asarray(v, dtype=np.uint64) & lo32 for v in ctr]
+    k0, k1 = int(key[0]) & 0xFFFFFFFF, int(key[1]) & 0xFFFFFFFF
+    for r in range(10):
+        if r:
+            k0, k1 = (k0 + w0) & 0xFFFFFFFF, (k1 + w1) & 0xFFFFFFFF
+        p0, p1 = m0 * c[0], m1 * c[2]  # < 2^64: exact in uint64
+        c = [(p1 >> np.uint64(32)) ^ c[1] ^ np.uint64(k0), p1 & lo32,
+             (p0 >> np.uint64(32)) ^ c[3] ^ np.uint64(k1), p0 & lo32]
+    return c
 
 
-def dropout_fwd(x, seed: int, stream: int, p: float):
+def words_philox4x32(seed: int, stream: int, n: int) -> np.ndarray:
+    """The product's default generator (include/memsave_b200.h MS_RNG_PHILOX4X32):
+    key = seed (lo, hi), counter = (j lo, j hi, stream lo, stream hi) for block j;
+    element 4j + i takes word i."""
+    nb = (n + 3) // 4
+    j = np.arange(nb, dtype=np.uint64)
+    lo32 = np.uint64(0xFFFFFFFF)
+    ctr = [j & lo32, j >> np.uint64(32), np.full(nb, stream & 0xFFFFFFFF, np.uint64),
+           np.full(nb, (stream >> 32) & 0xFFFFFFFF, np.uint64)]
+    c = philox4x32_10(ctr, (seed & 0xFFFFFFFF, (seed >> 32) & 0xFFFFFFFF))
+    return np.stack(c, axis=1).reshape(-1)[:n]
+
+
+def dropout_mask(seed: int, stream: int, p: float, n: int,
+                 generator: str = "reference") -> np.ndarray:
+    if generator == "reference":
+        return uniforms(seed, stream, n) >= p
+    import math
+    return words_philox4x32(seed, stream, n) >= np.uint64(math.ceil(p * 2.0 ** 32))
+
+
+def dropout_fwd(x, seed: int, stream: int, p: float, generator: str = "reference"):
     x = np.asarray(x, dtype=np.float64)
-    m = dropout_mask(seed, stream, p, x.size).reshape(x.shape)
+    m = dropout_mask(seed, stream, p, x.size, generator).reshape(x.shape)
     return np.where(m, x / (1.0 - p), 0.0), m
 
 
-def dropout_bwd(g, seed: int, stream: int, p: float):
+def dropout_bwd(g, seed: int, stream: int, p: float, generator: str = "reference"):
     """dX = G ⊙ mask / (1 − p) with the mask replayed from the key."""
-    return dropout_fwd(g, seed, stream, p)[0]
+    return dropout_fwd(g, seed, stream, p, generator)[0]

@@ -17,6 +17,7 @@ LIB_PATH = os.path.join(_HERE, "libmemsave_b200.so")
 MS_F32, MS_BF16, MS_F16 = 0, 1, 2
 MS_NCHW, MS_NHWC = 0, 1
 MS_CONV_FWD, MS_CONV_DX, MS_CONV_DW = 0, 1, 2
+MS_RNG_PHILOX4X32, MS_RNG_PHILOX4X64_REF = 0, 1
 
 _c_i64 = ctypes.c_int64
 _c_i32 = ctypes.c_int32
@@ -71,9 +72,9 @@ SIGNATURES = {
     "ms_conv_transpose2d_fwd": (_c_i32, [ctypes.POINTER(ConvDesc), _vp, _vp, _vp, _vp, _vp, _c_sz,
                                          _vp]),
     "ms_dropout_fwd": (_c_i32, [_c_i64, _c_i32, _vp, _vp, ctypes.c_uint64, ctypes.c_uint64,
-                                ctypes.c_double, _vp, _vp]),
+                                ctypes.c_double, _c_i32, _vp, _vp]),
     "ms_dropout_bwd": (_c_i32, [_c_i64, _c_i32, _vp, _vp, ctypes.c_uint64, ctypes.c_uint64,
-                                ctypes.c_double, _vp]),
+                                ctypes.c_double, _c_i32, _vp]),
     "ms_layernorm_workspace": (_c_sz, [_c_i64, _c_i64, _c_i32]),
     "ms_layernorm_fwd": (_c_i32, [_c_i64, _c_i64, _c_i32, _vp, _vp, _vp, ctypes.c_double, _vp,
                                   _vp, _vp, _vp]),

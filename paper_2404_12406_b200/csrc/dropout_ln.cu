@@ -2,8 +2,17 @@
 //
 // Dropout (rules.py:103-106 MEMSAVE row, saved.py:91-108 RngSeed, SPEC.md
 // forward_dropout): the keep mask is a pure function of (seed, stream, element
-// index), so backward regenerates it instead of reading a stored mask.  The
-// generator is the reference's own: leantape.core.Rng(seed, stream).uniform()
+// index), so backward regenerates it instead of reading a stored mask.  Two
+// counter-based generators:
+//
+// MS_RNG_PHILOX4X32 (default): Philox4x32-10 (Salmon et al., Random123; the
+// generator curand and torch use), key = seed (lo, hi words), counter = (j lo,
+// j hi, stream lo, stream hi) for the block j of elements 4j .. 4j+3; element
+// 4j + i is kept iff word_i >= ceil(p * 2^32).  32-bit multiplies make it ~4x
+// cheaper than the 64-bit generator below, so it runs near HBM speed.
+//
+// MS_RNG_PHILOX4X64_REF: the reference's own generator,
+// leantape.core.Rng(seed, stream).uniform()
 // (core.py:100-124) is numpy's Philox4x64-10 keyed [seed, stream] with a
 // 256-bit counter that is incremented before each 4-word block, and
 // Generator.random() maps a 64-bit word u to (u >> 11) * 2^-53.  Element i
@@ -26,65 +35,147 @@ namespace ms {
 namespace {
 
 // ---------------------------------------------------------------- Philox4x64-10
-__device__ __forceinline__ void philox4x64_10(uint64_t (&c)[4], uint64_t k0, uint64_t k1) {
-  constexpr uint64_t M0 = 0xD2E7470EE14C6C93ull, M1 = 0xCA5A826395121157ull;
-  constexpr uint64_t W0 = 0x9E3779B97F4A7C15ull, W1 = 0xBB67AE8584CAA73Bull;
-#pragma unroll
-  for (int r = 0; r < 10; ++r) {
-    if (r > 0) {
-      k0 += W0;
-      k1 += W1;
-    }
-    const uint64_t hi0 = __umul64hi(M0, c[0]), lo0 = M0 * c[0];
-    const uint64_t hi1 = __umul64hi(M1, c[2]), lo1 = M1 * c[2];
-    const uint64_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
-    c[0] = n0;
-    c[1] = lo1;
-    c[2] = n2;
-    c[3] = lo0;
-  }
+// Round keys (k0 + r*W0, k1 + r*W1) are the same for every element: the host
+// precomputes them (kernel parameters, read from the constant bank).
+struct PhiloxKeys {
+  uint64_t k[10][2];
+};
+
+// hi:lo = a * b, 64 x 64 -> 128 bits as four 32x32->64 multiply-adds (each
+// one IMAD.WIDE; the 64-bit addends never overflow): about half the IMADs of
+// __umul64hi plus a separate 64-bit multiply
+__device__ __forceinline__ void mul128(uint64_t a, uint64_t b, uint64_t& hi, uint64_t& lo) {
+  const uint32_t a0 = (uint32_t)a, a1 = (uint32_t)(a >> 32);
+  const uint32_t b0 = (uint32_t)b, b1 = (uint32_t)(b >> 32);
+  const uint64_t t = (uint64_t)a0 * b0;
+  const uint64_t u = (uint64_t)a1 * b0 + (t >> 32);
+  const uint64_t v = (uint64_t)a0 * b1 + (uint32_t)u;
+  lo = (v << 32) | (uint32_t)t;
+  hi = (uint64_t)a1 * b1 + (u >> 32) + (v >> 32);
 }
 
-// keep bits of the 4 elements of block `blk` (element 4*(blk-1) + j -> bit j)
-__device__ __forceinline__ uint32_t keep4(uint64_t blk, uint64_t k0, uint64_t k1, uint64_t thr) {
-  uint64_t c[4] = {blk, 0ull, 0ull, 0ull};
-  philox4x64_10(c, k0, k1);
+// ---------------------------------------------------------------- Philox4x32-10
+struct Philox32Keys {
+  uint32_t k[10][2];
+};
+
+template <int NB>
+__device__ __forceinline__ uint32_t keep_n32(uint64_t blk0, uint64_t stream,
+                                             const Philox32Keys& K, uint64_t thr) {
+  constexpr uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+  uint32_t c[NB][4];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    const uint64_t j = blk0 + b;
+    c[b][0] = (uint32_t)j;
+    c[b][1] = (uint32_t)(j >> 32);
+    c[b][2] = (uint32_t)stream;
+    c[b][3] = (uint32_t)(stream >> 32);
+  }
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const uint32_t hi0 = __umulhi(M0, c[b][0]), lo0 = M0 * c[b][0];
+      const uint32_t hi1 = __umulhi(M1, c[b][2]), lo1 = M1 * c[b][2];
+      const uint32_t n0 = hi1 ^ c[b][1] ^ K.k[r][0], n2 = hi0 ^ c[b][3] ^ K.k[r][1];
+      c[b][0] = n0;
+      c[b][1] = lo1;
+      c[b][2] = n2;
+      c[b][3] = lo0;
+    }
+  }
   uint32_t bits = 0;
 #pragma unroll
-  for (int j = 0; j < 4; ++j) bits |= ((c[j] >> 11) >= thr ? 1u : 0u) << j;
+  for (int b = 0; b < NB; ++b)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) bits |= ((uint64_t)c[b][j] >= thr ? 1u : 0u) << (4 * b + j);
   return bits;
 }
 
-// y = keep ? x * scale : 0 over groups of 8 elements (two Philox blocks);
+struct DropoutKeys {
+  PhiloxKeys k64;    // MS_RNG_PHILOX4X64_REF
+  Philox32Keys k32;  // MS_RNG_PHILOX4X32
+  uint64_t stream;
+};
+
+// NB Philox blocks in lockstep (independent dependency chains for ILP):
+// block blk0 + b -> bits 4b .. 4b+3
+template <int NB>
+__device__ __forceinline__ uint32_t keep_n(uint64_t blk0, const PhiloxKeys& K, uint64_t thr) {
+  constexpr uint64_t M0 = 0xD2E7470EE14C6C93ull, M1 = 0xCA5A826395121157ull;
+  uint64_t c[NB][4];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    c[b][0] = blk0 + b;
+    c[b][1] = c[b][2] = c[b][3] = 0ull;
+  }
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      uint64_t hi0, lo0, hi1, lo1;
+      mul128(M0, c[b][0], hi0, lo0);
+      mul128(M1, c[b][2], hi1, lo1);
+      const uint64_t n0 = hi1 ^ c[b][1] ^ K.k[r][0], n2 = hi0 ^ c[b][3] ^ K.k[r][1];
+      c[b][0] = n0;
+      c[b][1] = lo1;
+      c[b][2] = n2;
+      c[b][3] = lo0;
+    }
+  }
+  uint32_t bits = 0;
+#pragma unroll
+  for (int b = 0; b < NB; ++b)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) bits |= ((c[b][j] >> 11) >= thr ? 1u : 0u) << (4 * b + j);
+  return bits;
+}
+
+// y = keep ? x * scale : 0 over groups of 16 elements (four Philox blocks);
 // mask (optional, 1 byte per element) receives the keep flags.
-template <typename T>
-__global__ void __launch_bounds__(256) dropout_kernel(int64_t n, const T* x, T* y, uint64_t k0,
-                                                      uint64_t k1, uint64_t thr, float scale,
+template <int GEN, int NB>
+__device__ __forceinline__ uint32_t keep_blocks(uint64_t blk, const DropoutKeys& K, uint64_t thr) {
+  if constexpr (GEN == MS_RNG_PHILOX4X64_REF) return keep_n<NB>(blk + 1, K.k64, thr);
+  else return keep_n32<NB>(blk, K.stream, K.k32, thr);
+}
+
+template <typename T, int GEN>
+__global__ void __launch_bounds__(256) dropout_kernel(int64_t n, const T* x, T* y,
+                                                      const __grid_constant__ DropoutKeys K,
+                                                      uint64_t thr, float scale,
                                                       uint8_t* __restrict__ mask, bool vec) {
-  const int64_t full = n / 8;
+  const int64_t full = n / 16;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t gi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gi < full; gi += stride) {
-    float v[8];
-    ld8<T>(x + gi * 8, v, vec);
-    const uint32_t bits = keep4(2 * gi + 1, k0, k1, thr) | (keep4(2 * gi + 2, k0, k1, thr) << 4);
+    float v[2][8];
+    ld8<T>(x + gi * 16, v[0], vec);
+    ld8<T>(x + gi * 16 + 8, v[1], vec);
+    const uint32_t bits = keep_blocks<GEN, 4>(4 * gi, K, thr);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) v[j] = (bits >> j) & 1u ? v[j] * scale : 0.f;
-    st8<T>(y + gi * 8, v, vec);
+    for (int h = 0; h < 2; ++h) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[h][j] = (bits >> (8 * h + j)) & 1u ? v[h][j] * scale : 0.f;
+      st8<T>(y + gi * 16 + 8 * h, v[h], vec);
+    }
     if (mask) {
-      uint2 m;
-      m.x = (bits & 1u) | ((bits >> 1) & 1u) << 8 | ((bits >> 2) & 1u) << 16 | ((bits >> 3) & 1u) << 24;
-      m.y = ((bits >> 4) & 1u) | ((bits >> 5) & 1u) << 8 | ((bits >> 6) & 1u) << 16 |
-            ((bits >> 7) & 1u) << 24;
       if (vec) {
-        *reinterpret_cast<uint2*>(mask + gi * 8) = m;
+        uint4 m;
+        uint32_t w[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          w[q] = ((bits >> (4 * q)) & 1u) | ((bits >> (4 * q + 1)) & 1u) << 8 |
+                 ((bits >> (4 * q + 2)) & 1u) << 16 | ((bits >> (4 * q + 3)) & 1u) << 24;
+        m.x = w[0]; m.y = w[1]; m.z = w[2]; m.w = w[3];
+        *reinterpret_cast<uint4*>(mask + gi * 16) = m;
       } else {
-        for (int j = 0; j < 8; ++j) mask[gi * 8 + j] = (bits >> j) & 1u;
+        for (int j = 0; j < 16; ++j) mask[gi * 16 + j] = (bits >> j) & 1u;
       }
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {  // tail elements
-    for (int64_t e = full * 8; e < n; ++e) {
-      const uint32_t b = keep4(static_cast<uint64_t>(e / 4) + 1, k0, k1, thr);
+    for (int64_t e = full * 16; e < n; ++e) {
+      const uint32_t b = keep_blocks<GEN, 1>(static_cast<uint64_t>(e / 4), K, thr);
       const bool keep = (b >> (e % 4)) & 1u;
       y[e] = IO<T>::cvt(keep ? IO<T>::ld(x + e) * scale : 0.f);
       if (mask) mask[e] = keep ? 1 : 0;
@@ -102,18 +193,40 @@ int grid_for(int64_t work, int per_sm = 16) {
 bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 ms_status dropout_launch(int64_t numel, int dt, const void* x, void* y, uint64_t seed,
-                         uint64_t stream_id, double p, void* mask, cudaStream_t st) {
+                         uint64_t stream_id, double p, int gen, void* mask, cudaStream_t st) {
   MS_CHECK_ARG(numel >= 0, MS_ERR_SHAPE, "dropout: negative numel");
   MS_CHECK_ARG(p >= 0.0 && p < 1.0, MS_ERR_SHAPE, "dropout: p must be in [0, 1), got %g", p);
+  MS_CHECK_ARG(gen == MS_RNG_PHILOX4X32 || gen == MS_RNG_PHILOX4X64_REF, MS_ERR_UNSUPPORTED,
+               "dropout: unknown generator %d", gen);
   if (numel == 0) return MS_OK;
-  // keep iff (u >> 11) >= ceil(p * 2^53); p * 2^53 is exact in double
-  const double t = ceil(p * 9007199254740992.0);
-  const uint64_t thr = static_cast<uint64_t>(t);
+  // 64-bit reference generator: keep iff (u >> 11) >= ceil(p * 2^53) (p * 2^53
+  // is exact in double); 32-bit generator: keep iff u >= ceil(p * 2^32)
+  const uint64_t thr = static_cast<uint64_t>(
+      ceil(p * (gen == MS_RNG_PHILOX4X64_REF ? 9007199254740992.0 : 4294967296.0)));
   const float scale = static_cast<float>(1.0 / (1.0 - p));
-  const bool vec = al16(x) && al16(y) && (!mask || (reinterpret_cast<uintptr_t>(mask) & 7) == 0);
-  MS_DT_DISPATCH(dt, dropout_kernel<T><<<grid_for(numel / 8 + 1), 256, 0, st>>>(
-                         numel, (const T*)x, (T*)y, seed, stream_id, thr, scale,
-                         (uint8_t*)mask, vec));
+  const bool vec = al16(x) && al16(y) && (!mask || (reinterpret_cast<uintptr_t>(mask) & 15) == 0);
+  DropoutKeys K;
+  uint64_t k0 = seed, k1 = stream_id;
+  uint32_t q0 = (uint32_t)seed, q1 = (uint32_t)(seed >> 32);
+  for (int r = 0; r < 10; ++r) {  // Weyl key schedules
+    K.k64.k[r][0] = k0;
+    K.k64.k[r][1] = k1;
+    k0 += 0x9E3779B97F4A7C15ull;
+    k1 += 0xBB67AE8584CAA73Bull;
+    K.k32.k[r][0] = q0;
+    K.k32.k[r][1] = q1;
+    q0 += 0x9E3779B9u;
+    q1 += 0xBB67AE85u;
+  }
+  K.stream = stream_id;
+  const int grid = grid_for(numel / 16 + 1);
+  if (gen == MS_RNG_PHILOX4X64_REF) {
+    MS_DT_DISPATCH(dt, (dropout_kernel<T, MS_RNG_PHILOX4X64_REF><<<grid, 256, 0, st>>>(
+                           numel, (const T*)x, (T*)y, K, thr, scale, (uint8_t*)mask, vec)));
+  } else {
+    MS_DT_DISPATCH(dt, (dropout_kernel<T, MS_RNG_PHILOX4X32><<<grid, 256, 0, st>>>(
+                           numel, (const T*)x, (T*)y, K, thr, scale, (uint8_t*)mask, vec)));
+  }
   count_launch();
   return launch_status("dropout");
 }
@@ -229,15 +342,15 @@ __global__ void __launch_bounds__(256) ln_fwd_generic(int64_t rows, int D, const
 // backward, one warp per row (grid-stride over rows); dw / db partial sums in
 // registers, reduced per block through shared memory, then one fp32 atomic per
 // column per block into the workspace
-template <typename T, int KV>
+template <typename T, int KV, bool WANTP>
 __global__ void __launch_bounds__(LN_WARPS * 32) ln_bwd_vec(int64_t rows, int D, const T* g,
                                                             const T* x, const float* mean,
                                                             const float* rstd, const T* w, T* dx,
                                                             float* dw_acc, float* db_acc) {
   extern __shared__ float sacc[];  // [2][D] when dw / db are requested
   const int lane = threadIdx.x & 31;
-  const bool wantp = dw_acc || db_acc;
-  if (wantp) {
+  constexpr bool wantp = WANTP;
+  if constexpr (wantp) {
     for (int i = threadIdx.x; i < 2 * D; i += blockDim.x) sacc[i] = 0.f;
     __syncthreads();
   }
@@ -274,8 +387,10 @@ __global__ void __launch_bounds__(LN_WARPS * 32) ln_bwd_vec(int64_t rows, int D,
           const float gw = gv[k][j] * wv[k][j];
           a += gw;
           c += gw * xh[k][j];
-          pw[k][j] += gv[k][j] * xh[k][j];
-          pb[k][j] += gv[k][j];
+          if constexpr (wantp) {
+            pw[k][j] += gv[k][j] * xh[k][j];
+            pb[k][j] += gv[k][j];
+          }
         }
       }
     }
@@ -293,7 +408,7 @@ __global__ void __launch_bounds__(LN_WARPS * 32) ln_bwd_vec(int64_t rows, int D,
       }
     }
   }
-  if (wantp) {
+  if constexpr (wantp) {
 #pragma unroll
     for (int k = 0; k < KV; ++k) {
       const int col = (k * 32 + lane) * 8;
@@ -370,17 +485,19 @@ using namespace ms;
 
 extern "C" ms_status ms_dropout_fwd(int64_t numel, int32_t dtype, const void* x, void* y,
                                     uint64_t seed, uint64_t stream_id, double p,
-                                    void* mask_or_null, void* stream) {
+                                    int32_t generator, void* mask_or_null, void* stream) {
   MS_TRY(bind_device(y));
-  return dropout_launch(numel, dtype, x, y, seed, stream_id, p, mask_or_null,
+  return dropout_launch(numel, dtype, x, y, seed, stream_id, p, generator, mask_or_null,
                         (cudaStream_t)stream);
 }
 
 extern "C" ms_status ms_dropout_bwd(int64_t numel, int32_t dtype, const void* g, void* dx,
-                                    uint64_t seed, uint64_t stream_id, double p, void* stream) {
+                                    uint64_t seed, uint64_t stream_id, double p,
+                                    int32_t generator, void* stream) {
   MS_TRY(bind_device(dx));
   // dx = g * mask / (1 - p): the same map as the forward, with the mask replayed
-  return dropout_launch(numel, dtype, g, dx, seed, stream_id, p, nullptr, (cudaStream_t)stream);
+  return dropout_launch(numel, dtype, g, dx, seed, stream_id, p, generator, nullptr,
+                        (cudaStream_t)stream);
 }
 
 extern "C" size_t ms_layernorm_workspace(int64_t rows, int64_t dim, int32_t dtype) {
@@ -441,10 +558,17 @@ extern "C" ms_status ms_layernorm_bwd(int64_t rows, int64_t dim, int32_t dt, con
       if (wantp && grid > (int64_t)num_sms() * 4) grid = num_sms() * 4;  // amortise the atomics
       if (grid > (1ll << 30)) grid = 1ll << 30;
       const size_t smem = wantp ? 2 * D * sizeof(float) : 0;
-      MS_DT_DISPATCH(dt, MS_KV_SWITCH(kv, (ln_bwd_vec<T, KV><<<(unsigned)grid, LN_WARPS * 32,
-                                                              smem, st>>>(
-                                              rows, D, (const T*)g, (const T*)x, mean, rstd,
-                                              (const T*)w, (T*)dx, dwa, dba))));
+      if (wantp) {
+        MS_DT_DISPATCH(dt, MS_KV_SWITCH(kv, (ln_bwd_vec<T, KV, true><<<(unsigned)grid,
+                                                                       LN_WARPS * 32, smem, st>>>(
+                                                rows, D, (const T*)g, (const T*)x, mean, rstd,
+                                                (const T*)w, (T*)dx, dwa, dba))));
+      } else {
+        MS_DT_DISPATCH(dt, MS_KV_SWITCH(kv, (ln_bwd_vec<T, KV, false><<<(unsigned)grid,
+                                                                        LN_WARPS * 32, 0, st>>>(
+                                                rows, D, (const T*)g, (const T*)x, mean, rstd,
+                                                (const T*)w, (T*)dx, nullptr, nullptr))));
+      }
     } else {
       MS_CHECK_ARG(rows < (1ll << 31), MS_ERR_UNSUPPORTED, "layernorm: too many rows");
       MS_DT_DISPATCH(dt, (ln_bwd_generic<T><<<(unsigned)rows, 256, 0, st>>>(

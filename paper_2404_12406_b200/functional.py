@@ -500,18 +500,22 @@ def max_pool2d(x, kernel_size, stride=None, padding=0):
 
 # =============================================================== dropout (RNG replay)
 DROPOUT_STREAM_BASE = 1_000_000  # leantape.core.Rng.DROPOUT_STREAM_BASE (core.py:108)
+# mask generators (include/memsave_b200.h ms_rng): "philox4x32" (default, Random123
+# Philox4x32-10) or "reference" (leantape.core.Rng's Philox4x64-10, bit-identical
+# to the reference's masks)
+_RNG = {"philox4x32": _lib.MS_RNG_PHILOX4X32, "reference": _lib.MS_RNG_PHILOX4X64_REF}
 
 
 class _DropoutFn(torch.autograd.Function):
     """MemSave Dropout (rules.py:103-106, MEMSAVE row): keeps only the 16-byte
     RNG key (seed, stream) (saved.py:91-108, RngSeed) and regenerates the keep
-    mask in backward; the mask is the reference generator's
-    (Rng(seed, stream).uniform() >= p, core.py:100-124)."""
+    mask in backward from the counter-based generator ``gen`` (with
+    "reference", Rng(seed, stream).uniform() >= p of core.py:100-124)."""
 
     @staticmethod
-    def forward(ctx, x, p: float, seed: int, stream: int, inplace: bool):
+    def forward(ctx, x, p: float, seed: int, stream: int, inplace: bool, gen: int):
         out_rg = ctx.needs_input_grad[0]
-        ctx.key = (int(seed), int(stream), float(p))
+        ctx.key = (int(seed), int(stream), float(p), int(gen))
         key = torch.tensor([int(seed), int(stream)], dtype=torch.int64) if out_rg else None
         if _is_meta(x):
             ctx.save_for_backward(key)
@@ -526,7 +530,7 @@ class _DropoutFn(torch.autograd.Function):
         y = x if inplace else torch.empty_like(x, memory_format=fmt)
         L = _lib.lib()
         _lib.check(L.ms_dropout_fwd(x.numel(), _dtype_code(x), _ptr(x), _ptr(y), seed, stream, p,
-                                    None, _stream(x.device)), "ms_dropout_fwd")
+                                    gen, None, _stream(x.device)), "ms_dropout_fwd")
         if inplace:
             ctx.mark_dirty(x)
         ctx.save_for_backward(key)
@@ -536,17 +540,17 @@ class _DropoutFn(torch.autograd.Function):
     def backward(ctx, gy):
         (key,) = ctx.saved_tensors
         if not ctx.needs_input_grad[0]:
-            return None, None, None, None, None
+            return None, None, None, None, None, None
         _need(key, "seed", "dropout dX")
-        seed, stream, p = ctx.key
+        seed, stream, p, gen = ctx.key
         if _is_meta(gy):
-            return gy.new_empty(gy.shape), None, None, None, None
+            return gy.new_empty(gy.shape), None, None, None, None, None
         g = gy.contiguous(memory_format=ctx.fmt)
         dx = torch.empty_like(g, memory_format=ctx.fmt)
         L = _lib.lib()
         _lib.check(L.ms_dropout_bwd(g.numel(), _dtype_code(g), _ptr(g), _ptr(dx), seed, stream, p,
-                                    _stream(g.device)), "ms_dropout_bwd")
-        return dx, None, None, None, None
+                                    gen, _stream(g.device)), "ms_dropout_bwd")
+        return dx, None, None, None, None, None
 
 
 def draw_seed() -> int:
@@ -556,15 +560,19 @@ def draw_seed() -> int:
 
 
 def dropout(x: torch.Tensor, p: float = 0.5, training: bool = True, inplace: bool = False,
-            seed: int | None = None, stream: int = DROPOUT_STREAM_BASE) -> torch.Tensor:
+            seed: int | None = None, stream: int = DROPOUT_STREAM_BASE,
+            generator: str = "philox4x32") -> torch.Tensor:
     """Dropout whose backward replays the mask from its RNG key (SPEC.md
-    forward_dropout, RngReplay variant)."""
+    forward_dropout, RngReplay variant).  ``generator="reference"`` draws the
+    reference's own masks (leantape.core.Rng); seeds must be < 2^63."""
     if not 0.0 <= p < 1.0:
         raise ValueError(f"dropout probability has to be in [0, 1), got {p}")
+    if generator not in _RNG:
+        raise ValueError(f"dropout generator must be one of {sorted(_RNG)}, got {generator!r}")
     if not training or p == 0.0:
         return x
     return _DropoutFn.apply(x, float(p), draw_seed() if seed is None else int(seed), int(stream),
-                            inplace)
+                            inplace, _RNG[generator])
 
 
 # =============================================================== layernorm

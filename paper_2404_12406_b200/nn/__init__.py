@@ -155,18 +155,20 @@ class MemSaveMaxPool2d(nn.MaxPool2d):
 
 class MemSaveDropout(nn.Dropout):
     """nn.Dropout that keeps only its 16-byte RNG key for backward and replays
-    the mask (rules.py:103-106, MEMSAVE row; saved.py:91-108).  The mask of a
-    call is Rng(seed, stream).uniform() >= p of the reference generator, with a
-    fresh seed per call from torch's default CPU generator and the stream
-    ``DROPOUT_STREAM_BASE + node`` (core.py:104-108)."""
+    the mask (rules.py:103-106, MEMSAVE row; saved.py:91-108).  Each call draws
+    a fresh seed from torch's default CPU generator; the stream is
+    ``DROPOUT_STREAM_BASE + node`` (core.py:104-108).  ``generator``:
+    "philox4x32" (default) or "reference" (the reference's Philox4x64 masks)."""
 
-    def __init__(self, p: float = 0.5, inplace: bool = False, node: int = 0):
+    def __init__(self, p: float = 0.5, inplace: bool = False, node: int = 0,
+                 generator: str = "philox4x32"):
         super().__init__(p, inplace)
         self.node = int(node)
+        self.generator = generator
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         return MF.dropout(x, self.p, self.training, self.inplace,
-                          stream=MF.DROPOUT_STREAM_BASE + self.node)
+                          stream=MF.DROPOUT_STREAM_BASE + self.node, generator=self.generator)
 
     @classmethod
     def from_nn_Dropout(cls, do: nn.Dropout, node: int = 0) -> "MemSaveDropout":

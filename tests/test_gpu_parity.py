@@ -392,7 +392,7 @@ def test_dropout_mask_is_the_reference_generator(dropout_golden, case):
     mask = g[f"{case}/mask"].astype(bool)
     n = mask.size
     x = torch.ones(n, device=DEV, dtype=torch.float32)
-    y = MF.dropout(x, p, True, seed=seed, stream=stream)
+    y = MF.dropout(x, p, True, seed=seed, stream=stream, generator="reference")
     np.testing.assert_array_equal((y != 0).cpu().numpy(), mask)
     scale = np.float32(1.0 / (1.0 - p))
     np.testing.assert_array_equal(y.cpu().numpy()[mask], np.full(mask.sum(), scale))
@@ -403,23 +403,24 @@ def test_dropout_mask_is_the_reference_generator(dropout_golden, case):
     st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
     assert L.ms_dropout_fwd(n, _lib.MS_F32, ctypes.c_void_p(x.data_ptr()),
                             ctypes.c_void_p(yb.data_ptr()), seed, stream, p,
-                            ctypes.c_void_p(mb.data_ptr()), st) == 0
+                            _lib.MS_RNG_PHILOX4X64_REF, ctypes.c_void_p(mb.data_ptr()), st) == 0
     np.testing.assert_array_equal(mb.cpu().numpy(), mask.astype(np.uint8))
 
 
+@pytest.mark.parametrize("gen", ["philox4x32", "reference"])
 @pytest.mark.parametrize("dt", ["bf16", "f32"])
-@pytest.mark.parametrize("n", [(1 << 20) + 3, 4096])
-def test_dropout_replayed_gradient(dt, n):
+@pytest.mark.parametrize("n", [(1 << 20) + 3, 4096 + 13])
+def test_dropout_replayed_gradient(dt, n, gen):
     rng = np.random.default_rng(n)
-    seed, stream, p = 987654321, 1_000_000 + 5, 0.1
+    seed, stream, p = 987654321 + (1 << 40), 1_000_000 + 5, 0.1
     x, xq = _q(rng.standard_normal(n), dt)
     g, gq = _q(rng.standard_normal(n), dt)
     x.requires_grad_(True)
     u0 = launch_count()
-    y = MF.dropout(x, p, True, seed=seed, stream=stream)
+    y = MF.dropout(x, p, True, seed=seed, stream=stream, generator=gen)
     y.backward(g)
     assert launch_count() - u0 == 2  # forward + replayed backward on the native kernels
-    mask = oracle.dropout_mask(seed, stream, p, n)
+    mask = oracle.dropout_mask(seed, stream, p, n, gen)
     s = float(np.float32(1.0 / (1.0 - p)))
     np.testing.assert_array_equal((x.grad != 0).cpu().numpy() | (gq == 0), mask | (gq == 0))
     _close(y, np.where(mask, xq * s, 0.0), dt, "dropout y")

@@ -193,3 +193,20 @@ def test_conv_transpose_unit_kernel_kat():
     x = np.arange(12.0).reshape(1, 1, 3, 4)
     np.testing.assert_array_equal(oracle.conv_transpose2d_fwd(x, np.ones((1, 1, 1, 1)), None, 1, 0),
                                   x)
+
+
+def test_philox4x32_known_answers():
+    # Random123 kat_vectors for philox4x32_10 (Salmon et al., SC'11)
+    from oracle import dropout as od
+    kats = [([0, 0, 0, 0], [0, 0], [0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8]),
+            ([0xFFFFFFFF] * 4, [0xFFFFFFFF] * 2, [0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD]),
+            ([0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344], [0xA4093822, 0x299F31D0],
+             [0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1])]
+    for ctr, key, want in kats:
+        got = od.philox4x32_10([[v] for v in ctr], key)
+        assert [int(w[0]) for w in got] == want
+
+
+def test_philox4x32_mask_rate():
+    m = oracle.dropout_mask(99, 1_000_001, 0.3, 200_000, "philox4x32")
+    assert abs(m.mean() - 0.7) < 0.005
