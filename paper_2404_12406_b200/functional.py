@@ -244,6 +244,9 @@ class _Conv2dFn(torch.autograd.Function):
         w_dtype, w_cl = ctx.w_meta
         dx = dw = db = None
         if _is_meta(gy):
+            # mirror the CUDA path's allocations (the planner's ledger sees them):
+            # an expanded upstream gradient is materialised in the kernel layout
+            gy = _as_layout(gy, ctx.layouts[0])
             if need_x:
                 _need(w, "w", "conv2d dX")
                 dx = gy.new_empty(x_shape)
@@ -420,6 +423,7 @@ class _ReLUFn(torch.autograd.Function):
             return None, None
         mask = _need(mask, "mask", "relu dX")
         if _is_meta(gy):
+            gy = gy.contiguous(memory_format=ctx.fmt)  # mirrors the CUDA path's allocation
             return gy.new_empty(gy.shape), None
         g = gy.contiguous(memory_format=ctx.fmt)
         dx = torch.empty_like(g, memory_format=ctx.fmt)
@@ -544,6 +548,7 @@ class _DropoutFn(torch.autograd.Function):
         _need(key, "seed", "dropout dX")
         seed, stream, p, gen = ctx.key
         if _is_meta(gy):
+            gy = gy.contiguous()  # mirrors the CUDA path's allocation
             return gy.new_empty(gy.shape), None, None, None, None, None
         g = gy.contiguous(memory_format=ctx.fmt)
         dx = torch.empty_like(g, memory_format=ctx.fmt)

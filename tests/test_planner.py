@@ -1,0 +1,123 @@
+"""Planner / peak predictor (SPEC.md planner + memwatch).
+
+CPU tier: the analytic plan of the Fig. 1 deep CNN reproduces the reference's
+acceptance criterion 1 exactly, at desk scale (S = 131072 B).
+GPU tier: the planned peak equals torch.cuda.max_memory_allocated of the real
+run within the allocator's rounding + our kernels' workspaces.
+"""
+
+import pytest
+import torch
+
+from benchkit.models import DeepCNN
+from paper_2404_12406_b200.nn import convert_to_memory_saving
+from paper_2404_12406_b200.planner import CSV_HEADER, plan, plan_csv_row
+
+S = 4 * 8 * 32 * 32 * 4  # desk-scale activation (4, 8, 32, 32) f32 = 131072 B
+W = 8 * 8 * 3 * 3 * 4    # one kernel, 2304 B
+
+
+def _deep(L, trainable, policy):
+    m = DeepCNN(L)
+    for i, p in enumerate(m.parameters()):
+        p.requires_grad_(trainable(i))
+    if policy == "memsave":
+        convert_to_memory_saving(m)
+    return m
+
+
+def _plan(m, x_rg=False):
+    x = torch.empty(4, 8, 32, 32, requires_grad=x_rg)
+    return plan(m, [x], loss_fn=lambda mm, x: mm(x).sum())
+
+
+@pytest.mark.parametrize("L", [1, 2, 4, 8, 12])
+def test_fig1_tape_bytes(L):
+    # fully differentiable: tape = L*S under both policies (inputs of every layer)
+    for policy in ("naive", "memsave"):
+        assert _plan(_deep(L, lambda i: True, policy)).tape_bytes == L * S
+    # layer-4-only (k = 4): NAIVE keeps the inputs of layers 4..L, MEMSAVE only layer 4's
+    if L >= 4:
+        naive = _plan(_deep(L, lambda i: i == 3, "naive")).tape_bytes
+        plus = _plan(_deep(L, lambda i: i >= 3, "naive")).tape_bytes
+        assert naive == (L - 3) * S == plus  # "the same footprint as layers k+" (Fig. 1)
+        assert _plan(_deep(L, lambda i: i == 3, "memsave")).tape_bytes == S
+
+
+@pytest.mark.parametrize("L", [1, 2, 3, 8, 12])
+def test_fig1_fully_nondiff_forward_peak(L):
+    # nothing differentiable: peak = 2S (L = 1), 3S (L >= 2), independent of depth
+    pl = plan(_deep(L, lambda i: False, "memsave"), [torch.empty(4, 8, 32, 32)])
+    act_peak = pl.fwd_peak_bytes - pl.resident_bytes + S  # the input is part of the live set
+    assert act_peak == (2 * S if L == 1 else 3 * S)
+    assert pl.tape_bytes == 0
+
+
+def test_memsave_never_exceeds_naive():
+    for L in (2, 5, 9):
+        for tr in (lambda i: True, lambda i: i == 1, lambda i: False):
+            for x_rg in (False, True):
+                a = _plan(_deep(L, tr, "memsave"), x_rg).tape_bytes
+                b = _plan(_deep(L, tr, "naive"), x_rg).tape_bytes
+                assert a <= b
+
+
+def test_csv_schema():
+    assert CSV_HEADER == "net,layer,depth,scenario,policy,tape_bytes,peak_bytes,forward_ms,backward_ms"
+    row = plan_csv_row("deepcnn", "conv2d", 3, "Input", "memsave", 10, 20, 1.5, 2.5)
+    assert row == "deepcnn,conv2d,3,Input,memsave,10,20,1.5000,2.5000"
+
+
+def _measure(model, x, loss_fn):
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    torch.cuda.reset_peak_memory_stats()
+    base = torch.cuda.memory_allocated()
+    loss_fn(model, x).backward()
+    torch.cuda.synchronize()
+    return torch.cuda.max_memory_allocated() - base
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("scenario", ["layer1", "all", "input"])
+def test_planned_peak_matches_b200_fig1(scenario):
+    # BASELINE configs[0]: 8 conv(8->8, 3x3) layers, (32, 8, 256, 256) f32, S = 64 MiB
+    L, shape = 8, (32, 8, 256, 256)
+    tr = {"layer1": lambda i: i == 0, "all": lambda i: True, "input": lambda i: False}[scenario]
+    x_rg = scenario == "input"
+    for policy in ("naive", "memsave"):
+        torch.manual_seed(0)
+        m = _deep(L, tr, policy).cuda()
+        x = torch.randn(shape, device="cuda", requires_grad=x_rg)
+        loss = lambda mm, x: mm(x).sum()  # noqa: E731
+        pl = plan(m, [x], loss_fn=loss)
+        measured = _measure(m, x, loss)
+        predicted = pl.peak_bytes - pl.resident_bytes
+        print(policy, scenario, measured, predicted, measured / predicted)
+        if policy == "memsave":
+            # allocator granularity (512 B blocks) + kernel workspaces + the loss scalar
+            assert abs(measured - predicted) <= 0.01 * predicted + (2 << 20), \
+                (policy, scenario, measured, predicted)
+        else:
+            # stock cuDNN adds its algorithm workspace on top of the live set
+            assert measured >= predicted - (2 << 20)
+
+
+@pytest.mark.gpu
+def test_planned_peak_matches_b200_resnet18_input_only():
+    import torchvision
+    from benchkit.models import randomize_bn_stats
+    torch.manual_seed(0)
+    m = torchvision.models.resnet18()
+    randomize_bn_stats(m)
+    m = m.to(device="cuda", dtype=torch.bfloat16).to(memory_format=torch.channels_last).eval()
+    for p in m.parameters():
+        p.requires_grad_(False)
+    convert_to_memory_saving(m)
+    x = torch.randn(16, 3, 224, 224, device="cuda", dtype=torch.bfloat16)
+    x = x.contiguous(memory_format=torch.channels_last).requires_grad_(True)
+    loss = lambda mm, x: mm(x).float().sum()  # noqa: E731
+    pl = plan(m, [x], loss_fn=loss)
+    measured = _measure(m, x, loss)
+    predicted = pl.peak_bytes - pl.resident_bytes
+    assert abs(measured - predicted) <= 0.05 * predicted + (4 << 20), (measured, predicted)
