@@ -14,6 +14,7 @@
 // float32, NCHW 16-bit and channel counts that are not multiples of 8 run on
 // the SIMT direct kernels (simt.cu).
 #include <algorithm>
+#include <cstdlib>
 
 #include "misc.cuh"
 
@@ -60,6 +61,7 @@ struct ConvPlan {
   bool rowseg = false;  // fwd: <=4-channel stride-2 stem, row-segment loads
   int xw_pad = 0;       // rowseg: padded width of the 4-channel activation copy
   bool band = false;    // dx: <8-channel input gradient (the stem), band col2im
+  bool stem = false;    // dx: the 3-channel 7x7/2 stem, register col2im (stem_dgrad.cu)
   int band_h = 16;
   size_t ws_pad = 0, ws_w = 0, ws_acc = 0;
   size_t ws = 0;
@@ -118,6 +120,17 @@ ConvPlan plan(const ms_conv_desc* d, int pass, bool dx_bias = false) {
     p.ws = p.ws_pad + p.ws_w;
   } else if (pass == MS_CONV_DX) {
     if (d->k % 8 != 0) return p;  // SIMT
+    static const bool env_band = getenv("MS_STEM_BAND") != nullptr;  // A/B against the band kernel
+    if (!dx_bias && !env_band &&
+        stem_dgrad_ok(d->dtype, d->layout, (int)d->c, (int)d->r, (int)d->s, d->stride_h,
+                      d->stride_w, d->pad_h, d->pad_w, c.ow, d->k)) {
+      p.tc = true;
+      p.stem = true;
+      p.kpad = (int)d->k;
+      p.ws_w = align256(es * (size_t)taps * d->c * p.kpad);
+      p.ws = p.ws_w;
+      return p;
+    }
     if (!dx_bias && d->c == BAND_C && d->r == BAND_R && d->s == BAND_S && d->stride_w == BAND_SW &&
         d->stride_h == BAND_SW && c.ow <= BM && (int64_t)BAND_WINDOWS * BAND_WIN * 4 <= BAND_WINDOW_BYTES) {
       // the 3-channel 7x7/2 stem: per dX-row band, dY-row x W GEMM + col2im
@@ -277,6 +290,10 @@ ms_status dx_tc(const ms_conv_desc* d, const ConvPlan& p, const void* dy, const 
   const ConvDims c = dims_of(d);
   const int dt = d->dtype;
   if (p.band) return dx_band(d, p, dy, w, dx, ws, st);
+  if (p.stem) {
+    MS_TRY(repack_scatter(dt, c.k, c.c, c.r, c.s, p.kpad, d->wlayout, w, ws, st));
+    return stem_dgrad(dt, c.n, c.h, c.w, c.oh, c.ow, c.k, dy, ws, dx, st);
+  }
   void* wd = ws;
   MS_TRY(repack_dgrad(dt, c.k, c.c, c.r, c.s, p.kpad, d->wlayout, w, wd, st));
   GemmArgs g = base_args(dt);

@@ -19,6 +19,12 @@ ms_status wgrad_finalize(int dt, int K, int C, int R, int S, int wlayout, const 
 ms_status pad_channels(int dt, int64_t pixels, int c, int cpad, const void* x, void* out,
                        cudaStream_t st);
 
+// 3-channel 7x7 stride-2 pad-3 stem input-VJP with register col2im (stem_dgrad.cu)
+bool stem_dgrad_ok(int dt, int layout, int c, int r, int s, int sh, int sw, int ph, int pw,
+                   int64_t ow, int64_t k);
+ms_status stem_dgrad(int dt, int n, int h, int w, int p, int q, int k, const void* dy,
+                     const void* wt, void* dx, cudaStream_t st);
+
 inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 inline size_t align256(size_t v) { return (v + 255) & ~static_cast<size_t>(255); }
 
