@@ -106,6 +106,40 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+# ------------------------------------------------------------------ ncu traffic
+# dram__bytes_read.sum + dram__bytes_write.sum per launch of the step's top conv
+# kernels, from one `ncu --set full` capture each (tools/ncu_summary.py output,
+# committed under profiles/); keyed by (pass, C, R, stride) of the ResNet-18 shapes
+_NCU_CSV = os.path.join(ROOT, "profiles", "r1_ncu_r18_kernels.csv")
+_NCU_NAME = {("conv_fwd", 3, 7, 2): "stem_fwd", ("conv_dx", 3, 7, 2): "stem_dx",
+             ("conv_dx", 64, 3, 1): "layer1_dgrad"}
+_KERNEL_OF = {("conv_fwd", 3, 7, 2): "umma_gemm_kernel<64,0,0,LOAD_CONV_FPROP_ROWSEG>",
+              ("conv_dx", 3, 7, 2): "stem_dgrad_kernel",
+              ("conv_dx", 64, 3, 1): "umma_gemm_kernel<64,0,0,LOAD_CONV_DGRAD>"}
+
+
+def _kernel_key(e):
+    g = e["geom"]
+    return (e["kind"], g["c"], g["r"], g["stride"])
+
+
+def _ncu_traffic(e):
+    name = _NCU_NAME.get(_kernel_key(e))
+    if name is None or not os.path.exists(_NCU_CSV):
+        return None, None
+    import csv
+    vals = {}
+    with open(_NCU_CSV) as f:
+        for row in csv.DictReader(f):
+            if row["kernel"] == name and row["metric"] in ("dram__bytes_read.sum",
+                                                           "dram__bytes_write.sum"):
+                scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(row["unit"], 1)
+                vals[row["metric"]] = float(row["value"]) * scale
+    if len(vals) != 2:
+        return None, None
+    return int(sum(vals.values())), f"{os.path.relpath(_NCU_CSV, ROOT)}:{name}"
+
+
 # ------------------------------------------------------------------ GPU arm
 def _dist_setup(args):
     import torch
@@ -322,9 +356,13 @@ def gpu_main(args):
                 ent["count_per_step"] = cnt
                 layers.append(ent)
         dom = max(layers, key=lambda e: e["ms"] * e["count_per_step"])
+        traffic, tsrc = _ncu_traffic(dom)
         roof = {"bound": dom["bound"], "achieved": round(dom["achieved"], 2),
                 "peak": dom["peak"], "unit": dom["unit"], "frac": round(dom["frac"], 4),
-                "traffic": None, "kernel": "umma_gemm_kernel (%s)" % dom["kind"],
+                "traffic": traffic, "traffic_source": tsrc,
+                "algorithmic_bytes": dom["bytes"], "algorithmic_flops": dom["flops"],
+                "kernel": "%s (%s)" % (_KERNEL_OF.get(_kernel_key(dom), "umma_gemm_kernel"),
+                                       dom["kind"]),
                 "geom": dom["geom"], "launch_ms": round(dom["ms"], 4),
                 "per_unit": "2*N*OH*OW*K*C*R*S flops per launch (implicit GEMM)",
                 "peak_source": peaks["source"] + ", burst (kernel timed alone)"}

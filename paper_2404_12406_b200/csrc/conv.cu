@@ -187,6 +187,12 @@ ms_status fwd_rowseg(const ms_conv_desc* d, const ConvPlan& p, const void* x, co
   void* x4 = wsb;
   void* wr = wsb + p.ws_pad;
   MS_TRY(pad_rowseg(dt, c.n, c.h, c.w, c.c, c.pw, p.xw_pad, x, x4, st));
+  static const bool env_im2col = getenv("MS_STEM_IM2COL") != nullptr;  // A/B switch
+  if (!env_im2col && stem_fprop_ok(dt, d->layout, c.c, c.r, c.s, c.sh, c.sw, c.ph, c.pw, c.ow,
+                                   c.k) &&
+      stem_fprop_weight_bytes(c.k) <= p.ws_w)
+    return stem_fprop(dt, c.n, c.h, p.xw_pad, c.oh, c.ow, c.k, c.c, d->wlayout, x4, w, wr, bias, y,
+                      st);
   MS_TRY(repack_rowseg(dt, c.k, c.c, c.r, c.s, d->wlayout, w, wr, st));
   GemmArgs g = base_args(dt);
   g.M = c.n * c.oh * c.ow;

@@ -25,6 +25,15 @@ bool stem_dgrad_ok(int dt, int layout, int c, int r, int s, int sh, int sw, int 
 ms_status stem_dgrad(int dt, int n, int h, int w, int p, int q, int k, const void* dy,
                      const void* wt, void* dx, cudaStream_t st);
 
+// <= 4-channel 7x7 stride-2 pad-3 stem forward reading overlapping input rows in
+// place (stem_dgrad.cu); xp = pad_rowseg output, wb = stem_fprop_weight_bytes(k)
+bool stem_fprop_ok(int dt, int layout, int c, int r, int s, int sh, int sw, int ph, int pw,
+                   int64_t ow, int64_t k);
+size_t stem_fprop_weight_bytes(int k);
+ms_status stem_fprop(int dt, int n, int h, int wp, int p, int q, int k, int c, int wlayout,
+                     const void* xp, const void* w, void* wb, const void* bias, void* y,
+                     cudaStream_t st);
+
 inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 inline size_t align256(size_t v) { return (v + 255) & ~static_cast<size_t>(255); }
 

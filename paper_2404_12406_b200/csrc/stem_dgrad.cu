@@ -278,4 +278,296 @@ ms_status stem_dgrad(int dt, int n, int h, int w, int p, int q, int k, const voi
   return launch_status("stem_dgrad_kernel");
 }
 
+
+// ============================================================================
+// Forward of the same stem (<= 4-channel 7x7 / stride 2 / pad 3 convolution)
+// with the A operand read straight out of the input rows -- no im2col.
+//
+// In a 4-channel copy of the input padded by 3 pixels on the left, the K-slice
+// of output pixel ow for kernel row r (7 taps x 4 channels, 56 B, padded to
+// K = 32) starts at byte 16*ow of input row 2*oh-3+r.  A K-major no-swizzle
+// UMMA operand whose 8x16 B core matrices are 16 B apart along K (LBO = 16) and
+// 128 B apart along M (SBO = 128) describes exactly these overlapping rows, so
+// each input row is copied once per output row with one 1.8 KB bulk copy and
+// the tensor core reads the overlapping windows in place (the im2col variant
+// moves 4x the bytes through TMA).  The weight tile (7 x 32 x K) stays in
+// shared memory for the whole launch.  Output row tiles: M = 128 >= OW.
+// ============================================================================
+namespace {
+
+constexpr int SF_R = 7;
+constexpr int SF_SLOT = 2176;              // one padded input row (>= 16*127 + 64 bytes)
+constexpr int SF_STAGE = SF_R * SF_SLOT;   // the 7 input rows of one output row
+constexpr int SF_STAGES = 6;
+constexpr int SF_EPI = 4;
+constexpr int SF_THREADS = 64 + 32 * SF_EPI;
+
+struct StemFpropArgs {
+  int N, H, Wp;    // padded 4-channel input: [N][H][Wp][4]
+  int P, Q, K;     // output rows, columns, channels
+  int units;       // N * P output rows
+  void* y;         // [N][P][Q][K]
+  const void* bias;
+  int dt;
+  const void* xp;  // padded input
+  const void* wb;  // weights in core-matrix layout [r][kg 4][K][8]
+};
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(dst),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+constexpr int SF_STG = SF_EPI * 2 * 4096;  // per epilogue warp: 2 x (32 px x 128 B), SW128
+
+template <typename T>
+__global__ void __launch_bounds__(SF_THREADS, 1)
+    stem_fprop_kernel(const __grid_constant__ StemFpropArgs a,
+                      const __grid_constant__ CUtensorMap tma_y) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  const int b_bytes = SF_R * 4 * a.K * 16;
+  uint8_t* stg = smem;                         // TMA-store staging (1024-aligned)
+  uint8_t* sB = smem + SF_STG;
+  uint8_t* zero_row = sB + b_bytes;            // out-of-range input rows read zeros
+  uint8_t* ring = zero_row + SF_SLOT;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + SF_STAGES * SF_STAGE);
+  uint64_t* full_bar = bars;
+  uint64_t* empty_bar = bars + SF_STAGES;
+  uint64_t* tfull_bar = bars + 2 * SF_STAGES;
+  uint64_t* tempty_bar = bars + 2 * SF_STAGES + 2;
+  uint64_t* b_bar = bars + 2 * SF_STAGES + 4;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * SF_STAGES + 5);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  for (int i = threadIdx.x; i < SF_SLOT / 4; i += blockDim.x)
+    reinterpret_cast<uint32_t*>(zero_row)[i] = 0u;
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < SF_STAGES; ++i) {
+      mbar_init(smem_u32(&full_bar[i]), 1);
+      mbar_init(smem_u32(&empty_bar[i]), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(smem_u32(&tfull_bar[i]), 1);
+      mbar_init(smem_u32(&tempty_bar[i]), SF_EPI);
+    }
+    mbar_init(smem_u32(b_bar), 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(smem_u32(tmem_holder), 128);
+  fence_proxy_async_smem();  // the zero row is read by the tensor core (async proxy)
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  const uint32_t row_bytes = static_cast<uint32_t>(a.Wp) * 8u;
+
+  if (warp == 0) {
+    // ============================ bulk-copy producer ============================
+    if (lane == 0) {
+      mbar_arrive_expect_tx(smem_u32(b_bar), b_bytes);
+      bulk_g2s(smem_u32(sB), a.wb, b_bytes, smem_u32(b_bar));
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
+        const int n = u / a.P, oh = u - (u / a.P) * a.P;
+        mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
+        const uint32_t fb = smem_u32(&full_bar[stage]);
+        int rows = 0;
+        for (int r = 0; r < SF_R; ++r) {
+          const int h = 2 * oh - 3 + r;
+          rows += (h >= 0 && h < a.H) ? 1 : 0;
+        }
+        mbar_arrive_expect_tx(fb, rows * row_bytes);
+        for (int r = 0; r < SF_R; ++r) {
+          const int h = 2 * oh - 3 + r;
+          if (h >= 0 && h < a.H) {
+            const uint8_t* src = static_cast<const uint8_t*>(a.xp) +
+                                 (static_cast<int64_t>(n) * a.H + h) * row_bytes;
+            bulk_g2s(smem_u32(ring + stage * SF_STAGE + r * SF_SLOT), src, row_bytes, fb);
+          }
+        }
+        if (++stage == SF_STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ============================ MMA issuer ============================
+    if (lane == 0) {
+      const uint32_t idesc = make_idesc_f16(a.dt == MS_BF16 ? 1 : 0, BM, a.K, 0, 0);
+      mbar_wait(smem_u32(b_bar), 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++local) {
+        const int oh = u - (u / a.P) * a.P;
+        const int acc = local & 1;
+        mbar_wait(smem_u32(&tempty_bar[acc]), ((local >> 1) & 1) ^ 1);
+        mbar_wait(smem_u32(&full_bar[stage]), phase);
+        tc_fence_after();
+        const uint32_t dcol = tmem_base + acc * a.K;
+        bool first = true;
+#pragma unroll 1
+        for (int r = 0; r < SF_R; ++r) {
+          const int h = 2 * oh - 3 + r;
+          const uint32_t arow = (h >= 0 && h < a.H)
+                                    ? smem_u32(ring + stage * SF_STAGE + r * SF_SLOT)
+                                    : smem_u32(zero_row);
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {
+            // A: rows 16 B apart, K core matrices 16 B apart (overlapping windows)
+            const uint64_t ad = make_smem_desc(arow + half * 32, 16, 128, LAYOUT_SWIZZLE_NONE);
+            // B: [r][kg][K][8]: K core matrices 16*K B apart, 8-row groups 128 B apart
+            const uint64_t bd = make_smem_desc(smem_u32(sB) + (r * 4 + 2 * half) * a.K * 16,
+                                               a.K * 16, 128, LAYOUT_SWIZZLE_NONE);
+            umma_f16(dcol, ad, bd, idesc, first ? 0u : 1u);
+            first = false;
+          }
+        }
+        umma_commit(smem_u32(&empty_bar[stage]));
+        umma_commit(smem_u32(&tfull_bar[acc]));
+        if (++stage == SF_STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ============================ epilogue ============================
+    // thread = output pixel (TMEM lane); 64-channel rows staged in shared memory
+    // with the 128-byte swizzle and written by one TMA store per 32 pixels
+    // (a 3-D map [N*P][Q][K] clips the pixels past Q)
+    const int quarter = static_cast<int>(warp & 3);
+    const int ew = static_cast<int>(warp) - 2;
+    const int rw = static_cast<int>(lane);
+    int local = 0;
+    uint32_t nst = 0;
+    for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++local) {
+      const int buf = local & 1;
+      mbar_wait(smem_u32(&tfull_bar[buf]), (local >> 1) & 1);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + ((static_cast<uint32_t>(quarter) * 32u) << 16) + buf * a.K;
+#pragma unroll 1
+      for (int c0 = 0; c0 < a.K; c0 += 64) {
+        uint32_t v0[32], v1[32];
+        tmem_ld_32x32b_x32(taddr + c0, v0);
+        tmem_ld_32x32b_x32(taddr + c0 + 32, v1);
+        tmem_ld_wait_regs(v0);
+        tmem_ld_wait_regs(v1);
+        if (c0 + 64 >= a.K) {  // accumulator drained: release it to the next row's MMAs
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&tempty_bar[buf]));
+        }
+        uint8_t* sb = stg + (ew * 2 + (nst & 1)) * 4096;
+        if (lane == 0) bulk_wait_read<1>();  // the store issued 2 chunks ago has read sb
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          float f[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int ch = q * 8 + j;
+            f[j] = __uint_as_float(ch < 32 ? v0[ch] : v1[ch - 32]);
+            if (a.bias) f[j] += IO<T>::ld(static_cast<const T*>(a.bias) + c0 + ch);
+          }
+          uint4 pk;
+          pk.x = pack2<T>(f[0], f[1]);
+          pk.y = pack2<T>(f[2], f[3]);
+          pk.z = pack2<T>(f[4], f[5]);
+          pk.w = pack2<T>(f[6], f[7]);
+          *reinterpret_cast<uint4*>(sb + rw * 128 + ((q ^ (rw & 7)) << 4)) = pk;
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_3d(&tma_y, smem_u32(sb), c0, quarter * 32, u);
+          bulk_commit();
+        }
+        ++nst;
+      }
+    }
+    if (lane == 0) bulk_wait_all();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 128);
+  }
+}
+
+// [r][kg][K][8]: element j of row n in k-group kg = w[n][c][r][s], k = 8kg + j = 4s + c
+template <typename T>
+__global__ void repack_stem_fprop_kernel(int K, int C, int R, int S, int wlayout, const T* w,
+                                         T* out) {
+  const int total = R * 4 * K * 8;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int j = i % 8, n = (i / 8) % K, kg = (i / (8 * K)) % 4, r = i / (32 * K);
+    const int k = kg * 8 + j, s = k / 4, c = k % 4;
+    T v = IO<T>::cvt(0.f);
+    if (s < S && c < C)
+      v = wlayout == MS_NHWC ? w[(((int64_t)n * R + r) * S + s) * C + c]
+                             : w[(((int64_t)n * C + c) * R + r) * S + s];
+    out[i] = v;
+  }
+}
+
+}  // namespace
+
+bool stem_fprop_ok(int dt, int layout, int c, int r, int s, int sh, int sw, int ph, int pw,
+                   int64_t ow, int64_t k) {
+  return (dt == MS_BF16 || dt == MS_F16) && layout == MS_NHWC && c <= 4 && r == SF_R && s == 7 &&
+         sh == 2 && sw == 2 && ph == 3 && pw == 3 && ow <= BM && k % 64 == 0 && k <= 128;
+}
+
+size_t stem_fprop_weight_bytes(int k) { return (size_t)SF_R * 4 * k * 16; }
+
+// xp: pad_rowseg output [n][h][wp][4]; wb: workspace of stem_fprop_weight_bytes(k)
+ms_status stem_fprop(int dt, int n, int h, int wp, int p, int q, int k, int c, int wlayout,
+                     const void* xp, const void* w, void* wb, const void* bias, void* y,
+                     cudaStream_t st) {
+  const int total = SF_R * 4 * k * 8;
+  const int blocks = (total + 255) / 256;
+  if (dt == MS_BF16)
+    repack_stem_fprop_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>(
+        k, c, SF_R, 7, wlayout, (const __nv_bfloat16*)w, (__nv_bfloat16*)wb);
+  else
+    repack_stem_fprop_kernel<__half><<<blocks, 256, 0, st>>>(k, c, SF_R, 7, wlayout,
+                                                             (const __half*)w, (__half*)wb);
+  count_launch();
+  MS_TRY(launch_status("repack_stem_fprop"));
+  StemFpropArgs a{};
+  a.N = n; a.H = h; a.Wp = wp; a.P = p; a.Q = q; a.K = k;
+  a.units = n * p;
+  a.y = y; a.bias = bias; a.dt = dt; a.xp = xp; a.wb = wb;
+  const int smem =
+      SF_STG + (int)stem_fprop_weight_bytes(k) + SF_SLOT + SF_STAGES * SF_STAGE + 1024 + 256;
+  const int grid = a.units < num_sms() ? a.units : num_sms();
+  CUtensorMap ty;
+  const size_t es = dtype_size(dt);
+  const uint64_t dims[3] = {(uint64_t)k, (uint64_t)q, (uint64_t)n * p};
+  const uint64_t str[2] = {(uint64_t)k * es, (uint64_t)q * k * es};
+  const uint32_t box[3] = {64, 32, 1};
+  MS_TRY(make_tmap_nd(&ty, dt, y, 3, dims, str, box, 128));
+  if (dt == MS_BF16) {
+    auto kern = stem_fprop_kernel<__nv_bfloat16>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    kern<<<grid, SF_THREADS, smem, st>>>(a, ty);
+  } else {
+    auto kern = stem_fprop_kernel<__half>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    kern<<<grid, SF_THREADS, smem, st>>>(a, ty);
+  }
+  count_launch(1, KF_UMMA);
+  return launch_status("stem_fprop_kernel");
+}
+
 }  // namespace ms
