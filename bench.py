@@ -286,7 +286,10 @@ def gpu_main(args):
         pass  # weak scaling: every rank keeps the full per-GPU batch
     stock_model = copy.deepcopy(wl.model)
     layers_model = copy.deepcopy(wl.model) if not args.no_stock else None
-    convert_to_memory_saving(wl.model)
+    unfused_model = copy.deepcopy(wl.model) if not args.no_stock else None
+    # the product: every supported layer swapped, conv -> BN(eval) -> ReLU and
+    # add -> ReLU chains fused by the fx pass (same saved set, fewer HBM passes)
+    wl.model = convert_to_memory_saving(wl.model, fuse=not args.no_fuse)
     inputs = list(wl.make_batch(wl.batch, dev))
     if wl.input_requires_grad:
         inputs[0].requires_grad_(True)
@@ -346,6 +349,22 @@ def gpu_main(args):
             "swaps": "Linear, Conv2d, BatchNorm2d(eval) only"}
         del lstep, linputs
         torch.cuda.empty_cache()
+        if not args.no_fuse:  # every layer swapped, no fx fusion
+            unfused_model = convert_to_memory_saving(unfused_model, fuse=False)
+            uinputs = list(wl.make_batch(wl.batch, dev))
+            if wl.input_requires_grad:
+                uinputs[0].requires_grad_(True)
+            usync = TrainableGradAllReduce(unfused_model) if world > 1 else None
+            ums, ustep = run_arm(wl, unfused_model, uinputs, args.steps, args.warmup, world, dev,
+                                 usync)
+            upeak, uact = peak_memory(ustep, dev)
+            stock["memsave_unfused"] = {
+                "value": round(samples / (ums / 1e3), 2),
+                "ms_per_step": round(ums / args.steps, 4), "peak_mib": round(upeak, 1),
+                "activation_peak_mib": round(uact, 1),
+                "swaps": "all supported layers, convert_to_memory_saving(fuse=False)"}
+            del ustep, uinputs
+            torch.cuda.empty_cache()
 
     # ---------------- roofline of the dominant kernel (rank 0)
     roof = None
@@ -494,6 +513,8 @@ def main():
                     choices=["resnet18", "fig1", "resnet101", "vgg16", "bert", "llama"])
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--no-stock", action="store_true")
+    ap.add_argument("--no-fuse", action="store_true",
+                    help="product arm without the conv->BN->ReLU / add->ReLU fx fusion")
     ap.add_argument("--no-roofline", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)

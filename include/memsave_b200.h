@@ -135,6 +135,36 @@ MS_API ms_status ms_relu_fwd(int64_t numel, int32_t dtype, const void* x, void* 
 MS_API ms_status ms_relu_bwd(int64_t numel, int32_t dtype, const void* g, const void* mask,
                              void* dx, void* stream);
 
+/* y = relu(a + b) with the ReLU's bit mask: the residual add of a ResNet block
+ * fused with the ReLU that follows it (backward = ms_relu_bwd, whose result is
+ * the gradient of both a and b).  y may alias a or b.                       */
+MS_API ms_status ms_add_relu_fwd(int64_t numel, int32_t dtype, const void* a, const void* b,
+                                 void* y, void* mask_or_null, void* stream);
+
+/* ------------------------------------------------------------ conv2d + batchnorm2d(eval) [+ relu]
+ * The conv -> eval-BN (-> ReLU) chain of a frozen-normalisation network in one
+ * launch: the BN affine y = conv*s + t (s = w/sqrt(var+eps), t = b - mean*s)
+ * and the ReLU (keep bits to mask, as ms_relu_fwd) run in the conv's tcgen05
+ * epilogue; nothing is materialised between the three layers.  The saved set
+ * is the union of the three layers' rows (conv: W iff x needs a grad; BN with
+ * frozen parameters: nothing; ReLU: the bit mask).  16-bit NHWC, K % 8 == 0
+ * (MS_ERR_UNSUPPORTED otherwise: the caller runs the three layers).
+ * Workspace: ms_conv2d_bn_workspace(d).  Backward: ms_bn_relu_bwd then
+ * ms_conv2d_dx / ms_conv2d_dw.                                              */
+MS_API size_t ms_conv2d_bn_workspace(const ms_conv_desc* d);
+MS_API ms_status ms_conv2d_bn_fwd(const ms_conv_desc* d, const void* x, const void* w,
+                                  const void* bias_or_null, const void* bn_mean,
+                                  const void* bn_var, const void* bn_weight_or_null,
+                                  const void* bn_bias_or_null, int32_t bn_pdtype, double eps,
+                                  int32_t relu, void* y, void* mask_or_null, void* ws,
+                                  size_t ws_bytes, void* stream);
+/* dx = g * keep * w/sqrt(var+eps) per channel (NHWC, C % 8 == 0, 16-bit);
+ * mask_or_null = NULL for a conv -> BN chain without ReLU.                  */
+MS_API ms_status ms_bn_relu_bwd(int64_t numel, int64_t c, int32_t dtype, int32_t pdtype,
+                                const void* g, const void* mask_or_null, const void* mean,
+                                const void* var, const void* weight_or_null, double eps,
+                                void* dx, void* stream);
+
 /* ------------------------------------------------------------ maxpool2d (index map)
  * MemSave MaxPool2d (rules.py:108-109, saved.py:111-125, kernels
  * numpy_impl.py:54-78): the argmax is kept as the window-local offset

@@ -443,3 +443,75 @@ extern "C" ms_status ms_bn_eval_bwd(int64_t n, int64_t c, int64_t hw, int32_t la
   return ms::bn_eval_bwd(n, c, hw, layout, dtype, p, dy, x_or_null, dx_or_null, dw_or_null,
                          db_or_null, ws, ws_bytes, (cudaStream_t)stream);
 }
+
+// ---------------------------------------------------------------- BN-eval + ReLU backward
+// dx = g * keep * scale_c for the fused conv + BN-eval (+ ReLU) forward
+// (NHWC, C % 8 == 0): one mask byte = 8 consecutive channels of one pixel
+namespace ms {
+namespace {
+template <typename T>
+__global__ void __launch_bounds__(256) bn_relu_bwd_kernel(int64_t groups, int C, BnParams p,
+                                                          const T* __restrict__ g,
+                                                          const uint8_t* __restrict__ mask,
+                                                          T* __restrict__ dx) {
+  extern __shared__ float s_scale[];
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    float sc, sf, inv, mu;
+    bn_channel_consts(p, c, sc, sf, inv, mu);
+    s_scale[c] = sc;
+  }
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t g0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g0 < groups;
+       g0 += stride * BN_UNR) {
+    float v[BN_UNR][8];
+    uint32_t bits[BN_UNR];
+#pragma unroll
+    for (int u = 0; u < BN_UNR; ++u) {
+      const int64_t gi = g0 + u * stride;
+      if (gi < groups) {
+        load_vec<T, 8>(g + gi * 8, v[u]);
+        bits[u] = mask ? mask[gi] : 0xFFu;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < BN_UNR; ++u) {
+      const int64_t gi = g0 + u * stride;
+      if (gi >= groups) continue;
+      const int c0 = (int)((gi * 8) % C);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[u][j] = (bits[u] >> j) & 1u ? v[u][j] * s_scale[c0 + j] : 0.f;
+      store_vec<T, 8>(dx + gi * 8, v[u]);
+    }
+  }
+}
+}  // namespace
+}  // namespace ms
+
+extern "C" ms_status ms_bn_relu_bwd(int64_t numel, int64_t c, int32_t dtype, int32_t pdtype,
+                                    const void* g, const void* mask_or_null, const void* mean,
+                                    const void* var, const void* weight, double eps, void* dx,
+                                    void* stream) {
+  MS_TRY(ms::bind_device(dx));
+  MS_CHECK_ARG(numel >= 0 && c > 0 && c % 8 == 0 && c <= 8192 && numel % c == 0, MS_ERR_SHAPE,
+               "bn_relu_bwd: NHWC with C %% 8 == 0 required");
+  MS_CHECK_ARG(dtype == MS_BF16 || dtype == MS_F16, MS_ERR_DTYPE, "bn_relu_bwd: 16-bit only");
+  MS_CHECK_ARG(((reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(dx)) & 15) == 0,
+               MS_ERR_ALIGN, "bn_relu_bwd: 16-byte alignment");
+  if (numel == 0) return MS_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  ms::BnParams p{mean, var, weight, nullptr, pdtype, (float)eps};
+  const int64_t groups = numel / 8;
+  int64_t blocks = (groups + 255) / 256;
+  if (blocks > (int64_t)ms::num_sms() * 8) blocks = (int64_t)ms::num_sms() * 8;
+  const size_t smem = sizeof(float) * c;
+  if (dtype == MS_BF16)
+    ms::bn_relu_bwd_kernel<__nv_bfloat16><<<(unsigned)blocks, 256, smem, st>>>(
+        groups, (int)c, p, (const __nv_bfloat16*)g, (const uint8_t*)mask_or_null,
+        (__nv_bfloat16*)dx);
+  else
+    ms::bn_relu_bwd_kernel<__half><<<(unsigned)blocks, 256, smem, st>>>(
+        groups, (int)c, p, (const __half*)g, (const uint8_t*)mask_or_null, (__half*)dx);
+  ms::count_launch(1, ms::KF_BN);
+  return ms::launch_status("bn_relu_bwd");
+}

@@ -179,8 +179,25 @@ ConvShape shape_of(const ConvDims& c, int C, int H, int W, int cblocks, int wpit
 }
 
 // ----------------------------------------------------------------- forward
+// optional epilogue fusion of a following eval-BatchNorm (+ ReLU with its mask)
+struct Fuse {
+  const float* scale = nullptr;
+  const float* shift = nullptr;
+  int relu = 0;
+  uint8_t* mask = nullptr;
+};
+
+void apply_fuse(EpiParams& e, const Fuse* f) {
+  if (!f) return;
+  e.scale = f->scale;
+  e.shift = f->shift;
+  e.relu = f->relu;
+  e.mask = f->mask;
+}
+
 ms_status fwd_rowseg(const ms_conv_desc* d, const ConvPlan& p, const void* x, const void* w,
-                     const void* bias, void* y, void* ws, cudaStream_t st) {
+                     const void* bias, void* y, void* ws, cudaStream_t st,
+                     const Fuse* f = nullptr) {
   const ConvDims c = dims_of(d);
   const int dt = d->dtype;
   uint8_t* wsb = static_cast<uint8_t*>(ws);
@@ -192,7 +209,8 @@ ms_status fwd_rowseg(const ms_conv_desc* d, const ConvPlan& p, const void* x, co
                                    c.k) &&
       stem_fprop_weight_bytes(c.k) <= p.ws_w)
     return stem_fprop(dt, c.n, c.h, p.xw_pad, c.oh, c.ow, c.k, c.c, d->wlayout, x4, w, wr, bias, y,
-                      st);
+                      st, f ? f->scale : nullptr, f ? f->shift : nullptr, f ? f->relu : 0,
+                      f ? f->mask : nullptr);
   MS_TRY(repack_rowseg(dt, c.k, c.c, c.r, c.s, d->wlayout, w, wr, st));
   GemmArgs g = base_args(dt);
   g.M = c.n * c.oh * c.ow;
@@ -202,6 +220,7 @@ ms_status fwd_rowseg(const ms_conv_desc* d, const ConvPlan& p, const void* x, co
   g.num_tiles = c.n * c.oh * g.n_blocks;
   g.cv = shape_of(c, 4, c.h, p.xw_pad, 1, 32, c.oh, c.ow);
   g.epi = EpiParams{y, c.k, dt, 0, bias, dt};
+  apply_fuse(g.epi, f);
   TmapPack tm;
   const size_t es = dtype_size(dt);
   const uint64_t dims[4] = {32, (uint64_t)c.ow, (uint64_t)c.h, (uint64_t)c.n};
@@ -218,8 +237,8 @@ ms_status fwd_rowseg(const ms_conv_desc* d, const ConvPlan& p, const void* x, co
 }
 
 ms_status fwd_tc(const ms_conv_desc* d, const ConvPlan& p, const void* x, const void* w,
-                 const void* bias, void* y, void* ws, cudaStream_t st) {
-  if (p.rowseg) return fwd_rowseg(d, p, x, w, bias, y, ws, st);
+                 const void* bias, void* y, void* ws, cudaStream_t st, const Fuse* f = nullptr) {
+  if (p.rowseg) return fwd_rowseg(d, p, x, w, bias, y, ws, st, f);
   const ConvDims c = dims_of(d);
   const int dt = d->dtype;
   uint8_t* wsb = static_cast<uint8_t*>(ws);
@@ -246,6 +265,7 @@ ms_status fwd_tc(const ms_conv_desc* d, const ConvPlan& p, const void* x, const 
   g.k_blocks = (c.r * c.s + 7) / 8;  // C8 variant: 8 taps per k-block
   g.cv = shape_of(c, p.cpad8, c.h, c.w, p.c8 ? 1 : p.cpad / 64, p.cpad, c.oh, c.ow);
   g.epi = EpiParams{y, c.k, dt, 0, bias, dt};
+  apply_fuse(g.epi, f);
   TmapPack tm;
   const int lower[2] = {-c.pw, -c.ph};
   const int upper[2] = {c.pw - (c.s - 1), c.ph - (c.r - 1)};
@@ -536,4 +556,55 @@ extern "C" ms_status ms_conv_transpose2d_fwd(const ms_conv_desc* d, const void* 
   MS_TRY(s);
   if (bias) MS_TRY(add_channel_bias(d->dtype, d->layout, d->n, d->c, d->h * d->w, y, bias, st));
   return MS_OK;
+}
+
+// ----------------------------------------------------------------- conv + BN-eval (+ ReLU)
+namespace ms {
+namespace {
+__global__ void bn_scale_shift_kernel(int k, const void* mean, const void* var, const void* w,
+                                      const void* b, int pdt, float eps, float* scale,
+                                      float* shift) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= k) return;
+  const float mu = load_as_float(mean, pdt, c);
+  const float s = (w ? load_as_float(w, pdt, c) : 1.f) / sqrtf(load_as_float(var, pdt, c) + eps);
+  scale[c] = s;
+  shift[c] = (b ? load_as_float(b, pdt, c) : 0.f) - mu * s;
+}
+}  // namespace
+}  // namespace ms
+
+extern "C" size_t ms_conv2d_bn_workspace(const ms_conv_desc* d) {
+  if (validate(d) != MS_OK) return 0;
+  return plan(d, MS_CONV_FWD).ws + align256(2 * sizeof(float) * (size_t)d->k);
+}
+
+extern "C" ms_status ms_conv2d_bn_fwd(const ms_conv_desc* d, const void* x, const void* w,
+                                      const void* bias, const void* bn_mean, const void* bn_var,
+                                      const void* bn_weight, const void* bn_bias,
+                                      int32_t bn_pdtype, double eps, int32_t relu, void* y,
+                                      void* mask_or_null, void* ws, size_t ws_bytes,
+                                      void* stream) {
+  MS_TRY(validate(d));
+  MS_TRY(bind_device(y));
+  MS_CHECK_ARG(bn_mean && bn_var, MS_ERR_SHAPE, "conv+bn: running statistics required");
+  if (d->n == 0) return MS_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  ConvPlan p = plan(d, MS_CONV_FWD);
+  MS_CHECK_ARG(p.tc && d->k % 8 == 0, MS_ERR_UNSUPPORTED,
+               "conv+bn fusion needs the tcgen05 path (16-bit NHWC) and K %% 8 == 0");
+  MS_CHECK_ARG(ws && ws_bytes >= ms_conv2d_bn_workspace(d), MS_ERR_WORKSPACE,
+               "conv+bn: workspace %zu < %zu", ws_bytes, ms_conv2d_bn_workspace(d));
+  float* scale = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + p.ws);
+  float* shift = scale + d->k;
+  bn_scale_shift_kernel<<<(unsigned)((d->k + 127) / 128), 128, 0, st>>>(
+      (int)d->k, bn_mean, bn_var, bn_weight, bn_bias, bn_pdtype, (float)eps, scale, shift);
+  count_launch(1, KF_BN);
+  MS_TRY(launch_status("bn_scale_shift"));
+  Fuse f;
+  f.scale = scale;
+  f.shift = shift;
+  f.relu = relu;
+  f.mask = static_cast<uint8_t*>(mask_or_null);
+  return fwd_tc(d, p, x, w, bias, y, ws, st, &f);
 }

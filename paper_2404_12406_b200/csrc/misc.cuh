@@ -32,7 +32,8 @@ bool stem_fprop_ok(int dt, int layout, int c, int r, int s, int sh, int sw, int 
 size_t stem_fprop_weight_bytes(int k);
 ms_status stem_fprop(int dt, int n, int h, int wp, int p, int q, int k, int c, int wlayout,
                      const void* xp, const void* w, void* wb, const void* bias, void* y,
-                     cudaStream_t st);
+                     cudaStream_t st, const float* scale = nullptr, const float* shift = nullptr,
+                     int relu = 0, uint8_t* mask = nullptr);
 
 inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 inline size_t align256(size_t v) { return (v + 255) & ~static_cast<size_t>(255); }

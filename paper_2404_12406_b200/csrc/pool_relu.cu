@@ -41,9 +41,11 @@ __device__ __forceinline__ uint32_t relu8(float (&v)[8]) {
   return bits;
 }
 
+// y = relu(x [+ b]); b (nullable) is the residual operand of a fused add + ReLU
 template <typename T>
 __global__ void __launch_bounds__(256) relu_fwd_kernel(int64_t n, const T* x, T* y,
-                                                       uint8_t* __restrict__ mask, bool vec) {
+                                                       uint8_t* __restrict__ mask, bool vec,
+                                                       const T* b = nullptr) {
   const int64_t full = n / 8;  // complete groups
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t g0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g0 < full;
@@ -53,6 +55,18 @@ __global__ void __launch_bounds__(256) relu_fwd_kernel(int64_t n, const T* x, T*
     for (int u = 0; u < RELU_UNR; ++u) {
       const int64_t gi = g0 + u * stride;
       if (gi < full) ld8<T>(x + gi * 8, v[u], vec);
+    }
+    if (b) {
+      float w[RELU_UNR][8];
+#pragma unroll
+      for (int u = 0; u < RELU_UNR; ++u) {
+        const int64_t gi = g0 + u * stride;
+        if (gi < full) ld8<T>(b + gi * 8, w[u], vec);
+      }
+#pragma unroll
+      for (int u = 0; u < RELU_UNR; ++u)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[u][j] += w[u][j];
     }
 #pragma unroll
     for (int u = 0; u < RELU_UNR; ++u) {
@@ -67,7 +81,7 @@ __global__ void __launch_bounds__(256) relu_fwd_kernel(int64_t n, const T* x, T*
     const int64_t e = full * 8;
     uint32_t bits = 0;
     for (int j = 0; e + j < n; ++j) {
-      const float a = IO<T>::ld(x + e + j);
+      const float a = IO<T>::ld(x + e + j) + (b ? IO<T>::ld(b + e + j) : 0.f);
       const bool pos = !(a <= 0.f);
       bits |= (pos ? 1u : 0u) << j;
       y[e + j] = IO<T>::cvt(pos ? a : 0.f);
@@ -429,6 +443,19 @@ extern "C" ms_status ms_relu_fwd(int64_t numel, int32_t dt, const void* x, void*
                          numel, (const T*)x, (T*)y, (uint8_t*)mask_or_null, vec));
   count_launch();
   return launch_status("relu_fwd_kernel");
+}
+
+extern "C" ms_status ms_add_relu_fwd(int64_t numel, int32_t dt, const void* a, const void* b,
+                                     void* y, void* mask_or_null, void* stream) {
+  MS_CHECK_ARG(numel >= 0 && a && b && y, MS_ERR_SHAPE, "add_relu: bad arguments");
+  if (numel == 0) return MS_OK;
+  MS_TRY(bind_device(y));
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool vec = al16(a) && al16(b) && al16(y);
+  MS_DT_DISPATCH(dt, relu_fwd_kernel<T><<<grid_for((numel + 31) / 32), 256, 0, st>>>(
+                         numel, (const T*)a, (T*)y, (uint8_t*)mask_or_null, vec, (const T*)b));
+  count_launch();
+  return launch_status("add_relu_fwd_kernel");
 }
 
 extern "C" ms_status ms_relu_bwd(int64_t numel, int32_t dt, const void* g, const void* mask,

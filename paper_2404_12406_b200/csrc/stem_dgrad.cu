@@ -311,6 +311,10 @@ struct StemFpropArgs {
   int dt;
   const void* xp;  // padded input
   const void* wb;  // weights in core-matrix layout [r][kg 4][K][8]
+  const float* scale;  // fused eval-BN (nullable): y = conv * scale[k] + shift[k]
+  const float* shift;
+  int relu;            // fused ReLU; keep bits to mask (1 bit per element, NHWC order)
+  uint8_t* mask;
 };
 
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
@@ -470,6 +474,8 @@ __global__ void __launch_bounds__(SF_THREADS, 1)
         uint8_t* sb = stg + (ew * 2 + (nst & 1)) * 4096;
         if (lane == 0) bulk_wait_read<1>();  // the store issued 2 chunks ago has read sb
         __syncwarp();
+        const int ow = quarter * 32 + rw;
+        uint64_t keep = 0;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           float f[8];
@@ -478,6 +484,12 @@ __global__ void __launch_bounds__(SF_THREADS, 1)
             const int ch = q * 8 + j;
             f[j] = __uint_as_float(ch < 32 ? v0[ch] : v1[ch - 32]);
             if (a.bias) f[j] += IO<T>::ld(static_cast<const T*>(a.bias) + c0 + ch);
+            if (a.scale) f[j] = f[j] * __ldg(a.scale + c0 + ch) + __ldg(a.shift + c0 + ch);
+            if (a.relu) {
+              const bool pos = !(f[j] <= 0.f);
+              keep |= (pos ? 1ull : 0ull) << ch;
+              f[j] = pos ? f[j] : 0.f;
+            }
           }
           uint4 pk;
           pk.x = pack2<T>(f[0], f[1]);
@@ -486,6 +498,9 @@ __global__ void __launch_bounds__(SF_THREADS, 1)
           pk.w = pack2<T>(f[6], f[7]);
           *reinterpret_cast<uint4*>(sb + rw * 128 + ((q ^ (rw & 7)) << 4)) = pk;
         }
+        if (a.relu && a.mask && ow < a.Q)  // 64 channels = 8 mask bytes (K % 64 == 0)
+          reinterpret_cast<uint64_t*>(a.mask)[((static_cast<int64_t>(u) * a.Q + ow) * a.K + c0) >> 6] =
+              keep;
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
@@ -533,7 +548,8 @@ size_t stem_fprop_weight_bytes(int k) { return (size_t)SF_R * 4 * k * 16; }
 // xp: pad_rowseg output [n][h][wp][4]; wb: workspace of stem_fprop_weight_bytes(k)
 ms_status stem_fprop(int dt, int n, int h, int wp, int p, int q, int k, int c, int wlayout,
                      const void* xp, const void* w, void* wb, const void* bias, void* y,
-                     cudaStream_t st) {
+                     cudaStream_t st, const float* scale, const float* shift, int relu,
+                     uint8_t* mask) {
   const int total = SF_R * 4 * k * 8;
   const int blocks = (total + 255) / 256;
   if (dt == MS_BF16)
@@ -548,6 +564,7 @@ ms_status stem_fprop(int dt, int n, int h, int wp, int p, int q, int k, int c, i
   a.N = n; a.H = h; a.Wp = wp; a.P = p; a.Q = q; a.K = k;
   a.units = n * p;
   a.y = y; a.bias = bias; a.dt = dt; a.xp = xp; a.wb = wb;
+  a.scale = scale; a.shift = shift; a.relu = relu; a.mask = mask;
   const int smem =
       SF_STG + (int)stem_fprop_weight_bytes(k) + SF_SLOT + SF_STAGES * SF_STAGE + 1024 + 256;
   const int grid = a.units < num_sms() ? a.units : num_sms();

@@ -83,6 +83,13 @@ struct EpiParams {
   int atomic;        // 1: fp32 red.add into out (split-K / wgrad workspace)
   const void* bias;  // per-column bias (nullable)
   int bias_dtype;
+  // fused eval-BatchNorm + ReLU (conv forward): v = v * scale[col] + shift[col],
+  // then v = max(v, 0) with the keep bit of every element written to mask
+  // (1 bit per element in storage order, as ms_relu_fwd)
+  const float* scale;  // nullable
+  const float* shift;
+  int relu;
+  uint8_t* mask;       // nullable
 };
 
 struct GemmArgs {
@@ -683,6 +690,42 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
 #pragma unroll
             for (int j = 0; j < 32; ++j)
               if (nc + j < ncols) v[j] += load_as_float(e.bias, e.bias_dtype, nc + j);
+          }
+          if (e.scale != nullptr) {  // folded eval-BN: per-column affine in fp32
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              if (full) {
+                const float4 s4 = __ldg(reinterpret_cast<const float4*>(e.scale + nc) + q);
+                const float4 t4 = __ldg(reinterpret_cast<const float4*>(e.shift + nc) + q);
+                v[4 * q] = v[4 * q] * s4.x + t4.x;
+                v[4 * q + 1] = v[4 * q + 1] * s4.y + t4.y;
+                v[4 * q + 2] = v[4 * q + 2] * s4.z + t4.z;
+                v[4 * q + 3] = v[4 * q + 3] * s4.w + t4.w;
+              } else {
+#pragma unroll
+                for (int h = 0; h < 4; ++h)
+                  if (nc + 4 * q + h < ncols)
+                    v[4 * q + h] = v[4 * q + h] * e.scale[nc + 4 * q + h] + e.shift[nc + 4 * q + h];
+              }
+            }
+          }
+          if (e.relu) {
+            uint32_t bits = 0;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const bool pos = !(v[j] <= 0.f);  // NaN propagates, as ms_relu_fwd
+              bits |= (pos ? 1u : 0u) << j;
+              v[j] = pos ? v[j] : 0.f;
+            }
+            if (e.mask != nullptr && valid) {
+              const int64_t el = orow * e.ldc + col_base + c;  // first element of the chunk
+              if (full && (el & 31) == 0) {
+                reinterpret_cast<uint32_t*>(e.mask)[el >> 5] = bits;
+              } else {
+                for (int j = 0; j < 32 && nc + j < ncols; j += 8)
+                  e.mask[(el + j) >> 3] = static_cast<uint8_t>(bits >> j);
+              }
+            }
           }
           if (!valid && !tma_st) continue;
           if constexpr (Cfg::CAN_TMA_STORE) {

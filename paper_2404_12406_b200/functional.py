@@ -779,3 +779,209 @@ class _ConvTranspose2dFn(torch.autograd.Function):
 def conv_transpose2d(x, weight, bias=None, stride=1, padding=0, output_padding=0):
     """Differentiability-agnostic ``F.conv_transpose2d`` (groups = dilation = 1)."""
     return _ConvTranspose2dFn.apply(x, weight, bias, stride, padding, output_padding)
+
+
+# =============================================================== fused conv -> BN-eval (-> ReLU)
+def _bn_frozen_eval(bn) -> bool:
+    return (not bn.training and bn.running_mean is not None and bn.running_var is not None
+            and not any(p.requires_grad for p in bn.parameters()))
+
+
+class _ConvBNFn(torch.autograd.Function):
+    """conv2d -> BatchNorm2d(eval, frozen) [-> ReLU] in one tcgen05 launch (BN affine
+    and ReLU in the conv epilogue).  Saved set = the union of the three layers'
+    rows: W iff x needs a grad and x iff W needs one (rules.py:68-71, MEMSAVE),
+    nothing for the frozen eval-BN (rules.py:84-87), the ReLU bit mask iff the
+    output needs a grad (rules.py:98-101).  Backward: dg = g*mask*s per channel
+    (ms_bn_relu_bwd), then the conv products that were requested."""
+
+    @staticmethod
+    def forward(ctx, x, weight, bias, stride, padding, bn, relu: bool):
+        x_rg, w_rg, b_rg = ctx.needs_input_grad[0], ctx.needs_input_grad[1], ctx.needs_input_grad[2]
+        out_rg = x_rg or w_rg or b_rg
+        roles = saved_roles(x_rg, w_rg)
+        stride, padding = _pair(stride), _pair(padding)
+        oh, ow = _conv_out_hw(x.shape, weight.shape, stride, padding)
+        ctx.geom = (tuple(x.shape), tuple(weight.shape), stride, padding)
+        ctx.w_meta = (weight.dtype, False)
+        ctx.bn = (bn.running_mean, bn.running_var, bn.weight, float(bn.eps))
+        ctx.relu = bool(relu)
+        out_shape = (x.shape[0], weight.shape[0], oh, ow)
+        n_el = x.shape[0] * weight.shape[0] * oh * ow
+        if _is_meta(x, weight):
+            mask = (torch.empty((n_el + 7) // 8, dtype=torch.uint8, device="meta")
+                    if relu and out_rg else None)
+            ctx.save_for_backward(x if "x" in roles else None, weight if "w" in roles else None,
+                                  mask)
+            ctx.layouts = (_lib.MS_NCHW, _lib.MS_NCHW)
+            return x.new_empty(out_shape)
+        _require_cuda("conv_bn", x, weight, bias)
+        layout, wlayout = _conv_layouts(x, weight)
+        xl = _as_layout(x, layout)
+        wl = _as_layout(weight, wlayout)
+        ctx.layouts = (layout, wlayout)
+        dt = _dtype_code(x)
+        d = _conv_desc(x.shape, weight.shape, stride, padding, layout, wlayout, dt)
+        y = _empty4(out_shape, x, layout)
+        mask = torch.empty((n_el + 7) // 8, dtype=torch.uint8, device=x.device) \
+            if relu and out_rg else None
+        b = None if bias is None else bias.to(x.dtype).contiguous()
+        mean, var, bw, eps = ctx.bn
+        bb = bn.bias
+        L = _lib.lib()
+        ws, nb = _workspace(L.ms_conv2d_bn_workspace(ctypes.byref(d)), x.device)
+        _lib.check(L.ms_conv2d_bn_fwd(ctypes.byref(d), _ptr(xl), _ptr(wl), _ptr(b), _ptr(mean),
+                                      _ptr(var), _ptr(bw), _ptr(bb), _dtype_code(mean), eps,
+                                      int(relu), _ptr(y), _ptr(mask), _ptr(ws), nb,
+                                      _stream(x.device)), "ms_conv2d_bn_fwd")
+        ctx.save_for_backward(xl if "x" in roles else None, wl if "w" in roles else None, mask)
+        return y
+
+    @staticmethod
+    def backward(ctx, gy):
+        x, w, mask = ctx.saved_tensors
+        need_x, need_w, need_b = ctx.needs_input_grad[:3]
+        x_shape, w_shape, stride, padding = ctx.geom
+        dx = dw = db = None
+        layout, wlayout = ctx.layouts
+        g = _as_layout(gy, layout)
+        if ctx.relu:
+            _need(mask, "mask", "conv_bn_relu backward")
+        if _is_meta(g):  # mirror the CUDA path's allocations for the planner
+            folded = not ctx.relu and need_x and not need_w and not need_b
+            gc = g if folded else torch.empty_like(g)
+            if need_x:
+                _need(w, "w", "conv_bn dX")
+                dx = gc.new_empty(x_shape)
+            if need_w:
+                _need(x, "x", "conv_bn dW")
+                dw = gc.new_empty(w_shape)
+            if need_b:
+                db = gc.new_empty((w_shape[0],))
+            return dx, dw, db, None, None, None, None
+        mean, var, bw, eps = ctx.bn
+        L = _lib.lib()
+        st = _stream(g.device)
+        if not ctx.relu and need_x and not need_w and not need_b:
+            # no mask to apply: fold the BN scale into the (small) weight instead of
+            # scaling the (large) gradient -- dX = dgrad(g, W * s[k])
+            w = _need(w, "w", "conv_bn dX")
+            sc = (bw.float() if bw is not None else 1.0) * torch.rsqrt(var.float() + eps)
+            ws_ = (w.float() * sc.view(-1, 1, 1, 1)).to(w.dtype)
+            ws_ = _as_layout(ws_, wlayout)
+            d = _conv_desc(x_shape, w_shape, stride, padding, layout, wlayout, _dtype_code(g))
+            dx = _empty4(x_shape, g, layout)
+            wsp, nb = _workspace(L.ms_conv2d_workspace(ctypes.byref(d), _lib.MS_CONV_DX), g.device)
+            _lib.check(L.ms_conv2d_dx(ctypes.byref(d), _ptr(g), _ptr(ws_), _ptr(dx), _ptr(wsp), nb,
+                                      st), "ms_conv2d_dx")
+            return dx, None, None, None, None, None, None
+        gc = torch.empty_like(g, memory_format=torch.channels_last
+                              if layout == _lib.MS_NHWC else torch.contiguous_format)
+        _lib.check(L.ms_bn_relu_bwd(g.numel(), w_shape[0], _dtype_code(g), _dtype_code(mean),
+                                    _ptr(g), _ptr(mask), _ptr(mean), _ptr(var), _ptr(bw), eps,
+                                    _ptr(gc), st), "ms_bn_relu_bwd")
+        del g
+        dt = _dtype_code(gc)
+        d = _conv_desc(x_shape, w_shape, stride, padding, layout, wlayout, dt)
+        if need_x:
+            w = _need(w, "w", "conv_bn dX")
+            dx = _empty4(x_shape, gc, layout)
+            ws, nb = _workspace(L.ms_conv2d_workspace(ctypes.byref(d), _lib.MS_CONV_DX), gc.device)
+            _lib.check(L.ms_conv2d_dx(ctypes.byref(d), _ptr(gc), _ptr(w), _ptr(dx), _ptr(ws), nb,
+                                      st), "ms_conv2d_dx")
+        if need_w:
+            x = _need(x, "x", "conv_bn dW")
+            dw = torch.empty(w_shape, dtype=ctx.w_meta[0], device=gc.device,
+                             memory_format=torch.channels_last if wlayout == _lib.MS_NHWC
+                             else torch.contiguous_format)
+            ws, nb = _workspace(L.ms_conv2d_workspace(ctypes.byref(d), _lib.MS_CONV_DW), gc.device)
+            _lib.check(L.ms_conv2d_dw(ctypes.byref(d), _ptr(x), _ptr(gc), _ptr(dw), _ptr(ws), nb,
+                                      st), "ms_conv2d_dw")
+        if need_b:
+            db = torch.empty((w_shape[0],), dtype=gc.dtype, device=gc.device)
+            ws, nb = _workspace(4 * w_shape[0], gc.device)
+            _lib.check(L.ms_conv2d_db(ctypes.byref(d), _ptr(gc), _ptr(db), _ptr(ws), nb, st),
+                       "ms_conv2d_db")
+        return dx, dw, db, None, None, None, None
+
+
+def conv_bn_fusable(x: torch.Tensor, conv, bn) -> bool:
+    """The fused launch applies: frozen eval-mode BN, plain conv (groups = dilation
+    = 1, zeros padding), 16-bit activations on CUDA, K % 8 == 0."""
+    if not _bn_frozen_eval(bn) or x.dim() != 4:
+        return False
+    if conv.groups != 1 or tuple(conv.dilation) != (1, 1) or conv.padding_mode != "zeros":
+        return False
+    if isinstance(conv.padding, str) or conv.out_channels % 8:
+        return False
+    if x.device.type == "meta":
+        return x.dtype in (torch.bfloat16, torch.float16)
+    return x.device.type == "cuda" and x.dtype in (torch.bfloat16, torch.float16) \
+        and conv.weight.dtype == x.dtype and bn.running_mean.device == x.device
+
+
+def conv_bn_relu(x: torch.Tensor, conv, bn, with_relu: bool) -> torch.Tensor:
+    """conv -> bn -> (relu) of the given modules: one fused launch when
+    ``conv_bn_fusable`` holds, else the layers in sequence (BN in training mode
+    or with trainable parameters, float32, ...)."""
+    if conv_bn_fusable(x, conv, bn):
+        return _ConvBNFn.apply(x, conv.weight, conv.bias, conv.stride, conv.padding, bn,
+                               with_relu)
+    y = bn(conv(x))
+    if not with_relu:
+        return y
+    # the ReLU module was folded into this call: keep its MemSave storage (bit mask)
+    return relu(y) if y.device.type in ("cuda", "meta") else torch.relu(y)
+
+
+# =============================================================== fused residual add + ReLU
+class _AddReLUFn(torch.autograd.Function):
+    """relu(a + b) with the ReLU's bit mask (rules.py:98-101; the add saves
+    nothing, rules.py:116-117); backward: one masked gradient for both operands."""
+
+    @staticmethod
+    def forward(ctx, a, b):
+        out_rg = ctx.needs_input_grad[0] or ctx.needs_input_grad[1]
+        n = a.numel()
+        if _is_meta(a, b):
+            ctx.save_for_backward(torch.empty((n + 7) // 8, dtype=torch.uint8, device="meta")
+                                  if out_rg else None)
+            ctx.fmt = torch.contiguous_format
+            return a.new_empty(a.shape)
+        _require_cuda("add_relu", a, b)
+        fmt = _dense_format(a)
+        if fmt is None or _dense_format(b) != fmt or a.dtype != b.dtype or a.shape != b.shape:
+            raise RuntimeError("add_relu: operands must share shape, dtype and a dense layout")
+        ctx.fmt = fmt
+        y = torch.empty_like(a, memory_format=fmt)
+        mask = torch.empty((n + 7) // 8, dtype=torch.uint8, device=a.device) if out_rg else None
+        L = _lib.lib()
+        _lib.check(L.ms_add_relu_fwd(n, _dtype_code(a), _ptr(a), _ptr(b), _ptr(y), _ptr(mask),
+                                     _stream(a.device)), "ms_add_relu_fwd")
+        ctx.save_for_backward(mask)
+        return y
+
+    @staticmethod
+    def backward(ctx, gy):
+        (mask,) = ctx.saved_tensors
+        mask = _need(mask, "mask", "add_relu backward")
+        g = gy.contiguous(memory_format=ctx.fmt)
+        if _is_meta(g):
+            dx = g.new_empty(g.shape)
+            return (dx if ctx.needs_input_grad[0] else None,
+                    dx if ctx.needs_input_grad[1] else None)
+        dx = torch.empty_like(g, memory_format=ctx.fmt)
+        L = _lib.lib()
+        _lib.check(L.ms_relu_bwd(g.numel(), _dtype_code(g), _ptr(g), _ptr(mask), _ptr(dx),
+                                 _stream(g.device)), "ms_relu_bwd")
+        return (dx if ctx.needs_input_grad[0] else None,
+                dx if ctx.needs_input_grad[1] else None)
+
+
+def add_relu(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+    """relu(a + b) in one pass (the residual add of a ResNet block + its ReLU)."""
+    fa, fb = _dense_format(a), _dense_format(b)
+    if (a.device.type in ("cuda", "meta") and a.shape == b.shape and a.dtype == b.dtype
+            and fa is not None and fa == fb):
+        return _AddReLUFn.apply(a, b)
+    return relu(a + b)

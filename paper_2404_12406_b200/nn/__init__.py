@@ -18,7 +18,7 @@ from .. import functional as MF
 
 __all__ = ["MemSaveLinear", "MemSaveConv2d", "MemSaveBatchNorm2d", "MemSaveReLU",
            "MemSaveMaxPool2d", "MemSaveDropout", "MemSaveLayerNorm", "MemSaveConvTranspose2d",
-           "convert_to_memory_saving"]
+           "convert_to_memory_saving", "fuse_conv_bn_relu"]
 
 
 def _share_params(dst: nn.Module, src: nn.Module, clone: bool) -> None:
@@ -253,12 +253,104 @@ def _convert_one(mod: nn.Module, kinds: dict, clone_params: bool, counter: list)
     return None
 
 
+def _is_relu(node, modules) -> bool:
+    import operator  # noqa: F401
+    if node.op == "call_module":
+        return isinstance(modules.get(node.target), nn.ReLU)
+    if node.op == "call_function":
+        return node.target in (torch.relu, torch.nn.functional.relu, torch.relu_)
+    if node.op == "call_method":
+        return node.target in ("relu", "relu_")
+    return False
+
+
+def _is_add(node) -> bool:
+    import operator
+    if node.op == "call_function" and node.target in (operator.add, operator.iadd, torch.add):
+        return len(node.args) == 2 and not node.kwargs
+    if node.op == "call_method" and node.target in ("add", "add_"):
+        return len(node.args) == 2 and not node.kwargs
+    return False
+
+
+def fuse_conv_bn_relu(model: nn.Module, verbose: bool = False) -> nn.Module:
+    """Graph pass (torch.fx) that fuses, without changing parameters, buffers or
+    state_dict keys:
+
+    * ``conv -> BatchNorm2d [-> ReLU]`` into one call of
+      :func:`functional.conv_bn_relu` (BN affine + ReLU in the conv's tcgen05
+      epilogue when the BN is in eval mode with frozen parameters; the three
+      layers otherwise, decided at run time);
+    * ``a + b -> ReLU`` (the residual join of a ResNet block) into
+      :func:`functional.add_relu`.
+
+    Each intermediate is consumed only by the next op of the chain.  The saved
+    set is the union of the fused layers' storage rules.  Models that torch.fx
+    cannot trace are returned unchanged."""
+    import torch.fx as fx
+
+    class _Tracer(fx.Tracer):  # the memsave layers are leaves, like torch.nn layers
+        def is_leaf_module(self, m, qualname):
+            return isinstance(m, _MEMSAVE_TYPES) or super().is_leaf_module(m, qualname)
+
+    try:
+        gm = fx.GraphModule(model, _Tracer().trace(model), type(model).__name__)
+    except Exception as exc:  # data-dependent control flow, unsupported ops ...
+        if verbose:
+            print(f"memsave: fx tracing failed ({type(exc).__name__}); no fusion")
+        return model
+    modules = dict(gm.named_modules())
+    g = gm.graph
+    nfused = nadd = 0
+    for node in list(g.nodes):
+        if node.op != "call_module" or not isinstance(modules.get(node.target), nn.BatchNorm2d):
+            continue
+        src = node.args[0] if node.args else None
+        if (not isinstance(src, fx.Node) or src.op != "call_module"
+                or type(modules.get(src.target)) not in (nn.Conv2d, MemSaveConv2d)
+                or len(src.users) != 1 or len(node.args) != 1 or node.kwargs):
+            continue
+        users = list(node.users)
+        relu_node = users[0] if len(users) == 1 and _is_relu(users[0], modules) else None
+        last = relu_node or node
+        with g.inserting_before(node):
+            conv_ref = g.get_attr(src.target)
+            bn_ref = g.get_attr(node.target)
+            fused = g.call_function(MF.conv_bn_relu,
+                                    (src.args[0], conv_ref, bn_ref, relu_node is not None))
+        last.replace_all_uses_with(fused)
+        for dead in ([relu_node] if relu_node else []) + [node, src]:
+            g.erase_node(dead)
+        nfused += 1
+    for node in list(g.nodes):
+        if not _is_add(node) or len(node.users) != 1:
+            continue
+        r = next(iter(node.users))
+        if not _is_relu(r, modules):
+            continue
+        a, b = node.args
+        if not (isinstance(a, fx.Node) and isinstance(b, fx.Node)):
+            continue
+        with g.inserting_before(node):
+            fused = g.call_function(MF.add_relu, (a, b))
+        r.replace_all_uses_with(fused)
+        g.erase_node(r)
+        g.erase_node(node)
+        nadd += 1
+    g.lint()
+    gm.recompile()
+    if verbose:
+        print(f"memsave: fused {nfused} conv->bn[->relu] and {nadd} add->relu chains")
+    return gm
+
+
 def convert_to_memory_saving(model: nn.Module, linear: bool = True, conv2d: bool = True,
                              conv1d: bool = False, conv3d: bool = False,
                              batchnorm2d: bool = True, relu: bool = True,
                              maxpool2d: bool = True, layernorm: bool = True,
                              dropout: bool = True, conv_transpose2d: bool = True,
-                             verbose: bool = False, clone_params: bool = False) -> nn.Module:
+                             verbose: bool = False, clone_params: bool = False,
+                             fuse: bool = False) -> nn.Module:
     """Swap supported layers of ``model`` for their MemSave equivalents, in place.
 
     Mirrors the reference ``convert_network(net, target, layer_filter)``
@@ -268,7 +360,9 @@ def convert_to_memory_saving(model: nn.Module, linear: bool = True, conv2d: bool
     (1-byte argmax), Dropout (RNG replay; node i of the traversal draws from
     stream DROPOUT_STREAM_BASE + i), LayerNorm and ConvTranspose2d are swapped
     too; conv1d/3d are accepted for API compatibility and left untouched.
-    Returns the (possibly replaced) model.
+    ``fuse=True`` additionally runs :func:`fuse_conv_bn_relu` (returns an
+    ``fx.GraphModule`` sharing the parameters, or the model unchanged when it
+    cannot be traced).  Returns the (possibly replaced) model.
     """
     kinds = {"linear": linear, "conv2d": conv2d, "batchnorm2d": batchnorm2d, "relu": relu,
              "maxpool2d": maxpool2d, "layernorm": layernorm, "dropout": dropout,
@@ -292,4 +386,6 @@ def convert_to_memory_saving(model: nn.Module, linear: bool = True, conv2d: bool
                 walk(child, f"{prefix}{name}.")
 
     walk(model, "")
+    if fuse:
+        return fuse_conv_bn_relu(model, verbose=verbose)
     return model
