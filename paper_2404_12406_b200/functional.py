@@ -792,8 +792,11 @@ class _ConvBNFn(torch.autograd.Function):
     and ReLU in the conv epilogue).  Saved set = the union of the three layers'
     rows: W iff x needs a grad and x iff W needs one (rules.py:68-71, MEMSAVE),
     nothing for the frozen eval-BN (rules.py:84-87), the ReLU bit mask iff the
-    output needs a grad (rules.py:98-101).  Backward: dg = g*mask*s per channel
-    (ms_bn_relu_bwd), then the conv products that were requested."""
+    output needs a grad (rules.py:98-101; kept by _MaskScaleFn, which also
+    applies it).  Returns (y, mask).  Backward gets dL/d(conv * s): with a ReLU
+    that is the masked, scaled gradient from _MaskScaleFn; without one the BN
+    scale is folded into the dgrad weight (dX = dgrad(g, W * s)) so the large
+    gradient is never rescaled."""
 
     @staticmethod
     def forward(ctx, x, weight, bias, stride, padding, bn, relu: bool):
@@ -811,10 +814,11 @@ class _ConvBNFn(torch.autograd.Function):
         if _is_meta(x, weight):
             mask = (torch.empty((n_el + 7) // 8, dtype=torch.uint8, device="meta")
                     if relu and out_rg else None)
-            ctx.save_for_backward(x if "x" in roles else None, weight if "w" in roles else None,
-                                  mask)
+            ctx.save_for_backward(x if "x" in roles else None, weight if "w" in roles else None)
             ctx.layouts = (_lib.MS_NCHW, _lib.MS_NCHW)
-            return x.new_empty(out_shape)
+            if mask is not None:
+                ctx.mark_non_differentiable(mask)
+            return x.new_empty(out_shape), mask
         _require_cuda("conv_bn", x, weight, bias)
         layout, wlayout = _conv_layouts(x, weight)
         xl = _as_layout(x, layout)
@@ -834,22 +838,30 @@ class _ConvBNFn(torch.autograd.Function):
                                       _ptr(var), _ptr(bw), _ptr(bb), _dtype_code(mean), eps,
                                       int(relu), _ptr(y), _ptr(mask), _ptr(ws), nb,
                                       _stream(x.device)), "ms_conv2d_bn_fwd")
-        ctx.save_for_backward(xl if "x" in roles else None, wl if "w" in roles else None, mask)
-        return y
+        ctx.save_for_backward(xl if "x" in roles else None, wl if "w" in roles else None)
+        if mask is not None:
+            ctx.mark_non_differentiable(mask)
+        return y, mask
 
     @staticmethod
-    def backward(ctx, gy):
-        x, w, mask = ctx.saved_tensors
+    def backward(ctx, gy, _gmask=None):
+        x, w = ctx.saved_tensors
         need_x, need_w, need_b = ctx.needs_input_grad[:3]
         x_shape, w_shape, stride, padding = ctx.geom
         dx = dw = db = None
         layout, wlayout = ctx.layouts
+        mean, var, bw, eps = ctx.bn
         g = _as_layout(gy, layout)
-        if ctx.relu:
-            _need(mask, "mask", "conv_bn_relu backward")
+        del gy
+        if not ctx.relu:
+            # dL/dconv = g * s: fold s into W for dX; scale g only for dW / db
+            sc_w = need_x
+            need_scaled_g = need_w or need_b
+        else:
+            sc_w = False  # g arrives already masked and scaled (_MaskScaleFn)
+            need_scaled_g = False
         if _is_meta(g):  # mirror the CUDA path's allocations for the planner
-            folded = not ctx.relu and need_x and not need_w and not need_b
-            gc = g if folded else torch.empty_like(g)
+            gc = torch.empty_like(g) if need_scaled_g else g
             if need_x:
                 _need(w, "w", "conv_bn dX")
                 dx = gc.new_empty(x_shape)
@@ -859,50 +871,72 @@ class _ConvBNFn(torch.autograd.Function):
             if need_b:
                 db = gc.new_empty((w_shape[0],))
             return dx, dw, db, None, None, None, None
-        mean, var, bw, eps = ctx.bn
         L = _lib.lib()
         st = _stream(g.device)
-        if not ctx.relu and need_x and not need_w and not need_b:
-            # no mask to apply: fold the BN scale into the (small) weight instead of
-            # scaling the (large) gradient -- dX = dgrad(g, W * s[k])
-            w = _need(w, "w", "conv_bn dX")
-            sc = (bw.float() if bw is not None else 1.0) * torch.rsqrt(var.float() + eps)
-            ws_ = (w.float() * sc.view(-1, 1, 1, 1)).to(w.dtype)
-            ws_ = _as_layout(ws_, wlayout)
-            d = _conv_desc(x_shape, w_shape, stride, padding, layout, wlayout, _dtype_code(g))
-            dx = _empty4(x_shape, g, layout)
-            wsp, nb = _workspace(L.ms_conv2d_workspace(ctypes.byref(d), _lib.MS_CONV_DX), g.device)
-            _lib.check(L.ms_conv2d_dx(ctypes.byref(d), _ptr(g), _ptr(ws_), _ptr(dx), _ptr(wsp), nb,
-                                      st), "ms_conv2d_dx")
-            return dx, None, None, None, None, None, None
-        gc = torch.empty_like(g, memory_format=torch.channels_last
-                              if layout == _lib.MS_NHWC else torch.contiguous_format)
-        _lib.check(L.ms_bn_relu_bwd(g.numel(), w_shape[0], _dtype_code(g), _dtype_code(mean),
-                                    _ptr(g), _ptr(mask), _ptr(mean), _ptr(var), _ptr(bw), eps,
-                                    _ptr(gc), st), "ms_bn_relu_bwd")
-        del g
-        dt = _dtype_code(gc)
+        dt = _dtype_code(g)
         d = _conv_desc(x_shape, w_shape, stride, padding, layout, wlayout, dt)
         if need_x:
             w = _need(w, "w", "conv_bn dX")
-            dx = _empty4(x_shape, gc, layout)
-            ws, nb = _workspace(L.ms_conv2d_workspace(ctypes.byref(d), _lib.MS_CONV_DX), gc.device)
-            _lib.check(L.ms_conv2d_dx(ctypes.byref(d), _ptr(gc), _ptr(w), _ptr(dx), _ptr(ws), nb,
+            if sc_w:
+                sc = (bw.float() if bw is not None else 1.0) * torch.rsqrt(var.float() + eps)
+                w = _as_layout((w.float() * sc.view(-1, 1, 1, 1)).to(w.dtype), wlayout)
+            dx = _empty4(x_shape, g, layout)
+            wsp, nb = _workspace(L.ms_conv2d_workspace(ctypes.byref(d), _lib.MS_CONV_DX), g.device)
+            _lib.check(L.ms_conv2d_dx(ctypes.byref(d), _ptr(g), _ptr(w), _ptr(dx), _ptr(wsp), nb,
                                       st), "ms_conv2d_dx")
-        if need_w:
-            x = _need(x, "x", "conv_bn dW")
-            dw = torch.empty(w_shape, dtype=ctx.w_meta[0], device=gc.device,
-                             memory_format=torch.channels_last if wlayout == _lib.MS_NHWC
-                             else torch.contiguous_format)
-            ws, nb = _workspace(L.ms_conv2d_workspace(ctypes.byref(d), _lib.MS_CONV_DW), gc.device)
-            _lib.check(L.ms_conv2d_dw(ctypes.byref(d), _ptr(x), _ptr(gc), _ptr(dw), _ptr(ws), nb,
-                                      st), "ms_conv2d_dw")
-        if need_b:
-            db = torch.empty((w_shape[0],), dtype=gc.dtype, device=gc.device)
-            ws, nb = _workspace(4 * w_shape[0], gc.device)
-            _lib.check(L.ms_conv2d_db(ctypes.byref(d), _ptr(gc), _ptr(db), _ptr(ws), nb, st),
-                       "ms_conv2d_db")
+        if need_w or need_b:
+            gc = g
+            if need_scaled_g:
+                gc = torch.empty_like(g, memory_format=torch.channels_last
+                                      if layout == _lib.MS_NHWC else torch.contiguous_format)
+                _lib.check(L.ms_bn_relu_bwd(g.numel(), w_shape[0], dt, _dtype_code(mean), _ptr(g),
+                                            None, _ptr(mean), _ptr(var), _ptr(bw), eps, _ptr(gc),
+                                            st), "ms_bn_relu_bwd")
+            if need_w:
+                x = _need(x, "x", "conv_bn dW")
+                dw = torch.empty(w_shape, dtype=ctx.w_meta[0], device=gc.device,
+                                 memory_format=torch.channels_last if wlayout == _lib.MS_NHWC
+                                 else torch.contiguous_format)
+                wsp, nb = _workspace(L.ms_conv2d_workspace(ctypes.byref(d), _lib.MS_CONV_DW),
+                                     gc.device)
+                _lib.check(L.ms_conv2d_dw(ctypes.byref(d), _ptr(x), _ptr(gc), _ptr(dw), _ptr(wsp),
+                                          nb, st), "ms_conv2d_dw")
+            if need_b:
+                db = torch.empty((w_shape[0],), dtype=gc.dtype, device=gc.device)
+                wsp, nb = _workspace(4 * w_shape[0], gc.device)
+                _lib.check(L.ms_conv2d_db(ctypes.byref(d), _ptr(gc), _ptr(db), _ptr(wsp), nb, st),
+                           "ms_conv2d_db")
         return dx, dw, db, None, None, None, None
+
+
+class _MaskScaleFn(torch.autograd.Function):
+    """Identity in forward on the fused conv->BN->ReLU output; keeps the ReLU bit
+    mask and in backward returns g * keep * s (one pass, ms_bn_relu_bwd).  A
+    separate autograd node so the engine frees the incoming gradient before the
+    dgrad allocates dX (two activation-sized buffers live, as unfused)."""
+
+    @staticmethod
+    def forward(ctx, y, mask, bn):
+        ctx.bn = (bn.running_mean, bn.running_var, bn.weight, float(bn.eps))
+        ctx.save_for_backward(mask)
+        ctx.fmt = torch.channels_last if _is_channels_last(y) and not y.is_contiguous() \
+            else torch.contiguous_format
+        return y.view_as(y)
+
+    @staticmethod
+    def backward(ctx, gy):
+        (mask,) = ctx.saved_tensors
+        mask = _need(mask, "mask", "conv_bn_relu dX")
+        g = gy.contiguous(memory_format=ctx.fmt)
+        gc = torch.empty_like(g, memory_format=ctx.fmt)
+        if _is_meta(g):
+            return gc, None, None
+        mean, var, bw, eps = ctx.bn
+        L = _lib.lib()
+        _lib.check(L.ms_bn_relu_bwd(g.numel(), g.shape[1], _dtype_code(g), _dtype_code(mean),
+                                    _ptr(g), _ptr(mask), _ptr(mean), _ptr(var), _ptr(bw), eps,
+                                    _ptr(gc), _stream(g.device)), "ms_bn_relu_bwd")
+        return gc, None, None
 
 
 def conv_bn_fusable(x: torch.Tensor, conv, bn) -> bool:
@@ -925,8 +959,11 @@ def conv_bn_relu(x: torch.Tensor, conv, bn, with_relu: bool) -> torch.Tensor:
     ``conv_bn_fusable`` holds, else the layers in sequence (BN in training mode
     or with trainable parameters, float32, ...)."""
     if conv_bn_fusable(x, conv, bn):
-        return _ConvBNFn.apply(x, conv.weight, conv.bias, conv.stride, conv.padding, bn,
-                               with_relu)
+        y, mask = _ConvBNFn.apply(x, conv.weight, conv.bias, conv.stride, conv.padding, bn,
+                                  with_relu)
+        if with_relu and mask is not None:
+            return _MaskScaleFn.apply(y, mask, bn)
+        return y
     y = bn(conv(x))
     if not with_relu:
         return y

@@ -564,11 +564,18 @@ def test_conv_bn_relu_fused(case):
     _close(y, zr, "bf16", "conv_bn_relu y", ulps=2.01)
     g, gq = _q(rng.standard_normal(zr.shape), "bf16")
     y.backward(g)
-    # dX = conv_dx(g * keep * s); the kernel rounds g*keep*s to bf16 before the dgrad
     ym = y.detach().float().cpu().double().numpy()
-    keep_gpu = ym > 0 if with_relu else np.ones_like(ym, dtype=bool)
-    gc = oracle.round_to(np.where(keep_gpu, gq, 0.0) * oracle.round_to(sc, "f32").reshape(1, -1, 1, 1), "bf16")
-    _close(x.grad, oracle.conv2d_dx(gc, wq, s, p, h, w), "bf16", "conv_bn_relu dx", ulps=2.01)
+    if with_relu:
+        # dX = conv_dx(g * keep * s): the kernel rounds g*keep*s to bf16 before the dgrad
+        keep_gpu = ym > 0
+        gc = oracle.round_to(np.where(keep_gpu, gq, 0.0) *
+                             oracle.round_to(sc, "f32").reshape(1, -1, 1, 1), "bf16")
+        ref = oracle.conv2d_dx(gc, wq, s, p, h, w)
+    else:
+        # no mask: the BN scale is folded into the weight, dX = conv_dx(g, bf16(W * s))
+        wsq = oracle.round_to(wq * oracle.round_to(sc, "f32").reshape(-1, 1, 1, 1), "bf16")
+        ref = oracle.conv2d_dx(gq, wsq, s, p, h, w)
+    _close(x.grad, ref, "bf16", "conv_bn_relu dx", ulps=2.01)
 
 
 def test_add_relu():
