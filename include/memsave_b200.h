@@ -158,6 +158,14 @@ MS_API ms_status ms_conv2d_bn_fwd(const ms_conv_desc* d, const void* x, const vo
                                   const void* bn_bias_or_null, int32_t bn_pdtype, double eps,
                                   int32_t relu, void* y, void* mask_or_null, void* ws,
                                   size_t ws_bytes, void* stream);
+/* dX of the conv when a following eval-BN (no ReLU) scales its output: the scale
+ * w/sqrt(var+eps) is folded into the repacked dgrad weight, so dY is used as
+ * is (no pass over the gradient).  Workspace: ms_conv2d_workspace(d, MS_CONV_DX).
+ * MS_ERR_UNSUPPORTED outside the tcgen05 phase-GEMM dgrad.                  */
+MS_API ms_status ms_conv2d_bn_dx(const ms_conv_desc* d, const void* dy, const void* w,
+                                 const void* bn_var, const void* bn_weight_or_null,
+                                 int32_t bn_pdtype, double eps, void* dx, void* ws,
+                                 size_t ws_bytes, void* stream);
 /* dx = g * keep * w/sqrt(var+eps) per channel (NHWC, C % 8 == 0, 16-bit);
  * mask_or_null = NULL for a conv -> BN chain without ReLU.                  */
 MS_API ms_status ms_bn_relu_bwd(int64_t numel, int64_t c, int32_t dtype, int32_t pdtype,

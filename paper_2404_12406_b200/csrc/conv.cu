@@ -311,8 +311,16 @@ ms_status dx_band(const ms_conv_desc* d, const ConvPlan& p, const void* dy, cons
   return launch_umma(bn, 0, 0, LOAD_CONV_DGRAD_BAND, tm, g, st);
 }
 
+struct KScale {  // an eval-BN scale w/sqrt(var+eps) folded into the dgrad weight
+  const void* var = nullptr;
+  const void* weight = nullptr;
+  int pdt = 0;
+  float eps = 0.f;
+};
+
 ms_status dx_tc(const ms_conv_desc* d, const ConvPlan& p, const void* dy, const void* w, void* dx,
-                void* ws, cudaStream_t st, const void* bias = nullptr) {
+                void* ws, cudaStream_t st, const void* bias = nullptr,
+                const KScale* ks = nullptr) {
   const ConvDims c = dims_of(d);
   const int dt = d->dtype;
   if (p.band) return dx_band(d, p, dy, w, dx, ws, st);
@@ -321,7 +329,9 @@ ms_status dx_tc(const ms_conv_desc* d, const ConvPlan& p, const void* dy, const 
     return stem_dgrad(dt, c.n, c.h, c.w, c.oh, c.ow, c.k, dy, ws, dx, st);
   }
   void* wd = ws;
-  MS_TRY(repack_dgrad(dt, c.k, c.c, c.r, c.s, p.kpad, d->wlayout, w, wd, st));
+  MS_TRY(repack_dgrad(dt, c.k, c.c, c.r, c.s, p.kpad, d->wlayout, w, wd, st,
+                      ks ? ks->var : nullptr, ks ? ks->weight : nullptr, ks ? ks->pdt : 0,
+                      ks ? ks->eps : 0.f));
   GemmArgs g = base_args(dt);
   g.N = c.c;
   const TilePick tp = pick_tiles((int64_t)c.n * c.h * c.w / BM + 1, c.c, true, false);
@@ -607,4 +617,24 @@ extern "C" ms_status ms_conv2d_bn_fwd(const ms_conv_desc* d, const void* x, cons
   f.relu = relu;
   f.mask = static_cast<uint8_t*>(mask_or_null);
   return fwd_tc(d, p, x, w, bias, y, ws, st, &f);
+}
+
+extern "C" ms_status ms_conv2d_bn_dx(const ms_conv_desc* d, const void* dy, const void* w,
+                                     const void* bn_var, const void* bn_weight, int32_t bn_pdtype,
+                                     double eps, void* dx, void* ws, size_t ws_bytes,
+                                     void* stream) {
+  MS_TRY(validate(d));
+  MS_TRY(bind_device(dx));
+  if (d->n == 0) return MS_OK;
+  ConvPlan p = plan(d, MS_CONV_DX, /*dx_bias=*/true);  // the generic phase GEMM, no band kernel
+  MS_CHECK_ARG(p.tc && !p.stem && !p.band && bn_var, MS_ERR_UNSUPPORTED,
+               "conv+bn dx: the folded-scale path needs the tcgen05 phase GEMM");
+  MS_CHECK_ARG(ws_bytes >= p.ws && (p.ws == 0 || ws), MS_ERR_WORKSPACE,
+               "conv+bn dx: workspace %zu < %zu", ws_bytes, p.ws);
+  KScale ks;
+  ks.var = bn_var;
+  ks.weight = bn_weight;
+  ks.pdt = bn_pdtype;
+  ks.eps = (float)eps;
+  return dx_tc(d, p, dy, w, dx, ws, (cudaStream_t)stream, nullptr, &ks);
 }

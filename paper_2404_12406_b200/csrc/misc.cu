@@ -152,9 +152,12 @@ __global__ void repack_fprop_kernel(int K, int C, int R, int S, int cpad, int wl
 }
 
 // Input-VJP weight [c][tap][kpad] from OIHW/OHWI (B operand of the dgrad GEMM).
+// kvar (nullable): multiply output-channel k by kw[k] / sqrt(kvar[k] + eps) -- a
+// following eval-BatchNorm's scale folded into the input-VJP weight
 template <typename T>
 __global__ void repack_dgrad_kernel(int K, int C, int R, int S, int kpad, int wlayout,
-                                    const T* __restrict__ w, T* __restrict__ out) {
+                                    const T* __restrict__ w, T* __restrict__ out,
+                                    const void* kvar, const void* kw, int pdt, float eps) {
   const int64_t total = (int64_t)C * R * S * kpad;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -164,9 +167,15 @@ __global__ void repack_dgrad_kernel(int K, int C, int R, int S, int kpad, int wl
     const int c = (int)t;
     const int r = tap / S, s = tap % S;
     T v = IO<T>::cvt(0.f);
-    if (k < K)
+    if (k < K) {
       v = wlayout == MS_NHWC ? w[(((int64_t)k * R + r) * S + s) * C + c]
                              : w[(((int64_t)k * C + c) * R + r) * S + s];
+      if (kvar) {
+        const float sc = (kw ? load_as_float(kw, pdt, k) : 1.f) /
+                         sqrtf(load_as_float(kvar, pdt, k) + eps);
+        v = IO<T>::cvt(IO<T>::ld(&v) * sc);
+      }
+    }
     out[i] = v;
   }
 }
@@ -280,10 +289,11 @@ ms_status repack_fprop(int dt, int K, int C, int R, int S, int cpad, int wlayout
 }
 
 ms_status repack_dgrad(int dt, int K, int C, int R, int S, int kpad, int wlayout, const void* w,
-                       void* out, cudaStream_t st) {
+                       void* out, cudaStream_t st, const void* kvar, const void* kw, int pdt,
+                       float eps) {
   const int64_t total = (int64_t)C * R * S * kpad;
   MS_DT_DISPATCH(dt, repack_dgrad_kernel<T><<<grid_1d(total), 256, 0, st>>>(
-                         K, C, R, S, kpad, wlayout, (const T*)w, (T*)out));
+                         K, C, R, S, kpad, wlayout, (const T*)w, (T*)out, kvar, kw, pdt, eps));
   count_launch();
   return launch_status("repack_dgrad_kernel");
 }

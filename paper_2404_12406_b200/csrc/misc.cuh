@@ -7,7 +7,8 @@ namespace ms {
 ms_status repack_fprop(int dt, int K, int C, int R, int S, int cpad, int wlayout, const void* w,
                        void* out, cudaStream_t st);
 ms_status repack_dgrad(int dt, int K, int C, int R, int S, int kpad, int wlayout, const void* w,
-                       void* out, cudaStream_t st);
+                       void* out, cudaStream_t st, const void* kvar = nullptr,
+                       const void* kw = nullptr, int pdt = 0, float eps = 0.f);
 ms_status repack_scatter(int dt, int K, int C, int R, int S, int kpad, int wlayout, const void* w,
                          void* out, cudaStream_t st);
 ms_status repack_rowseg(int dt, int K, int C, int R, int S, int wlayout, const void* w, void* out,

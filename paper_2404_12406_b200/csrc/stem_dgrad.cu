@@ -327,6 +327,7 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 }
 
 constexpr int SF_STG = SF_EPI * 2 * 4096;  // per epilogue warp: 2 x (32 px x 128 B), SW128
+constexpr int SF_AFF = 2 * 128 * 4;         // fused eval-BN scale / shift (K <= 128)
 
 template <typename T>
 __global__ void __launch_bounds__(SF_THREADS, 1)
@@ -340,7 +341,8 @@ __global__ void __launch_bounds__(SF_THREADS, 1)
   uint8_t* sB = smem + SF_STG;
   uint8_t* zero_row = sB + b_bytes;            // out-of-range input rows read zeros
   uint8_t* ring = zero_row + SF_SLOT;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + SF_STAGES * SF_STAGE);
+  float* s_aff = reinterpret_cast<float*>(ring + SF_STAGES * SF_STAGE);  // [scale K][shift K]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + SF_STAGES * SF_STAGE + SF_AFF);
   uint64_t* full_bar = bars;
   uint64_t* empty_bar = bars + SF_STAGES;
   uint64_t* tfull_bar = bars + 2 * SF_STAGES;
@@ -352,6 +354,11 @@ __global__ void __launch_bounds__(SF_THREADS, 1)
   const uint32_t lane = lane_id();
   for (int i = threadIdx.x; i < SF_SLOT / 4; i += blockDim.x)
     reinterpret_cast<uint32_t*>(zero_row)[i] = 0u;
+  if (a.scale)
+    for (int i = threadIdx.x; i < a.K; i += blockDim.x) {
+      s_aff[i] = a.scale[i];
+      s_aff[a.K + i] = a.shift[i];
+    }
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < SF_STAGES; ++i) {
       mbar_init(smem_u32(&full_bar[i]), 1);
@@ -484,7 +491,7 @@ __global__ void __launch_bounds__(SF_THREADS, 1)
             const int ch = q * 8 + j;
             f[j] = __uint_as_float(ch < 32 ? v0[ch] : v1[ch - 32]);
             if (a.bias) f[j] += IO<T>::ld(static_cast<const T*>(a.bias) + c0 + ch);
-            if (a.scale) f[j] = f[j] * __ldg(a.scale + c0 + ch) + __ldg(a.shift + c0 + ch);
+            if (a.scale) f[j] = f[j] * s_aff[c0 + ch] + s_aff[a.K + c0 + ch];
             if (a.relu) {
               const bool pos = !(f[j] <= 0.f);
               keep |= (pos ? 1ull : 0ull) << ch;
@@ -566,7 +573,8 @@ ms_status stem_fprop(int dt, int n, int h, int wp, int p, int q, int k, int c, i
   a.y = y; a.bias = bias; a.dt = dt; a.xp = xp; a.wb = wb;
   a.scale = scale; a.shift = shift; a.relu = relu; a.mask = mask;
   const int smem =
-      SF_STG + (int)stem_fprop_weight_bytes(k) + SF_SLOT + SF_STAGES * SF_STAGE + 1024 + 256;
+      SF_STG + (int)stem_fprop_weight_bytes(k) + SF_SLOT + SF_STAGES * SF_STAGE + SF_AFF + 1024 +
+      256;
   const int grid = a.units < num_sms() ? a.units : num_sms();
   CUtensorMap ty;
   const size_t es = dtype_size(dt);

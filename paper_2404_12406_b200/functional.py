@@ -877,13 +877,21 @@ class _ConvBNFn(torch.autograd.Function):
         d = _conv_desc(x_shape, w_shape, stride, padding, layout, wlayout, dt)
         if need_x:
             w = _need(w, "w", "conv_bn dX")
-            if sc_w:
-                sc = (bw.float() if bw is not None else 1.0) * torch.rsqrt(var.float() + eps)
-                w = _as_layout((w.float() * sc.view(-1, 1, 1, 1)).to(w.dtype), wlayout)
             dx = _empty4(x_shape, g, layout)
             wsp, nb = _workspace(L.ms_conv2d_workspace(ctypes.byref(d), _lib.MS_CONV_DX), g.device)
-            _lib.check(L.ms_conv2d_dx(ctypes.byref(d), _ptr(g), _ptr(w), _ptr(dx), _ptr(wsp), nb,
-                                      st), "ms_conv2d_dx")
+            folded = False
+            if sc_w:  # BN scale folded into the repacked dgrad weight (no pass over g)
+                st_ = L.ms_conv2d_bn_dx(ctypes.byref(d), _ptr(g), _ptr(w), _ptr(var), _ptr(bw),
+                                        _dtype_code(var), eps, _ptr(dx), _ptr(wsp), nb, st)
+                folded = st_ == 0
+                if st_ not in (0, 4):  # 4 = MS_ERR_UNSUPPORTED: scale the weight here
+                    _lib.check(st_, "ms_conv2d_bn_dx")
+                if not folded:
+                    sc = (bw.float() if bw is not None else 1.0) * torch.rsqrt(var.float() + eps)
+                    w = _as_layout((w.float() * sc.view(-1, 1, 1, 1)).to(w.dtype), wlayout)
+            if not folded:
+                _lib.check(L.ms_conv2d_dx(ctypes.byref(d), _ptr(g), _ptr(w), _ptr(dx), _ptr(wsp),
+                                          nb, st), "ms_conv2d_dx")
         if need_w or need_b:
             gc = g
             if need_scaled_g:

@@ -21,13 +21,14 @@ ap.add_argument("--batch", type=int, default=0)
 ap.add_argument("--steps", type=int, default=4)
 ap.add_argument("--warmup", type=int, default=3)
 ap.add_argument("--stock", action="store_true")
+ap.add_argument("--no-fuse", action="store_true")
 a = ap.parse_args()
 
 dev = torch.device("cuda", 0)
 builder = BM.WORKLOADS[a.config]
 wl = builder(batch=a.batch) if a.batch else builder()
 if not a.stock:
-    convert_to_memory_saving(wl.model)
+    wl.model = convert_to_memory_saving(wl.model, fuse=not a.no_fuse)
 inputs = list(wl.make_batch(wl.batch, dev))
 if wl.input_requires_grad:
     inputs[0].requires_grad_(True)
