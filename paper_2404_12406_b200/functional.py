@@ -802,6 +802,7 @@ class _ConvBNFn(torch.autograd.Function):
     def forward(ctx, x, weight, bias, stride, padding, bn, relu: bool):
         x_rg, w_rg, b_rg = ctx.needs_input_grad[0], ctx.needs_input_grad[1], ctx.needs_input_grad[2]
         out_rg = x_rg or w_rg or b_rg
+        ctx.set_materialize_grads(False)  # the mask output never gets a gradient: no zero fill
         roles = saved_roles(x_rg, w_rg)
         stride, padding = _pair(stride), _pair(padding)
         oh, ow = _conv_out_hw(x.shape, weight.shape, stride, padding)
@@ -846,6 +847,8 @@ class _ConvBNFn(torch.autograd.Function):
     @staticmethod
     def backward(ctx, gy, _gmask=None):
         x, w = ctx.saved_tensors
+        if gy is None:  # grads are not materialised (set_materialize_grads(False))
+            return None, None, None, None, None, None, None
         need_x, need_w, need_b = ctx.needs_input_grad[:3]
         x_shape, w_shape, stride, padding = ctx.geom
         dx = dw = db = None
