@@ -156,8 +156,10 @@ MS_API ms_status ms_conv2d_bn_fwd(const ms_conv_desc* d, const void* x, const vo
                                   const void* bias_or_null, const void* bn_mean,
                                   const void* bn_var, const void* bn_weight_or_null,
                                   const void* bn_bias_or_null, int32_t bn_pdtype, double eps,
-                                  int32_t relu, void* y, void* mask_or_null, void* ws,
-                                  size_t ws_bytes, void* stream);
+                                  const void* residual_or_null, int32_t relu, void* y,
+                                  void* mask_or_null, void* ws, size_t ws_bytes, void* stream);
+/* residual_or_null: a tensor shaped like y added after the BN affine and before
+ * the ReLU (the conv -> BN -> add -> ReLU join of a ResNet block).          */
 /* dX of the conv when a following eval-BN (no ReLU) scales its output: the scale
  * w/sqrt(var+eps) is folded into the repacked dgrad weight, so dY is used as
  * is (no pass over the gradient).  Workspace: ms_conv2d_workspace(d, MS_CONV_DX).

@@ -68,7 +68,8 @@ SIGNATURES = {
     "ms_add_relu_fwd": (_c_i32, [_c_i64, _c_i32, _vp, _vp, _vp, _vp, _vp]),
     "ms_conv2d_bn_workspace": (_c_sz, [ctypes.POINTER(ConvDesc)]),
     "ms_conv2d_bn_fwd": (_c_i32, [ctypes.POINTER(ConvDesc), _vp, _vp, _vp, _vp, _vp, _vp, _vp,
-                                  _c_i32, ctypes.c_double, _c_i32, _vp, _vp, _vp, _c_sz, _vp]),
+                                  _c_i32, ctypes.c_double, _vp, _c_i32, _vp, _vp, _vp, _c_sz,
+                                  _vp]),
     "ms_conv2d_bn_dx": (_c_i32, [ctypes.POINTER(ConvDesc), _vp, _vp, _vp, _vp, _c_i32,
                                  ctypes.c_double, _vp, _vp, _c_sz, _vp]),
     "ms_bn_relu_bwd": (_c_i32, [_c_i64, _c_i64, _c_i32, _c_i32, _vp, _vp, _vp, _vp, _vp,

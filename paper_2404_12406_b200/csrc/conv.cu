@@ -185,6 +185,7 @@ struct Fuse {
   const float* shift = nullptr;
   int relu = 0;
   uint8_t* mask = nullptr;
+  const void* resid = nullptr;
 };
 
 void apply_fuse(EpiParams& e, const Fuse* f) {
@@ -193,6 +194,7 @@ void apply_fuse(EpiParams& e, const Fuse* f) {
   e.shift = f->shift;
   e.relu = f->relu;
   e.mask = f->mask;
+  e.resid = f->resid;
 }
 
 ms_status fwd_rowseg(const ms_conv_desc* d, const ConvPlan& p, const void* x, const void* w,
@@ -205,8 +207,8 @@ ms_status fwd_rowseg(const ms_conv_desc* d, const ConvPlan& p, const void* x, co
   void* wr = wsb + p.ws_pad;
   MS_TRY(pad_rowseg(dt, c.n, c.h, c.w, c.c, c.pw, p.xw_pad, x, x4, st));
   static const bool env_im2col = getenv("MS_STEM_IM2COL") != nullptr;  // A/B switch
-  if (!env_im2col && stem_fprop_ok(dt, d->layout, c.c, c.r, c.s, c.sh, c.sw, c.ph, c.pw, c.ow,
-                                   c.k) &&
+  if (!env_im2col && (!f || !f->resid) &&
+      stem_fprop_ok(dt, d->layout, c.c, c.r, c.s, c.sh, c.sw, c.ph, c.pw, c.ow, c.k) &&
       stem_fprop_weight_bytes(c.k) <= p.ws_w)
     return stem_fprop(dt, c.n, c.h, p.xw_pad, c.oh, c.ow, c.k, c.c, d->wlayout, x4, w, wr, bias, y,
                       st, f ? f->scale : nullptr, f ? f->shift : nullptr, f ? f->relu : 0,
@@ -592,9 +594,9 @@ extern "C" size_t ms_conv2d_bn_workspace(const ms_conv_desc* d) {
 extern "C" ms_status ms_conv2d_bn_fwd(const ms_conv_desc* d, const void* x, const void* w,
                                       const void* bias, const void* bn_mean, const void* bn_var,
                                       const void* bn_weight, const void* bn_bias,
-                                      int32_t bn_pdtype, double eps, int32_t relu, void* y,
-                                      void* mask_or_null, void* ws, size_t ws_bytes,
-                                      void* stream) {
+                                      int32_t bn_pdtype, double eps, const void* residual,
+                                      int32_t relu, void* y, void* mask_or_null, void* ws,
+                                      size_t ws_bytes, void* stream) {
   MS_TRY(validate(d));
   MS_TRY(bind_device(y));
   MS_CHECK_ARG(bn_mean && bn_var, MS_ERR_SHAPE, "conv+bn: running statistics required");
@@ -616,6 +618,9 @@ extern "C" ms_status ms_conv2d_bn_fwd(const ms_conv_desc* d, const void* x, cons
   f.shift = shift;
   f.relu = relu;
   f.mask = static_cast<uint8_t*>(mask_or_null);
+  f.resid = residual;
+  MS_CHECK_ARG(!residual || (reinterpret_cast<uintptr_t>(residual) & 15) == 0, MS_ERR_ALIGN,
+               "conv+bn: residual must be 16-byte aligned");
   return fwd_tc(d, p, x, w, bias, y, ws, st, &f);
 }
 

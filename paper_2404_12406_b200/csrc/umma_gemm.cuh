@@ -90,6 +90,8 @@ struct EpiParams {
   const float* shift;
   int relu;
   uint8_t* mask;       // nullable
+  const void* resid;   // nullable: residual added after the affine, before the ReLU
+                       // (same dtype / pitch as out)
 };
 
 struct GemmArgs {
@@ -707,6 +709,33 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
                   if (nc + 4 * q + h < ncols)
                     v[4 * q + h] = v[4 * q + h] * e.scale[nc + 4 * q + h] + e.shift[nc + 4 * q + h];
               }
+            }
+          }
+          if (e.resid != nullptr && valid) {  // fused residual join of a ResNet block
+            const int64_t el = orow * e.ldc + col_base + c;
+            const uint16_t* r16 = static_cast<const uint16_t*>(e.resid) + el;
+            if (full && (reinterpret_cast<uintptr_t>(r16) & 15) == 0) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const uint4 u = __ldg(reinterpret_cast<const uint4*>(r16) + q);
+                const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                  float lo, hi;
+                  if (e.out_dtype == MS_BF16) {
+                    lo = __uint_as_float(w4[h] << 16);
+                    hi = __uint_as_float(w4[h] & 0xFFFF0000u);
+                  } else {
+                    lo = __half2float(__ushort_as_half((unsigned short)(w4[h] & 0xFFFF)));
+                    hi = __half2float(__ushort_as_half((unsigned short)(w4[h] >> 16)));
+                  }
+                  v[q * 8 + 2 * h] += lo;
+                  v[q * 8 + 2 * h + 1] += hi;
+                }
+              }
+            } else {
+              for (int j = 0; j < 32; ++j)
+                if (nc + j < ncols) v[j] += load_as_float(e.resid, e.out_dtype, el + j);
             }
           }
           if (e.relu) {

@@ -799,10 +799,13 @@ class _ConvBNFn(torch.autograd.Function):
     gradient is never rescaled."""
 
     @staticmethod
-    def forward(ctx, x, weight, bias, stride, padding, bn, relu: bool):
+    def forward(ctx, x, weight, bias, residual, stride, padding, bn, relu: bool):
         x_rg, w_rg, b_rg = ctx.needs_input_grad[0], ctx.needs_input_grad[1], ctx.needs_input_grad[2]
-        out_rg = x_rg or w_rg or b_rg
+        out_rg = x_rg or w_rg or b_rg or ctx.needs_input_grad[3]
         ctx.set_materialize_grads(False)  # the mask output never gets a gradient: no zero fill
+        # the incoming gradient is already masked and scaled (_MaskScaleFn) only for
+        # conv -> BN -> ReLU without a residual; otherwise the BN scale is folded here
+        ctx.prescaled = bool(relu) and residual is None
         roles = saved_roles(x_rg, w_rg)
         stride, padding = _pair(stride), _pair(padding)
         oh, ow = _conv_out_hw(x.shape, weight.shape, stride, padding)
@@ -831,13 +834,14 @@ class _ConvBNFn(torch.autograd.Function):
         mask = torch.empty((n_el + 7) // 8, dtype=torch.uint8, device=x.device) \
             if relu and out_rg else None
         b = None if bias is None else bias.to(x.dtype).contiguous()
+        res = None if residual is None else _as_layout(residual, layout)
         mean, var, bw, eps = ctx.bn
         bb = bn.bias
         L = _lib.lib()
         ws, nb = _workspace(L.ms_conv2d_bn_workspace(ctypes.byref(d)), x.device)
         _lib.check(L.ms_conv2d_bn_fwd(ctypes.byref(d), _ptr(xl), _ptr(wl), _ptr(b), _ptr(mean),
                                       _ptr(var), _ptr(bw), _ptr(bb), _dtype_code(mean), eps,
-                                      int(relu), _ptr(y), _ptr(mask), _ptr(ws), nb,
+                                      _ptr(res), int(relu), _ptr(y), _ptr(mask), _ptr(ws), nb,
                                       _stream(x.device)), "ms_conv2d_bn_fwd")
         ctx.save_for_backward(xl if "x" in roles else None, wl if "w" in roles else None)
         if mask is not None:
@@ -848,7 +852,7 @@ class _ConvBNFn(torch.autograd.Function):
     def backward(ctx, gy, _gmask=None):
         x, w = ctx.saved_tensors
         if gy is None:  # grads are not materialised (set_materialize_grads(False))
-            return None, None, None, None, None, None, None
+            return None, None, None, None, None, None, None, None
         need_x, need_w, need_b = ctx.needs_input_grad[:3]
         x_shape, w_shape, stride, padding = ctx.geom
         dx = dw = db = None
@@ -856,7 +860,9 @@ class _ConvBNFn(torch.autograd.Function):
         mean, var, bw, eps = ctx.bn
         g = _as_layout(gy, layout)
         del gy
-        if not ctx.relu:
+        need_r = ctx.needs_input_grad[3]
+        d_res = g if need_r else None  # the residual's gradient is the (masked) gradient
+        if not ctx.prescaled:
             # dL/dconv = g * s: fold s into W for dX; scale g only for dW / db
             sc_w = need_x
             need_scaled_g = need_w or need_b
@@ -873,7 +879,7 @@ class _ConvBNFn(torch.autograd.Function):
                 dw = gc.new_empty(w_shape)
             if need_b:
                 db = gc.new_empty((w_shape[0],))
-            return dx, dw, db, None, None, None, None
+            return dx, dw, db, d_res, None, None, None, None
         L = _lib.lib()
         st = _stream(g.device)
         dt = _dtype_code(g)
@@ -917,7 +923,7 @@ class _ConvBNFn(torch.autograd.Function):
                 wsp, nb = _workspace(4 * w_shape[0], gc.device)
                 _lib.check(L.ms_conv2d_db(ctypes.byref(d), _ptr(gc), _ptr(db), _ptr(wsp), nb, st),
                            "ms_conv2d_db")
-        return dx, dw, db, None, None, None, None
+        return dx, dw, db, d_res, None, None, None, None
 
 
 class _MaskScaleFn(torch.autograd.Function):
@@ -928,7 +934,9 @@ class _MaskScaleFn(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, y, mask, bn):
-        ctx.bn = (bn.running_mean, bn.running_var, bn.weight, float(bn.eps))
+        # bn is None for the residual join: then only the ReLU mask is applied
+        ctx.bn = None if bn is None else (bn.running_mean, bn.running_var, bn.weight,
+                                          float(bn.eps))
         ctx.save_for_backward(mask)
         ctx.fmt = torch.channels_last if _is_channels_last(y) and not y.is_contiguous() \
             else torch.contiguous_format
@@ -942,8 +950,12 @@ class _MaskScaleFn(torch.autograd.Function):
         gc = torch.empty_like(g, memory_format=ctx.fmt)
         if _is_meta(g):
             return gc, None, None
-        mean, var, bw, eps = ctx.bn
         L = _lib.lib()
+        if ctx.bn is None:
+            _lib.check(L.ms_relu_bwd(g.numel(), _dtype_code(g), _ptr(g), _ptr(mask), _ptr(gc),
+                                     _stream(g.device)), "ms_relu_bwd")
+            return gc, None, None
+        mean, var, bw, eps = ctx.bn
         _lib.check(L.ms_bn_relu_bwd(g.numel(), g.shape[1], _dtype_code(g), _dtype_code(mean),
                                     _ptr(g), _ptr(mask), _ptr(mean), _ptr(var), _ptr(bw), eps,
                                     _ptr(gc), _stream(g.device)), "ms_bn_relu_bwd")
@@ -970,7 +982,7 @@ def conv_bn_relu(x: torch.Tensor, conv, bn, with_relu: bool) -> torch.Tensor:
     ``conv_bn_fusable`` holds, else the layers in sequence (BN in training mode
     or with trainable parameters, float32, ...)."""
     if conv_bn_fusable(x, conv, bn):
-        y, mask = _ConvBNFn.apply(x, conv.weight, conv.bias, conv.stride, conv.padding, bn,
+        y, mask = _ConvBNFn.apply(x, conv.weight, conv.bias, None, conv.stride, conv.padding, bn,
                                   with_relu)
         if with_relu and mask is not None:
             return _MaskScaleFn.apply(y, mask, bn)
@@ -980,6 +992,20 @@ def conv_bn_relu(x: torch.Tensor, conv, bn, with_relu: bool) -> torch.Tensor:
         return y
     # the ReLU module was folded into this call: keep its MemSave storage (bit mask)
     return relu(y) if y.device.type in ("cuda", "meta") else torch.relu(y)
+
+
+def conv_bn_add_relu(x: torch.Tensor, conv, bn, residual: torch.Tensor) -> torch.Tensor:
+    """relu(bn(conv(x)) + residual): the main branch and the join of a ResNet
+    block in one launch (residual added in the conv epilogue) when
+    ``conv_bn_fusable`` holds and the residual matches the output."""
+    if (conv_bn_fusable(x, conv, bn) and residual.dtype == x.dtype
+            and residual.device == x.device and residual.dim() == 4):
+        y, mask = _ConvBNFn.apply(x, conv.weight, conv.bias, residual, conv.stride, conv.padding,
+                                  bn, True)
+        if mask is not None:
+            return _MaskScaleFn.apply(y, mask, None)
+        return y
+    return add_relu(bn(conv(x)), residual)
 
 
 # =============================================================== fused residual add + ReLU

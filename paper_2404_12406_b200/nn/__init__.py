@@ -337,10 +337,31 @@ def fuse_conv_bn_relu(model: nn.Module, verbose: bool = False) -> nn.Module:
         g.erase_node(r)
         g.erase_node(node)
         nadd += 1
+    # conv -> bn (no relu) whose only consumer is an add -> relu join: one launch
+    # with the residual added in the conv epilogue
+    nres = 0
+    for node in list(g.nodes):
+        if node.op != "call_function" or node.target is not MF.add_relu:
+            continue
+        a, b = node.args
+        for main, other in ((a, b), (b, a)):
+            if (isinstance(main, fx.Node) and main.op == "call_function"
+                    and main.target is MF.conv_bn_relu and main.args[3] is False
+                    and len(main.users) == 1):
+                with g.inserting_before(node):
+                    fused = g.call_function(MF.conv_bn_add_relu,
+                                            (main.args[0], main.args[1], main.args[2], other))
+                node.replace_all_uses_with(fused)
+                g.erase_node(node)
+                g.erase_node(main)
+                nres += 1
+                break
+    g.eliminate_dead_code()
     g.lint()
     gm.recompile()
     if verbose:
-        print(f"memsave: fused {nfused} conv->bn[->relu] and {nadd} add->relu chains")
+        print(f"memsave: fused {nfused} conv->bn[->relu], {nadd} add->relu and {nres} "
+              f"conv->bn->add->relu chains")
     return gm
 
 

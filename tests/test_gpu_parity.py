@@ -630,3 +630,42 @@ def test_fused_resnet18_matches_unfused():
            for k, (y, g) in out.items() if k != "fp32"}
     assert err["fused"][0] <= 1.2 * err["stock"][0] + 1e-3, err
     assert err["fused"][1] <= 1.2 * err["stock"][1] + 1e-2, err
+
+
+@pytest.mark.parametrize("x_rg,r_rg", [(True, True), (True, False), (False, True)])
+def test_conv_bn_add_relu_fused(x_rg, r_rg):
+    n, c, h, w, k = 2, 64, 10, 10, 64
+    rng = np.random.default_rng(17)
+    x, xq = _q(rng.standard_normal((n, c, h, w)), "bf16")
+    wt, wq = _q(rng.standard_normal((k, c, 3, 3)) / np.sqrt(c * 9), "bf16")
+    res, rq = _q(rng.standard_normal((n, k, h, w)), "bf16")
+    conv = torch.nn.Conv2d(c, k, 3, 1, 1, bias=False).to(DEV, torch.bfloat16)
+    conv.weight.data.copy_(wt)
+    conv.weight.requires_grad_(False)
+    bn = torch.nn.BatchNorm2d(k).to(DEV, torch.bfloat16).eval()
+    bn.running_mean.copy_(torch.linspace(-0.2, 0.2, k))
+    bn.running_var.copy_(torch.linspace(0.5, 2.0, k))
+    bn.weight.data.copy_(torch.linspace(0.5, 1.5, k))
+    bn.bias.data.copy_(torch.linspace(-0.3, 0.3, k))
+    for prm in bn.parameters():
+        prm.requires_grad_(False)
+    x = x.contiguous(memory_format=torch.channels_last).requires_grad_(x_rg)
+    res = res.contiguous(memory_format=torch.channels_last).requires_grad_(r_rg)
+    u0 = launch_stats()["umma"]
+    y = MF.conv_bn_add_relu(x, conv, bn, res)
+    assert launch_stats()["umma"] - u0 == 1
+    mq = bn.running_mean.double().cpu().numpy()
+    vq = bn.running_var.double().cpu().numpy()
+    sc = bn.weight.double().cpu().numpy() / np.sqrt(vq + 1e-5)
+    sh = bn.bias.double().cpu().numpy() - mq * sc
+    z = oracle.conv2d_fwd(xq, wq, 1, 1) * sc.reshape(1, -1, 1, 1) + sh.reshape(1, -1, 1, 1) + rq
+    _close(y, np.maximum(z, 0), "bf16", "conv_bn_add_relu y", ulps=2.01)
+    g, gq = _q(rng.standard_normal(z.shape), "bf16")
+    y.backward(g)
+    keep = y.detach().float().cpu().double().numpy() > 0
+    gm = np.where(keep, gq, 0.0)
+    if r_rg:
+        _close(res.grad, gm, "bf16", "residual grad")
+    if x_rg:
+        wsq = oracle.round_to(wq * oracle.round_to(sc, "f32").reshape(-1, 1, 1, 1), "bf16")
+        _close(x.grad, oracle.conv2d_dx(gm, wsq, 1, 1, h, w), "bf16", "x grad", ulps=2.01)
