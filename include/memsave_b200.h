@@ -159,7 +159,8 @@ MS_API ms_status ms_conv2d_bn_fwd(const ms_conv_desc* d, const void* x, const vo
                                   const void* residual_or_null, int32_t relu, void* y,
                                   void* mask_or_null, void* ws, size_t ws_bytes, void* stream);
 /* residual_or_null: a tensor shaped like y added after the BN affine and before
- * the ReLU (the conv -> BN -> add -> ReLU join of a ResNet block).          */
+ * the ReLU (the conv -> BN -> add -> ReLU join of a ResNet block).  bn_mean =
+ * bn_var = NULL: no BN, i.e. conv [+ bias] -> ReLU (VGG).                   */
 /* dX of the conv when a following eval-BN (no ReLU) scales its output: the scale
  * w/sqrt(var+eps) is folded into the repacked dgrad weight, so dY is used as
  * is (no pass over the gradient).  Workspace: ms_conv2d_workspace(d, MS_CONV_DX).

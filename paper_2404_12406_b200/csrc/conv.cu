@@ -599,7 +599,8 @@ extern "C" ms_status ms_conv2d_bn_fwd(const ms_conv_desc* d, const void* x, cons
                                       size_t ws_bytes, void* stream) {
   MS_TRY(validate(d));
   MS_TRY(bind_device(y));
-  MS_CHECK_ARG(bn_mean && bn_var, MS_ERR_SHAPE, "conv+bn: running statistics required");
+  MS_CHECK_ARG((bn_mean && bn_var) || (!bn_mean && !bn_var), MS_ERR_SHAPE,
+               "conv+bn: give both running statistics (or neither for conv [+ relu] only)");
   if (d->n == 0) return MS_OK;
   cudaStream_t st = (cudaStream_t)stream;
   ConvPlan p = plan(d, MS_CONV_FWD);
@@ -607,15 +608,17 @@ extern "C" ms_status ms_conv2d_bn_fwd(const ms_conv_desc* d, const void* x, cons
                "conv+bn fusion needs the tcgen05 path (16-bit NHWC) and K %% 8 == 0");
   MS_CHECK_ARG(ws && ws_bytes >= ms_conv2d_bn_workspace(d), MS_ERR_WORKSPACE,
                "conv+bn: workspace %zu < %zu", ws_bytes, ms_conv2d_bn_workspace(d));
-  float* scale = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + p.ws);
-  float* shift = scale + d->k;
-  bn_scale_shift_kernel<<<(unsigned)((d->k + 127) / 128), 128, 0, st>>>(
-      (int)d->k, bn_mean, bn_var, bn_weight, bn_bias, bn_pdtype, (float)eps, scale, shift);
-  count_launch(1, KF_BN);
-  MS_TRY(launch_status("bn_scale_shift"));
   Fuse f;
-  f.scale = scale;
-  f.shift = shift;
+  if (bn_mean) {
+    float* scale = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + p.ws);
+    float* shift = scale + d->k;
+    bn_scale_shift_kernel<<<(unsigned)((d->k + 127) / 128), 128, 0, st>>>(
+        (int)d->k, bn_mean, bn_var, bn_weight, bn_bias, bn_pdtype, (float)eps, scale, shift);
+    count_launch(1, KF_BN);
+    MS_TRY(launch_status("bn_scale_shift"));
+    f.scale = scale;
+    f.shift = shift;
+  }
   f.relu = relu;
   f.mask = static_cast<uint8_t*>(mask_or_null);
   f.resid = residual;

@@ -805,13 +805,14 @@ class _ConvBNFn(torch.autograd.Function):
         ctx.set_materialize_grads(False)  # the mask output never gets a gradient: no zero fill
         # the incoming gradient is already masked and scaled (_MaskScaleFn) only for
         # conv -> BN -> ReLU without a residual; otherwise the BN scale is folded here
-        ctx.prescaled = bool(relu) and residual is None
+        ctx.prescaled = bool(relu) and residual is None and bn is not None
         roles = saved_roles(x_rg, w_rg)
         stride, padding = _pair(stride), _pair(padding)
         oh, ow = _conv_out_hw(x.shape, weight.shape, stride, padding)
         ctx.geom = (tuple(x.shape), tuple(weight.shape), stride, padding)
         ctx.w_meta = (weight.dtype, False)
-        ctx.bn = (bn.running_mean, bn.running_var, bn.weight, float(bn.eps))
+        ctx.bn = None if bn is None else (bn.running_mean, bn.running_var, bn.weight,
+                                          float(bn.eps))
         ctx.relu = bool(relu)
         out_shape = (x.shape[0], weight.shape[0], oh, ow)
         n_el = x.shape[0] * weight.shape[0] * oh * ow
@@ -835,12 +836,13 @@ class _ConvBNFn(torch.autograd.Function):
             if relu and out_rg else None
         b = None if bias is None else bias.to(x.dtype).contiguous()
         res = None if residual is None else _as_layout(residual, layout)
-        mean, var, bw, eps = ctx.bn
-        bb = bn.bias
+        mean, var, bw, eps = ctx.bn if bn is not None else (None, None, None, 0.0)
+        bb = None if bn is None else bn.bias
         L = _lib.lib()
         ws, nb = _workspace(L.ms_conv2d_bn_workspace(ctypes.byref(d)), x.device)
         _lib.check(L.ms_conv2d_bn_fwd(ctypes.byref(d), _ptr(xl), _ptr(wl), _ptr(b), _ptr(mean),
-                                      _ptr(var), _ptr(bw), _ptr(bb), _dtype_code(mean), eps,
+                                      _ptr(var), _ptr(bw), _ptr(bb),
+                                      _dtype_code(mean) if mean is not None else dt, eps,
                                       _ptr(res), int(relu), _ptr(y), _ptr(mask), _ptr(ws), nb,
                                       _stream(x.device)), "ms_conv2d_bn_fwd")
         ctx.save_for_backward(xl if "x" in roles else None, wl if "w" in roles else None)
@@ -857,12 +859,15 @@ class _ConvBNFn(torch.autograd.Function):
         x_shape, w_shape, stride, padding = ctx.geom
         dx = dw = db = None
         layout, wlayout = ctx.layouts
-        mean, var, bw, eps = ctx.bn
+        mean, var, bw, eps = ctx.bn if ctx.bn is not None else (None, None, None, 0.0)
         g = _as_layout(gy, layout)
         del gy
         need_r = ctx.needs_input_grad[3]
         d_res = g if need_r else None  # the residual's gradient is the (masked) gradient
-        if not ctx.prescaled:
+        if ctx.bn is None:  # conv [-> relu]: g (masked by _MaskScaleFn) is dL/dconv
+            sc_w = False
+            need_scaled_g = False
+        elif not ctx.prescaled:
             # dL/dconv = g * s: fold s into W for dX; scale g only for dW / db
             sc_w = need_x
             need_scaled_g = need_w or need_b
@@ -991,6 +996,30 @@ def conv_bn_relu(x: torch.Tensor, conv, bn, with_relu: bool) -> torch.Tensor:
     if not with_relu:
         return y
     # the ReLU module was folded into this call: keep its MemSave storage (bit mask)
+    return relu(y) if y.device.type in ("cuda", "meta") else torch.relu(y)
+
+
+def conv_relu_fusable(x: torch.Tensor, conv) -> bool:
+    if x.dim() != 4 or conv.groups != 1 or tuple(conv.dilation) != (1, 1):
+        return False
+    if conv.padding_mode != "zeros" or isinstance(conv.padding, str) or conv.out_channels % 8:
+        return False
+    if x.device.type == "meta":
+        return x.dtype in (torch.bfloat16, torch.float16)
+    return x.device.type == "cuda" and x.dtype in (torch.bfloat16, torch.float16) \
+        and conv.weight.dtype == x.dtype
+
+
+def conv_relu(x: torch.Tensor, conv) -> torch.Tensor:
+    """relu(conv(x)) with the ReLU (and its bit mask) in the conv epilogue (VGG);
+    the two memsave layers in sequence when the fused launch does not apply."""
+    if conv_relu_fusable(x, conv):
+        y, mask = _ConvBNFn.apply(x, conv.weight, conv.bias, None, conv.stride, conv.padding,
+                                  None, True)
+        if mask is not None:
+            return _MaskScaleFn.apply(y, mask, None)
+        return y
+    y = conv(x)
     return relu(y) if y.device.type in ("cuda", "meta") else torch.relu(y)
 
 

@@ -282,7 +282,9 @@ def fuse_conv_bn_relu(model: nn.Module, verbose: bool = False) -> nn.Module:
       epilogue when the BN is in eval mode with frozen parameters; the three
       layers otherwise, decided at run time);
     * ``a + b -> ReLU`` (the residual join of a ResNet block) into
-      :func:`functional.add_relu`.
+      :func:`functional.add_relu`, and ``conv -> BN -> add -> ReLU`` into
+      :func:`functional.conv_bn_add_relu` (residual read in the conv epilogue);
+    * ``conv -> ReLU`` (VGG) into :func:`functional.conv_relu`.
 
     Each intermediate is consumed only by the next op of the chain.  The saved
     set is the union of the fused layers' storage rules.  Models that torch.fx
@@ -337,6 +339,22 @@ def fuse_conv_bn_relu(model: nn.Module, verbose: bool = False) -> nn.Module:
         g.erase_node(r)
         g.erase_node(node)
         nadd += 1
+    # conv -> relu without a BN (VGG): ReLU and its mask in the conv epilogue
+    nrelu = 0
+    for node in list(g.nodes):
+        if node.op != "call_module" or type(modules.get(node.target)) not in (nn.Conv2d,
+                                                                             MemSaveConv2d):
+            continue
+        users = list(node.users)
+        if len(users) != 1 or not _is_relu(users[0], modules) or len(node.args) != 1:
+            continue
+        with g.inserting_before(node):
+            conv_ref = g.get_attr(node.target)
+            fused = g.call_function(MF.conv_relu, (node.args[0], conv_ref))
+        users[0].replace_all_uses_with(fused)
+        g.erase_node(users[0])
+        g.erase_node(node)
+        nrelu += 1
     # conv -> bn (no relu) whose only consumer is an add -> relu join: one launch
     # with the residual added in the conv epilogue
     nres = 0
@@ -360,8 +378,8 @@ def fuse_conv_bn_relu(model: nn.Module, verbose: bool = False) -> nn.Module:
     g.lint()
     gm.recompile()
     if verbose:
-        print(f"memsave: fused {nfused} conv->bn[->relu], {nadd} add->relu and {nres} "
-              f"conv->bn->add->relu chains")
+        print(f"memsave: fused {nfused} conv->bn[->relu], {nadd} add->relu, {nres} "
+              f"conv->bn->add->relu and {nrelu} conv->relu chains")
     return gm
 
 

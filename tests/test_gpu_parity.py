@@ -669,3 +669,31 @@ def test_conv_bn_add_relu_fused(x_rg, r_rg):
     if x_rg:
         wsq = oracle.round_to(wq * oracle.round_to(sc, "f32").reshape(-1, 1, 1, 1), "bf16")
         _close(x.grad, oracle.conv2d_dx(gm, wsq, 1, 1, h, w), "bf16", "x grad", ulps=2.01)
+
+
+@pytest.mark.parametrize("rg", [(1, 1, 1), (0, 1, 0), (1, 0, 0)])
+def test_conv_relu_fused(rg):
+    n, c, h, w, k = 2, 32, 12, 12, 64
+    rng = np.random.default_rng(23)
+    x, xq = _q(rng.standard_normal((n, c, h, w)), "bf16")
+    wt, wq = _q(rng.standard_normal((k, c, 3, 3)) / np.sqrt(c * 9), "bf16")
+    b, bq = _q(0.1 * rng.standard_normal(k), "bf16")
+    conv = torch.nn.Conv2d(c, k, 3, 1, 1).to(DEV, torch.bfloat16)
+    conv.weight.data.copy_(wt)
+    conv.bias.data.copy_(b)
+    conv.weight.requires_grad_(bool(rg[1]))
+    conv.bias.requires_grad_(bool(rg[2]))
+    x = x.contiguous(memory_format=torch.channels_last).requires_grad_(bool(rg[0]))
+    y = MF.conv_relu(x, conv)
+    z = oracle.conv2d_fwd(xq, wq, 1, 1) + bq.reshape(1, -1, 1, 1)
+    _close(y, np.maximum(z, 0), "bf16", "conv_relu y", ulps=2.01)
+    g, gq = _q(rng.standard_normal(z.shape), "bf16")
+    y.backward(g)
+    keep = y.detach().float().cpu().double().numpy() > 0
+    gm = np.where(keep, gq, 0.0)
+    if rg[0]:
+        _close(x.grad, oracle.conv2d_dx(gm, wq, 1, 1, h, w), "bf16", "conv_relu dx")
+    if rg[1]:
+        _close(conv.weight.grad, oracle.conv2d_dw(xq, gm, 1, 1, 3, 3), "bf16", "conv_relu dw")
+    if rg[2]:
+        _close(conv.bias.grad, gm.sum(axis=(0, 2, 3)), "bf16", "conv_relu db", ulps=2.01)
