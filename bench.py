@@ -16,7 +16,6 @@ no collective runs in the data path.
 from __future__ import annotations
 
 import argparse
-import copy
 import json
 import os
 import statistics
@@ -303,21 +302,20 @@ def gpu_main(args):
     pkg.lib()  # fail loudly if the native library is missing
 
     builder = BM.WORKLOADS[args.config]
-    wl = builder(batch=args.batch) if args.batch else builder()
-    if world > 1 and args.config != "resnet18":
-        pass  # weak scaling: every rank keeps the full per-GPU batch
-    stock_model = copy.deepcopy(wl.model)
-    layers_model = copy.deepcopy(wl.model) if not args.no_stock else None
-    unfused_model = copy.deepcopy(wl.model) if not args.no_stock else None
-    # the product: every supported layer swapped, conv -> BN(eval) -> ReLU and
-    # add -> ReLU chains fused by the fx pass (same saved set, fewer HBM passes)
+
+    def fresh():
+        """A new copy of the seeded workload (identical weights): only one model is
+        resident at a time, so every arm's peak is its own."""
+        return builder(batch=args.batch) if args.batch else builder()
+
+    # ---------------- memsave arm (the product): every supported layer swapped,
+    # conv -> BN(eval) -> ReLU, conv -> ReLU and residual joins fused by the fx pass
+    wl = fresh()
     wl.model = convert_to_memory_saving(wl.model, fuse=not args.no_fuse)
     inputs = list(wl.make_batch(wl.batch, dev))
     if wl.input_requires_grad:
         inputs[0].requires_grad_(True)
     sync = TrainableGradAllReduce(wl.model) if world > 1 else None
-
-    # ---------------- memsave arm (the product)
     n0 = pkg.launch_count()
     fam0 = pkg.launch_stats()
     with ClockSampler(local) as clocks:
@@ -330,63 +328,57 @@ def gpu_main(args):
     torch.cuda.synchronize(dev)
     per_step_launches = pkg.launch_count() - n1
     peak_mib, act_peak_mib = peak_memory(step, dev)
+    del step
+    inputs.clear()
+    torch.cuda.empty_cache()
     e2e_ms, e2e_wall, h2d, d2h = e2e_arm(wl, wl.model, args.steps, max(1, args.warmup // 2),
                                          world, dev, sync)
 
     samples = wl.batch * args.steps * world
     value = samples / (ms / 1e3)
     e2e_value = samples / (e2e_ms / 1e3)
+    wl.model = sync = None
+    torch.cuda.empty_cache()
+
+    def other_arm(convert_kwargs):
+        """(ms, peak MiB, activation peak MiB) of a fresh model, converted with
+        convert_kwargs (None = stock)."""
+        w2 = fresh()
+        if convert_kwargs is not None:
+            w2.model = convert_to_memory_saving(w2.model, **convert_kwargs)
+        ins = list(w2.make_batch(w2.batch, dev))
+        if w2.input_requires_grad:
+            ins[0].requires_grad_(True)
+        sy = TrainableGradAllReduce(w2.model) if world > 1 else None
+        ams, astep = run_arm(w2, w2.model, ins, args.steps, args.warmup, world, dev, sy)
+        apeak, aact = peak_memory(astep, dev)
+        del astep, ins, w2, sy
+        torch.cuda.empty_cache()
+        return ams, apeak, aact
 
     # ---------------- stock arm (same weights, unconverted) for the "vs PyTorch" part
-    del step
-    inputs.clear()
     stock = {}
     if not args.no_stock:
-        torch.cuda.empty_cache()
-        sinputs = list(wl.make_batch(wl.batch, dev))
-        if wl.input_requires_grad:
-            sinputs[0].requires_grad_(True)
-        ssync = TrainableGradAllReduce(stock_model) if world > 1 else None
-        sms, sstep = run_arm(wl, stock_model, sinputs, args.steps, args.warmup, world, dev, ssync)
-        speak, sact = peak_memory(sstep, dev)
+        sms, speak, sact = other_arm(None)
         stock = {"value": samples / (sms / 1e3), "ms_per_step": sms / args.steps,
                  "peak_mib": speak, "activation_peak_mib": sact,
                  "impl": "torch %s stock modules (cuDNN/cuBLAS), same weights/inputs"
                          % torch.__version__}
-        del sstep, sinputs
-        torch.cuda.empty_cache()
         # the north star's layer set only (Linear / Conv2d / BatchNorm2d-eval), ReLU and
         # MaxPool2d left stock: isolates the paper's Fig. 2 effect from the §8(f) swaps
-        convert_to_memory_saving(layers_model, relu=False, maxpool2d=False, dropout=False,
-                                 layernorm=False, conv_transpose2d=False)
-        linputs = list(wl.make_batch(wl.batch, dev))
-        if wl.input_requires_grad:
-            linputs[0].requires_grad_(True)
-        lsync = TrainableGradAllReduce(layers_model) if world > 1 else None
-        lms, lstep = run_arm(wl, layers_model, linputs, args.steps, args.warmup, world, dev, lsync)
-        lpeak, lact = peak_memory(lstep, dev)
+        lms, lpeak, lact = other_arm(dict(relu=False, maxpool2d=False, dropout=False,
+                                          layernorm=False, conv_transpose2d=False))
         stock["memsave_layers_only"] = {
             "value": round(samples / (lms / 1e3), 2), "ms_per_step": round(lms / args.steps, 4),
             "peak_mib": round(lpeak, 1), "activation_peak_mib": round(lact, 1),
             "swaps": "Linear, Conv2d, BatchNorm2d(eval) only"}
-        del lstep, linputs
-        torch.cuda.empty_cache()
         if not args.no_fuse:  # every layer swapped, no fx fusion
-            unfused_model = convert_to_memory_saving(unfused_model, fuse=False)
-            uinputs = list(wl.make_batch(wl.batch, dev))
-            if wl.input_requires_grad:
-                uinputs[0].requires_grad_(True)
-            usync = TrainableGradAllReduce(unfused_model) if world > 1 else None
-            ums, ustep = run_arm(wl, unfused_model, uinputs, args.steps, args.warmup, world, dev,
-                                 usync)
-            upeak, uact = peak_memory(ustep, dev)
+            ums, upeak, uact = other_arm(dict(fuse=False))
             stock["memsave_unfused"] = {
                 "value": round(samples / (ums / 1e3), 2),
                 "ms_per_step": round(ums / args.steps, 4), "peak_mib": round(upeak, 1),
                 "activation_peak_mib": round(uact, 1),
                 "swaps": "all supported layers, convert_to_memory_saving(fuse=False)"}
-            del ustep, uinputs
-            torch.cuda.empty_cache()
 
     # ---------------- roofline of the dominant kernel (rank 0)
     roof = None
@@ -416,7 +408,7 @@ def gpu_main(args):
     # ---------------- CPU baseline (rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(args.config, wl, min_seconds=args.cpu_seconds)
+        cpu = cpu_baseline(args.config, None, min_seconds=args.cpu_seconds)
 
     out = {
         "metric": METRIC,
