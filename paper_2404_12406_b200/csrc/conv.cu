@@ -62,6 +62,7 @@ struct ConvPlan {
   int xw_pad = 0;       // rowseg: padded width of the 4-channel activation copy
   bool band = false;    // dx: <8-channel input gradient (the stem), band col2im
   bool stem = false;    // dx: the 3-channel 7x7/2 stem, register col2im (stem_dgrad.cu)
+  bool halo3 = false;   // fwd / dx: 3x3/1/1 64->64 halo-tiled kernel (conv3x3.cu)
   int band_h = 16;
   size_t ws_pad = 0, ws_w = 0, ws_acc = 0;
   size_t ws = 0;
@@ -102,6 +103,12 @@ ConvPlan plan(const ms_conv_desc* d, int pass, bool dx_bias = false) {
   }
   if (pass == MS_CONV_FWD) {
     p.tc = true;
+    if (conv3x3_halo_ok(d->dtype, d->layout, (int)d->c, (int)d->k, (int)d->r, (int)d->s,
+                        d->stride_h, d->stride_w, d->pad_h, d->pad_w, (int)d->w)) {
+      p.halo3 = true;
+      p.ws = conv3x3_halo_workspace();
+      return p;
+    }
     if (rowseg_ok(d, c)) {
       p.rowseg = true;
       p.xw_pad = (int)std::max<int64_t>(d->w + 2 * d->pad_w, (int64_t)(c.ow - 1) * 2 + 8);
@@ -140,6 +147,14 @@ ConvPlan plan(const ms_conv_desc* d, int pass, bool dx_bias = false) {
       p.kpad = (int)round_up(d->k, 64);
       p.ws_w = align256(es * (size_t)taps * d->c * p.kpad);
       p.ws = p.ws_w;
+      return p;
+    }
+    if (conv3x3_halo_ok(d->dtype, d->layout, (int)d->k, (int)d->c, (int)d->r, (int)d->s,
+                        d->stride_h, d->stride_w, d->pad_h, d->pad_w, (int)d->w)) {
+      p.tc = true;
+      p.halo3 = true;
+      p.kpad = (int)round_up(d->k, 64);  // the phase-GEMM fallback (with a bias) uses it
+      p.ws = std::max(conv3x3_halo_workspace(), align256(es * (size_t)d->c * taps * p.kpad));
       return p;
     }
     if (d->stride_h > 2 || d->stride_w > 2) return p;  // SIMT
@@ -241,6 +256,11 @@ ms_status fwd_rowseg(const ms_conv_desc* d, const ConvPlan& p, const void* x, co
 ms_status fwd_tc(const ms_conv_desc* d, const ConvPlan& p, const void* x, const void* w,
                  const void* bias, void* y, void* ws, cudaStream_t st, const Fuse* f = nullptr) {
   if (p.rowseg) return fwd_rowseg(d, p, x, w, bias, y, ws, st, f);
+  if (p.halo3)
+    return conv3x3_halo(d->dtype, (int)d->n, (int)d->h, (int)d->w, d->wlayout, 0, x, w, ws, y,
+                        f ? f->scale : nullptr, f ? f->shift : nullptr, bias,
+                        f ? f->resid : nullptr, f ? f->relu : 0, f ? f->mask : nullptr, nullptr,
+                        nullptr, 0, 0.f, st);
   const ConvDims c = dims_of(d);
   const int dt = d->dtype;
   uint8_t* wsb = static_cast<uint8_t*>(ws);
@@ -326,6 +346,10 @@ ms_status dx_tc(const ms_conv_desc* d, const ConvPlan& p, const void* dy, const 
   const ConvDims c = dims_of(d);
   const int dt = d->dtype;
   if (p.band) return dx_band(d, p, dy, w, dx, ws, st);
+  if (p.halo3 && !bias)  // the input-VJP is the same 3x3 conv of dY with W transposed + flipped
+    return conv3x3_halo(d->dtype, (int)d->n, (int)d->h, (int)d->w, d->wlayout, 1, dy, w, ws, dx,
+                        nullptr, nullptr, nullptr, nullptr, 0, nullptr, ks ? ks->var : nullptr,
+                        ks ? ks->weight : nullptr, ks ? ks->pdt : 0, ks ? ks->eps : 0.f, st);
   if (p.stem) {
     MS_TRY(repack_scatter(dt, c.k, c.c, c.r, c.s, p.kpad, d->wlayout, w, ws, st));
     return stem_dgrad(dt, c.n, c.h, c.w, c.oh, c.ow, c.k, dy, ws, dx, st);

@@ -36,6 +36,17 @@ ms_status stem_fprop(int dt, int n, int h, int wp, int p, int q, int k, int c, i
                      cudaStream_t st, const float* scale = nullptr, const float* shift = nullptr,
                      int relu = 0, uint8_t* mask = nullptr);
 
+// 3x3/1/1 64->64-channel convolution, halo-tiled (conv3x3.cu); transpose = 1 is
+// the input-VJP of the same conv (x = dY, y = dX)
+bool conv3x3_halo_ok(int dt, int layout, int c, int k, int r, int s, int sh, int sw, int ph,
+                     int pw, int w);
+size_t conv3x3_halo_workspace();
+ms_status conv3x3_halo(int dt, int n, int h, int w, int wlayout, int transpose, const void* x,
+                       const void* wt, void* ws, void* y, const float* scale, const float* shift,
+                       const void* bias, const void* resid, int relu, uint8_t* mask,
+                       const void* ks_var, const void* ks_w, int ks_pdt, float ks_eps,
+                       cudaStream_t st);
+
 inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 inline size_t align256(size_t v) { return (v + 255) & ~static_cast<size_t>(255); }
 

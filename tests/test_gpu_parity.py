@@ -111,6 +111,9 @@ TC_CASES = [
     (2, 16, 12, 12, 24, 5, 1, 2),      # 5x5
     (3, 3, 45, 37, 64, 7, 2, 3),       # stem, odd sizes: C8 fprop + scatter dgrad
     (2, 8, 20, 20, 32, 3, 1, 1),       # C=8: C8 fprop, 8-channel dgrad phases
+    (2, 64, 9, 13, 64, 3, 1, 1),       # 64->64 3x3/1/1: halo kernel, odd H (partial tile)
+    (1, 64, 56, 56, 64, 3, 1, 1),      # ResNet layer1 geometry
+    (3, 64, 7, 62, 64, 3, 1, 1),       # widest row the 64-pixel pitch allows
 ]
 
 
@@ -530,6 +533,7 @@ def test_conv_transpose_tcgen05(case):
 
 # ------------------------------------------------------------------ fused conv -> BN-eval -> ReLU
 @pytest.mark.parametrize("case", [(2, 64, 14, 14, 128, 3, 1, 1, True), (2, 3, 32, 32, 64, 7, 2, 3, True),
+                                  (2, 64, 11, 20, 64, 3, 1, 1, True), (1, 64, 12, 9, 64, 3, 1, 1, False),
                                   (3, 128, 9, 9, 256, 3, 2, 1, False), (2, 64, 8, 8, 64, 1, 1, 0, True)])
 def test_conv_bn_relu_fused(case):
     n, c, h, w, k, r, s, p, with_relu = case
