@@ -171,11 +171,25 @@ def _max_over_ranks(v: float, world: int) -> float:
     return float(t.item())
 
 
+def prime(wl, model, dev):
+    """Setup, not a step: one fwd+bwd at batch 2 so every kernel image is loaded
+    (lazy module loading) and one-time host state exists before warm-up."""
+    import torch
+    ins = list(wl.make_batch(min(2, wl.batch), dev))
+    if wl.input_requires_grad:
+        ins[0].requires_grad_(True)
+    wl.loss_fn(model, *ins).backward()
+    for p in model.parameters():
+        p.grad = None
+    torch.cuda.synchronize(dev)
+
+
 def run_arm(wl, model, batch_inputs, steps, warmup, world, dev, sync=None):
     """Time `steps` fwd+bwd steps (device time, CUDA events, max over ranks)."""
     import torch
 
     x = batch_inputs[0]
+    prime(wl, model, dev)
 
     def step():
         if wl.input_requires_grad:
