@@ -111,10 +111,11 @@ class ClockSampler:
 # committed under profiles/); keyed by (pass, C, R, stride) of the ResNet-18 shapes
 _NCU_CSV = os.path.join(ROOT, "profiles", "r1_ncu_r18_kernels.csv")
 _NCU_NAME = {("conv_fwd", 3, 7, 2): "stem_fwd", ("conv_dx", 3, 7, 2): "stem_dx",
-             ("conv_dx", 64, 3, 1): "layer1_dgrad"}
-_KERNEL_OF = {("conv_fwd", 3, 7, 2): "umma_gemm_kernel<64,0,0,LOAD_CONV_FPROP_ROWSEG>",
+             ("conv_fwd", 64, 3, 1): "layer1_fwd", ("conv_dx", 64, 3, 1): "layer1_dgrad"}
+_KERNEL_OF = {("conv_fwd", 3, 7, 2): "stem_fprop_kernel",
               ("conv_dx", 3, 7, 2): "stem_dgrad_kernel",
-              ("conv_dx", 64, 3, 1): "umma_gemm_kernel<64,0,0,LOAD_CONV_DGRAD>"}
+              ("conv_fwd", 64, 3, 1): "conv3x3_halo_kernel",
+              ("conv_dx", 64, 3, 1): "conv3x3_halo_kernel (transposed)"}
 
 
 def _kernel_key(e):
@@ -402,7 +403,15 @@ def gpu_main(args):
             for ent in KB.conv_roofline(n, c, h, w, k, r, s, p, dev, peaks, reps=5):
                 ent["count_per_step"] = cnt
                 layers.append(ent)
-        dom = max(layers, key=lambda e: e["ms"] * e["count_per_step"])
+        # the same (pass, geometry) appears once per position in the network
+        tot = {}
+        for e in layers:
+            key = (e["kind"], tuple(sorted(e["geom"].items())))
+            tot[key] = tot.get(key, 0.0) + e["ms"] * e["count_per_step"]
+        dom = max(layers, key=lambda e: tot[(e["kind"], tuple(sorted(e["geom"].items())))])
+        dom = dict(dom, count_per_step=sum(
+            x["count_per_step"] for x in layers
+            if (x["kind"], x["geom"]) == (dom["kind"], dom["geom"])))
         traffic, tsrc = _ncu_traffic(dom)
         roof = {"bound": dom["bound"], "achieved": round(dom["achieved"], 2),
                 "peak": dom["peak"], "unit": dom["unit"], "frac": round(dom["frac"], 4),
@@ -411,6 +420,7 @@ def gpu_main(args):
                 "kernel": "%s (%s)" % (_KERNEL_OF.get(_kernel_key(dom), "umma_gemm_kernel"),
                                        dom["kind"]),
                 "geom": dom["geom"], "launch_ms": round(dom["ms"], 4),
+                "launches_per_step": dom["count_per_step"],
                 "per_unit": "2*N*OH*OW*K*C*R*S flops per launch (implicit GEMM)",
                 "peak_source": peaks["source"] + ", burst (kernel timed alone)"}
         total_conv_ms = sum(e["ms"] * e["count_per_step"] for e in layers)
