@@ -240,11 +240,17 @@ __device__ __forceinline__ float warp_sum(float v) {
 
 constexpr int LN_WARPS = 8;
 
-// one warp per row, KV slabs of 256 columns (8 per lane) held in registers
+// KV slabs of 256 columns (8 per lane) held in registers
+template <int KV> struct LnRows {  // rows per warp (2 halves the resident warps: slower)
+  static constexpr int BWD = 1;
+};
+
 template <typename T, int KV>
 __global__ void __launch_bounds__(LN_WARPS * 32) ln_fwd_vec(int64_t rows, int D, const T* x,
                                                             const T* w, const T* b, float eps,
                                                             T* y, float* mean, float* rstd) {
+  // one row per warp; w / b are read after the reductions so few registers are
+  // live and many warps per SM keep HBM busy (measured faster than prefetching)
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * LN_WARPS + (threadIdx.x >> 5);
   if (row >= rows) return;
@@ -295,6 +301,73 @@ __global__ void __launch_bounds__(LN_WARPS * 32) ln_fwd_vec(int64_t rows, int D,
   if (lane == 0) {
     if (mean) mean[row] = mu;
     if (rstd) rstd[row] = r;
+  }
+}
+
+// input-VJP only (frozen w / b: BERT's LayerNorms), LN_RPW rows per warp, all
+// loads issued up front
+template <typename T, int KV>
+__global__ void __launch_bounds__(LN_WARPS * 32) ln_bwd_dx_vec(int64_t rows, int D, const T* g,
+                                                               const T* x, const float* mean,
+                                                               const float* rstd, const T* w,
+                                                               T* dx) {
+  constexpr int LN_RPW = LnRows<KV>::BWD;
+  const int lane = threadIdx.x & 31;
+  const int64_t row0 = ((int64_t)blockIdx.x * LN_WARPS + (threadIdx.x >> 5)) * LN_RPW;
+  if (row0 >= rows) return;
+  float xv[LN_RPW][KV][8], gv[LN_RPW][KV][8], wv[KV][8];
+  float mu[LN_RPW], rs[LN_RPW];
+#pragma unroll
+  for (int rr = 0; rr < LN_RPW; ++rr) {
+    const int64_t row = row0 + rr < rows ? row0 + rr : row0;
+    mu[rr] = mean[row];
+    rs[rr] = rstd[row];
+#pragma unroll
+    for (int k = 0; k < KV; ++k) {
+      const int col = (k * 32 + lane) * 8;
+      if (col < D) {
+        ld8<T>(x + row * D + col, xv[rr][k], true);
+        ld8<T>(g + row * D + col, gv[rr][k], true);
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < KV; ++k) {
+    const int col = (k * 32 + lane) * 8;
+    if (col < D && w) {
+      ld8<T>(w + col, wv[k], true);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) wv[k][j] = 1.f;
+    }
+  }
+#pragma unroll
+  for (int rr = 0; rr < LN_RPW; ++rr) {
+    const int64_t row = row0 + rr;
+    if (row >= rows) break;
+    float a = 0.f, c = 0.f;
+#pragma unroll
+    for (int k = 0; k < KV; ++k)
+      if ((k * 32 + lane) * 8 < D)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          xv[rr][k][j] = (xv[rr][k][j] - mu[rr]) * rs[rr];
+          const float gw = gv[rr][k][j] * wv[k][j];
+          gv[rr][k][j] = gw;
+          a += gw;
+          c += gw * xv[rr][k][j];
+        }
+    const float ma = warp_sum(a) / D, mc = warp_sum(c) / D;
+#pragma unroll
+    for (int k = 0; k < KV; ++k) {
+      const int col = (k * 32 + lane) * 8;
+      if (col < D) {
+        float o[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[j] = rs[rr] * (gv[rr][k][j] - ma - xv[rr][k][j] * mc);
+        st8<T>(dx + row * D + col, o, true);
+      }
+    }
   }
 }
 
@@ -517,8 +590,8 @@ extern "C" ms_status ms_layernorm_fwd(int64_t rows, int64_t dim, int32_t dt, con
   const int kv = ln_kv(dim, dt, ps, 4);
   const int D = (int)dim;
   if (kv > 0) {
-    const unsigned grid = (unsigned)((rows + LN_WARPS - 1) / LN_WARPS);
-    MS_DT_DISPATCH(dt, MS_KV_SWITCH(kv, (ln_fwd_vec<T, KV><<<grid, LN_WARPS * 32, 0, st>>>(
+    MS_DT_DISPATCH(dt, MS_KV_SWITCH(kv, (ln_fwd_vec<T, KV><<<
+                           (unsigned)((rows + LN_WARPS - 1) / LN_WARPS), LN_WARPS * 32, 0, st>>>(
                                             rows, D, (const T*)x, (const T*)w, (const T*)b,
                                             (float)eps, (T*)y, mean, rstd))));
   } else {
@@ -564,10 +637,12 @@ extern "C" ms_status ms_layernorm_bwd(int64_t rows, int64_t dim, int32_t dt, con
                                                 rows, D, (const T*)g, (const T*)x, mean, rstd,
                                                 (const T*)w, (T*)dx, dwa, dba))));
       } else {
-        MS_DT_DISPATCH(dt, MS_KV_SWITCH(kv, (ln_bwd_vec<T, KV, false><<<(unsigned)grid,
-                                                                        LN_WARPS * 32, 0, st>>>(
+        MS_DT_DISPATCH(dt, MS_KV_SWITCH(kv, (ln_bwd_dx_vec<T, KV><<<
+                               (unsigned)((rows + LN_WARPS * LnRows<KV>::BWD - 1) /
+                                          (LN_WARPS * LnRows<KV>::BWD)),
+                               LN_WARPS * 32, 0, st>>>(
                                                 rows, D, (const T*)g, (const T*)x, mean, rstd,
-                                                (const T*)w, (T*)dx, nullptr, nullptr))));
+                                                (const T*)w, (T*)dx))));
       }
     } else {
       MS_CHECK_ARG(rows < (1ll << 31), MS_ERR_UNSUPPORTED, "layernorm: too many rows");
