@@ -172,7 +172,7 @@ def _max_over_ranks(v: float, world: int) -> float:
     return float(t.item())
 
 
-def prime(wl, model, dev):
+def prime(wl, model, dev, sync=None):
     """Setup, not a step: one fwd+bwd at batch 2 so every kernel image is loaded
     (lazy module loading) and one-time host state exists before warm-up."""
     import torch
@@ -180,6 +180,8 @@ def prime(wl, model, dev):
     if wl.input_requires_grad:
         ins[0].requires_grad_(True)
     wl.loss_fn(model, *ins).backward()
+    if sync is not None:  # the gradient hooks fired: complete their collectives
+        sync.finish()
     for p in model.parameters():
         p.grad = None
     torch.cuda.synchronize(dev)
@@ -190,7 +192,7 @@ def run_arm(wl, model, batch_inputs, steps, warmup, world, dev, sync=None):
     import torch
 
     x = batch_inputs[0]
-    prime(wl, model, dev)
+    prime(wl, model, dev, sync)
 
     def step():
         if wl.input_requires_grad:
