@@ -342,13 +342,15 @@ struct KScale {  // an eval-BN scale w/sqrt(var+eps) folded into the dgrad weigh
 
 ms_status dx_tc(const ms_conv_desc* d, const ConvPlan& p, const void* dy, const void* w, void* dx,
                 void* ws, cudaStream_t st, const void* bias = nullptr,
-                const KScale* ks = nullptr) {
+                const KScale* ks = nullptr, const void* addend = nullptr) {
   const ConvDims c = dims_of(d);
   const int dt = d->dtype;
+  MS_CHECK_ARG(!addend || (!p.band && !p.stem), MS_ERR_UNSUPPORTED,
+               "conv dx: no fused addend in the stem / band kernels");
   if (p.band) return dx_band(d, p, dy, w, dx, ws, st);
   if (p.halo3 && !bias)  // the input-VJP is the same 3x3 conv of dY with W transposed + flipped
     return conv3x3_halo(d->dtype, (int)d->n, (int)d->h, (int)d->w, d->wlayout, 1, dy, w, ws, dx,
-                        nullptr, nullptr, nullptr, nullptr, 0, nullptr, ks ? ks->var : nullptr,
+                        nullptr, nullptr, nullptr, addend, 0, nullptr, ks ? ks->var : nullptr,
                         ks ? ks->weight : nullptr, ks ? ks->pdt : 0, ks ? ks->eps : 0.f, st);
   if (p.stem) {
     MS_TRY(repack_scatter(dt, c.k, c.c, c.r, c.s, p.kpad, d->wlayout, w, ws, st));
@@ -405,6 +407,7 @@ ms_status dx_tc(const ms_conv_desc* d, const ConvPlan& p, const void* dy, const 
   g.nphases = np;
   g.num_tiles = tiles;
   g.epi = EpiParams{dx, c.c, dt, 0, bias, dt};  // bias: conv_transpose2d forward
+  g.epi.resid = addend;                          // dx = dgrad + addend (tee'd input)
   const int64_t wrow = (int64_t)c.r * c.s * p.kpad;
   MS_TRY(make_tmap_2d(&tm.b, dt, wd, wrow, c.c, wrow, BK, bn / tp.cl));
   return launch_umma(bn, 0, 0, LOAD_CONV_DGRAD, tm, g, st, tp.cl);
@@ -653,20 +656,23 @@ extern "C" ms_status ms_conv2d_bn_fwd(const ms_conv_desc* d, const void* x, cons
 
 extern "C" ms_status ms_conv2d_bn_dx(const ms_conv_desc* d, const void* dy, const void* w,
                                      const void* bn_var, const void* bn_weight, int32_t bn_pdtype,
-                                     double eps, void* dx, void* ws, size_t ws_bytes,
-                                     void* stream) {
+                                     double eps, const void* addend, void* dx, void* ws,
+                                     size_t ws_bytes, void* stream) {
   MS_TRY(validate(d));
   MS_TRY(bind_device(dx));
   if (d->n == 0) return MS_OK;
   ConvPlan p = plan(d, MS_CONV_DX, /*dx_bias=*/true);  // the generic phase GEMM, no band kernel
-  MS_CHECK_ARG(p.tc && !p.stem && !p.band && bn_var, MS_ERR_UNSUPPORTED,
-               "conv+bn dx: the folded-scale path needs the tcgen05 phase GEMM");
+  MS_CHECK_ARG(p.tc && !p.stem && !p.band, MS_ERR_UNSUPPORTED,
+               "conv+bn dx: the folded-scale / addend path needs the tcgen05 dgrad");
   MS_CHECK_ARG(ws_bytes >= p.ws && (p.ws == 0 || ws), MS_ERR_WORKSPACE,
                "conv+bn dx: workspace %zu < %zu", ws_bytes, p.ws);
+  MS_CHECK_ARG(!addend || (reinterpret_cast<uintptr_t>(addend) & 15) == 0, MS_ERR_ALIGN,
+               "conv+bn dx: addend must be 16-byte aligned");
   KScale ks;
   ks.var = bn_var;
   ks.weight = bn_weight;
   ks.pdt = bn_pdtype;
   ks.eps = (float)eps;
-  return dx_tc(d, p, dy, w, dx, ws, (cudaStream_t)stream, nullptr, &ks);
+  return dx_tc(d, p, dy, w, dx, ws, (cudaStream_t)stream, nullptr, bn_var ? &ks : nullptr,
+               addend);
 }

@@ -799,8 +799,11 @@ class _ConvBNFn(torch.autograd.Function):
     gradient is never rescaled."""
 
     @staticmethod
-    def forward(ctx, x, weight, bias, residual, stride, padding, bn, relu: bool):
+    def forward(ctx, x, weight, bias, residual, stride, padding, bn, relu: bool, tee=False):
+        # tee: also return x itself, for x's other consumer; backward then adds that
+        # consumer's gradient in the dgrad epilogue instead of the engine summing it
         x_rg, w_rg, b_rg = ctx.needs_input_grad[0], ctx.needs_input_grad[1], ctx.needs_input_grad[2]
+        ctx.tee = bool(tee)
         out_rg = x_rg or w_rg or b_rg or ctx.needs_input_grad[3]
         ctx.set_materialize_grads(False)  # the mask output never gets a gradient: no zero fill
         # the incoming gradient is already masked and scaled (_MaskScaleFn) only for
@@ -823,7 +826,7 @@ class _ConvBNFn(torch.autograd.Function):
             ctx.layouts = (_lib.MS_NCHW, _lib.MS_NCHW)
             if mask is not None:
                 ctx.mark_non_differentiable(mask)
-            return x.new_empty(out_shape), mask
+            return (x.new_empty(out_shape), mask, x) if tee else (x.new_empty(out_shape), mask)
         _require_cuda("conv_bn", x, weight, bias)
         layout, wlayout = _conv_layouts(x, weight)
         xl = _as_layout(x, layout)
@@ -848,13 +851,13 @@ class _ConvBNFn(torch.autograd.Function):
         ctx.save_for_backward(xl if "x" in roles else None, wl if "w" in roles else None)
         if mask is not None:
             ctx.mark_non_differentiable(mask)
-        return y, mask
+        return (y, mask, x) if tee else (y, mask)
 
     @staticmethod
-    def backward(ctx, gy, _gmask=None):
+    def backward(ctx, gy, _gmask=None, g_tee=None):
         x, w = ctx.saved_tensors
         if gy is None:  # grads are not materialised (set_materialize_grads(False))
-            return None, None, None, None, None, None, None, None
+            return g_tee, None, None, None, None, None, None, None, None
         need_x, need_w, need_b = ctx.needs_input_grad[:3]
         x_shape, w_shape, stride, padding = ctx.geom
         dx = dw = db = None
@@ -862,6 +865,8 @@ class _ConvBNFn(torch.autograd.Function):
         mean, var, bw, eps = ctx.bn if ctx.bn is not None else (None, None, None, 0.0)
         g = _as_layout(gy, layout)
         del gy
+        addend = _as_layout(g_tee, layout) if (need_x and g_tee is not None) else None
+        del g_tee
         need_r = ctx.needs_input_grad[3]
         d_res = g if need_r else None  # the residual's gradient is the (masked) gradient
         if ctx.bn is None:  # conv [-> relu]: g (masked by _MaskScaleFn) is dL/dconv
@@ -884,7 +889,7 @@ class _ConvBNFn(torch.autograd.Function):
                 dw = gc.new_empty(w_shape)
             if need_b:
                 db = gc.new_empty((w_shape[0],))
-            return dx, dw, db, d_res, None, None, None, None
+            return dx, dw, db, d_res, None, None, None, None, None
         L = _lib.lib()
         st = _stream(g.device)
         dt = _dtype_code(g)
@@ -894,18 +899,25 @@ class _ConvBNFn(torch.autograd.Function):
             dx = _empty4(x_shape, g, layout)
             wsp, nb = _workspace(L.ms_conv2d_workspace(ctypes.byref(d), _lib.MS_CONV_DX), g.device)
             folded = False
-            if sc_w:  # BN scale folded into the repacked dgrad weight (no pass over g)
-                st_ = L.ms_conv2d_bn_dx(ctypes.byref(d), _ptr(g), _ptr(w), _ptr(var), _ptr(bw),
-                                        _dtype_code(var), eps, _ptr(dx), _ptr(wsp), nb, st)
+            if sc_w or addend is not None:
+                # BN scale folded into the repacked dgrad weight (no pass over g) and/or
+                # the tee'd consumer's gradient added in the epilogue
+                st_ = L.ms_conv2d_bn_dx(ctypes.byref(d), _ptr(g), _ptr(w),
+                                        _ptr(var) if sc_w else None, _ptr(bw) if sc_w else None,
+                                        _dtype_code(var) if sc_w else dt, eps, _ptr(addend),
+                                        _ptr(dx), _ptr(wsp), nb, st)
                 folded = st_ == 0
                 if st_ not in (0, 4):  # 4 = MS_ERR_UNSUPPORTED: scale the weight here
                     _lib.check(st_, "ms_conv2d_bn_dx")
-                if not folded:
+                if not folded and sc_w:
                     sc = (bw.float() if bw is not None else 1.0) * torch.rsqrt(var.float() + eps)
                     w = _as_layout((w.float() * sc.view(-1, 1, 1, 1)).to(w.dtype), wlayout)
             if not folded:
                 _lib.check(L.ms_conv2d_dx(ctypes.byref(d), _ptr(g), _ptr(w), _ptr(dx), _ptr(wsp),
                                           nb, st), "ms_conv2d_dx")
+                if addend is not None:
+                    dx.add_(addend)
+            del addend
         if need_w or need_b:
             gc = g
             if need_scaled_g:
@@ -928,7 +940,7 @@ class _ConvBNFn(torch.autograd.Function):
                 wsp, nb = _workspace(4 * w_shape[0], gc.device)
                 _lib.check(L.ms_conv2d_db(ctypes.byref(d), _ptr(gc), _ptr(db), _ptr(wsp), nb, st),
                            "ms_conv2d_db")
-        return dx, dw, db, d_res, None, None, None, None
+        return dx, dw, db, d_res, None, None, None, None, None
 
 
 class _MaskScaleFn(torch.autograd.Function):
@@ -997,6 +1009,20 @@ def conv_bn_relu(x: torch.Tensor, conv, bn, with_relu: bool) -> torch.Tensor:
         return y
     # the ReLU module was folded into this call: keep its MemSave storage (bit mask)
     return relu(y) if y.device.type in ("cuda", "meta") else torch.relu(y)
+
+
+def conv_bn_relu_tee(x: torch.Tensor, conv, bn, with_relu: bool):
+    """(conv_bn_relu(x, conv, bn, with_relu), x'): x' is x itself (a view, no
+    copy) for x's other consumer, e.g. the identity or downsample branch of a
+    ResNet block.  Its gradient is added to dX inside the dgrad epilogue, which
+    replaces the engine's separate accumulation pass over the two gradients."""
+    if conv_bn_fusable(x, conv, bn):
+        y, mask, xt = _ConvBNFn.apply(x, conv.weight, conv.bias, None, conv.stride,
+                                      conv.padding, bn, with_relu, True)
+        if with_relu and mask is not None:
+            return _MaskScaleFn.apply(y, mask, bn), xt
+        return y, xt
+    return conv_bn_relu(x, conv, bn, with_relu), x
 
 
 def conv_relu_fusable(x: torch.Tensor, conv) -> bool:

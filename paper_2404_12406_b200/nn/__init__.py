@@ -11,6 +11,8 @@ replaces ``forward`` with the selective-save function from
 
 from __future__ import annotations
 
+import operator
+
 import torch
 from torch import nn
 
@@ -254,7 +256,6 @@ def _convert_one(mod: nn.Module, kinds: dict, clone_params: bool, counter: list)
 
 
 def _is_relu(node, modules) -> bool:
-    import operator  # noqa: F401
     if node.op == "call_module":
         return isinstance(modules.get(node.target), nn.ReLU)
     if node.op == "call_function":
@@ -265,7 +266,6 @@ def _is_relu(node, modules) -> bool:
 
 
 def _is_add(node) -> bool:
-    import operator
     if node.op == "call_function" and node.target in (operator.add, operator.iadd, torch.add):
         return len(node.args) == 2 and not node.kwargs
     if node.op == "call_method" and node.target in ("add", "add_"):
@@ -374,12 +374,35 @@ def fuse_conv_bn_relu(model: nn.Module, verbose: bool = False) -> nn.Module:
                 g.erase_node(main)
                 nres += 1
                 break
+    # a tensor read by a fused conv and by one more fused op (a ResNet block input:
+    # conv1 and the identity / downsample branch): the conv tees it, so the two
+    # gradients are summed in its dgrad epilogue rather than by a separate pass
+    ntee = 0
+    order = {n: i for i, n in enumerate(g.nodes)}
+    tee_ok = (MF.conv_bn_relu, MF.conv_bn_add_relu, MF.add_relu, MF.conv_relu)
+    for node in list(g.nodes):
+        users = sorted(node.users, key=order.get)
+        if len(users) != 2:
+            continue
+        u1, u2 = users
+        if (u1.op != "call_function" or u1.target is not MF.conv_bn_relu or u1.kwargs
+                or u1.args[0] is not node or sum(a is node for a in u1.args) != 1
+                or u2.op != "call_function" or u2.target not in tee_ok or u2.kwargs):
+            continue
+        with g.inserting_before(u1):
+            tee = g.call_function(MF.conv_bn_relu_tee, u1.args)
+            out = g.call_function(operator.getitem, (tee, 0))
+            alias = g.call_function(operator.getitem, (tee, 1))
+        u1.replace_all_uses_with(out)
+        g.erase_node(u1)
+        u2.args = tuple(alias if a is node else a for a in u2.args)
+        ntee += 1
     g.eliminate_dead_code()
     g.lint()
     gm.recompile()
     if verbose:
         print(f"memsave: fused {nfused} conv->bn[->relu], {nadd} add->relu, {nres} "
-              f"conv->bn->add->relu and {nrelu} conv->relu chains")
+              f"conv->bn->add->relu and {nrelu} conv->relu chains; {ntee} tee'd inputs")
     return gm
 
 

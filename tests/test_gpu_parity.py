@@ -582,6 +582,49 @@ def test_conv_bn_relu_fused(case):
     _close(x.grad, ref, "bf16", "conv_bn_relu dx", ulps=2.01)
 
 
+@pytest.mark.parametrize("case", [(2, 64, 11, 20, 64, 1, True),    # 3x3 halo dgrad
+                                  (2, 64, 9, 14, 128, 2, True),    # stride-2 phase GEMM
+                                  (2, 128, 7, 7, 128, 1, False),   # folded BN scale
+                                  (1, 64, 6, 6, 64, 1, False)])
+def test_conv_bn_relu_tee(case):
+    # x feeds the conv and a second consumer: the second consumer's gradient is
+    # added to dX inside the dgrad epilogue (one rounding of dgrad + addend)
+    n, c, h, w, k, s, with_relu = case
+    rng = np.random.default_rng(c + k + s)
+    x, xq = _q(rng.standard_normal((n, c, h, w)), "bf16")
+    wt, wq = _q(rng.standard_normal((k, c, 3, 3)) / np.sqrt(c * 9), "bf16")
+    conv = torch.nn.Conv2d(c, k, 3, s, 1, bias=False).to(DEV, torch.bfloat16)
+    conv.weight.data.copy_(wt)
+    conv.weight.requires_grad_(False)
+    bn = torch.nn.BatchNorm2d(k).to(DEV, torch.bfloat16).eval()
+    bn.running_mean.copy_(torch.linspace(-0.2, 0.2, k))
+    bn.running_var.copy_(torch.linspace(0.5, 2.0, k))
+    bn.weight.data.copy_(torch.linspace(0.5, 1.5, k))
+    bn.bias.data.copy_(torch.linspace(-0.3, 0.3, k))
+    for prm in bn.parameters():
+        prm.requires_grad_(False)
+    x = x.contiguous(memory_format=torch.channels_last).requires_grad_(True)
+    y, xa = MF.conv_bn_relu_tee(x, conv, bn, with_relu)
+    assert xa.data_ptr() == x.data_ptr()  # the tee is an alias, not a copy
+    vq = oracle.round_to(rng.standard_normal((n, c, h, w)), "bf16")
+    v = torch.from_numpy(vq).to(DEV, torch.bfloat16).contiguous(memory_format=torch.channels_last)
+    g, gq = _q(rng.standard_normal(tuple(y.shape)), "bf16")
+    ((y.float() * g.float()).sum() + (xa.float() * v.float()).sum()).backward()
+    vq_ = v.double().cpu().numpy()
+    varq = bn.running_var.double().cpu().numpy()
+    sc = bn.weight.double().cpu().numpy() / np.sqrt(varq + 1e-5)
+    ym = y.detach().float().cpu().double().numpy()
+    if with_relu:
+        keep = ym > 0
+        gc = oracle.round_to(np.where(keep, gq, 0.0) *
+                             oracle.round_to(sc, "f32").reshape(1, -1, 1, 1), "bf16")
+        ref = oracle.conv2d_dx(gc, wq, s, 1, h, w)
+    else:
+        wsq = oracle.round_to(wq * oracle.round_to(sc, "f32").reshape(-1, 1, 1, 1), "bf16")
+        ref = oracle.conv2d_dx(gq, wsq, s, 1, h, w)
+    _close(x.grad, ref + vq_, "bf16", "tee dx", ulps=2.01)
+
+
 def test_add_relu():
     rng = np.random.default_rng(3)
     a, aq = _q(rng.standard_normal((2, 32, 9, 9)), "bf16")
