@@ -196,8 +196,7 @@ ConvShape shape_of(const ConvDims& c, int C, int H, int W, int cblocks, int wpit
 // ----------------------------------------------------------------- forward
 // optional epilogue fusion of a following eval-BatchNorm (+ ReLU with its mask)
 struct Fuse {
-  const float* scale = nullptr;
-  const float* shift = nullptr;
+  BnFold bn;
   int relu = 0;
   uint8_t* mask = nullptr;
   const void* resid = nullptr;
@@ -205,8 +204,7 @@ struct Fuse {
 
 void apply_fuse(EpiParams& e, const Fuse* f) {
   if (!f) return;
-  e.scale = f->scale;
-  e.shift = f->shift;
+  e.bn = f->bn;
   e.relu = f->relu;
   e.mask = f->mask;
   e.resid = f->resid;
@@ -226,8 +224,7 @@ ms_status fwd_rowseg(const ms_conv_desc* d, const ConvPlan& p, const void* x, co
       stem_fprop_ok(dt, d->layout, c.c, c.r, c.s, c.sh, c.sw, c.ph, c.pw, c.ow, c.k) &&
       stem_fprop_weight_bytes(c.k) <= p.ws_w)
     return stem_fprop(dt, c.n, c.h, p.xw_pad, c.oh, c.ow, c.k, c.c, d->wlayout, x4, w, wr, bias, y,
-                      st, f ? f->scale : nullptr, f ? f->shift : nullptr, f ? f->relu : 0,
-                      f ? f->mask : nullptr);
+                      st, f ? f->bn : BnFold{}, f ? f->relu : 0, f ? f->mask : nullptr);
   MS_TRY(repack_rowseg(dt, c.k, c.c, c.r, c.s, d->wlayout, w, wr, st));
   GemmArgs g = base_args(dt);
   g.M = c.n * c.oh * c.ow;
@@ -258,8 +255,7 @@ ms_status fwd_tc(const ms_conv_desc* d, const ConvPlan& p, const void* x, const 
   if (p.rowseg) return fwd_rowseg(d, p, x, w, bias, y, ws, st, f);
   if (p.halo3)
     return conv3x3_halo(d->dtype, (int)d->n, (int)d->h, (int)d->w, d->wlayout, 0, x, w, ws, y,
-                        f ? f->scale : nullptr, f ? f->shift : nullptr, bias,
-                        f ? f->resid : nullptr, f ? f->relu : 0, f ? f->mask : nullptr, nullptr,
+                        f ? f->bn : BnFold{}, bias, f ? f->resid : nullptr, f ? f->relu : 0, f ? f->mask : nullptr, nullptr,
                         nullptr, 0, 0.f, st);
   const ConvDims c = dims_of(d);
   const int dt = d->dtype;
@@ -350,7 +346,7 @@ ms_status dx_tc(const ms_conv_desc* d, const ConvPlan& p, const void* dy, const 
   if (p.band) return dx_band(d, p, dy, w, dx, ws, st);
   if (p.halo3 && !bias)  // the input-VJP is the same 3x3 conv of dY with W transposed + flipped
     return conv3x3_halo(d->dtype, (int)d->n, (int)d->h, (int)d->w, d->wlayout, 1, dy, w, ws, dx,
-                        nullptr, nullptr, nullptr, addend, 0, nullptr, ks ? ks->var : nullptr,
+                        BnFold{}, nullptr, addend, 0, nullptr, ks ? ks->var : nullptr,
                         ks ? ks->weight : nullptr, ks ? ks->pdt : 0, ks ? ks->eps : 0.f, st);
   if (p.stem) {
     MS_TRY(repack_scatter(dt, c.k, c.c, c.r, c.s, p.kpad, d->wlayout, w, ws, st));
@@ -598,24 +594,9 @@ extern "C" ms_status ms_conv_transpose2d_fwd(const ms_conv_desc* d, const void* 
 }
 
 // ----------------------------------------------------------------- conv + BN-eval (+ ReLU)
-namespace ms {
-namespace {
-__global__ void bn_scale_shift_kernel(int k, const void* mean, const void* var, const void* w,
-                                      const void* b, int pdt, float eps, float* scale,
-                                      float* shift) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= k) return;
-  const float mu = load_as_float(mean, pdt, c);
-  const float s = (w ? load_as_float(w, pdt, c) : 1.f) / sqrtf(load_as_float(var, pdt, c) + eps);
-  scale[c] = s;
-  shift[c] = (b ? load_as_float(b, pdt, c) : 0.f) - mu * s;
-}
-}  // namespace
-}  // namespace ms
-
 extern "C" size_t ms_conv2d_bn_workspace(const ms_conv_desc* d) {
   if (validate(d) != MS_OK) return 0;
-  return plan(d, MS_CONV_FWD).ws + align256(2 * sizeof(float) * (size_t)d->k);
+  return plan(d, MS_CONV_FWD).ws;
 }
 
 extern "C" ms_status ms_conv2d_bn_fwd(const ms_conv_desc* d, const void* x, const void* w,
@@ -633,18 +614,16 @@ extern "C" ms_status ms_conv2d_bn_fwd(const ms_conv_desc* d, const void* x, cons
   ConvPlan p = plan(d, MS_CONV_FWD);
   MS_CHECK_ARG(p.tc && d->k % 8 == 0, MS_ERR_UNSUPPORTED,
                "conv+bn fusion needs the tcgen05 path (16-bit NHWC) and K %% 8 == 0");
-  MS_CHECK_ARG(ws && ws_bytes >= ms_conv2d_bn_workspace(d), MS_ERR_WORKSPACE,
-               "conv+bn: workspace %zu < %zu", ws_bytes, ms_conv2d_bn_workspace(d));
+  MS_CHECK_ARG(ws_bytes >= p.ws && (p.ws == 0 || ws), MS_ERR_WORKSPACE,
+               "conv+bn: workspace %zu < %zu", ws_bytes, p.ws);
   Fuse f;
-  if (bn_mean) {
-    float* scale = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + p.ws);
-    float* shift = scale + d->k;
-    bn_scale_shift_kernel<<<(unsigned)((d->k + 127) / 128), 128, 0, st>>>(
-        (int)d->k, bn_mean, bn_var, bn_weight, bn_bias, bn_pdtype, (float)eps, scale, shift);
-    count_launch(1, KF_BN);
-    MS_TRY(launch_status("bn_scale_shift"));
-    f.scale = scale;
-    f.shift = shift;
+  if (bn_mean) {  // folded per channel inside the conv epilogue (BnFold)
+    f.bn.mean = bn_mean;
+    f.bn.var = bn_var;
+    f.bn.w = bn_weight;
+    f.bn.b = bn_bias;
+    f.bn.pdt = bn_pdtype;
+    f.bn.eps = (float)eps;
   }
   f.relu = relu;
   f.mask = static_cast<uint8_t*>(mask_or_null);

@@ -39,8 +39,7 @@ struct H3Args {
   int units;
   int dt;
   void* y;
-  const float* scale;  // fused eval-BN (nullable)
-  const float* shift;
+  BnFold bn;           // fused eval-BN (bn.var nullable)
   const void* bias;    // conv bias (nullable)
   const void* resid;   // residual, shaped like y (nullable)
   int relu;
@@ -168,6 +167,11 @@ __global__ void __launch_bounds__(H3_THREADS, 1)
     const int j = j0 + rw;
     int local = 0;
     uint32_t nst = 0;
+    float bs0 = 1.f, bt0 = 0.f, bs1 = 1.f, bt1 = 0.f;  // eval-BN affine of channels lane, 32 + lane
+    if (a.bn.var) {
+      bn_fold(a.bn, rw, bs0, bt0);
+      bn_fold(a.bn, 32 + rw, bs1, bt1);
+    }
     for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++local) {
       const int n = u / a.tiles_per_img;
       const int oh = (u - n * a.tiles_per_img) * H3_ROWS + ti;
@@ -196,16 +200,11 @@ __global__ void __launch_bounds__(H3_THREADS, 1)
 #pragma unroll
           for (int q = 0; q < 32; ++q) f[q] += IO<T>::ld(static_cast<const T*>(a.bias) + c0 + q);
         }
-        if (a.scale) {
+        if (a.bn.var) {  // lane j holds channel c0 + j's folded BN affine
+          const float s_l = cc == 0 ? bs0 : bs1, t_l = cc == 0 ? bt0 : bt1;
 #pragma unroll
-          for (int q = 0; q < 32; q += 4) {
-            const float4 s4 = __ldg(reinterpret_cast<const float4*>(a.scale + c0 + q));
-            const float4 t4 = __ldg(reinterpret_cast<const float4*>(a.shift + c0 + q));
-            f[q] = f[q] * s4.x + t4.x;
-            f[q + 1] = f[q + 1] * s4.y + t4.y;
-            f[q + 2] = f[q + 2] * s4.z + t4.z;
-            f[q + 3] = f[q + 3] * s4.w + t4.w;
-          }
+          for (int q = 0; q < 32; ++q)
+            f[q] = f[q] * __shfl_sync(0xffffffffu, s_l, q) + __shfl_sync(0xffffffffu, t_l, q);
         }
         if (a.resid && valid) {
           const uint4* r4 = reinterpret_cast<const uint4*>(static_cast<const T*>(a.resid) +
@@ -301,8 +300,7 @@ size_t conv3x3_halo_workspace() { return align256((size_t)9 * H3_N * H3_C * 2); 
 // x [N][H][W][64] -> y [N][H][W][64] (NHWC); transpose = 1: the input-VJP (x = dY,
 // y = dX, weights transposed and flipped, optional folded BN scale in ks_*)
 ms_status conv3x3_halo(int dt, int n, int h, int w, int wlayout, int transpose, const void* x,
-                       const void* wt, void* ws, void* y, const float* scale, const float* shift,
-                       const void* bias, const void* resid, int relu, uint8_t* mask,
+                       const void* wt, void* ws, void* y, const BnFold& bn, const void* bias, const void* resid, int relu, uint8_t* mask,
                        const void* ks_var, const void* ks_w, int ks_pdt, float ks_eps,
                        cudaStream_t st) {
   const int total = 9 * H3_N * H3_C;
@@ -334,7 +332,7 @@ ms_status conv3x3_halo(int dt, int n, int h, int w, int wlayout, int transpose, 
   a.N = n; a.H = h; a.W = w;
   a.tiles_per_img = (h + H3_ROWS - 1) / H3_ROWS;
   a.units = n * a.tiles_per_img;
-  a.dt = dt; a.y = y; a.scale = scale; a.shift = shift; a.bias = bias; a.resid = resid;
+  a.dt = dt; a.y = y; a.bn = bn; a.bias = bias; a.resid = resid;
   a.relu = relu; a.mask = mask;
   const int grid = a.units < num_sms() ? a.units : num_sms();
   if (dt == MS_BF16) {

@@ -154,29 +154,33 @@ __global__ void repack_fprop_kernel(int K, int C, int R, int S, int cpad, int wl
 // Input-VJP weight [c][tap][kpad] from OIHW/OHWI (B operand of the dgrad GEMM).
 // kvar (nullable): multiply output-channel k by kw[k] / sqrt(kvar[k] + eps) -- a
 // following eval-BatchNorm's scale folded into the input-VJP weight
+// As a 32 x 32 tile transpose through shared memory: reads run along c
+// (contiguous in OHWI), writes along k; one tap per blockIdx.z.
 template <typename T>
-__global__ void repack_dgrad_kernel(int K, int C, int R, int S, int kpad, int wlayout,
-                                    const T* __restrict__ w, T* __restrict__ out,
-                                    const void* kvar, const void* kw, int pdt, float eps) {
-  const int64_t total = (int64_t)C * R * S * kpad;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t t = i;
-    const int k = t % kpad; t /= kpad;
-    const int tap = t % (R * S); t /= (R * S);
-    const int c = (int)t;
-    const int r = tap / S, s = tap % S;
-    T v = IO<T>::cvt(0.f);
-    if (k < K) {
-      v = wlayout == MS_NHWC ? w[(((int64_t)k * R + r) * S + s) * C + c]
-                             : w[(((int64_t)k * C + c) * R + r) * S + s];
-      if (kvar) {
-        const float sc = (kw ? load_as_float(kw, pdt, k) : 1.f) /
-                         sqrtf(load_as_float(kvar, pdt, k) + eps);
-        v = IO<T>::cvt(IO<T>::ld(&v) * sc);
-      }
+__global__ void repack_dgrad_tiled_kernel(int K, int C, int RS, int kpad, int wlayout,
+                                          const T* __restrict__ w, T* __restrict__ out,
+                                          const void* kvar, const void* kw, int pdt, float eps) {
+  __shared__ float tile[32][33];
+  const int k0 = blockIdx.x * 32, c0 = blockIdx.y * 32, tap = blockIdx.z;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int k = k0 + ty + 8 * i, c = c0 + tx;
+    float v = 0.f;
+    if (k < K && c < C) {
+      v = IO<T>::ld(w + (wlayout == MS_NHWC ? ((int64_t)k * RS + tap) * C + c
+                                            : ((int64_t)k * C + c) * RS + tap));
+      if (kvar)
+        v *= (kw ? load_as_float(kw, pdt, k) : 1.f) / sqrtf(load_as_float(kvar, pdt, k) + eps);
     }
-    out[i] = v;
+    tile[ty + 8 * i][tx] = v;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int c = c0 + ty + 8 * i, k = k0 + tx;
+    if (c < C && k < kpad)
+      out[((int64_t)c * RS + tap) * kpad + k] = IO<T>::cvt(tile[tx][ty + 8 * i]);
   }
 }
 
@@ -291,11 +295,11 @@ ms_status repack_fprop(int dt, int K, int C, int R, int S, int cpad, int wlayout
 ms_status repack_dgrad(int dt, int K, int C, int R, int S, int kpad, int wlayout, const void* w,
                        void* out, cudaStream_t st, const void* kvar, const void* kw, int pdt,
                        float eps) {
-  const int64_t total = (int64_t)C * R * S * kpad;
-  MS_DT_DISPATCH(dt, repack_dgrad_kernel<T><<<grid_1d(total), 256, 0, st>>>(
-                         K, C, R, S, kpad, wlayout, (const T*)w, (T*)out, kvar, kw, pdt, eps));
+  const dim3 grid((unsigned)((kpad + 31) / 32), (unsigned)((C + 31) / 32), (unsigned)(R * S));
+  MS_DT_DISPATCH(dt, repack_dgrad_tiled_kernel<T><<<grid, dim3(32, 8), 0, st>>>(
+                         K, C, R * S, kpad, wlayout, (const T*)w, (T*)out, kvar, kw, pdt, eps));
   count_launch();
-  return launch_status("repack_dgrad_kernel");
+  return launch_status("repack_dgrad_tiled_kernel");
 }
 
 ms_status repack_scatter(int dt, int K, int C, int R, int S, int kpad, int wlayout, const void* w,

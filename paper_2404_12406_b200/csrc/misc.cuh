@@ -33,8 +33,8 @@ bool stem_fprop_ok(int dt, int layout, int c, int r, int s, int sh, int sw, int 
 size_t stem_fprop_weight_bytes(int k);
 ms_status stem_fprop(int dt, int n, int h, int wp, int p, int q, int k, int c, int wlayout,
                      const void* xp, const void* w, void* wb, const void* bias, void* y,
-                     cudaStream_t st, const float* scale = nullptr, const float* shift = nullptr,
-                     int relu = 0, uint8_t* mask = nullptr);
+                     cudaStream_t st, const BnFold& bn = BnFold{}, int relu = 0,
+                     uint8_t* mask = nullptr);
 
 // 3x3/1/1 64->64-channel convolution, halo-tiled (conv3x3.cu); transpose = 1 is
 // the input-VJP of the same conv (x = dY, y = dX)
@@ -42,8 +42,7 @@ bool conv3x3_halo_ok(int dt, int layout, int c, int k, int r, int s, int sh, int
                      int pw, int w);
 size_t conv3x3_halo_workspace();
 ms_status conv3x3_halo(int dt, int n, int h, int w, int wlayout, int transpose, const void* x,
-                       const void* wt, void* ws, void* y, const float* scale, const float* shift,
-                       const void* bias, const void* resid, int relu, uint8_t* mask,
+                       const void* wt, void* ws, void* y, const BnFold& bn, const void* bias, const void* resid, int relu, uint8_t* mask,
                        const void* ks_var, const void* ks_w, int ks_pdt, float ks_eps,
                        cudaStream_t st);
 

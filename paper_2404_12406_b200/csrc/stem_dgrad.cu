@@ -311,8 +311,7 @@ struct StemFpropArgs {
   int dt;
   const void* xp;  // padded input
   const void* wb;  // weights in core-matrix layout [r][kg 4][K][8]
-  const float* scale;  // fused eval-BN (nullable): y = conv * scale[k] + shift[k]
-  const float* shift;
+  BnFold bn;           // fused eval-BN (bn.var nullable): y = conv * s[k] + t[k]
   int relu;            // fused ReLU; keep bits to mask (1 bit per element, NHWC order)
   uint8_t* mask;
 };
@@ -354,11 +353,8 @@ __global__ void __launch_bounds__(SF_THREADS, 1)
   const uint32_t lane = lane_id();
   for (int i = threadIdx.x; i < SF_SLOT / 4; i += blockDim.x)
     reinterpret_cast<uint32_t*>(zero_row)[i] = 0u;
-  if (a.scale)
-    for (int i = threadIdx.x; i < a.K; i += blockDim.x) {
-      s_aff[i] = a.scale[i];
-      s_aff[a.K + i] = a.shift[i];
-    }
+  if (a.bn.var)
+    for (int i = threadIdx.x; i < a.K; i += blockDim.x) bn_fold(a.bn, i, s_aff[i], s_aff[a.K + i]);
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < SF_STAGES; ++i) {
       mbar_init(smem_u32(&full_bar[i]), 1);
@@ -491,7 +487,7 @@ __global__ void __launch_bounds__(SF_THREADS, 1)
             const int ch = q * 8 + j;
             f[j] = __uint_as_float(ch < 32 ? v0[ch] : v1[ch - 32]);
             if (a.bias) f[j] += IO<T>::ld(static_cast<const T*>(a.bias) + c0 + ch);
-            if (a.scale) f[j] = f[j] * s_aff[c0 + ch] + s_aff[a.K + c0 + ch];
+            if (a.bn.var) f[j] = f[j] * s_aff[c0 + ch] + s_aff[a.K + c0 + ch];
             if (a.relu) {
               const bool pos = !(f[j] <= 0.f);
               keep |= (pos ? 1ull : 0ull) << ch;
@@ -555,8 +551,7 @@ size_t stem_fprop_weight_bytes(int k) { return (size_t)SF_R * 4 * k * 16; }
 // xp: pad_rowseg output [n][h][wp][4]; wb: workspace of stem_fprop_weight_bytes(k)
 ms_status stem_fprop(int dt, int n, int h, int wp, int p, int q, int k, int c, int wlayout,
                      const void* xp, const void* w, void* wb, const void* bias, void* y,
-                     cudaStream_t st, const float* scale, const float* shift, int relu,
-                     uint8_t* mask) {
+                     cudaStream_t st, const BnFold& bn, int relu, uint8_t* mask) {
   const int total = SF_R * 4 * k * 8;
   const int blocks = (total + 255) / 256;
   if (dt == MS_BF16)
@@ -571,7 +566,7 @@ ms_status stem_fprop(int dt, int n, int h, int wp, int p, int q, int k, int c, i
   a.N = n; a.H = h; a.Wp = wp; a.P = p; a.Q = q; a.K = k;
   a.units = n * p;
   a.y = y; a.bias = bias; a.dt = dt; a.xp = xp; a.wb = wb;
-  a.scale = scale; a.shift = shift; a.relu = relu; a.mask = mask;
+  a.bn = bn; a.relu = relu; a.mask = mask;
   const int smem =
       SF_STG + (int)stem_fprop_weight_bytes(k) + SF_SLOT + SF_STAGES * SF_STAGE + SF_AFF + 1024 +
       256;

@@ -83,11 +83,10 @@ struct EpiParams {
   int atomic;        // 1: fp32 red.add into out (split-K / wgrad workspace)
   const void* bias;  // per-column bias (nullable)
   int bias_dtype;
-  // fused eval-BatchNorm + ReLU (conv forward): v = v * scale[col] + shift[col],
-  // then v = max(v, 0) with the keep bit of every element written to mask
-  // (1 bit per element in storage order, as ms_relu_fwd)
-  const float* scale;  // nullable
-  const float* shift;
+  // fused eval-BatchNorm + ReLU (conv forward): v = v * s[col] + t[col] (bn.var
+  // != nullptr), then v = max(v, 0) with the keep bit of every element written to
+  // mask (1 bit per element in storage order, as ms_relu_fwd)
+  BnFold bn;
   int relu;
   uint8_t* mask;       // nullable
   const void* resid;   // nullable: residual added after the affine, before the ReLU
@@ -652,6 +651,10 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
         for (int ci = 0; ci < WCOLS / 32; ++ci) {
           const int c = c_lo + ci * 32;
           uint32_t r[32];
+          // eval-BN affine: lane j folds column n0 + c + j (loads overlap the TMEM read)
+          float bs = 1.f, bt = 0.f;
+          if (e.bn.var != nullptr && n0 + c + static_cast<int>(lane) < ncols)
+            bn_fold(e.bn, n0 + c + static_cast<int>(lane), bs, bt);
           __syncwarp();  // tcgen05.ld / wait are warp-collective: reconverge invalid rows
           if (!zero) {
             tmem_ld_32x32b_x32(taddr + c, r);
@@ -693,23 +696,10 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
             for (int j = 0; j < 32; ++j)
               if (nc + j < ncols) v[j] += load_as_float(e.bias, e.bias_dtype, nc + j);
           }
-          if (e.scale != nullptr) {  // folded eval-BN: per-column affine in fp32
+          if (e.bn.var != nullptr) {  // folded eval-BN: per-column affine in fp32
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              if (full) {
-                const float4 s4 = __ldg(reinterpret_cast<const float4*>(e.scale + nc) + q);
-                const float4 t4 = __ldg(reinterpret_cast<const float4*>(e.shift + nc) + q);
-                v[4 * q] = v[4 * q] * s4.x + t4.x;
-                v[4 * q + 1] = v[4 * q + 1] * s4.y + t4.y;
-                v[4 * q + 2] = v[4 * q + 2] * s4.z + t4.z;
-                v[4 * q + 3] = v[4 * q + 3] * s4.w + t4.w;
-              } else {
-#pragma unroll
-                for (int h = 0; h < 4; ++h)
-                  if (nc + 4 * q + h < ncols)
-                    v[4 * q + h] = v[4 * q + h] * e.scale[nc + 4 * q + h] + e.shift[nc + 4 * q + h];
-              }
-            }
+            for (int j = 0; j < 32; ++j)
+              v[j] = v[j] * __shfl_sync(0xffffffffu, bs, j) + __shfl_sync(0xffffffffu, bt, j);
           }
           if (e.resid != nullptr && valid) {  // fused residual join of a ResNet block
             const int64_t el = orow * e.ldc + col_base + c;
