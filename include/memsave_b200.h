@@ -161,18 +161,26 @@ MS_API ms_status ms_conv2d_bn_fwd(const ms_conv_desc* d, const void* x, const vo
 /* residual_or_null: a tensor shaped like y added after the BN affine and before
  * the ReLU (the conv -> BN -> add -> ReLU join of a ResNet block).  bn_mean =
  * bn_var = NULL: no BN, i.e. conv [+ bias] -> ReLU (VGG).                   */
-/* dX of the conv when a following eval-BN (no ReLU) scales its output: the scale
- * w/sqrt(var+eps) is folded into the repacked dgrad weight, so dY is used as
- * is (no pass over the gradient); bn_var = NULL: no scale.  addend_or_null: a
- * tensor shaped like dx added in the epilogue (dx = dgrad + addend), i.e. the
- * gradient x receives from its other consumer (the identity / downsample
- * branch of a ResNet block), summed here instead of by a separate pass.
+/* dX of a conv inside a fused chain, everything in the dgrad epilogue:
+ *   dx = [keep ? (dgrad(dy, W * s) + addend) : 0] * s_in
+ * s = w/sqrt(var+eps) of a following eval-BN without ReLU (bn_var = NULL: 1),
+ * folded into the repacked dgrad weight so dY is used as is;
+ * addend_or_null: shaped like dx, the gradient x receives from its other
+ * consumer (identity / downsample branch of a ResNet block);
+ * keep_or_null: the bit mask of the ReLU that produced x (1 bit per element,
+ * storage order, 4-byte aligned) -- that ReLU's backward;
+ * s_in = in_weight/sqrt(in_var+in_eps) of the eval-BN before that ReLU
+ * (in_var = NULL: 1).  The three replace separate passes over dx (the
+ * engine's gradient sum, ms_relu_bwd / ms_bn_relu_bwd).
  * Workspace: ms_conv2d_workspace(d, MS_CONV_DX).  MS_ERR_UNSUPPORTED outside
  * the tcgen05 dgrad (16-bit NHWC, phase GEMM or 3x3 halo kernel).           */
 MS_API ms_status ms_conv2d_bn_dx(const ms_conv_desc* d, const void* dy, const void* w,
                                  const void* bn_var_or_null, const void* bn_weight_or_null,
                                  int32_t bn_pdtype, double eps, const void* addend_or_null,
-                                 void* dx, void* ws, size_t ws_bytes, void* stream);
+                                 const void* keep_or_null, const void* in_var_or_null,
+                                 const void* in_weight_or_null, int32_t in_pdtype,
+                                 double in_eps, void* dx, void* ws, size_t ws_bytes,
+                                 void* stream);
 /* dx = g * keep * w/sqrt(var+eps) per channel (NHWC, C % 8 == 0, 16-bit);
  * mask_or_null = NULL for a conv -> BN chain without ReLU.                  */
 MS_API ms_status ms_bn_relu_bwd(int64_t numel, int64_t c, int32_t dtype, int32_t pdtype,

@@ -336,18 +336,30 @@ struct KScale {  // an eval-BN scale w/sqrt(var+eps) folded into the dgrad weigh
   float eps = 0.f;
 };
 
+// epilogue work of an input-VJP: dx = keep ? (dgrad + addend) : 0, times the
+// producer BN's scale when in_bn.var is set
+struct DxFuse {
+  const void* addend = nullptr;
+  const uint8_t* keep = nullptr;
+  BnFold in_bn;
+  bool any() const { return addend || keep || in_bn.var; }
+};
+
 ms_status dx_tc(const ms_conv_desc* d, const ConvPlan& p, const void* dy, const void* w, void* dx,
                 void* ws, cudaStream_t st, const void* bias = nullptr,
-                const KScale* ks = nullptr, const void* addend = nullptr) {
+                const KScale* ks = nullptr, const DxFuse* xf = nullptr) {
   const ConvDims c = dims_of(d);
   const int dt = d->dtype;
-  MS_CHECK_ARG(!addend || (!p.band && !p.stem), MS_ERR_UNSUPPORTED,
-               "conv dx: no fused addend in the stem / band kernels");
+  MS_CHECK_ARG(!xf || !xf->any() || (!p.band && !p.stem), MS_ERR_UNSUPPORTED,
+               "conv dx: no fused epilogue in the stem / band kernels");
+  const DxFuse none;
+  if (!xf) xf = &none;
   if (p.band) return dx_band(d, p, dy, w, dx, ws, st);
   if (p.halo3 && !bias)  // the input-VJP is the same 3x3 conv of dY with W transposed + flipped
     return conv3x3_halo(d->dtype, (int)d->n, (int)d->h, (int)d->w, d->wlayout, 1, dy, w, ws, dx,
-                        BnFold{}, nullptr, addend, 0, nullptr, ks ? ks->var : nullptr,
-                        ks ? ks->weight : nullptr, ks ? ks->pdt : 0, ks ? ks->eps : 0.f, st);
+                        xf->in_bn, nullptr, xf->addend, 0, nullptr, ks ? ks->var : nullptr,
+                        ks ? ks->weight : nullptr, ks ? ks->pdt : 0, ks ? ks->eps : 0.f, st,
+                        xf->keep, xf->in_bn.var != nullptr);
   if (p.stem) {
     MS_TRY(repack_scatter(dt, c.k, c.c, c.r, c.s, p.kpad, d->wlayout, w, ws, st));
     return stem_dgrad(dt, c.n, c.h, c.w, c.oh, c.ow, c.k, dy, ws, dx, st);
@@ -403,7 +415,10 @@ ms_status dx_tc(const ms_conv_desc* d, const ConvPlan& p, const void* dy, const 
   g.nphases = np;
   g.num_tiles = tiles;
   g.epi = EpiParams{dx, c.c, dt, 0, bias, dt};  // bias: conv_transpose2d forward
-  g.epi.resid = addend;                          // dx = dgrad + addend (tee'd input)
+  g.epi.resid = xf->addend;                      // dx = dgrad + addend (tee'd input)
+  g.epi.keep_in = xf->keep;
+  g.epi.bn = xf->in_bn;
+  g.epi.bn_post = xf->in_bn.var != nullptr;
   const int64_t wrow = (int64_t)c.r * c.s * p.kpad;
   MS_TRY(make_tmap_2d(&tm.b, dt, wd, wrow, c.c, wrow, BK, bn / tp.cl));
   return launch_umma(bn, 0, 0, LOAD_CONV_DGRAD, tm, g, st, tp.cl);
@@ -635,8 +650,10 @@ extern "C" ms_status ms_conv2d_bn_fwd(const ms_conv_desc* d, const void* x, cons
 
 extern "C" ms_status ms_conv2d_bn_dx(const ms_conv_desc* d, const void* dy, const void* w,
                                      const void* bn_var, const void* bn_weight, int32_t bn_pdtype,
-                                     double eps, const void* addend, void* dx, void* ws,
-                                     size_t ws_bytes, void* stream) {
+                                     double eps, const void* addend, const void* keep,
+                                     const void* in_var, const void* in_weight, int32_t in_pdtype,
+                                     double in_eps, void* dx, void* ws, size_t ws_bytes,
+                                     void* stream) {
   MS_TRY(validate(d));
   MS_TRY(bind_device(dx));
   if (d->n == 0) return MS_OK;
@@ -647,11 +664,19 @@ extern "C" ms_status ms_conv2d_bn_dx(const ms_conv_desc* d, const void* dy, cons
                "conv+bn dx: workspace %zu < %zu", ws_bytes, p.ws);
   MS_CHECK_ARG(!addend || (reinterpret_cast<uintptr_t>(addend) & 15) == 0, MS_ERR_ALIGN,
                "conv+bn dx: addend must be 16-byte aligned");
+  MS_CHECK_ARG(!keep || (reinterpret_cast<uintptr_t>(keep) & 3) == 0, MS_ERR_ALIGN,
+               "conv+bn dx: keep mask must be 4-byte aligned");
+  DxFuse xf;
+  xf.addend = addend;
+  xf.keep = static_cast<const uint8_t*>(keep);
+  xf.in_bn.var = in_var;
+  xf.in_bn.w = in_weight;
+  xf.in_bn.pdt = in_pdtype;
+  xf.in_bn.eps = (float)in_eps;
   KScale ks;
   ks.var = bn_var;
   ks.weight = bn_weight;
   ks.pdt = bn_pdtype;
   ks.eps = (float)eps;
-  return dx_tc(d, p, dy, w, dx, ws, (cudaStream_t)stream, nullptr, bn_var ? &ks : nullptr,
-               addend);
+  return dx_tc(d, p, dy, w, dx, ws, (cudaStream_t)stream, nullptr, bn_var ? &ks : nullptr, &xf);
 }

@@ -44,6 +44,8 @@ struct H3Args {
   const void* resid;   // residual, shaped like y (nullable)
   int relu;
   uint8_t* mask;
+  const uint8_t* keep_in;  // dgrad: the producer ReLU's mask, applied after resid
+  int bn_post;             // dgrad: then scale by the producer BN's s (bn)
 };
 
 // SW128 K-major descriptor whose start may sit at any 128-byte row of a
@@ -200,7 +202,7 @@ __global__ void __launch_bounds__(H3_THREADS, 1)
 #pragma unroll
           for (int q = 0; q < 32; ++q) f[q] += IO<T>::ld(static_cast<const T*>(a.bias) + c0 + q);
         }
-        if (a.bn.var) {  // lane j holds channel c0 + j's folded BN affine
+        if (a.bn.var && !a.bn_post) {  // lane j holds channel c0 + j's folded BN affine
           const float s_l = cc == 0 ? bs0 : bs1, t_l = cc == 0 ? bt0 : bt1;
 #pragma unroll
           for (int q = 0; q < 32; ++q)
@@ -216,6 +218,18 @@ __global__ void __launch_bounds__(H3_THREADS, 1)
 #pragma unroll
             for (int h = 0; h < 8; ++h) f[q * 8 + h] += IO<T>::ld(e + h);
           }
+        }
+        if (a.keep_in) {
+          const uint32_t kb =
+              valid ? __ldg(reinterpret_cast<const uint32_t*>(a.keep_in) + ((pix * H3_N + c0) >> 5))
+                    : 0u;
+#pragma unroll
+          for (int q = 0; q < 32; ++q) f[q] = ((kb >> q) & 1u) ? f[q] : 0.f;
+        }
+        if (a.bn_post) {
+          const float s_l = cc == 0 ? bs0 : bs1;
+#pragma unroll
+          for (int q = 0; q < 32; ++q) f[q] *= __shfl_sync(0xffffffffu, s_l, q);
         }
         if (a.relu) {
           uint32_t bits = 0;
@@ -302,7 +316,7 @@ size_t conv3x3_halo_workspace() { return align256((size_t)9 * H3_N * H3_C * 2); 
 ms_status conv3x3_halo(int dt, int n, int h, int w, int wlayout, int transpose, const void* x,
                        const void* wt, void* ws, void* y, const BnFold& bn, const void* bias, const void* resid, int relu, uint8_t* mask,
                        const void* ks_var, const void* ks_w, int ks_pdt, float ks_eps,
-                       cudaStream_t st) {
+                       cudaStream_t st, const uint8_t* keep_in, int bn_post) {
   const int total = 9 * H3_N * H3_C;
   if (dt == MS_BF16)
     repack_h3_kernel<__nv_bfloat16><<<(total + 255) / 256, 256, 0, st>>>(
@@ -333,7 +347,7 @@ ms_status conv3x3_halo(int dt, int n, int h, int w, int wlayout, int transpose, 
   a.tiles_per_img = (h + H3_ROWS - 1) / H3_ROWS;
   a.units = n * a.tiles_per_img;
   a.dt = dt; a.y = y; a.bn = bn; a.bias = bias; a.resid = resid;
-  a.relu = relu; a.mask = mask;
+  a.relu = relu; a.mask = mask; a.keep_in = keep_in; a.bn_post = bn_post;
   const int grid = a.units < num_sms() ? a.units : num_sms();
   if (dt == MS_BF16) {
     auto kern = conv3x3_halo_kernel<__nv_bfloat16>;

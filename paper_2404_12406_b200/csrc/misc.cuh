@@ -44,7 +44,7 @@ size_t conv3x3_halo_workspace();
 ms_status conv3x3_halo(int dt, int n, int h, int w, int wlayout, int transpose, const void* x,
                        const void* wt, void* ws, void* y, const BnFold& bn, const void* bias, const void* resid, int relu, uint8_t* mask,
                        const void* ks_var, const void* ks_w, int ks_pdt, float ks_eps,
-                       cudaStream_t st);
+                       cudaStream_t st, const uint8_t* keep_in = nullptr, int bn_post = 0);
 
 inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 inline size_t align256(size_t v) { return (v + 255) & ~static_cast<size_t>(255); }

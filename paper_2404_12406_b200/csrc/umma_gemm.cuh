@@ -91,6 +91,11 @@ struct EpiParams {
   uint8_t* mask;       // nullable
   const void* resid;   // nullable: residual added after the affine, before the ReLU
                        // (same dtype / pitch as out)
+  // input-VJP of a conv whose input came out of a ReLU [after an eval-BN]: after
+  // the addend (resid), v = keep ? v : 0 with keep_in the producer's bit mask
+  // (storage order), then v *= s[col] when bn_post (bn = the producer's BN)
+  const uint8_t* keep_in;
+  int bn_post;
 };
 
 struct GemmArgs {
@@ -696,7 +701,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
             for (int j = 0; j < 32; ++j)
               if (nc + j < ncols) v[j] += load_as_float(e.bias, e.bias_dtype, nc + j);
           }
-          if (e.bn.var != nullptr) {  // folded eval-BN: per-column affine in fp32
+          if (e.bn.var != nullptr && !e.bn_post) {  // folded eval-BN: per-column affine
 #pragma unroll
             for (int j = 0; j < 32; ++j)
               v[j] = v[j] * __shfl_sync(0xffffffffu, bs, j) + __shfl_sync(0xffffffffu, bt, j);
@@ -727,6 +732,24 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
               for (int j = 0; j < 32; ++j)
                 if (nc + j < ncols) v[j] += load_as_float(e.resid, e.out_dtype, el + j);
             }
+          }
+          if (e.keep_in != nullptr) {  // the producer ReLU's backward
+            uint32_t kb = 0;
+            if (valid) {
+              const int64_t el = orow * e.ldc + col_base + c;
+              if (full && (el & 31) == 0) {
+                kb = __ldg(reinterpret_cast<const uint32_t*>(e.keep_in) + (el >> 5));
+              } else {
+                for (int j = 0; j < 32 && nc + j < ncols; ++j)
+                  kb |= ((e.keep_in[(el + j) >> 3] >> ((el + j) & 7)) & 1u) << j;
+              }
+            }
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = ((kb >> j) & 1u) ? v[j] : 0.f;
+          }
+          if (e.bn_post) {  // the producer BN's scale (all lanes: warp-uniform)
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] *= __shfl_sync(0xffffffffu, bs, j);
           }
           if (e.relu) {
             uint32_t bits = 0;

@@ -799,11 +799,19 @@ class _ConvBNFn(torch.autograd.Function):
     gradient is never rescaled."""
 
     @staticmethod
-    def forward(ctx, x, weight, bias, residual, stride, padding, bn, relu: bool, tee=False):
+    def forward(ctx, x, weight, bias, residual, stride, padding, bn, relu: bool, tee=False,
+                in_mask=None, in_bn=None):
         # tee: also return x itself, for x's other consumer; backward then adds that
-        # consumer's gradient in the dgrad epilogue instead of the engine summing it
+        # consumer's gradient in the dgrad epilogue instead of the engine summing it.
+        # in_mask / in_bn: x came out of a fused ReLU [after eval-BN in_bn] whose
+        # backward (keep mask [and BN scale]) runs in this node's dgrad epilogue.
         x_rg, w_rg, b_rg = ctx.needs_input_grad[0], ctx.needs_input_grad[1], ctx.needs_input_grad[2]
         ctx.tee = bool(tee)
+        if in_mask is None:
+            in_bn = None
+        ctx.in_bn = None if in_bn is None else (in_bn.running_mean, in_bn.running_var,
+                                                in_bn.weight, float(in_bn.eps))
+        keep = in_mask if x_rg else None  # the ReLU mask rule (rules.py:98-101), kept here
         out_rg = x_rg or w_rg or b_rg or ctx.needs_input_grad[3]
         ctx.set_materialize_grads(False)  # the mask output never gets a gradient: no zero fill
         # the incoming gradient is already masked and scaled (_MaskScaleFn) only for
@@ -822,7 +830,8 @@ class _ConvBNFn(torch.autograd.Function):
         if _is_meta(x, weight):
             mask = (torch.empty((n_el + 7) // 8, dtype=torch.uint8, device="meta")
                     if relu and out_rg else None)
-            ctx.save_for_backward(x if "x" in roles else None, weight if "w" in roles else None)
+            ctx.save_for_backward(x if "x" in roles else None, weight if "w" in roles else None,
+                                  keep)
             ctx.layouts = (_lib.MS_NCHW, _lib.MS_NCHW)
             if mask is not None:
                 ctx.mark_non_differentiable(mask)
@@ -848,16 +857,19 @@ class _ConvBNFn(torch.autograd.Function):
                                       _dtype_code(mean) if mean is not None else dt, eps,
                                       _ptr(res), int(relu), _ptr(y), _ptr(mask), _ptr(ws), nb,
                                       _stream(x.device)), "ms_conv2d_bn_fwd")
-        ctx.save_for_backward(xl if "x" in roles else None, wl if "w" in roles else None)
+        ctx.save_for_backward(xl if "x" in roles else None, wl if "w" in roles else None, keep)
         if mask is not None:
             ctx.mark_non_differentiable(mask)
         return (y, mask, x) if tee else (y, mask)
 
     @staticmethod
     def backward(ctx, gy, _gmask=None, g_tee=None):
-        x, w = ctx.saved_tensors
+        x, w, keep = ctx.saved_tensors
+        nones = (None,) * 10
         if gy is None:  # grads are not materialised (set_materialize_grads(False))
-            return g_tee, None, None, None, None, None, None, None, None
+            if g_tee is None or not ctx.needs_input_grad[0]:
+                return (None,) + nones
+            return (_mask_scale(g_tee, keep, ctx.in_bn) if keep is not None else g_tee,) + nones
         need_x, need_w, need_b = ctx.needs_input_grad[:3]
         x_shape, w_shape, stride, padding = ctx.geom
         dx = dw = db = None
@@ -889,7 +901,7 @@ class _ConvBNFn(torch.autograd.Function):
                 dw = gc.new_empty(w_shape)
             if need_b:
                 db = gc.new_empty((w_shape[0],))
-            return dx, dw, db, d_res, None, None, None, None, None
+            return (dx, dw, db, d_res) + (None,) * 7
         L = _lib.lib()
         st = _stream(g.device)
         dt = _dtype_code(g)
@@ -899,12 +911,17 @@ class _ConvBNFn(torch.autograd.Function):
             dx = _empty4(x_shape, g, layout)
             wsp, nb = _workspace(L.ms_conv2d_workspace(ctypes.byref(d), _lib.MS_CONV_DX), g.device)
             folded = False
-            if sc_w or addend is not None:
-                # BN scale folded into the repacked dgrad weight (no pass over g) and/or
-                # the tee'd consumer's gradient added in the epilogue
+            ib = ctx.in_bn
+            if sc_w or addend is not None or keep is not None:
+                # BN scale folded into the repacked dgrad weight (no pass over g), the
+                # tee'd consumer's gradient and the producer ReLU [+BN]'s backward in
+                # the epilogue
                 st_ = L.ms_conv2d_bn_dx(ctypes.byref(d), _ptr(g), _ptr(w),
                                         _ptr(var) if sc_w else None, _ptr(bw) if sc_w else None,
                                         _dtype_code(var) if sc_w else dt, eps, _ptr(addend),
+                                        _ptr(keep), _ptr(ib[1]) if ib else None,
+                                        _ptr(ib[2]) if ib else None,
+                                        _dtype_code(ib[1]) if ib else dt, ib[3] if ib else 0.0,
                                         _ptr(dx), _ptr(wsp), nb, st)
                 folded = st_ == 0
                 if st_ not in (0, 4):  # 4 = MS_ERR_UNSUPPORTED: scale the weight here
@@ -917,6 +934,8 @@ class _ConvBNFn(torch.autograd.Function):
                                           nb, st), "ms_conv2d_dx")
                 if addend is not None:
                     dx.add_(addend)
+                if keep is not None:
+                    dx = _mask_scale(dx, keep, ib)
             del addend
         if need_w or need_b:
             gc = g
@@ -940,7 +959,29 @@ class _ConvBNFn(torch.autograd.Function):
                 wsp, nb = _workspace(4 * w_shape[0], gc.device)
                 _lib.check(L.ms_conv2d_db(ctypes.byref(d), _ptr(gc), _ptr(db), _ptr(wsp), nb, st),
                            "ms_conv2d_db")
-        return dx, dw, db, d_res, None, None, None, None, None
+        return (dx, dw, db, d_res) + (None,) * 7
+
+
+def _mask_scale(g: torch.Tensor, keep: torch.Tensor, bnp) -> torch.Tensor:
+    """g * keep [* s] as its own pass (ms_relu_bwd / ms_bn_relu_bwd): the fallback
+    of the ReLU [+ eval-BN] backward that a fused dgrad epilogue normally applies."""
+    keep = _need(keep, "mask", "ReLU backward")
+    fmt = torch.channels_last if _is_channels_last(g) and not g.is_contiguous() \
+        else torch.contiguous_format
+    g = g.contiguous(memory_format=fmt)
+    out = torch.empty_like(g, memory_format=fmt)
+    if _is_meta(g):
+        return out
+    L = _lib.lib()
+    if bnp is None:
+        _lib.check(L.ms_relu_bwd(g.numel(), _dtype_code(g), _ptr(g), _ptr(keep), _ptr(out),
+                                 _stream(g.device)), "ms_relu_bwd")
+    else:
+        mean, var, bw, eps = bnp
+        _lib.check(L.ms_bn_relu_bwd(g.numel(), g.shape[1], _dtype_code(g), _dtype_code(mean),
+                                    _ptr(g), _ptr(keep), _ptr(mean), _ptr(var), _ptr(bw), eps,
+                                    _ptr(out), _stream(g.device)), "ms_bn_relu_bwd")
+    return out
 
 
 class _MaskScaleFn(torch.autograd.Function):
@@ -994,21 +1035,61 @@ def conv_bn_fusable(x: torch.Tensor, conv, bn) -> bool:
         and conv.weight.dtype == x.dtype and bn.running_mean.device == x.device
 
 
+def _relu_keep_mask(y: torch.Tensor) -> torch.Tensor:
+    # a ReLU folded into a fused call keeps its MemSave storage (bit mask)
+    return relu(y) if y.device.type in ("cuda", "meta") else torch.relu(y)
+
+
+def fused_conv(x: torch.Tensor, conv, bn, relu_: bool, residual=None, tee: bool = False,
+               in_mask=None, in_bn=None, raw: bool = False):
+    """The general fused chain ``relu?(bn?(conv(x)) [+ residual])`` behind the
+    wrappers below and the graph pass (nn.fuse_conv_bn_relu).  Returns
+    ``(y, mask, alias)``:
+
+    * ``tee``: alias is x itself for x's other consumer (else None); that
+      consumer's gradient is summed into dX in the dgrad epilogue.
+    * ``raw``: the ReLU's backward is NOT applied here; mask is its bit mask
+      (else None) and the single consumer of y must be a fused conv that gets
+      it as ``in_mask`` (with ``in_bn`` = this BN when the chain has one and no
+      residual) and applies keep [* s] in its own dgrad epilogue.
+    * ``in_mask`` / ``in_bn``: the producer's mask / BN for the above.
+
+    One tcgen05 launch when the chain is fusable (frozen eval BN, 16-bit NHWC on
+    CUDA); otherwise the layers in sequence, the producer's deferred ReLU
+    backward applied first."""
+    if in_mask is None:
+        in_bn = None
+    ok = conv_bn_fusable(x, conv, bn) if bn is not None else conv_relu_fusable(x, conv)
+    if residual is not None:
+        ok = ok and residual.dtype == x.dtype and residual.device == x.device \
+            and residual.dim() == 4
+    if not ok:
+        if in_mask is not None:
+            x = _MaskScaleFn.apply(x, in_mask, in_bn)
+        y = conv(x)
+        if bn is not None:
+            y = bn(y)
+        if residual is not None:
+            y = add_relu(y, residual) if relu_ else y + residual
+        elif relu_:
+            y = _relu_keep_mask(y)
+        return y, None, (x if tee else None)
+    outs = _ConvBNFn.apply(x, conv.weight, conv.bias, residual, conv.stride, conv.padding, bn,
+                           relu_, tee, in_mask, in_bn)
+    y, mask = outs[0], outs[1]
+    if relu_ and mask is not None and not raw:
+        # conv -> BN -> ReLU: g * keep * s; with a residual (BN scale folded into the
+        # dgrad weight) or without a BN: g * keep
+        y = _MaskScaleFn.apply(y, mask, bn if residual is None else None)
+        mask = None
+    return y, (mask if raw else None), (outs[2] if tee else None)
+
+
 def conv_bn_relu(x: torch.Tensor, conv, bn, with_relu: bool) -> torch.Tensor:
     """conv -> bn -> (relu) of the given modules: one fused launch when
     ``conv_bn_fusable`` holds, else the layers in sequence (BN in training mode
     or with trainable parameters, float32, ...)."""
-    if conv_bn_fusable(x, conv, bn):
-        y, mask = _ConvBNFn.apply(x, conv.weight, conv.bias, None, conv.stride, conv.padding, bn,
-                                  with_relu)
-        if with_relu and mask is not None:
-            return _MaskScaleFn.apply(y, mask, bn)
-        return y
-    y = bn(conv(x))
-    if not with_relu:
-        return y
-    # the ReLU module was folded into this call: keep its MemSave storage (bit mask)
-    return relu(y) if y.device.type in ("cuda", "meta") else torch.relu(y)
+    return fused_conv(x, conv, bn, with_relu)[0]
 
 
 def conv_bn_relu_tee(x: torch.Tensor, conv, bn, with_relu: bool):
@@ -1016,13 +1097,8 @@ def conv_bn_relu_tee(x: torch.Tensor, conv, bn, with_relu: bool):
     copy) for x's other consumer, e.g. the identity or downsample branch of a
     ResNet block.  Its gradient is added to dX inside the dgrad epilogue, which
     replaces the engine's separate accumulation pass over the two gradients."""
-    if conv_bn_fusable(x, conv, bn):
-        y, mask, xt = _ConvBNFn.apply(x, conv.weight, conv.bias, None, conv.stride,
-                                      conv.padding, bn, with_relu, True)
-        if with_relu and mask is not None:
-            return _MaskScaleFn.apply(y, mask, bn), xt
-        return y, xt
-    return conv_bn_relu(x, conv, bn, with_relu), x
+    y, _, xt = fused_conv(x, conv, bn, with_relu, tee=True)
+    return y, xt
 
 
 def conv_relu_fusable(x: torch.Tensor, conv) -> bool:
@@ -1039,28 +1115,14 @@ def conv_relu_fusable(x: torch.Tensor, conv) -> bool:
 def conv_relu(x: torch.Tensor, conv) -> torch.Tensor:
     """relu(conv(x)) with the ReLU (and its bit mask) in the conv epilogue (VGG);
     the two memsave layers in sequence when the fused launch does not apply."""
-    if conv_relu_fusable(x, conv):
-        y, mask = _ConvBNFn.apply(x, conv.weight, conv.bias, None, conv.stride, conv.padding,
-                                  None, True)
-        if mask is not None:
-            return _MaskScaleFn.apply(y, mask, None)
-        return y
-    y = conv(x)
-    return relu(y) if y.device.type in ("cuda", "meta") else torch.relu(y)
+    return fused_conv(x, conv, None, True)[0]
 
 
 def conv_bn_add_relu(x: torch.Tensor, conv, bn, residual: torch.Tensor) -> torch.Tensor:
     """relu(bn(conv(x)) + residual): the main branch and the join of a ResNet
     block in one launch (residual added in the conv epilogue) when
     ``conv_bn_fusable`` holds and the residual matches the output."""
-    if (conv_bn_fusable(x, conv, bn) and residual.dtype == x.dtype
-            and residual.device == x.device and residual.dim() == 4):
-        y, mask = _ConvBNFn.apply(x, conv.weight, conv.bias, residual, conv.stride, conv.padding,
-                                  bn, True)
-        if mask is not None:
-            return _MaskScaleFn.apply(y, mask, None)
-        return y
-    return add_relu(bn(conv(x)), residual)
+    return fused_conv(x, conv, bn, True, residual)[0]
 
 
 # =============================================================== fused residual add + ReLU

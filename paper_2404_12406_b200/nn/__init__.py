@@ -374,35 +374,71 @@ def fuse_conv_bn_relu(model: nn.Module, verbose: bool = False) -> nn.Module:
                 g.erase_node(main)
                 nres += 1
                 break
-    # a tensor read by a fused conv and by one more fused op (a ResNet block input:
-    # conv1 and the identity / downsample branch): the conv tees it, so the two
-    # gradients are summed in its dgrad epilogue rather than by a separate pass
+    # generic form: every fused chain becomes fused_conv(...) -> (y, mask, alias)
+    gen = []
+    for node in list(g.nodes):
+        if node.op != "call_function" or node.target not in (MF.conv_bn_relu, MF.conv_relu,
+                                                             MF.conv_bn_add_relu):
+            continue
+        kw = {}
+        if node.target is MF.conv_bn_relu:
+            x, conv_ref, bn_ref, r = node.args
+        elif node.target is MF.conv_relu:
+            (x, conv_ref), bn_ref, r = node.args, None, True
+        else:
+            x, conv_ref, bn_ref, res = node.args
+            r, kw = True, {"residual": res}
+        with g.inserting_before(node):
+            f = g.call_function(MF.fused_conv, (x, conv_ref, bn_ref, r), kw)
+            y = g.call_function(operator.getitem, (f, 0))
+        node.replace_all_uses_with(y)
+        g.erase_node(node)
+        gen.append((f, y))
+    # a tensor read as the input of a fused conv and by one more fused chain (a
+    # ResNet block input: conv1 and the identity / downsample branch): the conv
+    # tees it, so the two gradients are summed in its dgrad epilogue rather than
+    # by a separate pass
     ntee = 0
     order = {n: i for i, n in enumerate(g.nodes)}
-    tee_ok = (MF.conv_bn_relu, MF.conv_bn_add_relu, MF.add_relu, MF.conv_relu)
     for node in list(g.nodes):
-        users = sorted(node.users, key=order.get)
+        users = sorted(node.users, key=lambda n: order.get(n, len(order)))
         if len(users) != 2:
             continue
         u1, u2 = users
-        if (u1.op != "call_function" or u1.target is not MF.conv_bn_relu or u1.kwargs
-                or u1.args[0] is not node or sum(a is node for a in u1.args) != 1
-                or u2.op != "call_function" or u2.target not in tee_ok or u2.kwargs):
+        if (u1.target is not MF.fused_conv or u1.args[0] is not node
+                or node in u1.args[1:] or node in u1.kwargs.values()
+                or u2.target is not MF.fused_conv):
             continue
-        with g.inserting_before(u1):
-            tee = g.call_function(MF.conv_bn_relu_tee, u1.args)
-            out = g.call_function(operator.getitem, (tee, 0))
-            alias = g.call_function(operator.getitem, (tee, 1))
-        u1.replace_all_uses_with(out)
-        g.erase_node(u1)
+        u1.kwargs = {**u1.kwargs, "tee": True}
+        with g.inserting_after(u1):
+            alias = g.call_function(operator.getitem, (u1, 2))
         u2.args = tuple(alias if a is node else a for a in u2.args)
+        u2.kwargs = {k: (alias if v is node else v) for k, v in u2.kwargs.items()}
         ntee += 1
+    # a fused ReLU whose output feeds only the input of another fused conv: that
+    # conv applies the ReLU's backward (keep mask [* BN scale]) in its dgrad
+    # epilogue instead of a separate pass over the gradient
+    nfwd = 0
+    for f, y in gen:
+        if not f.args[3] or len(y.users) != 1:
+            continue
+        c = next(iter(y.users))
+        if (c.target is not MF.fused_conv or c.args[0] is not y or y in c.args[1:]
+                or y in c.kwargs.values()):
+            continue
+        f.kwargs = {**f.kwargs, "raw": True}
+        with g.inserting_after(y):
+            m = g.call_function(operator.getitem, (f, 1))
+        in_bn = f.args[2] if "residual" not in f.kwargs else None
+        c.kwargs = {**c.kwargs, "in_mask": m, "in_bn": in_bn}
+        nfwd += 1
     g.eliminate_dead_code()
     g.lint()
     gm.recompile()
     if verbose:
         print(f"memsave: fused {nfused} conv->bn[->relu], {nadd} add->relu, {nres} "
-              f"conv->bn->add->relu and {nrelu} conv->relu chains; {ntee} tee'd inputs")
+              f"conv->bn->add->relu and {nrelu} conv->relu chains; {ntee} tee'd inputs, "
+              f"{nfwd} ReLU backwards moved into the consumer's dgrad")
     return gm
 
 

@@ -625,6 +625,59 @@ def test_conv_bn_relu_tee(case):
     _close(x.grad, ref + vq_, "bf16", "tee dx", ulps=2.01)
 
 
+@pytest.mark.parametrize("case", [(2, 64, 11, 20, 64, 1, True, True),     # halo dgrad
+                                  (2, 64, 9, 14, 128, 2, True, False),    # phase GEMM s2
+                                  (2, 128, 7, 7, 128, 1, False, True),    # generic s1
+                                  (1, 64, 6, 6, 64, 1, False, False)])
+def test_fused_conv_in_mask(case):
+    # x came out of a fused ReLU [after eval-BN bn_in] whose backward (keep bit
+    # mask [* s_in]) runs in this conv's dgrad epilogue, after the tee addend
+    n, c, h, w, k, s, with_in_bn, tee = case
+    rng = np.random.default_rng(c + k + s + 7)
+    x, xq = _q(rng.standard_normal((n, c, h, w)), "bf16")
+    wt, wq = _q(rng.standard_normal((k, c, 3, 3)) / np.sqrt(c * 9), "bf16")
+    conv = torch.nn.Conv2d(c, k, 3, s, 1, bias=False).to(DEV, torch.bfloat16)
+    conv.weight.data.copy_(wt)
+    conv.weight.requires_grad_(False)
+
+    def frozen_bn(ch, lo):
+        bn = torch.nn.BatchNorm2d(ch).to(DEV, torch.bfloat16).eval()
+        bn.running_mean.copy_(torch.linspace(-0.2, 0.2, ch))
+        bn.running_var.copy_(torch.linspace(0.5, 2.0, ch))
+        bn.weight.data.copy_(torch.linspace(lo, 1.5, ch))
+        bn.bias.data.copy_(torch.linspace(-0.3, 0.3, ch))
+        for prm in bn.parameters():
+            prm.requires_grad_(False)
+        return bn
+
+    bn = frozen_bn(k, 0.5)
+    bn_in = frozen_bn(c, 0.25) if with_in_bn else None
+    keep = rng.random((n, h, w, c)) < 0.6  # NHWC storage order of x
+    mask = torch.from_numpy(np.packbits(keep.reshape(-1), bitorder="little")).to(DEV)
+    keep_nchw = keep.transpose(0, 3, 1, 2)
+    x = x.contiguous(memory_format=torch.channels_last).requires_grad_(True)
+    y, _, xa = MF.fused_conv(x, conv, bn, False, tee=tee, in_mask=mask, in_bn=bn_in)
+    g, gq = _q(rng.standard_normal(tuple(y.shape)), "bf16")
+    loss = (y.float() * g.float()).sum()
+    vq = np.zeros(xq.shape)
+    if tee:
+        vq = oracle.round_to(rng.standard_normal(xq.shape), "bf16")
+        v = torch.from_numpy(vq).to(DEV, torch.bfloat16)
+        loss = loss + (xa.float() * v.float()).sum()
+    loss.backward()
+
+    def scale_of(m):
+        var = m.running_var.double().cpu().numpy()
+        return oracle.round_to(m.weight.double().cpu().numpy() / np.sqrt(var + 1e-5), "f32")
+
+    wsq = oracle.round_to(wq * scale_of(bn).reshape(-1, 1, 1, 1), "bf16")
+    ref = oracle.conv2d_dx(gq, wsq, s, 1, h, w) + vq
+    ref = np.where(keep_nchw, ref, 0.0)
+    if with_in_bn:
+        ref = ref * scale_of(bn_in).reshape(1, -1, 1, 1)
+    _close(x.grad, ref, "bf16", "in-mask dx", ulps=2.01)
+
+
 def test_add_relu():
     rng = np.random.default_rng(3)
     a, aq = _q(rng.standard_normal((2, 32, 9, 9)), "bf16")
