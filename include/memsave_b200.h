@@ -205,6 +205,15 @@ MS_API ms_status ms_maxpool2d_fwd(const ms_pool_desc* p, const void* x, void* y,
                                   void* idx_or_null, void* stream);
 MS_API ms_status ms_maxpool2d_bwd(const ms_pool_desc* p, const void* g, const void* idx,
                                   void* dx, void* stream);
+/* The same, with the backward of the ReLU [+ eval-BN] that produced x applied
+ * before the store: dx = keep ? dx * s_in : 0 (keep: that ReLU's bit mask in
+ * storage order; s_in = in_weight/sqrt(in_var+in_eps), in_var = NULL: 1) --
+ * replaces a separate ms_relu_bwd / ms_bn_relu_bwd pass over dx.
+ * MS_ERR_UNSUPPORTED outside the NHWC 3x3/2/1 kernel (C % 8 == 0, C <= 512). */
+MS_API ms_status ms_maxpool2d_relu_bwd(const ms_pool_desc* p, const void* g, const void* idx,
+                                       const void* keep, const void* in_var_or_null,
+                                       const void* in_weight_or_null, int32_t in_pdtype,
+                                       double in_eps, void* dx, void* stream);
 
 /* ------------------------------------------------------------ conv_transpose2d
  * ConvTranspose2d forward (rules.py:68-71; SPEC.md forward_conv_transpose2d:

@@ -79,6 +79,8 @@ SIGNATURES = {
     "ms_maxpool2d_out_w": (_c_i64, [ctypes.POINTER(PoolDesc)]),
     "ms_maxpool2d_fwd": (_c_i32, [ctypes.POINTER(PoolDesc), _vp, _vp, _vp, _vp]),
     "ms_maxpool2d_bwd": (_c_i32, [ctypes.POINTER(PoolDesc), _vp, _vp, _vp, _vp]),
+    "ms_maxpool2d_relu_bwd": (_c_i32, [ctypes.POINTER(PoolDesc), _vp, _vp, _vp, _vp, _vp, _c_i32,
+                                       ctypes.c_double, _vp, _vp]),
     "ms_conv_transpose2d_fwd": (_c_i32, [ctypes.POINTER(ConvDesc), _vp, _vp, _vp, _vp, _vp, _c_sz,
                                          _vp]),
     "ms_dropout_fwd": (_c_i32, [_c_i64, _c_i32, _vp, _vp, ctypes.c_uint64, ctypes.c_uint64,

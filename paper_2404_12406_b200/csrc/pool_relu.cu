@@ -126,6 +126,8 @@ __global__ void __launch_bounds__(256) relu_bwd_kernel(int64_t n, const T* g,
 }
 
 // ---------------------------------------------------------------- MaxPool2d
+constexpr int MAXPOOL_FUSED_C = 512;  // channels of the fused-epilogue scale table
+
 struct PoolDims {
   int n, c, h, w, oh, ow, kh, kw, sh, sw, ph, pw;
 };
@@ -301,7 +303,20 @@ __device__ __forceinline__ void route8(float (&acc)[8], const uint2 u, const flo
 template <typename T>
 __global__ void __launch_bounds__(256) maxpool_bwd_k3s2p1(PoolDims d, const T* __restrict__ g,
                                                           const uint8_t* __restrict__ idx,
-                                                          T* __restrict__ dx) {
+                                                          T* __restrict__ dx,
+                                                          const uint8_t* __restrict__ keep,
+                                                          const BnFold in_bn) {
+  // keep (nullable): the bit mask of the ReLU that produced x, and in_bn.var
+  // (nullable) the eval-BN before it: dx = keep ? dx * s : 0 (their backward)
+  __shared__ float s_sc[MAXPOOL_FUSED_C];
+  if (in_bn.var) {
+    for (int c = threadIdx.x; c < d.c; c += blockDim.x) {
+      float s, t_;
+      bn_fold(in_bn, c, s, t_);
+      s_sc[c] = s;
+    }
+    __syncthreads();
+  }
   const int G = d.c >> 3;
   const int jn = (d.w + 1) >> 1;
   const int in = (d.h + 1) >> 1;
@@ -341,6 +356,24 @@ __global__ void __launch_bounds__(256) maxpool_bwd_k3s2p1(PoolDims d, const T* _
   route8<T>(o11, u[1][0], gv[1][0], 2);  //                (i+1, j) r0 s2
   route8<T>(o11, u[1][1], gv[1][1], 0);  //                (i+1, j+1) r0 s0
   const int h0 = 2 * i, w0 = 2 * j;
+  if (keep || in_bn.var) {
+    auto fin = [&](float (&o)[8], int hh, int ww) {
+      if (hh >= d.h || ww >= d.w) return;
+      if (keep) {
+        const uint32_t kb = keep[(((int64_t)n * d.h + hh) * d.w + ww) * G + gg];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) o[q] = ((kb >> q) & 1u) ? o[q] : 0.f;
+      }
+      if (in_bn.var) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) o[q] *= s_sc[gg * 8 + q];
+      }
+    };
+    fin(o00, h0, w0);
+    fin(o01, h0, w0 + 1);
+    fin(o10, h0 + 1, w0);
+    fin(o11, h0 + 1, w0 + 1);
+  }
   T* base = dx + ((int64_t)n * d.h + h0) * d.w * d.c + gg * 8;
   st8<T>(base + (int64_t)w0 * d.c, o00, true);
   if (w0 + 1 < d.w) st8<T>(base + (int64_t)(w0 + 1) * d.c, o01, true);
@@ -530,8 +563,9 @@ extern "C" ms_status ms_maxpool2d_fwd(const ms_pool_desc* p, const void* x, void
   return launch_status("maxpool_fwd");
 }
 
-extern "C" ms_status ms_maxpool2d_bwd(const ms_pool_desc* p, const void* g, const void* idx,
-                                      void* dx, void* stream) {
+static ms_status maxpool_bwd_impl(const ms_pool_desc* p, const void* g, const void* idx,
+                                  const uint8_t* keep, const BnFold& in_bn, void* dx,
+                                  void* stream) {
   PoolDims d;
   MS_TRY(pool_dims(p, d));
   MS_CHECK_ARG(g && idx && dx, MS_ERR_SHAPE, "maxpool bwd: null tensor");
@@ -539,14 +573,19 @@ extern "C" ms_status ms_maxpool2d_bwd(const ms_pool_desc* p, const void* g, cons
   MS_TRY(bind_device(dx));
   cudaStream_t st = (cudaStream_t)stream;
   const int dt = p->dtype;
-  if (p->layout == MS_NHWC && d.c % 8 == 0 && al16(g) && al16(dx) &&
-      (reinterpret_cast<uintptr_t>(idx) & 7) == 0 &&
-      (int64_t)d.n * d.h * d.w * (d.c / 8) < (1ll << 31)) {
+  const bool fast = p->layout == MS_NHWC && d.c % 8 == 0 && al16(g) && al16(dx) &&
+                    (reinterpret_cast<uintptr_t>(idx) & 7) == 0 &&
+                    (int64_t)d.n * d.h * d.w * (d.c / 8) < (1ll << 31);
+  MS_CHECK_ARG((!keep && !in_bn.var) || (fast && is_k3s2p1(d) && d.c <= MAXPOOL_FUSED_C),
+               MS_ERR_UNSUPPORTED,
+               "maxpool bwd: the fused ReLU/BN backward needs the NHWC 3x3/2/1 kernel, C <= %d",
+               MAXPOOL_FUSED_C);
+  if (fast) {
     if (is_k3s2p1(d)) {
       const dim3 grid((unsigned)((((d.w + 1) / 2) * (d.c / 8) + 255) / 256),
                       (unsigned)(d.n * ((d.h + 1) / 2)));
-      MS_DT_DISPATCH(dt, maxpool_bwd_k3s2p1<T><<<grid, 256, 0, st>>>(d, (const T*)g,
-                                                                     (const uint8_t*)idx, (T*)dx));
+      MS_DT_DISPATCH(dt, maxpool_bwd_k3s2p1<T><<<grid, 256, 0, st>>>(
+                             d, (const T*)g, (const uint8_t*)idx, (T*)dx, keep, in_bn));
     } else {
       const int64_t work = (int64_t)d.n * d.h * d.w * (d.c / 8);
       MS_DT_DISPATCH(dt, maxpool_bwd_nhwc8<T><<<grid_for(work), 256, 0, st>>>(
@@ -560,4 +599,21 @@ extern "C" ms_status ms_maxpool2d_bwd(const ms_pool_desc* p, const void* g, cons
   }
   count_launch();
   return launch_status("maxpool_bwd");
+}
+
+extern "C" ms_status ms_maxpool2d_bwd(const ms_pool_desc* p, const void* g, const void* idx,
+                                      void* dx, void* stream) {
+  return maxpool_bwd_impl(p, g, idx, nullptr, BnFold{}, dx, stream);
+}
+
+extern "C" ms_status ms_maxpool2d_relu_bwd(const ms_pool_desc* p, const void* g, const void* idx,
+                                           const void* keep, const void* in_var,
+                                           const void* in_weight, int32_t in_pdtype,
+                                           double in_eps, void* dx, void* stream) {
+  BnFold bn;
+  bn.var = in_var;
+  bn.w = in_weight;
+  bn.pdt = in_pdtype;
+  bn.eps = (float)in_eps;
+  return maxpool_bwd_impl(p, g, idx, static_cast<const uint8_t*>(keep), bn, dx, stream);
 }

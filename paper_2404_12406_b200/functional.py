@@ -444,7 +444,13 @@ class _MaxPool2dFn(torch.autograd.Function):
     (rules.py:108-109; the reference's IndexMap, saved.py:111-125, is 4 bytes)."""
 
     @staticmethod
-    def forward(ctx, x, kernel_size, stride, padding):
+    def forward(ctx, x, kernel_size, stride, padding, in_mask=None, in_bn=None):
+        # in_mask / in_bn: x came out of a fused ReLU [after eval-BN]; its backward
+        # (keep [* s]) is applied in this backward's store (ms_maxpool2d_relu_bwd)
+        if in_mask is None:
+            in_bn = None
+        ctx.in_bn = None if in_bn is None else (in_bn.running_mean, in_bn.running_var,
+                                                in_bn.weight, float(in_bn.eps))
         kh, kw = _pair(kernel_size)
         sh, sw = _pair(stride)
         ph, pw = _pair(padding)
@@ -455,10 +461,11 @@ class _MaxPool2dFn(torch.autograd.Function):
         oh = (h + 2 * ph - kh) // sh + 1
         ow = (w + 2 * pw - kw) // sw + 1
         ctx.geom = (tuple(x.shape), kh, kw, sh, sw, ph, pw)
+        keep = in_mask if x_rg else None
         if _is_meta(x):
             ctx.layout = _lib.MS_NCHW
             ctx.save_for_backward(torch.empty((n, c, oh, ow), dtype=torch.uint8, device="meta")
-                                  if x_rg else None)
+                                  if x_rg else None, keep)
             return x.new_empty((n, c, oh, ow))
         _require_cuda("max_pool2d", x)
         layout = _lib.MS_NHWC if (_is_channels_last(x) and not x.is_contiguous()) else _lib.MS_NCHW
@@ -474,32 +481,49 @@ class _MaxPool2dFn(torch.autograd.Function):
         L = _lib.lib()
         _lib.check(L.ms_maxpool2d_fwd(ctypes.byref(d), _ptr(xl), _ptr(y), _ptr(idx),
                                       _stream(x.device)), "ms_maxpool2d_fwd")
-        ctx.save_for_backward(idx)
+        ctx.save_for_backward(idx, keep)
         return y
 
     @staticmethod
     def backward(ctx, gy):
-        (idx,) = ctx.saved_tensors
+        idx, keep = ctx.saved_tensors
+        nones = (None,) * 5
         if not ctx.needs_input_grad[0]:
-            return None, None, None, None
+            return (None,) + nones
         idx = _need(idx, "idx", "max_pool2d dX")
         x_shape, kh, kw, sh, sw, ph, pw = ctx.geom
         if _is_meta(gy):
-            return gy.new_empty(x_shape), None, None, None
+            return (gy.new_empty(x_shape),) + nones
         layout = ctx.layout
         g = _as_layout(gy, layout)
         n, c, h, w = x_shape
         d = _lib.PoolDesc(n, c, h, w, kh, kw, sh, sw, ph, pw, layout, _dtype_code(g))
         dx = _empty4(x_shape, g, layout)
         L = _lib.lib()
+        if keep is not None:
+            ib = ctx.in_bn
+            st_ = L.ms_maxpool2d_relu_bwd(ctypes.byref(d), _ptr(g), _ptr(idx), _ptr(keep),
+                                          _ptr(ib[1]) if ib else None, _ptr(ib[2]) if ib else None,
+                                          _dtype_code(ib[1]) if ib else 0, ib[3] if ib else 0.0,
+                                          _ptr(dx), _stream(g.device))
+            if st_ == 0:
+                return (dx,) + nones
+            if st_ != 4:  # 4 = MS_ERR_UNSUPPORTED: the unfused pair of passes
+                _lib.check(st_, "ms_maxpool2d_relu_bwd")
         _lib.check(L.ms_maxpool2d_bwd(ctypes.byref(d), _ptr(g), _ptr(idx), _ptr(dx),
                                       _stream(g.device)), "ms_maxpool2d_bwd")
-        return dx, None, None, None
+        if keep is not None:
+            dx = _mask_scale(dx, keep, ctx.in_bn)
+        return (dx,) + nones
 
 
-def max_pool2d(x, kernel_size, stride=None, padding=0):
-    """Max pooling whose backward reads a 1-byte argmax map (SPEC.md forward_maxpool2d)."""
-    return _MaxPool2dFn.apply(x, kernel_size, kernel_size if stride is None else stride, padding)
+def max_pool2d(x, kernel_size, stride=None, padding=0, in_mask=None, in_bn=None):
+    """Max pooling whose backward reads a 1-byte argmax map (SPEC.md forward_maxpool2d).
+    ``in_mask`` / ``in_bn``: x is the raw output of a fused conv -> [BN ->] ReLU
+    (fused_conv(raw=True)); the ReLU [+ BN scale] backward then runs in this
+    backward's store."""
+    return _MaxPool2dFn.apply(x, kernel_size, kernel_size if stride is None else stride, padding,
+                              in_mask, in_bn)
 
 
 # =============================================================== dropout (RNG replay)

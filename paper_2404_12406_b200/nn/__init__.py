@@ -423,14 +423,25 @@ def fuse_conv_bn_relu(model: nn.Module, verbose: bool = False) -> nn.Module:
         if not f.args[3] or len(y.users) != 1:
             continue
         c = next(iter(y.users))
-        if (c.target is not MF.fused_conv or c.args[0] is not y or y in c.args[1:]
-                or y in c.kwargs.values()):
+        pool = modules.get(c.target) if c.op == "call_module" else None
+        is_pool = (isinstance(pool, MemSaveMaxPool2d) and maxpool2d_supported(pool)
+                   and c.args == (y,) and not c.kwargs)
+        if not is_pool and (c.target is not MF.fused_conv or c.args[0] is not y
+                            or y in c.args[1:] or y in c.kwargs.values()):
             continue
         f.kwargs = {**f.kwargs, "raw": True}
         with g.inserting_after(y):
             m = g.call_function(operator.getitem, (f, 1))
         in_bn = f.args[2] if "residual" not in f.kwargs else None
-        c.kwargs = {**c.kwargs, "in_mask": m, "in_bn": in_bn}
+        if is_pool:  # the stem: conv -> BN -> ReLU -> MaxPool
+            with g.inserting_before(c):
+                mp = g.call_function(MF.max_pool2d, (y, pool.kernel_size, pool.stride,
+                                                     pool.padding),
+                                     {"in_mask": m, "in_bn": in_bn})
+            c.replace_all_uses_with(mp)
+            g.erase_node(c)
+        else:
+            c.kwargs = {**c.kwargs, "in_mask": m, "in_bn": in_bn}
         nfwd += 1
     g.eliminate_dead_code()
     g.lint()

@@ -349,6 +349,39 @@ def test_maxpool_padded(shape, k, s, p, dt):
     np.testing.assert_allclose(x.grad.float().cpu().numpy(), xt.grad.numpy(), rtol=1e-2, atol=1e-2)
 
 
+@pytest.mark.parametrize("shape,k,s,p", [((4, 64, 56, 56), 3, 2, 1), ((2, 24, 15, 13), 3, 2, 1),
+                                          ((3, 16, 10, 8), 3, 1, 1)])   # last: fallback passes
+@pytest.mark.parametrize("with_bn", [True, False])
+def test_maxpool_relu_bwd_fused(shape, k, s, p, with_bn):
+    # the stem's conv -> BN -> ReLU -> MaxPool: the ReLU keep mask and the BN
+    # scale applied in the maxpool backward's store
+    rng = np.random.default_rng(sum(shape) + with_bn)
+    x, xq = _q(np.abs(rng.standard_normal(shape)), "bf16")
+    x = x.contiguous(memory_format=torch.channels_last).requires_grad_(True)
+    n, c, h, w = shape
+    keep = rng.random((n, h, w, c)) < 0.7  # NHWC storage order
+    mask = torch.from_numpy(np.packbits(keep.reshape(-1), bitorder="little")).to(DEV)
+    bn = None
+    if with_bn:
+        bn = torch.nn.BatchNorm2d(c).to(DEV, torch.bfloat16).eval()
+        bn.running_var.copy_(torch.linspace(0.5, 2.0, c))
+        bn.weight.data.copy_(torch.linspace(0.25, 1.5, c))
+    y = MF.max_pool2d(x, k, s, p, in_mask=mask, in_bn=bn)
+    yr, local, flat = oracle.maxpool2d_fwd(xq, k, k, s, s, p, p)
+    g, gq = _q(rng.standard_normal(yr.shape), "bf16")
+    y.backward(g)
+    dxp = oracle.maxpool2d_bwd(gq, flat, h, w)
+    if s == 1:  # no fused kernel: maxpool backward, then ms_bn_relu_bwd (two roundings)
+        dxp = oracle.round_to(dxp, "bf16")
+    ref = np.where(keep.transpose(0, 3, 1, 2), dxp, 0.0)
+    if with_bn:
+        var = bn.running_var.double().cpu().numpy()
+        sc = oracle.round_to(bn.weight.detach().double().cpu().numpy() / np.sqrt(var + 1e-5),
+                             "f32")
+        ref = ref * sc.reshape(1, -1, 1, 1)
+    _close(x.grad, ref, "bf16", "maxpool+relu dx", ulps=2.01)
+
+
 @pytest.mark.parametrize("shape", [(2, 8, 40, 70), (1, 8, 16, 64), (3, 8, 33, 17)])
 def test_fig1_fp32_tiled_kernel(shape):
     # the specialised float32 8->8 3x3/1 kernels (fwd, dX via flipped weights, dW)
