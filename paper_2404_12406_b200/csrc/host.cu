@@ -337,6 +337,33 @@ int pick_bn(int64_t other_tiles, int64_t ncols) {
   return best;
 }
 
+int pair_slots() {
+  static int n = 0;
+  if (n == 0) {
+    auto kern = umma_gemm_kernel<256, 0, 0, LOAD_GEMM, 2>;
+    constexpr int smem = GemmCfg<256, 0, 0, LOAD_GEMM, 2>::SMEM_BYTES;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaLaunchConfig_t cfg{};
+    cfg.blockDim = dim3(GemmCfg<256, 0, 0, LOAD_GEMM, 2>::THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.gridDim = dim3(num_sms() / 2 * 2);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int c = 0;
+    if (cudaOccupancyMaxActiveClusters(&c, kern, &cfg) != cudaSuccess || c <= 0) {
+      cudaGetLastError();
+      c = num_sms() / 2;
+    }
+    n = c;
+  }
+  return n;
+}
+
 TilePick pick_tiles(int64_t m_blocks, int64_t cols, bool allow_pair, bool b_mn) {
   static const int env_cl = [] {
     const char* e = getenv("MS_GEMM_CLUSTER");

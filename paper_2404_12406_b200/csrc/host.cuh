@@ -62,5 +62,8 @@ struct TilePick {
   int cl, bn;
 };
 TilePick pick_tiles(int64_t m_blocks, int64_t ncols, bool allow_pair, bool mn_major_b);
+// co-resident CTA-pair clusters of the persistent GEMM (one CTA per SM; GPCs
+// with an odd SM count leave an SM out of the pairs)
+int pair_slots();
 
 }  // namespace ms

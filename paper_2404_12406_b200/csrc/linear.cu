@@ -20,6 +20,9 @@ struct LinPlan {
   int splits = 1;
   int kb_per_split = 0;
   int m_blocks = 0, n_blocks = 0, k_blocks = 0;
+  // last-wave K split (GemmArgs::tail_splits): tiles >= full_tiles run as
+  // tail_splits slices of tail_kbps k-blocks; partials in ws, then finalize
+  int full_tiles = 0, tail_splits = 0, tail_kbps = 0;
   size_t ws = 0;
 };
 
@@ -37,9 +40,11 @@ LinPlan plan_gemm(int64_t rows, int64_t cols, int64_t red, bool b_mn, bool allow
   p.n_blocks = (int)((cols + p.bn - 1) / p.bn);
   p.k_blocks = (int)((red + BK - 1) / BK);
   const int64_t tiles = (int64_t)((p.m_blocks + p.cl - 1) / p.cl) * p.n_blocks;
+  const int64_t slots = p.cl == 2 ? pair_slots() : sms;
   p.splits = 1;
-  if (allow_split && tiles * 2 <= sms / p.cl && p.k_blocks >= 8) {
-    int64_t s = (sms / p.cl + tiles - 1) / tiles;
+  if (allow_split && tiles * 2 <= slots && p.k_blocks >= 8) {
+    // split-K into fp32 (red.add): as many slices as fit in ONE wave
+    int64_t s = slots / tiles;
     const int64_t cap = p.k_blocks / 4;
     if (s > cap) s = cap;
     if (s < 1) s = 1;
@@ -47,8 +52,78 @@ LinPlan plan_gemm(int64_t rows, int64_t cols, int64_t red, bool b_mn, bool allow
   }
   p.kb_per_split = (p.k_blocks + p.splits - 1) / p.splits;
   p.splits = (p.k_blocks + p.kb_per_split - 1) / p.kb_per_split;
-  if (p.splits > 1) p.ws = align256(sizeof(float) * (size_t)rows * cols);
+  if (p.splits > 1) {
+    p.ws = align256(sizeof(float) * (size_t)rows * cols);
+    return p;
+  }
+  // The last wave of a persistent launch is partly idle when tiles % slots != 0
+  // (or the only wave, when tiles < slots).  Its r tiles are split into S
+  // K-slices (r*S units): the tail then costs ceil(r*S / slots) / S tile-times
+  // instead of one.  Pick S in 2..8 when that saves >= 15% of a tile-time and
+  // every slice keeps >= 16 k-blocks.
+  static const bool env_off = getenv("MS_GEMM_NO_TAIL_SPLIT") != nullptr;
+  const int64_t r = tiles % slots;
+  if (allow_split && !env_off && r > 0) {
+    double best = 1.0;
+    int bs = 0;
+    for (int s = 2; s <= 8; ++s) {
+      if (p.k_blocks / s < 16) break;  // short slices: the fp32 partials cost more
+      const double cost = (double)((r * s + slots - 1) / slots) / s;
+      if (cost < best - 0.15) {
+        best = cost;
+        bs = s;
+      }
+    }
+    if (bs) {
+      p.full_tiles = (int)(tiles - r);
+      p.tail_splits = bs;
+      p.tail_kbps = (p.k_blocks + bs - 1) / bs;
+      p.tail_splits = (p.k_blocks + p.tail_kbps - 1) / p.tail_kbps;
+      p.ws = align256(sizeof(float) * (size_t)r * p.tail_splits * p.cl * BM * p.bn);
+    }
+  }
   return p;
+}
+
+// out[rows of tail tile i] = sum of its tail_splits fp32 partials (bias already
+// added by slice 0), rounded once to the output dtype
+template <typename T>
+__global__ void tail_finalize_kernel(const float* __restrict__ ws, T* __restrict__ out,
+                                     int64_t ldc, int rows, int cols, int m_blocks, int n_blocks,
+                                     int n_fastest, int full_tiles, int splits, int tile_rows,
+                                     int bn) {
+  const int i = blockIdx.y;  // tail tile
+  const int tile = full_tiles + i;
+  const int mb = n_fastest ? (tile / n_blocks) % m_blocks : tile % m_blocks;
+  const int nb = n_fastest ? tile % n_blocks : (tile / m_blocks) % n_blocks;
+  const int m0 = mb * tile_rows;
+  const int n0 = nb * bn;
+  const int per_row = bn / 8;
+  const size_t tile_elems = (size_t)tile_rows * bn;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < tile_rows * per_row;
+       e += gridDim.x * blockDim.x) {
+    const int r = e / per_row, c = (e - r * per_row) * 8;
+    if (m0 + r >= rows || n0 + c >= cols) continue;
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int s = 0; s < splits; ++s) {
+      const float4* p = reinterpret_cast<const float4*>(
+          ws + ((size_t)i * splits + s) * tile_elems + (size_t)r * bn + c);
+      const float4 a = __ldg(p), b = __ldg(p + 1);
+      acc[0] += a.x; acc[1] += a.y; acc[2] += a.z; acc[3] += a.w;
+      acc[4] += b.x; acc[5] += b.y; acc[6] += b.z; acc[7] += b.w;
+    }
+    T* o = out + (int64_t)(m0 + r) * ldc + n0 + c;
+    if (n0 + c + 8 <= cols && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
+      uint4 u;
+      u.x = pack2<T>(acc[0], acc[1]);
+      u.y = pack2<T>(acc[2], acc[3]);
+      u.z = pack2<T>(acc[4], acc[5]);
+      u.w = pack2<T>(acc[6], acc[7]);
+      *reinterpret_cast<uint4*>(o) = u;
+    } else {
+      for (int j = 0; j < 8 && n0 + c + j < cols; ++j) o[j] = IO<T>::cvt(acc[j]);
+    }
+  }
 }
 
 LinPlan plan_linear(int64_t M, int64_t N, int64_t K, int dt, int pass) {
@@ -80,6 +155,18 @@ ms_status run_gemm(const LinPlan& p, int dt, int a_mn, int b_mn, const CUtensorM
   g.num_tiles = g.m_blocks * p.n_blocks * p.splits;
   g.ab_fmt = dt == MS_BF16 ? 1 : 0;
   g.nphases = 1;
+  // N-blocks fastest when B (cols x red) fits well inside L2 and A does not: the
+  // concurrent tiles then share their A rows and A streams from HBM once
+  {
+    static const int env_r = [] {
+      const char* e = getenv("MS_GEMM_RASTER");  // A/B: 0 = M fastest, 1 = N fastest
+      return e ? atoi(e) : -1;
+    }();
+    const double a_bytes = 2.0 * rows * (double)p.k_blocks * BK;
+    const double b_bytes = 2.0 * cols * (double)p.k_blocks * BK;
+    g.n_fastest = env_r >= 0 ? env_r
+                             : (p.n_blocks > 1 && b_bytes <= 32e6 && a_bytes > b_bytes ? 1 : 0);
+  }
   if (p.splits > 1) {
     MS_CHECK_ARG(ws && ws_bytes >= p.ws, MS_ERR_WORKSPACE, "linear: split-K workspace too small");
     cudaMemsetAsync(ws, 0, sizeof(float) * rows * cols, st);
@@ -90,6 +177,30 @@ ms_status run_gemm(const LinPlan& p, int dt, int a_mn, int b_mn, const CUtensorM
   }
   g.epi = EpiParams{out, ldc, dt, 0, bias, dt};
   MS_TRY(setup_tma_store(tm, g, dt, out, rows, cols, ldc));
+  if (p.tail_splits > 0) {
+    MS_CHECK_ARG(ws && ws_bytes >= p.ws, MS_ERR_WORKSPACE,
+                 "linear: tail-split workspace %zu < %zu", ws_bytes, p.ws);
+    g.full_tiles = p.full_tiles;
+    g.tail_splits = p.tail_splits;
+    g.tail_kbps = p.tail_kbps;
+    g.tail_ws = static_cast<float*>(ws);
+    const int tail = g.num_tiles - p.full_tiles;
+    g.num_tiles = p.full_tiles + tail * p.tail_splits;
+    MS_TRY(launch_umma(p.bn, a_mn, b_mn, LOAD_GEMM, tm, g, st, p.cl));
+    const int tile_rows = BM * p.cl;
+    const dim3 grid((unsigned)((tile_rows * (p.bn / 8) + 255) / 256), (unsigned)tail);
+    if (dt == MS_BF16)
+      tail_finalize_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(
+          static_cast<const float*>(ws), static_cast<__nv_bfloat16*>(out), ldc, (int)rows,
+          (int)cols, g.m_blocks, g.n_blocks, g.n_fastest, p.full_tiles, p.tail_splits, tile_rows,
+          p.bn);
+    else
+      tail_finalize_kernel<__half><<<grid, 256, 0, st>>>(
+          static_cast<const float*>(ws), static_cast<__half*>(out), ldc, (int)rows, (int)cols,
+          g.m_blocks, g.n_blocks, g.n_fastest, p.full_tiles, p.tail_splits, tile_rows, p.bn);
+    count_launch();
+    return launch_status("tail_finalize_kernel");
+  }
   return launch_umma(p.bn, a_mn, b_mn, LOAD_GEMM, tm, g, st, p.cl);
 }
 

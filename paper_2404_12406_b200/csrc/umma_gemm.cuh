@@ -107,6 +107,15 @@ struct GemmArgs {
   int num_tiles;
   int ab_fmt;        // 1 = bf16, 0 = fp16
   int tma_store;     // 1: epilogue stages 32x32 chunks in smem and stores them by TMA
+  // GEMM tail split: tiles [full_tiles, tiles) -- those of the last, partial wave
+  // -- run as tail_splits K-slices of tail_kbps k-blocks each; every slice stores
+  // its fp32 partial tile densely in tail_ws ([unit][CL*BM][BN]) and a finalize
+  // pass sums them (tail_splits = 0: off)
+  int full_tiles, tail_splits, tail_kbps;
+  float* tail_ws;
+  // GEMM raster order: 0 = M-blocks fastest (concurrent tiles share B), 1 =
+  // N-blocks fastest (they share A: A streams from HBM once when B fits in L2)
+  int n_fastest;
   ConvShape cv;
   int nphases;
   PhaseInfo phase[4];
@@ -127,6 +136,7 @@ struct TileInfo {
   int phase;         // dgrad: stride phase
   int tap;           // wgrad: kernel tap r*S+s
   int nsub;          // accumulations in this tile (BAND: dY rows; otherwise 1)
+  int unit;          // GEMM tail split: slice index (>= 0) of a tail tile, else -1
 };
 
 __device__ __forceinline__ int floor_div(int a, int b) {
@@ -139,6 +149,7 @@ __device__ __forceinline__ TileInfo decode_tile(const GemmArgs& g, int t, int cr
   ti.phase = 0;
   ti.tap = 0;
   ti.nsub = 1;
+  ti.unit = -1;
   if constexpr (MODE == LOAD_CONV_DGRAD) {
     int p = 0;
 #pragma unroll 1
@@ -165,11 +176,27 @@ __device__ __forceinline__ TileInfo decode_tile(const GemmArgs& g, int t, int cr
     ti.kb_end = g.k_blocks;
     ti.nsub = g.cv.band_sub;
   } else {
-    const int mb = t % g.m_blocks;  // CL == 2: m_blocks counts pairs of M tiles
-    int rest = t / g.m_blocks;
+    int split_t = 0;
+    if constexpr (MODE == LOAD_GEMM) {
+      if (g.tail_splits > 0 && t >= g.full_tiles) {  // K-slice of a last-wave tile
+        ti.unit = t - g.full_tiles;
+        split_t = ti.unit % g.tail_splits;
+        t = g.full_tiles + ti.unit / g.tail_splits;
+      }
+    }
+    int mb, rest;
+    if (MODE == LOAD_GEMM && g.n_fastest) {
+      ti.nb = t % g.n_blocks;
+      rest = t / g.n_blocks;
+      mb = rest % g.m_blocks;
+      rest /= g.m_blocks;
+    } else {
+      mb = t % g.m_blocks;  // CL == 2: m_blocks counts pairs of M tiles
+      rest = t / g.m_blocks;
+      ti.nb = rest % g.n_blocks;
+      rest /= g.n_blocks;
+    }
     ti.m0 = (CL * mb + crank) * BM;
-    ti.nb = rest % g.n_blocks;
-    rest /= g.n_blocks;
     if constexpr (MODE == LOAD_CONV_WGRAD) {
       ti.tap = rest % g.taps;
       const int split = rest / g.taps;
@@ -181,6 +208,9 @@ __device__ __forceinline__ TileInfo decode_tile(const GemmArgs& g, int t, int cr
     } else if constexpr (MODE == LOAD_CONV_FPROP_C8) {
       ti.kb_begin = 0;
       ti.kb_end = g.k_blocks;
+    } else if (ti.unit >= 0) {
+      ti.kb_begin = split_t * g.tail_kbps;
+      ti.kb_end = min(g.k_blocks, ti.kb_begin + g.tail_kbps);
     } else {
       const int split = rest;
       ti.kb_begin = split * g.kb_per_split;
@@ -609,15 +639,18 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
         const int acc = local & 1;
         const uint32_t use = static_cast<uint32_t>(local >> 1);
         ++local;
-        const bool tma_st = Cfg::CAN_TMA_STORE && g.tma_store;
+        const bool tail = ti.unit >= 0;  // fp32 partial of a K-sliced last-wave tile
+        const bool tma_st = Cfg::CAN_TMA_STORE && g.tma_store && !tail;
         const int ncols = g.N;
         // this warp drains columns [c_lo, c_lo + BN / EPI_H) of the accumulator
         constexpr int WCOLS = BN / Cfg::EPI_H;
         const int c_lo = (Cfg::EPI_H == 1 ? 0 : ((static_cast<int>(warp) - 2) >> 2)) * WCOLS;
         // 16-bit bias of this warp's columns, fetched before the accumulator wait
         // so its latency overlaps the main loop: lane j holds columns 8j .. 8j + 7
+        // (a K-sliced tile adds the bias in its first slice only)
         const bool bias_vec = e.bias != nullptr && e.bias_dtype != MS_F32 && (ncols & 7) == 0 &&
-                              (reinterpret_cast<uintptr_t>(e.bias) & 15) == 0;
+                              (reinterpret_cast<uintptr_t>(e.bias) & 15) == 0 &&
+                              ti.kb_begin == 0;
         uint4 bq = make_uint4(0u, 0u, 0u, 0u);
         if (bias_vec) {
           const int bc = n0 + c_lo + 8 * static_cast<int>(lane);
@@ -696,10 +729,20 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
                 v[q * 8 + 2 * h + 1] += hi;
               }
             }
-          } else if (e.bias != nullptr) {
+          } else if (e.bias != nullptr && ti.kb_begin == 0) {
 #pragma unroll
             for (int j = 0; j < 32; ++j)
               if (nc + j < ncols) v[j] += load_as_float(e.bias, e.bias_dtype, nc + j);
+          }
+          if (tail) {  // dense fp32 partial [unit][CL*BM][BN], summed by the finalize pass
+            if (valid) {
+              float* o = g.tail_ws +
+                         ((static_cast<int64_t>(ti.unit) * CL + crank) * BM + row) * BN + c;
+#pragma unroll
+              for (int j = 0; j < 32; j += 4)
+                *reinterpret_cast<float4*>(o + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+            }
+            continue;
           }
           if (e.bn.var != nullptr && !e.bn_post) {  // folded eval-BN: per-column affine
 #pragma unroll

@@ -180,6 +180,8 @@ LIN_CASES = [
     ((513,), 64, 8),          # N = 8
     ((2, 1024), 1024, 1536),  # CTA-pair tiles (M=256 MMA), several tiles per CTA
     ((1, 640), 384, 320),     # pair with a partial second M tile, N tail of a BN=64 pair
+    ((2, 1280), 1024, 2048),  # fwd: 80 pair tiles > 74 slots -> last wave K-split (tail)
+    ((2, 1280), 2048, 1024),  # dX: the same for the input-VJP (MN-major B)
 ]
 
 

@@ -31,12 +31,16 @@ for name in (sys.argv[1:] or list(SHAPES)):
     dx = torch.empty(M, K, device=dev, dtype=torch.bfloat16)
     dw = torch.empty(N, K, device=dev, dtype=torch.bfloat16)
     out = []
+    nb0 = max(L.ms_linear_workspace(M, N, K, 1, 0), 1)
+    nb1 = max(L.ms_linear_workspace(M, N, K, 1, 1), 1)
+    ws0 = torch.empty(nb0, dtype=torch.uint8, device=dev)
+    ws1 = torch.empty(nb1, dtype=torch.uint8, device=dev)
     for ps, fn_ours, fn_ref in (
-        ("fwd", lambda: L.ms_linear_fwd(M, N, K, 1, P(x), P(w), None, P(y), None, 0, st),
+        ("fwd", lambda: L.ms_linear_fwd(M, N, K, 1, P(x), P(w), None, P(y), P(ws0), nb0, st),
          lambda: torch.matmul(x, w.t(), out=y)),
-        ("fwd+bias", lambda: L.ms_linear_fwd(M, N, K, 1, P(x), P(w), P(b), P(y), None, 0, st),
+        ("fwd+bias", lambda: L.ms_linear_fwd(M, N, K, 1, P(x), P(w), P(b), P(y), P(ws0), nb0, st),
          lambda: torch.addmm(b, x, w.t(), out=y)),
-        ("dx", lambda: L.ms_linear_dx(M, N, K, 1, P(dy), P(w), P(dx), None, 0, st),
+        ("dx", lambda: L.ms_linear_dx(M, N, K, 1, P(dy), P(w), P(dx), P(ws1), nb1, st),
          lambda: torch.matmul(dy, w, out=dx)),
     ):
         ms = time_launches(fn_ours, 10, dev)
@@ -44,8 +48,8 @@ for name in (sys.argv[1:] or list(SHAPES)):
         fl = 2.0 * M * N * K
         out.append(f"{ps}: ours {ms:.3f} ms {fl / ms / 1e9:.0f} TF/s | cublas {ref:.3f} ms "
                    f"{fl / ref / 1e9:.0f} TF/s")
-    nbw = L.ms_linear_workspace(M, N, K, 1, 2)
-    ws = torch.empty(max(nbw, 1), dtype=torch.uint8, device=dev)
+    nbw = max(L.ms_linear_workspace(M, N, K, 1, 2), 1)
+    ws = torch.empty(nbw, dtype=torch.uint8, device=dev)
     ms = time_launches(lambda: L.ms_linear_dw(M, N, K, 1, P(x), P(dy), P(dw), P(ws), nbw, st),
                        10, dev)
     ref = time_launches(lambda: torch.matmul(dy.t(), x, out=dw), 10, dev)
