@@ -478,8 +478,14 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
     }
   } else if (warp == 1) {
     // ============================ MMA issuer ============================
-    if (lane == 0 && crank == 0) {
+    // The whole warp runs the loop, so the tile / stage arithmetic and the smem
+    // descriptors are warp-uniform (uniform registers), and an elect.sync lane
+    // issues.  (A lane-0-only loop makes the compiler wrap every tcgen05.mma in
+    // an ELECT / R2UR.BROADCAST waterfall -- as long as an N = 128 MMA itself.)
+    if (crank == 0) {
       const uint32_t idesc = make_idesc_f16(g.ab_fmt, BM * CL, BN, A_MN, B_MN);
+      const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem_base, 0);
+      const uint32_t ring_u = smem_u32(ring);
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
@@ -491,22 +497,26 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
           if constexpr (CL == 1) mbar_wait(smem_u32(&tempty_bar[acc]), (use & 1) ^ 1);
           else mbar_wait_cluster(smem_u32(&tempty_bar[acc]), (use & 1) ^ 1);
           tc_fence_after();
-          const uint32_t dcol = tmem_base + acc * BN;
+          const uint32_t dcol = tmem_u + acc * BN;
           if (ti.kb_end <= ti.kb_begin) {
             // empty reduction: the epilogue writes zeros
-            if constexpr (CL == 1) {
-              mbar_arrive(smem_u32(&tfull_bar[acc]));
-            } else {
-              for (int c = 0; c < CL; ++c)
-                mbar_arrive_cluster(mapa_shared(smem_u32(&tfull_bar[acc]), c));
+            if (elect_one()) {
+              if constexpr (CL == 1) {
+                mbar_arrive(smem_u32(&tfull_bar[acc]));
+              } else {
+                for (int c = 0; c < CL; ++c)
+                  mbar_arrive_cluster(mapa_shared(smem_u32(&tfull_bar[acc]), c));
+              }
             }
+            __syncwarp();
             continue;
           }
           for (int kb = ti.kb_begin; kb < ti.kb_end; ++kb) {
             mbar_wait(smem_u32(&full_bar[stage]), phase);
             tc_fence_after();
-            const uint32_t sA = smem_u32(ring + stage * Cfg::STAGE_BYTES);
+            const uint32_t sA = ring_u + stage * Cfg::STAGE_BYTES;
             const uint32_t sB = sA + Cfg::A_BYTES;
+            uint64_t ads[KMMA], bds[KMMA];
 #pragma unroll
             for (int k = 0; k < KMMA; ++k) {
               uint64_t ad, bd;
@@ -524,21 +534,34 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
                 bd = make_smem_desc(sB + k * 2048, 8192, 1024, LAYOUT_SWIZZLE_128B);
               else
                 bd = make_smem_desc(sB + k * 32, 16, 1024, LAYOUT_SWIZZLE_128B);
-              const uint32_t accum = (kb > ti.kb_begin || k > 0) ? 1u : 0u;
-              if constexpr (CL == 1) umma_f16(dcol, ad, bd, idesc, accum);
-              else umma_f16_cg2(dcol, ad, bd, idesc, accum);
+              ads[k] = ad;
+              bds[k] = bd;
             }
-            // frees the smem slot (in both CTAs of a pair) when the MMAs retire
-            if constexpr (CL > 1) umma_commit_cg2_mc(smem_u32(&empty_bar[stage]), (1u << CL) - 1);
-            else umma_commit(smem_u32(&empty_bar[stage]));
+            if (elect_one()) {
+#pragma unroll
+              for (int k = 0; k < KMMA; ++k) {
+                const uint32_t accum = (kb > ti.kb_begin || k > 0) ? 1u : 0u;
+                if constexpr (CL == 1) umma_f16(dcol, ads[k], bds[k], idesc, accum);
+                else umma_f16_cg2(dcol, ads[k], bds[k], idesc, accum);
+              }
+              // frees the smem slot (in both CTAs of a pair) when the MMAs retire
+              if constexpr (CL > 1)
+                umma_commit_cg2_mc(smem_u32(&empty_bar[stage]), (1u << CL) - 1);
+              else
+                umma_commit(smem_u32(&empty_bar[stage]));
+            }
+            __syncwarp();
             if (++stage == STAGES) {
               stage = 0;
               phase ^= 1;
             }
           }
           // accumulator ready for the epilogue (of both CTAs of a pair)
-          if constexpr (CL > 1) umma_commit_cg2_mc(smem_u32(&tfull_bar[acc]), (1u << CL) - 1);
-          else umma_commit(smem_u32(&tfull_bar[acc]));
+          if (elect_one()) {
+            if constexpr (CL > 1) umma_commit_cg2_mc(smem_u32(&tfull_bar[acc]), (1u << CL) - 1);
+            else umma_commit(smem_u32(&tfull_bar[acc]));
+          }
+          __syncwarp();
         }
       }
     }
