@@ -102,10 +102,13 @@ __global__ void __launch_bounds__(H3_THREADS, 1)
 
   if (warp == 0) {
     // ============================ TMA producer ============================
-    if (lane == 0) {
+    {  // whole warp (uniform coordinates), an elect.sync lane issues
       const uint32_t bb = smem_u32(b_bar);
-      mbar_arrive_expect_tx(bb, H3_B);
-      for (int t = 0; t < 9; ++t) tma_load_2d(smem_u32(sB + t * 8192), &tma_w, bb, 0, t * H3_N);
+      if (elect_one()) {
+        mbar_arrive_expect_tx(bb, H3_B);
+        for (int t = 0; t < 9; ++t) tma_load_2d(smem_u32(sB + t * 8192), &tma_w, bb, 0, t * H3_N);
+      }
+      __syncwarp();
       int stage = 0;
       uint32_t phase = 0;
       for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
@@ -114,10 +117,13 @@ __global__ void __launch_bounds__(H3_THREADS, 1)
         mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
         const uint32_t fb = smem_u32(&full_bar[stage]);
         const uint32_t sh = smem_u32(ring + stage * H3_HALO);
-        mbar_arrive_expect_tx(fb, H3_HALO);
+        if (elect_one()) {
+          mbar_arrive_expect_tx(fb, H3_HALO);
 #pragma unroll
-        for (int rr = 0; rr < H3_ROWS + 2; ++rr)  // input rows i0-1 .. i0+2, pixels -1 .. 62
-          tma_load_4d(sh + rr * H3_P * 128, &tma_x, fb, 0, -1, i0 - 1 + rr, n);
+          for (int rr = 0; rr < H3_ROWS + 2; ++rr)  // input rows i0-1 .. i0+2, pixels -1 .. 62
+            tma_load_4d(sh + rr * H3_P * 128, &tma_x, fb, 0, -1, i0 - 1 + rr, n);
+        }
+        __syncwarp();
         if (++stage == H3_STAGES) {
           stage = 0;
           phase ^= 1;
@@ -126,8 +132,12 @@ __global__ void __launch_bounds__(H3_THREADS, 1)
     }
   } else if (warp == 1) {
     // ============================ MMA issuer ============================
-    if (lane == 0) {
+    // whole warp: descriptors in uniform registers; an elect.sync lane issues
+    // the 36 MMAs of a tile back to back (no per-MMA ELECT / R2UR waterfall)
+    {
       const uint32_t idesc = make_idesc_f16(a.dt == MS_BF16 ? 1 : 0, BM, H3_N, 0, 0);
+      const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem_base, 0);
+      const uint32_t ring_u = smem_u32(ring), sB_u = smem_u32(sB);
       mbar_wait(smem_u32(b_bar), 0);
       int stage = 0;
       uint32_t phase = 0;
@@ -137,22 +147,25 @@ __global__ void __launch_bounds__(H3_THREADS, 1)
         mbar_wait(smem_u32(&tempty_bar[acc]), ((local >> 1) & 1) ^ 1);
         mbar_wait(smem_u32(&full_bar[stage]), phase);
         tc_fence_after();
-        const uint32_t dcol = tmem_base + acc * H3_N;
-        const uint32_t sh = smem_u32(ring + stage * H3_HALO);
+        const uint32_t dcol = tmem_u + acc * H3_N;
+        const uint32_t sh = ring_u + stage * H3_HALO;
+        if (elect_one()) {
 #pragma unroll
-        for (int t = 0; t < 9; ++t) {
-          const int r = t / 3, s = t - (t / 3) * 3;
-          // output pixel m' = i*64 + j reads halo row (i + r)*64 + (j + s)
-          const uint32_t arow = sh + (r * H3_P + s) * 128;
-          const uint32_t brow = smem_u32(sB + t * 8192);
+          for (int t = 0; t < 9; ++t) {
+            const int r = t / 3, s = t - (t / 3) * 3;
+            // output pixel m' = i*64 + j reads halo row (i + r)*64 + (j + s)
+            const uint32_t arow = sh + (r * H3_P + s) * 128;
+            const uint32_t brow = sB_u + t * 8192;
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            umma_f16(dcol, desc_sw128_rows(arow + k * 32),
-                     make_smem_desc(brow + k * 32, 16, 1024, LAYOUT_SWIZZLE_128B), idesc,
-                     (t > 0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < 4; ++k)
+              umma_f16(dcol, desc_sw128_rows(arow + k * 32),
+                       make_smem_desc(brow + k * 32, 16, 1024, LAYOUT_SWIZZLE_128B), idesc,
+                       (t > 0 || k > 0) ? 1u : 0u);
+          }
+          umma_commit(smem_u32(&empty_bar[stage]));
+          umma_commit(smem_u32(&tfull_bar[acc]));
         }
-        umma_commit(smem_u32(&empty_bar[stage]));
-        umma_commit(smem_u32(&tfull_bar[acc]));
+        __syncwarp();
         if (++stage == H3_STAGES) {
           stage = 0;
           phase ^= 1;

@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
 
   if (warp == 0) {
     // ============================ TMA producer ============================
-    if (lane == 0) {
+    {  // whole warp: uniform tile / stage arithmetic; an elect.sync lane issues
       int stage = 0;
       uint32_t phase = 0;
       for (int t = t_first; t < g.num_tiles; t += t_step) {
@@ -367,6 +367,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
                                         : mapa_shared(smem_u32(&full_bar[stage]), 0);
             const uint32_t sA = smem_u32(ring + stage * Cfg::STAGE_BYTES);
             const uint32_t sB = sA + Cfg::A_BYTES;
+            if (elect_one()) {
             if (crank == 0)
               mbar_arrive_expect_tx(smem_u32(&full_bar[stage]), CL * Cfg::STAGE_BYTES);
             if constexpr (MODE == LOAD_GEMM) {
@@ -468,6 +469,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
                 tma_load_im2col_4d(sB + j * 8192, &tm.b, fb, n0 + 64 * j, ow * g.cv.sw - g.cv.pw,
                                    oh * g.cv.sh - g.cv.ph, pn, (uint16_t)s, (uint16_t)r);
             }
+            }
+            __syncwarp();
             if (++stage == STAGES) {
               stage = 0;
               phase ^= 1;
