@@ -94,11 +94,14 @@ __global__ void __launch_bounds__(SD_THREADS, 1)
 
   if (warp == 0) {
     // ============================ TMA producer ============================
-    if (lane == 0) {
+    {  // whole warp (uniform operands), an elect.sync lane issues
       const uint32_t bb = smem_u32(b_bar);
-      mbar_arrive_expect_tx(bb, a.kblocks * SD_B_KB_BYTES);
-      for (int kb = 0; kb < a.kblocks; ++kb)
-        tma_load_2d(smem_u32(sB + kb * SD_B_KB_BYTES), &tma_w, bb, kb * 64, 0);
+      if (elect_one()) {
+        mbar_arrive_expect_tx(bb, a.kblocks * SD_B_KB_BYTES);
+        for (int kb = 0; kb < a.kblocks; ++kb)
+          tma_load_2d(smem_u32(sB + kb * SD_B_KB_BYTES), &tma_w, bb, kb * 64, 0);
+      }
+      __syncwarp();
       int stage = 0;
       uint32_t phase = 0;
       for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
@@ -109,10 +112,13 @@ __global__ void __launch_bounds__(SD_THREADS, 1)
             mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
             const uint32_t fb = smem_u32(&full_bar[stage]);
             const uint32_t sA = smem_u32(ring + stage * SD_A_BYTES);
-            mbar_arrive_expect_tx(fb, SD_A_BYTES);
+            if (elect_one()) {
+              mbar_arrive_expect_tx(fb, SD_A_BYTES);
 #pragma unroll
-            for (int w = 0; w < SD_SEGS; ++w)
-              tma_load_4d(sA + w * 4096, &tma_dy, fb, kb * 64, SD_SEG * w - 1, oh, n);
+              for (int w = 0; w < SD_SEGS; ++w)
+                tma_load_4d(sA + w * 4096, &tma_dy, fb, kb * 64, SD_SEG * w - 1, oh, n);
+            }
+            __syncwarp();
             if (++stage == SD_STAGES) {
               stage = 0;
               phase ^= 1;
@@ -123,8 +129,9 @@ __global__ void __launch_bounds__(SD_THREADS, 1)
     }
   } else if (warp == 1) {
     // ============================ MMA issuer ============================
-    if (lane == 0) {
+    {  // whole warp: descriptors in uniform registers; an elect.sync lane issues
       const uint32_t idesc = make_idesc_f16(a.dt == MS_BF16 ? 1 : 0, BM, SD_N, 0, 0);
+      const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem_base, 0);
       mbar_wait(smem_u32(b_bar), 0);
       int stage = 0;
       uint32_t phase = 0;
@@ -134,25 +141,29 @@ __global__ void __launch_bounds__(SD_THREADS, 1)
           const int acc = local & 1;
           mbar_wait(smem_u32(&tempty_bar[acc]), ((local >> 1) & 1) ^ 1);
           tc_fence_after();
-          const uint32_t dcol = tmem_base + acc * SD_N;
+          const uint32_t dcol = tmem_u + acc * SD_N;
           for (int kb = 0; kb < a.kblocks; ++kb) {
             mbar_wait(smem_u32(&full_bar[stage]), phase);
             tc_fence_after();
             const uint32_t sA = smem_u32(ring + stage * SD_A_BYTES);
             const uint32_t sBk = smem_u32(sB + kb * SD_B_KB_BYTES);
+            if (elect_one()) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const uint64_t ad = make_smem_desc(sA + k * 32, 16, 1024, LAYOUT_SWIZZLE_128B);
-              const uint64_t bd = make_smem_desc(sBk + k * 32, 16, 1024, LAYOUT_SWIZZLE_128B);
-              umma_f16(dcol, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+              for (int k = 0; k < 4; ++k) {
+                const uint64_t ad = make_smem_desc(sA + k * 32, 16, 1024, LAYOUT_SWIZZLE_128B);
+                const uint64_t bd = make_smem_desc(sBk + k * 32, 16, 1024, LAYOUT_SWIZZLE_128B);
+                umma_f16(dcol, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+              }
+              umma_commit(smem_u32(&empty_bar[stage]));
             }
-            umma_commit(smem_u32(&empty_bar[stage]));
+            __syncwarp();
             if (++stage == SD_STAGES) {
               stage = 0;
               phase ^= 1;
             }
           }
-          umma_commit(smem_u32(&tfull_bar[acc]));
+          if (elect_one()) umma_commit(smem_u32(&tfull_bar[acc]));
+          __syncwarp();
         }
       }
     }
@@ -377,9 +388,12 @@ __global__ void __launch_bounds__(SF_THREADS, 1)
 
   if (warp == 0) {
     // ============================ bulk-copy producer ============================
-    if (lane == 0) {
-      mbar_arrive_expect_tx(smem_u32(b_bar), b_bytes);
-      bulk_g2s(smem_u32(sB), a.wb, b_bytes, smem_u32(b_bar));
+    {  // whole warp (uniform operands), an elect.sync lane issues
+      if (elect_one()) {
+        mbar_arrive_expect_tx(smem_u32(b_bar), b_bytes);
+        bulk_g2s(smem_u32(sB), a.wb, b_bytes, smem_u32(b_bar));
+      }
+      __syncwarp();
       int stage = 0;
       uint32_t phase = 0;
       for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
@@ -391,15 +405,18 @@ __global__ void __launch_bounds__(SF_THREADS, 1)
           const int h = 2 * oh - 3 + r;
           rows += (h >= 0 && h < a.H) ? 1 : 0;
         }
-        mbar_arrive_expect_tx(fb, rows * row_bytes);
-        for (int r = 0; r < SF_R; ++r) {
-          const int h = 2 * oh - 3 + r;
-          if (h >= 0 && h < a.H) {
-            const uint8_t* src = static_cast<const uint8_t*>(a.xp) +
-                                 (static_cast<int64_t>(n) * a.H + h) * row_bytes;
-            bulk_g2s(smem_u32(ring + stage * SF_STAGE + r * SF_SLOT), src, row_bytes, fb);
+        if (elect_one()) {
+          mbar_arrive_expect_tx(fb, rows * row_bytes);
+          for (int r = 0; r < SF_R; ++r) {
+            const int h = 2 * oh - 3 + r;
+            if (h >= 0 && h < a.H) {
+              const uint8_t* src = static_cast<const uint8_t*>(a.xp) +
+                                   (static_cast<int64_t>(n) * a.H + h) * row_bytes;
+              bulk_g2s(smem_u32(ring + stage * SF_STAGE + r * SF_SLOT), src, row_bytes, fb);
+            }
           }
         }
+        __syncwarp();
         if (++stage == SF_STAGES) {
           stage = 0;
           phase ^= 1;
@@ -408,8 +425,9 @@ __global__ void __launch_bounds__(SF_THREADS, 1)
     }
   } else if (warp == 1) {
     // ============================ MMA issuer ============================
-    if (lane == 0) {
+    {  // whole warp: descriptors in uniform registers; an elect.sync lane issues
       const uint32_t idesc = make_idesc_f16(a.dt == MS_BF16 ? 1 : 0, BM, a.K, 0, 0);
+      const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem_base, 0);
       mbar_wait(smem_u32(b_bar), 0);
       int stage = 0;
       uint32_t phase = 0;
@@ -420,9 +438,9 @@ __global__ void __launch_bounds__(SF_THREADS, 1)
         mbar_wait(smem_u32(&tempty_bar[acc]), ((local >> 1) & 1) ^ 1);
         mbar_wait(smem_u32(&full_bar[stage]), phase);
         tc_fence_after();
-        const uint32_t dcol = tmem_base + acc * a.K;
-        bool first = true;
-#pragma unroll 1
+        const uint32_t dcol = tmem_u + acc * a.K;
+        uint64_t ads[2 * SF_R], bds[2 * SF_R];
+#pragma unroll
         for (int r = 0; r < SF_R; ++r) {
           const int h = 2 * oh - 3 + r;
           const uint32_t arow = (h >= 0 && h < a.H)
@@ -431,16 +449,19 @@ __global__ void __launch_bounds__(SF_THREADS, 1)
 #pragma unroll
           for (int half = 0; half < 2; ++half) {
             // A: rows 16 B apart, K core matrices 16 B apart (overlapping windows)
-            const uint64_t ad = make_smem_desc(arow + half * 32, 16, 128, LAYOUT_SWIZZLE_NONE);
+            ads[2 * r + half] = make_smem_desc(arow + half * 32, 16, 128, LAYOUT_SWIZZLE_NONE);
             // B: [r][kg][K][8]: K core matrices 16*K B apart, 8-row groups 128 B apart
-            const uint64_t bd = make_smem_desc(smem_u32(sB) + (r * 4 + 2 * half) * a.K * 16,
+            bds[2 * r + half] = make_smem_desc(smem_u32(sB) + (r * 4 + 2 * half) * a.K * 16,
                                                a.K * 16, 128, LAYOUT_SWIZZLE_NONE);
-            umma_f16(dcol, ad, bd, idesc, first ? 0u : 1u);
-            first = false;
           }
         }
-        umma_commit(smem_u32(&empty_bar[stage]));
-        umma_commit(smem_u32(&tfull_bar[acc]));
+        if (elect_one()) {
+#pragma unroll
+          for (int i = 0; i < 2 * SF_R; ++i) umma_f16(dcol, ads[i], bds[i], idesc, i ? 1u : 0u);
+          umma_commit(smem_u32(&empty_bar[stage]));
+          umma_commit(smem_u32(&tfull_bar[acc]));
+        }
+        __syncwarp();
         if (++stage == SF_STAGES) {
           stage = 0;
           phase ^= 1;
