@@ -37,11 +37,26 @@ def _dtype_code(t: torch.Tensor) -> int:
 
 
 def _ptr(t):
-    return None if t is None else ctypes.c_void_p(t.data_ptr())
+    # plain ints: the ctypes signatures declare c_void_p, which converts them
+    return None if t is None else t.data_ptr()
 
 
 def _stream(dev: torch.device):
-    return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+    # the raw cudaStream_t of the current stream, without a torch.cuda.Stream object
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
+    return torch._C._cuda_getCurrentRawStream(idx)
+
+
+_LIN_WS: dict = {}
+
+
+def _linear_ws(L, M, N, K, dt, pass_):
+    """ms_linear_workspace, memoised per shape (the plan is a pure function of it)."""
+    key = (M, N, K, dt, pass_)
+    nb = _LIN_WS.get(key)
+    if nb is None:
+        nb = _LIN_WS[key] = int(L.ms_linear_workspace(M, N, K, dt, pass_))
+    return nb
 
 
 def _workspace(nbytes: int, dev: torch.device):
@@ -98,7 +113,7 @@ class _LinearFn(torch.autograd.Function):
         y = torch.empty(out_shape, dtype=x.dtype, device=x.device)
         L = _lib.lib()
         dt = _dtype_code(x)
-        ws, nb = _workspace(L.ms_linear_workspace(M, N, K, dt, 0), x.device)
+        ws, nb = _workspace(_linear_ws(L, M, N, K, dt, 0), x.device)
         _lib.check(L.ms_linear_fwd(M, N, K, dt, _ptr(x2), _ptr(w), _ptr(b), _ptr(y), _ptr(ws), nb,
                                    _stream(x.device)), "ms_linear_fwd")
         return y
@@ -127,7 +142,7 @@ class _LinearFn(torch.autograd.Function):
             w = _need(w, "w", "linear dX")
             K = w.shape[1]
             dx = torch.empty(ctx.x_shape, dtype=g2.dtype, device=g2.device)
-            ws, nb = _workspace(L.ms_linear_workspace(M, N, K, dt, 1), g2.device)
+            ws, nb = _workspace(_linear_ws(L, M, N, K, dt, 1), g2.device)
             _lib.check(L.ms_linear_dx(M, N, K, dt, _ptr(g2), _ptr(w.contiguous()), _ptr(dx),
                                       _ptr(ws), nb, st), "ms_linear_dx")
         if need_w:
@@ -135,7 +150,7 @@ class _LinearFn(torch.autograd.Function):
             K = x.shape[-1]
             x2 = x.reshape(-1, K).contiguous()
             dw = torch.empty((N, K), dtype=g2.dtype, device=g2.device)
-            ws, nb = _workspace(L.ms_linear_workspace(M, N, K, dt, 2), g2.device)
+            ws, nb = _workspace(_linear_ws(L, M, N, K, dt, 2), g2.device)
             _lib.check(L.ms_linear_dw(M, N, K, dt, _ptr(x2), _ptr(g2), _ptr(dw), _ptr(ws), nb, st),
                        "ms_linear_dw")
         if need_b:
