@@ -26,9 +26,9 @@ constexpr int H3_N = 64;                    // output channels (UMMA N)
 constexpr int H3_P = 64;                    // halo row pitch in pixels
 constexpr int H3_ROWS = 2;                  // output rows per tile
 constexpr int H3_HALO = (H3_ROWS + 2) * H3_P * 128;  // 32 KB per stage
-constexpr int H3_STAGES = 4;
+constexpr int H3_STAGES = 3;
 constexpr int H3_B = 9 * H3_N * 128;        // 9 taps x [64 n][64 c]
-constexpr int H3_EPI = 4;
+constexpr int H3_EPI = 8;                   // 2 per TMEM lane quarter, 32 channels each
 constexpr int H3_THREADS = 64 + 32 * H3_EPI;
 constexpr int H3_STG = H3_EPI * 2 * 2048;   // TMA-store staging, 2 x (32 px x 32 ch) per warp
 constexpr int H3_SMEM = H3_B + H3_STAGES * H3_HALO + H3_STG + 1024 + 256;
@@ -174,19 +174,20 @@ __global__ void __launch_bounds__(H3_THREADS, 1)
     }
   } else {
     // ============================ epilogue ============================
+    // 8 warps: warp w drains TMEM lane quarter w % 4 (its pixels) and channel half
+    // (w - 2) / 4 -- twice the warps of one per quarter, so the fused epilogue
+    // (BN affine, residual / addend, masks) keeps up with the 36-MMA tiles
     const int quarter = static_cast<int>(warp & 3);
     const int ew = static_cast<int>(warp) - 2;
+    const int c0 = (ew >> 2) * 32;         // this warp's 32 output channels
     const int rw = static_cast<int>(lane);
     const int ti = quarter >> 1;           // output row within the tile
     const int j0 = (quarter & 1) * 32;     // first pixel of this warp's 32
     const int j = j0 + rw;
     int local = 0;
     uint32_t nst = 0;
-    float bs0 = 1.f, bt0 = 0.f, bs1 = 1.f, bt1 = 0.f;  // eval-BN affine of channels lane, 32 + lane
-    if (a.bn.var) {
-      bn_fold(a.bn, rw, bs0, bt0);
-      bn_fold(a.bn, 32 + rw, bs1, bt1);
-    }
+    float bs0 = 1.f, bt0 = 0.f;  // eval-BN affine of channel c0 + lane
+    if (a.bn.var) bn_fold(a.bn, c0 + rw, bs0, bt0);
     for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++local) {
       const int n = u / a.tiles_per_img;
       const int oh = (u - n * a.tiles_per_img) * H3_ROWS + ti;
@@ -197,29 +198,24 @@ __global__ void __launch_bounds__(H3_THREADS, 1)
       mbar_wait(smem_u32(&tfull_bar[buf]), (local >> 1) & 1);
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((static_cast<uint32_t>(quarter) * 32u) << 16) + buf * H3_N;
-      uint32_t v0[32], v1[32];
-      tmem_ld_32x32b_x32(taddr, v0);
-      tmem_ld_32x32b_x32(taddr + 32, v1);
+      uint32_t v0[32];
+      tmem_ld_32x32b_x32(taddr + c0, v0);
       tmem_ld_wait_regs(v0);
-      tmem_ld_wait_regs(v1);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&tempty_bar[buf]));
-#pragma unroll
-      for (int cc = 0; cc < 2; ++cc) {
-        const int c0 = cc * 32;
+      {
         float f[32];
 #pragma unroll
-        for (int q = 0; q < 32; ++q) f[q] = __uint_as_float(cc == 0 ? v0[q] : v1[q]);
+        for (int q = 0; q < 32; ++q) f[q] = __uint_as_float(v0[q]);
         if (a.bias) {
 #pragma unroll
           for (int q = 0; q < 32; ++q) f[q] += IO<T>::ld(static_cast<const T*>(a.bias) + c0 + q);
         }
         if (a.bn.var && !a.bn_post) {  // lane j holds channel c0 + j's folded BN affine
-          const float s_l = cc == 0 ? bs0 : bs1, t_l = cc == 0 ? bt0 : bt1;
 #pragma unroll
           for (int q = 0; q < 32; ++q)
-            f[q] = f[q] * __shfl_sync(0xffffffffu, s_l, q) + __shfl_sync(0xffffffffu, t_l, q);
+            f[q] = f[q] * __shfl_sync(0xffffffffu, bs0, q) + __shfl_sync(0xffffffffu, bt0, q);
         }
         if (a.resid && valid) {
           const uint4* r4 = reinterpret_cast<const uint4*>(static_cast<const T*>(a.resid) +
@@ -240,9 +236,8 @@ __global__ void __launch_bounds__(H3_THREADS, 1)
           for (int q = 0; q < 32; ++q) f[q] = ((kb >> q) & 1u) ? f[q] : 0.f;
         }
         if (a.bn_post) {
-          const float s_l = cc == 0 ? bs0 : bs1;
 #pragma unroll
-          for (int q = 0; q < 32; ++q) f[q] *= __shfl_sync(0xffffffffu, s_l, q);
+          for (int q = 0; q < 32; ++q) f[q] *= __shfl_sync(0xffffffffu, bs0, q);
         }
         if (a.relu) {
           uint32_t bits = 0;
