@@ -232,8 +232,15 @@ constexpr int pow2_cols(int c) {
 template <int BN, int A_MN, int B_MN, int MODE, int CL = 1>
 struct GemmCfg {
   static constexpr int KBYTES = MODE == LOAD_CONV_FPROP_ROWSEG ? 64 : 128;  // K bytes per row
-  static constexpr int A_BYTES = BM * KBYTES;
-  static constexpr int B_BYTES = BN / CL * KBYTES;  // this CTA's share of the B tile
+  // k-blocks per pipeline stage: 2 for the N = 128 CTA-pair convs, whose
+  // 4-MMA k-blocks (64 clk each) are too short to amortise one barrier round
+  // trip and one TMA issue per k-block
+  static constexpr int KS = (CL == 2 && BN == 128 &&
+                             (MODE == LOAD_CONV_FPROP || MODE == LOAD_CONV_DGRAD)) ? 2 : 1;
+  static constexpr int A_SUB = BM * KBYTES;          // one k-block of A
+  static constexpr int B_SUB = BN / CL * KBYTES;     // this CTA's share of one k-block of B
+  static constexpr int A_BYTES = KS * A_SUB;
+  static constexpr int B_BYTES = KS * B_SUB;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int EXTRA = MODE == LOAD_CONV_DGRAD_BAND ? BAND_WINDOW_BYTES : 0;
   // TMA-store staging: 4 epilogue warps x 4 buffers x (32 rows x 64 B)
@@ -360,16 +367,15 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
           ch = band_first_row(g.cv, b * g.cv.band_h);  // first dY row of the band
         }
         for (int sub = 0; sub < ti.nsub; ++sub) {
-          for (int kb = ti.kb_begin; kb < ti.kb_end; ++kb) {
+          for (int kb0 = ti.kb_begin; kb0 < ti.kb_end; kb0 += Cfg::KS) {
+            const int nkb = min(Cfg::KS, ti.kb_end - kb0);
             mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
             // CL = 2: both CTAs' loads complete on the even CTA's full barrier
             const uint32_t fb = CL == 1 ? smem_u32(&full_bar[stage])
                                         : mapa_shared(smem_u32(&full_bar[stage]), 0);
-            const uint32_t sA = smem_u32(ring + stage * Cfg::STAGE_BYTES);
-            const uint32_t sB = sA + Cfg::A_BYTES;
-            if (elect_one()) {
-            if (crank == 0)
-              mbar_arrive_expect_tx(smem_u32(&full_bar[stage]), CL * Cfg::STAGE_BYTES);
+            const uint32_t sA0 = smem_u32(ring + stage * Cfg::STAGE_BYTES);
+            // one k-block's TMA loads into (sA, sB)
+            auto issue = [&](const int kb, const uint32_t sA, const uint32_t sB) {
             if constexpr (MODE == LOAD_GEMM) {
               const int k0 = kb * BK;
               if constexpr (CL > 1) {
@@ -469,6 +475,13 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
                 tma_load_im2col_4d(sB + j * 8192, &tm.b, fb, n0 + 64 * j, ow * g.cv.sw - g.cv.pw,
                                    oh * g.cv.sh - g.cv.ph, pn, (uint16_t)s, (uint16_t)r);
             }
+            };
+            if (elect_one()) {
+              if (crank == 0)
+                mbar_arrive_expect_tx(smem_u32(&full_bar[stage]),
+                                      CL * nkb * (Cfg::A_SUB + Cfg::B_SUB));
+              for (int j = 0; j < nkb; ++j)
+                issue(kb0 + j, sA0 + j * Cfg::A_SUB, sA0 + Cfg::A_BYTES + j * Cfg::B_SUB);
             }
             __syncwarp();
             if (++stage == STAGES) {
@@ -514,14 +527,17 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
             __syncwarp();
             continue;
           }
-          for (int kb = ti.kb_begin; kb < ti.kb_end; ++kb) {
+          for (int kb0 = ti.kb_begin; kb0 < ti.kb_end; kb0 += Cfg::KS) {
+            const int nkb = min(Cfg::KS, ti.kb_end - kb0);
             mbar_wait(smem_u32(&full_bar[stage]), phase);
             tc_fence_after();
-            const uint32_t sA = ring_u + stage * Cfg::STAGE_BYTES;
-            const uint32_t sB = sA + Cfg::A_BYTES;
-            uint64_t ads[KMMA], bds[KMMA];
+            uint64_t ads[Cfg::KS * KMMA], bds[Cfg::KS * KMMA];
 #pragma unroll
-            for (int k = 0; k < KMMA; ++k) {
+            for (int kk = 0; kk < Cfg::KS * KMMA; ++kk) {
+              const int k = kk % KMMA, jsub = kk / KMMA;
+              const uint32_t sA = ring_u + stage * Cfg::STAGE_BYTES + jsub * Cfg::A_SUB;
+              const uint32_t sB = ring_u + stage * Cfg::STAGE_BYTES + Cfg::A_BYTES +
+                                  jsub * Cfg::B_SUB;
               uint64_t ad, bd;
               if constexpr (MODE == LOAD_CONV_FPROP_C8)  // core matrices 8 rows x 16 B
                 ad = make_smem_desc(sA + k * 4096, 2048, 128, LAYOUT_SWIZZLE_NONE);
@@ -537,15 +553,17 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
                 bd = make_smem_desc(sB + k * 2048, 8192, 1024, LAYOUT_SWIZZLE_128B);
               else
                 bd = make_smem_desc(sB + k * 32, 16, 1024, LAYOUT_SWIZZLE_128B);
-              ads[k] = ad;
-              bds[k] = bd;
+              ads[kk] = ad;
+              bds[kk] = bd;
             }
             if (elect_one()) {
 #pragma unroll
-              for (int k = 0; k < KMMA; ++k) {
-                const uint32_t accum = (kb > ti.kb_begin || k > 0) ? 1u : 0u;
-                if constexpr (CL == 1) umma_f16(dcol, ads[k], bds[k], idesc, accum);
-                else umma_f16_cg2(dcol, ads[k], bds[k], idesc, accum);
+              for (int kk = 0; kk < Cfg::KS * KMMA; ++kk) {
+                if (kk / KMMA < nkb) {
+                  const uint32_t accum = (kb0 > ti.kb_begin || kk > 0) ? 1u : 0u;
+                  if constexpr (CL == 1) umma_f16(dcol, ads[kk], bds[kk], idesc, accum);
+                  else umma_f16_cg2(dcol, ads[kk], bds[kk], idesc, accum);
+                }
               }
               // frees the smem slot (in both CTAs of a pair) when the MMAs retire
               if constexpr (CL > 1)
