@@ -235,8 +235,9 @@ struct GemmCfg {
   // k-blocks per pipeline stage: 2 for the N = 128 CTA-pair convs, whose
   // 4-MMA k-blocks (64 clk each) are too short to amortise one barrier round
   // trip and one TMA issue per k-block
-  static constexpr int KS = (CL == 2 && BN == 128 &&
-                             (MODE == LOAD_CONV_FPROP || MODE == LOAD_CONV_DGRAD)) ? 2 : 1;
+  static constexpr int KS = (((CL == 2 && BN == 128) || (CL == 1 && BN == 64)) &&
+                             (MODE == LOAD_CONV_FPROP || MODE == LOAD_CONV_DGRAD || MODE == LOAD_GEMM))
+                                ? 2 : 1;
   static constexpr int A_SUB = BM * KBYTES;          // one k-block of A
   static constexpr int B_SUB = BN / CL * KBYTES;     // this CTA's share of one k-block of B
   static constexpr int A_BYTES = KS * A_SUB;
