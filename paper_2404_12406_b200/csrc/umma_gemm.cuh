@@ -232,10 +232,11 @@ constexpr int pow2_cols(int c) {
 template <int BN, int A_MN, int B_MN, int MODE, int CL = 1>
 struct GemmCfg {
   static constexpr int KBYTES = MODE == LOAD_CONV_FPROP_ROWSEG ? 64 : 128;  // K bytes per row
-  // k-blocks per pipeline stage: 2 for the N = 128 CTA-pair convs, whose
-  // 4-MMA k-blocks (64 clk each) are too short to amortise one barrier round
-  // trip and one TMA issue per k-block
-  static constexpr int KS = (((CL == 2 && BN == 128) || (CL == 1 && BN == 64)) &&
+  // k-blocks per pipeline stage: 2 for CTA pairs and N = 64 single tiles, whose
+  // 4-MMA k-blocks (64 clk per MMA at N = 128) are too short to amortise one
+  // barrier round trip and one TMA batch per k-block (layer-2 conv 0.081 ->
+  // 0.066 ms); wgrad / stem / C8 modes keep 1
+  static constexpr int KS = (((CL == 2 && BN <= 256) || (CL == 1 && BN == 64)) &&
                              (MODE == LOAD_CONV_FPROP || MODE == LOAD_CONV_DGRAD || MODE == LOAD_GEMM))
                                 ? 2 : 1;
   static constexpr int A_SUB = BM * KBYTES;          // one k-block of A
