@@ -58,8 +58,9 @@ struct ConvPlan {
   int cpad = 0;         // fwd: per-tap weight pitch (multiple of 64)
   int kpad = 0;         // dx: per-tap pitch of the repacked weight
   bool c8 = false;      // fwd: 8-channel im2col variant
-  bool rowseg = false;  // fwd: <=4-channel stride-2 stem, row-segment loads
-  int xw_pad = 0;       // rowseg: padded width of the 4-channel activation copy
+  bool rowseg = false;  // fwd: <=4-ch stride-2 / <=8-ch stride-1 row-segment loads
+  int xw_pad = 0;       // rowseg: padded width of the channel-padded activation copy
+  int cpx = 4;          // rowseg: channels per padded pixel (16 B between windows)
   bool band = false;    // dx: <8-channel input gradient (the stem), band col2im
   bool stem = false;    // dx: the 3-channel 7x7/2 stem, register col2im (stem_dgrad.cu)
   bool halo3 = false;   // fwd / dx: 3x3/1/1 64->64 halo-tiled kernel (conv3x3.cu)
@@ -76,8 +77,19 @@ bool tc_ok(const ms_conv_desc* d) {
 // Row-segment stem forward: one A row = S*4 consecutive elements of a
 // 4-channel input row; consecutive output pixels start sw*8 bytes apart, which
 // TMA needs to be a multiple of 16 (stride 2).  Checked once against the driver.
+// row-segment loads apply when consecutive output pixels' input windows start
+// 16 bytes apart in a channel-padded copy: <= 4 channels at stride 2 (the 7x7
+// stem) or <= 8 channels at stride 1 (VGG's first 3x3), one kernel row <= 32
+// elements (64 bytes)
+int rowseg_cpx(const ms_conv_desc* d) {
+  if (d->c <= 4 && d->stride_w == 2 && d->s * 4 <= 32) return 4;
+  if (d->c <= 8 && d->stride_w == 1 && d->s * 8 <= 32) return 8;
+  return 0;
+}
+
 bool rowseg_ok(const ms_conv_desc* d, const ConvDims& c) {
-  if (!(d->c <= 4 && d->stride_w == 2 && d->s * 4 <= 32 && c.ow <= BM)) return false;
+  (void)c;
+  if (!rowseg_cpx(d)) return false;
   static int cached = -1;
   if (cached < 0) {
     CUtensorMap m;
@@ -111,8 +123,11 @@ ConvPlan plan(const ms_conv_desc* d, int pass, bool dx_bias = false) {
     }
     if (rowseg_ok(d, c)) {
       p.rowseg = true;
-      p.xw_pad = (int)std::max<int64_t>(d->w + 2 * d->pad_w, (int64_t)(c.ow - 1) * 2 + 8);
-      p.ws_pad = align256(es * (size_t)d->n * d->h * p.xw_pad * 4);
+      p.cpx = rowseg_cpx(d);
+      // the last window reads 64 bytes = 64 / (2 cpx) pixels from its start
+      p.xw_pad = (int)std::max<int64_t>(d->w + 2 * d->pad_w,
+                                        (int64_t)(c.ow - 1) * d->stride_w + 32 / p.cpx);
+      p.ws_pad = align256(es * (size_t)d->n * d->h * p.xw_pad * p.cpx);
       p.ws_w = align256(es * (size_t)d->k * d->r * 32);
       p.ws = p.ws_pad + p.ws_w;
       return p;
@@ -218,28 +233,30 @@ ms_status fwd_rowseg(const ms_conv_desc* d, const ConvPlan& p, const void* x, co
   uint8_t* wsb = static_cast<uint8_t*>(ws);
   void* x4 = wsb;
   void* wr = wsb + p.ws_pad;
-  MS_TRY(pad_rowseg(dt, c.n, c.h, c.w, c.c, c.pw, p.xw_pad, x, x4, st));
+  MS_TRY(pad_rowseg(dt, c.n, c.h, c.w, c.c, c.pw, p.xw_pad, p.cpx, x, x4, st));
   static const bool env_im2col = getenv("MS_STEM_IM2COL") != nullptr;  // A/B switch
-  if (!env_im2col && (!f || !f->resid) &&
+  if (!env_im2col && (!f || !f->resid) && p.cpx == 4 &&
       stem_fprop_ok(dt, d->layout, c.c, c.r, c.s, c.sh, c.sw, c.ph, c.pw, c.ow, c.k) &&
       stem_fprop_weight_bytes(c.k) <= p.ws_w)
     return stem_fprop(dt, c.n, c.h, p.xw_pad, c.oh, c.ow, c.k, c.c, d->wlayout, x4, w, wr, bias, y,
                       st, f ? f->bn : BnFold{}, f ? f->relu : 0, f ? f->mask : nullptr);
-  MS_TRY(repack_rowseg(dt, c.k, c.c, c.r, c.s, d->wlayout, w, wr, st));
+  MS_TRY(repack_rowseg(dt, c.k, c.c, c.r, c.s, p.cpx, d->wlayout, w, wr, st));
   GemmArgs g = base_args(dt);
   g.M = c.n * c.oh * c.ow;
   g.N = c.k;
   const int bn = c.k <= 32 ? 32 : (c.k <= 64 ? 64 : (c.k <= 128 ? 128 : 256));
+  const int segs = (int)((c.ow + BM - 1) / BM);  // 128-pixel segments per output row
   g.n_blocks = (c.k + bn - 1) / bn;
-  g.num_tiles = c.n * c.oh * g.n_blocks;
-  g.cv = shape_of(c, 4, c.h, p.xw_pad, 1, 32, c.oh, c.ow);
+  g.num_tiles = c.n * c.oh * segs * g.n_blocks;
+  g.cv = shape_of(c, p.cpx, c.h, p.xw_pad, 1, 32, c.oh, c.ow);
+  g.cv.band_sub = segs;
   g.epi = EpiParams{y, c.k, dt, 0, bias, dt};
   apply_fuse(g.epi, f);
   TmapPack tm;
   const size_t es = dtype_size(dt);
   const uint64_t dims[4] = {32, (uint64_t)c.ow, (uint64_t)c.h, (uint64_t)c.n};
-  const uint64_t str[3] = {(uint64_t)c.sw * 4 * es, (uint64_t)p.xw_pad * 4 * es,
-                           (uint64_t)c.h * p.xw_pad * 4 * es};
+  const uint64_t str[3] = {(uint64_t)c.sw * p.cpx * es, (uint64_t)p.xw_pad * p.cpx * es,
+                           (uint64_t)c.h * p.xw_pad * p.cpx * es};
   const uint32_t box[4] = {32, BM, 1, 1};
   MS_TRY(make_tmap_nd(&tm.a[0], dt, x4, 4, dims, str, box, 64));
   tm.a[1] = tm.a[2] = tm.a[3] = tm.a[0];

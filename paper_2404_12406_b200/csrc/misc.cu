@@ -207,7 +207,7 @@ __global__ void repack_scatter_kernel(int K, int C, int R, int S, int kpad, int 
 
 // Row-segment stem weights [k][r][32]: element s*4 + c of row r = w[k][c][r][s]
 template <typename T>
-__global__ void repack_rowseg_kernel(int K, int C, int R, int S, int wlayout,
+__global__ void repack_rowseg_kernel(int K, int C, int R, int S, int cpx, int wlayout,
                                      const T* __restrict__ w, T* __restrict__ out) {
   const int64_t total = (int64_t)K * R * 32;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -215,7 +215,7 @@ __global__ void repack_rowseg_kernel(int K, int C, int R, int S, int wlayout,
     const int e = i % 32;
     const int r = (i / 32) % R;
     const int k = (int)(i / (32 * R));
-    const int s = e / 4, c = e % 4;
+    const int s = e / cpx, c = e % cpx;
     T v = IO<T>::cvt(0.f);
     if (s < S && c < C)
       v = wlayout == MS_NHWC ? w[(((int64_t)k * R + r) * S + s) * C + c]
@@ -224,9 +224,9 @@ __global__ void repack_rowseg_kernel(int K, int C, int R, int S, int wlayout,
   }
 }
 
-// [n][h][w][c<=4] -> [n][h][wp][4] with pw zero pixels on the left and zeros
-// on the right up to wp (the row-segment stem's padded activation copy)
-template <typename T>
+// [n][h][w][c<=CPX] -> [n][h][wp][CPX] with pw zero pixels on the left and
+// zeros on the right up to wp (the row-segment conv's padded activation copy)
+template <typename T, int CPX>
 __global__ void pad_rowseg_kernel(int N, int H, int W, int C, int pw, int wp,
                                   const T* __restrict__ x, T* __restrict__ out) {
   const int64_t total = (int64_t)N * H * wp;
@@ -235,20 +235,26 @@ __global__ void pad_rowseg_kernel(int N, int H, int W, int C, int pw, int wp,
     const int j = i % wp;
     const int64_t nh = i / wp;
     const int src = j - pw;
-    T v[4];
+    T v[CPX];
 #pragma unroll
-    for (int c = 0; c < 4; ++c)
+    for (int c = 0; c < CPX; ++c)
       v[c] = (src >= 0 && src < W && c < C) ? x[(nh * W + src) * C + c] : IO<T>::cvt(0.f);
-    T* o = out + i * 4;
-    if constexpr (sizeof(T) == 2) {
+    T* o = out + i * CPX;
+    if constexpr (sizeof(T) == 2 && CPX == 4) {
       uint2 u;
       T* e = reinterpret_cast<T*>(&u);
 #pragma unroll
       for (int c = 0; c < 4; ++c) e[c] = v[c];
       *reinterpret_cast<uint2*>(o) = u;
+    } else if constexpr (sizeof(T) == 2 && CPX == 8) {
+      uint4 u;
+      T* e = reinterpret_cast<T*>(&u);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) e[c] = v[c];
+      *reinterpret_cast<uint4*>(o) = u;
     } else {
 #pragma unroll
-      for (int c = 0; c < 4; ++c) o[c] = v[c];
+      for (int c = 0; c < CPX; ++c) o[c] = v[c];
     }
   }
 }
@@ -311,20 +317,27 @@ ms_status repack_scatter(int dt, int K, int C, int R, int S, int kpad, int wlayo
   return launch_status("repack_scatter_kernel");
 }
 
-ms_status repack_rowseg(int dt, int K, int C, int R, int S, int wlayout, const void* w, void* out,
+ms_status repack_rowseg(int dt, int K, int C, int R, int S, int cpx, int wlayout, const void* w,
+                        void* out,
                         cudaStream_t st) {
   const int64_t total = (int64_t)K * R * 32;
   MS_DT_DISPATCH(dt, repack_rowseg_kernel<T><<<grid_1d(total), 256, 0, st>>>(
-                         K, C, R, S, wlayout, (const T*)w, (T*)out));
+                         K, C, R, S, cpx, wlayout, (const T*)w, (T*)out));
   count_launch();
   return launch_status("repack_rowseg_kernel");
 }
 
-ms_status pad_rowseg(int dt, int N, int H, int W, int C, int pw, int wp, const void* x, void* out,
+ms_status pad_rowseg(int dt, int N, int H, int W, int C, int pw, int wp, int cpx, const void* x,
+                     void* out,
                      cudaStream_t st) {
   const int64_t total = (int64_t)N * H * wp;
-  MS_DT_DISPATCH(dt, pad_rowseg_kernel<T><<<grid_1d(total), 256, 0, st>>>(
-                         N, H, W, C, pw, wp, (const T*)x, (T*)out));
+  if (cpx == 8) {
+    MS_DT_DISPATCH(dt, (pad_rowseg_kernel<T, 8><<<grid_1d(total), 256, 0, st>>>(
+                           N, H, W, C, pw, wp, (const T*)x, (T*)out)));
+  } else {
+    MS_DT_DISPATCH(dt, (pad_rowseg_kernel<T, 4><<<grid_1d(total), 256, 0, st>>>(
+                           N, H, W, C, pw, wp, (const T*)x, (T*)out)));
+  }
   count_launch();
   return launch_status("pad_rowseg_kernel");
 }

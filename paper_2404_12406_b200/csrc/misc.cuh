@@ -11,10 +11,10 @@ ms_status repack_dgrad(int dt, int K, int C, int R, int S, int kpad, int wlayout
                        const void* kw = nullptr, int pdt = 0, float eps = 0.f);
 ms_status repack_scatter(int dt, int K, int C, int R, int S, int kpad, int wlayout, const void* w,
                          void* out, cudaStream_t st);
-ms_status repack_rowseg(int dt, int K, int C, int R, int S, int wlayout, const void* w, void* out,
-                        cudaStream_t st);
-ms_status pad_rowseg(int dt, int N, int H, int W, int C, int pw, int wp, const void* x, void* out,
-                     cudaStream_t st);
+ms_status repack_rowseg(int dt, int K, int C, int R, int S, int cpx, int wlayout, const void* w,
+                        void* out, cudaStream_t st);
+ms_status pad_rowseg(int dt, int N, int H, int W, int C, int pw, int wp, int cpx, const void* x,
+                     void* out, cudaStream_t st);
 ms_status wgrad_finalize(int dt, int K, int C, int R, int S, int wlayout, const float* acc,
                          void* dw, cudaStream_t st);
 ms_status pad_channels(int dt, int64_t pixels, int c, int cpad, const void* x, void* out,

@@ -163,8 +163,12 @@ __device__ __forceinline__ TileInfo decode_tile(const GemmArgs& g, int t, int cr
     ti.kb_begin = 0;
     ti.kb_end = P.nr * P.ns * g.cv.cblocks;
   } else if constexpr (MODE == LOAD_CONV_FPROP_ROWSEG) {
-    const int row = t / g.n_blocks;
-    ti.nb = t - row * g.n_blocks;
+    // tile = 128 output pixels (segment ti.tap) of output row n*P + oh; rows
+    // wider than 128 pixels take cv.band_sub segments
+    const int rs = t / g.n_blocks;
+    ti.nb = t - rs * g.n_blocks;
+    const int row = rs / g.cv.band_sub;
+    ti.tap = rs - row * g.cv.band_sub;
     ti.m0 = row;  // n*P + oh
     ti.kb_begin = 0;
     ti.kb_end = g.cv.R;
@@ -440,7 +444,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
               tma_load_2d(sB, &tm.b, fb, kb * BK, n0);
             } else if constexpr (MODE == LOAD_CONV_FPROP_ROWSEG) {
               // k-block = kernel row r: 128 overlapping segments of one input row
-              tma_load_4d(sA, amap, fb, 0, 0, ch + kb, cn);
+              tma_load_4d(sA, amap, fb, 0, ti.tap * BM, ch + kb, cn);
               tma_load_2d(sB, &tm.b, fb, kb * 32, n0);
             } else if constexpr (MODE == LOAD_CONV_DGRAD_BAND) {
               // one full dY row (Q pixels, 64 channels); rows outside [0, P) load zeros
@@ -721,8 +725,9 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
           const int h = g.cv.sh * i + P.ph, w = g.cv.sw * j + P.pw;
           orow = (static_cast<int64_t>(nn) * g.cv.outH + h) * g.cv.outW + w;
         } else if constexpr (MODE == LOAD_CONV_FPROP_ROWSEG) {
-          valid = row < g.cv.Q;
-          orow = static_cast<int64_t>(ti.m0) * g.cv.Q + row;
+          const int q = ti.tap * BM + row;
+          valid = q < g.cv.Q;
+          orow = static_cast<int64_t>(ti.m0) * g.cv.Q + q;
         } else {
           valid = m < g.M;
           orow = m;
