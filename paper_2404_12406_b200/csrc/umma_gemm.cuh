@@ -240,9 +240,12 @@ struct GemmCfg {
   // 4-MMA k-blocks (64 clk per MMA at N = 128) are too short to amortise one
   // barrier round trip and one TMA batch per k-block (layer-2 conv 0.081 ->
   // 0.066 ms); wgrad / stem / C8 modes keep 1
-  static constexpr int KS = (((CL == 2 && BN <= 256) || (CL == 1 && BN == 64)) &&
-                             (MODE == LOAD_CONV_FPROP || MODE == LOAD_CONV_DGRAD || MODE == LOAD_GEMM))
-                                ? 2 : 1;
+  static constexpr int KS =
+      MODE == LOAD_CONV_FPROP_ROWSEG ? 4  // a whole 3x3 window (3 kernel rows) per stage
+      : (((CL == 2 && BN <= 256) || (CL == 1 && BN == 64)) &&
+         (MODE == LOAD_CONV_FPROP || MODE == LOAD_CONV_DGRAD || MODE == LOAD_GEMM))
+          ? 2
+          : 1;
   static constexpr int A_SUB = BM * KBYTES;          // one k-block of A
   static constexpr int B_SUB = BN / CL * KBYTES;     // this CTA's share of one k-block of B
   static constexpr int A_BYTES = KS * A_SUB;
