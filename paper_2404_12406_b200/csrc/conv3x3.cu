@@ -23,19 +23,30 @@ namespace {
 
 constexpr int H3_C = 64;                    // reduction channels (one 128-B row)
 constexpr int H3_N = 64;                    // output channels (UMMA N)
-constexpr int H3_P = 64;                    // halo row pitch in pixels
-constexpr int H3_ROWS = 2;                  // output rows per tile
-constexpr int H3_HALO = (H3_ROWS + 2) * H3_P * 128;  // 32 KB per stage
-constexpr int H3_STAGES = 3;
 constexpr int H3_B = 9 * H3_N * 128;        // 9 taps x [64 n][64 c]
 constexpr int H3_EPI = 8;                   // 2 per TMEM lane quarter, 32 channels each
 constexpr int H3_THREADS = 64 + 32 * H3_EPI;
 constexpr int H3_STG = H3_EPI * 2 * 2048;   // TMA-store staging, 2 x (32 px x 32 ch) per warp
-constexpr int H3_SMEM = H3_B + H3_STAGES * H3_HALO + H3_STG + 1024 + 256;
+
+// Tile geometry.  WIDE = 0 (rows of <= 62 pixels): 2 output rows at a 64-pixel
+// pitch.  WIDE = 1 (any width, VGG's 224): 1 output row segment of 128
+// pixels; its 130-pixel halo rows sit at a 136-pixel pitch (1024-byte aligned
+// TMA destinations), so tap (r, s) still reads rows r*136 + s .. + 127.
+template <int WIDE>
+struct H3Geo {
+  static constexpr int ROWS = WIDE ? 1 : 2;            // output rows per tile
+  static constexpr int SEG = WIDE ? 128 : 64;          // tile pixels per output row
+  static constexpr int P = WIDE ? 136 : 64;            // halo row pitch in pixels
+  static constexpr int BOXW = WIDE ? 130 : 64;         // halo pixels loaded per row
+  static constexpr int HALO = (ROWS + 2) * P * 128;    // bytes per stage
+  static constexpr int STAGES = WIDE ? 2 : 3;
+  static constexpr int SMEM = H3_B + STAGES * HALO + H3_STG + 1024 + 256;
+};
 
 struct H3Args {
   int N, H, W;        // activation (input == output spatial size)
-  int tiles_per_img;  // ceil(H / 2)
+  int tiles_per_img;  // ceil(H / ROWS) row tiles per image
+  int segs;           // WIDE: 128-pixel segments per row (else 1)
   int units;
   int dt;
   void* y;
@@ -57,7 +68,7 @@ __device__ __forceinline__ uint64_t desc_sw128_rows(uint32_t saddr) {
   return make_smem_desc(saddr, 16, 1024, LAYOUT_SWIZZLE_128B);
 }
 
-template <typename T>
+template <typename T, int WIDE>
 __global__ void __launch_bounds__(H3_THREADS, 1)
     conv3x3_halo_kernel(const __grid_constant__ CUtensorMap tma_x,
                         const __grid_constant__ CUtensorMap tma_w,
@@ -66,6 +77,8 @@ __global__ void __launch_bounds__(H3_THREADS, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
+  using G = H3Geo<WIDE>;
+  constexpr int H3_ROWS = G::ROWS, H3_P = G::P, H3_HALO = G::HALO, H3_STAGES = G::STAGES;
   uint8_t* sB = smem;
   uint8_t* ring = smem + H3_B;
   uint8_t* staging = ring + H3_STAGES * H3_HALO;
@@ -112,16 +125,18 @@ __global__ void __launch_bounds__(H3_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
-        const int n = u / a.tiles_per_img;
-        const int i0 = (u - n * a.tiles_per_img) * H3_ROWS;
+        const int n = u / (a.tiles_per_img * a.segs);
+        const int rem = u - n * (a.tiles_per_img * a.segs);
+        const int i0 = (rem / a.segs) * H3_ROWS;
+        const int x0 = (rem - (rem / a.segs) * a.segs) * G::SEG;
         mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
         const uint32_t fb = smem_u32(&full_bar[stage]);
         const uint32_t sh = smem_u32(ring + stage * H3_HALO);
         if (elect_one()) {
-          mbar_arrive_expect_tx(fb, H3_HALO);
+          mbar_arrive_expect_tx(fb, (H3_ROWS + 2) * G::BOXW * 128);
 #pragma unroll
-          for (int rr = 0; rr < H3_ROWS + 2; ++rr)  // input rows i0-1 .. i0+2, pixels -1 .. 62
-            tma_load_4d(sh + rr * H3_P * 128, &tma_x, fb, 0, -1, i0 - 1 + rr, n);
+          for (int rr = 0; rr < H3_ROWS + 2; ++rr)  // input rows i0-1 .., pixels x0-1 ..
+            tma_load_4d(sh + rr * H3_P * 128, &tma_x, fb, 0, x0 - 1, i0 - 1 + rr, n);
         }
         __syncwarp();
         if (++stage == H3_STAGES) {
@@ -181,19 +196,21 @@ __global__ void __launch_bounds__(H3_THREADS, 1)
     const int ew = static_cast<int>(warp) - 2;
     const int c0 = (ew >> 2) * 32;         // this warp's 32 output channels
     const int rw = static_cast<int>(lane);
-    const int ti = quarter >> 1;           // output row within the tile
-    const int j0 = (quarter & 1) * 32;     // first pixel of this warp's 32
+    const int ti = WIDE ? 0 : quarter >> 1;           // output row within the tile
+    const int j0 = WIDE ? quarter * 32 : (quarter & 1) * 32;  // first pixel of the warp's 32
     const int j = j0 + rw;
     int local = 0;
     uint32_t nst = 0;
     float bs0 = 1.f, bt0 = 0.f;  // eval-BN affine of channel c0 + lane
     if (a.bn.var) bn_fold(a.bn, c0 + rw, bs0, bt0);
     for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++local) {
-      const int n = u / a.tiles_per_img;
-      const int oh = (u - n * a.tiles_per_img) * H3_ROWS + ti;
+      const int n = u / (a.tiles_per_img * a.segs);
+      const int rem = u - n * (a.tiles_per_img * a.segs);
+      const int oh = (rem / a.segs) * H3_ROWS + ti;
+      const int x0 = (rem - (rem / a.segs) * a.segs) * G::SEG;
       const bool row_ok = oh < a.H;
-      const bool valid = row_ok && j < a.W;
-      const int64_t pix = (static_cast<int64_t>(n) * a.H + oh) * a.W + j;
+      const bool valid = row_ok && x0 + j < a.W;
+      const int64_t pix = (static_cast<int64_t>(n) * a.H + oh) * a.W + x0 + j;
       const int buf = local & 1;
       mbar_wait(smem_u32(&tfull_bar[buf]), (local >> 1) & 1);
       tc_fence_after();
@@ -265,7 +282,7 @@ __global__ void __launch_bounds__(H3_THREADS, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0 && row_ok) {
-          tma_store_3d(&tma_y, smem_u32(sb), c0, j0, n * a.H + oh);
+          tma_store_3d(&tma_y, smem_u32(sb), c0, x0 + j0, n * a.H + oh);
           bulk_commit();
         }
         ++nst;
@@ -313,8 +330,7 @@ bool conv3x3_halo_ok(int dt, int layout, int c, int k, int r, int s, int sh, int
                      int pw, int w) {
   static const bool off = getenv("MS_NO_HALO3") != nullptr;  // A/B switch
   return !off && (dt == MS_BF16 || dt == MS_F16) && layout == MS_NHWC && c == H3_C &&
-         k == H3_N && r == 3 && s == 3 && sh == 1 && sw == 1 && ph == 1 && pw == 1 &&
-         w + 2 <= H3_P;
+         k == H3_N && r == 3 && s == 3 && sh == 1 && sw == 1 && ph == 1 && pw == 1;
 }
 
 size_t conv3x3_halo_workspace() { return align256((size_t)9 * H3_N * H3_C * 2); }
@@ -337,10 +353,11 @@ ms_status conv3x3_halo(int dt, int n, int h, int w, int wlayout, int transpose, 
   MS_TRY(launch_status("repack_h3"));
   const size_t es = dtype_size(dt);
   CUtensorMap tx, tw, ty;
+  const bool wide = w + 2 > H3Geo<0>::P;  // rows wider than 62 pixels: 128-pixel segments
   {
     const uint64_t dims[4] = {(uint64_t)H3_C, (uint64_t)w, (uint64_t)h, (uint64_t)n};
     const uint64_t str[3] = {H3_C * es, (uint64_t)w * H3_C * es, (uint64_t)h * w * H3_C * es};
-    const uint32_t box[4] = {64, (uint32_t)H3_P, 1, 1};
+    const uint32_t box[4] = {64, (uint32_t)(wide ? H3Geo<1>::BOXW : H3Geo<0>::BOXW), 1, 1};
     MS_TRY(make_tmap_nd(&tx, dt, x, 4, dims, str, box, 128));
   }
   MS_TRY(make_tmap_2d(&tw, dt, ws, H3_C, 9 * H3_N, H3_C, 64, H3_N));
@@ -352,19 +369,23 @@ ms_status conv3x3_halo(int dt, int n, int h, int w, int wlayout, int transpose, 
   }
   H3Args a{};
   a.N = n; a.H = h; a.W = w;
-  a.tiles_per_img = (h + H3_ROWS - 1) / H3_ROWS;
-  a.units = n * a.tiles_per_img;
+  const int rows = wide ? H3Geo<1>::ROWS : H3Geo<0>::ROWS;
+  a.tiles_per_img = (h + rows - 1) / rows;
+  a.segs = wide ? (w + H3Geo<1>::SEG - 1) / H3Geo<1>::SEG : 1;
+  a.units = n * a.tiles_per_img * a.segs;
   a.dt = dt; a.y = y; a.bn = bn; a.bias = bias; a.resid = resid;
   a.relu = relu; a.mask = mask; a.keep_in = keep_in; a.bn_post = bn_post;
   const int grid = a.units < num_sms() ? a.units : num_sms();
+  auto go = [&](auto kern, int smem) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    kern<<<grid, H3_THREADS, smem, st>>>(tx, tw, ty, a);
+  };
   if (dt == MS_BF16) {
-    auto kern = conv3x3_halo_kernel<__nv_bfloat16>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, H3_SMEM);
-    kern<<<grid, H3_THREADS, H3_SMEM, st>>>(tx, tw, ty, a);
+    if (wide) go(conv3x3_halo_kernel<__nv_bfloat16, 1>, H3Geo<1>::SMEM);
+    else go(conv3x3_halo_kernel<__nv_bfloat16, 0>, H3Geo<0>::SMEM);
   } else {
-    auto kern = conv3x3_halo_kernel<__half>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, H3_SMEM);
-    kern<<<grid, H3_THREADS, H3_SMEM, st>>>(tx, tw, ty, a);
+    if (wide) go(conv3x3_halo_kernel<__half, 1>, H3Geo<1>::SMEM);
+    else go(conv3x3_halo_kernel<__half, 0>, H3Geo<0>::SMEM);
   }
   count_launch(1, KF_UMMA);
   return launch_status("conv3x3_halo_kernel");

@@ -114,6 +114,8 @@ TC_CASES = [
     (2, 64, 9, 13, 64, 3, 1, 1),       # 64->64 3x3/1/1: halo kernel, odd H (partial tile)
     (1, 64, 56, 56, 64, 3, 1, 1),      # ResNet layer1 geometry
     (3, 64, 7, 62, 64, 3, 1, 1),       # widest row the 64-pixel pitch allows
+    (1, 64, 5, 224, 64, 3, 1, 1),      # VGG conv1_2 rows: wide halo tiles, 2 x 128-px segments
+    (2, 64, 3, 130, 64, 3, 1, 1),      # wide halo: a 2-pixel last segment
     (2, 3, 20, 150, 64, 3, 1, 1),      # VGG conv1_1-like: 8-ch row segments, 2 segments/row
     (1, 5, 9, 33, 32, 3, 1, 1),        # 5 channels, one partial segment
 ]
