@@ -339,6 +339,58 @@ __global__ void __launch_bounds__(256) maxpool_fwd_k3s2p1(PoolDims d, const T* _
   }
 }
 
+// 2x2 / stride 2 / no padding (VGG): every tap is in range; packed 16-bit max
+// and first-equal argmax as in maxpool_fwd_k3s2p1.  2-D grid: blockIdx.y = n*oh.
+template <typename T>
+__global__ void __launch_bounds__(256) maxpool_fwd_k2s2(PoolDims d, const T* __restrict__ x,
+                                                        T* __restrict__ y,
+                                                        uint8_t* __restrict__ idx) {
+  using T2 = typename std::conditional<std::is_same<T, __half>::value, __half2,
+                                       __nv_bfloat162>::type;
+  const int G = d.c >> 3;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= d.ow * G) return;
+  const int ow = t / G;
+  const int gg = t - ow * G;
+  const int n = blockIdx.y / d.oh;
+  const int oh = blockIdx.y - n * d.oh;
+  const T* xn = x + ((int64_t)n * d.h + 2 * oh) * d.w * d.c + gg * 8;
+  uint4 raw[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    raw[k] = __ldg(reinterpret_cast<const uint4*>(xn + ((int64_t)(k >> 1) * d.w + 2 * ow + (k & 1)) *
+                                                           d.c));
+  uint32_t yv[4], ag[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    T2 m = *reinterpret_cast<const T2*>(reinterpret_cast<const uint32_t*>(&raw[0]) + q);
+#pragma unroll
+    for (int k = 1; k < 4; ++k)
+      m = __hmax2_nan(m, *reinterpret_cast<const T2*>(reinterpret_cast<const uint32_t*>(&raw[k]) + q));
+    yv[q] = 0u;
+    ag[q] = 0u;
+#pragma unroll
+    for (int k = 3; k >= 0; --k) {  // the last write wins: the first equal tap (or NaN)
+      const uint32_t vw = reinterpret_cast<const uint32_t*>(&raw[k])[q];
+      const T2 v2 = *reinterpret_cast<const T2*>(&vw);
+      const uint32_t hit = __heq2_mask(v2, m) | __hneu2_mask(v2, v2);
+      const uint32_t kk = (uint32_t)k | ((uint32_t)k << 16);
+      yv[q] = (yv[q] & ~hit) | (vw & hit);
+      ag[q] = (ag[q] & ~hit) | (kk & hit);
+    }
+  }
+  const int64_t o = (((int64_t)n * d.oh + oh) * d.ow + ow) * d.c + gg * 8;
+  *reinterpret_cast<uint4*>(y + o) = make_uint4(yv[0], yv[1], yv[2], yv[3]);
+  if (idx) {
+    uint2 u;
+    u.x = (ag[0] & 0xFFu) | ((ag[0] >> 8) & 0xFF00u) | ((ag[1] & 0xFFu) << 16) |
+          ((ag[1] >> 16) << 24);
+    u.y = (ag[2] & 0xFFu) | ((ag[2] >> 8) & 0xFF00u) | ((ag[3] & 0xFFu) << 16) |
+          ((ag[3] >> 16) << 24);
+    *reinterpret_cast<uint2*>(idx + o) = u;
+  }
+}
+
 // add g[j] to acc[j] for the channels whose window argmax is tap k
 template <typename T>
 __device__ __forceinline__ void route8(float (&acc)[8], const uint2 u, const float (&gv)[8],
@@ -603,8 +655,19 @@ extern "C" ms_status ms_maxpool2d_fwd(const ms_pool_desc* p, const void* x, void
                                                                      (uint8_t*)idx_or_null));
     } else {
       const int64_t work = (int64_t)d.n * d.oh * d.ow * (d.c / 8);
-      MS_DT_DISPATCH(dt, maxpool_fwd_nhwc8<T><<<grid_for(work), 256, 0, st>>>(
-                             d, (const T*)x, (T*)y, (uint8_t*)idx_or_null));
+      if (dtype_size(dt) == 2 && d.kh == 2 && d.kw == 2 && d.sh == 2 && d.sw == 2 && d.ph == 0 &&
+          d.pw == 0) {
+        const dim3 grid((unsigned)((d.ow * (d.c / 8) + 255) / 256), (unsigned)(d.n * d.oh));
+        if (dt == MS_BF16)
+          maxpool_fwd_k2s2<__nv_bfloat16><<<grid, 256, 0, st>>>(
+              d, (const __nv_bfloat16*)x, (__nv_bfloat16*)y, (uint8_t*)idx_or_null);
+        else
+          maxpool_fwd_k2s2<__half><<<grid, 256, 0, st>>>(d, (const __half*)x, (__half*)y,
+                                                          (uint8_t*)idx_or_null);
+      } else {
+        MS_DT_DISPATCH(dt, maxpool_fwd_nhwc8<T><<<grid_for(work), 256, 0, st>>>(
+                               d, (const T*)x, (T*)y, (uint8_t*)idx_or_null));
+      }
     }
   } else {
     const int64_t work = (int64_t)d.n * d.c * d.oh * d.ow;

@@ -336,7 +336,8 @@ def test_maxpool_golden():
 
 
 @pytest.mark.parametrize("shape,k,s,p", [((4, 64, 56, 56), 3, 2, 1), ((2, 24, 15, 13), 3, 2, 1),
-                                          ((2, 8, 9, 9), 2, 2, 0), ((3, 5, 10, 8), 3, 1, 1)])
+                                          ((2, 8, 9, 9), 2, 2, 0), ((3, 5, 10, 8), 3, 1, 1),
+                                          ((2, 64, 28, 28), 2, 2, 0)])
 @pytest.mark.parametrize("dt", ["bf16", "f32"])
 def test_maxpool_padded(shape, k, s, p, dt):
     rng = np.random.default_rng(sum(shape))
