@@ -125,6 +125,24 @@ MS_API ms_status ms_bn_eval_bwd(int64_t n, int64_t c, int64_t hw, int32_t layout
                          void* dw_or_null, void* db_or_null, void* ws, size_t ws_bytes,
                          void* stream);
 
+/* BN-eval -> ReLU in one pass, for BN layers whose affine is trainable (so the
+ * conv cannot absorb them): y = max(x*s + t, 0) with the ReLU bit mask (NHWC,
+ * 16-bit, C % 8 == 0, C <= 2048; x [n*hw][c]).  The backward applies the mask
+ * to dy and then the BN-eval VJP (dx, dw, db as requested; x needed for dw).
+ * Saved set = the union of the two rows (rules.py:84-87, 98-101).
+ * MS_ERR_UNSUPPORTED outside that layout.                                   */
+MS_API ms_status ms_bn_eval_relu_fwd(int64_t n, int64_t c, int64_t hw, int32_t dtype,
+                                     int32_t pdtype, const void* x, const void* mean,
+                                     const void* var, const void* weight_or_null,
+                                     const void* bias_or_null, double eps, void* y,
+                                     void* mask_or_null, void* stream);
+MS_API ms_status ms_bn_eval_relu_bwd(int64_t n, int64_t c, int64_t hw, int32_t dtype,
+                                     int32_t pdtype, const void* dy, const void* mask,
+                                     const void* x_or_null, const void* mean, const void* var,
+                                     const void* weight_or_null, double eps, void* dx_or_null,
+                                     void* dw_or_null, void* db_or_null, void* ws,
+                                     size_t ws_bytes, void* stream);
+
 /* ------------------------------------------------------------ relu (bit mask)
  * MemSave ReLU (rules.py:98-101, saved.py:53-71): y = max(x, 0) over a dense
  * buffer of `numel` elements (any memory format: the mask follows storage

@@ -195,7 +195,11 @@ constexpr int BN_UNR = 4;
 template <typename T, int VEC>
 __global__ void __launch_bounds__(256, 3) bn_fwd_nhwc_kernel(int64_t rows, int C, BnParams p,
                                                           const T* __restrict__ x,
-                                                          T* __restrict__ y) {
+                                                          T* __restrict__ y,
+                                                          uint8_t* __restrict__ relu_mask = nullptr,
+                                                          int relu = 0) {
+  // relu: y = max(bn(x), 0) and (when relu_mask) its keep bits, one byte per
+  // 8 channels of a pixel (storage order, as ms_relu_fwd; VEC == 8)
   const int G = C / VEC;
   const int rpb = 256 / G;
   const int tid = threadIdx.x;
@@ -219,9 +223,18 @@ __global__ void __launch_bounds__(256, 3) bn_fwd_nhwc_kernel(int64_t rows, int C
     for (int u = 0; u < BN_UNR; ++u) {
       const int64_t r = r0 + u * step;
       if (r < rows) {
+        uint32_t bits = 0;
 #pragma unroll
-        for (int j = 0; j < VEC; ++j) v[u][j] = v[u][j] * sc[j] + sf[j];
+        for (int j = 0; j < VEC; ++j) {
+          v[u][j] = v[u][j] * sc[j] + sf[j];
+          if (relu) {
+            const bool pos = !(v[u][j] <= 0.f);  // NaN propagates, as ms_relu_fwd
+            bits |= (pos ? 1u : 0u) << j;
+            v[u][j] = pos ? v[u][j] : 0.f;
+          }
+        }
         store_vec<T, VEC>(y + r * C + grp * VEC, v[u]);
+        if (relu_mask) relu_mask[(r * C + grp * VEC) / 8] = static_cast<uint8_t>(bits);
       }
     }
   }
@@ -233,7 +246,9 @@ __global__ void __launch_bounds__(256, WANT_DW ? 2 : 3) bn_bwd_nhwc_kernel(int64
                                                           const T* __restrict__ x,
                                                           T* __restrict__ dx,
                                                           float* __restrict__ acc_dw,
-                                                          float* __restrict__ acc_db) {
+                                                          float* __restrict__ acc_db,
+                                                          const uint8_t* __restrict__ keep = nullptr) {
+  // keep (nullable, VEC == 8): the following ReLU's mask, g := keep ? g : 0 first
   __shared__ float s_dw[2048], s_db[2048];
   const int G = C / VEC;
   const int rpb = 256 / G;
@@ -260,6 +275,11 @@ __global__ void __launch_bounds__(256, WANT_DW ? 2 : 3) bn_bwd_nhwc_kernel(int64
         if (r < rows) {
           load_vec<T, VEC>(g + r * C + grp * VEC, gv[u]);
           if constexpr (WANT_DW) load_vec<T, VEC>(x + r * C + grp * VEC, xv[u]);
+          if (keep) {
+            const uint32_t kb = keep[(r * C + grp * VEC) / 8];
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) gv[u][j] = ((kb >> j) & 1u) ? gv[u][j] : 0.f;
+          }
         }
       }
 #pragma unroll
@@ -363,6 +383,60 @@ ms_status bn_eval_fwd(int64_t n, int64_t c, int64_t hw, int layout, int dt, cons
   return launch_status("bn_fwd_kernel");
 }
 
+// BN-eval -> ReLU in one pass (NHWC, 16-bit, C % 8 == 0, C <= 2048): the
+// chain kept unfused around the conv when BN's affine is trainable
+ms_status bn_relu_eval_fwd(int64_t n, int64_t c, int64_t hw, int dt, const BnParams& p,
+                           const void* x, void* y, uint8_t* mask, cudaStream_t st) {
+  const int64_t rows = n * hw;
+  MS_CHECK_ARG(dtype_size(dt) == 2 && c % 8 == 0 && c <= 2048, MS_ERR_UNSUPPORTED,
+               "bn+relu: 16-bit NHWC with C %% 8 == 0 only");
+  if (rows == 0) return MS_OK;
+  if (dt == MS_BF16)
+    bn_fwd_nhwc_kernel<__nv_bfloat16, 8><<<nhwc_grid(rows, c / 8), 256, 0, st>>>(
+        rows, (int)c, p, (const __nv_bfloat16*)x, (__nv_bfloat16*)y, mask, 1);
+  else
+    bn_fwd_nhwc_kernel<__half, 8><<<nhwc_grid(rows, c / 8), 256, 0, st>>>(
+        rows, (int)c, p, (const __half*)x, (__half*)y, mask, 1);
+  count_launch(1, KF_BN);
+  return launch_status("bn_fwd_nhwc_kernel (relu)");
+}
+
+ms_status bn_relu_eval_bwd(int64_t n, int64_t c, int64_t hw, int dt, const BnParams& p,
+                           const void* g, const uint8_t* keep, const void* x, void* dx, void* dw,
+                           void* db, void* ws, size_t ws_bytes, cudaStream_t st) {
+  const int64_t rows = n * hw;
+  MS_CHECK_ARG(dtype_size(dt) == 2 && c % 8 == 0 && c <= 2048 && keep, MS_ERR_UNSUPPORTED,
+               "bn+relu bwd: 16-bit NHWC with C %% 8 == 0 and a mask only");
+  MS_CHECK_ARG(!(dw && !x), MS_ERR_SHAPE, "bn+relu bwd: dw requested without x");
+  float* acc_dw = nullptr;
+  float* acc_db = nullptr;
+  if (dw || db) {
+    MS_CHECK_ARG(ws && ws_bytes >= bn_eval_workspace_bytes(c), MS_ERR_WORKSPACE,
+                 "bn+relu bwd workspace too small");
+    cudaMemsetAsync(ws, 0, bn_eval_workspace_bytes(c), st);
+    if (dw) acc_dw = static_cast<float*>(ws);
+    if (db) acc_db = static_cast<float*>(ws) + c;
+  }
+  if (rows > 0 && (dx || dw || db)) {
+    auto go = [&](auto tag) {
+      using T = decltype(tag);
+      if (dw)
+        bn_bwd_nhwc_kernel<T, 8, true><<<nhwc_grid(rows, c / 8), 256, 0, st>>>(
+            rows, (int)c, p, (const T*)g, (const T*)x, (T*)dx, acc_dw, acc_db, keep);
+      else
+        bn_bwd_nhwc_kernel<T, 8, false><<<nhwc_grid(rows, c / 8), 256, 0, st>>>(
+            rows, (int)c, p, (const T*)g, (const T*)x, (T*)dx, acc_dw, acc_db, keep);
+    };
+    if (dt == MS_BF16) go(__nv_bfloat16{});
+    else go(__half{});
+    count_launch(1, KF_BN);
+    MS_TRY(launch_status("bn_bwd_nhwc_kernel (relu)"));
+  }
+  if (dw) MS_TRY(f32_to(acc_dw, dw, p.pdtype, c, nullptr, 1, st));
+  if (db) MS_TRY(f32_to(acc_db, db, p.pdtype, c, nullptr, 1, st));
+  return MS_OK;
+}
+
 ms_status bn_eval_bwd(int64_t n, int64_t c, int64_t hw, int layout, int dt, const BnParams& p,
                       const void* g, const void* x, void* dx, void* dw, void* db, void* ws,
                       size_t ws_bytes, cudaStream_t st) {
@@ -442,6 +516,33 @@ extern "C" ms_status ms_bn_eval_bwd(int64_t n, int64_t c, int64_t hw, int32_t la
   ms::BnParams p{mean, var, weight, nullptr, pdtype, (float)eps};
   return ms::bn_eval_bwd(n, c, hw, layout, dtype, p, dy, x_or_null, dx_or_null, dw_or_null,
                          db_or_null, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+extern "C" ms_status ms_bn_eval_relu_fwd(int64_t n, int64_t c, int64_t hw, int32_t dtype,
+                                         int32_t pdtype, const void* x, const void* mean,
+                                         const void* var, const void* weight, const void* bias,
+                                         double eps, void* y, void* mask_or_null, void* stream) {
+  MS_TRY(ms::bind_device(y));
+  MS_CHECK_ARG(n >= 0 && c > 0 && hw >= 0, MS_ERR_SHAPE, "bn+relu: bad shape");
+  MS_CHECK_ARG(x && y && mean && var, MS_ERR_SHAPE, "bn+relu: null tensor");
+  ms::BnParams p{mean, var, weight, bias, pdtype, (float)eps};
+  return ms::bn_relu_eval_fwd(n, c, hw, dtype, p, x, y, static_cast<uint8_t*>(mask_or_null),
+                              (cudaStream_t)stream);
+}
+
+extern "C" ms_status ms_bn_eval_relu_bwd(int64_t n, int64_t c, int64_t hw, int32_t dtype,
+                                         int32_t pdtype, const void* dy, const void* mask,
+                                         const void* x_or_null, const void* mean, const void* var,
+                                         const void* weight, double eps, void* dx_or_null,
+                                         void* dw_or_null, void* db_or_null, void* ws,
+                                         size_t ws_bytes, void* stream) {
+  MS_TRY(ms::bind_device(dy));
+  MS_CHECK_ARG(n >= 0 && c > 0 && hw >= 0, MS_ERR_SHAPE, "bn+relu bwd: bad shape");
+  MS_CHECK_ARG(dy && mask && mean && var, MS_ERR_SHAPE, "bn+relu bwd: null tensor");
+  ms::BnParams p{mean, var, weight, nullptr, pdtype, (float)eps};
+  return ms::bn_relu_eval_bwd(n, c, hw, dtype, p, dy, static_cast<const uint8_t*>(mask),
+                              x_or_null, dx_or_null, dw_or_null, db_or_null, ws, ws_bytes,
+                              (cudaStream_t)stream);
 }
 
 // ---------------------------------------------------------------- BN-eval + ReLU backward

@@ -386,6 +386,113 @@ class _BatchNorm2dEvalFn(torch.autograd.Function):
         return dx, dw, db, None, None, None
 
 
+class _BatchNorm2dEvalReLUFn(torch.autograd.Function):
+    """BatchNorm2d(eval) -> ReLU in one pass (ms_bn_eval_relu_fwd), for BN layers
+    with a trainable affine (which the conv epilogue cannot absorb).  Saved set
+    = the union of the two rows: x iff the BN weight needs a grad, the weight
+    iff x does (rules.py:84-87 linear family), the ReLU bit mask iff the output
+    needs a grad (rules.py:98-101).  Backward: one pass for keep * (BN VJP)."""
+
+    @staticmethod
+    def forward(ctx, x, weight, bias, running_mean, running_var, eps):
+        x_rg, w_rg, b_rg = ctx.needs_input_grad[:3]
+        roles = saved_roles(x_rg, w_rg)
+        out_rg = x_rg or w_rg or b_rg
+        ctx.stats = (running_mean, running_var)
+        ctx.eps = float(eps)
+        ctx.x_shape = tuple(x.shape)
+        ctx.p_dtypes = (None if weight is None else weight.dtype,
+                        None if bias is None else bias.dtype)
+        n_el = x.numel()
+        if _is_meta(x):
+            mask = torch.empty((n_el + 7) // 8, dtype=torch.uint8, device="meta") if out_rg \
+                else None
+            ctx.save_for_backward(x if "x" in roles else None, weight if "w" in roles else None,
+                                  mask)
+            return x.new_empty(x.shape)
+        _require_cuda("batch_norm_relu", x, weight, bias, running_mean, running_var)
+        xl = _as_layout(x, _lib.MS_NHWC)
+        n, c, h, w_ = x.shape
+        pdt_t = running_var.dtype
+        params = [t if (t is None or t.dtype == pdt_t) else t.to(pdt_t)
+                  for t in (running_mean, running_var, weight, bias)]
+        params = [None if t is None else t.contiguous() for t in params]
+        y = torch.empty_like(xl)
+        mask = torch.empty((n_el + 7) // 8, dtype=torch.uint8, device=x.device) if out_rg \
+            else None
+        L = _lib.lib()
+        _lib.check(L.ms_bn_eval_relu_fwd(n, c, h * w_, _dtype_code(x), _dtype_code(running_var),
+                                         _ptr(xl), _ptr(params[0]), _ptr(params[1]),
+                                         _ptr(params[2]), _ptr(params[3]), ctx.eps, _ptr(y),
+                                         _ptr(mask), _stream(x.device)), "ms_bn_eval_relu_fwd")
+        ctx.save_for_backward(xl if "x" in roles else None, weight if "w" in roles else None,
+                              mask)
+        return y
+
+    @staticmethod
+    def backward(ctx, gy):
+        x, weight, mask = ctx.saved_tensors
+        need_x, need_w, need_b = ctx.needs_input_grad[:3]
+        running_mean, running_var = ctx.stats
+        c = ctx.x_shape[1]
+        mask = _need(mask, "mask", "batchnorm2d+relu backward")
+        dx = dw = db = None
+        if _is_meta(gy):
+            if need_x:
+                dx = gy.new_empty(ctx.x_shape)
+            if need_w:
+                _need(x, "x", "batchnorm2d dW")
+                dw = gy.new_empty((c,))
+            if need_b:
+                db = gy.new_empty((c,))
+            return dx, dw, db, None, None, None
+        if need_x and ctx.p_dtypes[0] is not None:
+            weight = _need(weight, "w", "batchnorm2d dX")
+        if need_w:
+            x = _need(x, "x", "batchnorm2d dW")
+        g = _as_layout(gy, _lib.MS_NHWC)
+        n, _, h, w_ = ctx.x_shape
+        pdt_t = running_var.dtype
+        rm = running_mean.to(pdt_t).contiguous()
+        rv = running_var.contiguous()
+        wt = None if weight is None else weight.to(pdt_t).contiguous()
+        if need_x:
+            dx = torch.empty_like(g)
+        dw_t = torch.empty((c,), dtype=pdt_t, device=g.device) if need_w else None
+        db_t = torch.empty((c,), dtype=pdt_t, device=g.device) if need_b else None
+        L = _lib.lib()
+        ws, nb = _workspace(L.ms_bn_eval_workspace(n, c, h * w_, _lib.MS_NHWC)
+                            if (need_w or need_b) else 0, g.device)
+        _lib.check(L.ms_bn_eval_relu_bwd(n, c, h * w_, _dtype_code(g), _dtype_code(rv), _ptr(g),
+                                         _ptr(mask), _ptr(x if need_w else None), _ptr(rm),
+                                         _ptr(rv), _ptr(wt), ctx.eps, _ptr(dx), _ptr(dw_t),
+                                         _ptr(db_t), _ptr(ws), nb, _stream(g.device)),
+                   "ms_bn_eval_relu_bwd")
+        if need_w:
+            dw = dw_t.to(ctx.p_dtypes[0])
+        if need_b:
+            db = db_t.to(ctx.p_dtypes[1])
+        return dx, dw, db, None, None, None
+
+
+def bn_relu_fusable(x: torch.Tensor, bn) -> bool:
+    """The one-pass BN-eval -> ReLU kernel applies (any requires_grad of the affine)."""
+    if bn is None or bn.training or not bn.track_running_stats or bn.running_var is None:
+        return False
+    if x.dim() != 4 or x.shape[1] % 8 or x.shape[1] > 2048:
+        return False
+    if x.device.type == "meta":
+        return x.dtype in (torch.bfloat16, torch.float16)
+    return x.device.type == "cuda" and x.dtype in (torch.bfloat16, torch.float16) \
+        and _is_channels_last(x)
+
+
+def batch_norm_relu_eval(x, bn):
+    """relu(bn(x)) for an eval-mode BatchNorm2d module in one pass."""
+    return _BatchNorm2dEvalReLUFn.apply(x, bn.weight, bn.bias, bn.running_mean, bn.running_var,
+                                        bn.eps)
+
+
 def batch_norm_eval(x, running_mean, running_var, weight=None, bias=None, eps=1e-5):
     """Differentiability-agnostic eval-mode batch norm."""
     return _BatchNorm2dEvalFn.apply(x, weight, bias, running_mean, running_var, eps)
@@ -1106,6 +1213,9 @@ def fused_conv(x: torch.Tensor, conv, bn, relu_: bool, residual=None, tee: bool 
         if in_mask is not None:
             x = _MaskScaleFn.apply(x, in_mask, in_bn)
         y = conv(x)
+        if bn is not None and relu_ and residual is None and bn_relu_fusable(y, bn):
+            # BN not absorbable (trainable affine): BN -> ReLU still in one pass
+            return batch_norm_relu_eval(y, bn), None, (x if tee else None)
         if bn is not None:
             y = bn(y)
         if residual is not None:

@@ -718,6 +718,39 @@ def test_fused_conv_in_mask(case):
     _close(x.grad, ref, "bf16", "in-mask dx", ulps=2.01)
 
 
+@pytest.mark.parametrize("shape", [(2, 64, 9, 11), (3, 256, 7, 7)])
+def test_bn_relu_eval_trainable_affine(shape):
+    # BN(eval) with a trainable affine -> ReLU in one pass: y, dX, dW, db against
+    # float64 (BN scale rounded to fp32 as in the kernel)
+    n, c, h, w = shape
+    rng = np.random.default_rng(c + h)
+    x, xq = _q(rng.standard_normal(shape), "bf16")
+    x = x.contiguous(memory_format=torch.channels_last).requires_grad_(True)
+    bn = torch.nn.BatchNorm2d(c).to(DEV, torch.bfloat16).eval()
+    bn.running_mean.copy_(torch.linspace(-0.5, 0.5, c))
+    bn.running_var.copy_(torch.linspace(0.5, 2.0, c))
+    bn.weight.data.copy_(torch.linspace(0.5, 1.5, c))
+    bn.bias.data.copy_(torch.linspace(-0.3, 0.3, c))
+    assert MF.bn_relu_fusable(x, bn)
+    y = MF.batch_norm_relu_eval(x, bn)
+    g, gq = _q(rng.standard_normal(shape), "bf16")
+    y.backward(g.contiguous(memory_format=torch.channels_last))
+    mu = bn.running_mean.double().cpu().numpy().reshape(1, -1, 1, 1)
+    var = bn.running_var.double().cpu().numpy().reshape(1, -1, 1, 1)
+    wq = bn.weight.detach().double().cpu().numpy().reshape(1, -1, 1, 1)
+    bq = bn.bias.detach().double().cpu().numpy().reshape(1, -1, 1, 1)
+    inv = 1.0 / np.sqrt(var + 1e-5)
+    z = (xq - mu) * inv * wq + bq
+    keep = y.detach().float().cpu().double().numpy() > 0
+    _close(y, np.maximum(z, 0), "bf16", "bn_relu y", ulps=2.01)
+    gk = np.where(keep, gq, 0.0)
+    _close(x.grad, gk * wq * inv, "bf16", "bn_relu dx", ulps=2.01)
+    np.testing.assert_allclose(bn.weight.grad.double().cpu().numpy(),
+                               (gk * (xq - mu) * inv).sum(axis=(0, 2, 3)), rtol=2e-2, atol=2e-2)
+    np.testing.assert_allclose(bn.bias.grad.double().cpu().numpy(), gk.sum(axis=(0, 2, 3)),
+                               rtol=2e-2, atol=2e-2)
+
+
 def test_add_relu():
     rng = np.random.default_rng(3)
     a, aq = _q(rng.standard_normal((2, 32, 9, 9)), "bf16")
