@@ -1212,17 +1212,24 @@ def fused_conv(x: torch.Tensor, conv, bn, relu_: bool, residual=None, tee: bool 
     if not ok:
         if in_mask is not None:
             x = _MaskScaleFn.apply(x, in_mask, in_bn)
-        y = conv(x)
+        xt = x if tee else None
+        if tee and conv_relu_fusable(x, conv):
+            # the conv alone on the tcgen05 path, still tee'd: the other consumer's
+            # gradient is summed in its dgrad epilogue (BN / ReLU follow unfused)
+            y, _, xt = _ConvBNFn.apply(x, conv.weight, conv.bias, None, conv.stride,
+                                       conv.padding, None, False, True)
+        else:
+            y = conv(x)
         if bn is not None and relu_ and residual is None and bn_relu_fusable(y, bn):
             # BN not absorbable (trainable affine): BN -> ReLU still in one pass
-            return batch_norm_relu_eval(y, bn), None, (x if tee else None)
+            return batch_norm_relu_eval(y, bn), None, xt
         if bn is not None:
             y = bn(y)
         if residual is not None:
             y = add_relu(y, residual) if relu_ else y + residual
         elif relu_:
             y = _relu_keep_mask(y)
-        return y, None, (x if tee else None)
+        return y, None, xt
     outs = _ConvBNFn.apply(x, conv.weight, conv.bias, residual, conv.stride, conv.padding, bn,
                            relu_, tee, in_mask, in_bn)
     y, mask = outs[0], outs[1]
