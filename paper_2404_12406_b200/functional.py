@@ -1213,13 +1213,7 @@ def fused_conv(x: torch.Tensor, conv, bn, relu_: bool, residual=None, tee: bool 
         if in_mask is not None:
             x = _MaskScaleFn.apply(x, in_mask, in_bn)
         xt = x if tee else None
-        if tee and conv_relu_fusable(x, conv):
-            # the conv alone on the tcgen05 path, still tee'd: the other consumer's
-            # gradient is summed in its dgrad epilogue (BN / ReLU follow unfused)
-            y, _, xt = _ConvBNFn.apply(x, conv.weight, conv.bias, None, conv.stride,
-                                       conv.padding, None, False, True)
-        else:
-            y = conv(x)
+        y = conv(x)
         if bn is not None and relu_ and residual is None and bn_relu_fusable(y, bn):
             # BN not absorbable (trainable affine): BN -> ReLU still in one pass
             return batch_norm_relu_eval(y, bn), None, xt
