@@ -385,105 +385,105 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
             const uint32_t sA0 = smem_u32(ring + stage * Cfg::STAGE_BYTES);
             // one k-block's TMA loads into (sA, sB)
             auto issue = [&](const int kb, const uint32_t sA, const uint32_t sB) {
-            if constexpr (MODE == LOAD_GEMM) {
-              const int k0 = kb * BK;
-              if constexpr (CL > 1) {
-                if constexpr (A_MN) {
-                  tma_load_2d_cg2(sA, &tm.a[0], fb, ti.m0, k0);
-                  tma_load_2d_cg2(sA + 8192, &tm.a[0], fb, ti.m0 + 64, k0);
+              if constexpr (MODE == LOAD_GEMM) {
+                const int k0 = kb * BK;
+                if constexpr (CL > 1) {
+                  if constexpr (A_MN) {
+                    tma_load_2d_cg2(sA, &tm.a[0], fb, ti.m0, k0);
+                    tma_load_2d_cg2(sA + 8192, &tm.a[0], fb, ti.m0 + 64, k0);
+                  } else {
+                    tma_load_2d_cg2(sA, &tm.a[0], fb, k0, ti.m0);
+                  }
+                  const int nh = n0 + crank * (BN / CL);  // this CTA's half of the B tile
+                  if constexpr (B_MN) {
+  #pragma unroll
+                    for (int j = 0; j < BN / CL / 64; ++j)
+                      tma_load_2d_cg2(sB + j * 8192, &tm.b, fb, nh + 64 * j, k0);
+                  } else {
+                    tma_load_2d_cg2(sB, &tm.b, fb, k0, nh);
+                  }
                 } else {
-                  tma_load_2d_cg2(sA, &tm.a[0], fb, k0, ti.m0);
+                  if constexpr (A_MN) {
+                    tma_load_2d(sA, &tm.a[0], fb, ti.m0, k0);
+                    tma_load_2d(sA + 8192, &tm.a[0], fb, ti.m0 + 64, k0);
+                  } else {
+                    tma_load_2d(sA, &tm.a[0], fb, k0, ti.m0);
+                  }
                 }
-                const int nh = n0 + crank * (BN / CL);  // this CTA's half of the B tile
-                if constexpr (B_MN) {
-#pragma unroll
-                  for (int j = 0; j < BN / CL / 64; ++j)
-                    tma_load_2d_cg2(sB + j * 8192, &tm.b, fb, nh + 64 * j, k0);
+                if constexpr (CL > 1) {
+                } else if constexpr (B_MN) {
+  #pragma unroll
+                  for (int j = 0; j < BN / 64; ++j)
+                    tma_load_2d(sB + j * 8192, &tm.b, fb, n0 + 64 * j, k0);
                 } else {
-                  tma_load_2d_cg2(sB, &tm.b, fb, k0, nh);
+                  tma_load_2d(sB, &tm.b, fb, k0, n0);
                 }
-              } else {
-                if constexpr (A_MN) {
-                  tma_load_2d(sA, &tm.a[0], fb, ti.m0, k0);
-                  tma_load_2d(sA + 8192, &tm.a[0], fb, ti.m0 + 64, k0);
+              } else if constexpr (MODE == LOAD_CONV_FPROP) {
+                const int tap = kb / g.cv.cblocks;
+                const int cb = kb - tap * g.cv.cblocks;
+                const int r = tap / g.cv.S, s = tap - (tap / g.cv.S) * g.cv.S;
+                if constexpr (CL > 1) {
+                  tma_load_im2col_4d_cg2(sA, amap, fb, cb * 64, cw, ch, cn, (uint16_t)s, (uint16_t)r);
+                  tma_load_2d_cg2(sB, &tm.b, fb, tap * g.cv.wrow_cpad + cb * 64,
+                                  n0 + crank * (BN / CL));
                 } else {
-                  tma_load_2d(sA, &tm.a[0], fb, k0, ti.m0);
+                  tma_load_im2col_4d(sA, amap, fb, cb * 64, cw, ch, cn, (uint16_t)s, (uint16_t)r);
+                  tma_load_2d(sB, &tm.b, fb, tap * g.cv.wrow_cpad + cb * 64, n0);
                 }
-              }
-              if constexpr (CL > 1) {
-              } else if constexpr (B_MN) {
-#pragma unroll
+              } else if constexpr (MODE == LOAD_CONV_FPROP_C8) {
+                // 8 taps x 8 channels; each tap is one 128-pixel x 16-byte im2col box
+                const int taps = g.cv.R * g.cv.S;
+  #pragma unroll 1
+                for (int j = 0; j < 8; ++j) {
+                  const int tap = kb * 8 + j;
+                  if (tap < taps) {
+                    const int r = tap / g.cv.S, s = tap - (tap / g.cv.S) * g.cv.S;
+                    tma_load_im2col_4d(sA + j * 2048, amap, fb, 0, cw, ch, cn, (uint16_t)s,
+                                       (uint16_t)r);
+                  } else {  // past the last tap: an all-out-of-bounds box loads zeros
+                    tma_load_im2col_4d(sA + j * 2048, amap, fb, 0, cw, ch, g.cv.N, 0, 0);
+                  }
+                }
+                tma_load_2d(sB, &tm.b, fb, kb * BK, n0);
+              } else if constexpr (MODE == LOAD_CONV_FPROP_ROWSEG) {
+                // k-block = kernel row r: 128 overlapping segments of one input row
+                tma_load_4d(sA, amap, fb, 0, ti.tap * BM, ch + kb, cn);
+                tma_load_2d(sB, &tm.b, fb, kb * 32, n0);
+              } else if constexpr (MODE == LOAD_CONV_DGRAD_BAND) {
+                // one full dY row (Q pixels, 64 channels); rows outside [0, P) load zeros
+                tma_load_4d(sA, amap, fb, kb * BK, 0, ch + sub, cn);
+                tma_load_2d(sB, &tm.b, fb, kb * BK, n0);
+              } else if constexpr (MODE == LOAD_CONV_DGRAD) {
+                const PhaseInfo& P = g.phase[ti.phase];
+                const int cb = kb % g.cv.cblocks;
+                const int tt = kb / g.cv.cblocks;
+                const int ts = tt % P.ns, tr = tt / P.ns;
+                const int r = P.r0 + g.cv.sh * tr, s = P.s0 + g.cv.sw * ts;
+                if constexpr (CL > 1) {
+                  tma_load_im2col_4d_cg2(sA, amap, fb, cb * 64, cw, ch, cn,
+                                         (uint16_t)(P.ns - 1 - ts), (uint16_t)(P.nr - 1 - tr));
+                  tma_load_2d_cg2(sB, &tm.b, fb, (r * g.cv.S + s) * g.cv.wrow_cpad + cb * 64,
+                                  n0 + crank * (BN / CL));
+                } else {
+                  tma_load_im2col_4d(sA, amap, fb, cb * 64, cw, ch, cn, (uint16_t)(P.ns - 1 - ts),
+                                     (uint16_t)(P.nr - 1 - tr));
+                  tma_load_2d(sB, &tm.b, fb, (r * g.cv.S + s) * g.cv.wrow_cpad + cb * 64, n0);
+                }
+              } else {  // LOAD_CONV_WGRAD: K = output pixels
+                const int p0 = kb * BK;
+                const int pq = g.cv.P * g.cv.Q;
+                const int pn = p0 / pq;
+                const int rem = p0 - pn * pq;
+                const int oh = rem / g.cv.Q, ow = rem - (rem / g.cv.Q) * g.cv.Q;
+                const int tap = ti.tap;
+                const int r = tap / g.cv.S, s = tap - (tap / g.cv.S) * g.cv.S;
+                tma_load_2d(sA, &tm.a[0], fb, ti.m0, p0);
+                tma_load_2d(sA + 8192, &tm.a[0], fb, ti.m0 + 64, p0);
+  #pragma unroll
                 for (int j = 0; j < BN / 64; ++j)
-                  tma_load_2d(sB + j * 8192, &tm.b, fb, n0 + 64 * j, k0);
-              } else {
-                tma_load_2d(sB, &tm.b, fb, k0, n0);
+                  tma_load_im2col_4d(sB + j * 8192, &tm.b, fb, n0 + 64 * j, ow * g.cv.sw - g.cv.pw,
+                                     oh * g.cv.sh - g.cv.ph, pn, (uint16_t)s, (uint16_t)r);
               }
-            } else if constexpr (MODE == LOAD_CONV_FPROP) {
-              const int tap = kb / g.cv.cblocks;
-              const int cb = kb - tap * g.cv.cblocks;
-              const int r = tap / g.cv.S, s = tap - (tap / g.cv.S) * g.cv.S;
-              if constexpr (CL > 1) {
-                tma_load_im2col_4d_cg2(sA, amap, fb, cb * 64, cw, ch, cn, (uint16_t)s, (uint16_t)r);
-                tma_load_2d_cg2(sB, &tm.b, fb, tap * g.cv.wrow_cpad + cb * 64,
-                                n0 + crank * (BN / CL));
-              } else {
-                tma_load_im2col_4d(sA, amap, fb, cb * 64, cw, ch, cn, (uint16_t)s, (uint16_t)r);
-                tma_load_2d(sB, &tm.b, fb, tap * g.cv.wrow_cpad + cb * 64, n0);
-              }
-            } else if constexpr (MODE == LOAD_CONV_FPROP_C8) {
-              // 8 taps x 8 channels; each tap is one 128-pixel x 16-byte im2col box
-              const int taps = g.cv.R * g.cv.S;
-#pragma unroll 1
-              for (int j = 0; j < 8; ++j) {
-                const int tap = kb * 8 + j;
-                if (tap < taps) {
-                  const int r = tap / g.cv.S, s = tap - (tap / g.cv.S) * g.cv.S;
-                  tma_load_im2col_4d(sA + j * 2048, amap, fb, 0, cw, ch, cn, (uint16_t)s,
-                                     (uint16_t)r);
-                } else {  // past the last tap: an all-out-of-bounds box loads zeros
-                  tma_load_im2col_4d(sA + j * 2048, amap, fb, 0, cw, ch, g.cv.N, 0, 0);
-                }
-              }
-              tma_load_2d(sB, &tm.b, fb, kb * BK, n0);
-            } else if constexpr (MODE == LOAD_CONV_FPROP_ROWSEG) {
-              // k-block = kernel row r: 128 overlapping segments of one input row
-              tma_load_4d(sA, amap, fb, 0, ti.tap * BM, ch + kb, cn);
-              tma_load_2d(sB, &tm.b, fb, kb * 32, n0);
-            } else if constexpr (MODE == LOAD_CONV_DGRAD_BAND) {
-              // one full dY row (Q pixels, 64 channels); rows outside [0, P) load zeros
-              tma_load_4d(sA, amap, fb, kb * BK, 0, ch + sub, cn);
-              tma_load_2d(sB, &tm.b, fb, kb * BK, n0);
-            } else if constexpr (MODE == LOAD_CONV_DGRAD) {
-              const PhaseInfo& P = g.phase[ti.phase];
-              const int cb = kb % g.cv.cblocks;
-              const int tt = kb / g.cv.cblocks;
-              const int ts = tt % P.ns, tr = tt / P.ns;
-              const int r = P.r0 + g.cv.sh * tr, s = P.s0 + g.cv.sw * ts;
-              if constexpr (CL > 1) {
-                tma_load_im2col_4d_cg2(sA, amap, fb, cb * 64, cw, ch, cn,
-                                       (uint16_t)(P.ns - 1 - ts), (uint16_t)(P.nr - 1 - tr));
-                tma_load_2d_cg2(sB, &tm.b, fb, (r * g.cv.S + s) * g.cv.wrow_cpad + cb * 64,
-                                n0 + crank * (BN / CL));
-              } else {
-                tma_load_im2col_4d(sA, amap, fb, cb * 64, cw, ch, cn, (uint16_t)(P.ns - 1 - ts),
-                                   (uint16_t)(P.nr - 1 - tr));
-                tma_load_2d(sB, &tm.b, fb, (r * g.cv.S + s) * g.cv.wrow_cpad + cb * 64, n0);
-              }
-            } else {  // LOAD_CONV_WGRAD: K = output pixels
-              const int p0 = kb * BK;
-              const int pq = g.cv.P * g.cv.Q;
-              const int pn = p0 / pq;
-              const int rem = p0 - pn * pq;
-              const int oh = rem / g.cv.Q, ow = rem - (rem / g.cv.Q) * g.cv.Q;
-              const int tap = ti.tap;
-              const int r = tap / g.cv.S, s = tap - (tap / g.cv.S) * g.cv.S;
-              tma_load_2d(sA, &tm.a[0], fb, ti.m0, p0);
-              tma_load_2d(sA + 8192, &tm.a[0], fb, ti.m0 + 64, p0);
-#pragma unroll
-              for (int j = 0; j < BN / 64; ++j)
-                tma_load_im2col_4d(sB + j * 8192, &tm.b, fb, n0 + 64 * j, ow * g.cv.sw - g.cv.pw,
-                                   oh * g.cv.sh - g.cv.ph, pn, (uint16_t)s, (uint16_t)r);
-            }
             };
             if (elect_one()) {
               if (crank == 0)
