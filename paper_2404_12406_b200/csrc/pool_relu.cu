@@ -406,7 +406,7 @@ __device__ __forceinline__ void route8(float (&acc)[8], const uint2 u, const flo
 // cols 2j, 2j+1) x 8 channels reads the <= 4 windows (i..i+1) x (j..j+1) once
 // and writes the 4 input pixels (two 2-pixel runs), every dx element exactly once.
 template <typename T>
-__global__ void __launch_bounds__(256) maxpool_bwd_k3s2p1(PoolDims d, const T* __restrict__ g,
+__global__ void __launch_bounds__(256, 4) maxpool_bwd_k3s2p1(PoolDims d, const T* __restrict__ g,
                                                           const uint8_t* __restrict__ idx,
                                                           T* __restrict__ dx,
                                                           const uint8_t* __restrict__ keep,
