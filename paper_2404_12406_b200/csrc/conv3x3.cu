@@ -27,6 +27,7 @@ constexpr int H3_B = 9 * H3_N * 128;        // 9 taps x [64 n][64 c]
 constexpr int H3_EPI = 8;                   // 2 per TMEM lane quarter, 32 channels each
 constexpr int H3_THREADS = 64 + 32 * H3_EPI;
 constexpr int H3_STG = H3_EPI * 2 * 2048;   // TMA-store staging, 2 x (32 px x 32 ch) per warp
+constexpr int H3_ACC = 4;                   // TMEM accumulators (4 x 64 columns) in flight
 
 // Tile geometry.  WIDE = 0 (rows of <= 62 pixels): 2 output rows at a 64-pixel
 // pitch.  WIDE = 1 (any width, VGG's 224): 1 output row segment of 128
@@ -86,9 +87,9 @@ __global__ void __launch_bounds__(H3_THREADS, 1)
   uint64_t* full_bar = bars;
   uint64_t* empty_bar = bars + H3_STAGES;
   uint64_t* tfull_bar = bars + 2 * H3_STAGES;
-  uint64_t* tempty_bar = bars + 2 * H3_STAGES + 2;
-  uint64_t* b_bar = bars + 2 * H3_STAGES + 4;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * H3_STAGES + 5);
+  uint64_t* tempty_bar = bars + 2 * H3_STAGES + H3_ACC;
+  uint64_t* b_bar = bars + 2 * H3_STAGES + 2 * H3_ACC;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * H3_STAGES + 2 * H3_ACC + 1);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -97,7 +98,7 @@ __global__ void __launch_bounds__(H3_THREADS, 1)
       mbar_init(smem_u32(&full_bar[i]), 1);
       mbar_init(smem_u32(&empty_bar[i]), 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < H3_ACC; ++i) {
       mbar_init(smem_u32(&tfull_bar[i]), 1);
       mbar_init(smem_u32(&tempty_bar[i]), H3_EPI);
     }
@@ -107,7 +108,7 @@ __global__ void __launch_bounds__(H3_THREADS, 1)
     tma_prefetch_desc(&tma_w);
     tma_prefetch_desc(&tma_y);
   }
-  if (warp == 1) tmem_alloc(smem_u32(tmem_holder), 128);
+  if (warp == 1) tmem_alloc(smem_u32(tmem_holder), H3_ACC * H3_N);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -158,8 +159,8 @@ __global__ void __launch_bounds__(H3_THREADS, 1)
       uint32_t phase = 0;
       int local = 0;
       for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++local) {
-        const int acc = local & 1;
-        mbar_wait(smem_u32(&tempty_bar[acc]), ((local >> 1) & 1) ^ 1);
+        const int acc = local % H3_ACC;
+        mbar_wait(smem_u32(&tempty_bar[acc]), ((local / H3_ACC) & 1) ^ 1);
         mbar_wait(smem_u32(&full_bar[stage]), phase);
         tc_fence_after();
         const uint32_t dcol = tmem_u + acc * H3_N;
@@ -211,8 +212,8 @@ __global__ void __launch_bounds__(H3_THREADS, 1)
       const bool row_ok = oh < a.H;
       const bool valid = row_ok && x0 + j < a.W;
       const int64_t pix = (static_cast<int64_t>(n) * a.H + oh) * a.W + x0 + j;
-      const int buf = local & 1;
-      mbar_wait(smem_u32(&tfull_bar[buf]), (local >> 1) & 1);
+      const int buf = local % H3_ACC;
+      mbar_wait(smem_u32(&tfull_bar[buf]), (local / H3_ACC) & 1);
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((static_cast<uint32_t>(quarter) * 32u) << 16) + buf * H3_N;
       uint32_t v0[32];
@@ -293,7 +294,7 @@ __global__ void __launch_bounds__(H3_THREADS, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, 128);
+    tmem_dealloc(tmem_base, H3_ACC * H3_N);
   }
 }
 
