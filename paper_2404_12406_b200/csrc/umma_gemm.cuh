@@ -265,7 +265,10 @@ struct GemmCfg {
   static constexpr int SMEM_MAX = 227 * 1024;
   static constexpr int STAGES_MAX = (SMEM_MAX - 1280 - EXTRA - STG) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_MAX > 8 ? 8 : STAGES_MAX;
-  static constexpr int TMEM_COLS = pow2_cols(2 * BN);
+  // TMEM accumulators in flight: 4 when they fit the 512 columns (BN <= 128),
+  // so epilogue jitter does not stall the MMAs; the band dgrad keeps 2
+  static constexpr int NACC = (MODE != LOAD_CONV_DGRAD_BAND && 4 * BN <= 512) ? 4 : 2;
+  static constexpr int TMEM_COLS = pow2_cols(NACC * BN);
   static constexpr int SMEM_BYTES =
       STAGES * STAGE_BYTES + STG + EXTRA + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr int THREADS = 64 + 32 * EPI;
@@ -306,9 +309,10 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
       reinterpret_cast<uint64_t*>(staging + Cfg::STG + Cfg::EXTRA);
   uint64_t* full_bar = bars;
   uint64_t* empty_bar = bars + STAGES;
+  constexpr int NACC = Cfg::NACC;
   uint64_t* tfull_bar = bars + 2 * STAGES;
-  uint64_t* tempty_bar = bars + 2 * STAGES + 2;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+  uint64_t* tempty_bar = bars + 2 * STAGES + NACC;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 2 * NACC);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -318,7 +322,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
       mbar_init(smem_u32(&full_bar[i]), 1);
       mbar_init(smem_u32(&empty_bar[i]), 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NACC; ++i) {
       mbar_init(smem_u32(&tfull_bar[i]), 1);
       // CL = 2: one arrival per epilogue warp of both CTAs (on the even CTA's barrier)
       mbar_init(smem_u32(&tempty_bar[i]), CL == 1 ? Cfg::EPI * 32 : CL * Cfg::EPI);
@@ -517,8 +521,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
       for (int t = t_first; t < g.num_tiles; t += t_step) {
         TileInfo ti = decode_tile<MODE, CL>(g, t, crank);
         for (int sub = 0; sub < ti.nsub; ++sub, ++local) {
-          const int acc = local & 1;
-          const uint32_t use = static_cast<uint32_t>(local >> 1);
+          const int acc = local % NACC;
+          const uint32_t use = static_cast<uint32_t>(local / NACC);
           if constexpr (CL == 1) mbar_wait(smem_u32(&tempty_bar[acc]), (use & 1) ^ 1);
           else mbar_wait_cluster(smem_u32(&tempty_bar[acc]), (use & 1) ^ 1);
           tc_fence_after();
@@ -625,8 +629,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
                               static_cast<int>(lane);
         const int ow = row;
         for (int sub = 0; sub < ti.nsub; ++sub, ++local) {
-          const int acc = local & 1;
-          const uint32_t use = static_cast<uint32_t>(local >> 1);
+          const int acc = local % NACC;
+          const uint32_t use = static_cast<uint32_t>(local / NACC);
           mbar_wait(smem_u32(&tfull_bar[acc]), use & 1);
           tc_fence_after();
           const int oh = oh0 + sub;
@@ -689,8 +693,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
         for (int i = tid; i < BAND_WINDOWS * BAND_WIN; i += NT) region[i] = 0.f;
         asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
       } else {
-        const int acc = local & 1;
-        const uint32_t use = static_cast<uint32_t>(local >> 1);
+        const int acc = local % NACC;
+        const uint32_t use = static_cast<uint32_t>(local / NACC);
         ++local;
         const bool tail = ti.unit >= 0;  // fp32 partial of a K-sliced last-wave tile
         const bool tma_st = Cfg::CAN_TMA_STORE && g.tma_store && !tail;
