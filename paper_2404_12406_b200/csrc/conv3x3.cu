@@ -24,9 +24,7 @@ namespace {
 constexpr int H3_C = 64;                    // reduction channels (one 128-B row)
 constexpr int H3_N = 64;                    // output channels (UMMA N)
 constexpr int H3_B = 9 * H3_N * 128;        // 9 taps x [64 n][64 c]
-constexpr int H3_EPI = 8;                   // 2 per TMEM lane quarter, 32 channels each
-constexpr int H3_THREADS = 64 + 32 * H3_EPI;
-constexpr int H3_STG = H3_EPI * 2 * 2048;   // TMA-store staging, 2 x (32 px x 32 ch) per warp
+constexpr int H3_EPI = 8;  // warps per epilogue group: 2 per TMEM lane quarter, 32 ch each
 constexpr int H3_ACC = 4;                   // TMEM accumulators (4 x 64 columns) in flight
 
 // Tile geometry.  WIDE = 0 (rows of <= 62 pixels): 2 output rows at a 64-pixel
@@ -40,8 +38,14 @@ struct H3Geo {
   static constexpr int P = WIDE ? 136 : 64;            // halo row pitch in pixels
   static constexpr int BOXW = WIDE ? 130 : 64;         // halo pixels loaded per row
   static constexpr int HALO = (ROWS + 2) * P * 128;    // bytes per stage
-  static constexpr int STAGES = WIDE ? 2 : 3;
-  static constexpr int SMEM = H3_B + STAGES * HALO + H3_STG + 1024 + 256;
+  static constexpr int STAGES = 2;
+  // epilogue groups: 2 alternate tiles (16 warps) where the smem allows it, so
+  // the fused epilogue (residual / addend / masks) keeps pace with the MMAs
+  static constexpr int NG = WIDE ? 1 : 2;
+  static constexpr int EPI = NG * H3_EPI;
+  static constexpr int THREADS = 64 + 32 * EPI;
+  static constexpr int STG = EPI * 2 * 2048;  // TMA-store staging, 2 x (32 px x 32 ch) per warp
+  static constexpr int SMEM = H3_B + STAGES * HALO + STG + 1024 + 256;
 };
 
 struct H3Args {
@@ -70,7 +74,7 @@ __device__ __forceinline__ uint64_t desc_sw128_rows(uint32_t saddr) {
 }
 
 template <typename T, int WIDE>
-__global__ void __launch_bounds__(H3_THREADS, 1)
+__global__ void __launch_bounds__(H3Geo<WIDE>::THREADS, 1)
     conv3x3_halo_kernel(const __grid_constant__ CUtensorMap tma_x,
                         const __grid_constant__ CUtensorMap tma_w,
                         const __grid_constant__ CUtensorMap tma_y,
@@ -83,7 +87,7 @@ __global__ void __launch_bounds__(H3_THREADS, 1)
   uint8_t* sB = smem;
   uint8_t* ring = smem + H3_B;
   uint8_t* staging = ring + H3_STAGES * H3_HALO;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(staging + H3_STG);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(staging + G::STG);
   uint64_t* full_bar = bars;
   uint64_t* empty_bar = bars + H3_STAGES;
   uint64_t* tfull_bar = bars + 2 * H3_STAGES;
@@ -100,7 +104,7 @@ __global__ void __launch_bounds__(H3_THREADS, 1)
     }
     for (int i = 0; i < H3_ACC; ++i) {
       mbar_init(smem_u32(&tfull_bar[i]), 1);
-      mbar_init(smem_u32(&tempty_bar[i]), H3_EPI);
+      mbar_init(smem_u32(&tempty_bar[i]), H3_EPI);  // one group drains each tile
     }
     mbar_init(smem_u32(b_bar), 1);
     fence_mbar_init();
@@ -195,16 +199,18 @@ __global__ void __launch_bounds__(H3_THREADS, 1)
     // (BN affine, residual / addend, masks) keeps up with the 36-MMA tiles
     const int quarter = static_cast<int>(warp & 3);
     const int ew = static_cast<int>(warp) - 2;
-    const int c0 = (ew >> 2) * 32;         // this warp's 32 output channels
+    const int grp = ew / H3_EPI;           // epilogue group: tiles grp, grp + NG, ...
+    const int c0 = ((ew % H3_EPI) >> 2) * 32;  // this warp's 32 output channels
     const int rw = static_cast<int>(lane);
     const int ti = WIDE ? 0 : quarter >> 1;           // output row within the tile
     const int j0 = WIDE ? quarter * 32 : (quarter & 1) * 32;  // first pixel of the warp's 32
     const int j = j0 + rw;
-    int local = 0;
+    int local = grp;  // the CTA's tile sequence number (accumulator ring position)
     uint32_t nst = 0;
     float bs0 = 1.f, bt0 = 0.f;  // eval-BN affine of channel c0 + lane
     if (a.bn.var) bn_fold(a.bn, c0 + rw, bs0, bt0);
-    for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++local) {
+    for (int u = blockIdx.x + grp * gridDim.x; u < a.units;
+         u += G::NG * gridDim.x, local += G::NG) {
       const int n = u / (a.tiles_per_img * a.segs);
       const int rem = u - n * (a.tiles_per_img * a.segs);
       const int oh = (rem / a.segs) * H3_ROWS + ti;
@@ -377,16 +383,16 @@ ms_status conv3x3_halo(int dt, int n, int h, int w, int wlayout, int transpose, 
   a.dt = dt; a.y = y; a.bn = bn; a.bias = bias; a.resid = resid;
   a.relu = relu; a.mask = mask; a.keep_in = keep_in; a.bn_post = bn_post;
   const int grid = a.units < num_sms() ? a.units : num_sms();
-  auto go = [&](auto kern, int smem) {
+  auto go = [&](auto kern, int smem, int threads) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    kern<<<grid, H3_THREADS, smem, st>>>(tx, tw, ty, a);
+    kern<<<grid, threads, smem, st>>>(tx, tw, ty, a);
   };
   if (dt == MS_BF16) {
-    if (wide) go(conv3x3_halo_kernel<__nv_bfloat16, 1>, H3Geo<1>::SMEM);
-    else go(conv3x3_halo_kernel<__nv_bfloat16, 0>, H3Geo<0>::SMEM);
+    if (wide) go(conv3x3_halo_kernel<__nv_bfloat16, 1>, H3Geo<1>::SMEM, H3Geo<1>::THREADS);
+    else go(conv3x3_halo_kernel<__nv_bfloat16, 0>, H3Geo<0>::SMEM, H3Geo<0>::THREADS);
   } else {
-    if (wide) go(conv3x3_halo_kernel<__half, 1>, H3Geo<1>::SMEM);
-    else go(conv3x3_halo_kernel<__half, 0>, H3Geo<0>::SMEM);
+    if (wide) go(conv3x3_halo_kernel<__half, 1>, H3Geo<1>::SMEM, H3Geo<1>::THREADS);
+    else go(conv3x3_halo_kernel<__half, 0>, H3Geo<0>::SMEM, H3Geo<0>::THREADS);
   }
   count_launch(1, KF_UMMA);
   return launch_status("conv3x3_halo_kernel");
