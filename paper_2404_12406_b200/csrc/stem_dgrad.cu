@@ -310,8 +310,10 @@ constexpr int SF_R = 7;
 constexpr int SF_SLOT = 2176;              // one padded input row (>= 16*127 + 64 bytes)
 constexpr int SF_STAGE = SF_R * SF_SLOT;   // the 7 input rows of one output row
 constexpr int SF_STAGES = 6;
-constexpr int SF_EPI = 4;
-constexpr int SF_THREADS = 64 + 32 * SF_EPI;
+constexpr int SF_EPI = 4;   // warps per epilogue group (one per TMEM lane quarter)
+constexpr int SF_NG = 2;    // epilogue groups, draining alternate output rows
+constexpr int SF_ACC = 4;   // TMEM accumulators in flight (4 x K <= 512 columns)
+constexpr int SF_THREADS = 64 + 32 * SF_EPI * SF_NG;
 
 struct StemFpropArgs {
   int N, H, Wp;    // padded 4-channel input: [N][H][Wp][4]
@@ -336,7 +338,7 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
       : "memory");
 }
 
-constexpr int SF_STG = SF_EPI * 2 * 4096;  // per epilogue warp: 2 x (32 px x 128 B), SW128
+constexpr int SF_STG = SF_EPI * SF_NG * 2 * 4096;  // per epilogue warp: 2 x (32 px x 128 B), SW128
 constexpr int SF_AFF = 2 * 128 * 4;         // fused eval-BN scale / shift (K <= 128)
 
 template <typename T>
@@ -356,9 +358,9 @@ __global__ void __launch_bounds__(SF_THREADS, 1)
   uint64_t* full_bar = bars;
   uint64_t* empty_bar = bars + SF_STAGES;
   uint64_t* tfull_bar = bars + 2 * SF_STAGES;
-  uint64_t* tempty_bar = bars + 2 * SF_STAGES + 2;
-  uint64_t* b_bar = bars + 2 * SF_STAGES + 4;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * SF_STAGES + 5);
+  uint64_t* tempty_bar = bars + 2 * SF_STAGES + SF_ACC;
+  uint64_t* b_bar = bars + 2 * SF_STAGES + 2 * SF_ACC;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * SF_STAGES + 2 * SF_ACC + 1);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -371,14 +373,14 @@ __global__ void __launch_bounds__(SF_THREADS, 1)
       mbar_init(smem_u32(&full_bar[i]), 1);
       mbar_init(smem_u32(&empty_bar[i]), 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < SF_ACC; ++i) {
       mbar_init(smem_u32(&tfull_bar[i]), 1);
-      mbar_init(smem_u32(&tempty_bar[i]), SF_EPI);
+      mbar_init(smem_u32(&tempty_bar[i]), SF_EPI);  // one group drains each row
     }
     mbar_init(smem_u32(b_bar), 1);
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(smem_u32(tmem_holder), 128);
+  if (warp == 1) tmem_alloc(smem_u32(tmem_holder), SF_ACC * 128);
   fence_proxy_async_smem();  // the zero row is read by the tensor core (async proxy)
   tc_fence_before();
   __syncthreads();
@@ -434,8 +436,8 @@ __global__ void __launch_bounds__(SF_THREADS, 1)
       int local = 0;
       for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++local) {
         const int oh = u - (u / a.P) * a.P;
-        const int acc = local & 1;
-        mbar_wait(smem_u32(&tempty_bar[acc]), ((local >> 1) & 1) ^ 1);
+        const int acc = local % SF_ACC;
+        mbar_wait(smem_u32(&tempty_bar[acc]), ((local / SF_ACC) & 1) ^ 1);
         mbar_wait(smem_u32(&full_bar[stage]), phase);
         tc_fence_after();
         const uint32_t dcol = tmem_u + acc * a.K;
@@ -475,12 +477,14 @@ __global__ void __launch_bounds__(SF_THREADS, 1)
     // (a 3-D map [N*P][Q][K] clips the pixels past Q)
     const int quarter = static_cast<int>(warp & 3);
     const int ew = static_cast<int>(warp) - 2;
+    const int grp = ew / SF_EPI;  // this group drains output rows grp, grp + SF_NG, ...
     const int rw = static_cast<int>(lane);
-    int local = 0;
+    int local = grp;
     uint32_t nst = 0;
-    for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++local) {
-      const int buf = local & 1;
-      mbar_wait(smem_u32(&tfull_bar[buf]), (local >> 1) & 1);
+    for (int u = blockIdx.x + grp * gridDim.x; u < a.units;
+         u += SF_NG * gridDim.x, local += SF_NG) {
+      const int buf = local % SF_ACC;
+      mbar_wait(smem_u32(&tfull_bar[buf]), (local / SF_ACC) & 1);
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((static_cast<uint32_t>(quarter) * 32u) << 16) + buf * a.K;
 #pragma unroll 1
@@ -539,7 +543,7 @@ __global__ void __launch_bounds__(SF_THREADS, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, 128);
+    tmem_dealloc(tmem_base, SF_ACC * 128);
   }
 }
 
