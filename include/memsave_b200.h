@@ -142,6 +142,22 @@ MS_API ms_status ms_bn_eval_relu_bwd(int64_t n, int64_t c, int64_t hw, int32_t d
                                      const void* weight_or_null, double eps, void* dx_or_null,
                                      void* dw_or_null, void* db_or_null, void* ws,
                                      size_t ws_bytes, void* stream);
+/* The same with the residual add of a bottleneck block between BN and ReLU:
+ * y = max(bf16(x*s + t) + residual, 0) (the BN output rounded as the unfused
+ * chain stores it).  The backward also writes dy * keep to dresidual (the add's
+ * gradient for its other operand), in the same pass.                        */
+MS_API ms_status ms_bn_eval_add_relu_fwd(int64_t n, int64_t c, int64_t hw, int32_t dtype,
+                                         int32_t pdtype, const void* x, const void* residual,
+                                         const void* mean, const void* var,
+                                         const void* weight_or_null, const void* bias_or_null,
+                                         double eps, void* y, void* mask_or_null, void* stream);
+MS_API ms_status ms_bn_eval_add_relu_bwd(int64_t n, int64_t c, int64_t hw, int32_t dtype,
+                                         int32_t pdtype, const void* dy, const void* mask,
+                                         const void* x_or_null, const void* mean,
+                                         const void* var, const void* weight_or_null, double eps,
+                                         void* dx_or_null, void* dresidual_or_null,
+                                         void* dw_or_null, void* db_or_null, void* ws,
+                                         size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------------ relu (bit mask)
  * MemSave ReLU (rules.py:98-101, saved.py:53-71): y = max(x, 0) over a dense

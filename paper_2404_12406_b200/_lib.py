@@ -77,6 +77,11 @@ SIGNATURES = {
                                      _vp, ctypes.c_double, _vp, _vp, _vp]),
     "ms_bn_eval_relu_bwd": (_c_i32, [_c_i64, _c_i64, _c_i64, _c_i32, _c_i32, _vp, _vp, _vp, _vp,
                                      _vp, _vp, ctypes.c_double, _vp, _vp, _vp, _vp, _c_sz, _vp]),
+    "ms_bn_eval_add_relu_fwd": (_c_i32, [_c_i64, _c_i64, _c_i64, _c_i32, _c_i32, _vp, _vp, _vp,
+                                         _vp, _vp, _vp, ctypes.c_double, _vp, _vp, _vp]),
+    "ms_bn_eval_add_relu_bwd": (_c_i32, [_c_i64, _c_i64, _c_i64, _c_i32, _c_i32, _vp, _vp, _vp,
+                                         _vp, _vp, _vp, ctypes.c_double, _vp, _vp, _vp, _vp,
+                                         _vp, _c_sz, _vp]),
     "ms_bn_relu_bwd": (_c_i32, [_c_i64, _c_i64, _c_i32, _c_i32, _vp, _vp, _vp, _vp, _vp,
                                 ctypes.c_double, _vp, _vp]),
     "ms_maxpool2d_out_h": (_c_i64, [ctypes.POINTER(PoolDesc)]),

@@ -191,15 +191,17 @@ __global__ void __launch_bounds__(256) bn_bwd_kernel(int64_t total, int C, int64
 // per-channel constants live in registers, each thread keeps UNR 16-byte
 // loads in flight (memory-level parallelism for HBM).
 constexpr int BN_UNR = 4;
+constexpr int BN_FWD_UNR = 8;
 
-template <typename T, int VEC>
-__global__ void __launch_bounds__(256, 3) bn_fwd_nhwc_kernel(int64_t rows, int C, BnParams p,
+template <typename T, int VEC, bool RES = false, int U = BN_FWD_UNR>
+__global__ void __launch_bounds__(256, RES ? 2 : 3) bn_fwd_nhwc_kernel(int64_t rows, int C, BnParams p,
                                                           const T* __restrict__ x,
                                                           T* __restrict__ y,
                                                           uint8_t* __restrict__ relu_mask = nullptr,
-                                                          int relu = 0) {
-  // relu: y = max(bn(x), 0) and (when relu_mask) its keep bits, one byte per
-  // 8 channels of a pixel (storage order, as ms_relu_fwd; VEC == 8)
+                                                          int relu = 0,
+                                                          const T* __restrict__ resid = nullptr) {
+  // relu: y = max(bn(x) [+ resid], 0) and (when relu_mask) its keep bits, one
+  // byte per 8 channels of a pixel (storage order, as ms_relu_fwd; VEC == 8)
   const int G = C / VEC;
   const int rpb = 256 / G;
   const int tid = threadIdx.x;
@@ -211,29 +213,44 @@ __global__ void __launch_bounds__(256, 3) bn_fwd_nhwc_kernel(int64_t rows, int C
     float inv, mu;
     bn_channel_consts(p, grp * VEC + j, sc[j], sf[j], inv, mu);
   }
+  // raw 16-byte loads held packed (4 registers per row, not 8 floats), so
+  // BN_FWD_UNR rows per operand are in flight per thread before any store
+  static_assert(VEC * sizeof(T) == 16, "bn_fwd_nhwc: 16-byte vectors");
   const int64_t step = (int64_t)gridDim.x * rpb;
-  for (int64_t r0 = (int64_t)blockIdx.x * rpb + rl; r0 < rows; r0 += step * BN_UNR) {
-    float v[BN_UNR][VEC];
+  for (int64_t r0 = (int64_t)blockIdx.x * rpb + rl; r0 < rows; r0 += step * U) {
+    uint4 raw[U], rraw[RES ? U : 1];
 #pragma unroll
-    for (int u = 0; u < BN_UNR; ++u) {
-      const int64_t r = r0 + u * step;
-      if (r < rows) load_vec<T, VEC>(x + r * C + grp * VEC, v[u]);
-    }
-#pragma unroll
-    for (int u = 0; u < BN_UNR; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int64_t r = r0 + u * step;
       if (r < rows) {
+        raw[u] = __ldcs(reinterpret_cast<const uint4*>(x + r * C + grp * VEC));
+        if constexpr (RES)
+          rraw[u] = __ldcs(reinterpret_cast<const uint4*>(resid + r * C + grp * VEC));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t r = r0 + u * step;
+      if (r < rows) {
+        const T* xe = reinterpret_cast<const T*>(&raw[u]);
+        const T* re = reinterpret_cast<const T*>(&rraw[RES ? u : 0]);
+        float v[VEC];
         uint32_t bits = 0;
 #pragma unroll
         for (int j = 0; j < VEC; ++j) {
-          v[u][j] = v[u][j] * sc[j] + sf[j];
+          v[j] = IO<T>::ld(xe + j) * sc[j] + sf[j];
+          if constexpr (RES) {
+            // round the BN output first: the unfused chain adds two stored tensors
+            T t = IO<T>::cvt(v[j]);
+            v[j] = IO<T>::ld(&t) + IO<T>::ld(re + j);
+          }
           if (relu) {
-            const bool pos = !(v[u][j] <= 0.f);  // NaN propagates, as ms_relu_fwd
+            const bool pos = !(v[j] <= 0.f);  // NaN propagates, as ms_relu_fwd
             bits |= (pos ? 1u : 0u) << j;
-            v[u][j] = pos ? v[u][j] : 0.f;
+            v[j] = pos ? v[j] : 0.f;
           }
         }
-        store_vec<T, VEC>(y + r * C + grp * VEC, v[u]);
+        store_vec<T, VEC>(y + r * C + grp * VEC, v);
         if (relu_mask) relu_mask[(r * C + grp * VEC) / 8] = static_cast<uint8_t>(bits);
       }
     }
@@ -247,8 +264,10 @@ __global__ void __launch_bounds__(256, WANT_DW ? 2 : 3) bn_bwd_nhwc_kernel(int64
                                                           T* __restrict__ dx,
                                                           float* __restrict__ acc_dw,
                                                           float* __restrict__ acc_db,
-                                                          const uint8_t* __restrict__ keep = nullptr) {
-  // keep (nullable, VEC == 8): the following ReLU's mask, g := keep ? g : 0 first
+                                                          const uint8_t* __restrict__ keep = nullptr,
+                                                          T* __restrict__ gkeep = nullptr) {
+  // keep (nullable, VEC == 8): the following ReLU's mask, g := keep ? g : 0 first;
+  // gkeep (nullable): that masked g stored too (the residual operand's gradient)
   __shared__ float s_dw[2048], s_db[2048];
   const int G = C / VEC;
   const int rpb = 256 / G;
@@ -269,23 +288,24 @@ __global__ void __launch_bounds__(256, WANT_DW ? 2 : 3) bn_bwd_nhwc_kernel(int64
     for (int64_t r0 = (int64_t)blockIdx.x * rpb + rl; r0 < rows; r0 += step * BN_UNR) {
       float gv[BN_UNR][VEC];
       float xv[WANT_DW ? BN_UNR : 1][VEC];
+      uint32_t kb[BN_UNR];
 #pragma unroll
       for (int u = 0; u < BN_UNR; ++u) {
         const int64_t r = r0 + u * step;
+        kb[u] = 0xffu;
         if (r < rows) {
           load_vec<T, VEC>(g + r * C + grp * VEC, gv[u]);
           if constexpr (WANT_DW) load_vec<T, VEC>(x + r * C + grp * VEC, xv[u]);
-          if (keep) {
-            const uint32_t kb = keep[(r * C + grp * VEC) / 8];
-#pragma unroll
-            for (int j = 0; j < VEC; ++j) gv[u][j] = ((kb >> j) & 1u) ? gv[u][j] : 0.f;
-          }
+          if (keep) kb[u] = keep[(r * C + grp * VEC) / 8];
         }
       }
 #pragma unroll
       for (int u = 0; u < BN_UNR; ++u) {
         const int64_t r = r0 + u * step;
         if (r >= rows) continue;
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) gv[u][j] = ((kb[u] >> j) & 1u) ? gv[u][j] : 0.f;
+        if (gkeep) store_vec<T, VEC>(gkeep + r * C + grp * VEC, gv[u]);
         if (want_dx) {
           float o[VEC];
 #pragma unroll
@@ -349,10 +369,26 @@ static int bn_grid(int64_t nvec, int64_t C, int layout, int vec) {
 }
 
 // rows of an NHWC tensor, G channel groups per row: 256/G rows per block pass
-static int nhwc_grid(int64_t rows, int64_t G) {
+// occ: resident blocks per SM of the kernel (its __launch_bounds__ minimum,
+// which its register count meets exactly).  One wave: every thread loops over
+// rows, so the per-channel constants and the dW/db block reduction (2C global
+// atomics per block) are paid once per resident block, not once per 4 rows.
+static int bn_fwd_unr() {
+  static const int u = [] {
+    const char* e = getenv("MS_BN_FWD_UNR");
+    return e && atoi(e) == 4 ? 4 : BN_FWD_UNR;
+  }();
+  return u;
+}
+
+static int nhwc_grid(int64_t rows, int64_t G, int occ, int unr = BN_UNR) {
+  static const int waves = [] {
+    const char* e = getenv("MS_BN_WAVES");
+    return e ? atoi(e) : 1;
+  }();
   const int64_t rpb = 256 / G;
-  int64_t need = (rows + rpb * BN_UNR - 1) / (rpb * BN_UNR);
-  const int64_t cap = (int64_t)num_sms() * 8;
+  int64_t need = (rows + rpb * unr - 1) / (rpb * unr);
+  const int64_t cap = (int64_t)num_sms() * occ * (waves > 0 ? waves : 1);
   if (need > cap) need = cap;
   return (int)(need > 0 ? need : 1);
 }
@@ -369,8 +405,12 @@ ms_status bn_eval_fwd(int64_t n, int64_t c, int64_t hw, int layout, int dt, cons
     constexpr int V = 16 / sizeof(T);
     if (layout == MS_NHWC && can_vec(c, hw, layout, V, x, y, nullptr) && c / V <= 256) {
       const int64_t rows = n * hw;
-      bn_fwd_nhwc_kernel<T, V><<<nhwc_grid(rows, c / V), 256, 0, st>>>(rows, (int)c, p,
-                                                                      (const T*)x, (T*)y);
+      if (bn_fwd_unr() == 4)
+        bn_fwd_nhwc_kernel<T, V, false, 4><<<nhwc_grid(rows, c / V, 3, 4), 256, 0, st>>>(
+            rows, (int)c, p, (const T*)x, (T*)y);
+      else
+        bn_fwd_nhwc_kernel<T, V><<<nhwc_grid(rows, c / V, 3, BN_FWD_UNR), 256, 0, st>>>(
+            rows, (int)c, p, (const T*)x, (T*)y);
     } else if (can_vec(c, hw, layout, V, x, y, nullptr)) {
       bn_fwd_kernel<T, V><<<bn_grid(total / V, c, layout, V), 256, smem, st>>>(
           total, (int)c, hw, layout, p, (const T*)x, (T*)y);
@@ -386,24 +426,38 @@ ms_status bn_eval_fwd(int64_t n, int64_t c, int64_t hw, int layout, int dt, cons
 // BN-eval -> ReLU in one pass (NHWC, 16-bit, C % 8 == 0, C <= 2048): the
 // chain kept unfused around the conv when BN's affine is trainable
 ms_status bn_relu_eval_fwd(int64_t n, int64_t c, int64_t hw, int dt, const BnParams& p,
-                           const void* x, void* y, uint8_t* mask, cudaStream_t st) {
+                           const void* x, const void* resid, void* y, uint8_t* mask,
+                           cudaStream_t st) {
   const int64_t rows = n * hw;
   MS_CHECK_ARG(dtype_size(dt) == 2 && c % 8 == 0 && c <= 2048, MS_ERR_UNSUPPORTED,
                "bn+relu: 16-bit NHWC with C %% 8 == 0 only");
   if (rows == 0) return MS_OK;
-  if (dt == MS_BF16)
-    bn_fwd_nhwc_kernel<__nv_bfloat16, 8><<<nhwc_grid(rows, c / 8), 256, 0, st>>>(
-        rows, (int)c, p, (const __nv_bfloat16*)x, (__nv_bfloat16*)y, mask, 1);
-  else
-    bn_fwd_nhwc_kernel<__half, 8><<<nhwc_grid(rows, c / 8), 256, 0, st>>>(
-        rows, (int)c, p, (const __half*)x, (__half*)y, mask, 1);
+  auto go = [&](auto tag) {
+    using T = decltype(tag);
+    const bool u4 = bn_fwd_unr() == 4;
+    const int gr = nhwc_grid(rows, c / 8, resid ? 2 : 3, u4 ? 4 : BN_FWD_UNR);
+    if (resid && u4)
+      bn_fwd_nhwc_kernel<T, 8, true, 4><<<gr, 256, 0, st>>>(
+          rows, (int)c, p, (const T*)x, (T*)y, mask, 1, (const T*)resid);
+    else if (resid)
+      bn_fwd_nhwc_kernel<T, 8, true><<<gr, 256, 0, st>>>(
+          rows, (int)c, p, (const T*)x, (T*)y, mask, 1, (const T*)resid);
+    else if (u4)
+      bn_fwd_nhwc_kernel<T, 8, false, 4><<<gr, 256, 0, st>>>(
+          rows, (int)c, p, (const T*)x, (T*)y, mask, 1);
+    else
+      bn_fwd_nhwc_kernel<T, 8><<<gr, 256, 0, st>>>(rows, (int)c, p, (const T*)x, (T*)y, mask, 1);
+  };
+  if (dt == MS_BF16) go(__nv_bfloat16{});
+  else go(__half{});
   count_launch(1, KF_BN);
   return launch_status("bn_fwd_nhwc_kernel (relu)");
 }
 
 ms_status bn_relu_eval_bwd(int64_t n, int64_t c, int64_t hw, int dt, const BnParams& p,
-                           const void* g, const uint8_t* keep, const void* x, void* dx, void* dw,
-                           void* db, void* ws, size_t ws_bytes, cudaStream_t st) {
+                           const void* g, const uint8_t* keep, const void* x, void* dx,
+                           void* dresid, void* dw, void* db, void* ws, size_t ws_bytes,
+                           cudaStream_t st) {
   const int64_t rows = n * hw;
   MS_CHECK_ARG(dtype_size(dt) == 2 && c % 8 == 0 && c <= 2048 && keep, MS_ERR_UNSUPPORTED,
                "bn+relu bwd: 16-bit NHWC with C %% 8 == 0 and a mask only");
@@ -417,15 +471,17 @@ ms_status bn_relu_eval_bwd(int64_t n, int64_t c, int64_t hw, int dt, const BnPar
     if (dw) acc_dw = static_cast<float*>(ws);
     if (db) acc_db = static_cast<float*>(ws) + c;
   }
-  if (rows > 0 && (dx || dw || db)) {
+  if (rows > 0 && (dx || dresid || dw || db)) {
     auto go = [&](auto tag) {
       using T = decltype(tag);
       if (dw)
-        bn_bwd_nhwc_kernel<T, 8, true><<<nhwc_grid(rows, c / 8), 256, 0, st>>>(
-            rows, (int)c, p, (const T*)g, (const T*)x, (T*)dx, acc_dw, acc_db, keep);
+        bn_bwd_nhwc_kernel<T, 8, true><<<nhwc_grid(rows, c / 8, 2), 256, 0, st>>>(
+            rows, (int)c, p, (const T*)g, (const T*)x, (T*)dx, acc_dw, acc_db, keep,
+            (T*)dresid);
       else
-        bn_bwd_nhwc_kernel<T, 8, false><<<nhwc_grid(rows, c / 8), 256, 0, st>>>(
-            rows, (int)c, p, (const T*)g, (const T*)x, (T*)dx, acc_dw, acc_db, keep);
+        bn_bwd_nhwc_kernel<T, 8, false><<<nhwc_grid(rows, c / 8, 3), 256, 0, st>>>(
+            rows, (int)c, p, (const T*)g, (const T*)x, (T*)dx, acc_dw, acc_db, keep,
+            (T*)dresid);
     };
     if (dt == MS_BF16) go(__nv_bfloat16{});
     else go(__half{});
@@ -460,10 +516,10 @@ ms_status bn_eval_bwd(int64_t n, int64_t c, int64_t hw, int layout, int dt, cons
           c / V <= 256 && c <= 2048) {
         const int64_t rows = n * hw;
         if (dw)
-          bn_bwd_nhwc_kernel<T, V, true><<<nhwc_grid(rows, c / V), 256, 0, st>>>(
+          bn_bwd_nhwc_kernel<T, V, true><<<nhwc_grid(rows, c / V, 2), 256, 0, st>>>(
               rows, (int)c, p, (const T*)g, (const T*)x, (T*)dx, acc_dw, acc_db);
         else
-          bn_bwd_nhwc_kernel<T, V, false><<<nhwc_grid(rows, c / V), 256, 0, st>>>(
+          bn_bwd_nhwc_kernel<T, V, false><<<nhwc_grid(rows, c / V, 3), 256, 0, st>>>(
               rows, (int)c, p, (const T*)g, (const T*)x, (T*)dx, acc_dw, acc_db);
       } else if (can_vec(c, hw, layout, V, g, dw ? x : nullptr, dx)) {
         bn_bwd_kernel<T, V><<<bn_grid(total / V, c, layout, V), 256, smem, st>>>(
@@ -526,8 +582,21 @@ extern "C" ms_status ms_bn_eval_relu_fwd(int64_t n, int64_t c, int64_t hw, int32
   MS_CHECK_ARG(n >= 0 && c > 0 && hw >= 0, MS_ERR_SHAPE, "bn+relu: bad shape");
   MS_CHECK_ARG(x && y && mean && var, MS_ERR_SHAPE, "bn+relu: null tensor");
   ms::BnParams p{mean, var, weight, bias, pdtype, (float)eps};
-  return ms::bn_relu_eval_fwd(n, c, hw, dtype, p, x, y, static_cast<uint8_t*>(mask_or_null),
-                              (cudaStream_t)stream);
+  return ms::bn_relu_eval_fwd(n, c, hw, dtype, p, x, nullptr, y,
+                              static_cast<uint8_t*>(mask_or_null), (cudaStream_t)stream);
+}
+
+extern "C" ms_status ms_bn_eval_add_relu_fwd(int64_t n, int64_t c, int64_t hw, int32_t dtype,
+                                             int32_t pdtype, const void* x, const void* residual,
+                                             const void* mean, const void* var,
+                                             const void* weight, const void* bias, double eps,
+                                             void* y, void* mask_or_null, void* stream) {
+  MS_TRY(ms::bind_device(y));
+  MS_CHECK_ARG(n >= 0 && c > 0 && hw >= 0, MS_ERR_SHAPE, "bn+add+relu: bad shape");
+  MS_CHECK_ARG(x && residual && y && mean && var, MS_ERR_SHAPE, "bn+add+relu: null tensor");
+  ms::BnParams p{mean, var, weight, bias, pdtype, (float)eps};
+  return ms::bn_relu_eval_fwd(n, c, hw, dtype, p, x, residual, y,
+                              static_cast<uint8_t*>(mask_or_null), (cudaStream_t)stream);
 }
 
 extern "C" ms_status ms_bn_eval_relu_bwd(int64_t n, int64_t c, int64_t hw, int32_t dtype,
@@ -541,8 +610,24 @@ extern "C" ms_status ms_bn_eval_relu_bwd(int64_t n, int64_t c, int64_t hw, int32
   MS_CHECK_ARG(dy && mask && mean && var, MS_ERR_SHAPE, "bn+relu bwd: null tensor");
   ms::BnParams p{mean, var, weight, nullptr, pdtype, (float)eps};
   return ms::bn_relu_eval_bwd(n, c, hw, dtype, p, dy, static_cast<const uint8_t*>(mask),
-                              x_or_null, dx_or_null, dw_or_null, db_or_null, ws, ws_bytes,
-                              (cudaStream_t)stream);
+                              x_or_null, dx_or_null, nullptr, dw_or_null, db_or_null, ws,
+                              ws_bytes, (cudaStream_t)stream);
+}
+
+extern "C" ms_status ms_bn_eval_add_relu_bwd(int64_t n, int64_t c, int64_t hw, int32_t dtype,
+                                             int32_t pdtype, const void* dy, const void* mask,
+                                             const void* x_or_null, const void* mean,
+                                             const void* var, const void* weight, double eps,
+                                             void* dx_or_null, void* dresidual_or_null,
+                                             void* dw_or_null, void* db_or_null, void* ws,
+                                             size_t ws_bytes, void* stream) {
+  MS_TRY(ms::bind_device(dy));
+  MS_CHECK_ARG(n >= 0 && c > 0 && hw >= 0, MS_ERR_SHAPE, "bn+add+relu bwd: bad shape");
+  MS_CHECK_ARG(dy && mask && mean && var, MS_ERR_SHAPE, "bn+add+relu bwd: null tensor");
+  ms::BnParams p{mean, var, weight, nullptr, pdtype, (float)eps};
+  return ms::bn_relu_eval_bwd(n, c, hw, dtype, p, dy, static_cast<const uint8_t*>(mask),
+                              x_or_null, dx_or_null, dresidual_or_null, dw_or_null, db_or_null,
+                              ws, ws_bytes, (cudaStream_t)stream);
 }
 
 // ---------------------------------------------------------------- BN-eval + ReLU backward

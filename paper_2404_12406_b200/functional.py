@@ -391,13 +391,17 @@ class _BatchNorm2dEvalReLUFn(torch.autograd.Function):
     with a trainable affine (which the conv epilogue cannot absorb).  Saved set
     = the union of the two rows: x iff the BN weight needs a grad, the weight
     iff x does (rules.py:84-87 linear family), the ReLU bit mask iff the output
-    needs a grad (rules.py:98-101).  Backward: one pass for keep * (BN VJP)."""
+    needs a grad (rules.py:98-101).  Backward: one pass for keep * (BN VJP).
+
+    ``residual`` (optional): relu(bn(x) + residual), a bottleneck block's tail
+    (the add saves nothing, rules.py:116-117); its gradient g * keep is written
+    by the same backward pass (ms_bn_eval_add_relu_{fwd,bwd})."""
 
     @staticmethod
-    def forward(ctx, x, weight, bias, running_mean, running_var, eps):
+    def forward(ctx, x, weight, bias, running_mean, running_var, eps, residual=None):
         x_rg, w_rg, b_rg = ctx.needs_input_grad[:3]
         roles = saved_roles(x_rg, w_rg)
-        out_rg = x_rg or w_rg or b_rg
+        out_rg = x_rg or w_rg or b_rg or ctx.needs_input_grad[6]
         ctx.stats = (running_mean, running_var)
         ctx.eps = float(eps)
         ctx.x_shape = tuple(x.shape)
@@ -421,10 +425,24 @@ class _BatchNorm2dEvalReLUFn(torch.autograd.Function):
         mask = torch.empty((n_el + 7) // 8, dtype=torch.uint8, device=x.device) if out_rg \
             else None
         L = _lib.lib()
-        _lib.check(L.ms_bn_eval_relu_fwd(n, c, h * w_, _dtype_code(x), _dtype_code(running_var),
-                                         _ptr(xl), _ptr(params[0]), _ptr(params[1]),
-                                         _ptr(params[2]), _ptr(params[3]), ctx.eps, _ptr(y),
-                                         _ptr(mask), _stream(x.device)), "ms_bn_eval_relu_fwd")
+        if residual is None:
+            _lib.check(L.ms_bn_eval_relu_fwd(n, c, h * w_, _dtype_code(x),
+                                             _dtype_code(running_var), _ptr(xl),
+                                             _ptr(params[0]), _ptr(params[1]), _ptr(params[2]),
+                                             _ptr(params[3]), ctx.eps, _ptr(y), _ptr(mask),
+                                             _stream(x.device)), "ms_bn_eval_relu_fwd")
+        else:
+            _require_cuda("batch_norm_add_relu", residual)
+            if residual.shape != x.shape or residual.dtype != x.dtype:
+                raise RuntimeError("bn+add+relu: residual must match the BN input's shape "
+                                   "and dtype")
+            rl = _as_layout(residual, _lib.MS_NHWC)
+            _lib.check(L.ms_bn_eval_add_relu_fwd(n, c, h * w_, _dtype_code(x),
+                                                 _dtype_code(running_var), _ptr(xl), _ptr(rl),
+                                                 _ptr(params[0]), _ptr(params[1]),
+                                                 _ptr(params[2]), _ptr(params[3]), ctx.eps,
+                                                 _ptr(y), _ptr(mask), _stream(x.device)),
+                       "ms_bn_eval_add_relu_fwd")
         ctx.save_for_backward(xl if "x" in roles else None, weight if "w" in roles else None,
                               mask)
         return y
@@ -433,10 +451,11 @@ class _BatchNorm2dEvalReLUFn(torch.autograd.Function):
     def backward(ctx, gy):
         x, weight, mask = ctx.saved_tensors
         need_x, need_w, need_b = ctx.needs_input_grad[:3]
+        need_r = ctx.needs_input_grad[6]
         running_mean, running_var = ctx.stats
         c = ctx.x_shape[1]
         mask = _need(mask, "mask", "batchnorm2d+relu backward")
-        dx = dw = db = None
+        dx = dw = db = dr = None
         if _is_meta(gy):
             if need_x:
                 dx = gy.new_empty(ctx.x_shape)
@@ -445,7 +464,9 @@ class _BatchNorm2dEvalReLUFn(torch.autograd.Function):
                 dw = gy.new_empty((c,))
             if need_b:
                 db = gy.new_empty((c,))
-            return dx, dw, db, None, None, None
+            if need_r:
+                dr = gy.new_empty(ctx.x_shape)
+            return dx, dw, db, None, None, None, dr
         if need_x and ctx.p_dtypes[0] is not None:
             weight = _need(weight, "w", "batchnorm2d dX")
         if need_w:
@@ -458,21 +479,23 @@ class _BatchNorm2dEvalReLUFn(torch.autograd.Function):
         wt = None if weight is None else weight.to(pdt_t).contiguous()
         if need_x:
             dx = torch.empty_like(g)
+        if need_r:
+            dr = torch.empty_like(g)
         dw_t = torch.empty((c,), dtype=pdt_t, device=g.device) if need_w else None
         db_t = torch.empty((c,), dtype=pdt_t, device=g.device) if need_b else None
         L = _lib.lib()
         ws, nb = _workspace(L.ms_bn_eval_workspace(n, c, h * w_, _lib.MS_NHWC)
                             if (need_w or need_b) else 0, g.device)
-        _lib.check(L.ms_bn_eval_relu_bwd(n, c, h * w_, _dtype_code(g), _dtype_code(rv), _ptr(g),
-                                         _ptr(mask), _ptr(x if need_w else None), _ptr(rm),
-                                         _ptr(rv), _ptr(wt), ctx.eps, _ptr(dx), _ptr(dw_t),
-                                         _ptr(db_t), _ptr(ws), nb, _stream(g.device)),
-                   "ms_bn_eval_relu_bwd")
+        _lib.check(L.ms_bn_eval_add_relu_bwd(n, c, h * w_, _dtype_code(g), _dtype_code(rv),
+                                             _ptr(g), _ptr(mask), _ptr(x if need_w else None),
+                                             _ptr(rm), _ptr(rv), _ptr(wt), ctx.eps, _ptr(dx),
+                                             _ptr(dr), _ptr(dw_t), _ptr(db_t), _ptr(ws), nb,
+                                             _stream(g.device)), "ms_bn_eval_add_relu_bwd")
         if need_w:
             dw = dw_t.to(ctx.p_dtypes[0])
         if need_b:
             db = db_t.to(ctx.p_dtypes[1])
-        return dx, dw, db, None, None, None
+        return dx, dw, db, None, None, None, dr
 
 
 def bn_relu_fusable(x: torch.Tensor, bn) -> bool:
@@ -487,10 +510,10 @@ def bn_relu_fusable(x: torch.Tensor, bn) -> bool:
         and _is_channels_last(x)
 
 
-def batch_norm_relu_eval(x, bn):
-    """relu(bn(x)) for an eval-mode BatchNorm2d module in one pass."""
+def batch_norm_relu_eval(x, bn, residual=None):
+    """relu(bn(x) [+ residual]) for an eval-mode BatchNorm2d module in one pass."""
     return _BatchNorm2dEvalReLUFn.apply(x, bn.weight, bn.bias, bn.running_mean, bn.running_var,
-                                        bn.eps)
+                                        bn.eps, residual)
 
 
 def batch_norm_eval(x, running_mean, running_var, weight=None, bias=None, eps=1e-5):
@@ -1214,9 +1237,10 @@ def fused_conv(x: torch.Tensor, conv, bn, relu_: bool, residual=None, tee: bool 
             x = _MaskScaleFn.apply(x, in_mask, in_bn)
         xt = x if tee else None
         y = conv(x)
-        if bn is not None and relu_ and residual is None and bn_relu_fusable(y, bn):
-            # BN not absorbable (trainable affine): BN -> ReLU still in one pass
-            return batch_norm_relu_eval(y, bn), None, xt
+        if bn is not None and relu_ and bn_relu_fusable(y, bn) and (
+                residual is None or (residual.shape == y.shape and residual.dtype == y.dtype)):
+            # BN not absorbable (trainable affine): BN [-> + residual] -> ReLU in one pass
+            return batch_norm_relu_eval(y, bn, residual), None, xt
         if bn is not None:
             y = bn(y)
         if residual is not None:

@@ -751,6 +751,46 @@ def test_bn_relu_eval_trainable_affine(shape):
                                rtol=2e-2, atol=2e-2)
 
 
+@pytest.mark.parametrize("shape,resid_cl", [((2, 64, 9, 11), True), ((3, 256, 7, 7), False),
+                                            ((2, 1024, 5, 3), True)])
+def test_bn_add_relu_eval_trainable_affine(shape, resid_cl):
+    # a bottleneck tail with a trainable BN affine: relu(bn(x) + r) in one pass; dX, dW,
+    # db and the residual's gradient g * keep (bit-exact) from one backward pass
+    n, c, h, w = shape
+    rng = np.random.default_rng(c + h + 1)
+    x, xq = _q(rng.standard_normal(shape), "bf16")
+    r, rq = _q(rng.standard_normal(shape), "bf16")
+    x = x.contiguous(memory_format=torch.channels_last).requires_grad_(True)
+    r = (r.contiguous(memory_format=torch.channels_last) if resid_cl else r).requires_grad_(True)
+    bn = torch.nn.BatchNorm2d(c).to(DEV, torch.bfloat16).eval()
+    bn.running_mean.copy_(torch.linspace(-0.5, 0.5, c))
+    bn.running_var.copy_(torch.linspace(0.5, 2.0, c))
+    bn.weight.data.copy_(torch.linspace(0.5, 1.5, c))
+    bn.bias.data.copy_(torch.linspace(-0.3, 0.3, c))
+    y = MF.batch_norm_relu_eval(x, bn, r)
+    g, gq = _q(rng.standard_normal(shape), "bf16")
+    y.backward(g.contiguous(memory_format=torch.channels_last))
+    mu = bn.running_mean.double().cpu().numpy().reshape(1, -1, 1, 1)
+    var = bn.running_var.double().cpu().numpy().reshape(1, -1, 1, 1)
+    wq = bn.weight.detach().double().cpu().numpy().reshape(1, -1, 1, 1)
+    bq = bn.bias.detach().double().cpu().numpy().reshape(1, -1, 1, 1)
+    inv = 1.0 / np.sqrt(var + 1e-5)
+    z = oracle.round_to((xq - mu) * inv * wq + bq, "bf16")
+    yd = y.detach().float().cpu().double().numpy()
+    # BN output rounded to bf16 before the add (as the unfused chain stores it): allow a
+    # couple of bf16 ulps of |z| + |r| for the fp32-vs-f64 scale and the two roundings
+    tol = 2.0 ** -6 * (np.abs(z) + np.abs(rq)) + 1e-6
+    assert (np.abs(yd - np.maximum(z + rq, 0)) <= tol).all(), "bn_add_relu y"
+    keep = yd > 0
+    gk = np.where(keep, gq, 0.0)
+    np.testing.assert_array_equal(r.grad.float().cpu().double().numpy(), gk)
+    _close(x.grad, gk * wq * inv, "bf16", "bn_add_relu dx", ulps=2.01)
+    np.testing.assert_allclose(bn.weight.grad.double().cpu().numpy(),
+                               (gk * (xq - mu) * inv).sum(axis=(0, 2, 3)), rtol=2e-2, atol=2e-2)
+    np.testing.assert_allclose(bn.bias.grad.double().cpu().numpy(), gk.sum(axis=(0, 2, 3)),
+                               rtol=2e-2, atol=2e-2)
+
+
 def test_add_relu():
     rng = np.random.default_rng(3)
     a, aq = _q(rng.standard_normal((2, 32, 9, 9)), "bf16")
@@ -798,6 +838,43 @@ def test_fused_resnet18_matches_unfused():
         y = m(xi)
         y.float().sum().backward()
         out[name] = (y.float(), xi.grad.float())
+    ry, rg = out["fp32"]
+    err = {k: (((y - ry).norm() / ry.norm()).item(), ((g - rg).norm() / rg.norm()).item())
+           for k, (y, g) in out.items() if k != "fp32"}
+    assert err["fused"][0] <= 1.2 * err["stock"][0] + 1e-3, err
+    assert err["fused"][1] <= 1.2 * err["stock"][1] + 1e-2, err
+
+
+def test_fused_resnet50_trainable_bn_matches_unfused():
+    # the ResNet-101 fine-tuning shape of workload (BN affine trainable everywhere, BN
+    # eval, input without grad) on a ResNet-50 at 96x96: every bottleneck tail runs as
+    # one BN -> +residual -> ReLU pass.  Output and BN-affine gradients must be no
+    # further from fp32 than stock bf16 is.
+    import copy
+
+    import torchvision
+
+    from benchkit.models import randomize_bn_stats
+    from paper_2404_12406_b200.nn import convert_to_memory_saving
+    torch.manual_seed(0)
+    base = torchvision.models.resnet50().eval()
+    randomize_bn_stats(base)
+    for name, prm in base.named_parameters():
+        prm.requires_grad_(".bn" in name or "downsample.1" in name or name.startswith("bn1"))
+    cl = torch.channels_last
+    models = {
+        "fp32": copy.deepcopy(base).to(DEV).to(memory_format=cl),
+        "stock": copy.deepcopy(base).to(DEV, torch.bfloat16).to(memory_format=cl),
+        "fused": convert_to_memory_saving(copy.deepcopy(base), fuse=True)
+        .to(DEV, torch.bfloat16).to(memory_format=cl),
+    }
+    x = torch.randn(4, 3, 96, 96, device=DEV).contiguous(memory_format=cl)
+    out = {}
+    for name, m in models.items():
+        y = m(x.to(torch.float32 if name == "fp32" else torch.bfloat16))
+        y.float().sum().backward()
+        gw = torch.cat([p.grad.float().flatten() for p in m.parameters() if p.requires_grad])
+        out[name] = (y.float(), gw)
     ry, rg = out["fp32"]
     err = {k: (((y - ry).norm() / ry.norm()).item(), ((g - rg).norm() / rg.norm()).item())
            for k, (y, g) in out.items() if k != "fp32"}
