@@ -192,6 +192,7 @@ __global__ void __launch_bounds__(256) bn_bwd_kernel(int64_t total, int C, int64
 // loads in flight (memory-level parallelism for HBM).
 constexpr int BN_UNR = 4;
 constexpr int BN_FWD_UNR = 8;
+constexpr int BN_BWD_UNR = 4, BN_BWD_UNR_DW = 5;
 
 template <typename T, int VEC, bool RES = false, int U = BN_FWD_UNR>
 __global__ void __launch_bounds__(256, RES ? 2 : 3) bn_fwd_nhwc_kernel(int64_t rows, int C, BnParams p,
@@ -257,7 +258,7 @@ __global__ void __launch_bounds__(256, RES ? 2 : 3) bn_fwd_nhwc_kernel(int64_t r
   }
 }
 
-template <typename T, int VEC, bool WANT_DW>
+template <typename T, int VEC, bool WANT_DW, int U = (WANT_DW ? BN_BWD_UNR_DW : BN_BWD_UNR)>
 __global__ void __launch_bounds__(256, WANT_DW ? 2 : 3) bn_bwd_nhwc_kernel(int64_t rows, int C, BnParams p,
                                                           const T* __restrict__ g,
                                                           const T* __restrict__ x,
@@ -285,37 +286,42 @@ __global__ void __launch_bounds__(256, WANT_DW ? 2 : 3) bn_bwd_nhwc_kernel(int64
       pdw[j] = pdb[j] = 0.f;
     }
     const int64_t step = (int64_t)gridDim.x * rpb;
-    for (int64_t r0 = (int64_t)blockIdx.x * rpb + rl; r0 < rows; r0 += step * BN_UNR) {
-      float gv[BN_UNR][VEC];
-      float xv[WANT_DW ? BN_UNR : 1][VEC];
-      uint32_t kb[BN_UNR];
+    // raw 16-byte loads held packed until used (see bn_fwd_nhwc_kernel)
+    static_assert(VEC * sizeof(T) == 16, "bn_bwd_nhwc: 16-byte vectors");
+    for (int64_t r0 = (int64_t)blockIdx.x * rpb + rl; r0 < rows; r0 += step * U) {
+      uint4 graw[U], xraw[WANT_DW ? U : 1];
+      uint32_t kb[U];
 #pragma unroll
-      for (int u = 0; u < BN_UNR; ++u) {
+      for (int u = 0; u < U; ++u) {
         const int64_t r = r0 + u * step;
         kb[u] = 0xffu;
         if (r < rows) {
-          load_vec<T, VEC>(g + r * C + grp * VEC, gv[u]);
-          if constexpr (WANT_DW) load_vec<T, VEC>(x + r * C + grp * VEC, xv[u]);
+          graw[u] = __ldcs(reinterpret_cast<const uint4*>(g + r * C + grp * VEC));
+          if constexpr (WANT_DW)
+            xraw[u] = __ldcs(reinterpret_cast<const uint4*>(x + r * C + grp * VEC));
           if (keep) kb[u] = keep[(r * C + grp * VEC) / 8];
         }
       }
 #pragma unroll
-      for (int u = 0; u < BN_UNR; ++u) {
+      for (int u = 0; u < U; ++u) {
         const int64_t r = r0 + u * step;
         if (r >= rows) continue;
+        const T* ge = reinterpret_cast<const T*>(&graw[u]);
+        const T* xe = reinterpret_cast<const T*>(&xraw[WANT_DW ? u : 0]);
+        float gv[VEC];
 #pragma unroll
-        for (int j = 0; j < VEC; ++j) gv[u][j] = ((kb[u] >> j) & 1u) ? gv[u][j] : 0.f;
-        if (gkeep) store_vec<T, VEC>(gkeep + r * C + grp * VEC, gv[u]);
+        for (int j = 0; j < VEC; ++j) gv[j] = ((kb[u] >> j) & 1u) ? IO<T>::ld(ge + j) : 0.f;
+        if (gkeep) store_vec<T, VEC>(gkeep + r * C + grp * VEC, gv);
         if (want_dx) {
           float o[VEC];
 #pragma unroll
-          for (int j = 0; j < VEC; ++j) o[j] = gv[u][j] * sc[j];
+          for (int j = 0; j < VEC; ++j) o[j] = gv[j] * sc[j];
           store_vec<T, VEC>(dx + r * C + grp * VEC, o);
         }
 #pragma unroll
         for (int j = 0; j < VEC; ++j) {
-          pdb[j] += gv[u][j];
-          if constexpr (WANT_DW) pdw[j] += gv[u][j] * (xv[WANT_DW ? u : 0][j] - mu[j]) * inv[j];
+          pdb[j] += gv[j];
+          if constexpr (WANT_DW) pdw[j] += gv[j] * (IO<T>::ld(xe + j) - mu[j]) * inv[j];
         }
       }
     }
@@ -475,11 +481,11 @@ ms_status bn_relu_eval_bwd(int64_t n, int64_t c, int64_t hw, int dt, const BnPar
     auto go = [&](auto tag) {
       using T = decltype(tag);
       if (dw)
-        bn_bwd_nhwc_kernel<T, 8, true><<<nhwc_grid(rows, c / 8, 2), 256, 0, st>>>(
+        bn_bwd_nhwc_kernel<T, 8, true><<<nhwc_grid(rows, c / 8, 2, BN_BWD_UNR_DW), 256, 0, st>>>(
             rows, (int)c, p, (const T*)g, (const T*)x, (T*)dx, acc_dw, acc_db, keep,
             (T*)dresid);
       else
-        bn_bwd_nhwc_kernel<T, 8, false><<<nhwc_grid(rows, c / 8, 3), 256, 0, st>>>(
+        bn_bwd_nhwc_kernel<T, 8, false><<<nhwc_grid(rows, c / 8, 3, BN_BWD_UNR), 256, 0, st>>>(
             rows, (int)c, p, (const T*)g, (const T*)x, (T*)dx, acc_dw, acc_db, keep,
             (T*)dresid);
     };
@@ -516,10 +522,10 @@ ms_status bn_eval_bwd(int64_t n, int64_t c, int64_t hw, int layout, int dt, cons
           c / V <= 256 && c <= 2048) {
         const int64_t rows = n * hw;
         if (dw)
-          bn_bwd_nhwc_kernel<T, V, true><<<nhwc_grid(rows, c / V, 2), 256, 0, st>>>(
+          bn_bwd_nhwc_kernel<T, V, true><<<nhwc_grid(rows, c / V, 2, BN_BWD_UNR_DW), 256, 0, st>>>(
               rows, (int)c, p, (const T*)g, (const T*)x, (T*)dx, acc_dw, acc_db);
         else
-          bn_bwd_nhwc_kernel<T, V, false><<<nhwc_grid(rows, c / V, 3), 256, 0, st>>>(
+          bn_bwd_nhwc_kernel<T, V, false><<<nhwc_grid(rows, c / V, 3, BN_BWD_UNR), 256, 0, st>>>(
               rows, (int)c, p, (const T*)g, (const T*)x, (T*)dx, acc_dw, acc_db);
       } else if (can_vec(c, hw, layout, V, g, dw ? x : nullptr, dx)) {
         bn_bwd_kernel<T, V><<<bn_grid(total / V, c, layout, V), 256, smem, st>>>(
