@@ -379,6 +379,18 @@ static int bn_grid(int64_t nvec, int64_t C, int layout, int vec) {
 // which its register count meets exactly).  One wave: every thread loops over
 // rows, so the per-channel constants and the dW/db block reduction (2C global
 // atomics per block) are paid once per resident block, not once per 4 rows.
+// dW/db accumulators (ws = [dw | db], fp32) to the parameter dtype: one
+// launch when the caller's outputs are adjacent too (the host's (2, C) buffer)
+static ms_status store_dw_db(const float* acc_dw, const float* acc_db, void* dw, void* db,
+                             int pdtype, int64_t c, cudaStream_t st) {
+  if (dw && db && acc_db == acc_dw + c &&
+      static_cast<char*>(db) == static_cast<char*>(dw) + c * dtype_size(pdtype))
+    return f32_to(acc_dw, dw, pdtype, 2 * c, nullptr, 1, st);
+  if (dw) MS_TRY(f32_to(acc_dw, dw, pdtype, c, nullptr, 1, st));
+  if (db) MS_TRY(f32_to(acc_db, db, pdtype, c, nullptr, 1, st));
+  return MS_OK;
+}
+
 static int bn_fwd_unr() {
   static const int u = [] {
     const char* e = getenv("MS_BN_FWD_UNR");
@@ -494,8 +506,7 @@ ms_status bn_relu_eval_bwd(int64_t n, int64_t c, int64_t hw, int dt, const BnPar
     count_launch(1, KF_BN);
     MS_TRY(launch_status("bn_bwd_nhwc_kernel (relu)"));
   }
-  if (dw) MS_TRY(f32_to(acc_dw, dw, p.pdtype, c, nullptr, 1, st));
-  if (db) MS_TRY(f32_to(acc_db, db, p.pdtype, c, nullptr, 1, st));
+  return store_dw_db(acc_dw, acc_db, dw, db, p.pdtype, c, st);
   return MS_OK;
 }
 
@@ -538,8 +549,7 @@ ms_status bn_eval_bwd(int64_t n, int64_t c, int64_t hw, int layout, int dt, cons
     count_launch(1, KF_BN);
     MS_TRY(launch_status("bn_bwd_kernel"));
   }
-  if (dw) MS_TRY(f32_to(acc_dw, dw, p.pdtype, c, nullptr, 1, st));
-  if (db) MS_TRY(f32_to(acc_db, db, p.pdtype, c, nullptr, 1, st));
+  return store_dw_db(acc_dw, acc_db, dw, db, p.pdtype, c, st);
   return MS_OK;
 }
 

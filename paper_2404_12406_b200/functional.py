@@ -370,8 +370,11 @@ class _BatchNorm2dEvalFn(torch.autograd.Function):
         wt = None if weight is None else weight.to(pdt_t).contiguous()
         if need_x:
             dx = torch.empty_like(g)
-        dw_t = torch.empty((c,), dtype=pdt_t, device=g.device) if need_w else None
-        db_t = torch.empty((c,), dtype=pdt_t, device=g.device) if need_b else None
+        if need_w and need_b:  # adjacent: the library converts both in one launch
+            dw_t, db_t = torch.empty((2, c), dtype=pdt_t, device=g.device).unbind(0)
+        else:
+            dw_t = torch.empty((c,), dtype=pdt_t, device=g.device) if need_w else None
+            db_t = torch.empty((c,), dtype=pdt_t, device=g.device) if need_b else None
         L = _lib.lib()
         ws, nb = _workspace(L.ms_bn_eval_workspace(n, c, h * w_, layout) if (need_w or need_b)
                             else 0, g.device)
@@ -481,8 +484,11 @@ class _BatchNorm2dEvalReLUFn(torch.autograd.Function):
             dx = torch.empty_like(g)
         if need_r:
             dr = torch.empty_like(g)
-        dw_t = torch.empty((c,), dtype=pdt_t, device=g.device) if need_w else None
-        db_t = torch.empty((c,), dtype=pdt_t, device=g.device) if need_b else None
+        if need_w and need_b:  # adjacent: the library converts both in one launch
+            dw_t, db_t = torch.empty((2, c), dtype=pdt_t, device=g.device).unbind(0)
+        else:
+            dw_t = torch.empty((c,), dtype=pdt_t, device=g.device) if need_w else None
+            db_t = torch.empty((c,), dtype=pdt_t, device=g.device) if need_b else None
         L = _lib.lib()
         ws, nb = _workspace(L.ms_bn_eval_workspace(n, c, h * w_, _lib.MS_NHWC)
                             if (need_w or need_b) else 0, g.device)
