@@ -751,6 +751,18 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
           float bs = 1.f, bt = 0.f;
           if (e.bn.var != nullptr && n0 + c + static_cast<int>(lane) < ncols)
             bn_fold(e.bn, n0 + c + static_cast<int>(lane), bs, bt);
+          // residual chunk prefetched ahead of the TMEM read (its latency overlaps it)
+          uint4 rpre[4];
+          bool rpre_ok = false;
+          if (e.resid != nullptr && valid && !tail && n0 + c + 32 <= ncols) {
+            const uint16_t* r16 =
+                static_cast<const uint16_t*>(e.resid) + orow * e.ldc + col_base + c;
+            if ((reinterpret_cast<uintptr_t>(r16) & 15) == 0) {
+              rpre_ok = true;
+#pragma unroll
+              for (int q = 0; q < 4; ++q) rpre[q] = __ldg(reinterpret_cast<const uint4*>(r16) + q);
+            }
+          }
           __syncwarp();  // tcgen05.ld / wait are warp-collective: reconverge invalid rows
           if (!zero) {
             tmem_ld_32x32b_x32(taddr + c, r);
@@ -810,10 +822,10 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
           if (e.resid != nullptr && valid) {  // fused residual join of a ResNet block
             const int64_t el = orow * e.ldc + col_base + c;
             const uint16_t* r16 = static_cast<const uint16_t*>(e.resid) + el;
-            if (full && (reinterpret_cast<uintptr_t>(r16) & 15) == 0) {
+            if (rpre_ok) {
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
-                const uint4 u = __ldg(reinterpret_cast<const uint4*>(r16) + q);
+                const uint4 u = rpre[q];
                 const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
                 for (int h = 0; h < 4; ++h) {

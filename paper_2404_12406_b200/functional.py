@@ -19,6 +19,7 @@ specifies but does not ship):
 from __future__ import annotations
 
 import ctypes
+import os
 
 import torch
 
@@ -1241,8 +1242,13 @@ def fused_conv(x: torch.Tensor, conv, bn, relu_: bool, residual=None, tee: bool 
     if not ok:
         if in_mask is not None:
             x = _MaskScaleFn.apply(x, in_mask, in_bn)
-        xt = x if tee else None
-        y = conv(x)
+        if tee and _FALLBACK_TEE and conv_relu_fusable(x, conv):
+            # the conv alone still runs tee'd: x's other gradient summed in its dgrad
+            y, _, xt = _ConvBNFn.apply(x, conv.weight, conv.bias, None, conv.stride,
+                                       conv.padding, None, False, True)
+        else:
+            xt = x if tee else None
+            y = conv(x)
         if bn is not None and relu_ and bn_relu_fusable(y, bn) and (
                 residual is None or (residual.shape == y.shape and residual.dtype == y.dtype)):
             # BN not absorbable (trainable affine): BN [-> + residual] -> ReLU in one pass
@@ -1279,6 +1285,13 @@ def conv_bn_relu_tee(x: torch.Tensor, conv, bn, with_relu: bool):
     replaces the engine's separate accumulation pass over the two gradients."""
     y, _, xt = fused_conv(x, conv, bn, with_relu, tee=True)
     return y, xt
+
+
+# a tee'd conv runs through the fused kernel on the unfused (trainable-BN) path
+# too, so the block input's second gradient is summed in the dgrad epilogue
+# (residual-style addend prefetched ahead of the TMEM read) instead of by an
+# autograd add; MS_FALLBACK_TEE=0 restores the plain module call
+_FALLBACK_TEE = os.environ.get("MS_FALLBACK_TEE", "1") == "1"
 
 
 def conv_relu_fusable(x: torch.Tensor, conv) -> bool:
