@@ -1,13 +1,16 @@
-"""Alias of :mod:`paper_2404_12406_b200.nn` under the upstream package name."""
+"""Alias of :mod:`paper_2404_12406_b200.nn` under the upstream package name:
+every MemSave layer, the converter and the fusion pass."""
 
 from paper_2404_12406_b200.nn import (  # noqa: F401
     MemSaveBatchNorm2d,
     MemSaveConv2d,
+    MemSaveConvTranspose2d,
+    MemSaveDropout,
+    MemSaveLayerNorm,
     MemSaveLinear,
     MemSaveMaxPool2d,
     MemSaveReLU,
     convert_to_memory_saving,
+    fuse_conv_bn_relu,
 )
-
-__all__ = ["MemSaveLinear", "MemSaveConv2d", "MemSaveBatchNorm2d", "MemSaveReLU",
-           "MemSaveMaxPool2d", "convert_to_memory_saving"]
+from paper_2404_12406_b200.nn import __all__  # noqa: F401

@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(256) bn_bwd_kernel(int64_t total, int C, int64
 // per-channel constants live in registers, each thread keeps UNR 16-byte
 // loads in flight (memory-level parallelism for HBM).
 constexpr int BN_UNR = 4;
-constexpr int BN_FWD_UNR = 8;
+constexpr int BN_FWD_UNR = 6;  // 8 spilled under the 3-block register cap
 constexpr int BN_BWD_UNR = 4, BN_BWD_UNR_DW = 5;
 
 template <typename T, int VEC, bool RES = false, int U = BN_FWD_UNR>

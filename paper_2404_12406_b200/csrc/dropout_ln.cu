@@ -412,39 +412,61 @@ __global__ void __launch_bounds__(256) ln_fwd_generic(int64_t rows, int D, const
   }
 }
 
-// backward, one warp per row (grid-stride over rows); dw / db partial sums in
-// registers, reduced per block through shared memory, then one fp32 atomic per
-// column per block into the workspace
+// backward, one warp per row (grid-stride over rows).  dw / db partial sums:
+// in registers for rows of <= 1024 16-bit elements (KV <= 4); for longer rows
+// (KV > 4) the partials live in per-warp shared-memory slices (each lane owns
+// its 8-column chunks, so no atomics) and the weight row is read from shared
+// memory, which keeps the row's x-hat and g in registers without spilling.
+// The per-warp partials are reduced per block and added into the workspace with
+// one fp32 atomic per column per block.
+template <int KV>
+struct LnBwdSmem {
+  static constexpr bool PS = KV > 4;  // partials + weight row in shared memory
+};
+
 template <typename T, int KV, bool WANTP>
 __global__ void __launch_bounds__(LN_WARPS * 32) ln_bwd_vec(int64_t rows, int D, const T* g,
                                                             const T* x, const float* mean,
                                                             const float* rstd, const T* w, T* dx,
                                                             float* dw_acc, float* db_acc) {
-  extern __shared__ float sacc[];  // [2][D] when dw / db are requested
-  const int lane = threadIdx.x & 31;
+  // shared memory: register partials -> sacc[2][D];
+  //                smem partials    -> part[LN_WARPS][2][D], then wrow[D]
+  extern __shared__ float sacc[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   constexpr bool wantp = WANTP;
-  if constexpr (wantp) {
+  constexpr bool ps = WANTP && LnBwdSmem<KV>::PS;
+  float* part = sacc + (size_t)wid * 2 * D;       // this warp's [2][D] slice (ps)
+  float* wrow = sacc + (size_t)LN_WARPS * 2 * D;  // weight row (ps)
+  if constexpr (ps) {
+    for (int i = threadIdx.x; i < LN_WARPS * 2 * D; i += blockDim.x) sacc[i] = 0.f;
+    for (int i = threadIdx.x; i < D; i += blockDim.x) wrow[i] = w ? IO<T>::ld(w + i) : 1.f;
+    __syncthreads();
+  } else if constexpr (wantp) {
     for (int i = threadIdx.x; i < 2 * D; i += blockDim.x) sacc[i] = 0.f;
     __syncthreads();
   }
-  float wv[KV][8];
+  float wv[ps ? 1 : KV][8];
+  float pw[ps ? 1 : KV][8], pb[ps ? 1 : KV][8];
+  if constexpr (!ps) {
 #pragma unroll
-  for (int k = 0; k < KV; ++k) {
-    const int col = (k * 32 + lane) * 8;
-    if (col < D && w) {
-      ld8<T>(w + col, wv[k], true);
-    } else {
+    for (int k = 0; k < KV; ++k) {
+      const int col = (k * 32 + lane) * 8;
+      if (col < D && w) {
+        ld8<T>(w + col, wv[k], true);
+      } else {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) wv[k][j] = 1.f;
+        for (int j = 0; j < 8; ++j) wv[k][j] = 1.f;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) pw[k][j] = pb[k][j] = 0.f;
     }
   }
-  float pw[KV][8], pb[KV][8];
-#pragma unroll
-  for (int k = 0; k < KV; ++k)
-#pragma unroll
-    for (int j = 0; j < 8; ++j) pw[k][j] = pb[k][j] = 0.f;
+  auto wget = [&](int k, int j) -> float {
+    if constexpr (ps) return wrow[(k * 32 + lane) * 8 + j];
+    else return wv[k][j];
+  };
   const int64_t step = (int64_t)gridDim.x * LN_WARPS;
-  for (int64_t row = (int64_t)blockIdx.x * LN_WARPS + (threadIdx.x >> 5); row < rows; row += step) {
+  for (int64_t row = (int64_t)blockIdx.x * LN_WARPS + wid; row < rows; row += step) {
     const float mu = mean[row], r = rstd[row];
     float xh[KV][8], gv[KV][8];
     float a = 0.f, c = 0.f;
@@ -457,10 +479,30 @@ __global__ void __launch_bounds__(LN_WARPS * 32) ln_bwd_vec(int64_t rows, int D,
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           xh[k][j] = (xh[k][j] - mu) * r;
-          const float gw = gv[k][j] * wv[k][j];
+          const float gw = gv[k][j] * wget(k, j);
           a += gw;
           c += gw * xh[k][j];
-          if constexpr (wantp) {
+        }
+        if constexpr (ps) {
+          float4* pw4 = reinterpret_cast<float4*>(part + col);
+          float4* pb4 = reinterpret_cast<float4*>(part + D + col);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            float4 u = pw4[h], v = pb4[h];
+            u.x += gv[k][4 * h] * xh[k][4 * h];
+            u.y += gv[k][4 * h + 1] * xh[k][4 * h + 1];
+            u.z += gv[k][4 * h + 2] * xh[k][4 * h + 2];
+            u.w += gv[k][4 * h + 3] * xh[k][4 * h + 3];
+            v.x += gv[k][4 * h];
+            v.y += gv[k][4 * h + 1];
+            v.z += gv[k][4 * h + 2];
+            v.w += gv[k][4 * h + 3];
+            pw4[h] = u;
+            pb4[h] = v;
+          }
+        } else if constexpr (wantp) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
             pw[k][j] += gv[k][j] * xh[k][j];
             pb[k][j] += gv[k][j];
           }
@@ -475,13 +517,22 @@ __global__ void __launch_bounds__(LN_WARPS * 32) ln_bwd_vec(int64_t rows, int D,
         if (col < D) {
           float o[8];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) o[j] = r * (gv[k][j] * wv[k][j] - ma - xh[k][j] * mc);
+          for (int j = 0; j < 8; ++j) o[j] = r * (gv[k][j] * wget(k, j) - ma - xh[k][j] * mc);
           st8<T>(dx + row * D + col, o, true);
         }
       }
     }
   }
-  if constexpr (wantp) {
+  if constexpr (ps) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < 2 * D; i += blockDim.x) {
+      float t = 0.f;
+#pragma unroll
+      for (int q = 0; q < LN_WARPS; ++q) t += sacc[(size_t)q * 2 * D + i];
+      float* dst = i < D ? dw_acc : db_acc;
+      if (dst) atomicAdd(&dst[i < D ? i : i - D], t);
+    }
+  } else if constexpr (wantp) {
 #pragma unroll
     for (int k = 0; k < KV; ++k) {
       const int col = (k * 32 + lane) * 8;
@@ -630,12 +681,19 @@ extern "C" ms_status ms_layernorm_bwd(int64_t rows, int64_t dim, int32_t dt, con
       int64_t grid = (rows + LN_WARPS - 1) / LN_WARPS;
       if (wantp && grid > (int64_t)num_sms() * 4) grid = num_sms() * 4;  // amortise the atomics
       if (grid > (1ll << 30)) grid = 1ll << 30;
-      const size_t smem = wantp ? 2 * D * sizeof(float) : 0;
       if (wantp) {
-        MS_DT_DISPATCH(dt, MS_KV_SWITCH(kv, (ln_bwd_vec<T, KV, true><<<(unsigned)grid,
-                                                                       LN_WARPS * 32, smem, st>>>(
-                                                rows, D, (const T*)g, (const T*)x, mean, rstd,
-                                                (const T*)w, (T*)dx, dwa, dba))));
+        MS_DT_DISPATCH(dt, MS_KV_SWITCH(kv, ({
+          const size_t smem = LnBwdSmem<KV>::PS ? (size_t)(LN_WARPS * 2 + 1) * D * sizeof(float)
+                                                : (size_t)2 * D * sizeof(float);
+          auto kern = ln_bwd_vec<T, KV, true>;
+          if (smem > 48 * 1024)
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+          int64_t gr = grid;
+          if (LnBwdSmem<KV>::PS && gr > (int64_t)num_sms()) gr = num_sms();  // 1 block / SM
+          kern<<<(unsigned)gr, LN_WARPS * 32, smem, st>>>(rows, D, (const T*)g, (const T*)x,
+                                                          mean, rstd, (const T*)w, (T*)dx, dwa,
+                                                          dba);
+        })));
       } else {
         MS_DT_DISPATCH(dt, MS_KV_SWITCH(kv, (ln_bwd_dx_vec<T, KV><<<
                                (unsigned)((rows + LN_WARPS * LnRows<KV>::BWD - 1) /

@@ -1045,7 +1045,10 @@ class _ConvBNFn(torch.autograd.Function):
         if gy is None:  # grads are not materialised (set_materialize_grads(False))
             if g_tee is None or not ctx.needs_input_grad[0]:
                 return (None,) + nones
-            return (_mask_scale(g_tee, keep, ctx.in_bn) if keep is not None else g_tee,) + nones
+            if keep is None:
+                return (g_tee,) + nones
+            # the keep mask follows the kernel layout's element order (channel = idx % C)
+            return (_mask_scale(_as_layout(g_tee, ctx.layouts[0]), keep, ctx.in_bn),) + nones
         need_x, need_w, need_b = ctx.needs_input_grad[:3]
         x_shape, w_shape, stride, padding = ctx.geom
         dx = dw = db = None
@@ -1174,7 +1177,11 @@ class _MaskScaleFn(torch.autograd.Function):
         ctx.save_for_backward(mask)
         ctx.fmt = torch.channels_last if _is_channels_last(y) and not y.is_contiguous() \
             else torch.contiguous_format
-        return y.view_as(y)
+        # y (the fused conv's fresh output, saved by nobody) is returned as itself and
+        # marked dirty rather than as a view, so in-place consumers (ReLU(inplace=True),
+        # add_, inplace dropout) stay legal as on the unfused layers
+        ctx.mark_dirty(y)
+        return y
 
     @staticmethod
     def backward(ctx, gy):
@@ -1212,8 +1219,9 @@ def conv_bn_fusable(x: torch.Tensor, conv, bn) -> bool:
 
 
 def _relu_keep_mask(y: torch.Tensor) -> torch.Tensor:
-    # a ReLU folded into a fused call keeps its MemSave storage (bit mask)
-    return relu(y) if y.device.type in ("cuda", "meta") else torch.relu(y)
+    # a ReLU folded into a fused call keeps its MemSave storage (bit mask); CPU
+    # tensors raise inside relu() like every other entry point (no CPU path)
+    return relu(y)
 
 
 def fused_conv(x: torch.Tensor, conv, bn, relu_: bool, residual=None, tee: bool = False,
@@ -1236,13 +1244,18 @@ def fused_conv(x: torch.Tensor, conv, bn, relu_: bool, residual=None, tee: bool 
     if in_mask is None:
         in_bn = None
     ok = conv_bn_fusable(x, conv, bn) if bn is not None else conv_relu_fusable(x, conv)
-    if residual is not None:
-        ok = ok and residual.dtype == x.dtype and residual.device == x.device \
-            and residual.dim() == 4
+    if ok and residual is not None:
+        # the epilogue reads the residual at full output indexing: no broadcasting
+        oh, ow = _conv_out_hw(x.shape, conv.weight.shape, _pair(conv.stride), _pair(conv.padding))
+        ok = residual.dtype == x.dtype and residual.device == x.device \
+            and tuple(residual.shape) == (x.shape[0], conv.out_channels, oh, ow)
+    # tee only a differentiable x: otherwise the alias would make x's other
+    # consumer see requires_grad=True and run (and save for) a discarded dgrad
+    tee_grad = tee and x.requires_grad
     if not ok:
         if in_mask is not None:
             x = _MaskScaleFn.apply(x, in_mask, in_bn)
-        if tee and _FALLBACK_TEE and conv_relu_fusable(x, conv):
+        if tee_grad and _FALLBACK_TEE and conv_relu_fusable(x, conv):
             # the conv alone still runs tee'd: x's other gradient summed in its dgrad
             y, _, xt = _ConvBNFn.apply(x, conv.weight, conv.bias, None, conv.stride,
                                        conv.padding, None, False, True)
@@ -1261,14 +1274,15 @@ def fused_conv(x: torch.Tensor, conv, bn, relu_: bool, residual=None, tee: bool 
             y = _relu_keep_mask(y)
         return y, None, xt
     outs = _ConvBNFn.apply(x, conv.weight, conv.bias, residual, conv.stride, conv.padding, bn,
-                           relu_, tee, in_mask, in_bn)
+                           relu_, tee_grad, in_mask, in_bn)
     y, mask = outs[0], outs[1]
     if relu_ and mask is not None and not raw:
         # conv -> BN -> ReLU: g * keep * s; with a residual (BN scale folded into the
         # dgrad weight) or without a BN: g * keep
         y = _MaskScaleFn.apply(y, mask, bn if residual is None else None)
         mask = None
-    return y, (mask if raw else None), (outs[2] if tee else None)
+    alias = outs[2] if tee_grad else (x if tee else None)
+    return y, (mask if raw else None), alias
 
 
 def conv_bn_relu(x: torch.Tensor, conv, bn, with_relu: bool) -> torch.Tensor:

@@ -273,7 +273,8 @@ def _is_add(node) -> bool:
     return False
 
 
-def fuse_conv_bn_relu(model: nn.Module, verbose: bool = False) -> nn.Module:
+def fuse_conv_bn_relu(model: nn.Module, verbose: bool = False,
+                      kinds: dict | None = None) -> nn.Module:
     """Graph pass (torch.fx) that fuses, without changing parameters, buffers or
     state_dict keys:
 
@@ -288,8 +289,20 @@ def fuse_conv_bn_relu(model: nn.Module, verbose: bool = False) -> nn.Module:
 
     Each intermediate is consumed only by the next op of the chain.  The saved
     set is the union of the fused layers' storage rules.  Models that torch.fx
-    cannot trace are returned unchanged."""
+    cannot trace are returned unchanged.
+
+    ``kinds`` (the converter's kind filter, e.g. ``{"conv2d": False}``): a chain
+    is fused only if every layer in it is of an enabled kind, so a disabled
+    kind keeps its stock module and its stock storage."""
     import torch.fx as fx
+
+    kinds = {} if kinds is None else kinds
+    conv_types = (nn.Conv2d, MemSaveConv2d) if kinds.get("conv2d", True) else ()
+    bn_ok = kinds.get("batchnorm2d", True)
+    relu_ok = kinds.get("relu", True)
+
+    def is_relu(node):
+        return relu_ok and _is_relu(node, modules)
 
     class _Tracer(fx.Tracer):  # the memsave layers are leaves, like torch.nn layers
         def is_leaf_module(self, m, qualname):
@@ -305,15 +318,16 @@ def fuse_conv_bn_relu(model: nn.Module, verbose: bool = False) -> nn.Module:
     g = gm.graph
     nfused = nadd = 0
     for node in list(g.nodes):
-        if node.op != "call_module" or not isinstance(modules.get(node.target), nn.BatchNorm2d):
+        if (not bn_ok or node.op != "call_module"
+                or not isinstance(modules.get(node.target), nn.BatchNorm2d)):
             continue
         src = node.args[0] if node.args else None
         if (not isinstance(src, fx.Node) or src.op != "call_module"
-                or type(modules.get(src.target)) not in (nn.Conv2d, MemSaveConv2d)
+                or type(modules.get(src.target)) not in conv_types
                 or len(src.users) != 1 or len(node.args) != 1 or node.kwargs):
             continue
         users = list(node.users)
-        relu_node = users[0] if len(users) == 1 and _is_relu(users[0], modules) else None
+        relu_node = users[0] if len(users) == 1 and is_relu(users[0]) else None
         last = relu_node or node
         with g.inserting_before(node):
             conv_ref = g.get_attr(src.target)
@@ -328,7 +342,7 @@ def fuse_conv_bn_relu(model: nn.Module, verbose: bool = False) -> nn.Module:
         if not _is_add(node) or len(node.users) != 1:
             continue
         r = next(iter(node.users))
-        if not _is_relu(r, modules):
+        if not is_relu(r):
             continue
         a, b = node.args
         if not (isinstance(a, fx.Node) and isinstance(b, fx.Node)):
@@ -342,11 +356,10 @@ def fuse_conv_bn_relu(model: nn.Module, verbose: bool = False) -> nn.Module:
     # conv -> relu without a BN (VGG): ReLU and its mask in the conv epilogue
     nrelu = 0
     for node in list(g.nodes):
-        if node.op != "call_module" or type(modules.get(node.target)) not in (nn.Conv2d,
-                                                                             MemSaveConv2d):
+        if node.op != "call_module" or type(modules.get(node.target)) not in conv_types:
             continue
         users = list(node.users)
-        if len(users) != 1 or not _is_relu(users[0], modules) or len(node.args) != 1:
+        if len(users) != 1 or not is_relu(users[0]) or len(node.args) != 1:
             continue
         with g.inserting_before(node):
             conv_ref = g.get_attr(node.target)
@@ -496,5 +509,5 @@ def convert_to_memory_saving(model: nn.Module, linear: bool = True, conv2d: bool
 
     walk(model, "")
     if fuse:
-        return fuse_conv_bn_relu(model, verbose=verbose)
+        return fuse_conv_bn_relu(model, verbose=verbose, kinds=kinds)
     return model
