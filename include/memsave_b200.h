@@ -310,6 +310,12 @@ MS_API int64_t ms_launch_count(void);
 /* launches by kernel family: [0] tcgen05 GEMM/implicit-GEMM, [1] SIMT (CUDA-core)
  * GEMM/conv, [2] batchnorm, [3] reductions / casts / repacks */
 MS_API void ms_launch_stats(int64_t* out4);
+/* Caller contract for the calling thread: `device_plus_one` = d + 1 declares
+ * that CUDA device d owns every operand of the following calls (the PyTorch op
+ * layer passes the tensors' device), so entry points skip their per-call
+ * pointer-attribute query and only make d current; 0 (default) restores the
+ * query.  ctypes / FFI callers need not care. */
+MS_API void ms_set_device_bound(int32_t device_plus_one);
 
 #ifdef __cplusplus
 }

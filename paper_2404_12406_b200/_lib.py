@@ -106,6 +106,7 @@ SIGNATURES = {
     "ms_version": (_c_i32, []),
     "ms_launch_count": (_c_i64, []),
     "ms_launch_stats": (None, [ctypes.POINTER(_c_i64)]),
+    "ms_set_device_bound": (None, [_c_i32]),
 }
 
 _lock = threading.Lock()

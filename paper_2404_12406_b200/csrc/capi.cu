@@ -16,7 +16,10 @@ extern "C" const char* ms_status_string(int32_t s) {
 
 namespace ms {
 const char* last_error();
+void set_device_bound(int on);
 }
+
+extern "C" void ms_set_device_bound(int32_t on) { ms::set_device_bound(on); }
 
 extern "C" const char* ms_last_error(void) { return ms::last_error(); }
 extern "C" int32_t ms_version(void) { return 1; }

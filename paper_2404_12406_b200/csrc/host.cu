@@ -33,7 +33,22 @@ ms_status launch_status(const char* what) {
   return MS_OK;
 }
 
+static thread_local int t_device_bound = 0;
+void set_device_bound(int on) { t_device_bound = on; }
+
 ms_status bind_device(const void* p) {
+  if (t_device_bound > 0) {
+    // ms_set_device_bound(dev + 1): the caller named the device; no pointer query.
+    // cudaSetDevice still runs: it makes the device's primary context current on
+    // this thread (an autograd worker thread may have none yet, and the tensor-map
+    // encoders are driver calls)
+    if (cudaSetDevice(t_device_bound - 1) != cudaSuccess) {
+      set_error("cudaSetDevice(%d) failed", t_device_bound - 1);
+      cudaGetLastError();
+      return MS_ERR_LAUNCH;
+    }
+    return MS_OK;
+  }
   // The autograd engine calls backward on its own device thread, where neither
   // this library's runtime nor the driver API has a current context yet: bind
   // the device that owns the operand before any driver call (tensor-map

@@ -18,12 +18,12 @@ specifies but does not ship):
 
 from __future__ import annotations
 
-import ctypes
 import os
 
 import torch
 
 from . import _lib
+from ._ops import ops as _ops
 from .rules import MissingSavedValue, saved_roles
 
 _DT = {torch.float32: _lib.MS_F32, torch.bfloat16: _lib.MS_BF16, torch.float16: _lib.MS_F16}
@@ -37,33 +37,9 @@ def _dtype_code(t: torch.Tensor) -> int:
                         f"bfloat16 or float16") from None
 
 
-def _ptr(t):
-    # plain ints: the ctypes signatures declare c_void_p, which converts them
-    return None if t is None else t.data_ptr()
-
-
-def _stream(dev: torch.device):
-    # the raw cudaStream_t of the current stream, without a torch.cuda.Stream object
-    idx = dev.index if dev.index is not None else torch.cuda.current_device()
-    return torch._C._cuda_getCurrentRawStream(idx)
-
-
-_LIN_WS: dict = {}
-
-
-def _linear_ws(L, M, N, K, dt, pass_):
-    """ms_linear_workspace, memoised per shape (the plan is a pure function of it)."""
-    key = (M, N, K, dt, pass_)
-    nb = _LIN_WS.get(key)
-    if nb is None:
-        nb = _LIN_WS[key] = int(L.ms_linear_workspace(M, N, K, dt, pass_))
-    return nb
-
-
-def _workspace(nbytes: int, dev: torch.device):
-    if not nbytes:
-        return None, 0
-    return torch.empty(int(nbytes), dtype=torch.uint8, device=dev), int(nbytes)
+def _opt(t, want: bool):
+    """An op output that is empty when the product was not requested -> None."""
+    return t if want else None
 
 
 def _is_meta(*ts) -> bool:
@@ -105,19 +81,10 @@ class _LinearFn(torch.autograd.Function):
         _require_cuda("linear", x, weight, bias)
         if weight.dtype != x.dtype:
             raise TypeError(f"linear: input dtype {x.dtype} != weight dtype {weight.dtype}")
-        x2 = x.reshape(-1, K).contiguous()
-        w = weight.contiguous()
-        b = None if bias is None else bias.to(x.dtype).contiguous()
-        M = x2.shape[0]
-        # allocated in its final shape: returning a view of an internal buffer would
-        # make in-place consumers (e.g. ReLU(inplace=True)) illegal for autograd
-        y = torch.empty(out_shape, dtype=x.dtype, device=x.device)
-        L = _lib.lib()
-        dt = _dtype_code(x)
-        ws, nb = _workspace(_linear_ws(L, M, N, K, dt, 0), x.device)
-        _lib.check(L.ms_linear_fwd(M, N, K, dt, _ptr(x2), _ptr(w), _ptr(b), _ptr(y), _ptr(ws), nb,
-                                   _stream(x.device)), "ms_linear_fwd")
-        return y
+        _dtype_code(x)
+        # allocated in its final shape by the op: returning a view of an internal
+        # buffer would make in-place consumers (ReLU(inplace=True)) illegal
+        return _ops().linear_fwd(x, weight, bias)
 
     @staticmethod
     def backward(ctx, gy):
@@ -134,31 +101,15 @@ class _LinearFn(torch.autograd.Function):
             if need_b:
                 db = gy.new_empty((N,))
             return dx, dw, db
-        g2 = gy.reshape(-1, N).contiguous()
-        M = g2.shape[0]
-        L = _lib.lib()
-        dt = _dtype_code(g2)
-        st = _stream(g2.device)
+        O = _ops()
         if need_x:
             w = _need(w, "w", "linear dX")
-            K = w.shape[1]
-            dx = torch.empty(ctx.x_shape, dtype=g2.dtype, device=g2.device)
-            ws, nb = _workspace(_linear_ws(L, M, N, K, dt, 1), g2.device)
-            _lib.check(L.ms_linear_dx(M, N, K, dt, _ptr(g2), _ptr(w.contiguous()), _ptr(dx),
-                                      _ptr(ws), nb, st), "ms_linear_dx")
+            dx = O.linear_dx(gy, w, list(ctx.x_shape))
         if need_w:
             x = _need(x, "x", "linear dW")
-            K = x.shape[-1]
-            x2 = x.reshape(-1, K).contiguous()
-            dw = torch.empty((N, K), dtype=g2.dtype, device=g2.device)
-            ws, nb = _workspace(_linear_ws(L, M, N, K, dt, 2), g2.device)
-            _lib.check(L.ms_linear_dw(M, N, K, dt, _ptr(x2), _ptr(g2), _ptr(dw), _ptr(ws), nb, st),
-                       "ms_linear_dw")
+            dw = O.linear_dw(x, gy)
         if need_b:
-            db = torch.empty((N,), dtype=g2.dtype, device=g2.device)
-            ws, nb = _workspace(L.ms_bias_grad_workspace(M, N, dt), g2.device)
-            _lib.check(L.ms_bias_grad(M, N, dt, _ptr(g2), _ptr(db), _ptr(ws), nb, st),
-                       "ms_bias_grad")
+            db = O.bias_grad(gy, N)
         return dx, dw, db
 
 
@@ -194,13 +145,10 @@ def _as_layout(t: torch.Tensor, layout: int) -> torch.Tensor:
     return t.contiguous()
 
 
-def _conv_desc(x_shape, w_shape, stride, padding, layout, wlayout, dt) -> _lib.ConvDesc:
-    n, c, h, w = x_shape
-    k, c2, r, s = w_shape
-    if c2 != c:
-        raise RuntimeError(f"conv2d: input channels {c} != weight channels {c2} (groups unsupported)")
-    return _lib.ConvDesc(n, c, h, w, k, r, s, stride[0], stride[1], padding[0], padding[1],
-                         layout, wlayout, dt)
+def _check_conv_channels(x_shape, w_shape) -> None:
+    if w_shape[1] != x_shape[1]:
+        raise RuntimeError(f"conv2d: input channels {x_shape[1]} != weight channels {w_shape[1]} "
+                           f"(groups unsupported)")
 
 
 def _conv_out_hw(x_shape, w_shape, stride, padding):
@@ -210,11 +158,6 @@ def _conv_out_hw(x_shape, w_shape, stride, padding):
         raise RuntimeError(f"conv2d: empty output for input {tuple(x_shape)} / kernel "
                            f"{tuple(w_shape)}")
     return oh, ow
-
-
-def _empty4(shape, like: torch.Tensor, layout: int):
-    mf = torch.channels_last if layout == _lib.MS_NHWC else torch.contiguous_format
-    return torch.empty(shape, dtype=like.dtype, device=like.device, memory_format=mf)
 
 
 class _Conv2dFn(torch.autograd.Function):
@@ -242,15 +185,9 @@ class _Conv2dFn(torch.autograd.Function):
         wl = _as_layout(weight, wlayout)
         ctx.layouts = (layout, wlayout)
         ctx.save_for_backward(xl if "x" in roles else None, wl if "w" in roles else None)
-        dt = _dtype_code(x)
-        d = _conv_desc(x.shape, weight.shape, stride, padding, layout, wlayout, dt)
-        y = _empty4(out_shape, x, layout)
-        b = None if bias is None else bias.to(x.dtype).contiguous()
-        L = _lib.lib()
-        ws, nb = _workspace(L.ms_conv2d_workspace(ctypes.byref(d), _lib.MS_CONV_FWD), x.device)
-        _lib.check(L.ms_conv2d_fwd(ctypes.byref(d), _ptr(xl), _ptr(wl), _ptr(b), _ptr(y), _ptr(ws),
-                                   nb, _stream(x.device)), "ms_conv2d_fwd")
-        return y
+        _dtype_code(x)
+        _check_conv_channels(x.shape, weight.shape)
+        return _ops().conv2d_fwd(xl, wl, bias, list(stride), list(padding), layout, wlayout)
 
     @staticmethod
     def backward(ctx, gy):
@@ -274,29 +211,16 @@ class _Conv2dFn(torch.autograd.Function):
             return dx, dw, db, None, None
         layout, wlayout = ctx.layouts
         g = _as_layout(gy, layout)
-        dt = _dtype_code(g)
-        d = _conv_desc(x_shape, w_shape, stride, padding, layout, wlayout, dt)
-        L = _lib.lib()
-        st = _stream(g.device)
+        O = _ops()
+        geo = (list(stride), list(padding), layout, wlayout)
         if need_x:
             w = _need(w, "w", "conv2d dX")
-            dx = _empty4(x_shape, g, layout)
-            ws, nb = _workspace(L.ms_conv2d_workspace(ctypes.byref(d), _lib.MS_CONV_DX), g.device)
-            _lib.check(L.ms_conv2d_dx(ctypes.byref(d), _ptr(g), _ptr(w), _ptr(dx), _ptr(ws), nb,
-                                      st), "ms_conv2d_dx")
+            dx = O.conv2d_dx(g, w, list(x_shape), *geo)
         if need_w:
             x = _need(x, "x", "conv2d dW")
-            dw = torch.empty(w_shape, dtype=w_dtype, device=g.device,
-                             memory_format=torch.channels_last if wlayout == _lib.MS_NHWC
-                             else torch.contiguous_format)
-            ws, nb = _workspace(L.ms_conv2d_workspace(ctypes.byref(d), _lib.MS_CONV_DW), g.device)
-            _lib.check(L.ms_conv2d_dw(ctypes.byref(d), _ptr(x), _ptr(g), _ptr(dw), _ptr(ws), nb,
-                                      st), "ms_conv2d_dw")
+            dw = O.conv2d_dw(x, g, list(w_shape), *geo)
         if need_b:
-            db = torch.empty((w_shape[0],), dtype=g.dtype, device=g.device)
-            ws, nb = _workspace(4 * w_shape[0], g.device)
-            _lib.check(L.ms_conv2d_db(ctypes.byref(d), _ptr(g), _ptr(db), _ptr(ws), nb, st),
-                       "ms_conv2d_db")
+            db = O.conv2d_db(g, list(x_shape), list(w_shape), *geo)
         return dx, dw, db, None, None
 
 
@@ -329,18 +253,8 @@ class _BatchNorm2dEvalFn(torch.autograd.Function):
         xl = _as_layout(x, layout)
         ctx.layout = layout
         ctx.save_for_backward(xl if "x" in roles else None, weight if "w" in roles else None)
-        n, c, h, w_ = x.shape
-        pdt_t = running_var.dtype
-        params = [t if (t is None or t.dtype == pdt_t) else t.to(pdt_t)
-                  for t in (running_mean, running_var, weight, bias)]
-        params = [None if t is None else t.contiguous() for t in params]
-        y = torch.empty_like(xl)
-        L = _lib.lib()
-        _lib.check(L.ms_bn_eval_fwd(n, c, h * w_, layout, _dtype_code(x), _dtype_code(running_var),
-                                    _ptr(xl), _ptr(params[0]), _ptr(params[1]), _ptr(params[2]),
-                                    _ptr(params[3]), ctx.eps, _ptr(y), None, 0,
-                                    _stream(x.device)), "ms_bn_eval_fwd")
-        return y
+        _dtype_code(x)
+        return _ops().bn_eval_fwd(xl, running_mean, running_var, weight, bias, ctx.eps, layout)
 
     @staticmethod
     def backward(ctx, gy):
@@ -364,29 +278,15 @@ class _BatchNorm2dEvalFn(torch.autograd.Function):
             x = _need(x, "x", "batchnorm2d dW")
         layout = ctx.layout
         g = _as_layout(gy, layout)
-        n, _, h, w_ = ctx.x_shape
-        pdt_t = running_var.dtype
-        rm = running_mean.to(pdt_t).contiguous()
-        rv = running_var.contiguous()
-        wt = None if weight is None else weight.to(pdt_t).contiguous()
-        if need_x:
-            dx = torch.empty_like(g)
-        if need_w and need_b:  # adjacent: the library converts both in one launch
-            dw_t, db_t = torch.empty((2, c), dtype=pdt_t, device=g.device).unbind(0)
-        else:
-            dw_t = torch.empty((c,), dtype=pdt_t, device=g.device) if need_w else None
-            db_t = torch.empty((c,), dtype=pdt_t, device=g.device) if need_b else None
-        L = _lib.lib()
-        ws, nb = _workspace(L.ms_bn_eval_workspace(n, c, h * w_, layout) if (need_w or need_b)
-                            else 0, g.device)
-        _lib.check(L.ms_bn_eval_bwd(n, c, h * w_, layout, _dtype_code(g), _dtype_code(rv), _ptr(g),
-                                    _ptr(x if need_w else None), _ptr(rm), _ptr(rv), _ptr(wt),
-                                    ctx.eps, _ptr(dx), _ptr(dw_t), _ptr(db_t), _ptr(ws), nb,
-                                    _stream(g.device)), "ms_bn_eval_bwd")
+        # dW and db come back as the two rows of one [2, C] statistics-dtype buffer
+        dx_t, dwdb = _ops().bn_eval_bwd(g, x if need_w else None, running_mean, running_var,
+                                        weight, ctx.eps, layout, bool(need_x), bool(need_w),
+                                        bool(need_b))
+        dx = _opt(dx_t, need_x)
         if need_w:
-            dw = dw_t.to(ctx.p_dtypes[0])
+            dw = dwdb[0].to(ctx.p_dtypes[0])
         if need_b:
-            db = db_t.to(ctx.p_dtypes[1])
+            db = dwdb[1].to(ctx.p_dtypes[1])
         return dx, dw, db, None, None, None
 
 
@@ -420,33 +320,16 @@ class _BatchNorm2dEvalReLUFn(torch.autograd.Function):
             return x.new_empty(x.shape)
         _require_cuda("batch_norm_relu", x, weight, bias, running_mean, running_var)
         xl = _as_layout(x, _lib.MS_NHWC)
-        n, c, h, w_ = x.shape
-        pdt_t = running_var.dtype
-        params = [t if (t is None or t.dtype == pdt_t) else t.to(pdt_t)
-                  for t in (running_mean, running_var, weight, bias)]
-        params = [None if t is None else t.contiguous() for t in params]
-        y = torch.empty_like(xl)
-        mask = torch.empty((n_el + 7) // 8, dtype=torch.uint8, device=x.device) if out_rg \
-            else None
-        L = _lib.lib()
-        if residual is None:
-            _lib.check(L.ms_bn_eval_relu_fwd(n, c, h * w_, _dtype_code(x),
-                                             _dtype_code(running_var), _ptr(xl),
-                                             _ptr(params[0]), _ptr(params[1]), _ptr(params[2]),
-                                             _ptr(params[3]), ctx.eps, _ptr(y), _ptr(mask),
-                                             _stream(x.device)), "ms_bn_eval_relu_fwd")
-        else:
+        rl = None
+        if residual is not None:
             _require_cuda("batch_norm_add_relu", residual)
             if residual.shape != x.shape or residual.dtype != x.dtype:
                 raise RuntimeError("bn+add+relu: residual must match the BN input's shape "
                                    "and dtype")
             rl = _as_layout(residual, _lib.MS_NHWC)
-            _lib.check(L.ms_bn_eval_add_relu_fwd(n, c, h * w_, _dtype_code(x),
-                                                 _dtype_code(running_var), _ptr(xl), _ptr(rl),
-                                                 _ptr(params[0]), _ptr(params[1]),
-                                                 _ptr(params[2]), _ptr(params[3]), ctx.eps,
-                                                 _ptr(y), _ptr(mask), _stream(x.device)),
-                       "ms_bn_eval_add_relu_fwd")
+        y, mask = _ops().bn_relu_fwd(xl, rl, running_mean, running_var, weight, bias, ctx.eps,
+                                     bool(out_rg))
+        mask = _opt(mask, out_rg)
         ctx.save_for_backward(xl if "x" in roles else None, weight if "w" in roles else None,
                               mask)
         return y
@@ -476,32 +359,14 @@ class _BatchNorm2dEvalReLUFn(torch.autograd.Function):
         if need_w:
             x = _need(x, "x", "batchnorm2d dW")
         g = _as_layout(gy, _lib.MS_NHWC)
-        n, _, h, w_ = ctx.x_shape
-        pdt_t = running_var.dtype
-        rm = running_mean.to(pdt_t).contiguous()
-        rv = running_var.contiguous()
-        wt = None if weight is None else weight.to(pdt_t).contiguous()
-        if need_x:
-            dx = torch.empty_like(g)
-        if need_r:
-            dr = torch.empty_like(g)
-        if need_w and need_b:  # adjacent: the library converts both in one launch
-            dw_t, db_t = torch.empty((2, c), dtype=pdt_t, device=g.device).unbind(0)
-        else:
-            dw_t = torch.empty((c,), dtype=pdt_t, device=g.device) if need_w else None
-            db_t = torch.empty((c,), dtype=pdt_t, device=g.device) if need_b else None
-        L = _lib.lib()
-        ws, nb = _workspace(L.ms_bn_eval_workspace(n, c, h * w_, _lib.MS_NHWC)
-                            if (need_w or need_b) else 0, g.device)
-        _lib.check(L.ms_bn_eval_add_relu_bwd(n, c, h * w_, _dtype_code(g), _dtype_code(rv),
-                                             _ptr(g), _ptr(mask), _ptr(x if need_w else None),
-                                             _ptr(rm), _ptr(rv), _ptr(wt), ctx.eps, _ptr(dx),
-                                             _ptr(dr), _ptr(dw_t), _ptr(db_t), _ptr(ws), nb,
-                                             _stream(g.device)), "ms_bn_eval_add_relu_bwd")
+        dx_t, dr_t, dwdb = _ops().bn_add_relu_bwd(g, mask, x if need_w else None, running_mean,
+                                                  running_var, weight, ctx.eps, bool(need_x),
+                                                  bool(need_r), bool(need_w), bool(need_b))
+        dx, dr = _opt(dx_t, need_x), _opt(dr_t, need_r)
         if need_w:
-            dw = dw_t.to(ctx.p_dtypes[0])
+            dw = dwdb[0].to(ctx.p_dtypes[0])
         if need_b:
-            db = db_t.to(ctx.p_dtypes[1])
+            db = dwdb[1].to(ctx.p_dtypes[1])
         return dx, dw, db, None, None, None, dr
 
 
@@ -557,15 +422,14 @@ class _ReLUFn(torch.autograd.Function):
             fmt = torch.contiguous_format
             inplace = False
         ctx.fmt = fmt
-        n = x.numel()
-        mask = torch.empty((n + 7) // 8, dtype=torch.uint8, device=x.device) if x_rg else None
-        y = x if inplace else torch.empty_like(x, memory_format=fmt)
-        L = _lib.lib()
-        _lib.check(L.ms_relu_fwd(n, _dtype_code(x), _ptr(x), _ptr(y), _ptr(mask),
-                                 _stream(x.device)), "ms_relu_fwd")
+        _dtype_code(x)
         if inplace:
+            mask = _ops().relu_fwd_(x, bool(x_rg))
+            y = x
             ctx.mark_dirty(x)
-        ctx.save_for_backward(mask)
+        else:
+            y, mask = _ops().relu_fwd(x, bool(x_rg))
+        ctx.save_for_backward(_opt(mask, x_rg))
         return y
 
     @staticmethod
@@ -578,11 +442,7 @@ class _ReLUFn(torch.autograd.Function):
             gy = gy.contiguous(memory_format=ctx.fmt)  # mirrors the CUDA path's allocation
             return gy.new_empty(gy.shape), None
         g = gy.contiguous(memory_format=ctx.fmt)
-        dx = torch.empty_like(g, memory_format=ctx.fmt)
-        L = _lib.lib()
-        _lib.check(L.ms_relu_bwd(g.numel(), _dtype_code(g), _ptr(g), _ptr(mask), _ptr(dx),
-                                 _stream(g.device)), "ms_relu_bwd")
-        return dx, None
+        return _ops().relu_bwd(g, mask), None
 
 
 def relu(x: torch.Tensor, inplace: bool = False) -> torch.Tensor:
@@ -623,17 +483,9 @@ class _MaxPool2dFn(torch.autograd.Function):
         layout = _lib.MS_NHWC if (_is_channels_last(x) and not x.is_contiguous()) else _lib.MS_NCHW
         xl = _as_layout(x, layout)
         ctx.layout = layout
-        d = _lib.PoolDesc(n, c, h, w, kh, kw, sh, sw, ph, pw, layout, _dtype_code(x))
-        y = _empty4((n, c, oh, ow), x, layout)
-        idx = None
-        if x_rg:
-            mf = torch.channels_last if layout == _lib.MS_NHWC else torch.contiguous_format
-            idx = torch.empty((n, c, oh, ow), dtype=torch.uint8, device=x.device,
-                              memory_format=mf)
-        L = _lib.lib()
-        _lib.check(L.ms_maxpool2d_fwd(ctypes.byref(d), _ptr(xl), _ptr(y), _ptr(idx),
-                                      _stream(x.device)), "ms_maxpool2d_fwd")
-        ctx.save_for_backward(idx, keep)
+        _dtype_code(x)
+        y, idx = _ops().maxpool2d_fwd(xl, [kh, kw], [sh, sw], [ph, pw], layout, bool(x_rg))
+        ctx.save_for_backward(_opt(idx, x_rg), keep)
         return y
 
     @staticmethod
@@ -648,25 +500,13 @@ class _MaxPool2dFn(torch.autograd.Function):
             return (gy.new_empty(x_shape),) + nones
         layout = ctx.layout
         g = _as_layout(gy, layout)
-        n, c, h, w = x_shape
-        d = _lib.PoolDesc(n, c, h, w, kh, kw, sh, sw, ph, pw, layout, _dtype_code(g))
-        dx = _empty4(x_shape, g, layout)
-        L = _lib.lib()
+        geo = (list(x_shape), [kh, kw], [sh, sw], [ph, pw], layout)
         if keep is not None:
-            ib = ctx.in_bn
-            st_ = L.ms_maxpool2d_relu_bwd(ctypes.byref(d), _ptr(g), _ptr(idx), _ptr(keep),
-                                          _ptr(ib[1]) if ib else None, _ptr(ib[2]) if ib else None,
-                                          _dtype_code(ib[1]) if ib else 0, ib[3] if ib else 0.0,
-                                          _ptr(dx), _stream(g.device))
-            if st_ == 0:
-                return (dx,) + nones
-            if st_ != 4:  # 4 = MS_ERR_UNSUPPORTED: the unfused pair of passes
-                _lib.check(st_, "ms_maxpool2d_relu_bwd")
-        _lib.check(L.ms_maxpool2d_bwd(ctypes.byref(d), _ptr(g), _ptr(idx), _ptr(dx),
-                                      _stream(g.device)), "ms_maxpool2d_bwd")
-        if keep is not None:
-            dx = _mask_scale(dx, keep, ctx.in_bn)
-        return (dx,) + nones
+            # the producer ReLU [+ eval-BN]'s backward applied at the pool's store
+            ib = ctx.in_bn or (None, None, None, 0.0)
+            return (_ops().maxpool2d_relu_bwd(g, idx, keep, ib[0], ib[1], ib[2], ib[3], *geo),) \
+                + nones
+        return (_ops().maxpool2d_bwd(g, idx, *geo),) + nones
 
 
 def max_pool2d(x, kernel_size, stride=None, padding=0, in_mask=None, in_bn=None):
@@ -707,12 +547,13 @@ class _DropoutFn(torch.autograd.Function):
             fmt = torch.contiguous_format
             inplace = False
         ctx.fmt = fmt
-        y = x if inplace else torch.empty_like(x, memory_format=fmt)
-        L = _lib.lib()
-        _lib.check(L.ms_dropout_fwd(x.numel(), _dtype_code(x), _ptr(x), _ptr(y), seed, stream, p,
-                                    gen, None, _stream(x.device)), "ms_dropout_fwd")
+        _dtype_code(x)
         if inplace:
+            _ops().dropout_fwd_(x, p, seed, stream, gen)
+            y = x
             ctx.mark_dirty(x)
+        else:
+            y = _ops().dropout_fwd(x, p, seed, stream, gen)
         ctx.save_for_backward(key)
         return y
 
@@ -727,11 +568,7 @@ class _DropoutFn(torch.autograd.Function):
             gy = gy.contiguous()  # mirrors the CUDA path's allocation
             return gy.new_empty(gy.shape), None, None, None, None, None
         g = gy.contiguous(memory_format=ctx.fmt)
-        dx = torch.empty_like(g, memory_format=ctx.fmt)
-        L = _lib.lib()
-        _lib.check(L.ms_dropout_bwd(g.numel(), _dtype_code(g), _ptr(g), _ptr(dx), seed, stream, p,
-                                    gen, _stream(g.device)), "ms_dropout_bwd")
-        return dx, None, None, None, None, None
+        return _ops().dropout_bwd(g, p, seed, stream, gen), None, None, None, None, None
 
 
 def draw_seed() -> int:
@@ -783,17 +620,12 @@ class _LayerNormFn(torch.autograd.Function):
             ctx.save_for_backward(x if keep_x else None, mean, rstd, weight if x_rg else None)
             return x.new_empty(x.shape)
         _require_cuda("layer_norm", x, weight, bias)
+        _dtype_code(x)
         xc = x.contiguous()
         w = None if weight is None else weight.to(x.dtype).contiguous()
-        b = None if bias is None else bias.to(x.dtype).contiguous()
-        y = torch.empty_like(xc)
-        mean = torch.empty(rows, dtype=torch.float32, device=x.device) if keep_x else None
-        rstd = torch.empty(rows, dtype=torch.float32, device=x.device) if keep_x else None
-        L = _lib.lib()
-        _lib.check(L.ms_layernorm_fwd(rows, dim, _dtype_code(x), _ptr(xc), _ptr(w), _ptr(b),
-                                      float(eps), _ptr(y), _ptr(mean), _ptr(rstd),
-                                      _stream(x.device)), "ms_layernorm_fwd")
-        ctx.save_for_backward(xc if keep_x else None, mean, rstd, w if x_rg else None)
+        y, mean, rstd = _ops().layernorm_fwd(xc, w, bias, float(eps), dim, bool(keep_x))
+        ctx.save_for_backward(xc if keep_x else None, _opt(mean, keep_x), _opt(rstd, keep_x),
+                              w if x_rg else None)
         return y
 
     @staticmethod
@@ -815,28 +647,16 @@ class _LayerNormFn(torch.autograd.Function):
                 db = torch.empty(ctx.nshape, dtype=b_dt, device="meta")
             return dx, None, dw, db, None
         g = gy.contiguous()
-        dt = _dtype_code(g)
-        L = _lib.lib()
-        st = _stream(g.device)
         if need_x or need_w:
             x = _need(x, "x", "layer_norm dX/dW")
             _need(mean, "stats", "layer_norm dX/dW")
             if need_x and ctx.p_dtypes[0] is not None:
                 _need(w, "w", "layer_norm dX")
-            dx = torch.empty_like(g) if need_x else None
-            dwt = torch.empty(dim, dtype=g.dtype, device=g.device) if need_w else None
-            dbt = torch.empty(dim, dtype=g.dtype, device=g.device) if need_b else None
-            ws, nb = _workspace(L.ms_layernorm_workspace(rows, dim, dt) if (need_w or need_b)
-                                else 0, g.device)
-            _lib.check(L.ms_layernorm_bwd(rows, dim, dt, _ptr(g), _ptr(x), _ptr(mean), _ptr(rstd),
-                                          _ptr(w), _ptr(dx), _ptr(dwt), _ptr(dbt), _ptr(ws), nb,
-                                          st), "ms_layernorm_bwd")
-            dw, db = dwt, dbt
+            dxt, dwt, dbt = _ops().layernorm_bwd(g, x, mean, rstd, w, dim, bool(need_x),
+                                                 bool(need_w), bool(need_b))
+            dx, dw, db = _opt(dxt, need_x), _opt(dwt, need_w), _opt(dbt, need_b)
         elif need_b:  # db = sum_rows g: nothing saved is read
-            db = torch.empty(dim, dtype=g.dtype, device=g.device)
-            ws, nb = _workspace(L.ms_bias_grad_workspace(rows, dim, dt), g.device)
-            _lib.check(L.ms_bias_grad(rows, dim, dt, _ptr(g), _ptr(db), _ptr(ws), nb, st),
-                       "ms_bias_grad")
+            db = _ops().bias_grad(g, dim)
         if dw is not None:
             dw = dw.view(ctx.nshape).to(w_dt)
         if db is not None:
@@ -894,16 +714,9 @@ class _ConvTranspose2dFn(torch.autograd.Function):
         wl = _as_layout(weight, wlayout)
         ctx.layouts = (layout, wlayout)
         ctx.save_for_backward(xl if "x" in roles else None, wl if "w" in roles else None)
-        dt = _dtype_code(x)
-        d = _conv_desc(conv_x, (cin, cout, kh, kw), stride, padding, layout, wlayout, dt)
-        y = _empty4(conv_x, x, layout)
-        L = _lib.lib()
-        st = _stream(x.device)
-        b = None if bias is None else bias.to(x.dtype).contiguous()
-        ws, nb = _workspace(L.ms_conv2d_workspace(ctypes.byref(d), _lib.MS_CONV_DX), x.device)
-        _lib.check(L.ms_conv_transpose2d_fwd(ctypes.byref(d), _ptr(xl), _ptr(wl), _ptr(b), _ptr(y),
-                                             _ptr(ws), nb, st), "ms_conv_transpose2d_fwd")
-        return y
+        _dtype_code(x)
+        return _ops().conv_transpose2d_fwd(xl, wl, bias, list(conv_x), list(stride),
+                                           list(padding), layout, wlayout)
 
     @staticmethod
     def backward(ctx, gy):
@@ -923,32 +736,17 @@ class _ConvTranspose2dFn(torch.autograd.Function):
             return dx, dw, db, None, None, None
         layout, wlayout = ctx.layouts
         g = _as_layout(gy, layout)
-        dt = _dtype_code(g)
-        cin, cout, kh, kw = w_shape
-        d = _conv_desc(conv_x, (cin, cout, kh, kw), stride, padding, layout, wlayout, dt)
-        L = _lib.lib()
-        st = _stream(g.device)
+        O = _ops()
+        geo = (list(stride), list(padding), layout, wlayout)
         if need_x:  # dX = conv2d(g, W)
             w = _need(w, "w", "conv_transpose2d dX")
-            dx = _empty4(x_shape, g, layout)
-            ws, nb = _workspace(L.ms_conv2d_workspace(ctypes.byref(d), _lib.MS_CONV_FWD), g.device)
-            _lib.check(L.ms_conv2d_fwd(ctypes.byref(d), _ptr(g), _ptr(w), None, _ptr(dx),
-                                       _ptr(ws), nb, st), "ms_conv2d_fwd (conv_transpose2d dX)")
+            dx = O.conv2d_fwd(g, w, None, *geo)
         if need_w:  # dW = conv2d weight-VJP with the conv input g and conv output-grad x
             x = _need(x, "x", "conv_transpose2d dW")
-            dw = torch.empty(w_shape, dtype=ctx.w_meta, device=g.device,
-                             memory_format=torch.channels_last if wlayout == _lib.MS_NHWC
-                             else torch.contiguous_format)
-            ws, nb = _workspace(L.ms_conv2d_workspace(ctypes.byref(d), _lib.MS_CONV_DW), g.device)
-            _lib.check(L.ms_conv2d_dw(ctypes.byref(d), _ptr(g), _ptr(x), _ptr(dw), _ptr(ws), nb,
-                                      st), "ms_conv2d_dw (conv_transpose2d dW)")
+            dw = O.conv2d_dw(g, x, list(w_shape), *geo)
         if need_b:  # sum of g over (n, h, w) per output channel
-            n, c, h, w_ = conv_x
-            dd = _lib.ConvDesc(n, c, h, w_, c, 1, 1, 1, 1, 0, 0, layout, wlayout, dt)
-            db = torch.empty((cout,), dtype=g.dtype, device=g.device)
-            ws, nb = _workspace(4 * cout, g.device)
-            _lib.check(L.ms_conv2d_db(ctypes.byref(dd), _ptr(g), _ptr(db), _ptr(ws), nb, st),
-                       "ms_conv2d_db (conv_transpose2d db)")
+            c = conv_x[1]
+            db = O.conv2d_db(g, list(conv_x), [c, c, 1, 1], [1, 1], [0, 0], layout, wlayout)
         return dx, dw, db, None, None, None
 
 
@@ -1017,22 +815,14 @@ class _ConvBNFn(torch.autograd.Function):
         xl = _as_layout(x, layout)
         wl = _as_layout(weight, wlayout)
         ctx.layouts = (layout, wlayout)
-        dt = _dtype_code(x)
-        d = _conv_desc(x.shape, weight.shape, stride, padding, layout, wlayout, dt)
-        y = _empty4(out_shape, x, layout)
-        mask = torch.empty((n_el + 7) // 8, dtype=torch.uint8, device=x.device) \
-            if relu and out_rg else None
-        b = None if bias is None else bias.to(x.dtype).contiguous()
+        _dtype_code(x)
+        _check_conv_channels(x.shape, weight.shape)
         res = None if residual is None else _as_layout(residual, layout)
         mean, var, bw, eps = ctx.bn if bn is not None else (None, None, None, 0.0)
         bb = None if bn is None else bn.bias
-        L = _lib.lib()
-        ws, nb = _workspace(L.ms_conv2d_bn_workspace(ctypes.byref(d)), x.device)
-        _lib.check(L.ms_conv2d_bn_fwd(ctypes.byref(d), _ptr(xl), _ptr(wl), _ptr(b), _ptr(mean),
-                                      _ptr(var), _ptr(bw), _ptr(bb),
-                                      _dtype_code(mean) if mean is not None else dt, eps,
-                                      _ptr(res), int(relu), _ptr(y), _ptr(mask), _ptr(ws), nb,
-                                      _stream(x.device)), "ms_conv2d_bn_fwd")
+        y, mask = _ops().conv2d_bn_fwd(xl, wl, bias, mean, var, bw, bb, eps, res, bool(relu),
+                                       bool(out_rg), list(stride), list(padding), layout, wlayout)
+        mask = _opt(mask, relu and out_rg)
         ctx.save_for_backward(xl if "x" in roles else None, wl if "w" in roles else None, keep)
         if mask is not None:
             ctx.mark_non_differentiable(mask)
@@ -1081,63 +871,27 @@ class _ConvBNFn(torch.autograd.Function):
             if need_b:
                 db = gc.new_empty((w_shape[0],))
             return (dx, dw, db, d_res) + (None,) * 7
-        L = _lib.lib()
-        st = _stream(g.device)
-        dt = _dtype_code(g)
-        d = _conv_desc(x_shape, w_shape, stride, padding, layout, wlayout, dt)
+        O = _ops()
+        geo = (list(stride), list(padding), layout, wlayout)
         if need_x:
             w = _need(w, "w", "conv_bn dX")
-            dx = _empty4(x_shape, g, layout)
-            wsp, nb = _workspace(L.ms_conv2d_workspace(ctypes.byref(d), _lib.MS_CONV_DX), g.device)
-            folded = False
-            ib = ctx.in_bn
+            ib = ctx.in_bn or (None, None, None, 0.0)
             if sc_w or addend is not None or keep is not None:
                 # BN scale folded into the repacked dgrad weight (no pass over g), the
                 # tee'd consumer's gradient and the producer ReLU [+BN]'s backward in
-                # the epilogue
-                st_ = L.ms_conv2d_bn_dx(ctypes.byref(d), _ptr(g), _ptr(w),
-                                        _ptr(var) if sc_w else None, _ptr(bw) if sc_w else None,
-                                        _dtype_code(var) if sc_w else dt, eps, _ptr(addend),
-                                        _ptr(keep), _ptr(ib[1]) if ib else None,
-                                        _ptr(ib[2]) if ib else None,
-                                        _dtype_code(ib[1]) if ib else dt, ib[3] if ib else 0.0,
-                                        _ptr(dx), _ptr(wsp), nb, st)
-                folded = st_ == 0
-                if st_ not in (0, 4):  # 4 = MS_ERR_UNSUPPORTED: scale the weight here
-                    _lib.check(st_, "ms_conv2d_bn_dx")
-                if not folded and sc_w:
-                    sc = (bw.float() if bw is not None else 1.0) * torch.rsqrt(var.float() + eps)
-                    w = _as_layout((w.float() * sc.view(-1, 1, 1, 1)).to(w.dtype), wlayout)
-            if not folded:
-                _lib.check(L.ms_conv2d_dx(ctypes.byref(d), _ptr(g), _ptr(w), _ptr(dx), _ptr(wsp),
-                                          nb, st), "ms_conv2d_dx")
-                if addend is not None:
-                    dx.add_(addend)
-                if keep is not None:
-                    dx = _mask_scale(dx, keep, ib)
+                # the epilogue (the op runs the separate passes where it cannot)
+                dx = O.conv2d_bn_dx(g, w, var if sc_w else None, bw if sc_w else None, eps,
+                                    addend, keep, ib[0], ib[1], ib[2], ib[3], list(x_shape), *geo)
+            else:
+                dx = O.conv2d_dx(g, w, list(x_shape), *geo)
             del addend
         if need_w or need_b:
-            gc = g
-            if need_scaled_g:
-                gc = torch.empty_like(g, memory_format=torch.channels_last
-                                      if layout == _lib.MS_NHWC else torch.contiguous_format)
-                _lib.check(L.ms_bn_relu_bwd(g.numel(), w_shape[0], dt, _dtype_code(mean), _ptr(g),
-                                            None, _ptr(mean), _ptr(var), _ptr(bw), eps, _ptr(gc),
-                                            st), "ms_bn_relu_bwd")
+            gc = O.bn_relu_bwd(g, None, mean, var, bw, eps) if need_scaled_g else g
             if need_w:
                 x = _need(x, "x", "conv_bn dW")
-                dw = torch.empty(w_shape, dtype=ctx.w_meta[0], device=gc.device,
-                                 memory_format=torch.channels_last if wlayout == _lib.MS_NHWC
-                                 else torch.contiguous_format)
-                wsp, nb = _workspace(L.ms_conv2d_workspace(ctypes.byref(d), _lib.MS_CONV_DW),
-                                     gc.device)
-                _lib.check(L.ms_conv2d_dw(ctypes.byref(d), _ptr(x), _ptr(gc), _ptr(dw), _ptr(wsp),
-                                          nb, st), "ms_conv2d_dw")
+                dw = O.conv2d_dw(x, gc, list(w_shape), *geo)
             if need_b:
-                db = torch.empty((w_shape[0],), dtype=gc.dtype, device=gc.device)
-                wsp, nb = _workspace(4 * w_shape[0], gc.device)
-                _lib.check(L.ms_conv2d_db(ctypes.byref(d), _ptr(gc), _ptr(db), _ptr(wsp), nb, st),
-                           "ms_conv2d_db")
+                db = O.conv2d_db(gc, list(x_shape), list(w_shape), *geo)
         return (dx, dw, db, d_res) + (None,) * 7
 
 
@@ -1148,19 +902,12 @@ def _mask_scale(g: torch.Tensor, keep: torch.Tensor, bnp) -> torch.Tensor:
     fmt = torch.channels_last if _is_channels_last(g) and not g.is_contiguous() \
         else torch.contiguous_format
     g = g.contiguous(memory_format=fmt)
-    out = torch.empty_like(g, memory_format=fmt)
     if _is_meta(g):
-        return out
-    L = _lib.lib()
+        return torch.empty_like(g, memory_format=fmt)
     if bnp is None:
-        _lib.check(L.ms_relu_bwd(g.numel(), _dtype_code(g), _ptr(g), _ptr(keep), _ptr(out),
-                                 _stream(g.device)), "ms_relu_bwd")
-    else:
-        mean, var, bw, eps = bnp
-        _lib.check(L.ms_bn_relu_bwd(g.numel(), g.shape[1], _dtype_code(g), _dtype_code(mean),
-                                    _ptr(g), _ptr(keep), _ptr(mean), _ptr(var), _ptr(bw), eps,
-                                    _ptr(out), _stream(g.device)), "ms_bn_relu_bwd")
-    return out
+        return _ops().relu_bwd(g, keep)
+    mean, var, bw, eps = bnp
+    return _ops().bn_relu_bwd(g, keep, mean, var, bw, eps)
 
 
 class _MaskScaleFn(torch.autograd.Function):
@@ -1188,19 +935,12 @@ class _MaskScaleFn(torch.autograd.Function):
         (mask,) = ctx.saved_tensors
         mask = _need(mask, "mask", "conv_bn_relu dX")
         g = gy.contiguous(memory_format=ctx.fmt)
-        gc = torch.empty_like(g, memory_format=ctx.fmt)
         if _is_meta(g):
-            return gc, None, None
-        L = _lib.lib()
+            return torch.empty_like(g, memory_format=ctx.fmt), None, None
         if ctx.bn is None:
-            _lib.check(L.ms_relu_bwd(g.numel(), _dtype_code(g), _ptr(g), _ptr(mask), _ptr(gc),
-                                     _stream(g.device)), "ms_relu_bwd")
-            return gc, None, None
+            return _ops().relu_bwd(g, mask), None, None
         mean, var, bw, eps = ctx.bn
-        _lib.check(L.ms_bn_relu_bwd(g.numel(), g.shape[1], _dtype_code(g), _dtype_code(mean),
-                                    _ptr(g), _ptr(mask), _ptr(mean), _ptr(var), _ptr(bw), eps,
-                                    _ptr(gc), _stream(g.device)), "ms_bn_relu_bwd")
-        return gc, None, None
+        return _ops().bn_relu_bwd(g, mask, mean, var, bw, eps), None, None
 
 
 def conv_bn_fusable(x: torch.Tensor, conv, bn) -> bool:
@@ -1351,12 +1091,9 @@ class _AddReLUFn(torch.autograd.Function):
         if fmt is None or _dense_format(b) != fmt or a.dtype != b.dtype or a.shape != b.shape:
             raise RuntimeError("add_relu: operands must share shape, dtype and a dense layout")
         ctx.fmt = fmt
-        y = torch.empty_like(a, memory_format=fmt)
-        mask = torch.empty((n + 7) // 8, dtype=torch.uint8, device=a.device) if out_rg else None
-        L = _lib.lib()
-        _lib.check(L.ms_add_relu_fwd(n, _dtype_code(a), _ptr(a), _ptr(b), _ptr(y), _ptr(mask),
-                                     _stream(a.device)), "ms_add_relu_fwd")
-        ctx.save_for_backward(mask)
+        _dtype_code(a)
+        y, mask = _ops().add_relu_fwd(a, b, bool(out_rg))
+        ctx.save_for_backward(_opt(mask, out_rg))
         return y
 
     @staticmethod
@@ -1368,10 +1105,7 @@ class _AddReLUFn(torch.autograd.Function):
             dx = g.new_empty(g.shape)
             return (dx if ctx.needs_input_grad[0] else None,
                     dx if ctx.needs_input_grad[1] else None)
-        dx = torch.empty_like(g, memory_format=ctx.fmt)
-        L = _lib.lib()
-        _lib.check(L.ms_relu_bwd(g.numel(), _dtype_code(g), _ptr(g), _ptr(mask), _ptr(dx),
-                                 _stream(g.device)), "ms_relu_bwd")
+        dx = _ops().relu_bwd(g, mask)
         return (dx if ctx.needs_input_grad[0] else None,
                 dx if ctx.needs_input_grad[1] else None)
 

@@ -50,3 +50,59 @@ def test_invalid_descriptor_rejected_without_gpu():
     st = L.ms_conv2d_fwd(ctypes.byref(d), None, None, None, None, None, 0, None)
     assert st == 1  # MS_ERR_SHAPE
     assert b"non-positive" in L.ms_last_error()
+
+
+# ------------------------------------------------------------------ torch.ops.memsave
+OPS = ["linear_fwd", "linear_dx", "linear_dw", "bias_grad", "conv2d_fwd", "conv2d_dx",
+       "conv2d_dw", "conv2d_db", "conv_transpose2d_fwd", "bn_eval_fwd", "bn_eval_bwd",
+       "bn_relu_fwd", "bn_add_relu_bwd", "bn_relu_bwd", "relu_fwd", "relu_fwd_", "relu_bwd",
+       "add_relu_fwd", "maxpool2d_fwd", "maxpool2d_bwd", "maxpool2d_relu_bwd", "dropout_fwd",
+       "dropout_fwd_", "dropout_bwd", "layernorm_fwd", "layernorm_bwd", "conv2d_bn_fwd",
+       "conv2d_bn_dx"]
+
+
+def test_torch_op_library_registers_every_op():
+    import torch
+
+    from paper_2404_12406_b200._ops import ops
+    O = ops()
+    for name in OPS:
+        op = getattr(O, name)
+        # a CUDA kernel and a Meta kernel, no CPU kernel (no CPU path)
+        assert torch._C._dispatch_has_kernel_for_dispatch_key(op._qualified_op_name, "CUDA")
+        assert torch._C._dispatch_has_kernel_for_dispatch_key(op._qualified_op_name, "Meta")
+        assert not torch._C._dispatch_has_kernel_for_dispatch_key(op._qualified_op_name, "CPU")
+
+
+def test_torch_ops_meta_shapes_and_fake_tensors():
+    import torch
+    from torch._subclasses.fake_tensor import FakeTensorMode
+
+    from paper_2404_12406_b200._ops import ops
+    O = ops()
+    cl = torch.channels_last
+    x = torch.empty(4, 64, 9, 9, device="meta", dtype=torch.bfloat16).contiguous(memory_format=cl)
+    w = torch.empty(32, 64, 3, 3, device="meta", dtype=torch.bfloat16).contiguous(memory_format=cl)
+    y = O.conv2d_fwd(x, w, None, [2, 2], [1, 1], 1, 1)
+    assert y.shape == (4, 32, 5, 5) and y.is_contiguous(memory_format=cl)
+    dx = O.conv2d_dx(y, w, [4, 64, 9, 9], [2, 2], [1, 1], 1, 1)
+    assert dx.shape == x.shape and dx.is_contiguous(memory_format=cl)
+    y2, mask = O.conv2d_bn_fwd(x, w, None, None, None, None, None, 0.0, None, True, True,
+                               [1, 1], [1, 1], 1, 1)
+    assert mask.numel() == (4 * 32 * 9 * 9 + 7) // 8 and mask.dtype == torch.uint8
+    with FakeTensorMode():
+        xf = torch.empty(8, 512, 768, device="cuda", dtype=torch.bfloat16)
+        wf = torch.empty(3072, 768, device="cuda", dtype=torch.bfloat16)
+        yf = O.linear_fwd(xf, wf, None)
+        assert yf.shape == (8, 512, 3072) and yf.device.type == "cuda"
+        ln = O.layernorm_fwd(yf, None, None, 1e-5, 3072, True)
+        assert ln[1].shape == (8 * 512,) and ln[1].dtype == torch.float32
+
+
+def test_cpu_tensors_have_no_kernel():
+    import pytest
+    import torch
+
+    from paper_2404_12406_b200._ops import ops
+    with pytest.raises(NotImplementedError):
+        ops().relu_fwd(torch.randn(8), True)
