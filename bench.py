@@ -2,15 +2,24 @@
 """Benchmark: fwd+bwd throughput and peak memory of the selective-save layers
 on B200 vs stock PyTorch (BASELINE.json metric), one JSON line on rank 0.
 
-    python bench.py [--gpus N --steps K --warmup W --config resnet18|fig1]
+    python bench.py [--config bert|resnet18|resnet101|vgg16|fig1|llama]
+                    [--gpus N --steps K --warmup W]
     python bench.py --impl reference ...   # the reference's CPU algorithm, host cores
 
-Default workload = BASELINE.json configs[1]: ResNet-18, frozen weights,
-input-only gradient, batch 256x3x224x224 bf16, channels_last, eval-mode BN.
-A "step" = forward + cross-entropy + backward to the input (x.grad).  With N
-GPUs (torchrun) every rank runs the full per-GPU batch (weak scaling); the
-input-only workload has no trainable parameter, so the ranks are replicas and
-no collective runs in the data path.
+Default workload: the largest single-GPU configuration of BASELINE.json,
+configs[3] BERT-base (random init, attention Linear biases + classifier
+trainable, train mode with dropout 0.1), batch 64 x seq 512, bf16.  A "step" =
+forward + cross-entropy + backward (+ the data-parallel gradient exchange when
+N > 1).  Scaling follows SURVEY.md §8(d): the CNN and BERT configs split the
+global batch over the N ranks (strong scaling); Llama keeps 2 sequences per GPU
+(weak scaling).  With N > 1 (torchrun, or self-spawned by --gpus N) the
+trainable-subset gradients are all-reduced over NCCL (TrainableGradAllReduce);
+the stock arm uses DistributedDataParallel on the same requires_grad set.
+
+CNN configs run the step as a CUDA graph (paper_2404_12406_b200.graphs): every
+memsave op is a graph-capturable custom op, so the launch-bound steps (ResNet-101:
+~650 launches) replay without host work.  The stock arm is timed eager, with
+cudnn.benchmark, and graphed; speedup_vs_stock is against the best of them.
 """
 
 from __future__ import annotations
@@ -29,6 +38,18 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 METRIC = "peak fwd+bwd memory (MiB) and fwd+bwd samples/sec vs PyTorch, at 1/2/4/8 B200"
+DEFAULT_CONFIG = "bert"
+# scaling per SURVEY.md §8(d); graph: the step is CUDA-graph-safe (no host RNG per step)
+CONFIGS = {
+    "bert": dict(scaling="strong", graph=False,
+                 why_eager="dropout seeds are drawn on the host per call"),
+    "resnet18": dict(scaling="strong", graph=True),
+    "resnet101": dict(scaling="strong", graph=True),
+    "vgg16": dict(scaling="strong", graph=True),
+    "fig1": dict(scaling="strong", graph=True),
+    "llama": dict(scaling="weak", graph=False,
+                  why_eager="HF generation-time host logic in the model forward"),
+}
 
 
 def _peaks():
@@ -105,54 +126,17 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-# ------------------------------------------------------------------ ncu traffic
-# dram__bytes_read.sum + dram__bytes_write.sum per launch of the step's top conv
-# kernels, from one `ncu --set full` capture each (tools/ncu_summary.py output,
-# committed under profiles/); keyed by (pass, C, R, stride) of the ResNet-18 shapes
-_NCU_CSV = os.path.join(ROOT, "profiles", "r1_ncu_r18_kernels.csv")
-_NCU_NAME = {("conv_fwd", 3, 7, 2): "stem_fwd", ("conv_dx", 3, 7, 2): "stem_dx",
-             ("conv_fwd", 64, 3, 1): "layer1_fwd", ("conv_dx", 64, 3, 1): "layer1_dgrad"}
-_KERNEL_OF = {("conv_fwd", 3, 7, 2): "stem_fprop_kernel",
-              ("conv_dx", 3, 7, 2): "stem_dgrad_kernel",
-              ("conv_fwd", 64, 3, 1): "conv3x3_halo_kernel",
-              ("conv_dx", 64, 3, 1): "conv3x3_halo_kernel (transposed)"}
-
-
-def _kernel_key(e):
-    g = e["geom"]
-    return (e["kind"], g["c"], g["r"], g["stride"])
-
-
-def _ncu_traffic(e):
-    name = _NCU_NAME.get(_kernel_key(e))
-    if name is None or not os.path.exists(_NCU_CSV):
-        return None, None
-    import csv
-    vals = {}
-    with open(_NCU_CSV) as f:
-        for row in csv.DictReader(f):
-            if row["kernel"] == name and row["metric"] in ("dram__bytes_read.sum",
-                                                           "dram__bytes_write.sum"):
-                scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(row["unit"], 1)
-                vals[row["metric"]] = float(row["value"]) * scale
-    if len(vals) != 2:
-        return None, None
-    return int(sum(vals.values())), f"{os.path.relpath(_NCU_CSV, ROOT)}:{name}"
-
-
-# ------------------------------------------------------------------ GPU arm
-def _dist_setup(args):
+# ------------------------------------------------------------------ distributed
+def _dist_setup():
     import torch
     import torch.distributed as dist
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
     if world > 1 and not dist.is_initialized():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    elif world == 1:
-        torch.cuda.set_device(local)
     return world, rank, local
 
 
@@ -172,75 +156,110 @@ def _max_over_ranks(v: float, world: int) -> float:
     return float(t.item())
 
 
-def prime(wl, model, dev, sync=None):
-    """Setup, not a step: one fwd+bwd at batch 2 so every kernel image is loaded
-    (lazy module loading) and one-time host state exists before warm-up."""
+def _timed(fn, steps, warmup, world, dev):
+    """W untimed calls, then K timed calls bracketed by barrier + synchronize;
+    device ms over the K calls (CUDA events), max over ranks."""
     import torch
-    ins = list(wl.make_batch(min(2, wl.batch), dev))
-    if wl.input_requires_grad:
-        ins[0].requires_grad_(True)
-    wl.loss_fn(model, *ins).backward()
-    if sync is not None:  # the gradient hooks fired: complete their collectives
-        sync.finish()
-    for p in model.parameters():
-        p.grad = None
+    for _ in range(warmup):
+        fn()
     torch.cuda.synchronize(dev)
+    _barrier(world)
+    torch.cuda.synchronize(dev)
+    s = torch.cuda.Event(enable_timing=True)
+    e = torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(steps):
+        fn()
+    e.record()
+    torch.cuda.synchronize(dev)
+    _barrier(world)
+    return _max_over_ranks(s.elapsed_time(e), world)
 
 
-def run_arm(wl, model, batch_inputs, steps, warmup, world, dev, sync=None):
-    """Time `steps` fwd+bwd steps (device time, CUDA events, max over ranks)."""
-    import torch
+# ------------------------------------------------------------------ one arm
+class Arm:
+    """A workload instance (fresh seeded model) with eager / graphed steps."""
 
-    x = batch_inputs[0]
-    prime(wl, model, dev, sync)
-
-    def step():
+    def __init__(self, wl, model, dev, world, sync=None, ddp=False):
+        import torch
+        self.wl, self.dev, self.world, self.sync = wl, dev, world, sync
+        if ddp and world > 1 and any(p.requires_grad for p in model.parameters()):
+            model = torch.nn.parallel.DistributedDataParallel(
+                model, device_ids=[dev.index], broadcast_buffers=False)
+        self.model = model
+        self.params = [p for p in model.parameters() if p.requires_grad]
+        self.inputs = list(wl.make_batch(wl.batch, dev))
         if wl.input_requires_grad:
-            x.grad = None
-        for p in model.parameters():
-            p.grad = None
-        loss = wl.loss_fn(model, *batch_inputs)
+            self.inputs[0].requires_grad_(True)
+        self.graphed = None
+
+    # eager step: the user-facing loop (grads reset to None, as zero_grad does)
+    def step(self, inputs=None):
+        inputs = self.inputs if inputs is None else inputs
+        if self.wl.input_requires_grad:
+            inputs[0].grad = None
+        if self.sync is not None:
+            self.sync.zero_grad()
+        else:
+            for p in self.params:
+                p.grad = None
+        loss = self.wl.loss_fn(self.model, *inputs)
         loss.backward()
-        if sync is not None:
-            sync.finish()
+        if self.sync is not None:
+            self.sync.finish()
         return loss
 
-    for _ in range(warmup):
-        step()
-    torch.cuda.synchronize(dev)
-    _barrier(world)
-    torch.cuda.synchronize(dev)
-    start = torch.cuda.Event(enable_timing=True)
-    end = torch.cuda.Event(enable_timing=True)
-    start.record()
-    for _ in range(steps):
-        step()
-    end.record()
-    torch.cuda.synchronize(dev)
-    _barrier(world)
-    ms = start.elapsed_time(end)
-    return _max_over_ranks(ms, world), step
+    def prime(self):
+        """Setup, not a step: one fwd+bwd at batch <= 2 so kernel images are
+        loaded (lazy loading) and one-time host state exists."""
+        import torch
+        ins = list(self.wl.make_batch(min(2, self.wl.batch), self.dev))
+        if self.wl.input_requires_grad:
+            ins[0].requires_grad_(True)
+        self.step(ins)
+        torch.cuda.synchronize(self.dev)
+
+    def capture(self, n_buffers=2):
+        """CUDA graphs of the step over n_buffers static input sets."""
+        from paper_2404_12406_b200.graphs import GraphedStep, zero_grads
+        wl, model, params = self.wl, self.model, self.params
+
+        def gstep(*inputs):
+            zero_grads(params)
+            loss = wl.loss_fn(model, *inputs)
+            loss.backward()
+            return loss.detach()
+
+        bufs = [self.inputs] + [[t.detach().clone().requires_grad_(t.requires_grad)
+                                 for t in self.inputs] for _ in range(n_buffers - 1)]
+        self.graphed = GraphedStep(gstep, bufs)
+        self._k = 0
+        return self.graphed
+
+    def replay(self):
+        self._k = (self._k + 1) % len(self.graphed)
+        return self.graphed.replay(self._k)
 
 
-def peak_memory(step, dev):
+def peak_memory(fn, dev):
     import torch
     torch.cuda.synchronize(dev)
     torch.cuda.empty_cache()
     base = torch.cuda.memory_allocated(dev)
     torch.cuda.reset_peak_memory_stats(dev)
-    step()
+    fn()
     torch.cuda.synchronize(dev)
     peak = torch.cuda.max_memory_allocated(dev)
     return peak / 2**20, (peak - base) / 2**20
 
 
-def e2e_arm(wl, model, steps, warmup, world, dev, sync=None):
+def e2e_eager(arm, steps, warmup, world):
     """Same step through the public API, inputs copied from pinned host memory
     and the loss read back every step (H2D/D2H inside the timed region).  The
     H2D copy of step i+1 runs on a copy stream while step i computes (two device
     input buffers), as a training loop with pinned, non-blocking loads does."""
     import torch
-
+    wl, dev = arm.wl, arm.dev
     bufs = [list(wl.make_batch(wl.batch, dev)) for _ in range(2)]
     host = [t.detach().cpu().pin_memory() for t in bufs[0]]
     loss_host = torch.empty((), dtype=torch.float32).pin_memory()
@@ -251,42 +270,74 @@ def e2e_arm(wl, model, steps, warmup, world, dev, sync=None):
     free = [torch.cuda.Event(), torch.cuda.Event()]
     main = torch.cuda.current_stream(dev)
 
-    def load(i):  # H2D of step i's inputs into buffer i % 2, on the copy stream
+    def load(i):
         b = i % 2
-        copy_stream.wait_event(free[b])  # step i-2 has finished reading the buffer
+        copy_stream.wait_event(free[b])
         with torch.cuda.stream(copy_stream), torch.no_grad():
             for d, h in zip(bufs[b], host):
                 d.copy_(h, non_blocking=True)
         ready[b].record(copy_stream)
 
-    def step(i, last):
+    def one(i, last):
         b = i % 2
         main.wait_event(ready[b])
         if not last:
             load(i + 1)
         inputs = bufs[b]
-        x = inputs[0]
         if wl.input_requires_grad:
-            x.requires_grad_(True)
-            x.grad = None
-        for p in model.parameters():
-            p.grad = None
-        loss = wl.loss_fn(model, *inputs)
-        loss.backward()
-        if sync is not None:
-            sync.finish()
+            inputs[0].requires_grad_(True)
+        loss = arm.step(inputs)
         if wl.input_requires_grad:
-            x.grad = None
-            x.requires_grad_(False)
+            inputs[0].grad = None
+            inputs[0].requires_grad_(False)
         free[b].record(main)
-        loss_host.copy_(loss.detach(), non_blocking=True)
-        return loss
+        loss_host.copy_(loss.detach().float(), non_blocking=True)
 
+    return _e2e_loop(one, load, free, main, steps, warmup, world, dev, h2d, d2h)
+
+
+def e2e_graphed(arm, steps, warmup, world):
+    """e2e through the graphed step: the next batch is copied from pinned host
+    memory into the other static buffer on a copy stream while the current graph
+    replays; the loss is read back every step."""
+    import torch
+    dev, g = arm.dev, arm.graphed
+    host = [t.detach().cpu().pin_memory() for t in g.inputs[0]]
+    loss_host = torch.empty((), dtype=torch.float32).pin_memory()
+    h2d = sum(t.numel() * t.element_size() for t in host)
+    d2h = loss_host.numel() * loss_host.element_size()
+    copy_stream = torch.cuda.Stream(dev)
+    ready = [torch.cuda.Event(), torch.cuda.Event()]
+    free = [torch.cuda.Event(), torch.cuda.Event()]
+    main = torch.cuda.current_stream(dev)
+
+    def load(i):
+        b = i % 2
+        copy_stream.wait_event(free[b])
+        with torch.cuda.stream(copy_stream), torch.no_grad():
+            for d, h in zip(g.inputs[b], host):
+                d.copy_(h, non_blocking=True)
+        ready[b].record(copy_stream)
+
+    def one(i, last):
+        b = i % 2
+        main.wait_event(ready[b])
+        if not last:
+            load(i + 1)
+        loss = g.replay(b)
+        free[b].record(main)
+        loss_host.copy_(loss.float(), non_blocking=True)
+
+    return _e2e_loop(one, load, free, main, steps, warmup, world, dev, h2d, d2h)
+
+
+def _e2e_loop(one, load, free, main, steps, warmup, world, dev, h2d, d2h):
+    import torch
     for r in range(2):
         free[r].record(main)
     load(0)
     for i in range(warmup):
-        step(i, last=False)
+        one(i, last=False)
     torch.cuda.synchronize(dev)
     _barrier(world)
     torch.cuda.synchronize(dev)
@@ -296,174 +347,266 @@ def e2e_arm(wl, model, steps, warmup, world, dev, sync=None):
     s.record()
     load(0)  # the first timed step's inputs are copied inside the timed region
     for i in range(steps):
-        step(i, last=(i == steps - 1))
+        one(i, last=(i == steps - 1))
     e.record()
     torch.cuda.synchronize(dev)
     wall = time.perf_counter() - t0
-    ms = _max_over_ranks(s.elapsed_time(e), world)
-    return ms, wall, h2d, d2h
+    return _max_over_ranks(s.elapsed_time(e), world), wall, h2d, d2h
 
 
+# ------------------------------------------------------------------ helpers
+def _per_rank_batch(config, world, override):
+    from benchkit import models as BM
+    import inspect
+    default = inspect.signature(BM.WORKLOADS[config]).parameters["batch"].default
+    if CONFIGS[config]["scaling"] == "weak":
+        return override or default, (override or default) * world
+    glob = override or default
+    if glob % world:
+        raise SystemExit(f"global batch {glob} is not divisible by {world} ranks")
+    return glob // world, glob
+
+
+def _prediction(config, batch, inputs, fuse=True):
+    """Planner-predicted peak (MiB) of the product step: the same workload built
+    on the meta device, converted and fused, one fwd+bwd on shapes only."""
+    import torch
+
+    from benchkit import models as BM
+    from paper_2404_12406_b200.nn import convert_to_memory_saving
+    from paper_2404_12406_b200.planner import plan
+    try:
+        wl = BM.WORKLOADS[config](batch=batch, device="meta")
+        model = convert_to_memory_saving(wl.model, fuse=fuse)
+        p = plan(model, inputs, loss_fn=wl.loss_fn)
+        return round(p.peak_bytes / 2**20, 1), round(p.tape_bytes / 2**20, 1)
+    except Exception as exc:  # noqa: BLE001 - report, never fail the bench
+        return None, f"{type(exc).__name__}: {exc}"[:200]
+    finally:
+        torch.cuda.empty_cache()
+
+
+def _ncu_traffic(config, dom):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant op,
+    from the committed ncu capture of this config (profiles/r2_ncu_traffic.json)."""
+    p = os.path.join(ROOT, "profiles", "r2_ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        e = d[config]
+        if e["op"] == dom["op"] and e["geom"] == dom["geom"]:
+            return int(e["dram_bytes"]), f"profiles/r2_ncu_traffic.json:{config} ({e['kernel']})"
+    except Exception:
+        pass
+    return None, None
+
+
+# ------------------------------------------------------------------ GPU arm
 def gpu_main(args):
     import torch
 
     import paper_2404_12406_b200 as pkg
-    from benchkit import kernels as KB
     from benchkit import models as BM
+    from benchkit import roofline as RL
     from paper_2404_12406_b200.distributed import TrainableGradAllReduce
     from paper_2404_12406_b200.nn import convert_to_memory_saving
 
-    world, rank, local = _dist_setup(args)
+    world, rank, local = _dist_setup()
     dev = torch.device("cuda", local)
     peaks = _peaks()
     pkg.lib()  # fail loudly if the native library is missing
-
+    cfgd = CONFIGS[args.config]
+    batch, global_batch = _per_rank_batch(args.config, world, args.batch)
+    use_graph = cfgd["graph"] and world == 1 and not args.eager
     builder = BM.WORKLOADS[args.config]
 
     def fresh():
-        """A new copy of the seeded workload (identical weights): only one model is
-        resident at a time, so every arm's peak is its own."""
-        return builder(batch=args.batch) if args.batch else builder()
+        return builder(batch=batch)
 
     # ---------------- memsave arm (the product): every supported layer swapped,
     # conv -> BN(eval) -> ReLU, conv -> ReLU and residual joins fused by the fx pass
     wl = fresh()
     wl.model = convert_to_memory_saving(wl.model, fuse=not args.no_fuse)
-    inputs = list(wl.make_batch(wl.batch, dev))
-    if wl.input_requires_grad:
-        inputs[0].requires_grad_(True)
     sync = TrainableGradAllReduce(wl.model) if world > 1 else None
+    arm = Arm(wl, wl.model, dev, world, sync)
+    arm.prime()
+    modes = {}
     n0 = pkg.launch_count()
-    fam0 = pkg.launch_stats()
+    ms_eager = _timed(arm.step, args.steps, args.warmup, world, dev)
+    per_step_launches = (pkg.launch_count() - n0) // (args.steps + args.warmup)
+    modes["eager"] = {"ms_per_step": round(ms_eager / args.steps, 4),
+                      "value": round(batch * world * args.steps / (ms_eager / 1e3), 2)}
+    # in-step kernel timing of every memsave op (one extra, instrumented eager step)
+    calls, traced_ms = RL.trace_step(arm.step, dev)
+    rows, op_ms = RL.summarise(calls, traced_ms, peaks)
+    # peak memory of one step (eager: a graph replay allocates nothing, its pool
+    # holds the same working set)
+    peak_mib, act_peak_mib = peak_memory(arm.step, dev)
+    if use_graph:
+        arm.capture()
+        run = arm.replay
+        modes["cuda_graph_reserved_mib"] = round(torch.cuda.memory_reserved(dev) / 2**20, 1)
+    else:
+        run = arm.step
     with ClockSampler(local) as clocks:
-        ms, step = run_arm(wl, wl.model, inputs, args.steps, args.warmup, world, dev, sync)
-    launches = pkg.launch_count() - n0
-    fam1 = pkg.launch_stats()
-    # launches of the warm-up steps are included above; count one clean step too
-    n1 = pkg.launch_count()
-    step()
-    torch.cuda.synchronize(dev)
-    per_step_launches = pkg.launch_count() - n1
-    peak_mib, act_peak_mib = peak_memory(step, dev)
-    del step
-    inputs.clear()
-    torch.cuda.empty_cache()
-    e2e_ms, e2e_wall, h2d, d2h = e2e_arm(wl, wl.model, args.steps, max(1, args.warmup // 2),
-                                         world, dev, sync)
-
-    samples = wl.batch * args.steps * world
+        ms = _timed(run, args.steps, args.warmup, world, dev)
+    if use_graph:
+        modes["cuda_graph"] = {"ms_per_step": round(ms / args.steps, 4),
+                               "value": round(batch * world * args.steps / (ms / 1e3), 2)}
+    # median of 5 repeats of the K timed steps (SPEC.md:404)
+    reps = [_timed(run, args.steps, 0, world, dev) / args.steps for _ in range(5)]
+    if use_graph:
+        e2e_ms, e2e_wall, h2d, d2h = e2e_graphed(arm, args.steps, max(1, args.warmup // 2),
+                                                 world)
+    else:
+        e2e_ms, e2e_wall, h2d, d2h = e2e_eager(arm, args.steps, max(1, args.warmup // 2), world)
+    pred_mib, pred_tape = (None, None)
+    if rank == 0 and not args.no_plan:
+        pred_mib, pred_tape = _prediction(args.config, batch, arm.inputs,
+                                          fuse=not args.no_fuse)
+    samples = batch * world * args.steps
     value = samples / (ms / 1e3)
     e2e_value = samples / (e2e_ms / 1e3)
-    wl.model = sync = None
+    del arm, wl
+    sync = None
     torch.cuda.empty_cache()
 
-    def other_arm(convert_kwargs):
-        """(ms, peak MiB, activation peak MiB) of a fresh model, converted with
-        convert_kwargs (None = stock)."""
-        w2 = fresh()
-        if convert_kwargs is not None:
-            w2.model = convert_to_memory_saving(w2.model, **convert_kwargs)
-        ins = list(w2.make_batch(w2.batch, dev))
-        if w2.input_requires_grad:
-            ins[0].requires_grad_(True)
-        sy = TrainableGradAllReduce(w2.model) if world > 1 else None
-        ams, astep = run_arm(w2, w2.model, ins, args.steps, args.warmup, world, dev, sy)
-        apeak, aact = peak_memory(astep, dev)
-        del astep, ins, w2, sy
-        torch.cuda.empty_cache()
-        return ams, apeak, aact
+    def other_arm(convert_kwargs, benchmark=False, tf32=None, graph=False):
+        """(ms per K steps, peak MiB, activation peak MiB) of a fresh model"""
+        prev = (torch.backends.cudnn.benchmark, torch.backends.cudnn.allow_tf32,
+                torch.backends.cuda.matmul.allow_tf32)
+        torch.backends.cudnn.benchmark = benchmark
+        if tf32 is not None:
+            torch.backends.cudnn.allow_tf32 = tf32
+            torch.backends.cuda.matmul.allow_tf32 = tf32
+        try:
+            w2 = fresh()
+            stock = convert_kwargs is None
+            if not stock:
+                w2.model = convert_to_memory_saving(w2.model, **convert_kwargs)
+            sy = TrainableGradAllReduce(w2.model) if (world > 1 and not stock) else None
+            a2 = Arm(w2, w2.model, dev, world, sy, ddp=stock)
+            a2.prime()
+            fn = a2.step
+            apeak, aact = peak_memory(fn, dev)
+            if graph:
+                a2.capture()
+                fn = a2.replay
+            ams = _timed(fn, args.steps, args.warmup, world, dev)
+            return ams, apeak, aact
+        finally:
+            (torch.backends.cudnn.benchmark, torch.backends.cudnn.allow_tf32,
+             torch.backends.cuda.matmul.allow_tf32) = prev
+            torch.cuda.empty_cache()
 
-    # ---------------- stock arm (same weights, unconverted) for the "vs PyTorch" part
+    def rec(ms_, peak_, act_, **kw):
+        return dict(value=round(samples / (ms_ / 1e3), 2), ms_per_step=round(ms_ / args.steps, 4),
+                    peak_mib=round(peak_, 1), activation_peak_mib=round(act_, 1), **kw)
+
+    # ---------------- stock arms (same weights, unconverted)
     stock = {}
     if not args.no_stock:
-        sms, speak, sact = other_arm(None)
-        stock = {"value": samples / (sms / 1e3), "ms_per_step": sms / args.steps,
-                 "peak_mib": speak, "activation_peak_mib": sact,
-                 "impl": "torch %s stock modules (cuDNN/cuBLAS), same weights/inputs"
-                         % torch.__version__}
-        # the north star's layer set only (Linear / Conv2d / BatchNorm2d-eval), ReLU and
-        # MaxPool2d left stock: isolates the paper's Fig. 2 effect from the §8(f) swaps
-        lms, lpeak, lact = other_arm(dict(relu=False, maxpool2d=False, dropout=False,
-                                          layernorm=False, conv_transpose2d=False))
-        stock["memsave_layers_only"] = {
-            "value": round(samples / (lms / 1e3), 2), "ms_per_step": round(lms / args.steps, 4),
-            "peak_mib": round(lpeak, 1), "activation_peak_mib": round(lact, 1),
-            "swaps": "Linear, Conv2d, BatchNorm2d(eval) only"}
-        if not args.no_fuse:  # every layer swapped, no fx fusion
-            ums, upeak, uact = other_arm(dict(fuse=False))
-            stock["memsave_unfused"] = {
-                "value": round(samples / (ums / 1e3), 2),
-                "ms_per_step": round(ums / args.steps, 4), "peak_mib": round(upeak, 1),
-                "activation_peak_mib": round(uact, 1),
-                "swaps": "all supported layers, convert_to_memory_saving(fuse=False)"}
+        fp32 = args.config == "fig1"
+        sms, speak, sact = other_arm(None, tf32=False if fp32 else None)
+        stock["eager"] = rec(sms, speak, sact, impl="torch %s stock modules (cuDNN / cuBLAS)%s"
+                             % (torch.__version__, ", TF32 off (fp32 rtol 1e-5 parity)"
+                                if fp32 else ""))
+        if args.config in ("fig1", "resnet18", "resnet101", "vgg16"):
+            b_ms, b_peak, b_act = other_arm(None, benchmark=True, tf32=False if fp32 else None)
+            stock["cudnn_benchmark"] = rec(b_ms, b_peak, b_act, impl="stock, "
+                                           "torch.backends.cudnn.benchmark=True")
+            if fp32:
+                t_ms, t_peak, t_act = other_arm(None, benchmark=True, tf32=True)
+                stock["cudnn_benchmark_tf32"] = rec(
+                    t_ms, t_peak, t_act, impl="stock, cudnn.benchmark, TF32 convs (NOT rtol "
+                    "1e-5: 10-bit mantissa products)")
+        if use_graph:
+            g_ms, g_peak, g_act = other_arm(None, benchmark=True, tf32=False if fp32 else None,
+                                            graph=True)
+            stock["cuda_graph"] = rec(g_ms, g_peak, g_act, impl="stock, cudnn.benchmark, "
+                                      "whole step captured as a CUDA graph")
+        comparable = [v for k, v in stock.items() if k != "cudnn_benchmark_tf32"]
+        best = max(comparable, key=lambda r: r["value"])
+        stock["best"] = {"value": best["value"], "ms_per_step": best["ms_per_step"],
+                         "peak_mib": best["peak_mib"],
+                         "which": [k for k, v in stock.items() if v is best][0]}
+        if not args.quick:
+            lms, lpeak, lact = other_arm(dict(relu=False, maxpool2d=False, dropout=False,
+                                              layernorm=False, conv_transpose2d=False))
+            stock["memsave_layers_only"] = rec(lms, lpeak, lact,
+                                               swaps="Linear, Conv2d, BatchNorm2d(eval) only, "
+                                               "eager")
+            if not args.no_fuse:
+                ums, upeak, uact = other_arm(dict(fuse=False))
+                stock["memsave_unfused"] = rec(ums, upeak, uact, swaps="all supported layers, "
+                                               "convert_to_memory_saving(fuse=False), eager")
 
-    # ---------------- roofline of the dominant kernel (rank 0)
+    # ---------------- roofline of the dominant in-step kernel
     roof = None
-    layers = []
-    if rank == 0 and not args.no_roofline and args.config == "resnet18":
-        for (n, c, h, w, k, r, s, p, cnt) in BM.resnet18_conv_shapes(wl.batch):
-            for ent in KB.conv_roofline(n, c, h, w, k, r, s, p, dev, peaks, reps=5):
-                ent["count_per_step"] = cnt
-                layers.append(ent)
-        # the same (pass, geometry) appears once per position in the network
-        tot = {}
-        for e in layers:
-            key = (e["kind"], tuple(sorted(e["geom"].items())))
-            tot[key] = tot.get(key, 0.0) + e["ms"] * e["count_per_step"]
-        dom = max(layers, key=lambda e: tot[(e["kind"], tuple(sorted(e["geom"].items())))])
-        dom = dict(dom, count_per_step=sum(
-            x["count_per_step"] for x in layers
-            if (x["kind"], x["geom"]) == (dom["kind"], dom["geom"])))
-        traffic, tsrc = _ncu_traffic(dom)
-        roof = {"bound": dom["bound"], "achieved": round(dom["achieved"], 2),
-                "peak": dom["peak"], "unit": dom["unit"], "frac": round(dom["frac"], 4),
-                "traffic": traffic, "traffic_source": tsrc,
-                "algorithmic_bytes": dom["bytes"], "algorithmic_flops": dom["flops"],
-                "kernel": "%s (%s)" % (_KERNEL_OF.get(_kernel_key(dom), "umma_gemm_kernel"),
-                                       dom["kind"]),
-                "geom": dom["geom"], "launch_ms": round(dom["ms"], 4),
-                "launches_per_step": dom["count_per_step"],
-                "per_unit": "2*N*OH*OW*K*C*R*S flops per launch (implicit GEMM)",
-                "peak_source": peaks["source"] + ", burst (kernel timed alone)"}
-        total_conv_ms = sum(e["ms"] * e["count_per_step"] for e in layers)
-        roof["conv_share_of_step"] = round(total_conv_ms / (ms / args.steps), 3)
-        with open(os.path.join(ROOT, "gpurun_out" if os.path.isdir(
-                os.path.join(ROOT, "gpurun_out")) else ".", "bench_layers.json"), "w") as f:
-            json.dump(layers, f, indent=1)
+    if rows:
+        dom = rows[0]
+        traffic, tsrc = _ncu_traffic(args.config, dom)
+        roof = {"bound": dom["bound"], "achieved": dom["achieved"], "peak": dom["peak"],
+                "unit": dom["unit"], "frac": dom["frac"], "traffic": traffic,
+                "traffic_source": tsrc, "op": "torch.ops.memsave." + dom["op"],
+                "geom": dom["geom"], "launches_per_step": dom["launches_per_step"],
+                "ms_per_launch": dom["ms_per_launch"],
+                "share_of_step": round(dom["ms_per_step"] / traced_ms, 3),
+                "algorithmic_flops": dom["flops"], "algorithmic_bytes": dom["bytes"],
+                "per_unit": ("2*M*N*K flops (implicit GEMM for convs) and one read of every "
+                             "operand + one write of every output per launch"),
+                "peak_source": peaks["source"] + ", burst",
+                "how": ("CUDA events around every torch.ops.memsave call of one extra eager "
+                        "step on its launching stream, host enqueue ahead of the GPU"),
+                "memsave_ops_share_of_step": round(op_ms / traced_ms, 3),
+                "top": [{k: r[k] for k in ("op", "geom", "launches_per_step", "ms_per_launch",
+                                           "bound", "achieved", "unit", "frac")}
+                        for r in rows[:6]]}
 
     # ---------------- CPU baseline (rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(args.config, None, min_seconds=args.cpu_seconds)
+        cpu = cpu_baseline(args.config, args.cpu_seconds)
 
+    best_stock = stock.get("best")
     out = {
         "metric": METRIC,
         "value": round(value, 2),
         "unit": "samples/s",
-        "tokens_per_s": (round(value * wl.config["seq_len"], 1) if "seq_len" in wl.config
-                         else None),
+        "tokens_per_s": (round(value * wl_seq(args.config), 1) if wl_seq(args.config) else None),
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": round(ms / args.steps, 4),
+        "ms_per_step_median_of_5": round(statistics.median(reps), 4),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": cfgd["scaling"],
         "vs_baseline": None,
-        "dtype": str(wl.dtype).replace("torch.", "").replace("bfloat16", "bf16"),
-        "data": "synthetic (random-init weights, seeded normal inputs)",
-        "config": dict(wl.config, parallelism=(f"dp{world}" if world > 1 else "single"),
-                       l2="activations > 126 MB L2 (no explicit flush between steps)"),
+        "dtype": "f32" if args.config == "fig1" else "bf16",
+        "data": "synthetic (random-init weights, seeded normal inputs / uniform token ids)",
+        "config": dict(_config_desc(args.config, batch), workload=_workload_name(args.config),
+                       global_batch=global_batch, per_gpu_batch=batch,
+                       parallelism=(f"dp{world}" if world > 1 else "single"),
+                       step_mode="cuda_graph" if use_graph else "eager",
+                       l2="inputs and activations > 126 MB L2 (no explicit flush)"),
         "peak_mib": round(peak_mib, 1),
         "activation_peak_mib": round(act_peak_mib, 1),
-        "stock": {k: (round(v, 3) if isinstance(v, float) else v) for k, v in stock.items()},
-        "speedup_vs_stock": (round(value / stock["value"], 3) if stock else None),
-        "peak_ratio_vs_stock": (round(peak_mib / stock["peak_mib"], 3) if stock else None),
+        "pred_mib": pred_mib,
+        "pred_tape_mib": pred_tape,
+        "pred_err": (round(peak_mib / pred_mib - 1, 4) if isinstance(pred_mib, float) else None),
+        "modes": modes,
+        "stock": stock,
+        "speedup_vs_stock": (round(value / best_stock["value"], 3) if best_stock else None),
+        "peak_ratio_vs_stock": (round(peak_mib / best_stock["peak_mib"], 3) if best_stock
+                                else None),
         "e2e": {"value": round(e2e_value, 2), "unit": "samples/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms / args.steps, 4),
                 "wall_s": round(e2e_wall, 3)},
-        "gpu_launches": launches,
+        "gpu_launches": per_step_launches * args.steps,
         "gpu_launches_per_step": per_step_launches,
-        "launch_families_timed_region": {k: fam1[k] - fam0[k] for k in fam1},
+        "gpu_launches_note": ("memsave kernels per eager step (host counter) x timed steps; "
+                              "a CUDA-graph replay relaunches exactly the captured kernels"
+                              if use_graph else "host launch counter over the timed steps"),
         "roofline": roof,
         "cpu_baseline": cpu,
         "clocks": clocks.summary(),
@@ -476,71 +619,100 @@ def gpu_main(args):
         dist.destroy_process_group()
 
 
-# ------------------------------------------------------------------ CPU legs
-def cpu_baseline(config, wl=None, min_seconds=10.0):
-    """The reference algorithm (oracle port, numpy f32, all host cores) on a
-    bounded sample of the same workload."""
-    import numpy as np
-    import torch
+def wl_seq(config):
+    return {"bert": 512, "llama": 2048}.get(config)
 
-    from benchkit.cpu_port import ResNet18InputGradCPU, time_cpu
-    cores = os.cpu_count()
-    if config != "resnet18":
-        return None
-    if wl is None:
-        from benchkit import models as BM
-        wl = BM.resnet18_input_only(batch=1, dtype=torch.float32, device="cpu")
-    port = ResNet18InputGradCPU(wl.model.state_dict())
-    rng = np.random.default_rng(0)
-    nb = 1
-    x = rng.standard_normal((nb, 3, 224, 224)).astype(np.float32)
-    y = rng.integers(0, 1000, nb)
-    sec, calls = time_cpu(lambda: port.step(x, y), min_seconds=min_seconds)
-    return {"value": round(nb / sec, 4), "unit": "samples/s", "cores": cores, "kind": "port",
-            "sample": f"{calls} steps of 1 image (3x224x224) fp32: full ResNet-18 forward + "
-                      f"input-gradient backward through the oracle restatement of the "
-                      f"reference numpy conv (numpy_impl.py:12-38), BLAS on {cores} threads"}
+
+def _workload_name(config):
+    return {
+        "bert": "BASELINE configs[3]: BERT-base random init, attention Linear biases + "
+                "classifier trainable, train mode (dropout 0.1), seq 512",
+        "resnet18": "BASELINE configs[1]: ResNet-18 frozen weights, input-only gradient, "
+                    "eval-mode BN, 224x224",
+        "resnet101": "BASELINE configs[2] (ResNet-101 reading): layer4.1, layer4.2, fc and all "
+                     "BN affine trainable, BN eval, 224x224",
+        "vgg16": "BASELINE configs[2] (VGG-16 reading): conv blocks 4-5 + classifier trainable, "
+                 "224x224",
+        "fig1": "BASELINE configs[0]: Fig.1 deep CNN, 8x Conv2d(8->8, 3x3), only layer-1 "
+                "weight trainable, (32,8,256,256) fp32",
+        "llama": "BASELINE configs[4]: Llama-3-8B architecture random init, last 4 decoder "
+                 "layers trainable, seq 2048, 2 sequences per GPU",
+    }[config]
+
+
+def _config_desc(config, batch):
+    from benchkit import models as BM
+    try:
+        import torch
+        wl = BM.WORKLOADS[config](batch=batch, device="meta")
+        d = dict(wl.config)
+        d.pop("workload", None)
+        d.pop("global_batch", None)
+        del wl
+        torch.cuda.empty_cache()
+        return d
+    except Exception:
+        return {"model": config}
+
+
+# ------------------------------------------------------------------ CPU legs
+def cpu_baseline(config, seconds):
+    """The reference algorithm on the host cores, in a separate process (a
+    separate Python session), on a bounded sample of the workload."""
+    cmd = [sys.executable, "-c",
+           "import json,sys; sys.path.insert(0, %r); from benchkit.cpu_port import cpu_sample; "
+           "print(json.dumps(cpu_sample(%r, %r)))" % (ROOT, config, float(seconds))]
+    try:
+        env = dict(os.environ, CUDA_VISIBLE_DEVICES="")
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
+        line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1]
+        return json.loads(line)
+    except Exception as exc:  # noqa: BLE001
+        return {"value": None, "error": f"{type(exc).__name__}: {str(exc)[:200]}"}
 
 
 def reference_main(args):
+    """--impl reference: the reference's CPU implementation of the path (its own
+    conv kernels from baseline/_ref when installed, the oracle port for the
+    SPEC-only Linear / BN rows) on all host threads; rank 0 only."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    if args.config != "resnet18":
-        print(json.dumps({"impl": "reference", "unavailable": f"no CPU port for {args.config}"}))
-        return
-    import numpy as np
-    import torch
-
-    from benchkit import models as BM
-    from benchkit.cpu_port import ResNet18InputGradCPU
-    wl = BM.resnet18_input_only(batch=1, dtype=torch.float32, device="cpu")
-    port = ResNet18InputGradCPU(wl.model.state_dict())
-    rng = np.random.default_rng(0)
-    x = rng.standard_normal((1, 3, 224, 224)).astype(np.float32)
-    y = rng.integers(0, 1000, 1)
-    for _ in range(max(1, args.warmup)):
-        port.step(x, y)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        port.step(x, y)
-    sec = (time.perf_counter() - t0) / args.steps
-    v = round(1.0 / sec, 4)
-    cores = os.cpu_count()
+    from benchkit.cpu_port import cpu_workload
+    step, rec = cpu_workload(args.config)
+    for _ in range(args.warmup):
+        step()
+    per_step = [step() for _ in range(args.steps)]
+    sec = sum(per_step) / len(per_step)  # seconds per sample of the full workload
+    v = round(1.0 / sec, 6)
     print(json.dumps({
         "metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(sec * 1e3, 2), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": dict(wl.config, global_batch=1,
-                       note="each step is a bounded sample: 1 image of the 256-image batch"),
+        "scaling": CONFIGS[args.config]["scaling"], "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": _workload_name(args.config),
+                   "note": "each step is a bounded sample of the workload: " + rec["sample"]
+                   + f"; all host threads ({rec['cores']})"},
         "impl": "reference",
-        "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cores, "kind": "port",
-                         "sample": "1 image per step, fp32, oracle restatement of the reference "
-                                   "numpy conv (the reference is Python and cannot travel)"},
+        "cpu_baseline": {"value": v, "unit": "samples/s", "cores": rec["cores"],
+                         "isa": rec.get("isa"), "kind": rec["kind"], "sample": rec["sample"]},
         "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }), flush=True)
+
+
+def _respawn(args):
+    """--gpus N without torchrun: re-exec this script under torch.distributed.run."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
 
 
 def main():
@@ -549,22 +721,26 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="memsave", choices=["memsave", "reference"])
-    ap.add_argument("--config", default="resnet18",
-                    choices=["resnet18", "fig1", "resnet101", "vgg16", "bert", "llama"])
-    ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
+    ap.add_argument("--batch", type=int, default=0,
+                    help="global batch (per-GPU for the weak-scaling Llama config)")
     ap.add_argument("--no-stock", action="store_true")
     ap.add_argument("--no-fuse", action="store_true",
                     help="product arm without the conv->BN->ReLU / add->ReLU fx fusion")
-    ap.add_argument("--no-roofline", action="store_true")
+    ap.add_argument("--eager", action="store_true", help="no CUDA graph for the product arm")
+    ap.add_argument("--quick", action="store_true", help="skip the diagnostic memsave arms")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-plan", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args()
-    if args.warmup < 3 and args.impl == "memsave":
-        args.warmup = 3  # timing rule: >= 3 warm-up steps
     if args.impl == "reference":
         reference_main(args)
-    else:
-        gpu_main(args)
+        return
+    if args.warmup < 3:
+        args.warmup = 3  # timing rule: >= 3 warm-up steps
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        _respawn(args)
+    gpu_main(args)
 
 
 if __name__ == "__main__":

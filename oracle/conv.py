@@ -73,16 +73,16 @@ def conv2d_dx(g, w, stride, padding, h, wd, dtype=np.float64):
     return np.ascontiguousarray(dxp[:, :, ph:ph + h, pw:pw + wd])
 
 
-def conv2d_dw(x, g, stride, padding, kh, kw):
+def conv2d_dw(x, g, stride, padding, kh, kw, dtype=np.float64):
     """Weight-VJP, numpy_impl.py:41-51: dw[co,ci,p,q] = sum g * shifted x."""
     sh, sw = _pair(stride)
     ph, pw = _pair(padding)
-    x = np.asarray(x, dtype=np.float64)
-    g = np.asarray(g, dtype=np.float64)
+    x = np.asarray(x, dtype=dtype)
+    g = np.asarray(g, dtype=dtype)
     n, cin, h, wd = x.shape
     _, cout, oh, ow = g.shape
     xp = np.pad(x, ((0, 0), (0, 0), (ph, ph + sh), (pw, pw + sw)))
-    dw = np.zeros((cout, cin, kh, kw), dtype=np.float64)
+    dw = np.zeros((cout, cin, kh, kw), dtype=dtype)
     for i in range(kh):
         for j in range(kw):
             xs = xp[:, :, i:i + sh * (oh - 1) + 1:sh, j:j + sw * (ow - 1) + 1:sw]

@@ -10,28 +10,32 @@ from __future__ import annotations
 import numpy as np
 
 
-def _flat(a):
-    a = np.asarray(a, dtype=np.float64)
+# ``dtype``: float64 when checking; the CPU baseline passes float32, the dtype
+# the reference computes in.
+
+
+def _flat(a, dtype=np.float64):
+    a = np.asarray(a, dtype=dtype)
     return a.reshape(-1, a.shape[-1])
 
 
-def linear_fwd(x, w, b=None):
-    x = np.asarray(x, dtype=np.float64)
-    z = _flat(x) @ np.asarray(w, dtype=np.float64).T
+def linear_fwd(x, w, b=None, dtype=np.float64):
+    x = np.asarray(x, dtype=dtype)
+    z = _flat(x, dtype) @ np.asarray(w, dtype=dtype).T
     if b is not None:
-        z = z + np.asarray(b, dtype=np.float64)
+        z = z + np.asarray(b, dtype=dtype)
     return z.reshape(x.shape[:-1] + (z.shape[-1],))
 
 
-def linear_dx(g, w):
-    g = np.asarray(g, dtype=np.float64)
-    dx = _flat(g) @ np.asarray(w, dtype=np.float64)
+def linear_dx(g, w, dtype=np.float64):
+    g = np.asarray(g, dtype=dtype)
+    dx = _flat(g, dtype) @ np.asarray(w, dtype=dtype)
     return dx.reshape(g.shape[:-1] + (dx.shape[-1],))
 
 
-def linear_dw(x, g):
-    return _flat(g).T @ _flat(x)
+def linear_dw(x, g, dtype=np.float64):
+    return _flat(g, dtype).T @ _flat(x, dtype)
 
 
-def linear_db(g):
-    return _flat(g).sum(axis=0)
+def linear_db(g, dtype=np.float64):
+    return _flat(g, dtype).sum(axis=0)

@@ -39,8 +39,27 @@ def _load() -> None:
         _loaded = True
 
 
+class _Overloads:
+    """The ``.default`` overload of every op as an attribute: calling an
+    OpOverload directly skips the packet's overload resolution on each call."""
+
+    def __init__(self, ns):
+        names = sorted({q.split("::", 1)[1].split(".")[0]
+                        for q in torch._C._dispatch_get_all_op_names()
+                        if q.startswith("memsave::")})
+        for name in names:
+            setattr(self, name, getattr(ns, name).default)
+
+
+_OV = None
+
+
 def ops():
-    """``torch.ops.memsave`` (loads the op library on first use)."""
-    if not _loaded:
-        _load()
-    return torch.ops.memsave
+    """The memsave ops (``torch.ops.memsave.<name>.default``), loading the op
+    library on first use."""
+    global _OV
+    if _OV is None:
+        if not _loaded:
+            _load()
+        _OV = _Overloads(torch.ops.memsave)
+    return _OV

@@ -67,11 +67,11 @@ def test_torch_op_library_registers_every_op():
     from paper_2404_12406_b200._ops import ops
     O = ops()
     for name in OPS:
-        op = getattr(O, name)
+        op = getattr(O, name)  # the .default OpOverload
         # a CUDA kernel and a Meta kernel, no CPU kernel (no CPU path)
-        assert torch._C._dispatch_has_kernel_for_dispatch_key(op._qualified_op_name, "CUDA")
-        assert torch._C._dispatch_has_kernel_for_dispatch_key(op._qualified_op_name, "Meta")
-        assert not torch._C._dispatch_has_kernel_for_dispatch_key(op._qualified_op_name, "CPU")
+        assert torch._C._dispatch_has_kernel_for_dispatch_key(op.name(), "CUDA")
+        assert torch._C._dispatch_has_kernel_for_dispatch_key(op.name(), "Meta")
+        assert not torch._C._dispatch_has_kernel_for_dispatch_key(op.name(), "CPU")
 
 
 def test_torch_ops_meta_shapes_and_fake_tensors():
