@@ -112,6 +112,42 @@ class _Ledger(TorchDispatchMode):
         return out
 
 
+class _FusedSDPA:
+    """On CUDA, ``F.scaled_dot_product_attention`` runs a fused kernel (flash, or
+    memory-efficient when a mask is given) that keeps O(L) statistics, not the
+    L x L attention matrix; on ``meta`` its backend choice falls to the math path,
+    which materialises it.  While planning, route meta SDPA calls to the fused
+    kernels' own meta functions so the prediction matches the GPU run."""
+
+    def __enter__(self):
+        import torch.nn.functional as F
+        self._orig = F.scaled_dot_product_attention
+        orig = self._orig
+
+        def sdpa(q, k, v, attn_mask=None, dropout_p=0.0, is_causal=False, scale=None,
+                 enable_gqa=False):
+            if q.device.type != "meta":
+                return orig(q, k, v, attn_mask=attn_mask, dropout_p=dropout_p,
+                            is_causal=is_causal, scale=scale, enable_gqa=enable_gqa)
+            if enable_gqa and k.shape[-3] != q.shape[-3]:
+                rep = q.shape[-3] // k.shape[-3]
+                k = k.repeat_interleave(rep, dim=-3)
+                v = v.repeat_interleave(rep, dim=-3)
+            if attn_mask is None:
+                return torch.ops.aten._scaled_dot_product_flash_attention(
+                    q, k, v, dropout_p, is_causal, False, scale=scale)[0]
+            return torch.ops.aten._scaled_dot_product_efficient_attention(
+                q, k, v, attn_mask.expand(q.shape[0], q.shape[1], q.shape[2], k.shape[2]),
+                q.requires_grad, dropout_p, is_causal, scale=scale)[0]
+
+        F.scaled_dot_product_attention = sdpa
+        return self
+
+    def __exit__(self, *exc):
+        import torch.nn.functional as F
+        F.scaled_dot_product_attention = self._orig
+
+
 def _to_meta(model: nn.Module) -> nn.Module:
     m = copy.deepcopy(model).to("meta")
     for (_n, p), (_n2, p0) in zip(m.named_parameters(), model.named_parameters()):
@@ -164,7 +200,7 @@ def plan(model: nn.Module, inputs: Sequence[torch.Tensor],
         resident += _storage_nbytes(t)
     ledger.live = ledger.peak = resident
     try:
-        with ledger, torch.autograd.graph.saved_tensors_hooks(pack, lambda t: t):
+        with ledger, _FusedSDPA(), torch.autograd.graph.saved_tensors_hooks(pack, lambda t: t):
             out = loss_fn(mm, *metas) if loss_fn else mm(*metas)
             fwd_peak = ledger.peak
             if backward and isinstance(out, torch.Tensor) and out.requires_grad:
