@@ -467,8 +467,12 @@ def gpu_main(args):
     samples = batch * world * args.steps
     value = samples / (ms / 1e3)
     e2e_value = samples / (e2e_ms / 1e3)
-    del arm, wl
+    # release the product model before the other arms (their peaks are their own):
+    # `run` is a bound method of the arm and keeps it alive
+    del arm, wl, run
     sync = None
+    import gc
+    gc.collect()
     torch.cuda.empty_cache()
 
     def other_arm(convert_kwargs, benchmark=False, tf32=None, graph=False):
@@ -493,10 +497,13 @@ def gpu_main(args):
                 a2.capture()
                 fn = a2.replay
             ams = _timed(fn, args.steps, args.warmup, world, dev)
+            del fn, a2, w2, sy
             return ams, apeak, aact
         finally:
             (torch.backends.cudnn.benchmark, torch.backends.cudnn.allow_tf32,
              torch.backends.cuda.matmul.allow_tf32) = prev
+            import gc
+            gc.collect()
             torch.cuda.empty_cache()
 
     def rec(ms_, peak_, act_, **kw):

@@ -22,6 +22,10 @@ ap.add_argument("--steps", type=int, default=4)
 ap.add_argument("--warmup", type=int, default=3)
 ap.add_argument("--stock", action="store_true")
 ap.add_argument("--no-fuse", action="store_true")
+ap.add_argument("--mark", default="", help="memsave op whose calls get an NVTX range "
+                "'dominant' (ncu --nvtx --nvtx-include 'dominant/')")
+ap.add_argument("--mark-geom", default="", help="JSON geometry the marked call must match "
+                "(benchkit.roofline.work_of)")
 a = ap.parse_args()
 
 dev = torch.device("cuda", 0)
@@ -45,6 +49,30 @@ def step():
 for _ in range(a.warmup):
     step()
 torch.cuda.synchronize()
+if a.mark:
+    import json
+
+    from benchkit.roofline import work_of
+    from paper_2404_12406_b200 import _ops as OPS
+    want = json.loads(a.mark_geom) if a.mark_geom else None
+    real = OPS.ops()
+
+    class _Marker:
+        def __getattr__(self, name):
+            fn = getattr(real, name)
+            if name != a.mark:
+                return fn
+
+            def wrapped(*args):
+                hit = want is None or work_of(name, args)[2] == want
+                if hit:
+                    torch.cuda.nvtx.range_push("dominant")
+                out = fn(*args)
+                if hit:
+                    torch.cuda.nvtx.range_pop()
+                return out
+            return wrapped
+    OPS._OV = _Marker()
 torch.cuda.cudart().cudaProfilerStart()
 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 s.record()
