@@ -110,7 +110,14 @@ ConvPlan plan(const ms_conv_desc* d, int pass, bool dx_bias = false) {
   const size_t es = dtype_size(d->dtype);
   const int64_t taps = (int64_t)d->r * d->s;
   if (!tc_ok(d)) {
-    if (pass == MS_CONV_DW) p.ws = align256(simt_conv_dw_workspace(c));
+    if (pass == MS_CONV_DW) {
+      size_t w = simt_conv_dw_workspace(c);
+      if (d->dtype == MS_F32) {
+        const size_t s = small_conv_fp32_workspace(c, pass);
+        if (s > w) w = s;
+      }
+      p.ws = align256(w);
+    }
     return p;
   }
   if (pass == MS_CONV_FWD) {

@@ -27,6 +27,7 @@ ms_status simt_conv_dw(const ConvDims& d, int dt, int layout, int wlayout, const
 // MS_ERR_UNSUPPORTED when the geometry does not match
 ms_status small_conv_fp32(int pass, const ConvDims& d, int layout, int wlayout, const void* a,
                           const void* b, void* out, void* ws, size_t ws_bytes, cudaStream_t st);
+size_t small_conv_fp32_workspace(const ConvDims& d, int pass);
 
 // reductions / elementwise helpers (misc.cu)
 size_t colsum_workspace(int64_t cols);

@@ -147,8 +147,26 @@ __global__ void f64_to_f32_kernel(const double* a, float* b, int n) {
 }  // namespace
 
 // Returns MS_ERR_UNSUPPORTED when the geometry is not the specialised one.
+bool conv3x3_tf32_applies(const ConvDims& d, int layout, int wlayout, int pass);
+ms_status conv3x3_tf32(int pass, const ConvDims& d, const void* a, const void* b, void* out,
+                       cudaStream_t st);
+size_t conv3x3_c8_dw_workspace(const ConvDims& d);
+ms_status conv3x3_c8_dw(const ConvDims& d, const void* x, const void* g, void* dw, void* ws,
+                        size_t ws_bytes, cudaStream_t st);
+
+size_t small_conv_fp32_workspace(const ConvDims& d, int pass) {
+  if (pass == MS_CONV_DW && conv3x3_tf32_applies(d, MS_NCHW, MS_NCHW, MS_CONV_DW))
+    return conv3x3_c8_dw_workspace(d);
+  return pass == MS_CONV_DW ? sizeof(double) * 576 : 0;
+}
+
 ms_status small_conv_fp32(int pass, const ConvDims& d, int layout, int wlayout, const void* a,
                           const void* b, void* out, void* ws, size_t ws_bytes, cudaStream_t st) {
+  // tensor cores (3xTF32) for fwd / dX, the CUDA-core partial-sum kernel for dW
+  if (conv3x3_tf32_applies(d, layout, wlayout, pass)) {
+    if (pass == MS_CONV_DW) return conv3x3_c8_dw(d, a, b, out, ws, ws_bytes, st);
+    return conv3x3_tf32(pass, d, a, b, out, st);
+  }
   const bool ok = layout == MS_NCHW && wlayout == MS_NCHW && d.r == 3 && d.s == 3 && d.sh == 1 &&
                   d.sw == 1 && d.ph == 1 && d.pw == 1 && d.c == 8 && d.k == 8;
   if (!ok) return MS_ERR_UNSUPPORTED;

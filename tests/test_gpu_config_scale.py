@@ -282,3 +282,29 @@ def test_vgg16_layer_by_layer_vs_oracle():
     x = x.contiguous(memory_format=torch.channels_last)
     n = _layer_by_layer(m, x, "vgg16")
     assert n >= 30, n
+
+
+FIG1_SHAPES = [(2, 8, 20, 36), (1, 8, 9, 260), (3, 8, 64, 128), (32, 8, 256, 256)]
+
+
+@pytest.mark.parametrize("shape", FIG1_SHAPES)
+def test_fig1_conv_3xtf32_tensor_cores(shape):
+    """The Fig. 1 conv (8 -> 8, 3x3/1/1, fp32 NCHW) runs fwd and dX on the tcgen05
+    kind::tf32 kernel (3xTF32 split) and dW on the CUDA-core partial-sum kernel;
+    all three at the fp32 bar (rtol 1e-5 vs the f64 oracle)."""
+    n, c, h, w = shape
+    gen = torch.Generator(device=DEV).manual_seed(n * h + w)
+    x = torch.randn(shape, generator=gen, device=DEV).requires_grad_(True)
+    wt = (torch.randn((8, 8, 3, 3), generator=gen, device=DEV) / 24).requires_grad_(True)
+    g = torch.randn(shape, generator=gen, device=DEV)
+    u0 = launch_stats()["umma"]
+    y = MF.conv2d(x, wt, None, 1, 1)
+    y.backward(g)
+    torch.cuda.synchronize()
+    assert launch_stats()["umma"] - u0 >= 2  # fwd and dX on the tensor cores
+    k = min(n, 2)
+    xq, gq, wq = _np(x), _np(g), _np(wt)
+    oracle.assert_close_fp32(_np(y[:k]), oracle.conv2d_fwd(xq[:k], wq, 1, 1), what="y")
+    oracle.assert_close_fp32(_np(x.grad[:k]), oracle.conv2d_dx(gq[:k], wq, 1, 1, h, w),
+                             what="dx")
+    oracle.assert_close_fp32(_np(wt.grad), oracle.conv2d_dw(xq, gq, 1, 1, 3, 3), what="dW")

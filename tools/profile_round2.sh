@@ -24,4 +24,8 @@ for c in ${CONFIGS:-bert resnet18 resnet101 vgg16 fig1 llama r101bn r101bnf}; do
     --nvtx --nvtx-include "dominant/" -c 2 -f -o $OUT/r2_ncu_$c \
     python tools/prof_step.py --config $cfg --steps 1 --mark ${OP[$c]} --mark-geom "${GEOM[$c]}" \
     > $OUT/r2_ncu_$c.log 2>&1
+  # keep the summaries, not the (large) report
+  ncu -i $OUT/r2_ncu_$c.ncu-rep --page raw --csv > $OUT/r2_ncu_${c}_raw.csv 2>/dev/null
+  ncu -i $OUT/r2_ncu_$c.ncu-rep --page details --csv > $OUT/r2_ncu_${c}_details.csv 2>/dev/null
+  rm -f $OUT/r2_ncu_$c.ncu-rep
 done
