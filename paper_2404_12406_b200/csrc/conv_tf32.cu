@@ -15,7 +15,7 @@
 // and stores hi / lo for the 9 taps with tcgen05.st (144 columns).  The MMAs then
 // read A from TMEM (the "TS" form) and only the 512-byte weight tiles from
 // shared memory, so a K = 8 MMA is not paced by a 4 KB shared-memory A fetch.
-// Input rows arrive by TMA (3-D box [8 ch][1 row][132 px] of the NCHW tensor,
+// Input rows arrive by TMA (3-D box [8 ch][1 row][136 px] of the NCHW tensor,
 // zero fill outside the image = the padding); a CTA walks down a strip of rows
 // so each input row is loaded once per strip and serves three output rows.
 //
@@ -31,7 +31,8 @@ namespace {
 constexpr int T3_M = 128;            // output pixels per tile (a row segment)
 constexpr int T3_N = 16;             // MMA N: output channels padded to 16
 constexpr int T3_C = 8;              // input channels = one tf32 K step
-constexpr int T3_LW = 132;           // staged pixels per input row (w0-1 .. w0+130)
+constexpr int T3_LW = 136;           // staged pixels per input row (w0-4 .. w0+131): the
+                                     // innermost TMA coordinate must stay 16-byte aligned
 constexpr int T3_ROWB = T3_C * T3_LW * 4;  // bytes of one staged row
 constexpr int T3_SLOTS = 8;          // input-row ring
 constexpr int T3_R = 8;              // output rows per work unit
@@ -108,7 +109,7 @@ __device__ __forceinline__ void unit_coords(const T3Args& a, int u, int& n, int&
 __global__ void __launch_bounds__(T3_THREADS) conv3x3_tf32_kernel(const __grid_constant__
                                                                   CUtensorMap tx, T3Args a) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  float* ring = reinterpret_cast<float*>(smem);                       // [SLOTS][8][132]
+  float* ring = reinterpret_cast<float*>(smem);                       // [SLOTS][8][136]
   uint8_t* sB = smem + T3_SLOTS * T3_ROWB;                             // 18 x 512 B
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + 18 * 512);         // [SLOTS]
   uint64_t* mma_bar = full + T3_SLOTS;
@@ -179,7 +180,7 @@ __global__ void __launch_bounds__(T3_THREADS) conv3x3_tf32_kernel(const __grid_c
       const int slot = issued % T3_SLOTS;
       const uint32_t bar = smem_u32(&full[slot]);
       mbar_arrive_expect_tx(bar, T3_ROWB);
-      tma_load_3d(smem_u32(ring) + slot * T3_ROWB, &tx, bar, w0 - 1, h0 - 1 + j, n * T3_C);
+      tma_load_3d(smem_u32(ring) + slot * T3_ROWB, &tx, bar, w0 - 4, h0 - 1 + j, n * T3_C);
       ++issued;
     }
   };
@@ -214,7 +215,7 @@ __global__ void __launch_bounds__(T3_THREADS) conv3x3_tf32_kernel(const __grid_c
         mbar_wait(smem_u32(&full[e % T3_SLOTS]), (e / T3_SLOTS) & 1);
       }
       // ---- build A: thread tid = pixel w0 + tid; tap (r, s) reads input column
-      // w0 + tid + s - 1 = staged index tid + s
+      // w0 + tid + s - 1 = staged index tid + s + 3
 #pragma unroll
       for (int r = 0; r < 3; ++r) {
         const float* row = ring + ((base + t + r) % T3_SLOTS) * (T3_C * T3_LW);
@@ -223,7 +224,7 @@ __global__ void __launch_bounds__(T3_THREADS) conv3x3_tf32_kernel(const __grid_c
           uint32_t hi[8], lo[8];
 #pragma unroll
           for (int c = 0; c < T3_C; ++c) {
-            const float v = row[c * T3_LW + tid + s];
+            const float v = row[c * T3_LW + tid + s + 3];
             const float h = tf32_hi(v);
             hi[c] = __float_as_uint(h);
             lo[c] = __float_as_uint(v - h);

@@ -391,17 +391,22 @@ def test_maxpool_relu_bwd_fused(shape, k, s, p, with_bn):
 
 @pytest.mark.parametrize("shape", [(2, 8, 40, 70), (1, 8, 16, 64), (3, 8, 33, 17)])
 def test_fig1_fp32_tiled_kernel(shape):
-    # the specialised float32 8->8 3x3/1 kernels (fwd, dX via flipped weights, dW)
+    # the specialised float32 8->8 3x3/1 kernels (fwd, dX via flipped weights, dW):
+    # fwd / dX on the tcgen05 kind::tf32 kernel when W % 4 == 0 (16-byte TMA row
+    # pitch), else the CUDA-core tiled kernel; dW always on the CUDA cores
     rng = np.random.default_rng(shape[2])
     x, xq = _q(rng.standard_normal(shape), "f32")
     w, wq = _q(rng.standard_normal((8, 8, 3, 3)) / 8, "f32")
     g, gq = _q(rng.standard_normal(shape), "f32")
     x.requires_grad_(True)
     w.requires_grad_(True)
-    s0 = launch_stats()["simt"]
+    s0 = launch_stats()
     y = MF.conv2d(x, w, None, 1, 1)
     y.backward(g)
-    assert launch_stats()["simt"] - s0 >= 3
+    s1 = launch_stats()
+    tc = s1["umma"] - s0["umma"]
+    assert tc == (2 if shape[3] % 4 == 0 else 0)
+    assert s1["simt"] - s0["simt"] + tc >= 3
     _close(y, oracle.conv2d_fwd(xq, wq, 1, 1), "f32", "y")
     _close(x.grad, oracle.conv2d_dx(gq, wq, 1, 1, shape[2], shape[3]), "f32", "dx")
     _close(w.grad, oracle.conv2d_dw(xq, gq, 1, 1, 3, 3), "f32", "dw")
