@@ -155,6 +155,13 @@ ms_status run_gemm(const LinPlan& p, int dt, int a_mn, int b_mn, const CUtensorM
   g.num_tiles = g.m_blocks * p.n_blocks * p.splits;
   g.ab_fmt = dt == MS_BF16 ? 1 : 0;
   g.nphases = 1;
+  {
+    static const int env_dbg = [] {
+      const char* e = getenv("MS_GEMM_DBG");
+      return e ? atoi(e) : 0;
+    }();
+    g.dbg = env_dbg;
+  }
   // N-blocks fastest when B (cols x red) fits well inside L2 and A does not: the
   // concurrent tiles then share their A rows and A streams from HBM once
   {

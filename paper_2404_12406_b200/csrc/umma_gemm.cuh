@@ -116,6 +116,9 @@ struct GemmArgs {
   // GEMM raster order: 0 = M-blocks fastest (concurrent tiles share B), 1 =
   // N-blocks fastest (they share A: A streams from HBM once when B fits in L2)
   int n_fastest;
+  // profiling switch (MS_GEMM_DBG, GEMM mode only): bit 0 drops the epilogue's
+  // stores, bit 1 also its TMEM loads -- isolates the main loop's feed rate
+  int dbg;
   ConvShape cv;
   int nphases;
   PhaseInfo phase[4];
@@ -764,6 +767,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
             }
           }
           __syncwarp();  // tcgen05.ld / wait are warp-collective: reconverge invalid rows
+          if (MODE == LOAD_GEMM && (g.dbg & 2)) continue;
           if (!zero) {
             tmem_ld_32x32b_x32(taddr + c, r);
             tmem_ld_wait_regs(r);
@@ -773,6 +777,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
           }
           const int nc = n0 + c;  // first column of this chunk in GEMM-N space
           if (nc >= ncols) continue;  // warp-uniform
+          if (MODE == LOAD_GEMM && (g.dbg & 1)) continue;
           float v[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
