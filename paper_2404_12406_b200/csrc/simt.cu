@@ -71,11 +71,63 @@ __global__ void __launch_bounds__(256) simt_gemm_kernel(int M, int N, int K, con
   }
 }
 
+// Skinny outputs with a long reduction (e.g. a 2-class head: M = 64, N = 2,
+// K = 768): one warp per output element, lanes split K, shuffle reduction.
+// The 64 x 64 tile kernel would run one block down the whole K.
+template <typename T>
+__global__ void __launch_bounds__(256) simt_dot_kernel(int M, int N, int K, const T* __restrict__ A,
+                                                       int64_t sam, int64_t sak,
+                                                       const T* __restrict__ B, int64_t sbk,
+                                                       int64_t sbn, const T* __restrict__ bias,
+                                                       T* __restrict__ C, int64_t ldc) {
+  using AT = typename Acc<T>::type;
+  const int64_t o = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (o >= (int64_t)M * N) return;
+  const int m = (int)(o / N), n = (int)(o % N);
+  const T* a = A + m * sam;
+  const T* b = B + n * sbn;
+  AT acc = 0;
+  for (int k = lane; k < K; k += 32)
+    acc += static_cast<AT>(IO<T>::ld(a + k * sak)) * static_cast<AT>(IO<T>::ld(b + k * sbk));
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (lane == 0) {
+    if (bias) acc += static_cast<AT>(IO<T>::ld(bias + n));
+    C[m * ldc + n] = IO<T>::cvt(static_cast<float>(acc));
+  }
+}
+
 ms_status simt_gemm(int dt, int M, int N, int K, const void* A, int64_t sam, int64_t sak,
                     const void* B, int64_t sbk, int64_t sbn, const void* bias, void* C,
                     int64_t ldc, cudaStream_t st) {
   if (M <= 0 || N <= 0) return MS_OK;
   dim3 grid((N + 63) / 64, (M + 63) / 64);
+  if ((int64_t)grid.x * grid.y < 16 && K >= 256 && (int64_t)M * N <= (1 << 16)) {
+    const unsigned blocks = (unsigned)(((int64_t)M * N + 7) / 8);
+    switch (dt) {
+      case MS_F32:
+        simt_dot_kernel<float><<<blocks, 256, 0, st>>>(M, N, K, (const float*)A, sam, sak,
+                                                       (const float*)B, sbk, sbn,
+                                                       (const float*)bias, (float*)C, ldc);
+        break;
+      case MS_BF16:
+        simt_dot_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>(
+            M, N, K, (const __nv_bfloat16*)A, sam, sak, (const __nv_bfloat16*)B, sbk, sbn,
+            (const __nv_bfloat16*)bias, (__nv_bfloat16*)C, ldc);
+        break;
+      case MS_F16:
+        simt_dot_kernel<__half><<<blocks, 256, 0, st>>>(M, N, K, (const __half*)A, sam, sak,
+                                                        (const __half*)B, sbk, sbn,
+                                                        (const __half*)bias, (__half*)C, ldc);
+        break;
+      default:
+        set_error("simt_gemm: bad dtype %d", dt);
+        return MS_ERR_DTYPE;
+    }
+    count_launch(1, KF_SIMT);
+    return launch_status("simt_dot_kernel");
+  }
   switch (dt) {
     case MS_F32:
       simt_gemm_kernel<float><<<grid, 256, 0, st>>>(M, N, K, (const float*)A, sam, sak,

@@ -211,6 +211,29 @@ def test_linear(case, dt):
     _close(b.grad, oracle.linear_db(gq), dt, "db")
 
 
+@pytest.mark.parametrize("dt", ["bf16", "f32"])
+@pytest.mark.parametrize("shape", [(64, 768, 2), (5, 1000, 3), (64, 300, 1)])
+def test_linear_skinny_head(shape, dt):
+    """Classifier heads (N not a multiple of 8, long K): fwd on the warp-per-output
+    dot kernel, dX / dW on the tile kernel; against the f64 oracle."""
+    m, fin, fout = shape
+    rng = np.random.default_rng(m + fin + fout)
+    x, xq = _q(rng.standard_normal((m, fin)), dt)
+    w, wq = _q(rng.standard_normal((fout, fin)) / np.sqrt(fin), dt)
+    b, bq = _q(rng.standard_normal(fout), dt)
+    g, gq = _q(rng.standard_normal((m, fout)), dt)
+    for t in (x, w, b):
+        t.requires_grad_(True)
+    s0 = launch_stats()["simt"]
+    y = MF.linear(x, w, b)
+    y.backward(g)
+    assert launch_stats()["simt"] - s0 >= 3
+    _close(y, oracle.linear_fwd(xq, wq, bq), dt, "y")
+    _close(x.grad, oracle.linear_dx(gq, wq), dt, "dx")
+    _close(w.grad, oracle.linear_dw(xq, gq), dt, "dw")
+    _close(b.grad, oracle.linear_db(gq), dt, "db")
+
+
 def test_linear_golden(linbn_golden):
     g = linbn_golden
     for case in ("lin_small", "lin_3d"):
