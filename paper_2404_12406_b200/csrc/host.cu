@@ -307,6 +307,11 @@ ms_status launch_umma(int bn, int a_mn, int b_mn, int mode, const TmapPack& tm,
     if (!a_mn && !b_mn) { MS_BN_SWITCH(0, 0, LOAD_GEMM) }
     if (!a_mn && b_mn) { MS_BN_SWITCH(0, 1, LOAD_GEMM) }
     if (a_mn && b_mn) { MS_BN_SWITCH(1, 1, LOAD_GEMM) }
+  } else if (mode == LOAD_GEMM_3XTF32) {
+    switch (bn) {
+      case 128: return launch_t<128, 0, 0, LOAD_GEMM_3XTF32>(tm, g, st);
+      default: break;
+    }
   } else if (mode == LOAD_CONV_FPROP) {
     MS_BN_SWITCH(0, 0, LOAD_CONV_FPROP)
   } else if (mode == LOAD_CONV_DGRAD) {

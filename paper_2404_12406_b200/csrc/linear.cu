@@ -15,6 +15,7 @@ bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 struct LinPlan {
   bool tc = false;
+  bool tf32 = false;  // float32 on the tensor cores (3xTF32, LOAD_GEMM_3XTF32)
   int cl = 1;   // 2: B tile multicast across a CTA pair on adjacent M tiles
   int bn = 0;
   int splits = 1;
@@ -126,8 +127,30 @@ __global__ void tail_finalize_kernel(const float* __restrict__ ws, T* __restrict
   }
 }
 
+// float32: hi / lo planes of both operands, K-major, pitch rounded to 16 bytes
+constexpr int TF32_BN = 128;
+constexpr int TF32_KB_PER_SLICE = 8;  // 8 k-blocks of 32 = 256 products per TMEM accumulation
+int64_t tf32_pitch(int64_t red) { return (red + 3) / 4 * 4; }
+size_t tf32_ws(int64_t rows, int64_t cols, int64_t red) {
+  const int64_t ld = tf32_pitch(red);
+  return 2 * align256(sizeof(float) * (size_t)rows * ld) + 2 * align256(sizeof(float) * (size_t)cols * ld);
+}
+
 LinPlan plan_linear(int64_t M, int64_t N, int64_t K, int dt, int pass) {
   LinPlan p;
+  if (dt == MS_F32 && M > 0 && N > 0 && K > 0) {
+    // output rows x cols, reduction red of this pass
+    const int64_t rows = pass == 2 ? N : M, cols = pass == 0 ? N : K,
+                  red = pass == 0 ? K : (pass == 1 ? N : M);
+    static const bool env_off = getenv("MS_FP32_LINEAR") && getenv("MS_FP32_LINEAR")[0] == 's';
+    // small products stay on the CUDA cores (the split pre-pass would dominate)
+    if (!env_off && rows >= 64 && cols >= 32 && (double)rows * cols * red >= (double)(1 << 24)) {
+      p.tf32 = true;
+      p.bn = TF32_BN;
+      p.ws = tf32_ws(rows, cols, red);
+    }
+    return p;
+  }
   if (!is16(dt) || K % 8 || N % 8 || M <= 0 || N <= 0 || K <= 0) return p;  // SIMT
   if (pass == 0) return plan_gemm(M, N, K, false, true);
   if (pass == 1) return plan_gemm(M, K, N, true, true);
@@ -211,6 +234,91 @@ ms_status run_gemm(const LinPlan& p, int dt, int a_mn, int b_mn, const CUtensorM
   return launch_umma(p.bn, a_mn, b_mn, LOAD_GEMM, tm, g, st, p.cl);
 }
 
+// hi / lo tf32 planes of a float32 operand: element (r, c) = src[r * sr + c * sc]
+// -> hi[r][c], lo[r][c] (pitch ld), hi = v with the low 13 mantissa bits cleared
+// (exact in tf32), lo = v - hi (exact in fp32).  32 x 32 tiles through shared
+// memory, so both a row-major and a transposed source are read coalesced.
+__global__ void __launch_bounds__(256) split_tf32_kernel(int64_t R, int64_t C, const float* __restrict__ src,
+                                                         int64_t sr, int64_t sc, float* __restrict__ hi,
+                                                         float* __restrict__ lo, int64_t ld) {
+  __shared__ float t[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+  const bool c_fast = sc == 1;  // source contiguous along c (else along r)
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int a = ty + 8 * i;  // slow index within the tile
+    const int64_t r = c_fast ? r0 + a : r0 + tx, c = c_fast ? c0 + tx : c0 + a;
+    const float v = (r < R && c < C) ? __ldg(src + r * sr + c * sc) : 0.f;
+    if (c_fast) t[a][tx] = v;
+    else t[tx][a] = v;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int a = ty + 8 * i;
+    const int64_t r = r0 + a, c = c0 + tx;
+    if (r < R && c < C) {
+      const float v = t[a][tx];
+      const float h = __uint_as_float(__float_as_uint(v) & 0xffffe000u);
+      hi[r * ld + c] = h;
+      lo[r * ld + c] = v - h;
+    }
+  }
+}
+
+// out[rows][cols] (pitch ldc, fp32) = A . B^T (+ bias), A(r, k) = a[r*ar + k*ak],
+// B(n, k) = b[n*br + k*bk], on the tcgen05 kind::tf32 kernel (3xTF32)
+ms_status run_tf32(int64_t rows, int64_t cols, int64_t red, const float* a, int64_t ar, int64_t ak,
+                   const float* b, int64_t br, int64_t bk, float* out, int64_t ldc,
+                   const float* bias, void* ws, size_t ws_bytes, cudaStream_t st) {
+  MS_CHECK_ARG(ws && ws_bytes >= tf32_ws(rows, cols, red), MS_ERR_WORKSPACE,
+               "linear fp32: workspace %zu < %zu", ws_bytes, tf32_ws(rows, cols, red));
+  const int64_t ld = tf32_pitch(red);
+  uint8_t* w8 = static_cast<uint8_t*>(ws);
+  float* a_hi = reinterpret_cast<float*>(w8);
+  float* a_lo = reinterpret_cast<float*>(w8 + align256(sizeof(float) * rows * ld));
+  float* b_hi = reinterpret_cast<float*>(w8 + 2 * align256(sizeof(float) * rows * ld));
+  float* b_lo = reinterpret_cast<float*>(w8 + 2 * align256(sizeof(float) * rows * ld) +
+                                         align256(sizeof(float) * cols * ld));
+  split_tf32_kernel<<<dim3((unsigned)((red + 31) / 32), (unsigned)((rows + 31) / 32)), 256, 0, st>>>(
+      rows, red, a, ar, ak, a_hi, a_lo, ld);
+  split_tf32_kernel<<<dim3((unsigned)((red + 31) / 32), (unsigned)((cols + 31) / 32)), 256, 0, st>>>(
+      cols, red, b, br, bk, b_hi, b_lo, ld);
+  count_launch(2);
+  MS_TRY(launch_status("split_tf32_kernel"));
+  TmapPack tm;
+  MS_TRY(make_tmap_2d(&tm.a[0], MS_F32, a_hi, red, rows, ld, 32, BM));
+  MS_TRY(make_tmap_2d(&tm.a[1], MS_F32, a_lo, red, rows, ld, 32, BM));
+  MS_TRY(make_tmap_2d(&tm.b, MS_F32, b_hi, red, cols, ld, 32, TF32_BN));
+  MS_TRY(make_tmap_2d(&tm.a[2], MS_F32, b_lo, red, cols, ld, 32, TF32_BN));
+  tm.a[3] = tm.a[0];
+  GemmArgs g{};
+  g.M = (int)rows;
+  g.N = (int)cols;
+  g.m_blocks = (int)((rows + BM - 1) / BM);
+  g.n_blocks = (int)((cols + TF32_BN - 1) / TF32_BN);
+  g.k_blocks = (int)((red + 31) / 32);
+  // The tensor core's fp32 accumulation of a long reduction drifts past the
+  // fp32 bar (norm-wise 3e-5 at K = 2048-4096, measured): every tile
+  // accumulates at most 256 products of the reduction in TMEM, and the slices
+  // are added into the zeroed fp32 output with red.add.
+  g.kb_per_split = TF32_KB_PER_SLICE;
+  g.splits = (g.k_blocks + g.kb_per_split - 1) / g.kb_per_split;
+  g.taps = 1;
+  g.num_tiles = g.m_blocks * g.n_blocks * g.splits;
+  g.ab_fmt = 2;  // tf32
+  g.nphases = 1;
+  g.n_fastest = g.n_blocks > 1 && cols * red <= 4 * 1024 * 1024 && rows > cols ? 1 : 0;
+  if (g.splits > 1) {
+    MS_CHECK_ARG(cudaMemset2DAsync(out, sizeof(float) * ldc, 0, sizeof(float) * cols, rows, st) ==
+                     cudaSuccess,
+                 MS_ERR_LAUNCH, "linear fp32: memset failed");
+  }
+  g.epi = EpiParams{out, ldc, MS_F32, g.splits > 1 ? 1 : 0, bias, MS_F32};
+  return launch_umma(TF32_BN, 0, 0, LOAD_GEMM_3XTF32, tm, g, st, 1);
+}
+
 }  // namespace
 }  // namespace ms
 
@@ -235,6 +343,9 @@ extern "C" ms_status ms_linear_fwd(int64_t M, int64_t N, int64_t K, int32_t dt, 
     MS_TRY(make_tmap_2d(&tb, dt, w, K, N, K, BK, p.bn / p.cl));  // each CTA loads BN/cl rows
     return run_gemm(p, dt, 0, 0, ta, tb, M, N, y, N, bias, ws, ws_bytes, st);
   }
+  if (p.tf32)  // y[m,n] = sum_k x[m,k] w[n,k]
+    return run_tf32(M, N, K, (const float*)x, K, 1, (const float*)w, K, 1, (float*)y, N,
+                    (const float*)bias, ws, ws_bytes, st);
   // y[m,n] = sum_k x[m,k] w[n,k]
   return simt_gemm(dt, (int)M, (int)N, (int)K, x, K, 1, w, 1, K, bias, y, N, st);
 }
@@ -253,6 +364,9 @@ extern "C" ms_status ms_linear_dx(int64_t M, int64_t N, int64_t K, int32_t dt, c
     MS_TRY(make_tmap_2d(&tb, dt, w, K, N, K, 64, BK));   // B = W [N][K], MN-major
     return run_gemm(p, dt, 0, 1, ta, tb, M, K, dx, K, nullptr, ws, ws_bytes, st);
   }
+  if (p.tf32)  // dx[m,k] = sum_n dy[m,n] w[n,k]: A = dY, B(k, n) = w[n*K + k]
+    return run_tf32(M, K, N, (const float*)dy, N, 1, (const float*)w, 1, K, (float*)dx, K,
+                    nullptr, ws, ws_bytes, st);
   // dx[m,k] = sum_n dy[m,n] w[n,k]
   return simt_gemm(dt, (int)M, (int)K, (int)N, dy, N, 1, w, K, 1, nullptr, dx, K, st);
 }
@@ -273,6 +387,9 @@ extern "C" ms_status ms_linear_dw(int64_t M, int64_t N, int64_t K, int32_t dt, c
     MS_TRY(make_tmap_2d(&tb, dt, x, K, M, K, 64, BK));   // B = X, MN-major
     return run_gemm(p, dt, 1, 1, ta, tb, N, K, dw, K, nullptr, ws, ws_bytes, st);
   }
+  if (p.tf32)  // dw[n,k] = sum_m dy[m,n] x[m,k]: A(n, m) = dy[m*N + n], B(k, m) = x[m*K + k]
+    return run_tf32(N, K, M, (const float*)dy, 1, N, (const float*)x, 1, K, (float*)dw, K,
+                    nullptr, ws, ws_bytes, st);
   // dw[n,k] = sum_m dy[m,n] x[m,k]
   return simt_gemm(dt, (int)N, (int)K, (int)M, dy, 1, N, x, K, 1, nullptr, dw, K, st);
 }

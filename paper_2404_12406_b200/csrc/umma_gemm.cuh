@@ -8,6 +8,9 @@
 //   LOAD_CONV_FPROP_C8    forward for 8-channel activations (8 taps per k-block)
 //   LOAD_CONV_FPROP_ROWSEG forward for <=4-channel stride-2 stems: one k-block per
 //                     kernel row, A = overlapping input-row segments (4-D TMA)
+//   LOAD_GEMM_3XTF32  float32 GEMM (Linear fwd / dX / dW at fp32) on kind::tf32:
+//                     A and B arrive as hi / lo planes (K-major), and each k-step
+//                     issues hi*hi + hi*lo + lo*hi (3xTF32, ~fp32 accuracy)
 //   LOAD_CONV_DGRAD_BAND  input-VJP for <8-channel inputs (the stem's dX): per band
 //                     of dX rows, GEMM dY-row x W[(tap,c)] then a col2im into
 //                     warp-private shared windows (no atomics), direct store
@@ -31,7 +34,8 @@ enum : int {
   LOAD_CONV_WGRAD = 3,
   LOAD_CONV_FPROP_C8 = 4,
   LOAD_CONV_FPROP_ROWSEG = 6,
-  LOAD_CONV_DGRAD_BAND = 7
+  LOAD_CONV_DGRAD_BAND = 7,
+  LOAD_GEMM_3XTF32 = 8
 };
 constexpr int BAND_WINDOWS = 8;  // one private col2im window per epilogue warp
 constexpr int BAND_WINDOW_BYTES = 112 * 1024;
@@ -192,7 +196,7 @@ __device__ __forceinline__ TileInfo decode_tile(const GemmArgs& g, int t, int cr
       }
     }
     int mb, rest;
-    if (MODE == LOAD_GEMM && g.n_fastest) {
+    if ((MODE == LOAD_GEMM || MODE == LOAD_GEMM_3XTF32) && g.n_fastest) {
       ti.nb = t % g.n_blocks;
       rest = t / g.n_blocks;
       mb = rest % g.m_blocks;
@@ -251,8 +255,9 @@ struct GemmCfg {
           : 1;
   static constexpr int A_SUB = BM * KBYTES;          // one k-block of A
   static constexpr int B_SUB = BN / CL * KBYTES;     // this CTA's share of one k-block of B
-  static constexpr int A_BYTES = KS * A_SUB;
-  static constexpr int B_BYTES = KS * B_SUB;
+  static constexpr int PARTS = MODE == LOAD_GEMM_3XTF32 ? 2 : 1;  // hi / lo planes
+  static constexpr int A_BYTES = KS * A_SUB * PARTS;
+  static constexpr int B_BYTES = KS * B_SUB * PARTS;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int EXTRA = MODE == LOAD_CONV_DGRAD_BAND ? BAND_WINDOW_BYTES : 0;
   // TMA-store staging: 4 epilogue warps x 4 buffers x (32 rows x 64 B)
@@ -293,6 +298,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
   constexpr int KMMA = Cfg::KBYTES / 32;  // tcgen05.mma (K=16) per stage
   static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN");
   static_assert(MODE != LOAD_CONV_DGRAD_BAND || BN == 160, "band dgrad is specialised to BN=160");
+  static_assert(MODE != LOAD_GEMM_3XTF32 || (CL == 1 && Cfg::KS == 1), "3xTF32: 1 CTA, 1 k-block");
   static_assert(CL == 1 || MODE == LOAD_GEMM || MODE == LOAD_CONV_FPROP ||
                     MODE == LOAD_CONV_DGRAD,
                 "CTA pairs are implemented for GEMM and im2col conv fprop / dgrad");
@@ -425,6 +431,13 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
                 } else {
                   tma_load_2d(sB, &tm.b, fb, k0, n0);
                 }
+              } else if constexpr (MODE == LOAD_GEMM_3XTF32) {
+                // 128-byte rows = 32 fp32; a[0] / a[1] = A hi / lo, b / a[2] = B hi / lo
+                const int k0 = kb * 32;
+                tma_load_2d(sA, &tm.a[0], fb, k0, ti.m0);
+                tma_load_2d(sA + Cfg::A_SUB, &tm.a[1], fb, k0, ti.m0);
+                tma_load_2d(sB, &tm.b, fb, k0, n0);
+                tma_load_2d(sB + Cfg::B_SUB, &tm.a[2], fb, k0, n0);
               } else if constexpr (MODE == LOAD_CONV_FPROP) {
                 const int tap = kb / g.cv.cblocks;
                 const int cb = kb - tap * g.cv.cblocks;
@@ -495,7 +508,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
             if (elect_one()) {
               if (crank == 0)
                 mbar_arrive_expect_tx(smem_u32(&full_bar[stage]),
-                                      CL * nkb * (Cfg::A_SUB + Cfg::B_SUB));
+                                      CL * nkb * (Cfg::A_SUB + Cfg::B_SUB) * Cfg::PARTS);
               for (int j = 0; j < nkb; ++j)
                 issue(kb0 + j, sA0 + j * Cfg::A_SUB, sA0 + Cfg::A_BYTES + j * Cfg::B_SUB);
             }
@@ -577,8 +590,18 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
               for (int kk = 0; kk < Cfg::KS * KMMA; ++kk) {
                 if (kk / KMMA < nkb) {
                   const uint32_t accum = (kb0 > ti.kb_begin || kk > 0) ? 1u : 0u;
-                  if constexpr (CL == 1) umma_f16(dcol, ads[kk], bds[kk], idesc, accum);
-                  else umma_f16_cg2(dcol, ads[kk], bds[kk], idesc, accum);
+                  if constexpr (MODE == LOAD_GEMM_3XTF32) {
+                    // hi*hi + hi*lo + lo*hi (descriptor start +A_SUB / +B_SUB = lo plane)
+                    const uint64_t a_lo = ads[kk] + (uint64_t)(Cfg::A_SUB >> 4);
+                    const uint64_t b_lo = bds[kk] + (uint64_t)(Cfg::B_SUB >> 4);
+                    umma_tf32(dcol, ads[kk], bds[kk], idesc, accum);
+                    umma_tf32(dcol, ads[kk], b_lo, idesc, 1u);
+                    umma_tf32(dcol, a_lo, bds[kk], idesc, 1u);
+                  } else if constexpr (CL == 1) {
+                    umma_f16(dcol, ads[kk], bds[kk], idesc, accum);
+                  } else {
+                    umma_f16_cg2(dcol, ads[kk], bds[kk], idesc, accum);
+                  }
                 }
               }
               // frees the smem slot (in both CTAs of a pair) when the MMAs retire

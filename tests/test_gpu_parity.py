@@ -211,6 +211,37 @@ def test_linear(case, dt):
     _close(b.grad, oracle.linear_db(gq), dt, "db")
 
 
+F32_TC_CASES = [
+    ((512,), 256, 256),        # one wave, K = 8 k-blocks
+    ((3, 300), 1000, 520),     # K not a multiple of 32 (TMA zero fill), N tail of a BN=128 tile
+    ((2, 640), 768, 3072),     # BERT-like FFN shape, long K
+    ((4096,), 1023, 130),      # N, K odd: 16-byte row pitch only in the split planes
+]
+
+
+@pytest.mark.parametrize("case", F32_TC_CASES)
+def test_linear_fp32_tensor_cores(case):
+    """float32 Linear on tcgen05 kind::tf32 (3xTF32: hi*hi + hi*lo + lo*hi over
+    hi / lo planes split once per operand): fwd, dX, dW each one tensor-core
+    launch, all within the fp32 bar (rtol 1e-5 vs the f64 oracle)."""
+    lead, fin, fout = case
+    rng = np.random.default_rng(fin * 7 + fout)
+    x, xq = _q(rng.standard_normal(lead + (fin,)), "f32")
+    w, wq = _q(rng.standard_normal((fout, fin)) / np.sqrt(fin), "f32")
+    b, bq = _q(rng.standard_normal(fout), "f32")
+    g, gq = _q(rng.standard_normal(lead + (fout,)), "f32")
+    for t in (x, w, b):
+        t.requires_grad_(True)
+    u0 = launch_stats()["umma"]
+    y = MF.linear(x, w, b)
+    y.backward(g)
+    assert launch_stats()["umma"] - u0 == 3
+    _close(y, oracle.linear_fwd(xq, wq, bq), "f32", "y")
+    _close(x.grad, oracle.linear_dx(gq, wq), "f32", "dx")
+    _close(w.grad, oracle.linear_dw(xq, gq), "f32", "dw")
+    _close(b.grad, oracle.linear_db(gq), "f32", "db")
+
+
 @pytest.mark.parametrize("dt", ["bf16", "f32"])
 @pytest.mark.parametrize("shape", [(64, 768, 2), (5, 1000, 3), (64, 300, 1)])
 def test_linear_skinny_head(shape, dt):
