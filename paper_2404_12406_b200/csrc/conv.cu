@@ -271,6 +271,15 @@ ms_status fwd_rowseg(const ms_conv_desc* d, const ConvPlan& p, const void* x, co
   const uint64_t ws2[1] = {(uint64_t)c.r * 32 * es};
   const uint32_t wb[2] = {32, (uint32_t)bn};
   MS_TRY(make_tmap_nd(&tm.b, dt, wr, 2, wd, ws2, wb, 64));
+  // epilogue TMA stores through [N*OH][OW][K]: a 32-pixel x 32-channel chunk per
+  // warp, the pixel tail of a row's last segment clipped by the map
+  if (dt != MS_F32 && (reinterpret_cast<uintptr_t>(y) & 15) == 0 && (c.k * es) % 16 == 0) {
+    const uint64_t yd[3] = {(uint64_t)c.k, (uint64_t)c.ow, (uint64_t)c.n * c.oh};
+    const uint64_t ys[2] = {(uint64_t)c.k * es, (uint64_t)c.ow * c.k * es};
+    const uint32_t yb[3] = {32, 32, 1};
+    MS_TRY(make_tmap_nd(&tm.c, dt, y, 3, yd, ys, yb, 64));
+    g.tma_store = 1;
+  }
   return launch_umma(bn, 0, 0, LOAD_CONV_FPROP_ROWSEG, tm, g, st);
 }
 

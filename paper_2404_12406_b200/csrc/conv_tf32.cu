@@ -658,13 +658,17 @@ __global__ void __launch_bounds__(DW2_THREADS, 1)
     }
 }
 
+// out[o] = sum over partial slots b of part[b][o], in a fixed order: warp per
+// output, lane l adds slots l, l + 32, ... in fp64, then a fixed shuffle tree
 __global__ void dw_partials_sum(const float* __restrict__ part, int blocks, int outs,
                                 float* __restrict__ dw) {
-  const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  const int o = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (o >= outs) return;
   double s = 0.0;
-  for (int b = 0; b < blocks; ++b) s += (double)part[(size_t)b * outs + o];
-  dw[o] = (float)s;
+  for (int b = lane; b < blocks; b += 32) s += (double)part[(size_t)b * outs + o];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if (lane == 0) dw[o] = (float)s;
 }
 
 }  // namespace
@@ -773,7 +777,7 @@ ms_status conv3x3_c8_dw(const ConvDims& d, const void* x, const void* g, void* d
                                                           (const float*)g, part);
   }
   const int outs = d.k * T3_C * 9;
-  dw_partials_sum<<<(outs + 127) / 128, 128, 0, st>>>(part, slots, outs, (float*)dw);
+  dw_partials_sum<<<(outs + 7) / 8, 256, 0, st>>>(part, slots, outs, (float*)dw);
   count_launch(2, KF_SIMT);
   return launch_status("conv3x3_c8_dw");
 }

@@ -262,7 +262,8 @@ struct GemmCfg {
   static constexpr int EXTRA = MODE == LOAD_CONV_DGRAD_BAND ? BAND_WINDOW_BYTES : 0;
   // TMA-store staging: 4 epilogue warps x 4 buffers x (32 rows x 64 B)
   static constexpr bool CAN_TMA_STORE = MODE == LOAD_GEMM || MODE == LOAD_CONV_FPROP ||
-                                        MODE == LOAD_CONV_FPROP_C8;
+                                        MODE == LOAD_CONV_FPROP_C8 ||
+                                        MODE == LOAD_CONV_FPROP_ROWSEG;
   // epilogue warps: 8 (two per TMEM lane quarter, each draining half of the
   // columns) so a second warp per SM sub-partition hides TMEM-load / store
   // latency; the band dgrad has its own 8-window layout
@@ -937,7 +938,11 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
               fence_proxy_async_smem();
               __syncwarp();
               if (lane == 0) {
-                tma_store_2d(&tm.c, smem_u32(stg), nc, ti.m0 + static_cast<int>(quarter) * 32);
+                if constexpr (MODE == LOAD_CONV_FPROP_ROWSEG)  // [row][pixel][ch]: clips q >= Q
+                  tma_store_3d(&tm.c, smem_u32(stg), nc, ti.tap * BM + static_cast<int>(quarter) * 32,
+                               ti.m0);
+                else
+                  tma_store_2d(&tm.c, smem_u32(stg), nc, ti.m0 + static_cast<int>(quarter) * 32);
                 bulk_commit();
               }
               ++stg_count;

@@ -21,7 +21,7 @@ for c in ${CONFIGS:-bert resnet18 resnet101 vgg16 fig1 llama r101bn r101bnf}; do
       > $OUT/r2_launches_$c.log 2>&1
   fi
   timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off \
-    --nvtx --nvtx-include "dominant/" -c 2 -f -o $OUT/r2_ncu_$c \
+    --nvtx --nvtx-include "dominant/" -c 4 -f -o $OUT/r2_ncu_$c \
     python tools/prof_step.py --config $cfg --steps 1 --mark ${OP[$c]} --mark-geom "${GEOM[$c]}" \
     > $OUT/r2_ncu_$c.log 2>&1
   # keep the summaries, not the (large) report
