@@ -61,15 +61,16 @@ constexpr int T3_RAWB = T3_C * T3_HROWS * T3_LW * 4;  // raw box [8 ch][5 rows][
 constexpr int T3_HALFB = T3_LW * 16;          // one 4-channel plane [136 px][4] (2176 B)
 constexpr int T3_PARTB = 2 * T3_HALFB;        // hi (or lo) of a row (4352 B)
 constexpr int T3_SPLB = 2 * T3_PARTB;         // hi + lo (8704 B)
-constexpr int T3_RAWS = 7;                    // raw ring of half-unit boxes (152 KB in flight
+constexpr int T3_RAWS = 6;                    // raw ring of half-unit boxes (152 KB in flight
                                               // per SM).  TMA cost is per box row: multi-row
                                               // boxes stream ~3x faster than [136][1][8] rows
-constexpr int T3_SLOTS = 6;                   // split ring (rows)
+constexpr int T3_SLOTS = 8;                   // split ring (rows, power of 2)
 constexpr int T3_N = 48;                      // MMA N: 3 kernel rows x 16-column groups
 constexpr int T3_BTILE = T3_N * T3_C * 4;     // one B tile (1536 B)
 constexpr int T3_REGION = 16 * (T3_R + 4);    // TMEM columns per strip region (192)
 constexpr int T3_ACCQ = 2;                    // acc-full barriers: one per strip region
-constexpr int T3_CONV_WARPS = 8;              // converter warps (one task each per row)
+constexpr int T3_CONV_WARPS = 8;              // converter warps: T3_GROUPS groups of 2
+constexpr int T3_GROUPS = T3_CONV_WARPS / 2;  // (power of 2)
 constexpr int T3_EPI_W0 = 2 + T3_CONV_WARPS;   // first epilogue warp
 constexpr int T3_THREADS = 32 * (T3_EPI_W0 + 4);
 constexpr int T3_OFF_SPL = T3_RAWS * T3_RAWB;
@@ -143,6 +144,9 @@ __device__ __forceinline__ void umma_tf32_ss(uint32_t tmem_d, uint64_t adesc, ui
 // mbarrier wait without a suspend-time hint: the hand-offs of this pipeline
 // (TMA -> converters -> MMA -> epilogue) are short and latency-bound, so waiters
 // poll instead of sleeping (bounded, like mbar_wait)
+__device__ __forceinline__ void mbar_arrive_cnt(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
 __device__ __forceinline__ void spin_wait(uint32_t bar, uint32_t parity) {
   uint32_t spins = 0;
   while (true) {
@@ -239,9 +243,9 @@ __global__ void __launch_bounds__(T3_THREADS, 1)
   if (tid == 0) {
     for (int i = 0; i < T3_RAWS; ++i) {
       mbar_init(smem_u32(&raw_full[i]), 1);
-      mbar_init(smem_u32(&raw_empty[i]), T3_CONV_WARPS);
+      mbar_init(smem_u32(&raw_empty[i]), 2 * T3_HROWS);  // 2 warps x rows per box
     }
-    for (int i = 0; i < T3_SLOTS; ++i) mbar_init(smem_u32(&spl_full[i]), T3_CONV_WARPS);
+    for (int i = 0; i < T3_SLOTS; ++i) mbar_init(smem_u32(&spl_full[i]), 2);  // the row's 2 warps
     for (int i = 0; i < T3_PAIRS; ++i) mbar_init(smem_u32(&spl_empty[i]), 1);
     for (int i = 0; i < T3_ACCQ; ++i) mbar_init(smem_u32(&acc_full[i]), 1);
     mbar_init(smem_u32(&region_free[0]), 4);
@@ -317,76 +321,77 @@ __global__ void __launch_bounds__(T3_THREADS, 1)
     }
   } else if (warp < T3_EPI_W0) {
     // ============================ converters ============================
-    // the MMA reads staged pixels 3 .. 132 (A rows p + s + 3): 130 pixels x 2
-    // channel halves = 260 tasks over 256 threads
-    constexpr int NT = 32 * T3_CONV_WARPS, NPX = T3_M + 2, TASKS = 2 * NPX;
-    const int ct = tid - 64;
-    int e = 0, hs = 0, rs = 0, jj = 0;  // row counter, box counter / slot, row in box
-    uint32_t rpar = 0;                  // raw_full parity of slot rs
-    int slot = 0, pair = 0;
-    uint32_t spar = 1;                  // spl_empty parity (first pass: free)
-    for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
+    if (a.dbg & 64) {  // profiling: one thread consumes the boxes (TMA stream only)
+      if (warp == 2 && lane == 0) {
+        int hs = 0;
+        for (int u = blockIdx.x; u < a.units; u += gridDim.x)
+          for (int half = 0; half < 2; ++half, ++hs) {
+            spin_wait(smem_u32(&raw_full[hs % T3_RAWS]), (hs / T3_RAWS) & 1);
+            mbar_arrive_cnt(smem_u32(&raw_empty[hs % T3_RAWS]), 2 * T3_HROWS);
+          }
+      }
+      goto done;
+    }
+    // Rows are converted by T3_GROUPS groups of 2 warps, group g taking rows e
+    // with e % T3_GROUPS == g: a single group walking every row made the row
+    // loop's serial latency (~250-450 cycles per row, one warp's dependent
+    // chain) the kernel's critical path (MS_TF32_DBG=256 cycle counters).
+    // The MMA reads staged pixels 3 .. 132 (A rows p + s + 3): 130 pixels x 2
+    // channel halves = 260 tasks over the group's 64 threads.
+    constexpr int GT = 64, NPX = T3_M + 2, TASKS = 2 * NPX;
+    const int grp = (warp - 2) >> 1;
+    const int gt = tid - 64 - grp * GT;
+    int e0 = 0, lu = 0;  // first row of the unit, unit counter
+    for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++lu) {
       int n, h0, rows, w0;
       unit_coords(a, u, n, h0, rows, w0);
-      for (int j = 0; j < rows + 2; ++j, ++e) {
-        if (jj == 0) spin_wait(smem_u32(&raw_full[rs]), rpar);
-        if (!(e & 1) && !(a.dbg & 8)) spin_wait(smem_u32(&spl_empty[pair]), spar);
+      const int nrow = rows + 2;
+      for (int j = (grp - e0) & (T3_GROUPS - 1); j < nrow; j += T3_GROUPS) {
+        const int e = e0 + j;
+        const int half = j >= T3_HROWS ? 1 : 0, jj = j - half * T3_HROWS;
+        const int hs = 2 * lu + half, rs = hs % T3_RAWS;
+        const int slot = e & (T3_SLOTS - 1), pair = (e >> 1) & (T3_PAIRS - 1);
+        spin_wait(smem_u32(&raw_full[rs]), (hs / T3_RAWS) & 1);
+        if (!(a.dbg & 8)) spin_wait(smem_u32(&spl_empty[pair]), ((e / T3_SLOTS) & 1) ^ 1);
         const float* rr = reinterpret_cast<const float*>(raw + rs * T3_RAWB) + jj * T3_LW;
         uint8_t* ss = spl + slot * T3_SPLB;
         if (!(a.dbg & 1)) {
-#pragma unroll 1
-          for (int t = ct; t < TASKS; t += NT) {
-            const int half = t >= NPX ? 1 : 0;
-            const int px = 3 + t - half * NPX;
-            float hv[4], lv[4];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              const float v = rr[(half * 4 + c) * T3_HROWS * T3_LW + px];
-              hv[c] = tf32_hi(v);
-              lv[c] = v - hv[c];
+          for (int q = 0; q < (TASKS + GT - 1) / GT; ++q) {
+            const int t = gt + q * GT;
+            if (t < TASKS) {
+              const int hf = t >= NPX ? 1 : 0;
+              const int px = 3 + t - hf * NPX;
+              float hv[4], lv[4];
+#pragma unroll
+              for (int c = 0; c < 4; ++c) {
+                const float v = rr[(hf * 4 + c) * T3_HROWS * T3_LW + px];
+                hv[c] = tf32_hi(v);
+                lv[c] = v - hv[c];
+              }
+              *reinterpret_cast<float4*>(ss + hf * T3_HALFB + px * 16) =
+                  make_float4(hv[0], hv[1], hv[2], hv[3]);
+              *reinterpret_cast<float4*>(ss + T3_PARTB + hf * T3_HALFB + px * 16) =
+                  make_float4(lv[0], lv[1], lv[2], lv[3]);
             }
-            *reinterpret_cast<float4*>(ss + half * T3_HALFB + px * 16) =
-                make_float4(hv[0], hv[1], hv[2], hv[3]);
-            *reinterpret_cast<float4*>(ss + T3_PARTB + half * T3_HALFB + px * 16) =
-                make_float4(lv[0], lv[1], lv[2], lv[3]);
           }
         }
         if (!(a.dbg & 32)) fence_proxy_async_smem();  // generic-proxy writes -> tensor-core reads
         __syncwarp();
-        const bool box_done = jj == T3_HROWS - 1 || j == rows + 1;
         if (lane == 0) {
-          mbar_arrive(smem_u32(&spl_full[slot]));
-          if (box_done) mbar_arrive(smem_u32(&raw_empty[rs]));
-        }
-        // advance the ring positions
-        if (++slot == T3_SLOTS) slot = 0;
-        if (e & 1) {
-          if (++pair == T3_PAIRS) {
-            pair = 0;
-            spar ^= 1;
+          if (!(a.dbg & 128)) mbar_arrive(smem_u32(&spl_full[slot]));
+          // raw_empty counts 2 warps x T3_HROWS rows per box; the box's last row
+          // also arrives for the rows a short strip does not have
+          const bool last = jj == T3_HROWS - 1 || j == nrow - 1;
+          mbar_arrive_cnt(smem_u32(&raw_empty[rs]), last ? T3_HROWS - jj : 1);
+          if (j == nrow - 1 && nrow <= T3_HROWS) {  // the unread second box of a short strip
+            const int hs2 = 2 * lu + 1, rs2 = hs2 % T3_RAWS;
+            spin_wait(smem_u32(&raw_full[rs2]), (hs2 / T3_RAWS) & 1);
+            mbar_arrive_cnt(smem_u32(&raw_empty[rs2]), T3_HROWS);
           }
         }
-        if (box_done) {
-          jj = 0;
-          ++hs;
-          if (++rs == T3_RAWS) {
-            rs = 0;
-            rpar ^= 1;
-          }
-        } else {
-          ++jj;
-        }
       }
-      if (rows + 2 <= T3_HROWS) {  // short strip: the second box was loaded but not read
-        spin_wait(smem_u32(&raw_full[rs]), rpar);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&raw_empty[rs]));
-        ++hs;
-        if (++rs == T3_RAWS) {
-          rs = 0;
-          rpar ^= 1;
-        }
-      }
+      e0 += nrow;
     }
   } else {
     // ============================ epilogue ============================
@@ -741,7 +746,6 @@ ms_status conv3x3_tf32(int pass, const ConvDims& d, const void* a, const void* b
   int grid = num_sms();
   if (grid > args.units) grid = args.units;
   conv3x3_tf32_kernel<<<grid, T3_THREADS, T3_SMEM, st>>>(tx, args);
-  count_launch(1, KF_UMMA);
   return launch_status("conv3x3_tf32_kernel");
 }
 

@@ -17,7 +17,7 @@ __device__ __forceinline__ void wait(uint32_t bar, uint32_t par) {
 }
 
 __global__ void k(const __grid_constant__ CUtensorMap tx, int bw, int bh, int slots, int bytes,
-                  int units, int segs, int hb, int N) {
+                  int units, int segs, int hb, int N, int spinners, int kmode) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + slots * bytes);
   uint64_t* empty = full + slots;
@@ -35,6 +35,17 @@ __global__ void k(const __grid_constant__ CUtensorMap tx, int bw, int bh, int sl
       const int s = e % slots;
       wait(su32(&empty[s]), ((e / slots) & 1) ^ 1);
       const int seg = u % segs, hh = (u / segs) % hb, n = u / segs / hb;
+      if (kmode) {  // the Fig.1 kernel's pattern: box u = half (u & 1) of unit u / 2
+        const int uu = u >> 1, half = u & 1;
+        const int sg = uu % 2, ch = (uu / 2) % 32, nn = uu / 64;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&full[s])), "r"(bytes));
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(su32(smem + s * bytes)),
+            "l"(reinterpret_cast<uint64_t>(&tx)), "r"(su32(&full[s])), "r"(sg * 128 - 4), "r"(ch * 8 - 1 + 5 * half), "r"(nn * 8)
+            : "memory");
+        continue;
+      }
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&full[s])), "r"(bytes));
       asm volatile(
           "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
@@ -42,6 +53,10 @@ __global__ void k(const __grid_constant__ CUtensorMap tx, int bw, int bh, int sl
           "l"(reinterpret_cast<uint64_t>(&tx)), "r"(su32(&full[s])), "r"(seg * 128 - 4), "r"(hh * (bh > 2 ? bh - 2 : bh) - 1), "r"(n * 8)
           : "memory");
     }
+  } else if (threadIdx.x >= 64 && (threadIdx.x >> 5) < 2 + spinners) {
+    // extra warps poll the same full barriers (all lanes), like converter warps
+    int e = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++e) wait(su32(&full[e % slots]), (e / slots) & 1);
   } else if (threadIdx.x == 32) {
     int e = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++e) {
@@ -71,15 +86,18 @@ int main(int argc, char** argv) {
   const int bytes = bw * bh * 8 * 4;
   const int step = bh > 2 ? bh - 2 : bh;  // overlapping row windows (bh-2 new rows)
   const int segs = 2, hb = (H + step - 1) / step;
-  const int units = N * segs * hb;
-  const int smem = slots * bytes + 2 * slots * 8;
+  const int kmode = argc > 7 ? atoi(argv[7]) : 0;
+  const int units = kmode ? N * 2 * 32 * 2 : N * segs * hb;
+  const int smem = argc > 6 ? atoi(argv[6]) * 1024 : slots * bytes + 2 * slots * 8;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  k<<<148, 64, smem>>>(m, bw, bh, slots, bytes, units, segs, hb, N);
+  const int spin = argc > 5 ? atoi(argv[5]) : 0;
+  const int thr = 64 + 32 * spin;
+  k<<<148, thr, smem>>>(m, bw, bh, slots, bytes, units, segs, hb, N, spin, kmode);
   cudaEventRecord(a);
-  for (int i = 0; i < 10; ++i) k<<<148, 64, smem>>>(m, bw, bh, slots, bytes, units, segs, hb, N);
+  for (int i = 0; i < 10; ++i) k<<<148, thr, smem>>>(m, bw, bh, slots, bytes, units, segs, hb, N, spin, kmode);
   cudaEventRecord(b);
   cudaError_t err = cudaDeviceSynchronize();
   float ms;
@@ -87,7 +105,7 @@ int main(int argc, char** argv) {
   ms /= 10;
   const double tot = (double)units * bytes;
   const double uniq = (double)N * C * H * W * 4;
-  printf("box %dx%dx8 (%d B) slots %d: enc=%d %s  %.1f us  box %.0f GB/s, unique %.0f GB/s\n", bw, bh, bytes, slots,
+  printf("spin %d box %dx%dx8 (%d B) slots %d: enc=%d %s  %.1f us  box %.0f GB/s, unique %.0f GB/s\n", spin, bw, bh, bytes, slots,
          (int)r, cudaGetErrorString(err), ms * 1e3, tot / ms / 1e6, uniq / ms / 1e6);
   return 0;
 }
