@@ -394,7 +394,7 @@ def _ncu_traffic(config, dom):
         with open(p) as f:
             d = json.load(f)
         e = d[config]
-        if e["op"] == dom["op"] and e["geom"] == dom["geom"]:
+        if e["op"].split(".")[-1] == dom["op"].split(".")[-1] and e["geom"] == dom["geom"]:
             return int(e["dram_bytes"]), f"profiles/r2_ncu_traffic.json:{config} ({e['kernel']})"
     except Exception:
         pass

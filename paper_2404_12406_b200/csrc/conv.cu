@@ -134,6 +134,7 @@ ConvPlan plan(const ms_conv_desc* d, int pass, bool dx_bias = false) {
       // the last window reads 64 bytes = 64 / (2 cpx) pixels from its start
       p.xw_pad = (int)std::max<int64_t>(d->w + 2 * d->pad_w,
                                         (int64_t)(c.ow - 1) * d->stride_w + 32 / p.cpx);
+      if (p.cpx == 8 && d->stride_w == 1) p.xw_pad = (p.xw_pad + 7) / 8 * 8;  // 128-B row chunks
       p.ws_pad = align256(es * (size_t)d->n * d->h * p.xw_pad * p.cpx);
       p.ws_w = align256(es * (size_t)d->k * d->r * 32);
       p.ws = p.ws_pad + p.ws_w;
@@ -265,7 +266,16 @@ ms_status fwd_rowseg(const ms_conv_desc* d, const ConvPlan& p, const void* x, co
   const uint64_t str[3] = {(uint64_t)c.sw * p.cpx * es, (uint64_t)p.xw_pad * p.cpx * es,
                            (uint64_t)c.h * p.xw_pad * p.cpx * es};
   const uint32_t box[4] = {32, BM, 1, 1};
-  MS_TRY(make_tmap_nd(&tm.a[0], dt, x4, 4, dims, str, box, 64));
+  if (p.cpx == 8 && c.sw == 1 && p.xw_pad % 8 == 0) {
+    // contiguous row segments: [64 elements = 8 px][xw_pad / 8][H][N], 17 chunks per box
+    const uint64_t d8[4] = {64, (uint64_t)p.xw_pad / 8, (uint64_t)c.h, (uint64_t)c.n};
+    const uint64_t s8[3] = {128, (uint64_t)p.xw_pad * 8 * es, (uint64_t)c.h * p.xw_pad * 8 * es};
+    const uint32_t b8[4] = {64, ROWSEG8_A_TX / 128, 1, 1};
+    MS_TRY(make_tmap_nd(&tm.a[0], dt, x4, 4, d8, s8, b8, 0));
+    g.rowseg8 = 1;
+  } else {
+    MS_TRY(make_tmap_nd(&tm.a[0], dt, x4, 4, dims, str, box, 64));
+  }
   tm.a[1] = tm.a[2] = tm.a[3] = tm.a[0];
   const uint64_t wd[2] = {(uint64_t)c.r * 32, (uint64_t)c.k};
   const uint64_t ws2[1] = {(uint64_t)c.r * 32 * es};

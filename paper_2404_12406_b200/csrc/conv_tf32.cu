@@ -746,6 +746,7 @@ ms_status conv3x3_tf32(int pass, const ConvDims& d, const void* a, const void* b
   int grid = num_sms();
   if (grid > args.units) grid = args.units;
   conv3x3_tf32_kernel<<<grid, T3_THREADS, T3_SMEM, st>>>(tx, args);
+  count_launch(1, KF_UMMA);
   return launch_status("conv3x3_tf32_kernel");
 }
 

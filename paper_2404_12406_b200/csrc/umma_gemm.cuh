@@ -50,6 +50,7 @@ constexpr int BAND_WIN = BAND_H * BAND_ROWF;         // floats per window (3360)
 template <int V> struct IntC { static constexpr int value = V; };
 
 constexpr int BM = 128;        // UMMA M (cta_group::1)
+constexpr int ROWSEG8_A_TX = (BM + 8) * 16;  // rowseg8: one staged segment (136 px x 16 B)
 constexpr int BK = 64;         // K elements per stage (128 bytes of bf16)
 constexpr int UMMA_K = 16;     // K per tcgen05.mma for 16-bit inputs
 constexpr int EPI_WARPS = 4;
@@ -123,6 +124,11 @@ struct GemmArgs {
   // profiling switch (MS_GEMM_DBG, GEMM mode only): bit 0 drops the epilogue's
   // stores, bit 1 also its TMEM loads -- isolates the main loop's feed rate
   int dbg;
+  // LOAD_CONV_FPROP_ROWSEG with 8-channel stride-1 rows: stage each input row
+  // segment once ([136 px][8 ch], 16 B per pixel, no swizzle) and read tap pairs
+  // at 16-byte-shifted descriptor starts (LBO = 16 B: the next K core matrix is
+  // the next pixel) instead of 128 overlapping 64-byte windows per k-block
+  int rowseg8;
   ConvShape cv;
   int nphases;
   PhaseInfo phase[4];
@@ -468,7 +474,9 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
                 tma_load_2d(sB, &tm.b, fb, kb * BK, n0);
               } else if constexpr (MODE == LOAD_CONV_FPROP_ROWSEG) {
                 // k-block = kernel row r: 128 overlapping segments of one input row
-                tma_load_4d(sA, amap, fb, 0, ti.tap * BM, ch + kb, cn);
+                // (rowseg8: the contiguous segment, 17 x 128-byte chunks)
+                if (g.rowseg8) tma_load_4d(sA, amap, fb, 0, ti.tap * (BM / 8), ch + kb, cn);
+                else tma_load_4d(sA, amap, fb, 0, ti.tap * BM, ch + kb, cn);
                 tma_load_2d(sB, &tm.b, fb, kb * 32, n0);
               } else if constexpr (MODE == LOAD_CONV_DGRAD_BAND) {
                 // one full dY row (Q pixels, 64 channels); rows outside [0, P) load zeros
@@ -508,8 +516,12 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
             };
             if (elect_one()) {
               if (crank == 0)
-                mbar_arrive_expect_tx(smem_u32(&full_bar[stage]),
-                                      CL * nkb * (Cfg::A_SUB + Cfg::B_SUB) * Cfg::PARTS);
+                mbar_arrive_expect_tx(
+                    smem_u32(&full_bar[stage]),
+                    CL * nkb *
+                        ((MODE == LOAD_CONV_FPROP_ROWSEG && g.rowseg8 ? ROWSEG8_A_TX : Cfg::A_SUB) +
+                         Cfg::B_SUB) *
+                        Cfg::PARTS);
               for (int j = 0; j < nkb; ++j)
                 issue(kb0 + j, sA0 + j * Cfg::A_SUB, sA0 + Cfg::A_BYTES + j * Cfg::B_SUB);
             }
@@ -572,7 +584,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
               if constexpr (MODE == LOAD_CONV_FPROP_C8)  // core matrices 8 rows x 16 B
                 ad = make_smem_desc(sA + k * 4096, 2048, 128, LAYOUT_SWIZZLE_NONE);
               else if constexpr (MODE == LOAD_CONV_FPROP_ROWSEG)  // 64-byte rows
-                ad = make_smem_desc(sA + k * 32, 16, 512, LAYOUT_SWIZZLE_64B);
+                ad = g.rowseg8 ? make_smem_desc(sA + k * 32, 16, 128, LAYOUT_SWIZZLE_NONE)
+                               : make_smem_desc(sA + k * 32, 16, 512, LAYOUT_SWIZZLE_64B);
               else if constexpr (A_MN)
                 ad = make_smem_desc(sA + k * 2048, 8192, 1024, LAYOUT_SWIZZLE_128B);
               else

@@ -8,14 +8,15 @@ declare -A OP GEOM
 OP[bert]=linear_fwd;      GEOM[bert]='{"M": 32768, "N": 768, "K": 768}'
 OP[resnet18]=conv2d_bn_fwd; GEOM[resnet18]='{"x": [256, 64, 56, 56], "w": [64, 64, 3, 3], "stride": [1, 1], "pad": [1, 1]}'
 OP[resnet101]=conv2d_bn_dx; GEOM[resnet101]='{"x": [128, 1024, 14, 14], "w": [256, 1024, 1, 1], "stride": [1, 1], "pad": [0, 0]}'
-OP[vgg16]=conv2d_bn_fwd;  GEOM[vgg16]='{"x": [128, 3, 224, 224], "w": [64, 3, 3, 3], "stride": [1, 1], "pad": [1, 1]}'
+OP[vgg16]=conv2d_dw;  GEOM[vgg16]='{"x": [128, 512, 28, 28], "w": [512, 512, 3, 3], "stride": [1, 1], "pad": [1, 1]}'
+OP[vgg16c11]=conv2d_bn_fwd;  GEOM[vgg16c11]='{"x": [128, 3, 224, 224], "w": [64, 3, 3, 3], "stride": [1, 1], "pad": [1, 1]}'
 OP[fig1]=conv2d_fwd;      GEOM[fig1]='{"x": [32, 8, 256, 256], "w": [8, 8, 3, 3], "stride": [1, 1], "pad": [1, 1]}'
 OP[llama]=linear_fwd;     GEOM[llama]='{"M": 4096, "N": 14336, "K": 4096}'
 OP[r101bn]=bn_add_relu_bwd; GEOM[r101bn]='{"shape": [128, 1024, 14, 14]}'
 OP[r101bnf]=bn_relu_fwd; GEOM[r101bnf]='{"shape": [128, 1024, 14, 14]}'
 for c in ${CONFIGS:-bert resnet18 resnet101 vgg16 fig1 llama r101bn r101bnf}; do
-  cfg=$c; [[ $c == r101bn* ]] && cfg=resnet101
-  if [[ $c != r101bn* ]]; then
+  cfg=$c; [[ $c == r101bn* ]] && cfg=resnet101; [[ $c == vgg16c11 ]] && cfg=vgg16
+  if [[ $c != r101bn* && $c != vgg16c11 ]]; then
     timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off \
       --csv --log-file $OUT/r2_launches_$c.csv python tools/prof_step.py --config $cfg --steps 2 \
       > $OUT/r2_launches_$c.log 2>&1
