@@ -275,6 +275,12 @@ struct GemmCfg {
   // latency; the band dgrad has its own 8-window layout
   static constexpr int EPI = MODE == LOAD_CONV_DGRAD_BAND ? BAND_WINDOWS : (BN >= 64 ? 8 : 4);
   static constexpr int EPI_H = MODE == LOAD_CONV_DGRAD_BAND ? 1 : EPI / 4;  // warps per quarter
+  // BN = 64: the two warps of a TMEM lane quarter take alternate TILES (all 64
+  // columns each) instead of half the columns of every tile, so two tiles' fused
+  // epilogues are in flight (a 64-column tile's epilogue is latency-bound: VGG
+  // conv1_1 wrote 1.9 TB/s with one tile at a time)
+  static constexpr bool TILE_ALT = BN == 64 && CL == 1 && MODE != LOAD_CONV_DGRAD_BAND && EPI == 8;
+  static constexpr int COL_SPLIT = TILE_ALT ? 1 : EPI_H;  // warps sharing one tile's columns
   static constexpr int STG_BUFS = 4 / EPI_H;
   static constexpr int STG = CAN_TMA_STORE ? EPI * STG_BUFS * 2048 : 0;
   static constexpr int SMEM_MAX = 227 * 1024;
@@ -341,7 +347,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
     for (int i = 0; i < NACC; ++i) {
       mbar_init(smem_u32(&tfull_bar[i]), 1);
       // CL = 2: one arrival per epilogue warp of both CTAs (on the even CTA's barrier)
-      mbar_init(smem_u32(&tempty_bar[i]), CL == 1 ? Cfg::EPI * 32 : CL * Cfg::EPI);
+      mbar_init(smem_u32(&tempty_bar[i]),
+                CL == 1 ? (Cfg::TILE_ALT ? 4 : Cfg::EPI) * 32 : CL * Cfg::EPI);
     }
     fence_mbar_init();
     tma_prefetch_desc(&tm.b);
@@ -646,6 +653,23 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
     int local = 0;
     uint32_t stg_count = 0;  // TMA-store staging buffer parity
     const EpiParams& e = g.epi;
+    // eval-BN fold of this warp's columns, hoisted out of the tile loop when the
+    // columns never change (one N-block): the four parameter loads and the rsqrt
+    // otherwise sit on every tile's epilogue critical path
+    constexpr int NCH = (BN / Cfg::COL_SPLIT + 31) / 32;
+    float hs[NCH], ht[NCH];
+    const bool bn_hoist = MODE != LOAD_CONV_DGRAD_BAND && e.bn.var != nullptr && g.n_blocks == 1;
+    if (bn_hoist) {
+      const int c_lo0 =
+          (Cfg::COL_SPLIT == 1 ? 0 : ((static_cast<int>(warp) - 2) >> 2)) * (BN / Cfg::COL_SPLIT);
+#pragma unroll
+      for (int ci = 0; ci < NCH; ++ci) {
+        hs[ci] = 1.f;
+        ht[ci] = 0.f;
+        const int col = c_lo0 + ci * 32 + static_cast<int>(lane);
+        if (col < g.N) bn_fold(e.bn, col, hs[ci], ht[ci]);
+      }
+    }
     for (int t = t_first; t < g.num_tiles; t += t_step) {
       TileInfo ti = decode_tile<MODE, CL>(g, t, crank);
       const int n0 = ti.nb * BN;
@@ -736,12 +760,14 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
         const int acc = local % NACC;
         const uint32_t use = static_cast<uint32_t>(local / NACC);
         ++local;
+        // TILE_ALT: warps 2-5 take the CTA's even tiles, warps 6-9 the odd ones
+        if (Cfg::TILE_ALT && (((local - 1) & 1) != ((static_cast<int>(warp) - 2) >> 2))) continue;
         const bool tail = ti.unit >= 0;  // fp32 partial of a K-sliced last-wave tile
         const bool tma_st = Cfg::CAN_TMA_STORE && g.tma_store && !tail;
         const int ncols = g.N;
-        // this warp drains columns [c_lo, c_lo + BN / EPI_H) of the accumulator
-        constexpr int WCOLS = BN / Cfg::EPI_H;
-        const int c_lo = (Cfg::EPI_H == 1 ? 0 : ((static_cast<int>(warp) - 2) >> 2)) * WCOLS;
+        // this warp drains columns [c_lo, c_lo + BN / COL_SPLIT) of the accumulator
+        constexpr int WCOLS = BN / Cfg::COL_SPLIT;
+        const int c_lo = (Cfg::COL_SPLIT == 1 ? 0 : ((static_cast<int>(warp) - 2) >> 2)) * WCOLS;
         // 16-bit bias of this warp's columns, fetched before the accumulator wait
         // so its latency overlaps the main loop: lane j holds columns 8j .. 8j + 7
         // (a K-sliced tile adds the bias in its first slice only)
@@ -789,8 +815,16 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
           uint32_t r[32];
           // eval-BN affine: lane j folds column n0 + c + j (loads overlap the TMEM read)
           float bs = 1.f, bt = 0.f;
-          if (e.bn.var != nullptr && n0 + c + static_cast<int>(lane) < ncols)
+          if (bn_hoist) {
+#pragma unroll
+            for (int q = 0; q < NCH; ++q)
+              if (q == ci) {
+                bs = hs[q];
+                bt = ht[q];
+              }
+          } else if (e.bn.var != nullptr && n0 + c + static_cast<int>(lane) < ncols) {
             bn_fold(e.bn, n0 + c + static_cast<int>(lane), bs, bt);
+          }
           // residual chunk prefetched ahead of the TMEM read (its latency overlaps it)
           uint4 rpre[4];
           bool rpre_ok = false;

@@ -17,6 +17,8 @@ SHAPES = {
     "layer4": (256, 512, 7, 7, 512, 3, 1, 1),
     "down2": (256, 64, 56, 56, 128, 1, 2, 0),
     "l2s2": (256, 64, 56, 56, 128, 3, 2, 1),
+    "vggc11": (128, 3, 224, 224, 64, 3, 1, 1),
+    "vggc12": (128, 64, 224, 224, 64, 3, 1, 1),
 }
 
 dev = torch.device("cuda", 0)
