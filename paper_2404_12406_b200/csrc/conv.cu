@@ -197,6 +197,13 @@ ConvPlan plan(const ms_conv_desc* d, int pass, bool dx_bias = false) {
   return p;
 }
 
+// 1x1, stride 1, no padding: output pixel m reads input pixel m only
+bool is_pointwise(const ConvDims& c) {
+  static const bool off = getenv("MS_CONV1X1_IM2COL") != nullptr;  // A/B switch
+  return !off && c.r == 1 && c.s == 1 && c.sh == 1 && c.sw == 1 && c.ph == 0 && c.pw == 0 &&
+         c.oh == c.h && c.ow == c.w;
+}
+
 GemmArgs base_args(int dt) {
   GemmArgs g{};
   g.ab_fmt = dt == MS_BF16 ? 1 : 0;
@@ -319,6 +326,24 @@ ms_status fwd_tc(const ms_conv_desc* d, const ConvPlan& p, const void* x, const 
   g.N = c.k;
   const int m_tiles = (int)((M + BM - 1) / BM);
   const TilePick tp = pick_tiles(m_tiles, c.k, !p.c8, false);
+  if (is_pointwise(c) && !p.c8 && d->layout == MS_NHWC) {
+    // 1x1 / stride 1 / pad 0 over NHWC pixels is a plain GEMM: tiled TMA rows of
+    // x instead of im2col boxes, and the GEMM epilogue (TMA stores + fusion)
+    const int bn = tp.bn;
+    g.m_blocks = (m_tiles + tp.cl - 1) / tp.cl;
+    g.n_blocks = (c.k + bn - 1) / bn;
+    g.k_blocks = p.cpad / BK;
+    g.kb_per_split = g.k_blocks;
+    g.num_tiles = g.m_blocks * g.n_blocks;
+    g.epi = EpiParams{y, c.k, dt, 0, bias, dt};
+    apply_fuse(g.epi, f);
+    TmapPack tm;
+    MS_TRY(make_tmap_2d(&tm.a[0], dt, xsrc, p.cpad8, M, p.cpad8, BK, BM));
+    tm.a[1] = tm.a[2] = tm.a[3] = tm.a[0];
+    MS_TRY(make_tmap_2d(&tm.b, dt, wsrc, p.cpad, c.k, p.cpad, BK, bn / tp.cl));
+    MS_TRY(setup_tma_store(tm, g, dt, y, M, c.k, c.k));
+    return launch_umma(bn, 0, 0, LOAD_GEMM, tm, g, st, tp.cl);
+  }
   const int bn = tp.bn;
   g.m_blocks = (m_tiles + tp.cl - 1) / tp.cl;  // pairs of M tiles when clustered
   g.n_blocks = (c.k + bn - 1) / bn;
@@ -416,6 +441,28 @@ ms_status dx_tc(const ms_conv_desc* d, const ConvPlan& p, const void* dy, const 
   const TilePick tp = pick_tiles((int64_t)c.n * c.h * c.w / BM + 1, c.c, true, false);
   const int bn = tp.bn;
   g.n_blocks = (c.c + bn - 1) / bn;
+  if (is_pointwise(c) && d->layout == MS_NHWC) {
+    // 1x1 / stride 1: dX[px][c] = dY[px][k] . W'[c][k] (the repacked, BN-scaled
+    // weight) as a plain GEMM with the fused dgrad epilogue
+    const int64_t M = (int64_t)c.n * c.h * c.w;
+    const int m_tiles = (int)((M + BM - 1) / BM);
+    g.M = (int)M;
+    g.m_blocks = (m_tiles + tp.cl - 1) / tp.cl;
+    g.k_blocks = p.kpad / BK;
+    g.kb_per_split = g.k_blocks;
+    g.num_tiles = g.m_blocks * g.n_blocks;
+    g.epi = EpiParams{dx, c.c, dt, 0, bias, dt};
+    g.epi.resid = xf->addend;
+    g.epi.keep_in = xf->keep;
+    g.epi.bn = xf->in_bn;
+    g.epi.bn_post = xf->in_bn.var != nullptr;
+    TmapPack tm;
+    MS_TRY(make_tmap_2d(&tm.a[0], dt, dy, c.k, M, c.k, BK, BM));
+    tm.a[1] = tm.a[2] = tm.a[3] = tm.a[0];
+    MS_TRY(make_tmap_2d(&tm.b, dt, wd, p.kpad, c.c, p.kpad, BK, bn / tp.cl));
+    MS_TRY(setup_tma_store(tm, g, dt, dx, M, c.c, c.c));
+    return launch_umma(bn, 0, 0, LOAD_GEMM, tm, g, st, tp.cl);
+  }
   g.cv = shape_of(c, c.k, c.oh, c.ow, p.kpad / 64, p.kpad, c.h, c.w);
   TmapPack tm;
   int np = 0, tiles = 0;

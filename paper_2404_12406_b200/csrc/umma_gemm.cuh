@@ -809,6 +809,32 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
         if constexpr (MODE == LOAD_CONV_WGRAD) col_base += static_cast<int64_t>(ti.tap) * g.N;
 
         const uint32_t taddr = tmem_base + ((quarter * 32u) << 16) + acc * BN;
+        // residual / addend chunk and producer-ReLU keep bits of chunk cc, loaded
+        // one chunk ahead: their global-load latency overlaps the previous
+        // chunk's work instead of serialising every chunk (fused dgrad epilogues
+        // read an addend and a mask per 32 columns)
+        uint4 rnx[4];
+        bool rnx_ok = false, knx_ok = false;
+        uint32_t knx = 0;
+        auto prefetch = [&](int cc) {
+          const int cpf = c_lo + cc * 32;
+          rnx_ok = knx_ok = false;
+          if (!valid || tail || n0 + cpf + 32 > ncols) return;
+          const int64_t el = orow * e.ldc + col_base + cpf;
+          if (e.resid != nullptr) {
+            const uint16_t* r16 = static_cast<const uint16_t*>(e.resid) + el;
+            if ((reinterpret_cast<uintptr_t>(r16) & 15) == 0) {
+              rnx_ok = true;
+#pragma unroll
+              for (int q = 0; q < 4; ++q) rnx[q] = __ldg(reinterpret_cast<const uint4*>(r16) + q);
+            }
+          }
+          if (e.keep_in != nullptr && (el & 31) == 0) {
+            knx_ok = true;
+            knx = __ldg(reinterpret_cast<const uint32_t*>(e.keep_in) + (el >> 5));
+          }
+        };
+        prefetch(0);
 #pragma unroll 1
         for (int ci = 0; ci < WCOLS / 32; ++ci) {
           const int c = c_lo + ci * 32;
@@ -825,18 +851,13 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
           } else if (e.bn.var != nullptr && n0 + c + static_cast<int>(lane) < ncols) {
             bn_fold(e.bn, n0 + c + static_cast<int>(lane), bs, bt);
           }
-          // residual chunk prefetched ahead of the TMEM read (its latency overlaps it)
+          // this chunk's prefetched residual / keep bits; start the next chunk's
           uint4 rpre[4];
-          bool rpre_ok = false;
-          if (e.resid != nullptr && valid && !tail && n0 + c + 32 <= ncols) {
-            const uint16_t* r16 =
-                static_cast<const uint16_t*>(e.resid) + orow * e.ldc + col_base + c;
-            if ((reinterpret_cast<uintptr_t>(r16) & 15) == 0) {
-              rpre_ok = true;
 #pragma unroll
-              for (int q = 0; q < 4; ++q) rpre[q] = __ldg(reinterpret_cast<const uint4*>(r16) + q);
-            }
-          }
+          for (int q = 0; q < 4; ++q) rpre[q] = rnx[q];
+          const bool rpre_ok = rnx_ok, kpre_ok = knx_ok;
+          const uint32_t kpre = knx;
+          if (ci + 1 < WCOLS / 32) prefetch(ci + 1);
           __syncwarp();  // tcgen05.ld / wait are warp-collective: reconverge invalid rows
           if (MODE == LOAD_GEMM && (g.dbg & 2)) continue;
           if (!zero) {
@@ -923,8 +944,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
             }
           }
           if (e.keep_in != nullptr) {  // the producer ReLU's backward
-            uint32_t kb = 0;
-            if (valid) {
+            uint32_t kb = kpre_ok ? kpre : 0u;
+            if (valid && !kpre_ok) {
               const int64_t el = orow * e.ldc + col_base + c;
               if (full && (el & 31) == 0) {
                 kb = __ldg(reinterpret_cast<const uint32_t*>(e.keep_in) + (el >> 5));
