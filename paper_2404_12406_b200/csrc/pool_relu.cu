@@ -431,6 +431,18 @@ __global__ void __launch_bounds__(256, 4) maxpool_bwd_k3s2p1(PoolDims d, const T
   const int gg = t - j * G;
   const int n = blockIdx.y / in;
   const int i = blockIdx.y - n * in;
+  const int h0 = 2 * i, w0 = 2 * j;
+  // the producer ReLU's keep bits of the 4 output pixels, loaded with the
+  // windows (one memory round trip per thread instead of two)
+  uint32_t kb4[2][2] = {{0xFFu, 0xFFu}, {0xFFu, 0xFFu}};
+  if (keep) {
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+        if (h0 + a < d.h && w0 + b < d.w)
+          kb4[a][b] = __ldg(keep + (((int64_t)n * d.h + h0 + a) * d.w + w0 + b) * G + gg);
+  }
   float gv[2][2][8];
   uint2 u[2][2];
 #pragma unroll
@@ -460,12 +472,9 @@ __global__ void __launch_bounds__(256, 4) maxpool_bwd_k3s2p1(PoolDims d, const T
   route8<T>(o11, u[0][1], gv[0][1], 6);  //                (i, j+1) r2 s0
   route8<T>(o11, u[1][0], gv[1][0], 2);  //                (i+1, j) r0 s2
   route8<T>(o11, u[1][1], gv[1][1], 0);  //                (i+1, j+1) r0 s0
-  const int h0 = 2 * i, w0 = 2 * j;
   if (keep || in_bn.var) {
-    auto fin = [&](float (&o)[8], int hh, int ww) {
-      if (hh >= d.h || ww >= d.w) return;
+    auto fin = [&](float (&o)[8], uint32_t kb) {
       if (keep) {
-        const uint32_t kb = keep[(((int64_t)n * d.h + hh) * d.w + ww) * G + gg];
 #pragma unroll
         for (int q = 0; q < 8; ++q) o[q] = ((kb >> q) & 1u) ? o[q] : 0.f;
       }
@@ -474,10 +483,10 @@ __global__ void __launch_bounds__(256, 4) maxpool_bwd_k3s2p1(PoolDims d, const T
         for (int q = 0; q < 8; ++q) o[q] *= s_sc[gg * 8 + q];
       }
     };
-    fin(o00, h0, w0);
-    fin(o01, h0, w0 + 1);
-    fin(o10, h0 + 1, w0);
-    fin(o11, h0 + 1, w0 + 1);
+    fin(o00, kb4[0][0]);
+    fin(o01, kb4[0][1]);
+    fin(o10, kb4[1][0]);
+    fin(o11, kb4[1][1]);
   }
   T* base = dx + ((int64_t)n * d.h + h0) * d.w * d.c + gg * 8;
   st8<T>(base + (int64_t)w0 * d.c, o00, true);
