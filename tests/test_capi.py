@@ -44,6 +44,22 @@ def test_host_only_queries():
     assert L.ms_bn_eval_workspace(2, 64, 49, _lib.MS_NHWC) == 2 * 64 * 4
 
 
+def test_fp32_linear_workspace_is_the_tf32_split():
+    """float32 Linear (3xTF32) keeps hi / lo planes of both operands, K-major with
+    a 16-byte pitch, in the caller's workspace; small products stay on the SIMT
+    kernel and need none (csrc/linear.cu plan_linear)."""
+    L = _lib.lib()
+    al = lambda b: (b + 255) // 256 * 256  # noqa: E731
+    M, N, K = 4096, 1000, 130
+    ld = (K + 3) // 4 * 4
+    assert L.ms_linear_workspace(M, N, K, _lib.MS_F32, 0) == 2 * al(4 * M * ld) + 2 * al(4 * N * ld)
+    # dX: out M x K, reduction N; dW: out N x K, reduction M
+    ldn, ldm = (N + 3) // 4 * 4, (M + 3) // 4 * 4
+    assert L.ms_linear_workspace(M, N, K, _lib.MS_F32, 1) == 2 * al(4 * M * ldn) + 2 * al(4 * K * ldn)
+    assert L.ms_linear_workspace(M, N, K, _lib.MS_F32, 2) == 2 * al(4 * N * ldm) + 2 * al(4 * K * ldm)
+    assert L.ms_linear_workspace(64, 2, 768, _lib.MS_F32, 0) == 0  # classifier head: SIMT
+
+
 def test_invalid_descriptor_rejected_without_gpu():
     L = _lib.lib()
     d = _lib.ConvDesc(1, 0, 8, 8, 4, 3, 3, 1, 1, 1, 1, _lib.MS_NHWC, _lib.MS_NHWC, _lib.MS_BF16)
