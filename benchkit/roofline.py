@@ -22,6 +22,7 @@ import math
 from collections import OrderedDict
 
 import torch
+import torch.utils._python_dispatch  # noqa: F401  (TorchDispatchMode)
 
 from paper_2404_12406_b200 import _ops as OPS
 
@@ -135,24 +136,60 @@ def work_of(name, args):
     return 0.0, 0.0, {}
 
 
+# ops whose autograd lives in C++ (csrc/torch_ops.cpp): timed at the dispatcher
+# level, where the C++ forward / backward call their kernel ops
+_AUTOGRAD_OPS = {"linear"}
+
+
 class _Recorder:
     def __init__(self, real):
         self._real = real
         self.calls = []
+        self.busy = False  # inside a timed Python-level call (the mode below skips)
 
     def __getattr__(self, name):
         fn = getattr(self._real, name)
+        if name in _AUTOGRAD_OPS:
+            return fn  # its kernel ops are recorded by _DispatchRecorder
 
         def wrapped(*args):
             s = torch.cuda.Event(enable_timing=True)
             e = torch.cuda.Event(enable_timing=True)
-            s.record()
-            out = fn(*args)
-            e.record()
+            self.busy = True
+            try:
+                s.record()
+                out = fn(*args)
+                e.record()
+            finally:
+                self.busy = False
             flops, byts, geom = work_of(name, args)
             self.calls.append((name, s, e, flops, byts, geom))
             return out
         return wrapped
+
+
+class _DispatchRecorder(torch.utils._python_dispatch.TorchDispatchMode):
+    """Times the memsave kernel ops that C++ autograd code calls through the
+    dispatcher (memsave::linear's forward and backward); the mode is carried
+    into the autograd engine's backward thread."""
+
+    def __init__(self, rec):
+        super().__init__()
+        self.rec = rec
+
+    def __torch_dispatch__(self, func, types, args=(), kwargs=None):
+        kwargs = kwargs or {}
+        if func.namespace != "memsave" or self.rec.busy:
+            return func(*args, **kwargs)
+        name = func._opname
+        s = torch.cuda.Event(enable_timing=True)
+        e = torch.cuda.Event(enable_timing=True)
+        s.record()
+        out = func(*args, **kwargs)
+        e.record()
+        flops, byts, geom = work_of(name, args)
+        self.rec.calls.append((name, s, e, flops, byts, geom))
+        return out
 
 
 def trace_step(step, dev, sleep_s: float = 0.3):
@@ -166,9 +203,10 @@ def trace_step(step, dev, sleep_s: float = 0.3):
     s1 = torch.cuda.Event(enable_timing=True)
     OPS._OV = rec
     try:
-        s0.record()
-        step()
-        s1.record()
+        with _DispatchRecorder(rec):
+            s0.record()
+            step()
+            s1.record()
     finally:
         OPS._OV = real
     torch.cuda.synchronize(dev)

@@ -5,15 +5,20 @@
 // for the Meta key (the same allocations, no launch), so the ops are visible to
 // FakeTensor / torch.compile / torch.export and to CUDA-graph capture.
 //
-// The save decision is NOT here: the autograd.Functions in functional.py decide
-// at forward time, from ctx.needs_input_grad, which of X / W to keep (reference
-// rules.py:133-141) and call only the backward products that were requested.
+// The save decision for Linear is made here, in a C++ autograd Function
+// (memsave::linear, Autograd key): at forward time X is kept only if W requires
+// a gradient and W only if X does (reference rules.py:133-141), and backward
+// calls only the requested products -- without the per-call cost of a Python
+// autograd.Function (Linear is the most frequent memsave op in the transformer
+// steps).  The other layers decide in the autograd.Functions of functional.py.
 // Reference anchors: leantape.kernels.conv2d_fwd / conv2d_dx / conv2d_dw
 // (kernels/__init__.py:26-28), the Linear and BN-eval VJPs
 // and the autograd primitive the paper wraps them in.
 #include <ATen/ATen.h>
+#include <ATen/core/dispatch/Dispatcher.h>
 #include <ATen/cuda/CUDAContext.h>
 #include <c10/cuda/CUDAGuard.h>
+#include <torch/csrc/autograd/custom_function.h>
 #include <torch/library.h>
 
 #include <optional>
@@ -624,9 +629,78 @@ Tensor conv2d_bn_dx(const Tensor& g, const Tensor& w, const OptT& bn_var, const 
   return out;
 }
 
+// ------------------------------------------------ Linear with C++ autograd
+template <typename Sig>
+c10::TypedOperatorHandle<Sig> op_handle(const char* name) {
+  return c10::Dispatcher::singleton().findSchemaOrThrow(name, "").typed<Sig>();
+}
+
+struct LinearFn : public torch::autograd::Function<LinearFn> {
+  static Tensor forward(torch::autograd::AutogradContext* ctx, const Tensor& x, const Tensor& w,
+                        const OptT& b) {
+    // MemSave rule (rules.py:133-141): X iff W needs a grad, W iff X does;
+    // the bias needs nothing (rules.py:134-135)
+    const bool x_rg = x.requires_grad(), w_rg = w.requires_grad();
+    ctx->save_for_backward({w_rg ? x : Tensor(), x_rg ? w : Tensor()});
+    ctx->saved_data["x_shape"] = x.sizes().vec();
+    // a None bias is not an input variable of the node (needs_input_grad has 2 slots)
+    ctx->saved_data["has_b"] = has(b);
+    static auto fwd = op_handle<Tensor(const Tensor&, const Tensor&, const OptT&)>(
+        "memsave::linear_fwd");
+    at::AutoDispatchBelowADInplaceOrView guard;
+    return fwd.call(x, w, b);
+  }
+  static torch::autograd::variable_list backward(torch::autograd::AutogradContext* ctx,
+                                                 torch::autograd::variable_list grads) {
+    static auto dx_op =
+        op_handle<Tensor(const Tensor&, const Tensor&, IntArrayRef)>("memsave::linear_dx");
+    static auto dw_op = op_handle<Tensor(const Tensor&, const Tensor&)>("memsave::linear_dw");
+    static auto db_op = op_handle<Tensor(const Tensor&, int64_t)>("memsave::bias_grad");
+    const auto saved = ctx->get_saved_variables();
+    const Tensor& gy = grads[0];
+    Tensor dx, dw, db;
+    if (ctx->needs_input_grad(0)) {
+      TORCH_CHECK(saved[1].defined(), "MissingSavedValue: linear dX needs 'w' but the storage "
+                                      "rule did not keep it");
+      dx = dx_op.call(gy, saved[1], ctx->saved_data["x_shape"].toIntVector());
+    }
+    if (ctx->needs_input_grad(1)) {
+      TORCH_CHECK(saved[0].defined(), "MissingSavedValue: linear dW needs 'x' but the storage "
+                                      "rule did not keep it");
+      dw = dw_op.call(saved[0], gy);
+    }
+    if (ctx->saved_data["has_b"].toBool() && ctx->needs_input_grad(2))
+      db = db_op.call(gy, gy.size(-1));
+    return {dx, dw, db};
+  }
+};
+
+void check_linear(const Tensor& x, const Tensor& w, const OptT& b) {
+  for (const Tensor* t : {&x, &w, has(b) ? &*b : nullptr}) {
+    if (!t) continue;
+    TORCH_CHECK(t->is_cuda() || t->is_meta(), "memsave_b200.linear: tensors must be on a CUDA "
+                "device (got ", t->device(), "); this implementation has no CPU path");
+  }
+  TORCH_CHECK(w.dim() == 2 && x.dim() >= 1 && x.size(-1) == w.size(1), "linear: input last dim ",
+              x.size(-1), " != in_features ", w.size(-1));
+  TORCH_CHECK(x.scalar_type() == w.scalar_type(), "linear: input dtype ", x.scalar_type(),
+              " != weight dtype ", w.scalar_type());
+}
+
+Tensor linear_autograd(const Tensor& x, const Tensor& w, const OptT& b) {
+  check_linear(x, w, b);
+  return LinearFn::apply(x, w, b);
+}
+
+Tensor linear_noautograd(const Tensor& x, const Tensor& w, const OptT& b) {
+  check_linear(x, w, b);
+  return linear_fwd(x, w, b);
+}
+
 }  // namespace
 
 TORCH_LIBRARY(memsave, m) {
+  m.def("linear(Tensor x, Tensor w, Tensor? b) -> Tensor");
   m.def("linear_fwd(Tensor x, Tensor w, Tensor? b) -> Tensor");
   m.def("linear_dx(Tensor g, Tensor w, int[] x_shape) -> Tensor");
   m.def("linear_dw(Tensor x, Tensor g) -> Tensor");
@@ -709,5 +783,13 @@ TORCH_LIBRARY(memsave, m) {
   m.impl("conv2d_bn_fwd", &conv2d_bn_fwd);                   \
   m.impl("conv2d_bn_dx", &conv2d_bn_dx)
 
-TORCH_LIBRARY_IMPL(memsave, CUDA, m) { MS_IMPLS(m); }
-TORCH_LIBRARY_IMPL(memsave, Meta, m) { MS_IMPLS(m); }
+TORCH_LIBRARY_IMPL(memsave, CUDA, m) {
+  MS_IMPLS(m);
+  m.impl("linear", &linear_noautograd);
+}
+TORCH_LIBRARY_IMPL(memsave, Meta, m) {
+  MS_IMPLS(m);
+  m.impl("linear", &linear_noautograd);
+}
+TORCH_LIBRARY_IMPL(memsave, Autograd, m) { m.impl("linear", &linear_autograd); }
+// CPU tensors reach the autograd kernel too (then fail loudly in check_linear)

@@ -65,57 +65,16 @@ def _is_channels_last(t: torch.Tensor) -> bool:
 
 
 # =============================================================== linear
-class _LinearFn(torch.autograd.Function):
-    @staticmethod
-    def forward(ctx, x, weight, bias):
-        x_rg, w_rg = ctx.needs_input_grad[0], ctx.needs_input_grad[1]
-        roles = saved_roles(x_rg, w_rg)
-        ctx.save_for_backward(x if "x" in roles else None, weight if "w" in roles else None)
-        ctx.x_shape = x.shape
-        N, K = weight.shape
-        if x.shape[-1] != K:
-            raise RuntimeError(f"linear: input last dim {x.shape[-1]} != in_features {K}")
-        out_shape = tuple(x.shape[:-1]) + (N,)
-        if _is_meta(x, weight):
-            return x.new_empty(out_shape)
-        _require_cuda("linear", x, weight, bias)
-        if weight.dtype != x.dtype:
-            raise TypeError(f"linear: input dtype {x.dtype} != weight dtype {weight.dtype}")
-        _dtype_code(x)
-        # allocated in its final shape by the op: returning a view of an internal
-        # buffer would make in-place consumers (ReLU(inplace=True)) illegal
-        return _ops().linear_fwd(x, weight, bias)
-
-    @staticmethod
-    def backward(ctx, gy):
-        x, w = ctx.saved_tensors
-        need_x, need_w, need_b = ctx.needs_input_grad[:3]
-        dx = dw = db = None
-        N = gy.shape[-1]
-        if _is_meta(gy):
-            if need_x:
-                dx = gy.new_empty(ctx.x_shape)
-            if need_w:
-                x = _need(x, "x", "linear dW")
-                dw = gy.new_empty((N, x.shape[-1]))
-            if need_b:
-                db = gy.new_empty((N,))
-            return dx, dw, db
-        O = _ops()
-        if need_x:
-            w = _need(w, "w", "linear dX")
-            dx = O.linear_dx(gy, w, list(ctx.x_shape))
-        if need_w:
-            x = _need(x, "x", "linear dW")
-            dw = O.linear_dw(x, gy)
-        if need_b:
-            db = O.bias_grad(gy, N)
-        return dx, dw, db
-
-
 def linear(x: torch.Tensor, weight: torch.Tensor, bias: torch.Tensor | None = None):
-    """Differentiability-agnostic ``F.linear`` (SPEC.md:241-249)."""
-    return _LinearFn.apply(x, weight, bias)
+    """Differentiability-agnostic ``F.linear`` (SPEC.md:241-249).
+
+    ``torch.ops.memsave.linear`` is a C++ autograd Function (csrc/torch_ops.cpp,
+    ``LinearFn``): at forward time it keeps X only if the weight requires a
+    gradient and W only if X does (the linear family, rules.py:133-141), and its
+    backward launches only the requested products (dX, dW, db).  CPU tensors
+    raise (no CPU path); meta tensors take the same storage decisions without
+    arithmetic."""
+    return _ops().linear(x, weight, bias)
 
 
 # =============================================================== conv2d

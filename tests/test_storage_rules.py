@@ -232,3 +232,18 @@ def test_conv_transpose2d_saved_set(rules_golden, x_rg, w_rg, b_rg):
         out.sum().backward()
         assert (x.grad is not None) == x_rg and (w.grad is not None) == w_rg
         assert (b.grad is not None) == b_rg
+
+
+@pytest.mark.parametrize("x_rg,w_rg", [(True, False), (False, True), (True, True)])
+def test_linear_without_bias_backward_on_meta(x_rg, w_rg):
+    """memsave::linear with bias=None: the C++ autograd node has two inputs and
+    returns only the requested gradients (Llama-style bias-free projections)."""
+    x = torch.empty(4, 6, 7, device="meta").requires_grad_(x_rg)
+    w = torch.empty(3, 7, device="meta").requires_grad_(w_rg)
+    y = MF.linear(x, w, None)
+    y.sum().backward()
+    assert (x.grad is not None) == x_rg and (w.grad is not None) == w_rg
+    if x_rg:
+        assert x.grad.shape == x.shape
+    if w_rg:
+        assert w.grad.shape == w.shape
