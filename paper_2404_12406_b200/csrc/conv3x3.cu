@@ -16,6 +16,8 @@
 // Epilogue: 4 warps (TMEM lane quarters = 32 output pixels of one row), the
 // same fused eval-BN / residual / ReLU + bit mask as the generic kernel, TMA
 // stores through a 3-D map [N*H][W][K] that clips the pitch padding.
+#include <cstdlib>
+
 #include "misc.cuh"
 
 namespace ms {
@@ -62,6 +64,7 @@ struct H3Args {
   uint8_t* mask;
   const uint8_t* keep_in;  // dgrad: the producer ReLU's mask, applied after resid
   int bn_post;             // dgrad: then scale by the producer BN's s (bn)
+  int dbg;                 // profiling (MS_H3_DBG): 1 = every tap reads the s = 0 rows
 };
 
 // SW128 K-major descriptor whose start may sit at any 128-byte row of a
@@ -174,7 +177,7 @@ __global__ void __launch_bounds__(H3Geo<WIDE>::THREADS, 1)
           for (int t = 0; t < 9; ++t) {
             const int r = t / 3, s = t - (t / 3) * 3;
             // output pixel m' = i*64 + j reads halo row (i + r)*64 + (j + s)
-            const uint32_t arow = sh + (r * H3_P + s) * 128;
+            const uint32_t arow = sh + (r * H3_P + (a.dbg & 1 ? 0 : s)) * 128;
             const uint32_t brow = sB_u + t * 8192;
 #pragma unroll
             for (int k = 0; k < 4; ++k)
@@ -380,6 +383,13 @@ ms_status conv3x3_halo(int dt, int n, int h, int w, int wlayout, int transpose, 
   a.tiles_per_img = (h + rows - 1) / rows;
   a.segs = wide ? (w + H3Geo<1>::SEG - 1) / H3Geo<1>::SEG : 1;
   a.units = n * a.tiles_per_img * a.segs;
+  {
+    static const int env_dbg = [] {
+      const char* e = getenv("MS_H3_DBG");
+      return e ? atoi(e) : 0;
+    }();
+    a.dbg = env_dbg;
+  }
   a.dt = dt; a.y = y; a.bn = bn; a.bias = bias; a.resid = resid;
   a.relu = relu; a.mask = mask; a.keep_in = keep_in; a.bn_post = bn_post;
   const int grid = a.units < num_sms() ? a.units : num_sms();
