@@ -659,6 +659,11 @@ struct LinearFn : public torch::autograd::Function<LinearFn> {
     const auto saved = ctx->get_saved_variables();
     const Tensor& gy = grads[0];
     Tensor dx, dw, db;
+    // db first: dY was just written by the previous backward op and is still in
+    // L2, and the bias reduction writes almost nothing, so the dX / dW GEMMs
+    // that follow find dY there too
+    if (ctx->saved_data["has_b"].toBool() && ctx->needs_input_grad(2))
+      db = db_op.call(gy, gy.size(-1));
     if (ctx->needs_input_grad(0)) {
       TORCH_CHECK(saved[1].defined(), "MissingSavedValue: linear dX needs 'w' but the storage "
                                       "rule did not keep it");
@@ -669,8 +674,6 @@ struct LinearFn : public torch::autograd::Function<LinearFn> {
                                       "rule did not keep it");
       dw = dw_op.call(saved[0], gy);
     }
-    if (ctx->saved_data["has_b"].toBool() && ctx->needs_input_grad(2))
-      db = db_op.call(gy, gy.size(-1));
     return {dx, dw, db};
   }
 };
