@@ -266,7 +266,10 @@ __global__ void __launch_bounds__(256, WANT_DW ? 2 : 3) bn_bwd_nhwc_kernel(int64
                                                           float* __restrict__ acc_dw,
                                                           float* __restrict__ acc_db,
                                                           const uint8_t* __restrict__ keep = nullptr,
-                                                          T* __restrict__ gkeep = nullptr) {
+                                                          T* __restrict__ gkeep = nullptr,
+                                                          void* dw_out = nullptr,
+                                                          void* db_out = nullptr,
+                                                          unsigned* ticket = nullptr) {
   // keep (nullable, VEC == 8): the following ReLU's mask, g := keep ? g : 0 first;
   // gkeep (nullable): that masked g stored too (the residual operand's gradient)
   __shared__ float s_dw[2048], s_db[2048];
@@ -338,6 +341,22 @@ __global__ void __launch_bounds__(256, WANT_DW ? 2 : 3) bn_bwd_nhwc_kernel(int64
     for (int c = tid; c < C; c += 256) {
       if (want_dw) atomicAdd(acc_dw + c, s_dw[c]);
       if (want_db) atomicAdd(acc_db + c, s_db[c]);
+    }
+    if (ticket) {
+      // the last block to finish converts the fp32 sums to the parameter dtype
+      // (no separate f32_to launch; the ticket is zeroed with the accumulators)
+      __shared__ bool last;
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+      __syncthreads();
+      if (last) {
+        __threadfence();
+        for (int c = tid; c < C; c += 256) {
+          if (want_dw) store_from_float(dw_out, p.pdtype, c, __ldcg(acc_dw + c));
+          if (want_db) store_from_float(db_out, p.pdtype, c, __ldcg(acc_db + c));
+        }
+      }
     }
   }
 }
@@ -411,7 +430,8 @@ static int nhwc_grid(int64_t rows, int64_t G, int occ, int unr = BN_UNR) {
   return (int)(need > 0 ? need : 1);
 }
 
-size_t bn_eval_workspace_bytes(int64_t c) { return sizeof(float) * 2 * (size_t)c; }
+// [dw | db] fp32 accumulators, then the finalize ticket of bn_bwd_nhwc_kernel
+size_t bn_eval_workspace_bytes(int64_t c) { return sizeof(float) * 2 * (size_t)c + 16; }
 
 ms_status bn_eval_fwd(int64_t n, int64_t c, int64_t hw, int layout, int dt, const BnParams& p,
                       const void* x, void* y, cudaStream_t st) {
@@ -492,19 +512,22 @@ ms_status bn_relu_eval_bwd(int64_t n, int64_t c, int64_t hw, int dt, const BnPar
   if (rows > 0 && (dx || dresid || dw || db)) {
     auto go = [&](auto tag) {
       using T = decltype(tag);
+      unsigned* tk = (dw || db) ? reinterpret_cast<unsigned*>(static_cast<float*>(ws) + 2 * c)
+                                : nullptr;
       if (dw)
         bn_bwd_nhwc_kernel<T, 8, true><<<nhwc_grid(rows, c / 8, 2, BN_BWD_UNR_DW), 256, 0, st>>>(
             rows, (int)c, p, (const T*)g, (const T*)x, (T*)dx, acc_dw, acc_db, keep,
-            (T*)dresid);
+            (T*)dresid, dw, db, tk);
       else
         bn_bwd_nhwc_kernel<T, 8, false><<<nhwc_grid(rows, c / 8, 3, BN_BWD_UNR), 256, 0, st>>>(
             rows, (int)c, p, (const T*)g, (const T*)x, (T*)dx, acc_dw, acc_db, keep,
-            (T*)dresid);
+            (T*)dresid, dw, db, tk);
     };
     if (dt == MS_BF16) go(__nv_bfloat16{});
     else go(__half{});
     count_launch(1, KF_BN);
     MS_TRY(launch_status("bn_bwd_nhwc_kernel (relu)"));
+    return MS_OK;  // dW / db converted by the kernel's last block
   }
   return store_dw_db(acc_dw, acc_db, dw, db, p.pdtype, c, st);
   return MS_OK;
@@ -525,6 +548,7 @@ ms_status bn_eval_bwd(int64_t n, int64_t c, int64_t hw, int layout, int dt, cons
     if (dw) acc_dw = static_cast<float*>(ws);
     if (db) acc_db = static_cast<float*>(ws) + c;
   }
+  bool fused_store = false;  // dW / db converted by the NHWC kernel's last block
   if (total > 0 && (dx || dw || db)) {
     const size_t smem = sizeof(float) * 5 * c;
     MS_DT_DISPATCH(dt, {
@@ -532,12 +556,17 @@ ms_status bn_eval_bwd(int64_t n, int64_t c, int64_t hw, int layout, int dt, cons
       if (layout == MS_NHWC && can_vec(c, hw, layout, V, g, dw ? x : nullptr, dx) &&
           c / V <= 256 && c <= 2048) {
         const int64_t rows = n * hw;
+        unsigned* tk = (dw || db) ? reinterpret_cast<unsigned*>(static_cast<float*>(ws) + 2 * c)
+                                  : nullptr;
         if (dw)
           bn_bwd_nhwc_kernel<T, V, true><<<nhwc_grid(rows, c / V, 2, BN_BWD_UNR_DW), 256, 0, st>>>(
-              rows, (int)c, p, (const T*)g, (const T*)x, (T*)dx, acc_dw, acc_db);
+              rows, (int)c, p, (const T*)g, (const T*)x, (T*)dx, acc_dw, acc_db, nullptr,
+              nullptr, dw, db, tk);
         else
           bn_bwd_nhwc_kernel<T, V, false><<<nhwc_grid(rows, c / V, 3, BN_BWD_UNR), 256, 0, st>>>(
-              rows, (int)c, p, (const T*)g, (const T*)x, (T*)dx, acc_dw, acc_db);
+              rows, (int)c, p, (const T*)g, (const T*)x, (T*)dx, acc_dw, acc_db, nullptr,
+              nullptr, dw, db, tk);
+        fused_store = true;
       } else if (can_vec(c, hw, layout, V, g, dw ? x : nullptr, dx)) {
         bn_bwd_kernel<T, V><<<bn_grid(total / V, c, layout, V), 256, smem, st>>>(
             total, (int)c, hw, layout, p, (const T*)g, (const T*)x, (T*)dx, acc_dw, acc_db);
@@ -549,6 +578,7 @@ ms_status bn_eval_bwd(int64_t n, int64_t c, int64_t hw, int layout, int dt, cons
     count_launch(1, KF_BN);
     MS_TRY(launch_status("bn_bwd_kernel"));
   }
+  if (fused_store) return MS_OK;
   return store_dw_db(acc_dw, acc_db, dw, db, p.pdtype, c, st);
   return MS_OK;
 }

@@ -41,7 +41,8 @@ def test_host_only_queries():
     assert L.ms_conv2d_out_w(ctypes.byref(d)) == 112
     # stem: 3 channels -> padded activation copy + repacked weight in the workspace
     assert L.ms_conv2d_workspace(ctypes.byref(d), _lib.MS_CONV_FWD) > 0
-    assert L.ms_bn_eval_workspace(2, 64, 49, _lib.MS_NHWC) == 2 * 64 * 4
+    # fp32 dW | db accumulators + the finalize ticket of the NHWC backward
+    assert L.ms_bn_eval_workspace(2, 64, 49, _lib.MS_NHWC) == 2 * 64 * 4 + 16
 
 
 def test_fp32_linear_workspace_is_the_tf32_split():
