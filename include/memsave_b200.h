@@ -91,7 +91,8 @@ MS_API ms_status ms_conv2d_dx(const ms_conv_desc* d, const void* dy, const void*
 /* dw = conv2d weight-VJP of dy with x; dw has layout d->wlayout and dtype d->dtype */
 MS_API ms_status ms_conv2d_dw(const ms_conv_desc* d, const void* x, const void* dy, void* dw, void* ws,
                        size_t ws_bytes, void* stream);
-/* db[k] = sum of dy over n, oh, ow (dy in d->layout, db in d->dtype) */
+/* db[k] = sum of dy over n, oh, ow (dy in d->layout, db in d->dtype);
+ * ws_bytes >= ms_bias_grad_workspace(0, d->k, d->dtype) */
 MS_API ms_status ms_conv2d_db(const ms_conv_desc* d, const void* dy, void* db, void* ws,
                        size_t ws_bytes, void* stream);
 

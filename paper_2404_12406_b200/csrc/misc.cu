@@ -10,7 +10,8 @@ namespace ms {
 // atomic per column per block.
 template <typename T>
 __global__ void __launch_bounds__(256) colsum_kernel(int64_t rows, int64_t cols, const T* __restrict__ g,
-                                                    float* __restrict__ acc, int64_t rows_per_block) {
+                                                    float* __restrict__ acc, int64_t rows_per_block,
+                                                    void* out, int odt, unsigned* ticket) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t c0 = (blockIdx.x * 32 + lane) * 8;
   float s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -56,6 +57,17 @@ __global__ void __launch_bounds__(256) colsum_kernel(int64_t rows, int64_t cols,
     for (int w = 0; w < 8; ++w) v += red[w][i];
     const int64_t c = blockIdx.x * 256 + i;
     if (c < cols) atomicAdd(acc + c, v);
+  }
+  // the last block converts the sums to the output dtype (no separate launch;
+  // the ticket is zeroed with the accumulators)
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x * gridDim.y - 1;
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    for (int64_t c = threadIdx.x; c < cols; c += 256) store_from_float(out, odt, c, __ldcg(acc + c));
   }
 }
 
@@ -106,7 +118,8 @@ static int grid_1d(int64_t total, int per_thread = 1) {
     default: set_error("bad dtype %d", dt); return MS_ERR_DTYPE;   \
   }
 
-size_t colsum_workspace(int64_t cols) { return sizeof(float) * (size_t)cols; }
+// [cols] fp32 accumulators, then the finalize ticket
+size_t colsum_workspace(int64_t cols) { return sizeof(float) * (size_t)cols + 16; }
 
 ms_status f32_to(const float* src, void* dst, int dt, int64_t count, const void* bias,
                  int64_t bias_period, cudaStream_t st) {
@@ -120,7 +133,8 @@ ms_status f32_to(const float* src, void* dst, int dt, int64_t count, const void*
 ms_status colsum(int64_t rows, int64_t cols, int dt, const void* g, void* db, int odt, void* ws,
                  cudaStream_t st) {
   float* acc = static_cast<float*>(ws);
-  cudaMemsetAsync(acc, 0, sizeof(float) * cols, st);
+  unsigned* ticket = reinterpret_cast<unsigned*>(acc + cols);
+  cudaMemsetAsync(acc, 0, colsum_workspace(cols), st);
   const int64_t gx = (cols + 255) / 256;
   int64_t gy = ((int64_t)num_sms() * 4 + gx - 1) / gx;
   int64_t per = (rows + gy - 1) / gy;
@@ -128,10 +142,10 @@ ms_status colsum(int64_t rows, int64_t cols, int dt, const void* g, void* db, in
   gy = (rows + per - 1) / per;
   if (gy < 1) gy = 1;
   dim3 grid((unsigned)gx, (unsigned)gy);
-  MS_DT_DISPATCH(dt, colsum_kernel<T><<<grid, 256, 0, st>>>(rows, cols, (const T*)g, acc, per));
+  MS_DT_DISPATCH(dt, colsum_kernel<T><<<grid, 256, 0, st>>>(rows, cols, (const T*)g, acc, per, db,
+                                                             odt, ticket));
   count_launch();
-  MS_TRY(launch_status("colsum_kernel"));
-  return f32_to(acc, db, odt, cols, nullptr, 1, st);
+  return launch_status("colsum_kernel");
 }
 
 ms_status planesum(int64_t n, int64_t c, int64_t hw, int dt, const void* g, void* db, int odt,

@@ -245,7 +245,7 @@ Tensor conv2d_db(const Tensor& g, IntArrayRef x_shape, IntArrayRef w_shape, IntA
   Tensor db = at::empty({d.k}, g.options());
   if (g.is_meta()) return db;
   Launch L(g);
-  const size_t nb = 4 * (size_t)d.k;
+  const size_t nb = ms_bias_grad_workspace(0, d.k, dt);  // fp32 sums + finalize ticket
   Tensor ws = wsp(nb, g);
   ok(ms_conv2d_db(&d, cp(g), mp(db), mp(ws), nb, L.stream), "conv2d_db");
   return db;
