@@ -48,6 +48,14 @@ def work_of(name, args):
         return t.element_size()
 
     a = args
+    if name == "linear_bwd":  # (x_shape, w_shape, dtype size, need_dx, need_dw)
+        xs, ws_, es, ndx, ndw = a
+        N, K = ws_
+        M = int(math.prod(xs)) // K
+        n = int(ndx) + int(ndw)
+        return 2.0 * M * N * K * n, es * n * (M * K + N * K + M * N), dict(M=M, N=N, K=K)
+    if name == "linear":
+        name = "linear_fwd"
     if name in ("linear_fwd", "linear_dx", "linear_dw"):
         if name == "linear_fwd":
             x, w = a[0], a[1]
@@ -136,42 +144,53 @@ def work_of(name, args):
     return 0.0, 0.0, {}
 
 
-# ops whose autograd lives in C++ (csrc/torch_ops.cpp): timed at the dispatcher
-# level, where the C++ forward / backward call their kernel ops
-_AUTOGRAD_OPS = {"linear"}
-
-
 class _Recorder:
+    """Brackets every torch.ops.memsave call with CUDA events.  memsave::linear
+    runs its backward in C++ (csrc/torch_ops.cpp), invisible to this wrapper:
+    its forward call is timed as ``linear_fwd``, and hooks on the output's
+    grad_fn time the kernel ops its backward node dispatches."""
+
     def __init__(self, real):
         self._real = real
         self.calls = []
-        self.busy = False  # inside a timed Python-level call (the mode below skips)
 
     def __getattr__(self, name):
         fn = getattr(self._real, name)
-        if name in _AUTOGRAD_OPS:
-            return fn  # its kernel ops are recorded by _DispatchRecorder
 
         def wrapped(*args):
             s = torch.cuda.Event(enable_timing=True)
             e = torch.cuda.Event(enable_timing=True)
-            self.busy = True
-            try:
-                s.record()
-                out = fn(*args)
-                e.record()
-            finally:
-                self.busy = False
+            s.record()
+            out = fn(*args)
+            e.record()
             flops, byts, geom = work_of(name, args)
-            self.calls.append((name, s, e, flops, byts, geom))
+            self.calls.append(("linear_fwd" if name == "linear" else name, s, e, flops, byts,
+                               geom))
+            if name == "linear" and out.grad_fn is not None:
+                self._hook_backward(out, args)
             return out
         return wrapped
 
+    def _hook_backward(self, out, args):
+        # a dispatch mode active only while this backward node runs (on the
+        # autograd thread) times each kernel op the C++ backward calls
+        node = out.grad_fn
+        state = {}
+
+        def pre(grad_outputs):
+            state["mode"] = _DispatchRecorder(self)
+            state["mode"].__enter__()
+
+        def post(grad_inputs, grad_outputs):
+            state.pop("mode").__exit__(None, None, None)
+
+        node.register_prehook(pre)
+        node.register_hook(post)
+
 
 class _DispatchRecorder(torch.utils._python_dispatch.TorchDispatchMode):
-    """Times the memsave kernel ops that C++ autograd code calls through the
-    dispatcher (memsave::linear's forward and backward); the mode is carried
-    into the autograd engine's backward thread."""
+    """Times the memsave kernel ops dispatched from C++ (memsave::linear's
+    backward: bias_grad, linear_dx, linear_dw)."""
 
     def __init__(self, rec):
         super().__init__()
@@ -179,7 +198,7 @@ class _DispatchRecorder(torch.utils._python_dispatch.TorchDispatchMode):
 
     def __torch_dispatch__(self, func, types, args=(), kwargs=None):
         kwargs = kwargs or {}
-        if func.namespace != "memsave" or self.rec.busy:
+        if func.namespace != "memsave":
             return func(*args, **kwargs)
         name = func._opname
         s = torch.cuda.Event(enable_timing=True)
@@ -203,10 +222,9 @@ def trace_step(step, dev, sleep_s: float = 0.3):
     s1 = torch.cuda.Event(enable_timing=True)
     OPS._OV = rec
     try:
-        with _DispatchRecorder(rec):
-            s0.record()
-            step()
-            s1.record()
+        s0.record()
+        step()
+        s1.record()
     finally:
         OPS._OV = real
     torch.cuda.synchronize(dev)

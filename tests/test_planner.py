@@ -121,3 +121,35 @@ def test_planned_peak_matches_b200_resnet18_input_only():
     measured = _measure(m, x, loss)
     predicted = pl.peak_bytes - pl.resident_bytes
     assert abs(measured - predicted) <= 0.05 * predicted + (4 << 20), (measured, predicted)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("config,batch", [("resnet101", 8), ("vgg16", 8), ("bert", 4)])
+def test_planned_peak_matches_b200_configs(config, batch):
+    """The planner's meta-device prediction of a whole config step (converted and
+    fused as the bench runs it: weights + trainable grads + the rule-predicted
+    saved set + live transients) equals torch.cuda.max_memory_allocated of the
+    real step, at reduced batch (SURVEY.md §8(d) peak-memory target)."""
+    from benchkit import models as BM
+    wl = BM.WORKLOADS[config](batch=batch)
+    model = convert_to_memory_saving(wl.model, fuse=True)
+    dev = torch.device("cuda", 0)
+    inputs = list(wl.make_batch(batch, dev))
+    if wl.input_requires_grad:
+        inputs[0].requires_grad_(True)
+    wl.loss_fn(model, *inputs).backward()  # warm-up step (one-time allocations)
+    torch.cuda.synchronize()
+    for p in model.parameters():
+        p.grad = None
+    if wl.input_requires_grad:
+        inputs[0].grad = None
+    torch.cuda.empty_cache()
+    torch.cuda.reset_peak_memory_stats()
+    wl.loss_fn(model, *inputs).backward()
+    torch.cuda.synchronize()
+    measured = torch.cuda.max_memory_allocated()
+    mwl = BM.WORKLOADS[config](batch=batch, device="meta")
+    mmodel = convert_to_memory_saving(mwl.model, fuse=True)
+    predicted = plan(mmodel, inputs, loss_fn=mwl.loss_fn).peak_bytes
+    print(config, measured / 2**20, predicted / 2**20)
+    assert abs(measured - predicted) <= 0.03 * predicted + (16 << 20), (config, measured, predicted)
