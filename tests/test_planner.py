@@ -127,9 +127,10 @@ def test_planned_peak_matches_b200_resnet18_input_only():
 @pytest.mark.parametrize("config,batch", [("resnet101", 8), ("bert", 4)])
 def test_planned_peak_matches_b200_configs(config, batch):
     """The planner's meta-device prediction of a whole config step (converted and
-    fused as the bench runs it: weights + trainable grads + the rule-predicted
-    saved set + live transients) equals torch.cuda.max_memory_allocated of the
-    real step (SURVEY.md §8(d) peak-memory target).  VGG-16 is left to the
+    fused as the bench runs it: trainable grads + the rule-predicted saved set +
+    live transients above the resident weights and inputs) equals the peak that
+    torch.cuda.max_memory_allocated reports above the between-steps baseline
+    (SURVEY.md §8(d) peak-memory target).  VGG-16 is left to the
     bench line's pred_err (0.1 % at batch 128): at small batch its 273 MB of
     trainable-layer gradients dominate and the ledger's allocation order
     over-predicts the peak by ~20 % -- a known planner limit."""
@@ -148,11 +149,16 @@ def test_planned_peak_matches_b200_configs(config, batch):
         inputs[0].grad = None
     torch.cuda.empty_cache()
     torch.cuda.reset_peak_memory_stats()
+    # what stays allocated between steps (weights, inputs, and library state the
+    # warm-up step left behind: the 32 MiB cuBLAS workspace) is the baseline;
+    # the planner's counterpart is its resident set
+    base = torch.cuda.memory_allocated()
     wl.loss_fn(model, *inputs).backward()
     torch.cuda.synchronize()
-    measured = torch.cuda.max_memory_allocated()
+    measured = torch.cuda.max_memory_allocated() - base
     mwl = BM.WORKLOADS[config](batch=batch, device="meta")
     mmodel = convert_to_memory_saving(mwl.model, fuse=True)
-    predicted = plan(mmodel, inputs, loss_fn=mwl.loss_fn).peak_bytes
+    pl = plan(mmodel, inputs, loss_fn=mwl.loss_fn)
+    predicted = pl.peak_bytes - pl.resident_bytes
     print(config, measured / 2**20, predicted / 2**20)
     assert abs(measured - predicted) <= 0.03 * predicted + (16 << 20), (config, measured, predicted)
