@@ -102,6 +102,14 @@ MS_API size_t ms_linear_workspace(int64_t M, int64_t N, int64_t K, int32_t dtype
 MS_API ms_status ms_linear_fwd(int64_t M, int64_t N, int64_t K, int32_t dtype, const void* x,
                         const void* w, const void* bias, void* y, void* ws, size_t ws_bytes,
                         void* stream);
+/* Linear -> GELU (erf form, torch gelu approximate='none') in one call: pre =
+ * x·wᵀ + b (kept: it is what the GELU's VJP reads) and y = gelu(pre), the GELU
+ * applied to the rounded pre in the GEMM epilogue (tcgen05 path) or by a second
+ * launch (other paths).  ws as ms_linear_workspace(M, N, K, dtype, 0).  Replaces
+ * the pair forward_linear (kernels/__init__.py:26-28) + the consumer's GELU.  */
+MS_API ms_status ms_linear_gelu_fwd(int64_t M, int64_t N, int64_t K, int32_t dtype,
+                             const void* x, const void* w, const void* bias, void* pre,
+                             void* y, void* ws, size_t ws_bytes, void* stream);
 MS_API ms_status ms_linear_dx(int64_t M, int64_t N, int64_t K, int32_t dtype, const void* dy,
                        const void* w, void* dx, void* ws, size_t ws_bytes, void* stream);
 MS_API ms_status ms_linear_dw(int64_t M, int64_t N, int64_t K, int32_t dtype, const void* x,
@@ -110,6 +118,11 @@ MS_API ms_status ms_linear_dw(int64_t M, int64_t N, int64_t K, int32_t dtype, co
 MS_API size_t ms_bias_grad_workspace(int64_t rows, int64_t cols, int32_t dtype);
 MS_API ms_status ms_bias_grad(int64_t rows, int64_t cols, int32_t dtype, const void* g, void* db,
                        void* ws, size_t ws_bytes, void* stream);
+
+/* GELU (erf form) and its VJP dx = g * gelu'(pre), elementwise over numel  */
+MS_API ms_status ms_gelu_fwd(int64_t numel, int32_t dtype, const void* x, void* y, void* stream);
+MS_API ms_status ms_gelu_bwd(int64_t numel, int32_t dtype, const void* g, const void* pre,
+                      void* dx, void* stream);
 
 /* ------------------------------------------------------------ batchnorm2d (eval)
  * x/y/dy/dx: [n, c, hw] (MS_NCHW) or [n, hw, c] (MS_NHWC) in `dtype`.

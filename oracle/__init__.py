@@ -23,6 +23,7 @@ from .pool import maxpool2d_fwd, maxpool2d_bwd, relu_fwd, relu_bwd  # noqa: F401
 from .rules import Policy, storage_decision, linear_family  # noqa: F401
 from .dropout import dropout_fwd, dropout_bwd, dropout_mask, uniforms  # noqa: F401
 from .layernorm import layernorm_fwd, layernorm_bwd  # noqa: F401
+from .gelu import gelu_fwd, gelu_bwd  # noqa: F401
 from .conv_transpose import (conv_transpose2d_fwd, conv_transpose2d_dx,  # noqa: F401
                              conv_transpose2d_dw, conv_transpose2d_db)
 from .tolerance import assert_close_fp32, assert_close_lowp, round_to  # noqa: F401

@@ -54,6 +54,10 @@ SIGNATURES = {
     "ms_conv2d_db": (_c_i32, [ctypes.POINTER(ConvDesc), _vp, _vp, _vp, _c_sz, _vp]),
     "ms_linear_workspace": (_c_sz, [_c_i64, _c_i64, _c_i64, _c_i32, _c_i32]),
     "ms_linear_fwd": (_c_i32, [_c_i64, _c_i64, _c_i64, _c_i32, _vp, _vp, _vp, _vp, _vp, _c_sz, _vp]),
+    "ms_linear_gelu_fwd": (_c_i32, [_c_i64, _c_i64, _c_i64, _c_i32, _vp, _vp, _vp, _vp, _vp, _vp,
+                                    _c_sz, _vp]),
+    "ms_gelu_fwd": (_c_i32, [_c_i64, _c_i32, _vp, _vp, _vp]),
+    "ms_gelu_bwd": (_c_i32, [_c_i64, _c_i32, _vp, _vp, _vp, _vp]),
     "ms_linear_dx": (_c_i32, [_c_i64, _c_i64, _c_i64, _c_i32, _vp, _vp, _vp, _vp, _c_sz, _vp]),
     "ms_linear_dw": (_c_i32, [_c_i64, _c_i64, _c_i64, _c_i32, _vp, _vp, _vp, _vp, _c_sz, _vp]),
     "ms_bias_grad_workspace": (_c_sz, [_c_i64, _c_i64, _c_i32]),

@@ -218,6 +218,10 @@ ms_status setup_tma_store(TmapPack& tm, GemmArgs& g, int dt, void* out, int64_t 
   const uint64_t strides[1] = {(uint64_t)ldc * 2};
   const uint32_t box[2] = {32, 32};
   MS_TRY(make_tmap_nd(&tm.c, dt, out, 2, dims, strides, box, 64));
+  if (g.epi.act_out) {
+    if (reinterpret_cast<uintptr_t>(g.epi.act_out) & 15) return MS_OK;  // direct stores
+    MS_TRY(make_tmap_nd(&tm.c2, dt, g.epi.act_out, 2, dims, strides, box, 64));
+  }
   g.tma_store = 1;
   return MS_OK;
 }

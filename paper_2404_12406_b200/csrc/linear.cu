@@ -86,13 +86,30 @@ LinPlan plan_gemm(int64_t rows, int64_t cols, int64_t red, bool b_mn, bool allow
   return p;
 }
 
+// 8 consecutive 16-bit outputs (one 16-byte store when vec, else the first left)
+template <typename T>
+__device__ __forceinline__ void store8(T* o, const float (&v)[8], bool vec, int left) {
+  if (vec) {
+    uint4 u;
+    u.x = pack2<T>(v[0], v[1]);
+    u.y = pack2<T>(v[2], v[3]);
+    u.z = pack2<T>(v[4], v[5]);
+    u.w = pack2<T>(v[6], v[7]);
+    *reinterpret_cast<uint4*>(o) = u;
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j < left) o[j] = IO<T>::cvt(v[j]);
+  }
+}
+
 // out[rows of tail tile i] = sum of its tail_splits fp32 partials (bias already
 // added by slice 0), rounded once to the output dtype
 template <typename T>
 __global__ void tail_finalize_kernel(const float* __restrict__ ws, T* __restrict__ out,
                                      int64_t ldc, int rows, int cols, int m_blocks, int n_blocks,
                                      int n_fastest, int full_tiles, int splits, int tile_rows,
-                                     int bn) {
+                                     int bn, T* __restrict__ act_out) {
   const int i = blockIdx.y;  // tail tile
   const int tile = full_tiles + i;
   const int mb = n_fastest ? (tile / n_blocks) % m_blocks : tile % m_blocks;
@@ -113,16 +130,13 @@ __global__ void tail_finalize_kernel(const float* __restrict__ ws, T* __restrict
       acc[0] += a.x; acc[1] += a.y; acc[2] += a.z; acc[3] += a.w;
       acc[4] += b.x; acc[5] += b.y; acc[6] += b.z; acc[7] += b.w;
     }
-    T* o = out + (int64_t)(m0 + r) * ldc + n0 + c;
-    if (n0 + c + 8 <= cols && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
-      uint4 u;
-      u.x = pack2<T>(acc[0], acc[1]);
-      u.y = pack2<T>(acc[2], acc[3]);
-      u.z = pack2<T>(acc[4], acc[5]);
-      u.w = pack2<T>(acc[6], acc[7]);
-      *reinterpret_cast<uint4*>(o) = u;
-    } else {
-      for (int j = 0; j < 8 && n0 + c + j < cols; ++j) o[j] = IO<T>::cvt(acc[j]);
+    const int64_t off = (int64_t)(m0 + r) * ldc + n0 + c;
+    const bool vec = n0 + c + 8 <= cols && ((reinterpret_cast<uintptr_t>(out + off) & 15) == 0);
+    store8(out + off, acc, vec, cols - n0 - c);
+    if (act_out) {  // fused GELU of the rounded pre-activation
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = gelu_erf(IO<T>::ld_val(IO<T>::cvt(acc[j])));
+      store8(act_out + off, acc, vec, cols - n0 - c);
     }
   }
 }
@@ -159,7 +173,8 @@ LinPlan plan_linear(int64_t M, int64_t N, int64_t K, int dt, int pass) {
 
 ms_status run_gemm(const LinPlan& p, int dt, int a_mn, int b_mn, const CUtensorMap& ta,
                    const CUtensorMap& tb, int64_t rows, int64_t cols, void* out, int64_t ldc,
-                   const void* bias, void* ws, size_t ws_bytes, cudaStream_t st) {
+                   const void* bias, void* ws, size_t ws_bytes, cudaStream_t st,
+                   void* act_out = nullptr) {
   TmapPack tm;
   tm.a[0] = ta;
   tm.a[1] = ta;
@@ -203,9 +218,11 @@ ms_status run_gemm(const LinPlan& p, int dt, int a_mn, int b_mn, const CUtensorM
     g.epi = EpiParams{ws, cols, MS_F32, 1, nullptr, 0};
     MS_TRY(launch_umma(p.bn, a_mn, b_mn, LOAD_GEMM, tm, g, st, p.cl));
     MS_CHECK_ARG(ldc == cols, MS_ERR_UNSUPPORTED, "linear: split-K needs dense output");
-    return f32_to(static_cast<const float*>(ws), out, dt, rows * cols, bias, cols, st);
+    MS_TRY(f32_to(static_cast<const float*>(ws), out, dt, rows * cols, bias, cols, st));
+    return act_out ? gelu_fwd(rows * cols, dt, out, act_out, st) : MS_OK;
   }
   g.epi = EpiParams{out, ldc, dt, 0, bias, dt};
+  g.epi.act_out = act_out;
   MS_TRY(setup_tma_store(tm, g, dt, out, rows, cols, ldc));
   if (p.tail_splits > 0) {
     MS_CHECK_ARG(ws && ws_bytes >= p.ws, MS_ERR_WORKSPACE,
@@ -223,11 +240,12 @@ ms_status run_gemm(const LinPlan& p, int dt, int a_mn, int b_mn, const CUtensorM
       tail_finalize_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(
           static_cast<const float*>(ws), static_cast<__nv_bfloat16*>(out), ldc, (int)rows,
           (int)cols, g.m_blocks, g.n_blocks, g.n_fastest, p.full_tiles, p.tail_splits, tile_rows,
-          p.bn);
+          p.bn, static_cast<__nv_bfloat16*>(act_out));
     else
       tail_finalize_kernel<__half><<<grid, 256, 0, st>>>(
           static_cast<const float*>(ws), static_cast<__half*>(out), ldc, (int)rows, (int)cols,
-          g.m_blocks, g.n_blocks, g.n_fastest, p.full_tiles, p.tail_splits, tile_rows, p.bn);
+          g.m_blocks, g.n_blocks, g.n_fastest, p.full_tiles, p.tail_splits, tile_rows, p.bn,
+          static_cast<__half*>(act_out));
     count_launch();
     return launch_status("tail_finalize_kernel");
   }
@@ -348,6 +366,26 @@ extern "C" ms_status ms_linear_fwd(int64_t M, int64_t N, int64_t K, int32_t dt, 
                     (const float*)bias, ws, ws_bytes, st);
   // y[m,n] = sum_k x[m,k] w[n,k]
   return simt_gemm(dt, (int)M, (int)N, (int)K, x, K, 1, w, 1, K, bias, y, N, st);
+}
+
+extern "C" ms_status ms_linear_gelu_fwd(int64_t M, int64_t N, int64_t K, int32_t dt,
+                                        const void* x, const void* w, const void* bias, void* pre,
+                                        void* y, void* ws, size_t ws_bytes, void* stream) {
+  MS_TRY(bind_device(y));
+  cudaStream_t st = (cudaStream_t)stream;
+  MS_CHECK_ARG(M >= 0 && N > 0 && K > 0, MS_ERR_SHAPE, "linear_gelu: bad shape");
+  MS_CHECK_ARG(pre != nullptr && y != nullptr && pre != y, MS_ERR_SHAPE,
+               "linear_gelu: needs distinct pre-activation and output buffers");
+  if (M == 0) return MS_OK;
+  LinPlan p = plan_linear(M, N, K, dt, 0);
+  if (p.tc && al16(x) && al16(w) && al16(pre) && al16(y)) {  // GELU in the GEMM epilogue
+    CUtensorMap ta, tb;
+    MS_TRY(make_tmap_2d(&ta, dt, x, K, M, K, BK, BM));
+    MS_TRY(make_tmap_2d(&tb, dt, w, K, N, K, BK, p.bn / p.cl));
+    return run_gemm(p, dt, 0, 0, ta, tb, M, N, pre, N, bias, ws, ws_bytes, st, y);
+  }
+  MS_TRY(ms_linear_fwd(M, N, K, dt, x, w, bias, pre, ws, ws_bytes, stream));
+  return gelu_fwd(M * N, dt, pre, y, st);
 }
 
 extern "C" ms_status ms_linear_dx(int64_t M, int64_t N, int64_t K, int32_t dt, const void* dy,

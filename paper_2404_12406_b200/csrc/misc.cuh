@@ -46,6 +46,10 @@ ms_status conv3x3_halo(int dt, int n, int h, int w, int wlayout, int transpose, 
                        const void* ks_var, const void* ks_w, int ks_pdt, float ks_eps,
                        cudaStream_t st, const uint8_t* keep_in = nullptr, int bn_post = 0);
 
+// elementwise GELU (erf form) and its VJP dx = g * gelu'(pre) (misc.cu)
+ms_status gelu_fwd(int64_t n, int dt, const void* x, void* y, cudaStream_t st);
+ms_status gelu_bwd(int64_t n, int dt, const void* g, const void* pre, void* dx, cudaStream_t st);
+
 inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 inline size_t align256(size_t v) { return (v + 255) & ~static_cast<size_t>(255); }
 

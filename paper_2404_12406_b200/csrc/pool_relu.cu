@@ -574,10 +574,94 @@ S4 strides_of(int layout, int64_t c, int64_t h, int64_t w) {
 
 bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+// ---------------------------------------------------------------- GELU
+// Elementwise GELU (erf form) and its VJP, the unfused halves of a Linear ->
+// GELU pair (the forward is normally fused into the GEMM epilogue).  The erf
+// makes them issue-bound rather than HBM-bound: GELU_UNR groups of 8 per
+// thread (loads first) keep the registers low enough for full occupancy.
+constexpr int GELU_UNR = 1;
+template <typename T, bool BWD>
+__global__ void __launch_bounds__(256) gelu_kernel(int64_t n, const T* __restrict__ a,
+                                                   const T* __restrict__ pre, T* __restrict__ y,
+                                                   bool vec) {
+  const int64_t groups = (n + 7) / 8;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t g0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g0 < groups;
+       g0 += stride * GELU_UNR) {
+    float v[GELU_UNR][8], x[GELU_UNR][8];
+#pragma unroll
+    for (int u = 0; u < GELU_UNR; ++u) {
+      const int64_t gi = g0 + u * stride;
+      if (gi >= groups) continue;
+      const bool full = gi * 8 + 8 <= n;
+      if (full) {
+        ld8<T>(a + gi * 8, v[u], vec);
+        if (BWD) ld8<T>(pre + gi * 8, x[u], vec);
+      } else {
+        for (int j = 0; j < 8; ++j) {
+          v[u][j] = gi * 8 + j < n ? IO<T>::ld(a + gi * 8 + j) : 0.f;
+          if (BWD) x[u][j] = gi * 8 + j < n ? IO<T>::ld(pre + gi * 8 + j) : 0.f;
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < GELU_UNR; ++u) {
+      const int64_t gi = g0 + u * stride;
+      if (gi >= groups) continue;
+#pragma unroll
+      if constexpr (BWD) {
+        gelu_grad_n<8>(x[u], v[u]);
+      } else {
+        gelu_n<8>(v[u]);  // the GEMM epilogue's evaluation (bit-identical to erff)
+      }
+      if (gi * 8 + 8 <= n) {
+        st8<T>(y + gi * 8, v[u], vec);
+      } else {
+        for (int j = 0; j < 8 && gi * 8 + j < n; ++j) y[gi * 8 + j] = IO<T>::cvt(v[u][j]);
+      }
+    }
+  }
+}
+
 }  // namespace
+
+ms_status gelu_fwd(int64_t n, int dt, const void* x, void* y, cudaStream_t st) {
+  if (n <= 0) return MS_OK;
+  const bool vec = al16(x) && al16(y);
+  MS_DT_DISPATCH(dt, (gelu_kernel<T, false><<<grid_for((n + 7) / 8), 256, 0, st>>>(
+                         n, (const T*)x, nullptr, (T*)y, vec)));
+  count_launch();
+  return launch_status("gelu_kernel");
+}
+
+ms_status gelu_bwd(int64_t n, int dt, const void* g, const void* pre, void* dx, cudaStream_t st) {
+  if (n <= 0) return MS_OK;
+  const bool vec = al16(g) && al16(pre) && al16(dx);
+  MS_DT_DISPATCH(dt, (gelu_kernel<T, true><<<grid_for((n + 7) / 8), 256, 0, st>>>(
+                         n, (const T*)g, (const T*)pre, (T*)dx, vec)));
+  count_launch();
+  return launch_status("gelu_bwd_kernel");
+}
+
 }  // namespace ms
 
 using namespace ms;
+
+extern "C" ms_status ms_gelu_fwd(int64_t numel, int32_t dt, const void* x, void* y,
+                                 void* stream) {
+  MS_CHECK_ARG(numel >= 0 && x && y, MS_ERR_SHAPE, "gelu: bad arguments");
+  if (numel == 0) return MS_OK;
+  MS_TRY(bind_device(y));
+  return gelu_fwd(numel, dt, x, y, (cudaStream_t)stream);
+}
+
+extern "C" ms_status ms_gelu_bwd(int64_t numel, int32_t dt, const void* g, const void* pre,
+                                 void* dx, void* stream) {
+  MS_CHECK_ARG(numel >= 0 && g && pre && dx, MS_ERR_SHAPE, "gelu bwd: bad arguments");
+  if (numel == 0) return MS_OK;
+  MS_TRY(bind_device(dx));
+  return gelu_bwd(numel, dt, g, pre, dx, (cudaStream_t)stream);
+}
 
 extern "C" ms_status ms_relu_fwd(int64_t numel, int32_t dt, const void* x, void* y,
                                  void* mask_or_null, void* stream) {

@@ -184,6 +184,48 @@ Tensor linear_dw(const Tensor& x, const Tensor& g) {
   return dw;
 }
 
+// pre = x·wᵀ + b and y = gelu(pre) in one GEMM (GELU in the epilogue)
+std::tuple<Tensor, Tensor> linear_gelu_fwd(const Tensor& x, const Tensor& w, const OptT& b) {
+  const int64_t N = w.size(0), K = w.size(1);
+  TORCH_CHECK(x.size(-1) == K, "linear_gelu: input last dim ", x.size(-1), " != in_features ", K);
+  auto shape = x.sizes().vec();
+  shape.back() = N;
+  Tensor pre = at::empty(shape, x.options()), y = at::empty(shape, x.options());
+  if (x.is_meta()) return {pre, y};
+  Tensor x2 = x.reshape({-1, K}).contiguous(), wc = w.contiguous();
+  Tensor bb = as_dtype(b, x.scalar_type());
+  const int64_t M = x2.size(0);
+  const int dt = dtc(x.scalar_type());
+  Launch L(x);
+  const size_t nb = ms_linear_workspace(M, N, K, dt, 0);
+  Tensor ws = wsp(nb, x);
+  ok(ms_linear_gelu_fwd(M, N, K, dt, cp(x2), cp(wc), cp(bb), mp(pre), mp(y), mp(ws), nb,
+                        L.stream),
+     "linear_gelu_fwd");
+  return {pre, y};
+}
+
+Tensor gelu_fwd(const Tensor& x) {
+  Tensor xc = x.contiguous();
+  Tensor y = at::empty_like(xc);
+  if (x.is_meta()) return y;
+  Launch L(x);
+  ok(ms_gelu_fwd(xc.numel(), dtc(x.scalar_type()), cp(xc), mp(y), L.stream), "gelu_fwd");
+  return y;
+}
+
+// dx = g * gelu'(pre)
+Tensor gelu_bwd(const Tensor& g, const Tensor& pre) {
+  TORCH_CHECK(g.sizes() == pre.sizes() && g.scalar_type() == pre.scalar_type(),
+              "gelu_bwd: gradient and pre-activation differ in shape or dtype");
+  Tensor gc = g.contiguous(), pc = pre.contiguous();
+  Tensor dx = at::empty_like(gc);
+  if (g.is_meta()) return dx;
+  Launch L(g);
+  ok(ms_gelu_bwd(gc.numel(), dtc(g.scalar_type()), cp(gc), cp(pc), mp(dx), L.stream), "gelu_bwd");
+  return dx;
+}
+
 // db[c] = sum_r g[r, c] over g viewed [rows, cols]
 Tensor bias_grad(const Tensor& g, int64_t cols) {
   Tensor db = at::empty({cols}, g.options());
@@ -678,6 +720,51 @@ struct LinearFn : public torch::autograd::Function<LinearFn> {
   }
 };
 
+// Linear -> GELU as one node: the saved set is the union of the two layers'
+// rules -- X iff W needs a grad, W iff X does (rules.py:133-141), and the GELU's
+// input (the pre-activation), which its VJP reads under every policy
+struct LinearGeluFn : public torch::autograd::Function<LinearGeluFn> {
+  static Tensor forward(torch::autograd::AutogradContext* ctx, const Tensor& x, const Tensor& w,
+                        const OptT& b) {
+    const bool x_rg = x.requires_grad(), w_rg = w.requires_grad();
+    static auto fwd = op_handle<std::tuple<Tensor, Tensor>(const Tensor&, const Tensor&,
+                                                           const OptT&)>("memsave::linear_gelu_fwd");
+    Tensor pre, y;
+    {
+      at::AutoDispatchBelowADInplaceOrView guard;
+      std::tie(pre, y) = fwd.call(x, w, b);
+    }
+    ctx->save_for_backward({w_rg ? x : Tensor(), x_rg ? w : Tensor(), pre});
+    ctx->saved_data["x_shape"] = x.sizes().vec();
+    ctx->saved_data["has_b"] = has(b);
+    return y;
+  }
+  static torch::autograd::variable_list backward(torch::autograd::AutogradContext* ctx,
+                                                 torch::autograd::variable_list grads) {
+    static auto gb_op = op_handle<Tensor(const Tensor&, const Tensor&)>("memsave::gelu_bwd");
+    static auto dx_op =
+        op_handle<Tensor(const Tensor&, const Tensor&, IntArrayRef)>("memsave::linear_dx");
+    static auto dw_op = op_handle<Tensor(const Tensor&, const Tensor&)>("memsave::linear_dw");
+    static auto db_op = op_handle<Tensor(const Tensor&, int64_t)>("memsave::bias_grad");
+    const auto saved = ctx->get_saved_variables();
+    const Tensor gz = gb_op.call(grads[0].contiguous(), saved[2]);  // dL/d pre
+    Tensor dx, dw, db;
+    if (ctx->saved_data["has_b"].toBool() && ctx->needs_input_grad(2))
+      db = db_op.call(gz, gz.size(-1));
+    if (ctx->needs_input_grad(0)) {
+      TORCH_CHECK(saved[1].defined(), "MissingSavedValue: linear dX needs 'w' but the storage "
+                                      "rule did not keep it");
+      dx = dx_op.call(gz, saved[1], ctx->saved_data["x_shape"].toIntVector());
+    }
+    if (ctx->needs_input_grad(1)) {
+      TORCH_CHECK(saved[0].defined(), "MissingSavedValue: linear dW needs 'x' but the storage "
+                                      "rule did not keep it");
+      dw = dw_op.call(saved[0], gz);
+    }
+    return {dx, dw, db};
+  }
+};
+
 void check_linear(const Tensor& x, const Tensor& w, const OptT& b) {
   for (const Tensor* t : {&x, &w, has(b) ? &*b : nullptr}) {
     if (!t) continue;
@@ -700,12 +787,26 @@ Tensor linear_noautograd(const Tensor& x, const Tensor& w, const OptT& b) {
   return linear_fwd(x, w, b);
 }
 
+Tensor linear_gelu_autograd(const Tensor& x, const Tensor& w, const OptT& b) {
+  check_linear(x, w, b);
+  return LinearGeluFn::apply(x, w, b);
+}
+
+Tensor linear_gelu_noautograd(const Tensor& x, const Tensor& w, const OptT& b) {
+  check_linear(x, w, b);
+  return std::get<1>(linear_gelu_fwd(x, w, b));
+}
+
 }  // namespace
 
 TORCH_LIBRARY(memsave, m) {
   m.def("linear(Tensor x, Tensor w, Tensor? b) -> Tensor");
   m.def("linear_fwd(Tensor x, Tensor w, Tensor? b) -> Tensor");
   m.def("linear_dx(Tensor g, Tensor w, int[] x_shape) -> Tensor");
+  m.def("linear_gelu(Tensor x, Tensor w, Tensor? b) -> Tensor");
+  m.def("linear_gelu_fwd(Tensor x, Tensor w, Tensor? b) -> (Tensor, Tensor)");
+  m.def("gelu_fwd(Tensor x) -> Tensor");
+  m.def("gelu_bwd(Tensor g, Tensor pre) -> Tensor");
   m.def("linear_dw(Tensor x, Tensor g) -> Tensor");
   m.def("bias_grad(Tensor g, int cols) -> Tensor");
   m.def("conv2d_fwd(Tensor x, Tensor w, Tensor? b, int[] stride, int[] padding, int layout, "
@@ -759,6 +860,9 @@ TORCH_LIBRARY(memsave, m) {
 #define MS_IMPLS(m)                                          \
   m.impl("linear_fwd", &linear_fwd);                         \
   m.impl("linear_dx", &linear_dx);                           \
+  m.impl("linear_gelu_fwd", &linear_gelu_fwd);               \
+  m.impl("gelu_fwd", &gelu_fwd);                             \
+  m.impl("gelu_bwd", &gelu_bwd);                             \
   m.impl("linear_dw", &linear_dw);                           \
   m.impl("bias_grad", &bias_grad);                           \
   m.impl("conv2d_fwd", &conv2d_fwd);                         \
@@ -789,10 +893,15 @@ TORCH_LIBRARY(memsave, m) {
 TORCH_LIBRARY_IMPL(memsave, CUDA, m) {
   MS_IMPLS(m);
   m.impl("linear", &linear_noautograd);
+  m.impl("linear_gelu", &linear_gelu_noautograd);
 }
 TORCH_LIBRARY_IMPL(memsave, Meta, m) {
   MS_IMPLS(m);
   m.impl("linear", &linear_noautograd);
+  m.impl("linear_gelu", &linear_gelu_noautograd);
 }
-TORCH_LIBRARY_IMPL(memsave, Autograd, m) { m.impl("linear", &linear_autograd); }
+TORCH_LIBRARY_IMPL(memsave, Autograd, m) {
+  m.impl("linear", &linear_autograd);
+  m.impl("linear_gelu", &linear_gelu_autograd);
+}
 // CPU tensors reach the autograd kernel too (then fail loudly in check_linear)

@@ -101,6 +101,10 @@ struct EpiParams {
   // (storage order), then v *= s[col] when bn_post (bn = the producer's BN)
   const uint8_t* keep_in;
   int bn_post;
+  // fused GELU (Linear -> GELU): out keeps the pre-activation (what the GELU's
+  // backward reads) and act_out receives gelu(pre) of the ROUNDED pre, exactly
+  // what a separate gelu launch would read and write (same dtype / pitch)
+  void* act_out;
 };
 
 struct GemmArgs {
@@ -122,7 +126,8 @@ struct GemmArgs {
   // N-blocks fastest (they share A: A streams from HBM once when B fits in L2)
   int n_fastest;
   // profiling switch (MS_GEMM_DBG, GEMM mode only): bit 0 drops the epilogue's
-  // stores, bit 1 also its TMEM loads -- isolates the main loop's feed rate
+  // stores, bit 1 also its TMEM loads -- isolates the main loop's feed rate;
+  // fused GELU: bit 2 skips its arithmetic, bit 3 its second output
   int dbg;
   // LOAD_CONV_FPROP_ROWSEG with 8-channel stride-1 rows: stage each input row
   // segment once ([136 px][8 ch], 16 B per pixel, no swizzle) and read tap pairs
@@ -139,7 +144,36 @@ struct TmapPack {
   CUtensorMap a[4];  // A operand (per dgrad phase; a[0] otherwise)
   CUtensorMap b;     // B operand
   CUtensorMap c;     // output (GEMM / conv fwd, 16-bit): box {32 cols, 32 rows}, SW64
+  CUtensorMap c2;    // second output of a fused GELU (EpiParams::act_out), as c
 };
+
+// 32 consecutive 16-bit outputs of one row from fp32 (vector stores when the
+// chunk is whole and 16-byte aligned, else the first `left` elements)
+__device__ __forceinline__ void store_row32(void* out, int dt, int64_t off, const float (&v)[32],
+                                            bool full, int left) {
+  uint16_t* o = static_cast<uint16_t*>(out) + off;
+  if (full && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
+    uint32_t p[16];
+    if (dt == MS_BF16) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) p[j] = pack2<__nv_bfloat16>(v[2 * j], v[2 * j + 1]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) p[j] = pack2<__half>(v[2 * j], v[2 * j + 1]);
+    }
+#pragma unroll
+    for (int j = 0; j < 16; j += 4)
+      *reinterpret_cast<uint4*>(o + 2 * j) = make_uint4(p[j], p[j + 1], p[j + 2], p[j + 3]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)  // constant indices: v stays in registers
+      if (j < left) store_from_float(out, dt, off + j, v[j]);
+  }
+}
+
+#ifndef GELU_ILP
+#define GELU_ILP 4  // erf evaluations interleaved by the fused GELU epilogue
+#endif
 
 struct TileInfo {
   int m0;            // first output row of the tile (phase-local for dgrad; row id
@@ -979,41 +1013,76 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
               }
             }
           }
+          // fused GELU: after the pre-activation is stored, v becomes gelu(v rounded)
+          // in place (no second array: the 32 independent evaluations keep the
+          // registers to interleave) and is stored to act_out the same way
+          const bool act = e.act_out != nullptr && !(g.dbg & 8);
+          auto to_act = [&]() {
+            if (g.dbg & 4) return;
+            // dtype branch outside the element loop: branch-free bodies let the
+            // compiler interleave the 32 independent erf evaluations
+            if (e.out_dtype == MS_BF16) {
+              // round to bf16 (nearest-even) with integer ops instead of the
+              // quarter-rate conversion unit, which MUFU.EX2 also needs
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                const uint32_t b = __float_as_uint(v[j]);
+                v[j] = __uint_as_float((b + 0x7fffu + ((b >> 16) & 1u)) & 0xffff0000u);
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = __half2float(__float2half_rn(v[j]));
+            }
+#pragma unroll
+            for (int j0 = 0; j0 < 32; j0 += GELU_ILP) {
+              float q[GELU_ILP];
+#pragma unroll
+              for (int k = 0; k < GELU_ILP; ++k) q[k] = v[j0 + k];
+              gelu_n<GELU_ILP>(q);
+#pragma unroll
+              for (int k = 0; k < GELU_ILP; ++k) v[j0 + k] = q[k];
+            }
+          };
           if (!valid && !tma_st) continue;
           if constexpr (Cfg::CAN_TMA_STORE) {
             if (tma_st) {
               // pack, stage this warp's 32 rows x 32 columns (64-byte rows, 64B swizzle),
               // and let one lane store the chunk with TMA (clips the M / N tails)
-              uint32_t p[16];
-              if (e.out_dtype == MS_BF16) {
-#pragma unroll
-                for (int j = 0; j < 16; ++j) p[j] = pack2<__nv_bfloat16>(v[2 * j], v[2 * j + 1]);
-              } else {
-#pragma unroll
-                for (int j = 0; j < 16; ++j) p[j] = pack2<__half>(v[2 * j], v[2 * j + 1]);
-              }
               const int ew = static_cast<int>(warp) - 2;
-              uint8_t* stg = staging + (ew * Cfg::STG_BUFS + (stg_count % Cfg::STG_BUFS)) * 2048;
               static_assert(Cfg::STG_BUFS >= 2, "staging ring");
-              // the store issued STG_BUFS chunks ago has finished reading this buffer
-              if (lane == 0) bulk_wait_read<Cfg::STG_BUFS - 1>();
-              __syncwarp();
-              const int rw = static_cast<int>(lane);
+#pragma unroll 1
+              for (int pass = 0; pass < (act ? 2 : 1); ++pass) {
+                if (pass == 1) to_act();
+                uint32_t p[16];
+                if (e.out_dtype == MS_BF16) {
 #pragma unroll
-              for (int q = 0; q < 4; ++q)
-                *reinterpret_cast<uint4*>(stg + rw * 64 + ((q ^ ((rw >> 1) & 3)) << 4)) =
-                    make_uint4(p[4 * q], p[4 * q + 1], p[4 * q + 2], p[4 * q + 3]);
-              fence_proxy_async_smem();
-              __syncwarp();
-              if (lane == 0) {
-                if constexpr (MODE == LOAD_CONV_FPROP_ROWSEG)  // [row][pixel][ch]: clips q >= Q
-                  tma_store_3d(&tm.c, smem_u32(stg), nc, ti.tap * BM + static_cast<int>(quarter) * 32,
-                               ti.m0);
-                else
-                  tma_store_2d(&tm.c, smem_u32(stg), nc, ti.m0 + static_cast<int>(quarter) * 32);
-                bulk_commit();
+                  for (int j = 0; j < 16; ++j) p[j] = pack2<__nv_bfloat16>(v[2 * j], v[2 * j + 1]);
+                } else {
+#pragma unroll
+                  for (int j = 0; j < 16; ++j) p[j] = pack2<__half>(v[2 * j], v[2 * j + 1]);
+                }
+                uint8_t* stg = staging + (ew * Cfg::STG_BUFS + (stg_count % Cfg::STG_BUFS)) * 2048;
+                // the store issued STG_BUFS chunks ago has finished reading this buffer
+                if (lane == 0) bulk_wait_read<Cfg::STG_BUFS - 1>();
+                __syncwarp();
+                const int rw = static_cast<int>(lane);
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                  *reinterpret_cast<uint4*>(stg + rw * 64 + ((q ^ ((rw >> 1) & 3)) << 4)) =
+                      make_uint4(p[4 * q], p[4 * q + 1], p[4 * q + 2], p[4 * q + 3]);
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                  if constexpr (MODE == LOAD_CONV_FPROP_ROWSEG)  // [row][pixel][ch]: clips q >= Q
+                    tma_store_3d(&tm.c, smem_u32(stg), nc,
+                                 ti.tap * BM + static_cast<int>(quarter) * 32, ti.m0);
+                  else
+                    tma_store_2d(pass ? &tm.c2 : &tm.c, smem_u32(stg), nc,
+                                 ti.m0 + static_cast<int>(quarter) * 32);
+                  bulk_commit();
+                }
+                ++stg_count;
               }
-              ++stg_count;
               continue;
             }
           }
@@ -1039,23 +1108,10 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
                 if (nc + j < ncols) o[j] = v[j];
             }
           } else {
-            uint16_t* o = static_cast<uint16_t*>(e.out) + off;
-            if (full && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
-              uint32_t p[16];
-              if (e.out_dtype == MS_BF16) {
-#pragma unroll
-                for (int j = 0; j < 16; ++j) p[j] = pack2<__nv_bfloat16>(v[2 * j], v[2 * j + 1]);
-              } else {
-#pragma unroll
-                for (int j = 0; j < 16; ++j) p[j] = pack2<__half>(v[2 * j], v[2 * j + 1]);
-              }
-#pragma unroll
-              for (int j = 0; j < 16; j += 4)
-                *reinterpret_cast<uint4*>(o + 2 * j) =
-                    make_uint4(p[j], p[j + 1], p[j + 2], p[j + 3]);
-            } else {
-              for (int j = 0; j < 32; ++j)
-                if (nc + j < ncols) store_from_float(e.out, e.out_dtype, off + j, v[j]);
+            store_row32(e.out, e.out_dtype, off, v, full, ncols - nc);
+            if (act) {
+              to_act();
+              store_row32(e.act_out, e.out_dtype, off, v, full, ncols - nc);
             }
           }
         }

@@ -77,6 +77,18 @@ def linear(x: torch.Tensor, weight: torch.Tensor, bias: torch.Tensor | None = No
     return _ops().linear(x, weight, bias)
 
 
+def linear_gelu(x: torch.Tensor, weight: torch.Tensor, bias: torch.Tensor | None = None):
+    """``gelu(linear(x))`` (erf GELU, ``approximate='none'``) as one node.
+
+    ``torch.ops.memsave.linear_gelu`` (csrc/torch_ops.cpp, ``LinearGeluFn``)
+    writes the pre-activation and the GELU output from the same GEMM epilogue
+    instead of a second pass over the pre-activation.  The saved set is the
+    union of the two layers' rules: X iff W requires a gradient, W iff X does
+    (rules.py:133-141), and the pre-activation (the GELU's input, which its VJP
+    reads).  Values equal ``gelu(linear(x))`` computed op by op."""
+    return _ops().linear_gelu(x, weight, bias)
+
+
 # =============================================================== conv2d
 def _pair(v):
     if isinstance(v, (tuple, list)):

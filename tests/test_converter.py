@@ -85,3 +85,75 @@ def test_cpu_tensors_fail_loudly():
     m = MemSaveLinear(4, 3)
     with pytest.raises(RuntimeError, match="no CPU path"):
         m(torch.randn(2, 4))
+
+
+class _Act(nn.Module):  # an activation wrapper that fx traces through (HF style)
+    def forward(self, x):
+        return nn.functional.gelu(x)
+
+
+class _Intermediate(nn.Module):
+    def __init__(self):
+        super().__init__()
+        self.dense = nn.Linear(8, 16)
+        self.act = _Act()
+
+    def forward(self, h):
+        return self.act(self.dense(h))
+
+
+class _Block(nn.Module):
+    def __init__(self):
+        super().__init__()
+        self.inter = _Intermediate()
+        self.out = nn.Linear(16, 8)
+        self.tanh_mlp = nn.Sequential(nn.Linear(8, 8), nn.GELU(approximate="tanh"))
+
+    def forward(self, x, mask=None):  # optional argument: not traced as a whole
+        if mask is not None:
+            x = x * mask
+        return self.out(self.inter(x)) + self.tanh_mlp(x)
+
+
+def test_fuse_linear_gelu_per_module():
+    from paper_2404_12406_b200.nn import fuse_linear_gelu
+    torch.manual_seed(0)
+    net = _Block()
+    sd = {k: v.clone() for k, v in net.state_dict().items()}
+    convert_to_memory_saving(net, fuse=True)
+    assert not isinstance(net.inter, torch.fx.GraphModule)  # opt-in pass
+    fuse_linear_gelu(net)
+    code = net.inter.code
+    assert "_gelu_layer" in code and "gelu(" not in code.replace("_gelu_layer", "")
+    # the tanh GELU and the module with an optional argument are left alone
+    assert type(net.tanh_mlp) is nn.Sequential and isinstance(net.tanh_mlp[1], nn.GELU)
+    assert not isinstance(net, torch.fx.GraphModule)
+    assert net.state_dict().keys() == sd.keys()
+    assert all(torch.equal(net.state_dict()[k], v) for k, v in sd.items())
+    # idempotent: a second pass finds nothing more
+    assert fuse_linear_gelu(net) is net
+    # shapes and gradients flow on meta
+    mnet = _Block().to("meta")
+    fuse_linear_gelu(convert_to_memory_saving(mnet))
+    x = torch.empty(4, 8, device="meta", requires_grad=True)
+    mnet(x).sum().backward()
+    assert x.grad.shape == x.shape and mnet.inter.dense.weight.grad.shape == (16, 8)
+
+
+def test_fuse_linear_gelu_bert_intermediate_blocks():
+    from transformers import BertConfig, BertForSequenceClassification
+
+    from paper_2404_12406_b200.nn import fuse_linear_gelu
+    cfg = BertConfig(num_hidden_layers=2, hidden_size=64, num_attention_heads=2,
+                     intermediate_size=128, attn_implementation="sdpa")
+    with torch.device("meta"):
+        m = BertForSequenceClassification(cfg)
+    keys = list(m.state_dict().keys())
+    m = fuse_linear_gelu(convert_to_memory_saving(m, fuse=True))
+    for layer in m.bert.encoder.layer:
+        assert isinstance(layer.intermediate, torch.fx.GraphModule)
+        assert "_gelu_layer" in layer.intermediate.code
+        assert type(layer.output.dense) is MemSaveLinear
+    assert list(m.state_dict().keys()) == keys
+    ids = torch.zeros(2, 16, dtype=torch.long, device="meta")
+    m(input_ids=ids).logits.sum().backward()

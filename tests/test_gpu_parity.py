@@ -265,6 +265,80 @@ def test_linear_skinny_head(shape, dt):
     _close(b.grad, oracle.linear_db(gq), dt, "db")
 
 
+@pytest.mark.parametrize("dt", ["bf16", "fp16", "f32"])
+def test_gelu_kernels(dt):
+    """ms_gelu_fwd / ms_gelu_bwd against the f64 definition (1 ulp of the
+    storage type) and against torch's own gelu kernels (same fp32 formula)."""
+    rng = np.random.default_rng(5)
+    n = 1 << 20 | 13  # ragged tail
+    x, xq = _q(rng.standard_normal(n) * 3, dt)
+    g, gq = _q(rng.standard_normal(n), dt)
+    MF._ops()  # loads the op library
+    ops = torch.ops.memsave
+    y = ops.gelu_fwd(x)
+    dx = ops.gelu_bwd(g, x)
+    _close(y, oracle.gelu_fwd(xq), dt, "gelu y")
+    _close(dx, oracle.gelu_bwd(gq, xq), dt, "gelu dx")
+    ty = torch.nn.functional.gelu(x)
+    tdx = torch.ops.aten.gelu_backward(g, x)
+    for ours, stock in ((y, ty), (dx, tdx)):
+        same = (ours == stock).float().mean().item()
+        print(dt, "bit-identical to torch:", same)
+        torch.testing.assert_close(ours, stock, rtol=2 ** -7 if dt != "f32" else 1e-6,
+                                   atol=1e-6)
+    # the forward's erf (interleaved restatement of CUDA's erff) is bit-identical
+    # to torch's gelu over every 16-bit input and 16M random fp32 inputs
+    if dt == "f32":
+        xs = torch.cat([torch.arange(1 << 16, dtype=torch.int32).to(torch.int16)
+                        .view(torch.bfloat16).float().to(DEV),
+                        torch.randn(1 << 24, device=DEV) * 4])
+    else:
+        xs = torch.arange(1 << 16, dtype=torch.int32).to(torch.int16).view(TDT[dt]).to(DEV)
+    ys, ts = ops.gelu_fwd(xs), torch.nn.functional.gelu(xs)
+    both_nan = torch.isnan(ys) & torch.isnan(ts)
+    assert bool(((ys == ts) | both_nan).all()), int((~((ys == ts) | both_nan)).sum())
+
+
+LINEAR_GELU_CASES = [((4096,), 768, 3072), ((3, 100), 200, 72), ((2, 64), 96, 40)]
+
+
+@pytest.mark.parametrize("dt", ["bf16", "f32"])
+@pytest.mark.parametrize("case", LINEAR_GELU_CASES)
+def test_linear_gelu(case, dt):
+    """Linear -> GELU in one node: the pre-activation equals the Linear's, the
+    output is the GELU of the stored pre-activation (GEMM epilogue on the
+    tcgen05 path: one launch), and the VJPs match the f64 composition."""
+    lead, fin, fout = case
+    rng = np.random.default_rng(fin * 3 + fout)
+    x, xq = _q(rng.standard_normal(lead + (fin,)), dt)
+    w, wq = _q(rng.standard_normal((fout, fin)) / np.sqrt(fin), dt)
+    b, bq = _q(rng.standard_normal(fout), dt)
+    g, gq = _q(rng.standard_normal(lead + (fout,)), dt)
+    MF._ops()
+    pre, y0 = torch.ops.memsave.linear_gelu_fwd(x, w, b)
+    c0, u0 = launch_count(), launch_stats()["umma"]
+    pre2, _ = torch.ops.memsave.linear_gelu_fwd(x, w, b)
+    if dt == "bf16" and fin % 8 == 0 and fout % 8 == 0:
+        assert launch_count() - c0 == 1 and launch_stats()["umma"] - u0 == 1
+    assert torch.equal(pre, pre2)
+    assert torch.equal(pre, MF.linear(x, w, b))  # the same GEMM, bit for bit
+    _close(pre, oracle.linear_fwd(xq, wq, bq), dt, "pre")
+    pq = pre.double().cpu().numpy()
+    _close(y0, oracle.gelu_fwd(pq), dt, "y = gelu(pre)")
+    assert torch.equal(y0, torch.ops.memsave.gelu_fwd(pre))  # epilogue == elementwise kernel
+    for t in (x, w, b):
+        t.requires_grad_(True)
+    y = MF.linear_gelu(x, w, b)
+    assert torch.equal(y.detach(), y0)
+    y.backward(g)
+    gz = torch.ops.memsave.gelu_bwd(g, pre)
+    _close(gz, oracle.gelu_bwd(gq, pq), dt, "dL/dpre")
+    zq = gz.double().cpu().numpy()
+    _close(x.grad, oracle.linear_dx(zq, wq), dt, "dx")
+    _close(w.grad, oracle.linear_dw(xq, zq), dt, "dw")
+    _close(b.grad, oracle.linear_db(zq), dt, "db")
+
+
 def test_linear_golden(linbn_golden):
     g = linbn_golden
     for case in ("lin_small", "lin_3d"):

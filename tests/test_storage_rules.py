@@ -247,3 +247,20 @@ def test_linear_without_bias_backward_on_meta(x_rg, w_rg):
         assert x.grad.shape == x.shape
     if w_rg:
         assert w.grad.shape == w.shape
+
+
+@pytest.mark.parametrize("x_rg,w_rg,b_rg", FLAGS)
+def test_linear_gelu_saved_set(rules_golden, x_rg, w_rg, b_rg):
+    """The fused Linear -> GELU node saves the Linear's rule set plus the GELU's
+    input (the pre-activation, its VJP's only need), and nothing else."""
+    x, w, b = _make((6, 5, 7), x_rg), _make((3, 7), w_rg), _make((3,), b_rg)
+    out, roles = _run(MF.linear_gelu, (x, w, b), {(6, 5, 7): "x", (3, 7): "w", (6, 5, 3): "pre"})
+    want = _golden_saves(rules_golden, "linear", x_rg, w_rg, b_rg)
+    if x_rg or w_rg or b_rg:
+        want = sorted(want + ["pre"])
+    assert roles == want
+    assert out.shape == (6, 5, 3)
+    if out.requires_grad:
+        out.sum().backward()
+        assert (x.grad is not None) == x_rg and (w.grad is not None) == w_rg
+        assert (b.grad is not None) == b_rg
