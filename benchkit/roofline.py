@@ -42,6 +42,12 @@ def _conv_work(xs, ws, stride, pad, es):
     return flops, byts, ys
 
 
+# ops whose backward is a C++ autograd node: their Python-level call is the
+# forward, recorded under the forward kernel op's name
+_AUTOGRAD_FWD = {"linear": "linear_fwd", "linear_gelu": "linear_gelu_fwd",
+                 "linear_dropout_add": "linear_dropout_add_fwd"}
+
+
 def work_of(name, args):
     """(flops, bytes, geometry) of one op call, from its arguments."""
     def es_of(t):
@@ -54,8 +60,14 @@ def work_of(name, args):
         M = int(math.prod(xs)) // K
         n = int(ndx) + int(ndw)
         return 2.0 * M * N * K * n, es * n * (M * K + N * K + M * N), dict(M=M, N=N, K=K)
-    if name == "linear":
-        name = "linear_fwd"
+    name = _AUTOGRAD_FWD.get(name, name)
+    if name in ("linear_gelu_fwd", "linear_dropout_add_fwd"):
+        x, w = a[0], a[1]
+        N, K = w.shape
+        M = x.numel() // K
+        es = es_of(x)
+        # + the GELU's second output / the residual read
+        return 2.0 * M * N * K, es * (M * K + N * K + 2 * M * N), dict(M=M, N=N, K=K)
     if name in ("linear_fwd", "linear_dx", "linear_dw"):
         if name == "linear_fwd":
             x, w = a[0], a[1]
@@ -133,6 +145,10 @@ def work_of(name, args):
         nx = _numel(xs)
         extra = nx / 8.0 if name == "maxpool2d_relu_bwd" else 0
         return float(nx), es * (n + nx) + n + extra, dict(x=list(xs))
+    if name == "gelu_fwd":
+        return 20.0 * n, 2.0 * es * n, dict(shape=list(t0.shape))
+    if name == "gelu_bwd":
+        return 30.0 * n, 3.0 * es * n, dict(shape=list(t0.shape))
     if name in ("dropout_fwd", "dropout_fwd_", "dropout_bwd"):
         return float(n), 2.0 * es * n, dict(shape=list(t0.shape))
     if name == "layernorm_fwd":
@@ -146,9 +162,10 @@ def work_of(name, args):
 
 class _Recorder:
     """Brackets every torch.ops.memsave call with CUDA events.  memsave::linear
-    runs its backward in C++ (csrc/torch_ops.cpp), invisible to this wrapper:
-    its forward call is timed as ``linear_fwd``, and hooks on the output's
-    grad_fn time the kernel ops its backward node dispatches."""
+    (and the fused linear_gelu / linear_dropout_add) run their backward in C++
+    (csrc/torch_ops.cpp), invisible to this wrapper: the forward call is timed
+    under the forward kernel op's name, and hooks on the output's grad_fn time
+    the kernel ops its backward node dispatches."""
 
     def __init__(self, real):
         self._real = real
@@ -164,9 +181,8 @@ class _Recorder:
             out = fn(*args)
             e.record()
             flops, byts, geom = work_of(name, args)
-            self.calls.append(("linear_fwd" if name == "linear" else name, s, e, flops, byts,
-                               geom))
-            if name == "linear" and out.grad_fn is not None:
+            self.calls.append((_AUTOGRAD_FWD.get(name, name), s, e, flops, byts, geom))
+            if name in _AUTOGRAD_FWD and out.grad_fn is not None:
                 self._hook_backward(out, args)
             return out
         return wrapped

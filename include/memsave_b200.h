@@ -110,6 +110,17 @@ MS_API ms_status ms_linear_fwd(int64_t M, int64_t N, int64_t K, int32_t dtype, c
 MS_API ms_status ms_linear_gelu_fwd(int64_t M, int64_t N, int64_t K, int32_t dtype,
                              const void* x, const void* w, const void* bias, void* pre,
                              void* y, void* ws, size_t ws_bytes, void* stream);
+/* Linear -> dropout -> + residual (a transformer block's output projection)
+ * in one call: y = r + dropout_p(x·wᵀ + b), each intermediate rounded to
+ * `dtype` as the separate launches round it, the mask drawn exactly as
+ * ms_dropout_fwd(numel = M*N, seed, stream_id, p, generator) draws it (so
+ * ms_dropout_bwd replays it for the VJP).  p = 0: y = r + (x·wᵀ + b).  r: [M, N]
+ * like y (y must not alias r).  ws as ms_linear_workspace(M, N, K, dtype, 0).  */
+MS_API ms_status ms_linear_dropout_add_fwd(int64_t M, int64_t N, int64_t K, int32_t dtype,
+                                    const void* x, const void* w, const void* bias,
+                                    const void* r, double p, uint64_t seed, uint64_t stream_id,
+                                    int32_t generator, void* y, void* ws, size_t ws_bytes,
+                                    void* stream);
 MS_API ms_status ms_linear_dx(int64_t M, int64_t N, int64_t K, int32_t dtype, const void* dy,
                        const void* w, void* dx, void* ws, size_t ws_bytes, void* stream);
 MS_API ms_status ms_linear_dw(int64_t M, int64_t N, int64_t K, int32_t dtype, const void* x,

@@ -12,6 +12,7 @@ from paper_2404_12406_b200.nn import (  # noqa: F401
     MemSaveReLU,
     convert_to_memory_saving,
     fuse_conv_bn_relu,
+    fuse_linear_dropout_add,
     fuse_linear_gelu,
 )
 from paper_2404_12406_b200.nn import __all__  # noqa: F401

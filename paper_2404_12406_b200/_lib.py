@@ -56,6 +56,9 @@ SIGNATURES = {
     "ms_linear_fwd": (_c_i32, [_c_i64, _c_i64, _c_i64, _c_i32, _vp, _vp, _vp, _vp, _vp, _c_sz, _vp]),
     "ms_linear_gelu_fwd": (_c_i32, [_c_i64, _c_i64, _c_i64, _c_i32, _vp, _vp, _vp, _vp, _vp, _vp,
                                     _c_sz, _vp]),
+    "ms_linear_dropout_add_fwd": (_c_i32, [_c_i64, _c_i64, _c_i64, _c_i32, _vp, _vp, _vp, _vp,
+                                           ctypes.c_double, ctypes.c_uint64, ctypes.c_uint64,
+                                           _c_i32, _vp, _vp, _c_sz, _vp]),
     "ms_gelu_fwd": (_c_i32, [_c_i64, _c_i32, _vp, _vp, _vp]),
     "ms_gelu_bwd": (_c_i32, [_c_i64, _c_i32, _vp, _vp, _vp, _vp]),
     "ms_linear_dx": (_c_i32, [_c_i64, _c_i64, _c_i64, _c_i32, _vp, _vp, _vp, _vp, _c_sz, _vp]),

@@ -29,6 +29,7 @@
 // One warp per row; rows up to 2048 elements live in registers (8 per lane per
 // 256-column slab), longer or unaligned rows take a block-per-row loop.
 #include "misc.cuh"
+#include "rng.cuh"
 #include "vec.cuh"
 
 namespace ms {
@@ -54,44 +55,7 @@ __device__ __forceinline__ void mul128(uint64_t a, uint64_t b, uint64_t& hi, uin
   hi = (uint64_t)a1 * b1 + (u >> 32) + (v >> 32);
 }
 
-// ---------------------------------------------------------------- Philox4x32-10
-struct Philox32Keys {
-  uint32_t k[10][2];
-};
-
-template <int NB>
-__device__ __forceinline__ uint32_t keep_n32(uint64_t blk0, uint64_t stream,
-                                             const Philox32Keys& K, uint64_t thr) {
-  constexpr uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
-  uint32_t c[NB][4];
-#pragma unroll
-  for (int b = 0; b < NB; ++b) {
-    const uint64_t j = blk0 + b;
-    c[b][0] = (uint32_t)j;
-    c[b][1] = (uint32_t)(j >> 32);
-    c[b][2] = (uint32_t)stream;
-    c[b][3] = (uint32_t)(stream >> 32);
-  }
-#pragma unroll
-  for (int r = 0; r < 10; ++r) {
-#pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      const uint32_t hi0 = __umulhi(M0, c[b][0]), lo0 = M0 * c[b][0];
-      const uint32_t hi1 = __umulhi(M1, c[b][2]), lo1 = M1 * c[b][2];
-      const uint32_t n0 = hi1 ^ c[b][1] ^ K.k[r][0], n2 = hi0 ^ c[b][3] ^ K.k[r][1];
-      c[b][0] = n0;
-      c[b][1] = lo1;
-      c[b][2] = n2;
-      c[b][3] = lo0;
-    }
-  }
-  uint32_t bits = 0;
-#pragma unroll
-  for (int b = 0; b < NB; ++b)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) bits |= ((uint64_t)c[b][j] >= thr ? 1u : 0u) << (4 * b + j);
-  return bits;
-}
+// Philox4x32-10: rng.cuh (shared with the GEMM epilogue's fused dropout)
 
 struct DropoutKeys {
   PhiloxKeys k64;    // MS_RNG_PHILOX4X64_REF
@@ -207,17 +171,13 @@ ms_status dropout_launch(int64_t numel, int dt, const void* x, void* y, uint64_t
   const bool vec = al16(x) && al16(y) && (!mask || (reinterpret_cast<uintptr_t>(mask) & 15) == 0);
   DropoutKeys K;
   uint64_t k0 = seed, k1 = stream_id;
-  uint32_t q0 = (uint32_t)seed, q1 = (uint32_t)(seed >> 32);
-  for (int r = 0; r < 10; ++r) {  // Weyl key schedules
+  for (int r = 0; r < 10; ++r) {  // Weyl key schedule
     K.k64.k[r][0] = k0;
     K.k64.k[r][1] = k1;
     k0 += 0x9E3779B97F4A7C15ull;
     k1 += 0xBB67AE8584CAA73Bull;
-    K.k32.k[r][0] = q0;
-    K.k32.k[r][1] = q1;
-    q0 += 0x9E3779B9u;
-    q1 += 0xBB67AE85u;
   }
+  K.k32 = philox32_keys(seed);
   K.stream = stream_id;
   const int grid = grid_for(numel / 16 + 1);
   if (gen == MS_RNG_PHILOX4X64_REF) {

@@ -5,6 +5,7 @@
 #include <cstdlib>
 
 #include "misc.cuh"
+#include "rng.cuh"
 
 namespace ms {
 
@@ -109,7 +110,9 @@ template <typename T>
 __global__ void tail_finalize_kernel(const float* __restrict__ ws, T* __restrict__ out,
                                      int64_t ldc, int rows, int cols, int m_blocks, int n_blocks,
                                      int n_fastest, int full_tiles, int splits, int tile_rows,
-                                     int bn, T* __restrict__ act_out) {
+                                     int bn, T* __restrict__ act_out,
+                                     const T* __restrict__ resid, const __grid_constant__ DropEpi drop,
+                                     int round_lin) {
   const int i = blockIdx.y;  // tail tile
   const int tile = full_tiles + i;
   const int mb = n_fastest ? (tile / n_blocks) % m_blocks : tile % m_blocks;
@@ -132,6 +135,22 @@ __global__ void tail_finalize_kernel(const float* __restrict__ ws, T* __restrict
     }
     const int64_t off = (int64_t)(m0 + r) * ldc + n0 + c;
     const bool vec = n0 + c + 8 <= cols && ((reinterpret_cast<uintptr_t>(out + off) & 15) == 0);
+    if (round_lin) {  // the epilogue's Linear -> dropout -> + residual, same roundings
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = IO<T>::ld_val(IO<T>::cvt(acc[j]));
+      if (drop.on) {  // off % 4 == 0: Philox blocks off/4, off/4 + 1
+        const uint32_t kb = keep_n32<2>(static_cast<uint64_t>(off) >> 2, drop.stream, drop.keys,
+                                        drop.thr);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          acc[j] = ((kb >> j) & 1u) ? IO<T>::ld_val(IO<T>::cvt(acc[j] * drop.scale)) : 0.f;
+      }
+      if (resid) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (n0 + c + j < cols) acc[j] += IO<T>::ld(resid + off + j);
+      }
+    }
     store8(out + off, acc, vec, cols - n0 - c);
     if (act_out) {  // fused GELU of the rounded pre-activation
 #pragma unroll
@@ -171,10 +190,16 @@ LinPlan plan_linear(int64_t M, int64_t N, int64_t K, int dt, int pass) {
   return plan_gemm(N, K, M, true, true);
 }
 
-ms_status run_gemm(const LinPlan& p, int dt, int a_mn, int b_mn, const CUtensorMap& ta,
+// act_out: fused GELU output (EpiParams::act_out); resid / drop: a fused
+// dropout + residual add after the bias (EpiParams::drop, round_lin; the tail
+// finalize applies them to K-split last-wave tiles)
+ms_status run_gemm(const LinPlan& p0, int dt, int a_mn, int b_mn, const CUtensorMap& ta,
                    const CUtensorMap& tb, int64_t rows, int64_t cols, void* out, int64_t ldc,
                    const void* bias, void* ws, size_t ws_bytes, cudaStream_t st,
-                   void* act_out = nullptr) {
+                   void* act_out = nullptr, const void* resid = nullptr,
+                   const DropEpi* drop = nullptr) {
+  const LinPlan& p = p0;
+  const bool post = resid != nullptr || drop != nullptr;
   TmapPack tm;
   tm.a[0] = ta;
   tm.a[1] = ta;
@@ -213,6 +238,7 @@ ms_status run_gemm(const LinPlan& p, int dt, int a_mn, int b_mn, const CUtensorM
                              : (p.n_blocks > 1 && b_bytes <= 32e6 && a_bytes > b_bytes ? 1 : 0);
   }
   if (p.splits > 1) {
+    MS_CHECK_ARG(!post, MS_ERR_UNSUPPORTED, "linear: split-K with a fused dropout / residual");
     MS_CHECK_ARG(ws && ws_bytes >= p.ws, MS_ERR_WORKSPACE, "linear: split-K workspace too small");
     cudaMemsetAsync(ws, 0, sizeof(float) * rows * cols, st);
     g.epi = EpiParams{ws, cols, MS_F32, 1, nullptr, 0};
@@ -223,6 +249,11 @@ ms_status run_gemm(const LinPlan& p, int dt, int a_mn, int b_mn, const CUtensorM
   }
   g.epi = EpiParams{out, ldc, dt, 0, bias, dt};
   g.epi.act_out = act_out;
+  if (post) {
+    g.epi.resid = resid;
+    if (drop) g.epi.drop = *drop;
+    g.epi.round_lin = 1;
+  }
   MS_TRY(setup_tma_store(tm, g, dt, out, rows, cols, ldc));
   if (p.tail_splits > 0) {
     MS_CHECK_ARG(ws && ws_bytes >= p.ws, MS_ERR_WORKSPACE,
@@ -240,12 +271,14 @@ ms_status run_gemm(const LinPlan& p, int dt, int a_mn, int b_mn, const CUtensorM
       tail_finalize_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(
           static_cast<const float*>(ws), static_cast<__nv_bfloat16*>(out), ldc, (int)rows,
           (int)cols, g.m_blocks, g.n_blocks, g.n_fastest, p.full_tiles, p.tail_splits, tile_rows,
-          p.bn, static_cast<__nv_bfloat16*>(act_out));
+          p.bn, static_cast<__nv_bfloat16*>(act_out), static_cast<const __nv_bfloat16*>(resid),
+          g.epi.drop, g.epi.round_lin);
     else
       tail_finalize_kernel<__half><<<grid, 256, 0, st>>>(
           static_cast<const float*>(ws), static_cast<__half*>(out), ldc, (int)rows, (int)cols,
           g.m_blocks, g.n_blocks, g.n_fastest, p.full_tiles, p.tail_splits, tile_rows, p.bn,
-          static_cast<__half*>(act_out));
+          static_cast<__half*>(act_out), static_cast<const __half*>(resid), g.epi.drop,
+          g.epi.round_lin);
     count_launch();
     return launch_status("tail_finalize_kernel");
   }
@@ -386,6 +419,42 @@ extern "C" ms_status ms_linear_gelu_fwd(int64_t M, int64_t N, int64_t K, int32_t
   }
   MS_TRY(ms_linear_fwd(M, N, K, dt, x, w, bias, pre, ws, ws_bytes, stream));
   return gelu_fwd(M * N, dt, pre, y, st);
+}
+
+extern "C" ms_status ms_linear_dropout_add_fwd(int64_t M, int64_t N, int64_t K, int32_t dt,
+                                               const void* x, const void* w, const void* bias,
+                                               const void* resid, double p, uint64_t seed,
+                                               uint64_t stream_id, int32_t gen, void* y, void* ws,
+                                               size_t ws_bytes, void* stream) {
+  MS_TRY(bind_device(y));
+  cudaStream_t st = (cudaStream_t)stream;
+  MS_CHECK_ARG(M >= 0 && N > 0 && K > 0 && resid != nullptr && y != resid, MS_ERR_SHAPE,
+               "linear_dropout_add: bad arguments");
+  MS_CHECK_ARG(p >= 0.0 && p < 1.0, MS_ERR_SHAPE, "linear_dropout_add: p must be in [0, 1)");
+  if (M == 0) return MS_OK;
+  LinPlan pl = plan_linear(M, N, K, dt, 0);
+  const bool drop = p > 0.0;
+  // the epilogue draws the default generator's bits for whole 4-element blocks
+  if (pl.tc && pl.splits == 1 && N % 4 == 0 && al16(x) && al16(w) && al16(y) && al16(resid) &&
+      (!drop || gen == MS_RNG_PHILOX4X32)) {
+    CUtensorMap ta, tb;
+    MS_TRY(make_tmap_2d(&ta, dt, x, K, M, K, BK, BM));
+    MS_TRY(make_tmap_2d(&tb, dt, w, K, N, K, BK, pl.bn / pl.cl));
+    DropEpi d{};
+    if (drop) {
+      d.keys = philox32_keys(seed);
+      d.stream = stream_id;
+      d.thr = static_cast<uint64_t>(ceil(p * 4294967296.0));
+      d.scale = static_cast<float>(1.0 / (1.0 - p));
+      d.on = 1;
+    }
+    return run_gemm(pl, dt, 0, 0, ta, tb, M, N, y, N, bias, ws, ws_bytes, st, nullptr, resid,
+                    drop ? &d : nullptr);
+  }
+  // the three launches
+  MS_TRY(ms_linear_fwd(M, N, K, dt, x, w, bias, y, ws, ws_bytes, stream));
+  if (drop) MS_TRY(ms_dropout_fwd(M * N, dt, y, y, seed, stream_id, p, gen, nullptr, stream));
+  return add_inplace(M * N, dt, y, resid, st);
 }
 
 extern "C" ms_status ms_linear_dx(int64_t M, int64_t N, int64_t K, int32_t dt, const void* dy,

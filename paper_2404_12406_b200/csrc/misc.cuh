@@ -50,6 +50,9 @@ ms_status conv3x3_halo(int dt, int n, int h, int w, int wlayout, int transpose, 
 ms_status gelu_fwd(int64_t n, int dt, const void* x, void* y, cudaStream_t st);
 ms_status gelu_bwd(int64_t n, int dt, const void* g, const void* pre, void* dx, cudaStream_t st);
 
+// y += r elementwise (16-bit: rounded once, as torch's add)
+ms_status add_inplace(int64_t n, int dt, void* y, const void* r, cudaStream_t st);
+
 inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 inline size_t align256(size_t v) { return (v + 255) & ~static_cast<size_t>(255); }
 

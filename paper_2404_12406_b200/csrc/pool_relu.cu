@@ -625,6 +625,36 @@ __global__ void __launch_bounds__(256) gelu_kernel(int64_t n, const T* __restric
 
 }  // namespace
 
+namespace {
+template <typename T>
+__global__ void __launch_bounds__(256) add_kernel(int64_t n, T* __restrict__ y,
+                                                  const T* __restrict__ r, bool vec) {
+  const int64_t groups = (n + 7) / 8;
+  for (int64_t gi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gi < groups;
+       gi += (int64_t)gridDim.x * blockDim.x) {
+    if (gi * 8 + 8 <= n) {
+      float a[8], b[8];
+      ld8<T>(y + gi * 8, a, vec);
+      ld8<T>(r + gi * 8, b, vec);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) a[j] += b[j];
+      st8<T>(y + gi * 8, a, vec);
+    } else {
+      for (int64_t e = gi * 8; e < n; ++e) y[e] = IO<T>::cvt(IO<T>::ld(y + e) + IO<T>::ld(r + e));
+    }
+  }
+}
+}  // namespace
+
+ms_status add_inplace(int64_t n, int dt, void* y, const void* r, cudaStream_t st) {
+  if (n <= 0) return MS_OK;
+  const bool vec = al16(y) && al16(r);
+  MS_DT_DISPATCH(dt, (add_kernel<T><<<grid_for((n + 7) / 8), 256, 0, st>>>(n, (T*)y, (const T*)r,
+                                                                          vec)));
+  count_launch();
+  return launch_status("add_kernel");
+}
+
 ms_status gelu_fwd(int64_t n, int dt, const void* x, void* y, cudaStream_t st) {
   if (n <= 0) return MS_OK;
   const bool vec = al16(x) && al16(y);

@@ -205,6 +205,32 @@ std::tuple<Tensor, Tensor> linear_gelu_fwd(const Tensor& x, const Tensor& w, con
   return {pre, y};
 }
 
+// y = r + dropout_p(x·wᵀ + b) in one GEMM (dropout and the add in the epilogue)
+Tensor linear_dropout_add_fwd(const Tensor& x, const Tensor& w, const OptT& b, const Tensor& r,
+                              double p, int64_t seed, int64_t stream_id, int64_t gen) {
+  const int64_t N = w.size(0), K = w.size(1);
+  TORCH_CHECK(x.size(-1) == K, "linear_dropout_add: input last dim ", x.size(-1),
+              " != in_features ", K);
+  auto shape = x.sizes().vec();
+  shape.back() = N;
+  TORCH_CHECK(r.sizes().vec() == shape && r.scalar_type() == x.scalar_type(),
+              "linear_dropout_add: residual ", r.sizes(), " does not match the output ",
+              c10::IntArrayRef(shape));
+  Tensor y = at::empty(shape, x.options());
+  if (x.is_meta()) return y;
+  Tensor x2 = x.reshape({-1, K}).contiguous(), wc = w.contiguous(), rc = r.contiguous();
+  Tensor bb = as_dtype(b, x.scalar_type());
+  const int64_t M = x2.size(0);
+  const int dt = dtc(x.scalar_type());
+  Launch L(x);
+  const size_t nb = ms_linear_workspace(M, N, K, dt, 0);
+  Tensor ws = wsp(nb, x);
+  ok(ms_linear_dropout_add_fwd(M, N, K, dt, cp(x2), cp(wc), cp(bb), cp(rc), p, (uint64_t)seed,
+                               (uint64_t)stream_id, (int32_t)gen, mp(y), mp(ws), nb, L.stream),
+     "linear_dropout_add_fwd");
+  return y;
+}
+
 Tensor gelu_fwd(const Tensor& x) {
   Tensor xc = x.contiguous();
   Tensor y = at::empty_like(xc);
@@ -765,6 +791,70 @@ struct LinearGeluFn : public torch::autograd::Function<LinearGeluFn> {
   }
 };
 
+// Linear -> dropout -> + residual as one node: the saved set is the Linear's
+// rule (rules.py:133-141) plus the dropout's 16-byte RNG key (rules.py:103-106,
+// kept as node data, not a tensor); the add saves nothing (rules.py:116-117)
+struct LinearDropoutAddFn : public torch::autograd::Function<LinearDropoutAddFn> {
+  static Tensor forward(torch::autograd::AutogradContext* ctx, const Tensor& x, const Tensor& w,
+                        const OptT& b, const Tensor& r, double p, int64_t seed, int64_t stream_id,
+                        int64_t gen) {
+    const bool x_rg = x.requires_grad(), w_rg = w.requires_grad();
+    static auto fwd = op_handle<Tensor(const Tensor&, const Tensor&, const OptT&, const Tensor&,
+                                       double, int64_t, int64_t, int64_t)>(
+        "memsave::linear_dropout_add_fwd");
+    Tensor y;
+    {
+      at::AutoDispatchBelowADInplaceOrView guard;
+      y = fwd.call(x, w, b, r, p, seed, stream_id, gen);
+    }
+    ctx->save_for_backward({w_rg ? x : Tensor(), x_rg ? w : Tensor()});
+    ctx->saved_data["x_shape"] = x.sizes().vec();
+    ctx->saved_data["has_b"] = has(b);
+    ctx->saved_data["p"] = p;
+    ctx->saved_data["seed"] = seed;
+    ctx->saved_data["stream"] = stream_id;
+    ctx->saved_data["gen"] = gen;
+    return y;
+  }
+  static torch::autograd::variable_list backward(torch::autograd::AutogradContext* ctx,
+                                                 torch::autograd::variable_list grads) {
+    static auto drop_op = op_handle<Tensor(const Tensor&, double, int64_t, int64_t, int64_t)>(
+        "memsave::dropout_bwd");
+    static auto dx_op =
+        op_handle<Tensor(const Tensor&, const Tensor&, IntArrayRef)>("memsave::linear_dx");
+    static auto dw_op = op_handle<Tensor(const Tensor&, const Tensor&)>("memsave::linear_dw");
+    static auto db_op = op_handle<Tensor(const Tensor&, int64_t)>("memsave::bias_grad");
+    const auto saved = ctx->get_saved_variables();
+    const bool has_b = ctx->saved_data["has_b"].toBool();
+    const int ir = has_b ? 3 : 2;  // input slot of r (a None bias is not an input)
+    const Tensor gy = grads[0].contiguous();
+    const double p = ctx->saved_data["p"].toDouble();
+    Tensor dx, dw, db, dr;
+    if (ctx->needs_input_grad(ir)) dr = gy;  // the add passes the gradient through
+    const bool lin = ctx->needs_input_grad(0) || ctx->needs_input_grad(1) ||
+                     (has_b && ctx->needs_input_grad(2));
+    if (lin) {
+      // the mask replayed from its key (dropout's VJP), then the Linear's VJPs
+      const Tensor gz = p > 0.0 ? drop_op.call(gy, p, ctx->saved_data["seed"].toInt(),
+                                               ctx->saved_data["stream"].toInt(),
+                                               ctx->saved_data["gen"].toInt())
+                                : gy;
+      if (has_b && ctx->needs_input_grad(2)) db = db_op.call(gz, gz.size(-1));
+      if (ctx->needs_input_grad(0)) {
+        TORCH_CHECK(saved[1].defined(), "MissingSavedValue: linear dX needs 'w' but the storage "
+                                        "rule did not keep it");
+        dx = dx_op.call(gz, saved[1], ctx->saved_data["x_shape"].toIntVector());
+      }
+      if (ctx->needs_input_grad(1)) {
+        TORCH_CHECK(saved[0].defined(), "MissingSavedValue: linear dW needs 'x' but the storage "
+                                        "rule did not keep it");
+        dw = dw_op.call(saved[0], gz);
+      }
+    }
+    return {dx, dw, db, dr, Tensor(), Tensor(), Tensor(), Tensor()};
+  }
+};
+
 void check_linear(const Tensor& x, const Tensor& w, const OptT& b) {
   for (const Tensor* t : {&x, &w, has(b) ? &*b : nullptr}) {
     if (!t) continue;
@@ -787,6 +877,22 @@ Tensor linear_noautograd(const Tensor& x, const Tensor& w, const OptT& b) {
   return linear_fwd(x, w, b);
 }
 
+Tensor linear_dropout_add_autograd(const Tensor& x, const Tensor& w, const OptT& b,
+                                   const Tensor& r, double p, int64_t seed, int64_t stream_id,
+                                   int64_t gen) {
+  check_linear(x, w, b);
+  TORCH_CHECK(r.is_cuda() || r.is_meta(), "memsave_b200.linear_dropout_add: residual must be on "
+              "a CUDA device; this implementation has no CPU path");
+  return LinearDropoutAddFn::apply(x, w, b, r, p, seed, stream_id, gen);
+}
+
+Tensor linear_dropout_add_noautograd(const Tensor& x, const Tensor& w, const OptT& b,
+                                     const Tensor& r, double p, int64_t seed, int64_t stream_id,
+                                     int64_t gen) {
+  check_linear(x, w, b);
+  return linear_dropout_add_fwd(x, w, b, r, p, seed, stream_id, gen);
+}
+
 Tensor linear_gelu_autograd(const Tensor& x, const Tensor& w, const OptT& b) {
   check_linear(x, w, b);
   return LinearGeluFn::apply(x, w, b);
@@ -804,6 +910,10 @@ TORCH_LIBRARY(memsave, m) {
   m.def("linear_fwd(Tensor x, Tensor w, Tensor? b) -> Tensor");
   m.def("linear_dx(Tensor g, Tensor w, int[] x_shape) -> Tensor");
   m.def("linear_gelu(Tensor x, Tensor w, Tensor? b) -> Tensor");
+  m.def("linear_dropout_add(Tensor x, Tensor w, Tensor? b, Tensor r, float p, int seed, "
+        "int stream_id, int gen) -> Tensor");
+  m.def("linear_dropout_add_fwd(Tensor x, Tensor w, Tensor? b, Tensor r, float p, int seed, "
+        "int stream_id, int gen) -> Tensor");
   m.def("linear_gelu_fwd(Tensor x, Tensor w, Tensor? b) -> (Tensor, Tensor)");
   m.def("gelu_fwd(Tensor x) -> Tensor");
   m.def("gelu_bwd(Tensor g, Tensor pre) -> Tensor");
@@ -861,6 +971,7 @@ TORCH_LIBRARY(memsave, m) {
   m.impl("linear_fwd", &linear_fwd);                         \
   m.impl("linear_dx", &linear_dx);                           \
   m.impl("linear_gelu_fwd", &linear_gelu_fwd);               \
+  m.impl("linear_dropout_add_fwd", &linear_dropout_add_fwd); \
   m.impl("gelu_fwd", &gelu_fwd);                             \
   m.impl("gelu_bwd", &gelu_bwd);                             \
   m.impl("linear_dw", &linear_dw);                           \
@@ -894,14 +1005,17 @@ TORCH_LIBRARY_IMPL(memsave, CUDA, m) {
   MS_IMPLS(m);
   m.impl("linear", &linear_noautograd);
   m.impl("linear_gelu", &linear_gelu_noautograd);
+  m.impl("linear_dropout_add", &linear_dropout_add_noautograd);
 }
 TORCH_LIBRARY_IMPL(memsave, Meta, m) {
   MS_IMPLS(m);
   m.impl("linear", &linear_noautograd);
   m.impl("linear_gelu", &linear_gelu_noautograd);
+  m.impl("linear_dropout_add", &linear_dropout_add_noautograd);
 }
 TORCH_LIBRARY_IMPL(memsave, Autograd, m) {
   m.impl("linear", &linear_autograd);
   m.impl("linear_gelu", &linear_gelu_autograd);
+  m.impl("linear_dropout_add", &linear_dropout_add_autograd);
 }
 // CPU tensors reach the autograd kernel too (then fail loudly in check_linear)

@@ -24,6 +24,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "rng.cuh"
 
 namespace ms {
 
@@ -105,6 +106,13 @@ struct EpiParams {
   // backward reads) and act_out receives gelu(pre) of the ROUNDED pre, exactly
   // what a separate gelu launch would read and write (same dtype / pitch)
   void* act_out;
+  // Linear -> dropout -> + residual (a transformer block's output projection):
+  // the linear output is rounded to the storage type, dropped with the mask the
+  // dropout kernels draw for the same (seed, stream, element) and rounded
+  // again, then resid is added -- bit for bit the three separate launches
+  // (round_lin: round before the residual add even without dropout)
+  DropEpi drop;
+  int round_lin;
 };
 
 struct GemmArgs {
@@ -944,6 +952,31 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
                 *reinterpret_cast<float4*>(o + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
             }
             continue;
+          }
+          if (e.round_lin) {
+            auto round_all = [&]() {
+              if (e.out_dtype == MS_BF16) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = __bfloat162float(__float2bfloat16_rn(v[j]));
+              } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = __half2float(__float2half_rn(v[j]));
+              }
+            };
+            round_all();  // the Linear's output as stored
+            if (e.drop.on) {
+              // elements el .. el + 31 of the output (el % 4 == 0: N and the
+              // pitch are multiples of 4): Philox blocks el/4 .. el/4 + 7
+              const int64_t el = orow * e.ldc + col_base + c;
+              const uint32_t klo = keep_n32<4>(static_cast<uint64_t>(el) >> 2, e.drop.stream,
+                                               e.drop.keys, e.drop.thr);
+              const uint32_t khi = keep_n32<4>((static_cast<uint64_t>(el) >> 2) + 4, e.drop.stream,
+                                               e.drop.keys, e.drop.thr);
+              const uint32_t kb = klo | (khi << 16);
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = ((kb >> j) & 1u) ? v[j] * e.drop.scale : 0.f;
+              round_all();  // the dropout's output as stored
+            }
           }
           if (e.bn.var != nullptr && !e.bn_post) {  // folded eval-BN: per-column affine
 #pragma unroll

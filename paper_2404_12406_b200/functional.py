@@ -89,6 +89,30 @@ def linear_gelu(x: torch.Tensor, weight: torch.Tensor, bias: torch.Tensor | None
     return _ops().linear_gelu(x, weight, bias)
 
 
+def linear_dropout_add(x: torch.Tensor, weight: torch.Tensor, bias, residual: torch.Tensor,
+                       p: float = 0.1, training: bool = True, seed: int | None = None,
+                       stream: int | None = None, generator: str = "philox4x32") -> torch.Tensor:
+    """``residual + dropout(linear(x))`` as one node (a transformer block's
+    output projection before its LayerNorm).
+
+    ``torch.ops.memsave.linear_dropout_add`` (``LinearDropoutAddFn``) applies
+    the dropout and the residual add in the GEMM epilogue; every intermediate is
+    rounded as the separate launches round it and the mask is the one
+    :func:`dropout` draws for the same (seed, stream), so values equal the
+    three ops.  Saved set: the Linear's rule (rules.py:133-141) and the
+    dropout's RNG key (rules.py:103-106); the add keeps nothing.  ``stream``
+    defaults to DROPOUT_STREAM_BASE like :func:`dropout`."""
+    if not 0.0 <= p < 1.0:
+        raise ValueError(f"dropout probability has to be in [0, 1), got {p}")
+    if generator not in _RNG:
+        raise ValueError(f"dropout generator must be one of {sorted(_RNG)}, got {generator!r}")
+    pe = float(p) if training else 0.0
+    sd = (draw_seed() if seed is None else int(seed)) if pe > 0.0 else 0
+    return _ops().linear_dropout_add(x, weight, bias, residual, pe, sd,
+                                     DROPOUT_STREAM_BASE if stream is None else int(stream),
+                                     _RNG[generator])
+
+
 # =============================================================== conv2d
 def _pair(v):
     if isinstance(v, (tuple, list)):

@@ -20,7 +20,8 @@ from .. import functional as MF
 
 __all__ = ["MemSaveLinear", "MemSaveConv2d", "MemSaveBatchNorm2d", "MemSaveReLU",
            "MemSaveMaxPool2d", "MemSaveDropout", "MemSaveLayerNorm", "MemSaveConvTranspose2d",
-           "convert_to_memory_saving", "fuse_conv_bn_relu", "fuse_linear_gelu"]
+           "convert_to_memory_saving", "fuse_conv_bn_relu", "fuse_linear_gelu",
+           "fuse_linear_dropout_add"]
 
 
 def _share_params(dst: nn.Module, src: nn.Module, clone: bool) -> None:
@@ -524,19 +525,59 @@ def _rewrite_linear_gelu(gm) -> int:
     return n
 
 
-def fuse_linear_gelu(model: nn.Module, verbose: bool = False) -> nn.Module:
-    """Fuses ``MemSaveLinear -> GELU(erf)`` into one :func:`functional.linear_gelu`
-    node (GELU in the GEMM epilogue, pre-activation and output from one pass).
-    Opt-in: at BERT's FFN shape (32768 x 3072 x 768) the fused launch takes
-    285 us against 136 us + 112 us for the GEMM and torch's GELU -- the erf's
-    ~17 instructions per element in the 8 epilogue warps outlast the MMAs.
+def _dropout_add_layer(x: torch.Tensor, lin: nn.Linear, drop, other: torch.Tensor):
+    y_shape = tuple(x.shape[:-1]) + (lin.out_features,)
+    if (tuple(other.shape) != y_shape or other.dtype != x.dtype
+            or type(drop) is not MemSaveDropout or drop.inplace):
+        return drop(lin(x)) + other
+    return MF.linear_dropout_add(x, lin.weight, lin.bias, other, drop.p, drop.training,
+                                 stream=MF.DROPOUT_STREAM_BASE + drop.node,
+                                 generator=drop.generator)
 
-    Transformer models rarely trace as a whole, so the pass works per module:
-    a module whose ``forward`` takes only required arguments and whose trace is
-    a plain chain of leaf layers, GELUs and adds (e.g. a BERT intermediate block:
-    ``gelu(dense(x))``) is replaced by its rewritten ``fx.GraphModule`` (same
-    parameters and state_dict keys); any other module is searched recursively.
-    Returns the model (or its replacement when the root itself was rewritten)."""
+
+def _rewrite_linear_dropout_add(gm) -> int:
+    """dense -> MemSaveDropout -> add(., other) with single-use intermediates"""
+    import torch.fx as fx
+
+    modules = dict(gm.named_modules())
+    g = gm.graph
+    n = 0
+    for node in list(g.nodes):
+        if node.op != "call_module" or type(modules.get(node.target)) is not MemSaveLinear:
+            continue
+        if len(node.users) != 1 or len(node.args) != 1 or node.kwargs:
+            continue
+        d = next(iter(node.users))
+        if (d.op != "call_module" or type(modules.get(d.target)) is not MemSaveDropout
+                or len(d.users) != 1 or d.args != (node,) or d.kwargs):
+            continue
+        a = next(iter(d.users))
+        if not _is_add(a) or a.op != "call_function":
+            continue
+        other = a.args[1] if a.args[0] is d else a.args[0]
+        if other is d or not isinstance(other, fx.Node) or not isinstance(node.args[0], fx.Node):
+            continue
+        with g.inserting_before(a):
+            lref = g.get_attr(node.target)
+            dref = g.get_attr(d.target)
+            fused = g.call_function(_dropout_add_layer, (node.args[0], lref, dref, other))
+        a.replace_all_uses_with(fused)
+        for dead in (a, d, node):
+            g.erase_node(dead)
+        n += 1
+    if n:
+        g.eliminate_dead_code()
+        g.lint()
+        gm.recompile()
+    return n
+
+
+def _fuse_per_module(model: nn.Module, rewrite, what: str, verbose: bool) -> nn.Module:
+    """Runs ``rewrite`` on the traced graph of every module whose ``forward``
+    takes only required arguments and traces to a plain chain of leaf layers,
+    GELUs and adds (e.g. BERT's intermediate / output blocks); a rewritten
+    module is replaced by its ``fx.GraphModule`` (same parameters and state_dict
+    keys), any other module is searched recursively."""
     import inspect
 
     import torch.fx as fx
@@ -567,7 +608,7 @@ def fuse_linear_gelu(model: nn.Module, verbose: bool = False) -> nn.Module:
             return None
         if not _simple_graph(gm, dict(gm.named_modules())):
             return None
-        k = _rewrite_linear_gelu(gm)
+        k = rewrite(gm)
         total[0] += k
         return gm if k else None
 
@@ -575,6 +616,7 @@ def fuse_linear_gelu(model: nn.Module, verbose: bool = False) -> nn.Module:
         for name, child in list(parent.named_children()):
             new = try_mod(child)
             if new is not None:
+                new.train(child.training)
                 setattr(parent, name, new)
             else:
                 walk(child)
@@ -583,8 +625,29 @@ def fuse_linear_gelu(model: nn.Module, verbose: bool = False) -> nn.Module:
     if top is None:
         walk(model)
     if verbose:
-        print(f"memsave: fused {total[0]} linear->gelu pairs")
+        print(f"memsave: fused {total[0]} {what}")
     return top if top is not None else model
+
+
+def fuse_linear_gelu(model: nn.Module, verbose: bool = False) -> nn.Module:
+    """Fuses ``MemSaveLinear -> GELU(erf)`` into one :func:`functional.linear_gelu`
+    node (GELU in the GEMM epilogue, pre-activation and output from one pass).
+    Opt-in: at BERT's FFN shape (32768 x 3072 x 768) the fused launch takes
+    285 us against 136 us + 112 us for the GEMM and torch's GELU -- the erf's
+    ~17 instructions per element in the 8 epilogue warps outlast the MMAs.
+    Works per module (:func:`_fuse_per_module`); returns the model (or its
+    replacement when the root itself was rewritten)."""
+    return _fuse_per_module(model, _rewrite_linear_gelu, "linear->gelu pairs", verbose)
+
+
+def fuse_linear_dropout_add(model: nn.Module, verbose: bool = False) -> nn.Module:
+    """Fuses ``MemSaveLinear -> MemSaveDropout -> + residual`` (a transformer
+    block's output projection) into one :func:`functional.linear_dropout_add`
+    node: dropout and residual add in the GEMM epilogue, values and saved set
+    equal to the three layers'.  Works per module like :func:`fuse_linear_gelu`;
+    run by ``convert_to_memory_saving(fuse=True)``."""
+    return _fuse_per_module(model, _rewrite_linear_dropout_add, "linear->dropout->add chains",
+                            verbose)
 
 
 def convert_to_memory_saving(model: nn.Module, linear: bool = True, conv2d: bool = True,
@@ -603,9 +666,9 @@ def convert_to_memory_saving(model: nn.Module, linear: bool = True, conv2d: bool
     (1-byte argmax), Dropout (RNG replay; node i of the traversal draws from
     stream DROPOUT_STREAM_BASE + i), LayerNorm and ConvTranspose2d are swapped
     too; conv1d/3d are accepted for API compatibility and left untouched.
-    ``fuse=True`` additionally runs :func:`fuse_conv_bn_relu` (returns an
-    ``fx.GraphModule`` sharing the parameters, or the model unchanged when it
-    cannot be traced).  :func:`fuse_linear_gelu` is opt-in (measured slower
+    ``fuse=True`` additionally runs :func:`fuse_linear_dropout_add` (per
+    module) and :func:`fuse_conv_bn_relu` (returns an ``fx.GraphModule``
+    sharing the parameters, or the model unchanged when it cannot be traced).  :func:`fuse_linear_gelu` is opt-in (measured slower
     than the two launches on B200 at the BERT FFN shape).
     Returns the (possibly replaced) model.
     """
@@ -632,5 +695,7 @@ def convert_to_memory_saving(model: nn.Module, linear: bool = True, conv2d: bool
 
     walk(model, "")
     if fuse:
+        if linear and dropout:
+            model = fuse_linear_dropout_add(model, verbose=verbose)
         return fuse_conv_bn_relu(model, verbose=verbose, kinds=kinds)
     return model

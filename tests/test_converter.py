@@ -157,3 +157,32 @@ def test_fuse_linear_gelu_bert_intermediate_blocks():
     assert list(m.state_dict().keys()) == keys
     ids = torch.zeros(2, 16, dtype=torch.long, device="meta")
     m(input_ids=ids).logits.sum().backward()
+
+
+def test_fuse_linear_dropout_add_bert_output_blocks():
+    """convert_to_memory_saving(fuse=True) turns BERT's attention-output and
+    output blocks (dense -> dropout -> + input -> LayerNorm) into the fused node;
+    parameters, state_dict keys and the train/eval switch are kept."""
+    from transformers import BertConfig, BertForSequenceClassification
+    cfg = BertConfig(num_hidden_layers=2, hidden_size=64, num_attention_heads=2,
+                     intermediate_size=128, attn_implementation="sdpa")
+    with torch.device("meta"):
+        m = BertForSequenceClassification(cfg)
+    keys = list(m.state_dict().keys())
+    m = convert_to_memory_saving(m, fuse=True)
+    for layer in m.bert.encoder.layer:
+        for blk in (layer.attention.output, layer.output):
+            assert isinstance(blk, torch.fx.GraphModule)
+            assert "_dropout_add_layer" in blk.code
+        assert not isinstance(layer.intermediate, torch.fx.GraphModule)
+    assert list(m.state_dict().keys()) == keys
+    m.eval()
+    assert not m.bert.encoder.layer[0].output.dropout.training
+    ids = torch.zeros(2, 16, dtype=torch.long, device="meta")
+    m.train()
+    m(input_ids=ids).logits.sum().backward()
+    # converting without dropout leaves the blocks alone
+    with torch.device("meta"):
+        m2 = BertForSequenceClassification(cfg)
+    convert_to_memory_saving(m2, fuse=True, dropout=False)
+    assert not isinstance(m2.bert.encoder.layer[0].output, torch.fx.GraphModule)

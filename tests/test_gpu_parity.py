@@ -339,6 +339,51 @@ def test_linear_gelu(case, dt):
     _close(b.grad, oracle.linear_db(zq), dt, "db")
 
 
+LINEAR_DROP_CASES = [((8, 512), 768, 768), ((4, 512), 3072, 768), ((3, 100), 200, 72),
+                     ((2, 64), 96, 40)]
+
+
+@pytest.mark.parametrize("p", [0.1, 0.0])
+@pytest.mark.parametrize("case", LINEAR_DROP_CASES)
+def test_linear_dropout_add(case, p):
+    """Linear -> dropout -> + residual in one node equals the three memsave ops
+    bit for bit (forward with the same seed / stream, and every VJP); the
+    tcgen05 shapes run it as ONE launch (dropout and add in the epilogue)."""
+    lead, fin, fout = case
+    rng = np.random.default_rng(fin + 5 * fout)
+    x, xq = _q(rng.standard_normal(lead + (fin,)), "bf16")
+    w, wq = _q(rng.standard_normal((fout, fin)) / np.sqrt(fin), "bf16")
+    b, _ = _q(rng.standard_normal(fout), "bf16")
+    r, _ = _q(rng.standard_normal(lead + (fout,)), "bf16")
+    g, _ = _q(rng.standard_normal(lead + (fout,)), "bf16")
+    seed, stream = 12345, MF.DROPOUT_STREAM_BASE + 3
+    MF._ops()
+    c0, u0 = launch_count(), launch_stats()["umma"]
+    y = MF.linear_dropout_add(x, w, b, r, p, True, seed=seed, stream=stream)
+    if fin % 8 == 0 and fout % 8 == 0 and x.numel() // fin >= 128:
+        # one GEMM (+ the K-split last wave's finalize, which applies the same steps)
+        assert launch_count() - c0 <= 2 and launch_stats()["umma"] - u0 == 1
+    ref = MF.dropout(MF.linear(x, w, b), p, True, seed=seed, stream=stream) + r
+    assert torch.equal(y, ref)
+    if p > 0:  # the mask really drops about p of the elements
+        lin = MF.linear(x, w, b)
+        frac = ((y == r) & (lin != 0)).float().mean().item()
+        assert abs(frac - p) < 0.05, frac
+    ts = [t.detach().clone().requires_grad_(True) for t in (x, w, b, r)]
+    us = [t.detach().clone().requires_grad_(True) for t in (x, w, b, r)]
+    MF.linear_dropout_add(*ts, p, True, seed=seed, stream=stream).backward(g)
+    (MF.dropout(MF.linear(*us[:3]), p, True, seed=seed, stream=stream) + us[3]).backward(g)
+    for a, c, what in zip(ts, us, ("dx", "dw", "db", "dr")):
+        if what in ("dw", "db"):  # fp32 atomics (split-K, column sums): order-dependent
+            torch.testing.assert_close(a.grad, c.grad, rtol=2 ** -7, atol=0, msg=what)
+        else:
+            assert torch.equal(a.grad, c.grad), what
+    # eval: no dropout, the Linear (oracle-checked in test_linear) + the residual
+    lin = MF.linear(x, w, b)
+    _close(lin, oracle.linear_fwd(xq, wq, b.double().cpu().numpy()), "bf16", "linear")
+    assert torch.equal(MF.linear_dropout_add(x, w, b, r, p, False), lin + r)
+
+
 def test_linear_golden(linbn_golden):
     g = linbn_golden
     for case in ("lin_small", "lin_3d"):

@@ -264,3 +264,20 @@ def test_linear_gelu_saved_set(rules_golden, x_rg, w_rg, b_rg):
         out.sum().backward()
         assert (x.grad is not None) == x_rg and (w.grad is not None) == w_rg
         assert (b.grad is not None) == b_rg
+
+
+@pytest.mark.parametrize("x_rg,w_rg,b_rg", FLAGS)
+@pytest.mark.parametrize("r_rg", [False, True])
+def test_linear_dropout_add_saved_set(rules_golden, x_rg, w_rg, b_rg, r_rg):
+    """Linear -> dropout -> + residual as one node saves exactly the Linear's
+    rule set: the dropout keeps its 16-byte key as node data, the add nothing."""
+    x, w, b = _make((6, 5, 7), x_rg), _make((3, 7), w_rg), _make((3,), b_rg)
+    r = _make((6, 5, 3), r_rg)
+    out, roles = _run(lambda *t: MF.linear_dropout_add(*t, p=0.1, seed=7), (x, w, b, r),
+                      {(6, 5, 7): "x", (3, 7): "w"})
+    assert roles == _golden_saves(rules_golden, "linear", x_rg, w_rg, b_rg)
+    assert out.shape == (6, 5, 3)
+    if out.requires_grad:
+        out.sum().backward()
+        assert (x.grad is not None) == x_rg and (w.grad is not None) == w_rg
+        assert (b.grad is not None) == b_rg and (r.grad is not None) == r_rg
