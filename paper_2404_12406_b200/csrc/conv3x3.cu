@@ -83,8 +83,8 @@ __global__ void __launch_bounds__(H3Geo<WIDE>::THREADS, 1)
                         const __grid_constant__ CUtensorMap tma_y,
                         const __grid_constant__ H3Args a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
+  // aligned by an offset from the shared array (keeps the accesses STS / LDS)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   using G = H3Geo<WIDE>;
   constexpr int H3_ROWS = G::ROWS, H3_P = G::P, H3_HALO = G::HALO, H3_STAGES = G::STAGES;
   uint8_t* sB = smem;

@@ -363,9 +363,10 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
   const int t_step = static_cast<int>(gridDim.x) / CL;
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // 1024-byte alignment for the swizzle atoms
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
+  // 1024-byte alignment for the swizzle atoms, by an offset from the shared
+  // array (an integer round trip would make the pointer generic: the staging
+  // and band-window accesses would compile to generic ST/LD instead of STS/LDS)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* ring = smem;
   uint8_t* staging = smem + STAGES * Cfg::STAGE_BYTES;  // TMA-store chunks (1024-aligned)
   float* region = reinterpret_cast<float*>(staging + Cfg::STG);  // band windows
