@@ -393,9 +393,11 @@ def _ncu_traffic(config, dom):
     try:
         with open(p) as f:
             d = json.load(f)
-        e = d[config]
-        if e["op"].split(".")[-1] == dom["op"].split(".")[-1] and e["geom"] == dom["geom"]:
-            return int(e["dram_bytes"]), f"profiles/r2_ncu_traffic.json:{config} ({e['kernel']})"
+        es = d[config]
+        for e in es if isinstance(es, list) else [es]:
+            if e["op"].split(".")[-1] == dom["op"].split(".")[-1] and e["geom"] == dom["geom"]:
+                return int(e["dram_bytes"]), \
+                    f"profiles/r2_ncu_traffic.json:{config} ({e['kernel']})"
     except Exception:
         pass
     return None, None

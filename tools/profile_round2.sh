@@ -6,6 +6,8 @@ cd "$(dirname "$0")/.."
 OUT=gpurun_out
 declare -A OP GEOM
 OP[bert]=linear_fwd;      GEOM[bert]='{"M": 32768, "N": 768, "K": 768}'
+OP[bertdx]=linear_dx;     GEOM[bertdx]='{"M": 32768, "N": 768, "K": 768}'
+OP[bertlda]=linear_dropout_add_fwd; GEOM[bertlda]='{"M": 32768, "N": 768, "K": 3072}'
 OP[resnet18]=conv2d_bn_fwd; GEOM[resnet18]='{"x": [256, 64, 56, 56], "w": [64, 64, 3, 3], "stride": [1, 1], "pad": [1, 1]}'
 OP[resnet101]=conv2d_bn_dx; GEOM[resnet101]='{"x": [128, 1024, 14, 14], "w": [256, 1024, 1, 1], "stride": [1, 1], "pad": [0, 0]}'
 OP[vgg16]=conv2d_dw;  GEOM[vgg16]='{"x": [128, 512, 28, 28], "w": [512, 512, 3, 3], "stride": [1, 1], "pad": [1, 1]}'
@@ -16,7 +18,8 @@ OP[r101bn]=bn_add_relu_bwd; GEOM[r101bn]='{"shape": [128, 1024, 14, 14]}'
 OP[r101bnf]=bn_relu_fwd; GEOM[r101bnf]='{"shape": [128, 1024, 14, 14]}'
 for c in ${CONFIGS:-bert resnet18 resnet101 vgg16 fig1 llama r101bn r101bnf}; do
   cfg=$c; [[ $c == r101bn* ]] && cfg=resnet101; [[ $c == vgg16c11 ]] && cfg=vgg16
-  if [[ $c != r101bn* && $c != vgg16c11 ]]; then
+  [[ $c == bert?* ]] && cfg=bert
+  if [[ $c != r101bn* && $c != vgg16c11 && $c != bert?* ]]; then
     timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off \
       --csv --log-file $OUT/r2_launches_$c.csv python tools/prof_step.py --config $cfg --steps 2 \
       > $OUT/r2_launches_$c.log 2>&1
