@@ -384,6 +384,22 @@ def test_linear_dropout_add(case, p):
     assert torch.equal(MF.linear_dropout_add(x, w, b, r, p, False), lin + r)
 
 
+@pytest.mark.parametrize("dt,gen", [("f32", "philox4x32"), ("bf16", "reference"),
+                                    ("fp16", "philox4x32")])
+def test_linear_dropout_add_other_paths(dt, gen):
+    """float32 (3xTF32 GEMM), the reference generator and fp16 run the three
+    launches (or fp16's epilogue) and still equal the composed ops bit for bit."""
+    rng = np.random.default_rng(17)
+    x, _ = _q(rng.standard_normal((3, 128, 256)), dt)
+    w, _ = _q(rng.standard_normal((192, 256)) / 16.0, dt)
+    b, _ = _q(rng.standard_normal(192), dt)
+    r, _ = _q(rng.standard_normal((3, 128, 192)), dt)
+    kw = dict(seed=99, stream=MF.DROPOUT_STREAM_BASE + 1, generator=gen)
+    y = MF.linear_dropout_add(x, w, b, r, 0.25, True, **kw)
+    ref = MF.dropout(MF.linear(x, w, b), 0.25, True, **kw) + r
+    assert torch.equal(y, ref)
+
+
 def test_linear_golden(linbn_golden):
     g = linbn_golden
     for case in ("lin_small", "lin_3d"):
