@@ -113,6 +113,8 @@ __global__ void tail_finalize_kernel(const float* __restrict__ ws, T* __restrict
                                      int bn, T* __restrict__ act_out,
                                      const T* __restrict__ resid, const __grid_constant__ DropEpi drop,
                                      int round_lin) {
+  // launched as a programmatic dependent of the GEMM: wait for its partials
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int i = blockIdx.y;  // tail tile
   const int tile = full_tiles + i;
   const int mb = n_fastest ? (tile / n_blocks) % m_blocks : tile % m_blocks;
@@ -267,19 +269,35 @@ ms_status run_gemm(const LinPlan& p0, int dt, int a_mn, int b_mn, const CUtensor
     MS_TRY(launch_umma(p.bn, a_mn, b_mn, LOAD_GEMM, tm, g, st, p.cl));
     const int tile_rows = BM * p.cl;
     const dim3 grid((unsigned)((tile_rows * (p.bn / 8) + 255) / 256), (unsigned)tail);
+    // programmatic dependent launch: scheduled while the GEMM still runs (its
+    // blocks wait in griddepcontrol.wait), so the launch latency is hidden
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e;
     if (dt == MS_BF16)
-      tail_finalize_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(
-          static_cast<const float*>(ws), static_cast<__nv_bfloat16*>(out), ldc, (int)rows,
-          (int)cols, g.m_blocks, g.n_blocks, g.n_fastest, p.full_tiles, p.tail_splits, tile_rows,
-          p.bn, static_cast<__nv_bfloat16*>(act_out), static_cast<const __nv_bfloat16*>(resid),
-          g.epi.drop, g.epi.round_lin);
+      e = cudaLaunchKernelEx(&cfg, tail_finalize_kernel<__nv_bfloat16>,
+                             static_cast<const float*>(ws), static_cast<__nv_bfloat16*>(out), ldc,
+                             (int)rows, (int)cols, g.m_blocks, g.n_blocks, g.n_fastest,
+                             p.full_tiles, p.tail_splits, tile_rows, p.bn,
+                             static_cast<__nv_bfloat16*>(act_out),
+                             static_cast<const __nv_bfloat16*>(resid), g.epi.drop,
+                             g.epi.round_lin);
     else
-      tail_finalize_kernel<__half><<<grid, 256, 0, st>>>(
-          static_cast<const float*>(ws), static_cast<__half*>(out), ldc, (int)rows, (int)cols,
-          g.m_blocks, g.n_blocks, g.n_fastest, p.full_tiles, p.tail_splits, tile_rows, p.bn,
-          static_cast<__half*>(act_out), static_cast<const __half*>(resid), g.epi.drop,
-          g.epi.round_lin);
+      e = cudaLaunchKernelEx(&cfg, tail_finalize_kernel<__half>, static_cast<const float*>(ws),
+                             static_cast<__half*>(out), ldc, (int)rows, (int)cols, g.m_blocks,
+                             g.n_blocks, g.n_fastest, p.full_tiles, p.tail_splits, tile_rows,
+                             p.bn, static_cast<__half*>(act_out),
+                             static_cast<const __half*>(resid), g.epi.drop, g.epi.round_lin);
     count_launch();
+    MS_CHECK_ARG(e == cudaSuccess, MS_ERR_LAUNCH, "tail_finalize_kernel: %s",
+                 cudaGetErrorString(e));
     return launch_status("tail_finalize_kernel");
   }
   return launch_umma(p.bn, a_mn, b_mn, LOAD_GEMM, tm, g, st, p.cl);

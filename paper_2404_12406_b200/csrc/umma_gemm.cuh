@@ -358,6 +358,11 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
                     MODE == LOAD_CONV_DGRAD,
                 "CTA pairs are implemented for GEMM and im2col conv fprop / dgrad");
   static_assert(CL == 1 || (BN / CL) % 16 == 0, "pair: B half must be a multiple of 16 rows");
+  // a follow-up launched with programmatic stream serialization (the last-wave
+  // K-split finalize) may be scheduled now: its blocks wait in
+  // griddepcontrol.wait until this grid has finished, so only the launch
+  // latency overlaps (no effect on launches without the attribute)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int crank = CL > 1 ? static_cast<int>(cluster_ctarank()) : 0;
   const int t_first = static_cast<int>(blockIdx.x) / CL;
   const int t_step = static_cast<int>(gridDim.x) / CL;
