@@ -226,6 +226,15 @@ ms_status setup_tma_store(TmapPack& tm, GemmArgs& g, int dt, void* out, int64_t 
   return MS_OK;
 }
 
+// programmatic dependent launch of the GEMM / conv kernels (MS_PDL=0: off)
+static bool use_pdl() {
+  static const bool on = [] {
+    const char* e = getenv("MS_PDL");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
+
 // ------------------------------------------------------------------ dispatch
 template <int BN, int A_MN, int B_MN, int MODE, int CL = 1>
 static ms_status launch_t(const TmapPack& tm, const GemmArgs& g, cudaStream_t st) {
@@ -236,17 +245,27 @@ static ms_status launch_t(const TmapPack& tm, const GemmArgs& g, cudaStream_t st
   if (g.num_tiles <= 0) return MS_OK;
   if constexpr (CL == 1) {
     const int grid = g.num_tiles < sms ? g.num_tiles : sms;
-    kern<<<grid, GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, smem, st>>>(tm, g);
+    const cudaError_t e = use_pdl()
+        ? launch_pdl(kern, dim3(grid), dim3(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS), smem, st,
+                     tm, g)
+        : (kern<<<grid, GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, smem, st>>>(tm, g),
+           cudaSuccess);
+    if (e != cudaSuccess) {
+      set_error("cudaLaunchKernelEx: %s", cudaGetErrorString(e));
+      return MS_ERR_LAUNCH;
+    }
   } else {
     cudaLaunchConfig_t cfg{};
     cfg.blockDim = dim3(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = CL;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     // persistent grid = the clusters that can be co-resident (GPCs with an odd
@@ -263,6 +282,7 @@ static ms_status launch_t(const TmapPack& tm, const GemmArgs& g, cudaStream_t st
     }
     const int clusters = g.num_tiles < max_clusters ? g.num_tiles : max_clusters;
     cfg.gridDim = dim3(clusters * CL);
+    cfg.numAttrs = use_pdl() ? 2 : 1;
     const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tm, g);
     if (e != cudaSuccess) {
       set_error("cudaLaunchKernelEx (cluster %d): %s", CL, cudaGetErrorString(e));

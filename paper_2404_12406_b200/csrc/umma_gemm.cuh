@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
   // K-split finalize) may be scheduled now: its blocks wait in
   // griddepcontrol.wait until this grid has finished, so only the launch
   // latency overlaps (no effect on launches without the attribute)
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  pdl_trigger();
   const int crank = CL > 1 ? static_cast<int>(cluster_ctarank()) : 0;
   const int t_first = static_cast<int>(blockIdx.x) / CL;
   const int t_step = static_cast<int>(gridDim.x) / CL;
@@ -413,6 +413,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
   if constexpr (CL > 1) cluster_sync();  // peer barriers initialised before any remote signal
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  pdl_wait();  // the prologue above may overlap the previous kernel (launch_pdl)
 
   if (warp == 0) {
     // ============================ TMA producer ============================
