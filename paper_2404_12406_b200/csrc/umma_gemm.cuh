@@ -975,11 +975,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, A_MN, B_MN, MODE, CL>::THREADS, 1)
               // elements el .. el + 31 of the output (el % 4 == 0: N and the
               // pitch are multiples of 4): Philox blocks el/4 .. el/4 + 7
               const int64_t el = orow * e.ldc + col_base + c;
-              const uint32_t klo = keep_n32<4>(static_cast<uint64_t>(el) >> 2, e.drop.stream,
-                                               e.drop.keys, e.drop.thr);
-              const uint32_t khi = keep_n32<4>((static_cast<uint64_t>(el) >> 2) + 4, e.drop.stream,
-                                               e.drop.keys, e.drop.thr);
-              const uint32_t kb = klo | (khi << 16);
+              const uint32_t kb = keep_n32<8>(static_cast<uint64_t>(el) >> 2, e.drop.stream,
+                                              e.drop.keys, e.drop.thr);
 #pragma unroll
               for (int j = 0; j < 32; ++j) v[j] = ((kb >> j) & 1u) ? v[j] * e.drop.scale : 0.f;
               round_all();  // the dropout's output as stored
