@@ -127,3 +127,40 @@ def test_saved_set_through_the_op_layer():
             MF.linear(x, w)
         assert any(t is x for t in saved) == w_rg
         assert any(t is w for t in saved) == x_rg
+
+
+@pytest.mark.gpu
+def test_bert_fused_output_projection_matches_unfused():
+    """A small BERT in train mode (dropout 0.1) converted with fuse=True (the
+    attention-output and output blocks become Linear -> dropout -> + residual
+    nodes) gives the same logits, bit for bit, as the unfused memsave model
+    under the same seeds, and the same trainable-bias gradients (up to the
+    order of the fp32 atomics in the column sums)."""
+    import copy
+
+    from transformers import BertConfig, BertForSequenceClassification
+
+    from paper_2404_12406_b200.nn import convert_to_memory_saving
+    torch.manual_seed(0)
+    cfg = BertConfig(num_hidden_layers=2, hidden_size=128, num_attention_heads=2,
+                     intermediate_size=256, attn_implementation="sdpa")
+    base = BertForSequenceClassification(cfg).to("cuda", torch.bfloat16).train()
+    for name, p in base.named_parameters():
+        p.requires_grad_(name.startswith("classifier.") or (
+            ".attention." in name and name.endswith(".bias") and "LayerNorm" not in name))
+    a = convert_to_memory_saving(copy.deepcopy(base), fuse=False)
+    b = convert_to_memory_saving(copy.deepcopy(base), fuse=True)
+    assert isinstance(b.bert.encoder.layer[0].output, torch.fx.GraphModule)
+    ids = torch.randint(0, cfg.vocab_size, (4, 64), device="cuda")
+    outs = []
+    for m in (a, b):
+        torch.manual_seed(123)
+        logits = m(input_ids=ids).logits
+        logits.float().square().sum().backward()
+        outs.append((logits.detach(), {n: p.grad for n, p in m.named_parameters()
+                                       if p.requires_grad}))
+    assert torch.equal(outs[0][0], outs[1][0])
+    assert outs[0][1].keys() == outs[1][1].keys()
+    for n in outs[0][1]:
+        torch.testing.assert_close(outs[0][1][n], outs[1][1][n], rtol=2 ** -6, atol=1e-3,
+                                   msg=n)
